@@ -1,0 +1,378 @@
+"""Benchmark: clause x assignment tests/s of the GpuShareSat filter on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C3]
+
+One step = one exchange round over the configured workload: encode the
+round's snapshots (K1/K2) and test every stored clause against every
+assignment (K3 + report emission K4 + activity bump K5).  Metric =
+clause x assignment tests per second (= the reference's lane_tests /
+busy_seconds, instrumentation.py:248-250).
+
+* value: snapshots already resident in HBM when the timed region starts;
+  device time of K steps via CUDA events on the library's stream.
+* e2e:   the same round through the C ABI with HOST buffers: pinned int8
+  snapshots copied H2D, round, report records copied D2H, every step.
+* roofline: the trigger kernel's algorithmic bytes (SURVEY.md §8(d):
+  4*sum(L) + (V+1)*(A/4 + 3G/8) + 16*P) over its event-timed duration,
+  against MEASURED_PEAKS.json hbm_gbs.
+* cpu_baseline: the C oracle (a port of the reference algorithm) on the
+  box's host cores, rank 0 only, on a bounded slice of the same workload.
+
+Multi-GPU (torchrun): every rank holds its own C3-sized clause shard
+(weak scaling); rank 0 stages and encodes the round, the packed tables are
+broadcast over NVLink with NCCL, every rank tests its shard, and the time is
+the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2012_03119_b200 import workload as W  # noqa: E402
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic(config):
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            d = json.load(fh)
+        return d.get(config)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling during the timed region (B200_PROFILING.md recipe)
+
+REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, device=0):
+        self.samples = []
+        self.proc = None
+        self.device = device
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 3:
+                try:
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except ValueError:
+                    pass
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = sorted(s[0] for s in self.samples)
+        reasons = set()
+        for _, _, r in self.samples:
+            for bit, name in REASON_BITS.items():
+                if r & bit and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+
+def build_shard(cfg: W.Config, rank: int):
+    rng = np.random.default_rng(cfg.seed + 1000 * rank)
+    buckets = W.clause_buckets(cfg.n_clauses, cfg.num_vars, rng, cfg.size_lo, cfg.size_hi)
+    flat, offs, ids = W.flatten(buckets, id0=rank * cfg.n_clauses)
+    return buckets, flat, offs, ids
+
+
+def algorithmic_bytes(sum_lits, num_vars, A, G, P):
+    """literal stream once, packed tables once, 16 B per report."""
+    return 4 * sum_lits + (num_vars + 1) * (A / 4 + 3 * G / 8) + 16 * P
+
+
+def cpu_baseline(cfg: W.Config, snaps, gl, gt, slice_clauses=2_000_000, repeats=1):
+    """The C oracle (port of the reference algorithm, oracle/tsg_oracle.c) with
+    all host threads on a bounded slice of the workload."""
+    from oracle import oracle as O
+    rng = np.random.default_rng(cfg.seed + 777)
+    b = W.clause_buckets(slice_clauses, cfg.num_vars, rng, cfg.size_lo, cfg.size_hi)
+    flat, offs, ids = W.flatten(b)
+    st = O.OracleStore()
+    st.insert_flat(flat, offs, ids)
+    threads = os.cpu_count() or 1
+    best = None
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        _, ctr = st.test_round(cfg.num_vars, snaps, gl, gt, 32, 32, 1.0, nthreads=threads)
+        dt = time.perf_counter() - t0
+        rate = ctr["lane_tests"] / dt
+        best = rate if best is None else max(best, rate)
+    return {"value": best, "unit": "clause_assignment_tests/s", "cores": threads, "kind": "port",
+            "sample": f"{slice_clauses} clauses of the {cfg.name} generator x {snaps.shape[0]} assignments, "
+                      f"one round, oracle/tsg_oracle.c with {threads} pthreads"}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    rng = np.random.default_rng(cfg.seed + 999)
+    snaps = W.snapshots(cfg.threads, cfg.lanes, cfg.num_vars, rng)
+    gl, gt = W.groups_for(cfg.threads, cfg.lanes)
+    from oracle import oracle as O
+    b = W.clause_buckets(1_000_000, cfg.num_vars, np.random.default_rng(cfg.seed + 777), cfg.size_lo, cfg.size_hi)
+    flat, offs, ids = W.flatten(b)
+    st = O.OracleStore()
+    st.insert_flat(flat, offs, ids)
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        st.test_round(cfg.num_vars, snaps, gl, gt, 32, 32, 1.0, nthreads=threads)
+    t0 = time.perf_counter()
+    tests = 0
+    for _ in range(args.steps):
+        _, ctr = st.test_round(cfg.num_vars, snaps, gl, gt, 32, 32, 1.0, nthreads=threads)
+        tests += ctr["lane_tests"]
+    dt = time.perf_counter() - t0
+    v = tests / dt
+    sample = (f"1000000 clauses of the {cfg.name} generator x {snaps.shape[0]} assignments per step, "
+              f"oracle/tsg_oracle.c (C port of engine.py:238-467) with {threads} pthreads")
+    print(json.dumps({
+        "impl": "reference", "metric": "clause_assignment_tests_per_second", "value": v,
+        "unit": "clause_assignment_tests/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.n_clauses} clauses (size U[2,30]) x {cfg.assignments} "
+                               f"assignments ({cfg.threads} threads x {cfg.lanes}), {cfg.num_vars} vars",
+                   "parallelism": f"host threads x{threads}"},
+        "cpu_baseline": {"value": v, "unit": "clause_assignment_tests/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "clause_assignment_tests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3", choices=sorted(W.CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = W.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2012_03119_b200.native import NativeEngine
+
+    t_build = time.perf_counter()
+    buckets, flat, offs, ids = build_shard(cfg, rank)
+    sum_lits = int(offs[-1])
+    eng = NativeEngine(cfg.num_vars, 32, 32, device=local, timing=True, report_capacity=8 << 20)
+    eng.add_clauses(flat, offs, ids)
+    del flat
+    rng = np.random.default_rng(cfg.seed + 999)
+    snaps = W.snapshots(cfg.threads, cfg.lanes, cfg.num_vars, rng)  # same on every rank
+    gl, gt = W.groups_for(cfg.threads, cfg.lanes)
+    A = int(snaps.shape[0])
+    G = len(gl)
+    build_s = time.perf_counter() - t_build
+
+    stream = torch.cuda.ExternalStream(eng.stream(), device=torch.device("cuda", local))
+    # device-resident snapshots (pitch multiple of 16) for the `value` leg
+    pitch = (cfg.num_vars + 1 + 15) // 16 * 16
+    d_snaps = torch.zeros((A, pitch), dtype=torch.int8, device=f"cuda:{local}")
+    d_snaps[:, :cfg.num_vars + 1] = torch.from_numpy(snaps).to(d_snaps.device)
+    torch.cuda.synchronize()
+    eng.stage_device(d_snaps.data_ptr(), A, pitch)
+    eng.prepare(gl, gt)
+
+    tables_t = None
+    if dist is not None:
+        ptr, nbytes = eng.tables()
+
+        class _CAI:
+            __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3,
+                                        "stream": None}
+        tables_t = torch.as_tensor(_CAI(), device=f"cuda:{local}")
+
+    launches_per_step = 2 * ((G + 31) // 32)
+
+    def step():
+        if rank == 0:
+            eng.encode()
+        if tables_t is not None:
+            with torch.cuda.stream(stream):
+                dist.broadcast(tables_t, src=0)
+        return eng.test(1.0)
+
+    for _ in range(args.warmup):
+        res = step()
+    eng.sync()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    test_ms = []
+    enc_ms = []
+    reports = []
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+        for _ in range(args.steps):
+            res = step()
+            test_ms.append(res.test_ms)
+            enc_ms.append(res.encode_ms)
+            reports.append(res.reports)
+        with torch.cuda.stream(stream):
+            e1.record(stream)
+        eng.sync()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+    elapsed_ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([elapsed_ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    ms_per_step = elapsed_ms / args.steps
+    tests_per_step = res.lane_tests * world
+    value = tests_per_step / (ms_per_step * 1e-3)
+
+    # ---- e2e: host buffers through the C ABI -------------------------------
+    e2e = None
+    h_snaps = torch.from_numpy(snaps).pin_memory()
+    rec_buf = None
+    e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
+    if world == 1:
+        from paper_2012_03119_b200 import _lib
+        import ctypes as C
+        rec_buf = torch.empty((8 << 20) * 32, dtype=torch.uint8).pin_memory()
+        L = eng.L
+
+        def e2e_step():
+            _lib.check(L.tsg_stage_snapshots(eng.h, C.c_void_p(h_snaps.data_ptr()), A, cfg.num_vars + 1, 0))
+            r = eng.round(gl, gt, 1.0)
+            got = C.c_int64(0)
+            n = min(r.reports, (8 << 20))
+            _lib.check(L.tsg_fetch_reports(eng.h, C.c_void_p(rec_buf.data_ptr()), n, C.byref(got)))
+            return r
+        for _ in range(2):
+            e2e_step()
+        eng.sync()
+        w0 = time.perf_counter()
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+        d2h = 0
+        for _ in range(e2e_steps):
+            r = e2e_step()
+            d2h += r.reports * 32 + 24
+        with torch.cuda.stream(stream):
+            e1.record(stream)
+        eng.sync()
+        wall = time.perf_counter() - w0
+        e2e_ms = e0.elapsed_time(e1) / e2e_steps
+        e2e = {"value": r.lane_tests / (e2e_ms * 1e-3), "unit": "clause_assignment_tests/s",
+               "h2d_bytes_per_step": int(A * (cfg.num_vars + 1)), "d2h_bytes_per_step": int(d2h / e2e_steps),
+               "ms_per_step": e2e_ms, "wall_ms_per_step": wall / e2e_steps * 1e3}
+
+    # ---- roofline of the trigger kernel --------------------------------------
+    peak, peak_kind = load_peaks()
+    test_ms_avg = float(np.mean(test_ms))
+    P = float(np.mean(reports))
+    b_alg = algorithmic_bytes(sum_lits, cfg.num_vars, A, G, P)
+    achieved = b_alg / (test_ms_avg * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": load_traffic(cfg.name), "kernel": "tsg::k_test",
+                "kernel_ms": test_ms_avg, "encode_ms": float(np.mean(enc_ms)),
+                "algorithmic_bytes": b_alg, "peak_kind": peak_kind}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(cfg, snaps, gl, gt)
+        except Exception as exc:  # reported, never fatal
+            cpu = {"value": None, "error": str(exc)}
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": "clause_assignment_tests_per_second", "value": value, "unit": "clause_assignment_tests/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: {cfg.n_clauses} clauses/GPU (size U[2,30], mean 16) x "
+                                   f"{A} assignments ({cfg.threads} threads x {cfg.lanes}), {cfg.num_vars} vars, "
+                                   f"seed {cfg.seed}",
+                       "clauses_per_gpu": cfg.n_clauses, "assignments": A, "groups": G, "num_vars": cfg.num_vars,
+                       "sum_literals_per_gpu": sum_lits, "reports_per_step": P,
+                       "l2": "inputs larger than L2 (640 MB clause DB + 205 MB snapshots per GPU vs 126 MB L2)",
+                       "parallelism": f"clause shards x{world}, tables broadcast (NCCL)" if world > 1 else "1 GPU"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": launches_per_step * args.steps,
+            "build_seconds": build_s,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    eng.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,172 @@
+/*
+ * tsg.h -- C ABI of the B200-native GpuShareSat clause-usefulness filter.
+ *
+ * This is the drop-in boundary for the hot path of the reference engine
+ * (/root/reference/pkg/src/triggersat/engine.py, class Engine): the clause
+ * store, the assignment encoder, the two-stage trigger test and report
+ * emission.  The Python mirror of the reference API
+ * (paper_2012_03119_b200/engine.py, bitpack.py) binds exactly these entry
+ * points with ctypes; INTEGRATION.md shows the binding a reference maintainer
+ * would add.  Plain pointers and sizes only: no torch types cross the ABI.
+ *
+ * Threading: one handle belongs to one engine-worker thread (the reference
+ * runs run_round / reduce_store only on its worker, engine.py:257-264).  All
+ * calls on a handle are serialised on the handle's CUDA stream.  Calls that
+ * return host data synchronise that stream before returning.
+ *
+ * Errors: every entry point returns TSG_OK or a TSG_E* code; tsg_last_error()
+ * gives the thread's last message.  The Python layer maps TSG_EINVAL to
+ * ValueError, TSG_ECAPACITY to CapacityError, TSG_ERANGE to IndexError and
+ * the rest to RuntimeError, matching bitpack.py:30-36,92-103 / engine.py:64-74.
+ * There is no CPU fallback: without a CUDA device every compute call fails
+ * with TSG_ECUDA.
+ */
+#ifndef TSG_H
+#define TSG_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSG_ABI_VERSION 1
+
+#define TSG_OK 0
+#define TSG_EINVAL 1    /* ValueError    (bad width / length / config)   */
+#define TSG_ECAPACITY 2 /* CapacityError (bitpack.py:28-29)              */
+#define TSG_ERANGE 3    /* IndexError                                    */
+#define TSG_ECUDA 4     /* CUDA runtime failure or no device             */
+#define TSG_ENOMEM 5    /* device allocation failed                      */
+
+typedef struct tsg_engine tsg_engine;
+
+/* EngineConfig knobs that reach the device (engine.py:44-74).  The queue,
+ * decay and reduce knobs stay in the host layer, as in the reference. */
+typedef struct tsg_config {
+    int32_t lane_width;      /* 1..64, EngineConfig.lane_width (engine.py:56)   */
+    int32_t group_width;     /* 1..64, EngineConfig.group_width (engine.py:57)  */
+    int32_t device;          /* CUDA device ordinal                              */
+    int32_t flags;           /* TSG_F_* below                                    */
+    int64_t report_capacity; /* initial device report buffer (records); 0=auto  */
+} tsg_config;
+
+#define TSG_F_TIMING 1 /* record CUDA events around encode/test (fills *_ms) */
+
+/* Per-round figures, the quantities engine.py:437-467 adds to its counters. */
+typedef struct tsg_round_result {
+    int64_t reports;                  /* records emitted after (eid, tid) dedup   */
+    int64_t clauses_tested;           /* engine.py:445 (once per chunk)           */
+    int64_t aggregate_tests;          /* engine.py:446                            */
+    int64_t aggregate_tests_negative; /* engine.py:465-467                        */
+    int64_t lane_tests;               /* engine.py:447                            */
+    int64_t lane_triggers;            /* engine.py:461                            */
+    int32_t n_chunks;                 /* ceil(n_groups / group_width)             */
+    int32_t reruns;                   /* report-buffer overflow replays           */
+    double encode_ms;                 /* device time, TSG_F_TIMING only           */
+    double test_ms;                   /* device time of the trigger kernels       */
+} tsg_round_result;
+
+/* One report record (engine.py:90-102 Report minus the literals, which the
+ * host keeps).  `group` is the global group index in round order
+ * (engine.py:390-399); the destination thread is the group's tid.  Sorting
+ * by (group / group_width, bucket, slot, group) reproduces the reference's
+ * emission order (engine.py:403-464). */
+typedef struct tsg_report {
+    int64_t engine_id;
+    uint64_t lane_mask;
+    int32_t group;
+    int32_t bucket; /* bucket creation rank (dict insertion order)             */
+    int64_t slot;   /* slot inside the bucket                                  */
+} tsg_report;
+
+const char* tsg_last_error(void);
+int tsg_abi_version(void);
+int tsg_device_count(int32_t* n);
+
+/* Engine(num_vars, thread_count, EngineConfig) -- engine.py:266-301 */
+int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out);
+int tsg_destroy(tsg_engine* h);
+
+/* ---- clause store (engine.py:122-235) -------------------------------------
+ * _integrate_exports / ClauseStore.insert (engine.py:348-358, 213-219):
+ * append n clauses in order.  Clause i has literals lits[offsets[i] ..
+ * offsets[i+1]), engine id ids[i], origin origins[i]; all start at
+ * `activity`.  Buckets are created in first-seen size order. */
+int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets,
+                    int64_t n, const int64_t* ids, const int32_t* origins,
+                    double activity);
+int tsg_store_size(tsg_engine* h, int64_t* n);               /* len(store)        */
+int tsg_bucket_count(tsg_engine* h, int32_t* nb);            /* buckets (created) */
+int tsg_bucket_info(tsg_engine* h, int32_t b, int32_t* size, int64_t* count);
+/* copy bucket b back: lits clause-major (count*size), ids, origins,
+ * activities; any pointer may be NULL (engine.py:165-169, 221-231) */
+int tsg_bucket_read(tsg_engine* h, int32_t b, int32_t* lits, int64_t* ids,
+                    int32_t* origins, double* acts);
+/* ClauseStore.scale_activities (engine.py:233-235) */
+int tsg_scale_activities(tsg_engine* h, double factor);
+/* reduce_store selection + compaction (engine.py:476-500): remove the
+ * `target` smallest (activity, engine_id) among clauses with id <
+ * eligible_below; order-preserving compaction per bucket.  removed_ids (may be
+ * NULL, else room for `target`) receives the removed ids in key order. */
+int tsg_reduce(tsg_engine* h, int64_t eligible_below, int64_t target,
+               int64_t* removed, int64_t* removed_ids);
+/* explicit delete (streaming config C4): remove the listed ids if present,
+ * order-preserving (the compact(keep) of engine.py:184-200). */
+int tsg_remove_clauses(tsg_engine* h, const int64_t* ids, int64_t n, int64_t* removed);
+
+/* ---- one exchange round (engine.py:369-467) ---------------------------------
+ * 1. tsg_stage_snapshots: the round's snapshots, already grouped in round
+ *    order (tids ascending, lane_width per group, engine.py:390-399), as rows of
+ *    num_vars+1 int8 values ({1,-1,0}; anything non-zero and not 1 reads as
+ *    False, like bitpack.py:108-109).  `row_pitch` is the byte distance between
+ *    rows at `rows`; on_device=1 means `rows` is a device pointer.
+ * 2. tsg_round: encode (K1/K2) and test (K3+K4+K5) every chunk of
+ *    group_width groups against every bucket; bumps activities by
+ *    activity_inc * hits (engine.py:460, fp64, no FMA).
+ * 3. tsg_fetch_reports: copy the round's report records out.
+ * The split form (prepare / encode / tables / test) exists for multi-GPU:
+ * rank 0 encodes, the packed tables are broadcast over NVLink, every rank
+ * tests its own clause shard. */
+int tsg_stage_snapshots(tsg_engine* h, const int8_t* rows, int64_t n_rows,
+                        int64_t row_pitch, int32_t on_device);
+int tsg_round(tsg_engine* h, const int32_t* group_lanes, const int32_t* group_tid,
+              int32_t n_groups, double activity_inc, tsg_round_result* out);
+int tsg_round_prepare(tsg_engine* h, const int32_t* group_lanes,
+                      const int32_t* group_tid, int32_t n_groups);
+int tsg_round_encode(tsg_engine* h);
+int tsg_round_tables(tsg_engine* h, void** device_ptr, int64_t* bytes);
+int tsg_round_test(tsg_engine* h, double activity_inc, tsg_round_result* out);
+int tsg_fetch_reports(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n);
+/* device pointer + count of the round's records (for device-side consumers) */
+int tsg_reports_device(tsg_engine* h, void** device_ptr, int64_t* n);
+int tsg_sync(tsg_engine* h);
+/* the handle's CUDA stream (cudaStream_t), for interop */
+int tsg_stream(tsg_engine* h, void** stream);
+
+/* ---- standalone bit-parallel kernels (bitpack.py) ----------------------------
+ * Same device code as the engine path, exposed for the library-level API.
+ * All arrays are host arrays of uint64 words indexed by variable (slot 0
+ * unused), exactly the reference's numpy layout (bitpack.py:96-97). */
+/* pack_assignments (bitpack.py:81-117): n rows of num_vars+1 int8 */
+int tsg_pack(int32_t device, const int8_t* rows, int64_t n, int64_t row_pitch,
+             int32_t num_vars, int32_t lane_width, uint64_t* is_true, uint64_t* is_set);
+/* build_aggregate_batch (bitpack.py:211-244) from n_groups packed batches laid
+ * out [n_groups][num_vars+1] */
+int tsg_aggregate(int32_t device, const uint64_t* is_true, const uint64_t* is_set,
+                  const int32_t* lane_counts, int32_t n_groups, int32_t num_vars,
+                  int32_t group_width, uint64_t* cbt, uint64_t* cbf, uint64_t* cbu);
+/* assignment_trigger (bitpack.py:120-135) for n clauses at once */
+int tsg_lane_trigger(int32_t device, const uint64_t* is_true, const uint64_t* is_set,
+                     int32_t num_vars, int32_t lane_width, uint64_t lane_mask,
+                     const int32_t* lits, const int64_t* offsets, int64_t n,
+                     uint64_t* masks);
+/* aggregate_trigger (bitpack.py:247-271) for n clauses at once */
+int tsg_aggregate_trigger(int32_t device, const uint64_t* cbt, const uint64_t* cbf,
+                          const uint64_t* cbu, int32_t num_vars, int32_t group_width,
+                          int32_t group_count, const int32_t* lits,
+                          const int64_t* offsets, int64_t n, uint64_t* words);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

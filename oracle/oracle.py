@@ -60,6 +60,7 @@ def lib():
         L.ora_store_new.restype = P
         L.ora_store_free.argtypes = [P]
         L.ora_store_insert.argtypes = [P, P, C.c_int32, C.c_int64, C.c_int32, C.c_double]
+        L.ora_store_insert_many.argtypes = [P, P, P, C.c_int64, P, P, C.c_double]
         L.ora_store_size.argtypes = [P]
         L.ora_store_size.restype = C.c_int64
         L.ora_store_nbuckets.argtypes = [P]
@@ -150,6 +151,16 @@ class OracleStore:
     def insert_many(self, clauses, ids, origins, activity):
         for c, i, o in zip(clauses, ids, origins):
             self.insert(c, int(i), int(o), activity)
+
+    def insert_flat(self, flat, offsets, ids, origins=None, activity=1.0):
+        flat = np.ascontiguousarray(flat, np.int32)
+        if flat.size == 0:
+            flat = np.zeros(1, np.int32)
+        offsets = np.ascontiguousarray(offsets, np.int64)
+        ids = np.ascontiguousarray(ids, np.int64)
+        org = None if origins is None else np.ascontiguousarray(origins, np.int32)
+        lib().ora_store_insert_many(self.h, _p(flat), _p(offsets), len(offsets) - 1, _p(ids),
+                                    _p(org) if org is not None else None, activity)
 
     def __len__(self):
         return int(lib().ora_store_size(self.h))

@@ -163,6 +163,14 @@ void ora_store_insert(ora_store* s, const int32_t* lits, int32_t size,
     b->count++;
 }
 
+void ora_store_insert_many(ora_store* s, const int32_t* lits, const int64_t* offsets,
+                           int64_t n, const int64_t* ids, const int32_t* origins,
+                           double activity) {
+    for (int64_t i = 0; i < n; ++i)
+        ora_store_insert(s, lits + offsets[i], (int32_t)(offsets[i + 1] - offsets[i]), ids[i],
+                         origins ? origins[i] : 0, activity);
+}
+
 int64_t ora_store_size(const ora_store* s) {
     int64_t n = 0;
     for (int32_t i = 0; i < s->nb; ++i) n += s->b[i].count;

@@ -71,6 +71,10 @@ void ora_store_free(ora_store* s);
 /* ClauseStore.insert / _SizeBucket.insert, engine.py:150-163, 213-219 */
 void ora_store_insert(ora_store* s, const int32_t* lits, int32_t size,
                       int64_t engine_id, int32_t origin, double activity);
+/* bulk form: clause i = lits[offsets[i]..offsets[i+1]) */
+void ora_store_insert_many(ora_store* s, const int32_t* lits, const int64_t* offsets,
+                           int64_t n, const int64_t* ids, const int32_t* origins,
+                           double activity);
 int64_t ora_store_size(const ora_store* s);
 int32_t ora_store_nbuckets(const ora_store* s);
 /* bucket b in creation order: size and count */

@@ -1,0 +1,138 @@
+"""ctypes bindings of libtsg.so (include/tsg.h).
+
+The product has exactly one compute path: the CUDA library.  If the library
+is missing or no CUDA device is present, every compute call raises -- there
+is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtsg.so")
+
+TSG_OK, TSG_EINVAL, TSG_ECAPACITY, TSG_ERANGE, TSG_ECUDA, TSG_ENOMEM = range(6)
+TSG_F_TIMING = 1
+
+
+class CapacityError(ValueError):
+    """More assignments or groups than the configured word width holds
+    (bitpack.py:28-29)."""
+
+
+class TsgError(RuntimeError):
+    """CUDA-side failure (no device, launch error, out of memory)."""
+
+
+class tsg_config(C.Structure):
+    _fields_ = [("lane_width", C.c_int32), ("group_width", C.c_int32), ("device", C.c_int32),
+                ("flags", C.c_int32), ("report_capacity", C.c_int64)]
+
+
+class tsg_round_result(C.Structure):
+    _fields_ = [("reports", C.c_int64), ("clauses_tested", C.c_int64), ("aggregate_tests", C.c_int64),
+                ("aggregate_tests_negative", C.c_int64), ("lane_tests", C.c_int64),
+                ("lane_triggers", C.c_int64), ("n_chunks", C.c_int32), ("reruns", C.c_int32),
+                ("encode_ms", C.c_double), ("test_ms", C.c_double)]
+
+
+REPORT_DTYPE = np.dtype([("engine_id", "<i8"), ("lane_mask", "<u8"), ("group", "<i4"),
+                         ("bucket", "<i4"), ("slot", "<i8")])
+assert REPORT_DTYPE.itemsize == 32
+
+# every symbol include/tsg.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "tsg_last_error", "tsg_abi_version", "tsg_device_count", "tsg_create", "tsg_destroy",
+    "tsg_add_clauses", "tsg_store_size", "tsg_bucket_count", "tsg_bucket_info", "tsg_bucket_read",
+    "tsg_scale_activities", "tsg_reduce", "tsg_remove_clauses", "tsg_stage_snapshots", "tsg_round",
+    "tsg_round_prepare", "tsg_round_encode", "tsg_round_tables", "tsg_round_test", "tsg_fetch_reports",
+    "tsg_reports_device", "tsg_sync", "tsg_stream", "tsg_pack", "tsg_aggregate", "tsg_lane_trigger",
+    "tsg_aggregate_trigger",
+)
+
+_lib = None
+_lock = threading.Lock()
+
+
+def _declare(L):
+    P, I32, I64, D = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+    pI64 = C.POINTER(C.c_int64)
+    sig = {
+        "tsg_last_error": ([], C.c_char_p),
+        "tsg_abi_version": ([], C.c_int),
+        "tsg_device_count": ([C.POINTER(C.c_int32)], C.c_int),
+        "tsg_create": ([I32, C.POINTER(tsg_config), C.POINTER(P)], C.c_int),
+        "tsg_destroy": ([P], C.c_int),
+        "tsg_add_clauses": ([P, P, P, I64, P, P, D], C.c_int),
+        "tsg_store_size": ([P, pI64], C.c_int),
+        "tsg_bucket_count": ([P, C.POINTER(C.c_int32)], C.c_int),
+        "tsg_bucket_info": ([P, I32, C.POINTER(C.c_int32), pI64], C.c_int),
+        "tsg_bucket_read": ([P, I32, P, P, P, P], C.c_int),
+        "tsg_scale_activities": ([P, D], C.c_int),
+        "tsg_reduce": ([P, I64, I64, pI64, P], C.c_int),
+        "tsg_remove_clauses": ([P, P, I64, pI64], C.c_int),
+        "tsg_stage_snapshots": ([P, P, I64, I64, I32], C.c_int),
+        "tsg_round": ([P, P, P, I32, D, C.POINTER(tsg_round_result)], C.c_int),
+        "tsg_round_prepare": ([P, P, P, I32], C.c_int),
+        "tsg_round_encode": ([P], C.c_int),
+        "tsg_round_tables": ([P, C.POINTER(P), pI64], C.c_int),
+        "tsg_round_test": ([P, D, C.POINTER(tsg_round_result)], C.c_int),
+        "tsg_fetch_reports": ([P, P, I64, pI64], C.c_int),
+        "tsg_reports_device": ([P, C.POINTER(P), pI64], C.c_int),
+        "tsg_sync": ([P], C.c_int),
+        "tsg_stream": ([P, C.POINTER(P)], C.c_int),
+        "tsg_pack": ([I32, P, I64, I64, I32, I32, P, P], C.c_int),
+        "tsg_aggregate": ([I32, P, P, P, I32, I32, I32, P, P, P], C.c_int),
+        "tsg_lane_trigger": ([I32, P, P, I32, I32, C.c_uint64, P, P, I64, P], C.c_int),
+        "tsg_aggregate_trigger": ([I32, P, P, P, I32, I32, I32, P, P, I64, P], C.c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+
+
+def load(path: str = LIB_PATH):
+    """Load libtsg.so (building it first if the sources are newer)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            from . import build as _build
+            if not os.path.exists(path):
+                _build.build()
+            L = C.CDLL(path)
+            _declare(L)
+            _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc == TSG_OK:
+        return
+    msg = (load().tsg_last_error() or b"").decode(errors="replace")
+    if rc == TSG_EINVAL:
+        raise ValueError(msg)
+    if rc == TSG_ECAPACITY:
+        raise CapacityError(msg)
+    if rc == TSG_ERANGE:
+        raise IndexError(msg)
+    if rc == TSG_ENOMEM:
+        raise MemoryError(msg)
+    raise TsgError(msg)
+
+
+def ptr(a):
+    """Raw pointer of a numpy array (or None)."""
+    if a is None:
+        return None
+    return C.c_void_p(a.ctypes.data)
+
+
+def device_count() -> int:
+    n = C.c_int32(0)
+    load().tsg_device_count(C.byref(n))
+    return n.value

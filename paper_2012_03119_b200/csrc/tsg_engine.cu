@@ -1,0 +1,782 @@
+// tsg_engine.cu -- C ABI (include/tsg.h) over the sm_100a kernels.
+//
+// Host runtime of the device engine: bucket bookkeeping, staging, chunking,
+// kernel launches on one CUDA stream per handle, report-buffer management,
+// store maintenance with CUB sort/select for the rare reduce path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include "../../include/tsg.h"
+#include "tsg_kernels.cuh"
+#include "tsg_store.cuh"
+
+using namespace tsg;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(call)                                                                           \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess) {                                                           \
+            return fail(e_ == cudaErrorMemoryAllocation ? TSG_ENOMEM : TSG_ECUDA, "%s: %s (%s:%d)", \
+                        #call, cudaGetErrorString(e_), __FILE__, __LINE__);                \
+        }                                                                                  \
+    } while (0)
+
+#define CKR(expr)                 \
+    do {                          \
+        int r_ = (expr);          \
+        if (r_ != TSG_OK) return r_; \
+    } while (0)
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+int grid_for(int64_t n, int threads = 256, int cap = 148 * 16) {
+    int64_t b = (n + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > cap) b = cap;
+    return (int)b;
+}
+
+struct Bucket {
+    int32_t size = 0, rank = 0;
+    int64_t count = 0, cap = 0;  // cap: multiple of STRIDE
+    int32_t* lits = nullptr;
+    double* acts = nullptr;
+    int64_t* ids = nullptr;
+    int32_t* origins = nullptr;
+};
+
+}  // namespace
+
+struct tsg_engine {
+    int dev = 0;
+    int nsm = 148;
+    int32_t V = 0;
+    tsg_config cfg{};
+    cudaStream_t st = nullptr;
+    std::vector<Bucket> buckets;
+    std::unordered_map<int32_t, int> by_size;
+
+    // staged snapshot rows
+    const int8_t* rows = nullptr;  // device rows used by the encoder (owned or aliased)
+    int8_t* rows_own = nullptr;
+    int64_t rows_cap = 0, pitch = 0, n_rows = 0;
+
+    // round description
+    int32_t n_groups = 0, n_chunks = 0;
+    std::vector<int32_t> glanes, gtid;
+    std::vector<int64_t> grow0;
+    std::vector<int64_t> chunk_off;  // byte offset of each chunk's tables
+    int8_t* tables = nullptr;
+    int64_t tables_cap = 0, tables_bytes = 0;
+
+    BucketDesc* d_desc = nullptr;
+    int64_t desc_cap = 0;
+    std::vector<BucketDesc> h_desc;
+    int64_t n_tiles = 0;
+
+    tsg_report* out = nullptr;
+    int64_t out_cap = 0, n_out = 0;
+    unsigned long long* ctr = nullptr;      // device [0..3]
+    unsigned long long* h_ctr = nullptr;    // pinned [4]
+    int64_t* carry = nullptr;
+    int64_t carry_cap = 0;
+    int64_t round_seq = 0;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    int test_grid = 0;
+};
+
+namespace {
+
+struct DevGuard {
+    int prev = -1;
+    explicit DevGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DevGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+int dalloc(tsg_engine* h, void** p, int64_t bytes) {
+    *p = nullptr;
+    if (bytes <= 0) return TSG_OK;
+    CK(cudaMallocAsync(p, (size_t)bytes, h->st));
+    return TSG_OK;
+}
+
+void dfree(tsg_engine* h, void* p) {
+    if (p) cudaFreeAsync(p, h->st);
+}
+
+template <class T>
+int dgrow(tsg_engine* h, T** p, int64_t* cap, int64_t need, bool keep = false, int64_t keep_elems = 0) {
+    if (need <= *cap) return TSG_OK;
+    int64_t nc = std::max<int64_t>(need, *cap * 2);
+    T* np = nullptr;
+    CKR(dalloc(h, (void**)&np, nc * (int64_t)sizeof(T)));
+    if (keep && *p && keep_elems)
+        CK(cudaMemcpyAsync(np, *p, keep_elems * sizeof(T), cudaMemcpyDeviceToDevice, h->st));
+    dfree(h, *p);
+    *p = np;
+    *cap = nc;
+    return TSG_OK;
+}
+
+int bucket_reserve(tsg_engine* h, Bucket& b, int64_t need) {
+    if (need <= b.cap) return TSG_OK;
+    // _SizeBucket._grow doubles with a floor of 4 blocks (engine.py:141-148)
+    int64_t nc = std::max<int64_t>(b.cap ? b.cap : 4 * STRIDE, 4 * STRIDE);
+    while (nc < need) nc *= 2;
+    int32_t *lits = nullptr, *org = nullptr;
+    double* acts = nullptr;
+    int64_t* ids = nullptr;
+    CKR(dalloc(h, (void**)&lits, nc * (int64_t)std::max(b.size, 1) * 4));
+    CKR(dalloc(h, (void**)&acts, nc * 8));
+    CKR(dalloc(h, (void**)&ids, nc * 8));
+    CKR(dalloc(h, (void**)&org, nc * 4));
+    if (b.count) {
+        int64_t used = round_up(b.count, STRIDE);
+        if (b.size) CK(cudaMemcpyAsync(lits, b.lits, used * b.size * 4, cudaMemcpyDeviceToDevice, h->st));
+        CK(cudaMemcpyAsync(acts, b.acts, b.count * 8, cudaMemcpyDeviceToDevice, h->st));
+        CK(cudaMemcpyAsync(ids, b.ids, b.count * 8, cudaMemcpyDeviceToDevice, h->st));
+        CK(cudaMemcpyAsync(org, b.origins, b.count * 4, cudaMemcpyDeviceToDevice, h->st));
+    }
+    dfree(h, b.lits); dfree(h, b.acts); dfree(h, b.ids); dfree(h, b.origins);
+    b.lits = lits; b.acts = acts; b.ids = ids; b.origins = org;
+    b.cap = nc;
+    return TSG_OK;
+}
+
+bool wide_lane(const tsg_engine* h) { return h->cfg.lane_width > 32; }
+bool wide_group(const tsg_engine* h) { return h->cfg.group_width > 32; }
+int64_t agg_entry_bytes(const tsg_engine* h) { return wide_group(h) ? 32 : 16; }
+int64_t lane_entry_bytes(const tsg_engine* h) { return wide_lane(h) ? 16 : 8; }
+
+template <class LW, class GW>
+int launch_encode(tsg_engine* h, int c) {
+    EncodeChunk ec{};
+    int32_t g0 = c * h->cfg.group_width;
+    ec.G = std::min(h->cfg.group_width, h->n_groups - g0);
+    ec.num_vars = h->V;
+    ec.pitch = h->pitch;
+    for (int g = 0; g < ec.G; ++g) {
+        ec.row0[g] = h->grow0[g0 + g];
+        ec.lanes[g] = h->glanes[g0 + g];
+    }
+    auto* agg = reinterpret_cast<AggEntry<GW>*>(h->tables + h->chunk_off[c]);
+    auto* lane = reinterpret_cast<LaneEntry<LW>*>(h->tables + h->chunk_off[c] + (int64_t)(h->V + 2) * sizeof(AggEntry<GW>));
+    dim3 grid((unsigned)((h->V + 2 + 127) / 128)), block(32, 8);
+    k_encode<LW, GW><<<grid, block, 0, h->st>>>(h->rows, ec, lane, agg);
+    CK(cudaGetLastError());
+    return TSG_OK;
+}
+
+int do_encode(tsg_engine* h) {
+    for (int c = 0; c < h->n_chunks; ++c) {
+        int r;
+        if (wide_lane(h)) r = wide_group(h) ? launch_encode<uint64_t, uint64_t>(h, c) : launch_encode<uint64_t, uint32_t>(h, c);
+        else r = wide_group(h) ? launch_encode<uint32_t, uint64_t>(h, c) : launch_encode<uint32_t, uint32_t>(h, c);
+        if (r) return r;
+    }
+    return TSG_OK;
+}
+
+template <class LW, class GW>
+int launch_test(tsg_engine* h, int c, double inc, int emit_only) {
+    TestParams<LW, GW> p{};
+    int32_t g0 = c * h->cfg.group_width;
+    int32_t G = std::min(h->cfg.group_width, h->n_groups - g0);
+    p.buckets = h->d_desc;
+    p.nb = (int32_t)h->h_desc.size();
+    p.G = G;
+    p.n_tiles = h->n_tiles;
+    p.agg = reinterpret_cast<const AggEntry<GW>*>(h->tables + h->chunk_off[c]);
+    p.lane = reinterpret_cast<const LaneEntry<LW>*>(h->tables + h->chunk_off[c] + (int64_t)(h->V + 2) * sizeof(AggEntry<GW>));
+    p.sentinel = h->V + 1;
+    p.g0 = g0;
+    p.group_mask = width_mask<GW>(G);
+    p.inc = inc;
+    p.out = h->out;
+    p.ctr = h->ctr;
+    p.out_cap = h->out_cap;
+    p.carry = h->carry;
+    p.stamp_base = (h->round_seq & 0x7fffffff) << 32;
+    p.carry_in_tid = (c > 0 && h->gtid[g0] == h->gtid[g0 - 1]) ? h->gtid[g0] : -1;
+    p.carry_out_tid = (g0 + G < h->n_groups && h->gtid[g0 + G - 1] == h->gtid[g0 + G]) ? h->gtid[g0 + G - 1] : -1;
+    p.emit_only = emit_only;
+    for (int g = 0; g < G; ++g) {
+        p.tid[g] = h->gtid[g0 + g];
+        p.lane_mask[g] = width_mask<LW>(h->glanes[g0 + g]);
+    }
+    if (h->n_tiles == 0) return TSG_OK;
+    if (!h->test_grid) {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_test<LW, GW>, 256, 0);
+        h->test_grid = std::max(1, per_sm) * h->nsm;
+    }
+    int64_t want = (h->n_tiles + 7) / 8;
+    int grid = (int)std::min<int64_t>(want, h->test_grid);
+    k_test<LW, GW><<<grid, 256, 0, h->st>>>(p);
+    CK(cudaGetLastError());
+    return TSG_OK;
+}
+
+int run_tests(tsg_engine* h, double inc, int emit_only) {
+    for (int c = 0; c < h->n_chunks; ++c) {
+        int r;
+        if (wide_lane(h)) r = wide_group(h) ? launch_test<uint64_t, uint64_t>(h, c, inc, emit_only) : launch_test<uint64_t, uint32_t>(h, c, inc, emit_only);
+        else r = wide_group(h) ? launch_test<uint32_t, uint64_t>(h, c, inc, emit_only) : launch_test<uint32_t, uint32_t>(h, c, inc, emit_only);
+        if (r) return r;
+    }
+    return TSG_OK;
+}
+
+int64_t store_size(const tsg_engine* h) {
+    int64_t n = 0;
+    for (auto& b : h->buckets) n += b.count;
+    return n;
+}
+
+int build_desc(tsg_engine* h) {
+    h->h_desc.clear();
+    int64_t tiles = 0;
+    for (auto& b : h->buckets) {
+        if (!b.count) continue;
+        BucketDesc d{};
+        d.lits = b.lits; d.acts = b.acts; d.ids = b.ids;
+        d.size = b.size; d.rank = b.rank; d.count = b.count; d.tile0 = tiles;
+        tiles += (b.count + STRIDE - 1) / STRIDE;
+        h->h_desc.push_back(d);
+    }
+    h->n_tiles = tiles;
+    CKR(dgrow(h, &h->d_desc, &h->desc_cap, std::max<int64_t>(1, (int64_t)h->h_desc.size())));
+    if (!h->h_desc.empty())
+        CK(cudaMemcpyAsync(h->d_desc, h->h_desc.data(), h->h_desc.size() * sizeof(BucketDesc),
+                           cudaMemcpyHostToDevice, h->st));
+    return TSG_OK;
+}
+
+int validate_handle(tsg_engine* h) {
+    if (!h) return fail(TSG_EINVAL, "null engine handle");
+    return TSG_OK;
+}
+
+// compact every bucket by keep flags laid out in global (bucket order) index
+int compact_all(tsg_engine* h, const uint8_t* keep, const std::vector<int64_t>& base) {
+    int64_t* sel = nullptr;
+    int64_t* nsel = nullptr;
+    int64_t maxc = 0;
+    for (auto& b : h->buckets) maxc = std::max(maxc, b.count);
+    if (!maxc) return TSG_OK;
+    CKR(dalloc(h, (void**)&sel, maxc * 8));
+    CKR(dalloc(h, (void**)&nsel, 8));
+    size_t tmp_bytes = 0;
+    thrust::counting_iterator<int64_t> cnt(0);
+    cub::DeviceSelect::Flagged(nullptr, tmp_bytes, cnt, keep, sel, nsel, maxc, h->st);
+    void* tmp = nullptr;
+    CKR(dalloc(h, &tmp, (int64_t)tmp_bytes + 16));
+    for (size_t bi = 0; bi < h->buckets.size(); ++bi) {
+        Bucket& b = h->buckets[bi];
+        if (!b.count) continue;
+        CK(cub::DeviceSelect::Flagged(tmp, tmp_bytes, cnt, keep + base[bi], sel, nsel, b.count, h->st));
+        int64_t kept = 0;
+        CK(cudaMemcpyAsync(&kept, nsel, 8, cudaMemcpyDeviceToHost, h->st));
+        CK(cudaStreamSynchronize(h->st));
+        if (kept == b.count) continue;
+        Bucket nb = b;
+        nb.lits = nullptr; nb.acts = nullptr; nb.ids = nullptr; nb.origins = nullptr;
+        nb.cap = b.cap;  // keep capacity (the reference never shrinks, engine.py:184-200)
+        CKR(dalloc(h, (void**)&nb.lits, nb.cap * (int64_t)std::max(b.size, 1) * 4));
+        CKR(dalloc(h, (void**)&nb.acts, nb.cap * 8));
+        CKR(dalloc(h, (void**)&nb.ids, nb.cap * 8));
+        CKR(dalloc(h, (void**)&nb.origins, nb.cap * 4));
+        if (kept) {
+            k_compact<<<grid_for(kept), 256, 0, h->st>>>(sel, kept, b.size, b.lits, b.acts, b.ids, b.origins,
+                                                         nb.lits, nb.acts, nb.ids, nb.origins);
+            CK(cudaGetLastError());
+        }
+        dfree(h, b.lits); dfree(h, b.acts); dfree(h, b.ids); dfree(h, b.origins);
+        nb.count = kept;
+        b = nb;
+    }
+    dfree(h, tmp); dfree(h, sel); dfree(h, nsel);
+    return TSG_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* tsg_last_error(void) { return g_err.c_str(); }
+void tsg__set_error(const char* msg) { g_err = msg ? msg : ""; }
+int tsg_abi_version(void) { return TSG_ABI_VERSION; }
+
+int tsg_device_count(int32_t* n) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) { *n = 0; return fail(TSG_ECUDA, "cudaGetDeviceCount: %s", cudaGetErrorString(e)); }
+    *n = c;
+    return TSG_OK;
+}
+
+int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
+    if (!out || !cfg) return fail(TSG_EINVAL, "null argument");
+    *out = nullptr;
+    if (num_vars < 0 || num_vars > (1 << 30)) return fail(TSG_EINVAL, "num_vars out of range: %d", num_vars);
+    if (cfg->lane_width < 1 || cfg->lane_width > 64) return fail(TSG_EINVAL, "lane_width must be in 1..64, got %d", cfg->lane_width);
+    if (cfg->group_width < 1 || cfg->group_width > 64) return fail(TSG_EINVAL, "group_width must be in 1..64, got %d", cfg->group_width);
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(TSG_ECUDA, "no CUDA device");
+    if (cfg->device < 0 || cfg->device >= ndev) return fail(TSG_EINVAL, "device %d out of range (%d)", cfg->device, ndev);
+    auto* h = new tsg_engine();
+    h->dev = cfg->device;
+    h->cfg = *cfg;
+    h->V = num_vars;
+    DevGuard g(h->dev);
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, h->dev) != cudaSuccess) { delete h; return fail(TSG_ECUDA, "device properties"); }
+    h->nsm = prop.multiProcessorCount;
+    if (cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking) != cudaSuccess) { delete h; return fail(TSG_ECUDA, "stream"); }
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, h->dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    for (auto& e : h->ev) cudaEventCreate(&e);
+    if (cudaMallocHost(&h->h_ctr, 4 * sizeof(unsigned long long)) != cudaSuccess) { delete h; return fail(TSG_ECUDA, "pinned alloc"); }
+    if (dalloc(h, (void**)&h->ctr, 4 * sizeof(unsigned long long))) { delete h; return TSG_ENOMEM; }
+    h->out_cap = cfg->report_capacity > 0 ? cfg->report_capacity : (1 << 16);
+    if (dalloc(h, (void**)&h->out, h->out_cap * (int64_t)sizeof(tsg_report))) { delete h; return TSG_ENOMEM; }
+    *out = h;
+    return TSG_OK;
+}
+
+int tsg_destroy(tsg_engine* h) {
+    if (!h) return TSG_OK;
+    DevGuard g(h->dev);
+    cudaStreamSynchronize(h->st);
+    for (auto& b : h->buckets) { dfree(h, b.lits); dfree(h, b.acts); dfree(h, b.ids); dfree(h, b.origins); }
+    dfree(h, h->rows_own); dfree(h, h->tables); dfree(h, h->d_desc); dfree(h, h->out);
+    dfree(h, h->ctr); dfree(h, h->carry);
+    cudaStreamSynchronize(h->st);
+    if (h->h_ctr) cudaFreeHost(h->h_ctr);
+    for (auto& e : h->ev) if (e) cudaEventDestroy(e);
+    cudaStreamDestroy(h->st);
+    delete h;
+    return TSG_OK;
+}
+
+int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, int64_t n,
+                    const int64_t* ids, const int32_t* origins, double activity) {
+    CKR(validate_handle(h));
+    if (n <= 0) return TSG_OK;
+    if (!offsets || !ids || !origins) return fail(TSG_EINVAL, "null argument");
+    DevGuard g(h->dev);
+    // group clauses by size, preserving arrival order; new sizes create buckets
+    // in first-seen order (dict insertion order of ClauseStore.buckets)
+    std::vector<int> bucket_of(n);
+    std::vector<int64_t> per_bucket_n;
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t s64 = offsets[i + 1] - offsets[i];
+        if (s64 < 0 || s64 > (1 << 24)) return fail(TSG_EINVAL, "bad clause size");
+        int32_t s = (int32_t)s64;
+        for (int64_t j = offsets[i]; j < offsets[i + 1]; ++j) {
+            int64_t v = lits[j] < 0 ? -(int64_t)lits[j] : lits[j];
+            if (v > h->V) return fail(TSG_ERANGE, "literal %d out of range for %d variables", lits[j], h->V);
+        }
+        auto it = h->by_size.find(s);
+        int bi;
+        if (it == h->by_size.end()) {
+            bi = (int)h->buckets.size();
+            Bucket b;
+            b.size = s;
+            b.rank = bi;
+            h->buckets.push_back(b);
+            h->by_size[s] = bi;
+        } else {
+            bi = it->second;
+        }
+        bucket_of[i] = bi;
+        if ((int64_t)per_bucket_n.size() <= bi) per_bucket_n.resize(bi + 1, 0);
+        per_bucket_n[bi]++;
+    }
+    // per bucket: gather clause-major literals + metadata on the host, one H2D each
+    std::vector<std::vector<int64_t>> members(h->buckets.size());
+    for (int64_t i = 0; i < n; ++i) members[bucket_of[i]].push_back(i);
+    for (size_t bi = 0; bi < members.size(); ++bi) {
+        auto& mem = members[bi];
+        if (mem.empty()) continue;
+        Bucket& b = h->buckets[bi];
+        int64_t k = (int64_t)mem.size();
+        CKR(bucket_reserve(h, b, b.count + k));
+        std::vector<int32_t> hl((size_t)(k * b.size));
+        std::vector<int64_t> hid(k);
+        std::vector<int32_t> hor(k);
+        for (int64_t c = 0; c < k; ++c) {
+            int64_t i = mem[c];
+            if (b.size) memcpy(&hl[c * b.size], lits + offsets[i], b.size * 4);
+            hid[c] = ids[i];
+            hor[c] = origins[i];
+        }
+        if (b.size) {
+            int32_t* tmp = nullptr;
+            CKR(dalloc(h, (void**)&tmp, k * b.size * 4));
+            CK(cudaMemcpyAsync(tmp, hl.data(), k * b.size * 4, cudaMemcpyHostToDevice, h->st));
+            k_append<<<grid_for(k * b.size), 256, 0, h->st>>>(tmp, k, b.size, b.count, b.lits);
+            CK(cudaGetLastError());
+            dfree(h, tmp);
+        }
+        CK(cudaMemcpyAsync(b.ids + b.count, hid.data(), k * 8, cudaMemcpyHostToDevice, h->st));
+        CK(cudaMemcpyAsync(b.origins + b.count, hor.data(), k * 4, cudaMemcpyHostToDevice, h->st));
+        k_fill_f64<<<grid_for(k), 256, 0, h->st>>>(b.acts + b.count, k, activity);
+        CK(cudaGetLastError());
+        b.count += k;
+        CK(cudaStreamSynchronize(h->st));  // host vectors go out of scope
+    }
+    return TSG_OK;
+}
+
+int tsg_store_size(tsg_engine* h, int64_t* n) {
+    CKR(validate_handle(h));
+    *n = store_size(h);
+    return TSG_OK;
+}
+
+int tsg_bucket_count(tsg_engine* h, int32_t* nb) {
+    CKR(validate_handle(h));
+    *nb = (int32_t)h->buckets.size();
+    return TSG_OK;
+}
+
+int tsg_bucket_info(tsg_engine* h, int32_t b, int32_t* size, int64_t* count) {
+    CKR(validate_handle(h));
+    if (b < 0 || b >= (int32_t)h->buckets.size()) return fail(TSG_ERANGE, "bucket %d out of range", b);
+    *size = h->buckets[b].size;
+    *count = h->buckets[b].count;
+    return TSG_OK;
+}
+
+int tsg_bucket_read(tsg_engine* h, int32_t bi, int32_t* lits, int64_t* ids, int32_t* origins, double* acts) {
+    CKR(validate_handle(h));
+    if (bi < 0 || bi >= (int32_t)h->buckets.size()) return fail(TSG_ERANGE, "bucket %d out of range", bi);
+    DevGuard g(h->dev);
+    Bucket& b = h->buckets[bi];
+    if (!b.count) return TSG_OK;
+    if (lits && b.size) {
+        int32_t* tmp = nullptr;
+        CKR(dalloc(h, (void**)&tmp, b.count * b.size * 4));
+        k_deinterleave<<<grid_for(b.count * b.size), 256, 0, h->st>>>(b.lits, b.count, b.size, tmp);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(lits, tmp, b.count * b.size * 4, cudaMemcpyDeviceToHost, h->st));
+        dfree(h, tmp);
+    }
+    if (ids) CK(cudaMemcpyAsync(ids, b.ids, b.count * 8, cudaMemcpyDeviceToHost, h->st));
+    if (origins) CK(cudaMemcpyAsync(origins, b.origins, b.count * 4, cudaMemcpyDeviceToHost, h->st));
+    if (acts) CK(cudaMemcpyAsync(acts, b.acts, b.count * 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    return TSG_OK;
+}
+
+int tsg_scale_activities(tsg_engine* h, double factor) {
+    CKR(validate_handle(h));
+    DevGuard g(h->dev);
+    for (auto& b : h->buckets)
+        if (b.count) k_scale_f64<<<grid_for(b.count), 256, 0, h->st>>>(b.acts, b.count, factor);
+    CK(cudaGetLastError());
+    return TSG_OK;
+}
+
+int tsg_reduce(tsg_engine* h, int64_t eligible_below, int64_t target, int64_t* removed, int64_t* removed_ids) {
+    CKR(validate_handle(h));
+    DevGuard g(h->dev);
+    *removed = 0;
+    int64_t total = store_size(h);
+    if (total == 0 || target <= 0) return TSG_OK;
+    std::vector<int64_t> base(h->buckets.size());
+    int64_t acc = 0;
+    for (size_t i = 0; i < h->buckets.size(); ++i) { base[i] = acc; acc += h->buckets[i].count; }
+    uint64_t *ka = nullptr, *ki = nullptr, *ka2 = nullptr, *ki2 = nullptr;
+    int64_t *ix = nullptr, *ix2 = nullptr, *doomed_ids = nullptr;
+    uint8_t* keep = nullptr;
+    CKR(dalloc(h, (void**)&ka, total * 8)); CKR(dalloc(h, (void**)&ki, total * 8));
+    CKR(dalloc(h, (void**)&ka2, total * 8)); CKR(dalloc(h, (void**)&ki2, total * 8));
+    CKR(dalloc(h, (void**)&ix, total * 8)); CKR(dalloc(h, (void**)&ix2, total * 8));
+    CKR(dalloc(h, (void**)&keep, total));
+    CK(cudaMemsetAsync(h->ctr + 3, 0, 8, h->st));
+    for (size_t i = 0; i < h->buckets.size(); ++i) {
+        Bucket& b = h->buckets[i];
+        if (!b.count) continue;
+        k_reduce_keys<<<grid_for(b.count), 256, 0, h->st>>>(b.acts, b.ids, b.count, base[i], eligible_below,
+                                                            ka, ki, ix, h->ctr + 3);
+    }
+    CK(cudaGetLastError());
+    // stable LSD: sort by id, then stably by activity bits => (activity, id) order (engine.py:488)
+    size_t tb = 0, tb2 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, ki, ki2, ix, ix2, total, 0, 64, h->st);
+    cub::DeviceRadixSort::SortPairs(nullptr, tb2, ka, ka2, ix, ix2, total, 0, 64, h->st);
+    void* tmp = nullptr;
+    CKR(dalloc(h, &tmp, (int64_t)std::max(tb, tb2) + 16));
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, ki, ki2, ix, ix2, total, 0, 64, h->st));
+    k_gather_u64<<<grid_for(total), 256, 0, h->st>>>(ka, ix2, total, ka2);  // act keys in id order
+    CK(cudaGetLastError());
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, ka2, ka, ix2, ix, total, 0, 64, h->st));
+    unsigned long long n_el = 0;
+    CK(cudaMemcpyAsync(&n_el, h->ctr + 3, 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    int64_t rem = std::min<int64_t>(target, (int64_t)n_el);
+    if (rem > 0) {
+        CK(cudaMemsetAsync(keep, 1, total, h->st));
+        CKR(dalloc(h, (void**)&doomed_ids, rem * 8));
+        k_mark_doomed<<<grid_for(rem), 256, 0, h->st>>>(ix, rem, keep, ki, doomed_ids);
+        CK(cudaGetLastError());
+        if (removed_ids) CK(cudaMemcpyAsync(removed_ids, doomed_ids, rem * 8, cudaMemcpyDeviceToHost, h->st));
+        CKR(compact_all(h, keep, base));
+    }
+    dfree(h, tmp); dfree(h, ka); dfree(h, ki); dfree(h, ka2); dfree(h, ki2); dfree(h, ix); dfree(h, ix2);
+    dfree(h, keep); dfree(h, doomed_ids);
+    CK(cudaStreamSynchronize(h->st));
+    *removed = rem;
+    return TSG_OK;
+}
+
+int tsg_remove_clauses(tsg_engine* h, const int64_t* ids, int64_t n, int64_t* removed) {
+    CKR(validate_handle(h));
+    DevGuard g(h->dev);
+    *removed = 0;
+    int64_t total = store_size(h);
+    if (total == 0 || n <= 0) return TSG_OK;
+    std::vector<int64_t> del(ids, ids + n);
+    std::sort(del.begin(), del.end());
+    std::vector<int64_t> base(h->buckets.size());
+    int64_t acc = 0;
+    for (size_t i = 0; i < h->buckets.size(); ++i) { base[i] = acc; acc += h->buckets[i].count; }
+    int64_t* d_del = nullptr;
+    uint8_t* keep = nullptr;
+    CKR(dalloc(h, (void**)&d_del, n * 8));
+    CKR(dalloc(h, (void**)&keep, total));
+    CK(cudaMemcpyAsync(d_del, del.data(), n * 8, cudaMemcpyHostToDevice, h->st));
+    CK(cudaMemsetAsync(h->ctr + 3, 0, 8, h->st));
+    for (size_t i = 0; i < h->buckets.size(); ++i) {
+        Bucket& b = h->buckets[i];
+        if (!b.count) continue;
+        k_mark_deleted<<<grid_for(b.count), 256, 0, h->st>>>(b.ids, b.count, base[i], d_del, n, keep, h->ctr + 3);
+    }
+    CK(cudaGetLastError());
+    unsigned long long gone = 0;
+    CK(cudaMemcpyAsync(&gone, h->ctr + 3, 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    if (gone) CKR(compact_all(h, keep, base));
+    dfree(h, d_del); dfree(h, keep);
+    CK(cudaStreamSynchronize(h->st));
+    *removed = (int64_t)gone;
+    return TSG_OK;
+}
+
+int tsg_stage_snapshots(tsg_engine* h, const int8_t* rows, int64_t n_rows, int64_t row_pitch, int32_t on_device) {
+    CKR(validate_handle(h));
+    DevGuard g(h->dev);
+    if (n_rows < 0) return fail(TSG_EINVAL, "n_rows < 0");
+    if (n_rows > 0 && row_pitch < h->V + 1) return fail(TSG_EINVAL, "row pitch %lld < num_vars+1", (long long)row_pitch);
+    h->n_rows = n_rows;
+    if (n_rows == 0) return TSG_OK;
+    if (on_device && row_pitch % 4 == 0) {  // encode straight from the caller's HBM rows
+        h->rows = rows;
+        h->pitch = row_pitch;
+        return TSG_OK;
+    }
+    int64_t pitch = round_up(h->V + 1, 16);
+    int64_t need = pitch * n_rows;
+    if (need > h->rows_cap) {
+        dfree(h, h->rows_own);
+        h->rows_own = nullptr;
+        int64_t cap = std::max(need, h->rows_cap * 2);
+        CKR(dalloc(h, (void**)&h->rows_own, cap));
+        CK(cudaMemsetAsync(h->rows_own, 0, cap, h->st));  // pad bytes stay zero (Undef)
+        h->rows_cap = cap;
+    }
+    CK(cudaMemcpy2DAsync(h->rows_own, pitch, rows, row_pitch, h->V + 1, n_rows,
+                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDefault, h->st));
+    h->rows = h->rows_own;
+    h->pitch = pitch;
+    return TSG_OK;
+}
+
+int tsg_round_prepare(tsg_engine* h, const int32_t* group_lanes, const int32_t* group_tid, int32_t n_groups) {
+    CKR(validate_handle(h));
+    DevGuard g(h->dev);
+    if (n_groups < 0) return fail(TSG_EINVAL, "n_groups < 0");
+    h->n_groups = n_groups;
+    h->glanes.assign(group_lanes, group_lanes + n_groups);
+    h->gtid.assign(group_tid, group_tid + n_groups);
+    h->grow0.resize(n_groups);
+    int64_t r = 0;
+    for (int i = 0; i < n_groups; ++i) {
+        if (h->glanes[i] < 0 || h->glanes[i] > h->cfg.lane_width)
+            return fail(TSG_ECAPACITY, "%d assignments exceed lane width %d", h->glanes[i], h->cfg.lane_width);
+        h->grow0[i] = r;
+        r += h->glanes[i];
+    }
+    h->n_chunks = (n_groups + h->cfg.group_width - 1) / h->cfg.group_width;
+    h->chunk_off.resize(h->n_chunks);
+    int64_t off = 0;
+    for (int c = 0; c < h->n_chunks; ++c) {
+        int G = std::min(h->cfg.group_width, n_groups - c * h->cfg.group_width);
+        h->chunk_off[c] = off;
+        off += round_up((int64_t)(h->V + 2) * agg_entry_bytes(h), 256);
+        off += round_up((int64_t)(h->V + 2) * G * lane_entry_bytes(h), 256);
+    }
+    h->tables_bytes = off;
+    if (off > h->tables_cap) {
+        dfree(h, h->tables);
+        h->tables = nullptr;
+        CKR(dalloc(h, (void**)&h->tables, off));
+        h->tables_cap = off;
+    }
+    return TSG_OK;
+}
+
+int tsg_round_encode(tsg_engine* h) {
+    CKR(validate_handle(h));
+    DevGuard g(h->dev);
+    int64_t need_rows = h->n_groups ? h->grow0.back() + h->glanes.back() : 0;
+    if (need_rows > h->n_rows) return fail(TSG_EINVAL, "groups need %lld rows, %lld staged", (long long)need_rows, (long long)h->n_rows);
+    if (!h->n_chunks) return TSG_OK;
+    bool timing = h->cfg.flags & TSG_F_TIMING;
+    if (timing) CK(cudaEventRecord(h->ev[0], h->st));
+    CKR(do_encode(h));
+    if (timing) CK(cudaEventRecord(h->ev[1], h->st));
+    return TSG_OK;
+}
+
+int tsg_round_tables(tsg_engine* h, void** device_ptr, int64_t* bytes) {
+    CKR(validate_handle(h));
+    *device_ptr = h->tables;
+    *bytes = h->tables_bytes;
+    return TSG_OK;
+}
+
+int tsg_round_test(tsg_engine* h, double activity_inc, tsg_round_result* out) {
+    CKR(validate_handle(h));
+    DevGuard g(h->dev);
+    tsg_round_result res{};
+    res.n_chunks = h->n_chunks;
+    h->n_out = 0;
+    h->round_seq++;
+    if (h->n_chunks) {
+        CKR(build_desc(h));
+        if (h->n_chunks > 1) CKR(dgrow(h, &h->carry, &h->carry_cap, std::max<int64_t>(1, h->n_tiles * STRIDE)));
+        CK(cudaMemsetAsync(h->ctr, 0, 3 * sizeof(unsigned long long), h->st));
+        bool timing = h->cfg.flags & TSG_F_TIMING;
+        if (timing) CK(cudaEventRecord(h->ev[2], h->st));
+        CKR(run_tests(h, activity_inc, 0));
+        if (timing) CK(cudaEventRecord(h->ev[3], h->st));
+        CK(cudaMemcpyAsync(h->h_ctr, h->ctr, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
+        CK(cudaStreamSynchronize(h->st));
+        int64_t n_rec = (int64_t)h->h_ctr[0];
+        int64_t positives = (int64_t)h->h_ctr[1];
+        res.lane_triggers = (int64_t)h->h_ctr[2];
+        if (n_rec > h->out_cap) {  // overflow: grow, replay emission only (no side effects)
+            dfree(h, h->out);
+            h->out = nullptr;
+            h->out_cap = n_rec + n_rec / 4 + 1024;
+            CKR(dalloc(h, (void**)&h->out, h->out_cap * (int64_t)sizeof(tsg_report)));
+            CK(cudaMemsetAsync(h->ctr, 0, sizeof(unsigned long long), h->st));
+            CKR(run_tests(h, activity_inc, 1));
+            CK(cudaMemcpyAsync(h->h_ctr, h->ctr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
+            CK(cudaStreamSynchronize(h->st));
+            if ((int64_t)h->h_ctr[0] != n_rec) return fail(TSG_ECUDA, "report replay mismatch");
+            res.reruns = 1;
+        }
+        h->n_out = n_rec;
+        int64_t n = store_size(h);
+        int64_t lanes_total = 0;
+        for (int c = 0; c < h->n_chunks; ++c) {
+            int32_t g0 = c * h->cfg.group_width;
+            int G = std::min(h->cfg.group_width, h->n_groups - g0);
+            int64_t lanes = 0;
+            for (int gg = 0; gg < G; ++gg) lanes += h->glanes[g0 + gg];
+            res.aggregate_tests += n * G;
+            lanes_total += lanes;
+        }
+        res.clauses_tested = n * h->n_chunks;
+        res.lane_tests = n * lanes_total;
+        res.aggregate_tests_negative = res.aggregate_tests - positives;
+        res.reports = n_rec;
+        if (timing) {
+            float ms = 0;
+            if (cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]) == cudaSuccess) res.encode_ms = ms;
+            if (cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]) == cudaSuccess) res.test_ms = ms;
+        }
+    }
+    if (out) *out = res;
+    return TSG_OK;
+}
+
+int tsg_round(tsg_engine* h, const int32_t* group_lanes, const int32_t* group_tid, int32_t n_groups,
+              double activity_inc, tsg_round_result* out) {
+    CKR(tsg_round_prepare(h, group_lanes, group_tid, n_groups));
+    CKR(tsg_round_encode(h));
+    return tsg_round_test(h, activity_inc, out);
+}
+
+int tsg_fetch_reports(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n) {
+    CKR(validate_handle(h));
+    DevGuard g(h->dev);
+    int64_t k = std::min(cap, h->n_out);
+    if (k > 0) {
+        CK(cudaMemcpyAsync(out, h->out, k * sizeof(tsg_report), cudaMemcpyDeviceToHost, h->st));
+        CK(cudaStreamSynchronize(h->st));
+    }
+    *n = k;
+    return TSG_OK;
+}
+
+int tsg_reports_device(tsg_engine* h, void** device_ptr, int64_t* n) {
+    CKR(validate_handle(h));
+    *device_ptr = h->out;
+    *n = h->n_out;
+    return TSG_OK;
+}
+
+int tsg_sync(tsg_engine* h) {
+    CKR(validate_handle(h));
+    DevGuard g(h->dev);
+    CK(cudaStreamSynchronize(h->st));
+    return TSG_OK;
+}
+
+int tsg_stream(tsg_engine* h, void** stream) {
+    CKR(validate_handle(h));
+    *stream = (void*)h->st;
+    return TSG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,124 @@
+// tsg_store.cuh -- clause-store maintenance kernels: append (K6), reduce key
+// build (K7), order-preserving compaction (K8), activity scaling (K9), and the
+// literal de-interleave used by store views.  Maintenance runs between rounds;
+// none of it is on the per-round hot path.
+#pragma once
+#include <cstdint>
+
+#include "tsg_device.cuh"
+
+namespace tsg {
+
+// K6: scatter n clause-major clauses (n x size) into interleaved slots
+// [count0, count0+n) of a bucket (engine.py:150-163).
+__global__ void k_append(const int32_t* __restrict__ src, int64_t n, int32_t size, int64_t count0,
+                         int32_t* __restrict__ dst) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t total = n * size;
+    for (; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t c = i / size;
+        int32_t j = (int32_t)(i - c * size);
+        int64_t slot = count0 + c;
+        dst[(slot / STRIDE) * size * STRIDE + (int64_t)j * STRIDE + (slot % STRIDE)] = src[i];
+    }
+}
+
+__global__ void k_fill_f64(double* p, int64_t n, double v) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+// K9: ClauseStore.scale_activities (engine.py:233-235)
+__global__ void k_scale_f64(double* p, int64_t n, double f) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = __dmul_rn(p[i], f);
+}
+
+// interleaved -> clause-major (lits_at / literal_columns, engine.py:165-182)
+__global__ void k_deinterleave(const int32_t* __restrict__ src, int64_t n, int32_t size,
+                               int32_t* __restrict__ dst) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t total = n * size;
+    for (; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t c = i / size;
+        int32_t j = (int32_t)(i - c * size);
+        dst[i] = src[(c / STRIDE) * size * STRIDE + (int64_t)j * STRIDE + (c % STRIDE)];
+    }
+}
+
+// K7: reduce keys over the whole store.  Eligible clauses (id < watermark,
+// engine.py:486) get their activity bits as key (non-negative doubles order
+// like their IEEE bit patterns); ineligible ones sort last.
+__global__ void k_reduce_keys(const double* __restrict__ acts, const int64_t* __restrict__ ids,
+                              int64_t n, int64_t base, int64_t watermark,
+                              uint64_t* __restrict__ key_act, uint64_t* __restrict__ key_id,
+                              int64_t* __restrict__ idx, unsigned long long* n_eligible) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long mine = 0;
+    for (; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        bool el = ids[i] < watermark;
+        key_act[base + i] = el ? (uint64_t)__double_as_longlong(acts[i]) : ~0ull;
+        key_id[base + i] = (uint64_t)ids[i];
+        idx[base + i] = base + i;
+        mine += el;
+    }
+    for (int d = 16; d > 0; d >>= 1) mine += __shfl_down_sync(0xffffffffu, mine, d);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(n_eligible, mine);
+}
+
+__global__ void k_gather_u64(const uint64_t* __restrict__ src, const int64_t* __restrict__ idx, int64_t n,
+                             uint64_t* __restrict__ dst) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i < n; i += (int64_t)gridDim.x * blockDim.x) dst[i] = src[idx[i]];
+}
+
+__global__ void k_mark_doomed(const int64_t* __restrict__ idx, int64_t n, uint8_t* __restrict__ keep,
+                              const uint64_t* __restrict__ key_id, int64_t* __restrict__ doomed_ids) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        keep[idx[i]] = 0;
+        doomed_ids[i] = (int64_t)key_id[idx[i]];
+    }
+}
+
+// explicit delete: keep[i] = ids[i] not in sorted(del)
+__global__ void k_mark_deleted(const int64_t* __restrict__ ids, int64_t n, int64_t base,
+                               const int64_t* __restrict__ del, int64_t nd, uint8_t* __restrict__ keep,
+                               unsigned long long* removed) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long mine = 0;
+    for (; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t x = ids[i];
+        int64_t lo = 0, hi = nd;
+        while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            if (del[mid] < x) lo = mid + 1; else hi = mid;
+        }
+        bool gone = lo < nd && del[lo] == x;
+        keep[base + i] = !gone;
+        mine += gone;
+    }
+    for (int d = 16; d > 0; d >>= 1) mine += __shfl_down_sync(0xffffffffu, mine, d);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(removed, mine);
+}
+
+// K8: order-preserving compaction, _SizeBucket.compact (engine.py:184-200).
+// src_slot[k] = old slot of new slot k (from a stable select of kept slots).
+__global__ void k_compact(const int64_t* __restrict__ src_slot, int64_t kept, int32_t size,
+                          const int32_t* __restrict__ lits_in, const double* __restrict__ acts_in,
+                          const int64_t* __restrict__ ids_in, const int32_t* __restrict__ org_in,
+                          int32_t* __restrict__ lits_out, double* __restrict__ acts_out,
+                          int64_t* __restrict__ ids_out, int32_t* __restrict__ org_out) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; k < kept; k += (int64_t)gridDim.x * blockDim.x) {
+        int64_t o = src_slot[k];
+        acts_out[k] = acts_in[o];
+        ids_out[k] = ids_in[o];
+        org_out[k] = org_in[o];
+        const int32_t* s = lits_in + (o / STRIDE) * size * STRIDE + (o % STRIDE);
+        int32_t* d = lits_out + (k / STRIDE) * size * STRIDE + (k % STRIDE);
+        for (int j = 0; j < size; ++j) d[(int64_t)j * STRIDE] = s[(int64_t)j * STRIDE];
+    }
+}
+
+}  // namespace tsg

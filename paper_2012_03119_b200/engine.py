@@ -1,0 +1,446 @@
+"""The clause-exchange engine on a B200: drop-in for triggersat.engine.Engine.
+
+Same public surface as the reference (engine.py:44-525): ``EngineConfig``,
+``AssignmentSnapshot``, ``Report``, ``RoundResult``, ``RoundTrace`` and
+``Engine`` with ``add_clause`` / ``submit_assignment`` / ``drain_reports`` /
+``run_round`` / ``reduce_store`` / ``serve`` / ``raw_counters`` / ``store`` /
+``counters`` / ``trace`` / ``config``.  The host keeps what the reference
+keeps on its producer side -- the id lock, the staging list, the per-thread
+snapshot and report queues (engine.py:273-279) -- and the clause store lives
+in HBM behind the C ABI (include/tsg.h): size buckets, activities, ids and
+the round's kernels.  The only host copy of clause data is the literal tuple
+per engine id that Reports carry (engine.py:90-102).
+
+There is no CPU path: constructing an Engine without the CUDA library or a
+CUDA device raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+import time
+from collections import deque
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _lib
+from ._lib import REPORT_DTYPE, check, ptr
+
+#: Activities are rescaled when the bump increment passes this (engine.py:39-40).
+_ACTIVITY_RESCALE = 1e100
+
+
+@dataclass
+class EngineConfig:
+    """Tunables, identical to the reference (engine.py:44-74) plus the device
+    ordinal and the initial report-buffer size."""
+
+    max_clauses: int = 5_000_000
+    assignment_queue_capacity: Optional[int] = None
+    lane_width: int = 32
+    group_width: int = 32
+    activity_decay: float = 0.999
+    reduce_keep_fraction: float = 0.5
+    interleave_stride: int = 32
+    trace: bool = False
+    device: int = 0
+    report_capacity: int = 0
+    timing: bool = False
+
+    def __post_init__(self):
+        if self.max_clauses < 1:
+            raise ValueError("max_clauses must be >= 1")
+        if not 0 < self.activity_decay <= 1:
+            raise ValueError("activity_decay must be in (0, 1]")
+        if not 0 < self.reduce_keep_fraction < 1:
+            raise ValueError("reduce_keep_fraction must be in (0, 1)")
+        if self.assignment_queue_capacity is None:
+            self.assignment_queue_capacity = 2 * self.lane_width
+        if self.assignment_queue_capacity < 1:
+            raise ValueError("assignment_queue_capacity must be >= 1")
+
+
+@dataclass
+class AssignmentSnapshot:
+    """One thread's trail at a propagation fixpoint (engine.py:77-87)."""
+
+    thread_id: int
+    values: np.ndarray
+    seq: int
+
+
+@dataclass
+class Report:
+    """A stored clause that triggered for ``destination`` (engine.py:90-102)."""
+
+    destination: int
+    lits: tuple
+    engine_id: int
+    lane_mask: int
+
+
+@dataclass
+class RoundResult:
+    reports_emitted: int = 0
+    clauses_tested: int = 0
+    assignments_consumed: int = 0
+    aggregate_tests_negative: int = 0
+
+
+@dataclass
+class RoundTrace:
+    snapshots: list
+    store: list
+    reports: list
+
+
+class BucketView:
+    """Live view of one device size bucket (the reference's _SizeBucket,
+    engine.py:122-200).  Every attribute read fetches from HBM."""
+
+    def __init__(self, engine: "Engine", index: int, size: int):
+        self._e, self.index, self.size = engine, index, size
+
+    @property
+    def count(self) -> int:
+        s = C.c_int32(0)
+        n = C.c_int64(0)
+        check(self._e._L.tsg_bucket_info(self._e._h, self.index, C.byref(s), C.byref(n)))
+        return n.value
+
+    def _read(self, lits=False, ids=False, origins=False, acts=False):
+        n = self.count
+        out = [np.zeros((n, self.size), np.int32) if lits else None,
+               np.zeros(n, np.int64) if ids else None,
+               np.zeros(n, np.int32) if origins else None,
+               np.zeros(n, np.float64) if acts else None]
+        if n:
+            check(self._e._L.tsg_bucket_read(self._e._h, self.index, *(ptr(a) for a in out)))
+        return out
+
+    @property
+    def activities(self) -> np.ndarray:
+        return self._read(acts=True)[3]
+
+    @property
+    def engine_ids(self) -> np.ndarray:
+        return self._read(ids=True)[1]
+
+    @property
+    def origins(self) -> np.ndarray:
+        return self._read(origins=True)[2]
+
+    def lits_at(self, slot: int) -> tuple:
+        return tuple(int(x) for x in self._read(lits=True)[0][slot])
+
+    def literal_columns(self) -> list:
+        lits = self._read(lits=True)[0]
+        return [lits[:, j].copy() for j in range(self.size)]
+
+
+class DeviceClauseStore:
+    """The clause store as seen from the host (engine.py:203-235)."""
+
+    def __init__(self, engine: "Engine"):
+        self._e = engine
+
+    def __len__(self) -> int:
+        n = C.c_int64(0)
+        check(self._e._L.tsg_store_size(self._e._h, C.byref(n)))
+        return n.value
+
+    @property
+    def buckets(self) -> Dict[int, BucketView]:
+        """Size -> bucket, in creation order (dict insertion order)."""
+        nb = C.c_int32(0)
+        check(self._e._L.tsg_bucket_count(self._e._h, C.byref(nb)))
+        out = {}
+        for b in range(nb.value):
+            s = C.c_int32(0)
+            n = C.c_int64(0)
+            check(self._e._L.tsg_bucket_info(self._e._h, b, C.byref(s), C.byref(n)))
+            out[s.value] = BucketView(self._e, b, s.value)
+        return out
+
+    def clauses(self):
+        """(engine_id, lits, origin, activity), sorted by size then slot (engine.py:221-231)."""
+        for size, bv in sorted(self.buckets.items()):
+            lits, ids, org, acts = bv._read(True, True, True, True)
+            for k in range(len(ids)):
+                yield int(ids[k]), tuple(int(x) for x in lits[k]), int(org[k]), float(acts[k])
+
+    def scale_activities(self, factor: float) -> None:
+        check(self._e._L.tsg_scale_activities(self._e._h, factor))
+
+
+class Engine:
+    """Owns the HBM clause store and runs the exchange rounds on the GPU."""
+
+    def __init__(self, num_vars: int, thread_count: int, config: Optional[EngineConfig] = None):
+        self.config = config or EngineConfig()
+        self.num_vars = num_vars
+        self.thread_count = thread_count
+        self._L = _lib.load()
+        cfg = _lib.tsg_config(self.config.lane_width, self.config.group_width, self.config.device,
+                              _lib.TSG_F_TIMING if self.config.timing else 0,
+                              self.config.report_capacity)
+        h = C.c_void_p()
+        check(self._L.tsg_create(num_vars, C.byref(cfg), C.byref(h)))
+        self._h = h
+        self.store = DeviceClauseStore(self)
+        self._lits: Dict[int, tuple] = {}
+
+        self._id_lock = threading.Lock()
+        self._next_id = 0
+        self._staged: List[Tuple[int, tuple, int]] = []
+
+        self._queue_lock = threading.Lock()
+        self._snapshots: Dict[int, deque] = {t: deque() for t in range(thread_count)}
+        self._reports: Dict[int, deque] = {t: deque() for t in range(thread_count)}
+
+        self._activity_inc = 1.0
+        self._reduce_watermark = 0
+        self.last_round: Optional[_lib.tsg_round_result] = None
+
+        self.counters = {
+            "rounds": 0, "clauses_added": 0, "clauses_dropped": 0, "clauses_removed": 0,
+            "reduces": 0, "snapshots_accepted": 0, "snapshots_dropped": 0,
+            "snapshots_consumed": 0, "aggregate_tests": 0, "aggregate_tests_negative": 0,
+            "lane_tests": 0, "lane_triggers": 0, "reports_delivered": 0, "busy_seconds": 0.0,
+        }
+        self.trace: List[RoundTrace] = []
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._L.tsg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------
+    # producer side (solver threads), engine.py:305-343
+
+    def add_clause(self, lits: Sequence[int], origin: int) -> int:
+        lits = tuple(lits)
+        with self._id_lock:
+            engine_id = self._next_id
+            self._next_id += 1
+            self._staged.append((engine_id, lits, origin))
+        return engine_id
+
+    def submit_assignment(self, snapshot) -> bool:
+        cap = self.config.assignment_queue_capacity
+        with self._queue_lock:
+            q = self._snapshots.setdefault(snapshot.thread_id, deque())
+            if len(q) >= cap:
+                self.counters["snapshots_dropped"] += 1
+                return False
+            q.append(snapshot)
+            self.counters["snapshots_accepted"] += 1
+            return True
+
+    def drain_reports(self, thread_id: int) -> List[Report]:
+        with self._queue_lock:
+            q = self._reports.get(thread_id)
+            if not q:
+                return []
+            out = list(q)
+            q.clear()
+            return out
+
+    # ------------------------------------------------------------------
+    # engine worker side
+
+    def _insert(self, batch) -> None:
+        """Append staged (id, lits, origin) to the device store at the current
+        activity increment (engine.py:357)."""
+        if not batch:
+            return
+        n = len(batch)
+        offs = np.zeros(n + 1, dtype=np.int64)
+        for i, (_, lits, _) in enumerate(batch):
+            offs[i + 1] = offs[i] + len(lits)
+        flat = np.zeros(max(int(offs[-1]), 1), dtype=np.int32)
+        for i, (_, lits, _) in enumerate(batch):
+            if lits:
+                flat[offs[i]:offs[i + 1]] = lits
+        ids = np.fromiter((b[0] for b in batch), dtype=np.int64, count=n)
+        org = np.fromiter((b[2] for b in batch), dtype=np.int32, count=n)
+        check(self._L.tsg_add_clauses(self._h, ptr(flat), ptr(offs), n, ptr(ids), ptr(org),
+                                      self._activity_inc))
+        for eid, lits, _ in batch:
+            self._lits[eid] = lits
+        self.counters["clauses_added"] += n
+
+    def _integrate_exports(self) -> None:
+        """engine.py:348-358, batched: insert while there is room; when full,
+        reduce once per incoming clause and drop it if still full."""
+        with self._id_lock:
+            staged, self._staged = self._staged, []
+        i, n = 0, len(staged)
+        size = len(self.store)
+        while i < n:
+            room = self.config.max_clauses - size
+            if room > 0:
+                take = staged[i:i + room]
+                self._insert(take)
+                size += len(take)
+                i += len(take)
+                continue
+            self.reduce_store()
+            size = len(self.store)
+            if size >= self.config.max_clauses:
+                self.counters["clauses_dropped"] += 1
+                i += 1
+
+    def _drain_snapshots(self) -> Dict[int, list]:
+        with self._queue_lock:
+            pending = {}
+            for tid, q in self._snapshots.items():
+                if q:
+                    pending[tid] = list(q)
+                    q.clear()
+            return pending
+
+    def run_round(self) -> RoundResult:
+        """engine.py:369-435 with the test phase on the GPU."""
+        started = time.perf_counter()
+        self._integrate_exports()
+        store_snapshot = None
+        if self.config.trace:
+            store_snapshot = [(eid, lits) for eid, lits, _, _ in self.store.clauses()]
+        pending = self._drain_snapshots()
+        result = RoundResult()
+        result.assignments_consumed = sum(len(v) for v in pending.values())
+        self.counters["snapshots_consumed"] += result.assignments_consumed
+
+        # grouping (engine.py:390-399): tids ascending, lane_width per group
+        lane_width = self.config.lane_width
+        rows, lanes, tids = [], [], []
+        for tid in sorted(pending):
+            snaps = pending[tid]
+            for i in range(0, len(snaps), lane_width):
+                chunk = snaps[i:i + lane_width]
+                for j, s in enumerate(chunk):
+                    vals = np.asarray(s.values, dtype=np.int8)
+                    if vals.shape[0] != self.num_vars + 1:
+                        raise ValueError(f"assignment {j} has {vals.shape[0]} slots, "
+                                         f"expected {self.num_vars + 1}")
+                    rows.append(vals)
+                lanes.append(len(chunk))
+                tids.append(tid)
+
+        reports: List[Report] = []
+        if lanes:
+            block = np.ascontiguousarray(np.stack(rows))
+            check(self._L.tsg_stage_snapshots(self._h, ptr(block), block.shape[0], block.shape[1], 0))
+            gl = np.asarray(lanes, dtype=np.int32)
+            gt = np.asarray(tids, dtype=np.int32)
+            res = _lib.tsg_round_result()
+            check(self._L.tsg_round(self._h, ptr(gl), ptr(gt), len(lanes), self._activity_inc, C.byref(res)))
+            self.last_round = res
+            self.counters["aggregate_tests"] += res.aggregate_tests
+            self.counters["lane_tests"] += res.lane_tests
+            self.counters["lane_triggers"] += res.lane_triggers
+            self.counters["aggregate_tests_negative"] += res.aggregate_tests_negative
+            result.clauses_tested = res.clauses_tested
+            result.aggregate_tests_negative = res.aggregate_tests_negative
+            recs = self._fetch(res.reports)
+            if len(recs):
+                gw = self.config.group_width
+                grp = recs["group"].astype(np.int64)
+                order = np.lexsort((grp, recs["slot"], recs["bucket"], grp // gw))
+                recs = recs[order]
+                lits_of = self._lits
+                for eid, mask, g in zip(recs["engine_id"].tolist(), recs["lane_mask"].tolist(),
+                                        recs["group"].tolist()):
+                    tid = tids[g]
+                    reports.append(Report(tid, lits_of[eid], eid, mask))
+
+        if reports:
+            with self._queue_lock:
+                for rep in reports:
+                    self._reports.setdefault(rep.destination, deque()).append(rep)
+            self.counters["reports_delivered"] += len(reports)
+            result.reports_emitted = len(reports)
+
+        if result.assignments_consumed:  # engine.py:416-420
+            self._activity_inc /= self.config.activity_decay
+            if self._activity_inc > _ACTIVITY_RESCALE:
+                self.store.scale_activities(1.0 / _ACTIVITY_RESCALE)
+                self._activity_inc /= _ACTIVITY_RESCALE
+
+        if len(self.store) > self.config.max_clauses:
+            self.reduce_store()
+
+        if self.config.trace:
+            self.trace.append(RoundTrace(
+                snapshots=[(s.thread_id, np.array(s.values, copy=True))
+                           for snaps in pending.values() for s in snaps],
+                store=store_snapshot, reports=list(reports)))
+
+        self.counters["rounds"] += 1
+        self.counters["busy_seconds"] += time.perf_counter() - started
+        return result
+
+    def _fetch(self, n: int) -> np.ndarray:
+        recs = np.zeros(n, dtype=REPORT_DTYPE)
+        if n:
+            got = C.c_int64(0)
+            check(self._L.tsg_fetch_reports(self._h, ptr(recs), n, C.byref(got)))
+            recs = recs[:got.value]
+        return recs
+
+    def reduce_store(self) -> int:
+        """engine.py:469-505; selection and compaction run on the GPU."""
+        total = len(self.store)
+        if total == 0:
+            self._reduce_watermark = self._next_id
+            return 0
+        target = int(total * (1.0 - self.config.reduce_keep_fraction))
+        removed = C.c_int64(0)
+        ids = np.zeros(max(target, 1), dtype=np.int64)
+        check(self._L.tsg_reduce(self._h, self._reduce_watermark, target, C.byref(removed), ptr(ids)))
+        for eid in ids[:removed.value].tolist():
+            self._lits.pop(eid, None)
+        with self._id_lock:
+            self._reduce_watermark = self._next_id
+        self.counters["reduces"] += 1
+        self.counters["clauses_removed"] += removed.value
+        return removed.value
+
+    def remove_clauses(self, engine_ids: Sequence[int]) -> int:
+        """Explicit deletion (streaming config C4); order-preserving like
+        _SizeBucket.compact (engine.py:184-200).  Ids still staged (added since
+        the last round) or already gone are ignored."""
+        ids = np.asarray(list(engine_ids), dtype=np.int64)
+        if ids.size == 0:
+            return 0
+        removed = C.c_int64(0)
+        check(self._L.tsg_remove_clauses(self._h, ptr(ids), ids.size, C.byref(removed)))
+        for eid in ids.tolist():
+            self._lits.pop(eid, None)
+        self.counters["clauses_deleted"] = self.counters.get("clauses_deleted", 0) + removed.value
+        return removed.value
+
+    def serve(self, stop: threading.Event, idle_sleep: float = 0.0005) -> None:
+        while not stop.is_set():
+            result = self.run_round()
+            if result.assignments_consumed == 0:
+                time.sleep(idle_sleep)
+
+    def raw_counters(self) -> dict:
+        out = dict(self.counters)
+        out["store_size"] = len(self.store)
+        with self._id_lock:
+            out["staged_pending"] = len(self._staged)
+        with self._queue_lock:
+            out["reports_pending"] = sum(len(q) for q in self._reports.values())
+            out["snapshots_pending"] = sum(len(q) for q in self._snapshots.values())
+        return out

@@ -1,0 +1,139 @@
+"""Thin object wrapper of one C-ABI engine handle (include/tsg.h).
+
+Used by the Engine mirror's bulk paths, bench.py and the multi-GPU runner:
+bulk clause ingest from flat arrays, snapshot staging from host or device
+memory, split encode/test for table broadcast, record fetch.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Tuple
+
+import numpy as np
+
+from . import _lib
+from ._lib import REPORT_DTYPE, check, ptr
+
+
+class NativeEngine:
+    def __init__(self, num_vars: int, lane_width: int = 32, group_width: int = 32, device: int = 0,
+                 timing: bool = False, report_capacity: int = 0):
+        self.L = _lib.load()
+        self.num_vars = num_vars
+        self.lane_width, self.group_width = lane_width, group_width
+        cfg = _lib.tsg_config(lane_width, group_width, device, _lib.TSG_F_TIMING if timing else 0,
+                              report_capacity)
+        h = C.c_void_p()
+        check(self.L.tsg_create(num_vars, C.byref(cfg), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.tsg_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- store -----------------------------------------------------------
+    def add_clauses(self, flat: np.ndarray, offsets: np.ndarray, ids: np.ndarray,
+                    origins: Optional[np.ndarray] = None, activity: float = 1.0) -> None:
+        n = len(offsets) - 1
+        if origins is None:
+            origins = np.zeros(n, np.int32)
+        flat = np.ascontiguousarray(flat, np.int32)
+        if flat.size == 0:
+            flat = np.zeros(1, np.int32)
+        check(self.L.tsg_add_clauses(self.h, ptr(flat), ptr(np.ascontiguousarray(offsets, np.int64)), n,
+                                     ptr(np.ascontiguousarray(ids, np.int64)),
+                                     ptr(np.ascontiguousarray(origins, np.int32)), activity))
+
+    def __len__(self) -> int:
+        n = C.c_int64(0)
+        check(self.L.tsg_store_size(self.h, C.byref(n)))
+        return n.value
+
+    def buckets(self):
+        """[(size, lits[count,size], ids, origins, acts)] in creation order."""
+        nb = C.c_int32(0)
+        check(self.L.tsg_bucket_count(self.h, C.byref(nb)))
+        out = []
+        for b in range(nb.value):
+            s, n = C.c_int32(0), C.c_int64(0)
+            check(self.L.tsg_bucket_info(self.h, b, C.byref(s), C.byref(n)))
+            lits = np.zeros((n.value, s.value), np.int32)
+            ids = np.zeros(n.value, np.int64)
+            org = np.zeros(n.value, np.int32)
+            acts = np.zeros(n.value, np.float64)
+            if n.value:
+                check(self.L.tsg_bucket_read(self.h, b, ptr(lits), ptr(ids), ptr(org), ptr(acts)))
+            out.append((s.value, lits, ids, org, acts))
+        return out
+
+    def reduce(self, eligible_below: int, target: int) -> np.ndarray:
+        removed = C.c_int64(0)
+        ids = np.zeros(max(target, 1), np.int64)
+        check(self.L.tsg_reduce(self.h, eligible_below, target, C.byref(removed), ptr(ids)))
+        return ids[:removed.value]
+
+    def remove(self, ids) -> int:
+        a = np.ascontiguousarray(ids, np.int64)
+        removed = C.c_int64(0)
+        check(self.L.tsg_remove_clauses(self.h, ptr(a if a.size else np.zeros(1, np.int64)), a.size,
+                                        C.byref(removed)))
+        return removed.value
+
+    def scale(self, factor: float) -> None:
+        check(self.L.tsg_scale_activities(self.h, factor))
+
+    # ---- round ------------------------------------------------------------
+    def stage(self, rows: np.ndarray) -> None:
+        rows = np.ascontiguousarray(rows, np.int8)
+        check(self.L.tsg_stage_snapshots(self.h, ptr(rows), rows.shape[0], rows.shape[1], 0))
+
+    def stage_device(self, dptr: int, n_rows: int, pitch: int) -> None:
+        check(self.L.tsg_stage_snapshots(self.h, C.c_void_p(dptr), n_rows, pitch, 1))
+
+    def prepare(self, group_lanes, group_tid) -> None:
+        self._gl = np.ascontiguousarray(group_lanes, np.int32)
+        self._gt = np.ascontiguousarray(group_tid, np.int32)
+        check(self.L.tsg_round_prepare(self.h, ptr(self._gl), ptr(self._gt), len(self._gl)))
+
+    def encode(self) -> None:
+        check(self.L.tsg_round_encode(self.h))
+
+    def tables(self) -> Tuple[int, int]:
+        p, n = C.c_void_p(), C.c_int64(0)
+        check(self.L.tsg_round_tables(self.h, C.byref(p), C.byref(n)))
+        return p.value or 0, n.value
+
+    def test(self, activity_inc: float = 1.0) -> _lib.tsg_round_result:
+        res = _lib.tsg_round_result()
+        check(self.L.tsg_round_test(self.h, activity_inc, C.byref(res)))
+        return res
+
+    def round(self, group_lanes, group_tid, activity_inc: float = 1.0) -> _lib.tsg_round_result:
+        gl = np.ascontiguousarray(group_lanes, np.int32)
+        gt = np.ascontiguousarray(group_tid, np.int32)
+        res = _lib.tsg_round_result()
+        check(self.L.tsg_round(self.h, ptr(gl), ptr(gt), len(gl), activity_inc, C.byref(res)))
+        return res
+
+    def fetch(self, n: int, out: Optional[np.ndarray] = None) -> np.ndarray:
+        if out is None or len(out) < n:
+            out = np.zeros(max(n, 1), REPORT_DTYPE)
+        got = C.c_int64(0)
+        if n:
+            check(self.L.tsg_fetch_reports(self.h, ptr(out), n, C.byref(got)))
+        return out[:got.value]
+
+    def sync(self) -> None:
+        check(self.L.tsg_sync(self.h))
+
+    def stream(self) -> int:
+        s = C.c_void_p()
+        check(self.L.tsg_stream(self.h, C.byref(s)))
+        return s.value or 0

@@ -1,0 +1,55 @@
+"""CPU-side checks of the C ABI: the in-tree library loads without a GPU and
+exports every entry point include/tsg.h declares; without a device the
+product fails loudly instead of falling back to a CPU path."""
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "tsg.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\**\s+\**(tsg_[a-z_0-9]+)\s*\(", src, re.M)))
+
+
+def test_header_declares_the_bound_symbols():
+    from paper_2012_03119_b200 import _lib
+    assert set(header_symbols()) == set(_lib.EXPORTS)
+
+
+def test_library_loads_and_exports_every_symbol():
+    from paper_2012_03119_b200 import _lib
+    L = _lib.load()
+    for name in header_symbols():
+        assert hasattr(L, name), name
+    assert L.tsg_abi_version() == 1
+
+
+def test_no_cpu_fallback_without_device():
+    from paper_2012_03119_b200 import _lib
+    import paper_2012_03119_b200 as P
+    if _lib.device_count() > 0:
+        pytest.skip("a CUDA device is present")
+    with pytest.raises(P.TsgError):
+        P.Engine(10, 2)
+    with pytest.raises(P.TsgError):
+        P.pack_assignments([[0, 1]], 1, 8)
+
+
+def test_host_side_validation_matches_reference():
+    import paper_2012_03119_b200 as P
+    with pytest.raises(ValueError):
+        P.EngineConfig(max_clauses=0)
+    with pytest.raises(ValueError):
+        P.EngineConfig(activity_decay=0.0)
+    with pytest.raises(ValueError):
+        P.EngineConfig(reduce_keep_fraction=1.0)
+    with pytest.raises(ValueError):
+        P.EngineConfig(assignment_queue_capacity=0)
+    assert P.EngineConfig(lane_width=8).assignment_queue_capacity == 16
+    with pytest.raises(P.CapacityError):
+        P.pack_assignments([[0, 0]] * 3, 1, lane_width=2)
+    with pytest.raises(ValueError):
+        P.pack_assignments([], 1, lane_width=65)

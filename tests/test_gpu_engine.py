@@ -1,0 +1,259 @@
+"""The GPU Engine vs the reference (golden scenarios recorded from the
+reference Engine itself) and vs the CPU oracle at config sizes.
+
+Parity bar: bit-exact -- identical ordered report lists per thread,
+identical counters, identical store contents with activities compared as
+float.hex (engine.py:460 rounding, no FMA)."""
+import threading
+import time
+
+import numpy as np
+import pytest
+
+from golden_io import engine_golden
+from gpu_util import require_device
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    require_device()
+    import paper_2012_03119_b200 as P
+    return P
+
+
+def replay(P, spec):
+    eng = P.Engine(spec["num_vars"], spec["threads"], P.EngineConfig(**spec["config"]))
+    for op, exp in zip(spec["ops"], spec["expect"]):
+        if op[0] == "add":
+            assert eng.add_clause(op[1], origin=op[2]) == exp["id"]
+        elif op[0] == "submit":
+            snap = P.AssignmentSnapshot(op[1], np.asarray(op[3], dtype=np.int8), op[2])
+            assert eng.submit_assignment(snap) == exp["ok"]
+        else:
+            if op[0] == "round":
+                r = eng.run_round()
+                got = [r.reports_emitted, r.clauses_tested, r.assignments_consumed, r.aggregate_tests_negative]
+                assert got == exp["result"], spec["name"]
+            else:
+                assert eng.reduce_store() == exp["removed"], spec["name"]
+            for t in spec["observe_threads"]:
+                got = [[list(r.lits), r.engine_id, r.lane_mask, r.destination] for r in eng.drain_reports(t)]
+                assert got == exp["reports"][str(t)], (spec["name"], t)
+            counters = {k: v for k, v in eng.raw_counters().items() if k != "busy_seconds"}
+            assert counters == exp["counters"], spec["name"]
+            store = [[eid, list(l), o, float(a).hex()] for eid, l, o, a in eng.store.clauses()]
+            assert store == exp["store"], spec["name"]
+            assert [[s, b.count] for s, b in eng.store.buckets.items()] == exp["bucket_order"]
+            assert float(eng._activity_inc).hex() == exp["activity_inc"]
+    eng.close()
+
+
+def test_reference_scenarios_bit_exact(P):
+    for spec in engine_golden():
+        replay(P, spec)
+
+
+# ---- ported from the reference's tests/test_engine.py ---------------------
+
+def snap(P, tid, seq, nv, mapping):
+    v = np.zeros(nv + 1, dtype=np.int8)
+    for k, w in mapping.items():
+        v[k] = w
+    return P.AssignmentSnapshot(tid, v, seq)
+
+
+def test_trigger_bumps_activity(P):
+    e = P.Engine(2, 1)
+    e.add_clause((1,), origin=0)
+    e.run_round()
+    bucket = e.store.buckets[1]
+    before = float(bucket.activities[0])
+    e.submit_assignment(snap(P, 0, 0, 2, {1: -1}))
+    e.run_round()
+    assert float(bucket.activities[0]) > before
+
+
+def test_trace_records_snapshots_store_and_reports(P):
+    e = P.Engine(2, 1, P.EngineConfig(trace=True))
+    e.add_clause((1, 2), origin=0)
+    e.submit_assignment(snap(P, 0, 0, 2, {1: -1, 2: -1}))
+    e.run_round()
+    assert len(e.trace) == 1
+    t = e.trace[0]
+    assert t.store == [(0, (1, 2))]
+    tid, values = t.snapshots[0]
+    assert tid == 0 and values[1] == -1
+    assert len(t.reports) == 1
+
+
+def test_serve_loop_runs_until_stopped(P):
+    e = P.Engine(2, 1)
+    e.add_clause((1, 2), origin=0)
+    stop = threading.Event()
+    w = threading.Thread(target=e.serve, args=(stop,))
+    w.start()
+    e.submit_assignment(snap(P, 0, 0, 2, {1: -1, 2: -1}))
+    deadline = time.time() + 10
+    reps = []
+    while time.time() < deadline and not reps:
+        reps = e.drain_reports(0)
+        time.sleep(0.005)
+    stop.set()
+    w.join(timeout=10)
+    assert not w.is_alive() and len(reps) == 1
+
+
+def test_raw_counters_and_empty_round(P):
+    e = P.Engine(2, 1)
+    e.add_clause((1,), origin=0)
+    e.submit_assignment(snap(P, 0, 0, 2, {}))
+    c = e.raw_counters()
+    assert c["staged_pending"] == 1 and c["snapshots_pending"] == 1 and c["reports_pending"] == 0
+    e2 = P.Engine(2, 1)
+    r = e2.run_round()
+    assert r.assignments_consumed == 0 and r.reports_emitted == 0 and e2.counters["rounds"] == 1
+
+
+def test_literal_out_of_range_raises(P):
+    e = P.Engine(3, 1)
+    e.add_clause((1, 7), origin=0)
+    with pytest.raises(IndexError):
+        e.run_round()
+
+
+# ---- config-scale parity vs the CPU oracle ---------------------------------
+
+def run_both(P, cfg_name=None, n=None, threads=None, lanes=None, nv=None, lane_width=32, group_width=32,
+             seed=0, inc=1.0, rounds=1, size_lo=2, size_hi=30):
+    from paper_2012_03119_b200 import workload as W
+    from paper_2012_03119_b200.native import NativeEngine
+    if cfg_name:
+        c = W.CONFIGS[cfg_name]
+        n, threads, lanes, nv, seed = c.n_clauses, c.threads, c.lanes, c.num_vars, c.seed
+    rng = np.random.default_rng(seed)
+    buckets = W.clause_buckets(n, nv, rng, size_lo, size_hi)
+    flat, offs, ids = W.flatten(buckets)
+    org = (ids % 7).astype(np.int32)
+    dev = NativeEngine(nv, lane_width, group_width)
+    dev.add_clauses(flat, offs, ids, org, 1.0)
+    ora = O.OracleStore()
+    k = 0
+    for s, arr in buckets.items():
+        for row in arr:
+            ora.insert(row.tolist(), int(ids[k]), int(org[k]), 1.0)
+            k += 1
+    for r in range(rounds):
+        snaps = W.snapshots(threads, lanes, nv, rng)
+        gl, gt = W.groups_for(threads, lanes, lane_width)
+        dev.stage(snaps)
+        res = dev.round(gl, gt, inc)
+        recs = dev.fetch(res.reports)
+        orecs, octr = ora.test_round(nv, snaps, gl, gt, lane_width, group_width, inc, nthreads=8)
+        gw = group_width
+        order = np.lexsort((recs["group"], recs["slot"], recs["bucket"], recs["group"] // gw))
+        recs = recs[order]
+        assert len(recs) == len(orecs)
+        for f in ("engine_id", "lane_mask", "group", "bucket", "slot"):
+            assert np.array_equal(recs[f], orecs[f]), f
+        assert res.clauses_tested == octr["clauses_tested"]
+        assert res.aggregate_tests == octr["aggregate_tests"]
+        assert res.aggregate_tests_negative == octr["aggregate_tests_negative"]
+        assert res.lane_tests == octr["lane_tests"]
+        assert res.lane_triggers == octr["lane_triggers"]
+        inc = inc / 0.999
+    for (s, lits, ids_d, org_d, acts_d), (s2, n2, lits2, ids2, org2, acts2) in zip(dev.buckets(), ora.buckets()):
+        assert s == s2 and np.array_equal(lits, lits2) and np.array_equal(ids_d, ids2)
+        assert np.array_equal(org_d, org2)
+        assert np.array_equal(acts_d.view(np.uint64), acts2.view(np.uint64))  # bit-exact fp64
+    return res
+
+
+def test_c1_parity_vs_oracle(P):
+    res = run_both(P, "C1", rounds=2)
+    assert res.reports > 0 and res.lane_triggers > 0
+
+
+@pytest.mark.parametrize("lw,gw,threads,lanes", [(32, 32, 3, 40), (64, 64, 2, 64), (64, 8, 5, 70),
+                                                 (7, 3, 4, 20), (1, 64, 3, 30), (32, 16, 40, 32)])
+def test_widths_and_multichunk_parity(P, lw, gw, threads, lanes):
+    run_both(P, n=20_000, threads=threads, lanes=lanes, nv=300, lane_width=lw, group_width=gw,
+             seed=lw * 100 + gw, rounds=2, size_lo=0, size_hi=12)
+
+
+def test_long_clauses_parity(P):
+    run_both(P, n=3000, threads=4, lanes=32, nv=2000, seed=9, size_lo=100, size_hi=400)
+
+
+def test_reduce_and_remove_parity(P):
+    from paper_2012_03119_b200 import workload as W
+    from paper_2012_03119_b200.native import NativeEngine
+    rng = np.random.default_rng(3)
+    nv = 500
+    buckets = W.clause_buckets(30_000, nv, rng, 1, 20)
+    flat, offs, ids = W.flatten(buckets)
+    org = np.zeros(len(ids), np.int32)
+    dev = NativeEngine(nv)
+    dev.add_clauses(flat, offs, ids, org, 1.0)
+    ora = O.OracleStore()
+    k = 0
+    for s, arr in buckets.items():
+        for row in arr:
+            ora.insert(row.tolist(), int(ids[k]), 0, 1.0)
+            k += 1
+    inc = 1.0
+    for r in range(3):  # create activity diversity with ties
+        snaps = W.snapshots(2, 32, nv, rng)
+        gl, gt = W.groups_for(2, 32)
+        dev.stage(snaps)
+        dev.round(gl, gt, inc)
+        ora.test_round(nv, snaps, gl, gt, 32, 32, inc)
+        inc *= 2
+    got = dev.reduce(20_000, 9_000)
+    n, want = ora.reduce(20_000, 9_000)
+    assert np.array_equal(got, want)
+    dels = rng.choice(ids, 2000, replace=False)
+    assert dev.remove(dels) == ora.remove(dels.tolist())
+    dev.scale(1e-100)
+    ora.scale(1e-100)
+    for (s, lits, i1, o1, a1), (s2, n2, lits2, i2, o2, a2) in zip(dev.buckets(), ora.buckets()):
+        assert np.array_equal(lits, lits2) and np.array_equal(i1, i2)
+        assert np.array_equal(a1.view(np.uint64), a2.view(np.uint64))
+    # the store keeps testing correctly after compaction
+    snaps = W.snapshots(2, 32, nv, rng)
+    gl, gt = W.groups_for(2, 32)
+    dev.stage(snaps)
+    res = dev.round(gl, gt, 3.0)
+    recs, ctr = ora.test_round(nv, snaps, gl, gt, 32, 32, 3.0)
+    assert res.reports == len(recs) and res.lane_triggers == ctr["lane_triggers"]
+
+
+def test_report_buffer_overflow_replay(P):
+    from paper_2012_03119_b200 import workload as W
+    from paper_2012_03119_b200.native import NativeEngine
+    rng = np.random.default_rng(11)
+    nv = 50
+    buckets = W.clause_buckets(50_000, nv, rng, 1, 3)
+    flat, offs, ids = W.flatten(buckets)
+    dev = NativeEngine(nv, report_capacity=16)
+    dev.add_clauses(flat, offs, ids)
+    snaps = W.snapshots(4, 32, nv, rng)
+    gl, gt = W.groups_for(4, 32)
+    dev.stage(snaps)
+    res = dev.round(gl, gt, 1.0)
+    assert res.reruns == 1 and res.reports > 16
+    ora = O.OracleStore()
+    k = 0
+    for s, arr in buckets.items():
+        for row in arr:
+            ora.insert(row.tolist(), int(ids[k]), 0, 1.0)
+            k += 1
+    orecs, octr = ora.test_round(nv, snaps, gl, gt, 32, 32, 1.0)
+    recs = dev.fetch(res.reports)
+    assert sorted(zip(recs["engine_id"].tolist(), recs["group"].tolist(), recs["lane_mask"].tolist())) == \
+        sorted(zip(orecs["engine_id"].tolist(), orecs["group"].tolist(), orecs["lane_mask"].tolist()))
+    acts_dev = np.concatenate([b[4] for b in dev.buckets()])
+    acts_ora = np.concatenate([b[5] for b in ora.buckets()])
+    assert np.array_equal(acts_dev.view(np.uint64), acts_ora.view(np.uint64))
