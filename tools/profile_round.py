@@ -1,0 +1,37 @@
+"""Run a few device-resident rounds of a config (for ncu / nsys-less profiling).
+
+    python tools/profile_round.py [C3] [rounds]
+"""
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2012_03119_b200 import workload as W  # noqa: E402
+from paper_2012_03119_b200.native import NativeEngine  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "C3"
+rounds = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+cfg = W.CONFIGS[name]
+rng = np.random.default_rng(cfg.seed)
+b = W.clause_buckets(cfg.n_clauses, cfg.num_vars, rng)
+flat, offs, ids = W.flatten(b)
+eng = NativeEngine(cfg.num_vars, timing=True, report_capacity=8 << 20)
+eng.add_clauses(flat, offs, ids)
+snaps = W.snapshots(cfg.threads, cfg.lanes, cfg.num_vars, np.random.default_rng(cfg.seed + 999))
+gl, gt = W.groups_for(cfg.threads, cfg.lanes)
+pitch = (cfg.num_vars + 1 + 15) // 16 * 16
+d = torch.zeros((snaps.shape[0], pitch), dtype=torch.int8, device="cuda")
+d[:, :cfg.num_vars + 1] = torch.from_numpy(snaps).cuda()
+torch.cuda.synchronize()
+eng.stage_device(d.data_ptr(), snaps.shape[0], pitch)
+eng.prepare(gl, gt)
+for r in range(rounds):
+    eng.encode()
+    res = eng.test(1.0)
+    print(f"round {r}: encode {res.encode_ms:.3f} ms test {res.test_ms:.3f} ms reports {res.reports} "
+          f"lane_triggers {res.lane_triggers} neg {res.aggregate_tests_negative}/{res.aggregate_tests}", flush=True)
