@@ -13,7 +13,7 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtsg.so")
+LIB_PATH = os.environ.get("TSG_LIB", os.path.join(HERE, "libtsg.so"))
 
 TSG_OK, TSG_EINVAL, TSG_ECAPACITY, TSG_ERANGE, TSG_ECUDA, TSG_ENOMEM = range(6)
 TSG_F_TIMING = 1

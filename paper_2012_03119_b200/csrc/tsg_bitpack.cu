@@ -150,12 +150,14 @@ int tsg_pack(int32_t device, const int8_t* rows, int64_t n, int64_t row_pitch, i
     CK2(cudaMemset(d_rows.p, 0, std::max<int64_t>(pitch * n, 16)));
     if (n) CK2(cudaMemcpy2D(d_rows.p, pitch, rows, row_pitch, num_vars + 1, n, cudaMemcpyHostToDevice));
     int64_t nv2 = (int64_t)num_vars + 2;
-    const int64_t lane_bytes = (nv2 * (int64_t)sizeof(LaneEntry<uint64_t>) + 255) / 256 * 256;
+    const int64_t vstride = (nv2 + 3) / 4 * 4;
+    const int64_t lane_bytes = (vstride * (int64_t)sizeof(LaneEntry<uint64_t>) + 255) / 256 * 256;
     CK2(cudaMalloc(&d_lane.p, lane_bytes + nv2 * sizeof(AggEntry<uint64_t>)));
     EncodeChunk c{};
     c.G = 1;
     c.num_vars = num_vars;
     c.pitch = pitch;
+    c.vstride = vstride;
     c.row0[0] = 0;
     c.lanes[0] = (int32_t)n;
     auto* lane = (LaneEntry<uint64_t>*)d_lane.p;

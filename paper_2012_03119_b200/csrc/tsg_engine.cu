@@ -99,9 +99,12 @@ struct tsg_engine {
     int64_t n_tiles = 0;
 
     tsg_report* out = nullptr;
-    int64_t out_cap = 0, n_out = 0;
-    unsigned long long* ctr = nullptr;      // device [0..3]
-    unsigned long long* h_ctr = nullptr;    // pinned [4]
+    int64_t out_cap = 0, n_out = 0, n_alloc = 0;
+    tsg_report* out2 = nullptr;             // compaction target for fetch
+    int64_t out2_cap = 0;
+    bool compacted = true;
+    unsigned long long* ctr = nullptr;      // device [0..7]: [0..3] round counters, [4] maintenance scratch
+    unsigned long long* h_ctr = nullptr;    // pinned [8]
     int64_t* carry = nullptr;
     int64_t carry_cap = 0;
     int64_t round_seq = 0;
@@ -177,6 +180,8 @@ int bucket_reserve(tsg_engine* h, Bucket& b, int64_t need) {
 bool wide_lane(const tsg_engine* h) { return h->cfg.lane_width > 32; }
 bool wide_group(const tsg_engine* h) { return h->cfg.group_width > 32; }
 int64_t agg_entry_bytes(const tsg_engine* h) { return wide_group(h) ? 32 : 16; }
+int64_t vstride(const tsg_engine* h) { return round_up((int64_t)h->V + 2, 4); }
+int64_t agg_bytes(const tsg_engine* h) { return round_up((int64_t)(h->V + 2) * agg_entry_bytes(h), 256); }
 int64_t lane_entry_bytes(const tsg_engine* h) { return wide_lane(h) ? 16 : 8; }
 
 template <class LW, class GW>
@@ -186,12 +191,13 @@ int launch_encode(tsg_engine* h, int c) {
     ec.G = std::min(h->cfg.group_width, h->n_groups - g0);
     ec.num_vars = h->V;
     ec.pitch = h->pitch;
+    ec.vstride = vstride(h);
     for (int g = 0; g < ec.G; ++g) {
         ec.row0[g] = h->grow0[g0 + g];
         ec.lanes[g] = h->glanes[g0 + g];
     }
     auto* agg = reinterpret_cast<AggEntry<GW>*>(h->tables + h->chunk_off[c]);
-    auto* lane = reinterpret_cast<LaneEntry<LW>*>(h->tables + h->chunk_off[c] + (int64_t)(h->V + 2) * sizeof(AggEntry<GW>));
+    auto* lane = reinterpret_cast<LaneEntry<LW>*>(h->tables + h->chunk_off[c] + agg_bytes(h));
     dim3 grid((unsigned)((h->V + 2 + 127) / 128)), block(32, 8);
     k_encode<LW, GW><<<grid, block, 0, h->st>>>(h->rows, ec, lane, agg);
     CK(cudaGetLastError());
@@ -218,7 +224,8 @@ int launch_test(tsg_engine* h, int c, double inc, int emit_only) {
     p.G = G;
     p.n_tiles = h->n_tiles;
     p.agg = reinterpret_cast<const AggEntry<GW>*>(h->tables + h->chunk_off[c]);
-    p.lane = reinterpret_cast<const LaneEntry<LW>*>(h->tables + h->chunk_off[c] + (int64_t)(h->V + 2) * sizeof(AggEntry<GW>));
+    p.lane = reinterpret_cast<const LaneEntry<LW>*>(h->tables + h->chunk_off[c] + agg_bytes(h));
+    p.vstride = vstride(h);
     p.sentinel = h->V + 1;
     p.g0 = g0;
     p.group_mask = width_mask<GW>(G);
@@ -330,6 +337,30 @@ int compact_all(tsg_engine* h, const uint8_t* keep, const std::vector<int64_t>& 
     return TSG_OK;
 }
 
+struct ValidReport {
+    __host__ __device__ bool operator()(const tsg_report& r) const { return r.engine_id >= 0; }
+};
+
+// squeeze the padding slots out of the round's records (order-preserving)
+int compact_reports(tsg_engine* h) {
+    if (h->compacted) return TSG_OK;
+    CKR(dgrow(h, &h->out2, &h->out2_cap, std::max<int64_t>(h->n_out, 1)));
+    int64_t* nsel = nullptr;
+    CKR(dalloc(h, (void**)&nsel, 8));
+    size_t tb = 0;
+    cub::DeviceSelect::If(nullptr, tb, h->out, h->out2, nsel, h->n_alloc, ValidReport(), h->st);
+    void* tmp = nullptr;
+    CKR(dalloc(h, &tmp, (int64_t)tb + 16));
+    CK(cub::DeviceSelect::If(tmp, tb, h->out, h->out2, nsel, h->n_alloc, ValidReport(), h->st));
+    dfree(h, tmp);
+    dfree(h, nsel);
+    std::swap(h->out, h->out2);
+    std::swap(h->out_cap, h->out2_cap);
+    h->n_alloc = h->n_out;
+    h->compacted = true;
+    return TSG_OK;
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -371,8 +402,8 @@ int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     for (auto& e : h->ev) cudaEventCreate(&e);
-    if (cudaMallocHost(&h->h_ctr, 4 * sizeof(unsigned long long)) != cudaSuccess) { delete h; return fail(TSG_ECUDA, "pinned alloc"); }
-    if (dalloc(h, (void**)&h->ctr, 4 * sizeof(unsigned long long))) { delete h; return TSG_ENOMEM; }
+    if (cudaMallocHost(&h->h_ctr, 8 * sizeof(unsigned long long)) != cudaSuccess) { delete h; return fail(TSG_ECUDA, "pinned alloc"); }
+    if (dalloc(h, (void**)&h->ctr, 8 * sizeof(unsigned long long))) { delete h; return TSG_ENOMEM; }
     h->out_cap = cfg->report_capacity > 0 ? cfg->report_capacity : (1 << 16);
     if (dalloc(h, (void**)&h->out, h->out_cap * (int64_t)sizeof(tsg_report))) { delete h; return TSG_ENOMEM; }
     *out = h;
@@ -385,7 +416,7 @@ int tsg_destroy(tsg_engine* h) {
     cudaStreamSynchronize(h->st);
     for (auto& b : h->buckets) { dfree(h, b.lits); dfree(h, b.acts); dfree(h, b.ids); dfree(h, b.origins); }
     dfree(h, h->rows_own); dfree(h, h->tables); dfree(h, h->d_desc); dfree(h, h->out);
-    dfree(h, h->ctr); dfree(h, h->carry);
+    dfree(h, h->ctr); dfree(h, h->carry); dfree(h, h->out2);
     cudaStreamSynchronize(h->st);
     if (h->h_ctr) cudaFreeHost(h->h_ctr);
     for (auto& e : h->ev) if (e) cudaEventDestroy(e);
@@ -530,12 +561,12 @@ int tsg_reduce(tsg_engine* h, int64_t eligible_below, int64_t target, int64_t* r
     CKR(dalloc(h, (void**)&ka2, total * 8)); CKR(dalloc(h, (void**)&ki2, total * 8));
     CKR(dalloc(h, (void**)&ix, total * 8)); CKR(dalloc(h, (void**)&ix2, total * 8));
     CKR(dalloc(h, (void**)&keep, total));
-    CK(cudaMemsetAsync(h->ctr + 3, 0, 8, h->st));
+    CK(cudaMemsetAsync(h->ctr + 4, 0, 8, h->st));
     for (size_t i = 0; i < h->buckets.size(); ++i) {
         Bucket& b = h->buckets[i];
         if (!b.count) continue;
         k_reduce_keys<<<grid_for(b.count), 256, 0, h->st>>>(b.acts, b.ids, b.count, base[i], eligible_below,
-                                                            ka, ki, ix, h->ctr + 3);
+                                                            ka, ki, ix, h->ctr + 4);
     }
     CK(cudaGetLastError());
     // stable LSD: sort by id, then stably by activity bits => (activity, id) order (engine.py:488)
@@ -549,7 +580,7 @@ int tsg_reduce(tsg_engine* h, int64_t eligible_below, int64_t target, int64_t* r
     CK(cudaGetLastError());
     CK(cub::DeviceRadixSort::SortPairs(tmp, tb, ka2, ka, ix2, ix, total, 0, 64, h->st));
     unsigned long long n_el = 0;
-    CK(cudaMemcpyAsync(&n_el, h->ctr + 3, 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaMemcpyAsync(&n_el, h->ctr + 4, 8, cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
     int64_t rem = std::min<int64_t>(target, (int64_t)n_el);
     if (rem > 0) {
@@ -583,15 +614,15 @@ int tsg_remove_clauses(tsg_engine* h, const int64_t* ids, int64_t n, int64_t* re
     CKR(dalloc(h, (void**)&d_del, n * 8));
     CKR(dalloc(h, (void**)&keep, total));
     CK(cudaMemcpyAsync(d_del, del.data(), n * 8, cudaMemcpyHostToDevice, h->st));
-    CK(cudaMemsetAsync(h->ctr + 3, 0, 8, h->st));
+    CK(cudaMemsetAsync(h->ctr + 4, 0, 8, h->st));
     for (size_t i = 0; i < h->buckets.size(); ++i) {
         Bucket& b = h->buckets[i];
         if (!b.count) continue;
-        k_mark_deleted<<<grid_for(b.count), 256, 0, h->st>>>(b.ids, b.count, base[i], d_del, n, keep, h->ctr + 3);
+        k_mark_deleted<<<grid_for(b.count), 256, 0, h->st>>>(b.ids, b.count, base[i], d_del, n, keep, h->ctr + 4);
     }
     CK(cudaGetLastError());
     unsigned long long gone = 0;
-    CK(cudaMemcpyAsync(&gone, h->ctr + 3, 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaMemcpyAsync(&gone, h->ctr + 4, 8, cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
     if (gone) CKR(compact_all(h, keep, base));
     dfree(h, d_del); dfree(h, keep);
@@ -650,8 +681,8 @@ int tsg_round_prepare(tsg_engine* h, const int32_t* group_lanes, const int32_t* 
     for (int c = 0; c < h->n_chunks; ++c) {
         int G = std::min(h->cfg.group_width, n_groups - c * h->cfg.group_width);
         h->chunk_off[c] = off;
-        off += round_up((int64_t)(h->V + 2) * agg_entry_bytes(h), 256);
-        off += round_up((int64_t)(h->V + 2) * G * lane_entry_bytes(h), 256);
+        off += agg_bytes(h);
+        off += round_up(vstride(h) * G * lane_entry_bytes(h), 256);
     }
     h->tables_bytes = off;
     if (off > h->tables_cap) {
@@ -689,33 +720,39 @@ int tsg_round_test(tsg_engine* h, double activity_inc, tsg_round_result* out) {
     tsg_round_result res{};
     res.n_chunks = h->n_chunks;
     h->n_out = 0;
+    h->n_alloc = 0;
+    h->compacted = true;
     h->round_seq++;
     if (h->n_chunks) {
         CKR(build_desc(h));
         if (h->n_chunks > 1) CKR(dgrow(h, &h->carry, &h->carry_cap, std::max<int64_t>(1, h->n_tiles * STRIDE)));
-        CK(cudaMemsetAsync(h->ctr, 0, 3 * sizeof(unsigned long long), h->st));
+        CK(cudaMemsetAsync(h->ctr, 0, 4 * sizeof(unsigned long long), h->st));
         bool timing = h->cfg.flags & TSG_F_TIMING;
         if (timing) CK(cudaEventRecord(h->ev[2], h->st));
         CKR(run_tests(h, activity_inc, 0));
         if (timing) CK(cudaEventRecord(h->ev[3], h->st));
-        CK(cudaMemcpyAsync(h->h_ctr, h->ctr, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
+        CK(cudaMemcpyAsync(h->h_ctr, h->ctr, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
         CK(cudaStreamSynchronize(h->st));
-        int64_t n_rec = (int64_t)h->h_ctr[0];
+        int64_t n_slots = (int64_t)h->h_ctr[0];
         int64_t positives = (int64_t)h->h_ctr[1];
         res.lane_triggers = (int64_t)h->h_ctr[2];
-        if (n_rec > h->out_cap) {  // overflow: grow, replay emission only (no side effects)
+        int64_t n_rec = (int64_t)h->h_ctr[3];
+        if (n_slots > h->out_cap) {  // overflow: grow, replay emission only (no side effects)
             dfree(h, h->out);
             h->out = nullptr;
-            h->out_cap = n_rec + n_rec / 4 + 1024;
+            h->out_cap = n_slots + n_slots / 4 + 1024;
             CKR(dalloc(h, (void**)&h->out, h->out_cap * (int64_t)sizeof(tsg_report)));
-            CK(cudaMemsetAsync(h->ctr, 0, sizeof(unsigned long long), h->st));
+            CK(cudaMemsetAsync(h->ctr, 0, 4 * sizeof(unsigned long long), h->st));
             CKR(run_tests(h, activity_inc, 1));
-            CK(cudaMemcpyAsync(h->h_ctr, h->ctr, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
+            CK(cudaMemcpyAsync(h->h_ctr, h->ctr, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
             CK(cudaStreamSynchronize(h->st));
-            if ((int64_t)h->h_ctr[0] != n_rec) return fail(TSG_ECUDA, "report replay mismatch");
+            if ((int64_t)h->h_ctr[3] != n_rec || (int64_t)h->h_ctr[0] != n_slots)
+                return fail(TSG_ECUDA, "report replay mismatch");
             res.reruns = 1;
         }
         h->n_out = n_rec;
+        h->n_alloc = n_slots;
+        h->compacted = n_slots == n_rec;
         int64_t n = store_size(h);
         int64_t lanes_total = 0;
         for (int c = 0; c < h->n_chunks; ++c) {
@@ -750,6 +787,7 @@ int tsg_round(tsg_engine* h, const int32_t* group_lanes, const int32_t* group_ti
 int tsg_fetch_reports(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n) {
     CKR(validate_handle(h));
     DevGuard g(h->dev);
+    CKR(compact_reports(h));
     int64_t k = std::min(cap, h->n_out);
     if (k > 0) {
         CK(cudaMemcpyAsync(out, h->out, k * sizeof(tsg_report), cudaMemcpyDeviceToHost, h->st));
@@ -761,6 +799,8 @@ int tsg_fetch_reports(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n) {
 
 int tsg_reports_device(tsg_engine* h, void** device_ptr, int64_t* n) {
     CKR(validate_handle(h));
+    DevGuard g(h->dev);
+    CKR(compact_reports(h));
     *device_ptr = h->out;
     *n = h->n_out;
     return TSG_OK;

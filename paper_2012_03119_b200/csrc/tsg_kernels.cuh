@@ -1,39 +1,77 @@
 // tsg_kernels.cuh -- the hot-path kernels (sm_100a).
 //
-//   K1+K2  k_encode        int8 snapshots -> lane words + aggregates   (bitpack.py:81-117, 152-167, 211-244)
-//   K3+K4+K5 k_test        two-stage trigger test, report emission,
-//                          activity bump, counters                      (engine.py:238-254, 437-467)
+//   K1+K2    k_encode  int8 snapshots -> lane words + aggregates   (bitpack.py:81-117, 152-167, 211-244)
+//   K3+K4+K5 k_test    two-stage trigger test, report emission,
+//                      activity bump, counters                      (engine.py:238-254, 437-467)
 //
-// Both are HBM/L2-bound integer kernels; DESIGN.md §4 gives their rooflines.
+// Both are memory-bound integer kernels; DESIGN.md §4 gives their rooflines.
 #pragma once
-#include <cstdint>
 #include <climits>
+#include <cstdint>
 
-#include "tsg_device.cuh"
 #include "../../include/tsg.h"
+#include "tsg_device.cuh"
 
 namespace tsg {
 
 constexpr int MAXG = 64;
 
+#ifndef TSG_TEST_MIN_BLOCKS
+#define TSG_TEST_MIN_BLOCKS 4
+#endif
+
 // ---------------------------------------------------------------------------
-// K1+K2: encoder.  Block = 32 x 8 threads covers 128 variables of one chunk.
-// Thread (x, y) owns variables 4x..4x+3 of the tile and groups y, y+8, ...;
-// for each group it reads the group's lane rows as one u32 (4 variables) per
-// row -- every warp load is one coalesced 128-byte segment of a row -- and
-// turns bytes into lane bits with SIMD byte compares.  Aggregate bits are
-// OR-reduced across groups in shared memory.
+// K1+K2: encoder.
+//
+// Block = 32 x 8 threads covers 128 variables of one chunk.  Thread (x, y)
+// owns variables 4x..4x+3 and groups y, y+8, ...  For each group it streams
+// the group's rows as one u32 (4 variables) per row, so every warp load is a
+// coalesced 128-byte row segment.  Bytes become lane bits without per-bit
+// work: exact per-byte "== TRUE" / "!= UNDEF" masks land in each byte's MSB
+// (SWAR zero-byte tests), and eight rows are transposed into one byte per
+// variable by shift-merging the MSB masks.  Lane words are written
+// group-major (lane[g][v]), four consecutive variables per thread, so the
+// stores are contiguous; aggregate bits are OR-reduced across groups in
+// shared memory.
 
 struct EncodeChunk {
-    int32_t G;               // groups in the chunk
+    int32_t G;            // groups in the chunk
     int32_t num_vars;
-    int64_t pitch;           // bytes between rows (multiple of 4)
-    int64_t row0[MAXG];      // first row of each group
-    int32_t lanes[MAXG];     // rows (lanes) of each group
+    int64_t pitch;        // bytes between rows (multiple of 4)
+    int64_t vstride;      // lane-table row length (num_vars + 2)
+    int64_t row0[MAXG];   // first row of each group
+    int32_t lanes[MAXG];  // rows (lanes) of each group
 };
 
+// 0x80 in every byte of w that is != 0
+__device__ __forceinline__ uint32_t nz_msb(uint32_t w) {
+    uint32_t t = (w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;
+    return (t | w) & 0x80808080u;
+}
+// 0x80 in every byte of w that is == 0x01 (TRUE)
+__device__ __forceinline__ uint32_t eq1_msb(uint32_t w) {
+    uint32_t y = w ^ 0x01010101u;
+    uint32_t t = (y & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;
+    return ~(t | y) & 0x80808080u;
+}
+
+template <class LW>
+__device__ __forceinline__ void st_lane4(LaneEntry<LW>* p, const LW* t, const LW* s);
+template <>
+__device__ __forceinline__ void st_lane4<uint32_t>(LaneEntry<uint32_t>* p, const uint32_t* t, const uint32_t* s) {
+    uint4* q = reinterpret_cast<uint4*>(p);
+    q[0] = make_uint4(t[0], s[0], t[1], s[1]);
+    q[1] = make_uint4(t[2], s[2], t[3], s[3]);
+}
+template <>
+__device__ __forceinline__ void st_lane4<uint64_t>(LaneEntry<uint64_t>* p, const uint64_t* t, const uint64_t* s) {
+    ulonglong2* q = reinterpret_cast<ulonglong2*>(p);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) q[b] = make_ulonglong2(t[b], s[b]);
+}
+
 template <class LW, class GW>
-__global__ void __launch_bounds__(256) k_encode(const int8_t* __restrict__ rows, const EncodeChunk c,
+__global__ void __launch_bounds__(256) k_encode(const int8_t* __restrict__ rows, const __grid_constant__ EncodeChunk c,
                                                 LaneEntry<LW>* __restrict__ lane,
                                                 AggEntry<GW>* __restrict__ agg) {
     __shared__ GW sT[128], sF[128], sU[128];
@@ -48,16 +86,34 @@ __global__ void __launch_bounds__(256) k_encode(const int8_t* __restrict__ rows,
         LW tw[4] = {0, 0, 0, 0}, sw[4] = {0, 0, 0, 0};
         if (v0 <= V) {
             const int8_t* base = rows + c.row0[g] * c.pitch + v0;
-#pragma unroll 4
-            for (int i = 0; i < n; ++i) {
-                uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(base + (int64_t)i * c.pitch));
-                uint32_t e1 = __vcmpeq4(w, 0x01010101u);  // byte == TRUE
-                uint32_t nz = __vcmpne4(w, 0u);           // byte != UNDEF
+            for (int r0 = 0; r0 < n; r0 += 8) {
+                uint32_t w[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    w[k] = (r0 + k < n) ? __ldg(reinterpret_cast<const uint32_t*>(base + (int64_t)(r0 + k) * c.pitch)) : 0u;
+                uint32_t aT = 0, aS = 0;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {  // row r0+k ends at bit k of each byte
+                    aT = ((aT >> 1) & 0x7F7F7F7Fu) | eq1_msb(w[k]);
+                    aS = ((aS >> 1) & 0x7F7F7F7Fu) | nz_msb(w[k]);
+                }
 #pragma unroll
                 for (int b = 0; b < 4; ++b) {
-                    tw[b] |= (LW)((e1 >> (8 * b)) & 1u) << i;
-                    sw[b] |= (LW)((nz >> (8 * b)) & 1u) << i;
+                    tw[b] |= (LW)((aT >> (8 * b)) & 0xFFu) << r0;
+                    sw[b] |= (LW)((aS >> (8 * b)) & 0xFFu) << r0;
                 }
+            }
+        }
+        if (v0 == 0) { tw[0] = 0; sw[0] = 0; }  // slot 0 is never set (bitpack.py:110-111)
+        LaneEntry<LW>* dst = lane + (int64_t)g * c.vstride + v0;
+        if (v0 + 3 <= V + 1) {
+            if (v0 + 3 == V + 1) { tw[3] = 0; sw[3] = ~LW(0); }  // sentinel: always False
+            st_lane4<LW>(dst, tw, sw);
+        } else {
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                if (v0 + b <= V) dst[b] = LaneEntry<LW>{tw[b], sw[b]};
+                else if (v0 + b == V + 1) dst[b] = LaneEntry<LW>{LW(0), ~LW(0)};
             }
         }
         const LW lm = width_mask<LW>(n);
@@ -65,18 +121,10 @@ __global__ void __launch_bounds__(256) k_encode(const int8_t* __restrict__ rows,
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
             const int64_t v = v0 + b;
-            if (v <= V) {
-                LW tv = v == 0 ? LW(0) : tw[b];
-                LW sv = v == 0 ? LW(0) : sw[b];
-                lane[v * c.G + g] = LaneEntry<LW>{tv, sv};
-                if (v != 0) {
-                    // AggregateAssignment.from_packed, bitpack.py:156-166
-                    if (tv != 0) or_shared(&sT[4 * x + b], bit);
-                    if ((sv & ~tv) != 0) or_shared(&sF[4 * x + b], bit);
-                    if (n == 0 || (~sv & lm) != 0) or_shared(&sU[4 * x + b], bit);
-                }
-            } else if (v == V + 1) {
-                lane[v * c.G + g] = LaneEntry<LW>{LW(0), ~LW(0)};  // sentinel: always False
+            if (v >= 1 && v <= V) {  // AggregateAssignment.from_packed, bitpack.py:156-166
+                if (tw[b] != 0) or_shared(&sT[4 * x + b], bit);
+                if ((sw[b] & ~tw[b]) != 0) or_shared(&sF[4 * x + b], bit);
+                if (n == 0 || (~sw[b] & lm) != 0) or_shared(&sU[4 * x + b], bit);
             }
         }
     }
@@ -92,16 +140,20 @@ __global__ void __launch_bounds__(256) k_encode(const int8_t* __restrict__ rows,
 // K3+K4+K5: trigger test.  Persistent grid; one warp per tile of 32 clauses
 // of one bucket, one clause per lane.
 //
-// Stage 1 (aggregate filter, engine.py:238-254) walks the clause's literals
-// four at a time (four coalesced literal-row loads, then four L2 gathers into
-// the aggregate table) and stops as soon as every group is negative: the
-// live set (all_false | one_undef) only shrinks, so a zero word is final and
-// the remaining literals cannot change the result.
+// Software pipeline: while a warp tests tile t it already has the first PF
+// literal rows of its next tile in flight (registers), so the HBM latency
+// of the literal stream overlaps the L2 gathers of the current tile.
+// Stage 1 (aggregate filter, engine.py:238-254) walks literals four at a
+// time and stops as soon as every group is negative: the live set
+// (all_false | one_undef) only shrinks, so a zero word is final.
 // Stage 2 (lane test, bitpack.py:120-135) runs per positive group in
-// ascending order with the same early exit.  Every triggering group bumps the
-// clause's activity by inc * popcount (fp64, explicit round-to-nearest ops,
-// no FMA: engine.py:460); the first triggering group of each thread emits the
-// report (engine.py:462-464).  Records are allocated with one atomic per warp.
+// ascending order with the same early exit, reusing the prefetched
+// literals.  Every triggering group bumps the clause's activity by
+// inc * popcount (fp64 round-to-nearest mul then add, no FMA:
+// engine.py:460); the first triggering group of each thread emits the
+// report (engine.py:462-464).  Report slots are reserved once per warp for
+// an upper bound (the positive-group count); unused slots are written as
+// padding (engine_id = -1) and squeezed out when the records are fetched.
 
 struct BucketDesc {
     const int32_t* lits;
@@ -120,13 +172,14 @@ struct TestParams {
     int32_t G;                 // groups in this chunk
     int64_t n_tiles;
     const AggEntry<GW>* agg;
-    const LaneEntry<LW>* lane;
+    const LaneEntry<LW>* lane; // [G][vstride]
+    int64_t vstride;
     int32_t sentinel;          // num_vars + 1
     int32_t g0;                // global index of the chunk's first group
     GW group_mask;
     double inc;
     tsg_report* out;
-    unsigned long long* ctr;   // [0] records, [1] aggregate positives, [2] lane triggers
+    unsigned long long* ctr;   // [0] slots reserved, [1] aggregate positives, [2] lane triggers, [3] reports
     int64_t out_cap;
     int64_t* carry;            // per-clause "(round, tid) reported" stamp for multi-chunk rounds
     int64_t stamp_base;        // round sequence << 32
@@ -137,100 +190,103 @@ struct TestParams {
     LW lane_mask[MAXG];
 };
 
-template <class LW, class GW>
-__global__ void __launch_bounds__(256) k_test(const __grid_constant__ TestParams<LW, GW> p) {
-    const int lane = threadIdx.x & 31;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    unsigned long long pos_acc = 0, trig_acc = 0;
-    LW masks[MAXG];
+constexpr int PF = 8;               // literal rows prefetched per tile
+constexpr int SMEM_BUCKETS = 1024;  // bucket table cached in shared memory
 
-    for (int64_t tile = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; tile < p.n_tiles;
-         tile += nwarps) {
-        int lo = 0, hi = p.nb - 1;
+__device__ __forceinline__ void st_report(tsg_report* p, int64_t eid, uint64_t mask, int32_t group,
+                                          int32_t bucket, int64_t slot) {
+    reinterpret_cast<ulonglong2*>(p)[0] = make_ulonglong2((unsigned long long)eid, (unsigned long long)mask);
+    reinterpret_cast<int4*>(p)[1] = make_int4(group, bucket, (int)(uint32_t)slot, (int)(slot >> 32));
+}
+
+struct Tile {
+    const BucketDesc* bd;
+    const int32_t* lp;  // this lane's literal 0 (row stride STRIDE)
+    int64_t slot;
+    int size;
+    bool active;
+};
+
+__device__ __forceinline__ int find_bucket(const int64_t* s_tile0, const BucketDesc* buckets, int nb, int64_t tile) {
+    int lo = 0, hi = nb - 1;
+    if (nb <= SMEM_BUCKETS) {
         while (lo < hi) {
             int mid = (lo + hi + 1) >> 1;
-            if (p.buckets[mid].tile0 <= tile) lo = mid; else hi = mid - 1;
+            if (s_tile0[mid] <= tile) lo = mid; else hi = mid - 1;
         }
-        const BucketDesc* bd = p.buckets + lo;
-        const int size = bd->size;
-        const int64_t blk = tile - bd->tile0;
-        const int64_t slot = blk * STRIDE + lane;
-        const bool active = slot < bd->count;
-        const int32_t* lp = bd->lits + blk * (int64_t)size * STRIDE + lane;
+    } else {
+        while (lo < hi) {
+            int mid = (lo + hi + 1) >> 1;
+            if (buckets[mid].tile0 <= tile) lo = mid; else hi = mid - 1;
+        }
+    }
+    return lo;
+}
+
+template <class LW, class GW>
+__device__ __forceinline__ Tile open_tile(const TestParams<LW, GW>& p, const int64_t* s_tile0, int64_t tile, int lane,
+                                          int32_t (&buf)[PF]) {
+    Tile t;
+    t.bd = p.buckets + find_bucket(s_tile0, p.buckets, p.nb, tile);
+    t.size = t.bd->size;
+    const int64_t blk = tile - t.bd->tile0;
+    t.slot = blk * STRIDE + lane;
+    t.active = t.slot < t.bd->count;
+    t.lp = t.bd->lits + blk * (int64_t)t.size * STRIDE + lane;
+#pragma unroll
+    for (int u = 0; u < PF; ++u) buf[u] = (t.active && u < t.size) ? __ldg(t.lp + u * STRIDE) : p.sentinel;
+    return t;
+}
+
+template <class LW, class GW>
+__global__ void __launch_bounds__(256, TSG_TEST_MIN_BLOCKS) k_test(const __grid_constant__ TestParams<LW, GW> p) {
+    __shared__ int64_t s_tile0[SMEM_BUCKETS];
+    __shared__ unsigned long long s_acc[3][8];
+    for (int i = threadIdx.x; i < p.nb && i < SMEM_BUCKETS; i += blockDim.x) s_tile0[i] = p.buckets[i].tile0;
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long pos_acc = 0, trig_acc = 0, rep_acc = 0;
+
+    int64_t tile = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int32_t cur[PF], nxt[PF];
+    Tile T{};
+    if (tile < p.n_tiles) T = open_tile(p, s_tile0, tile, lane, cur);
+
+    for (; tile < p.n_tiles; tile += nwarps) {
+        Tile N{};
+        if (tile + nwarps < p.n_tiles) N = open_tile(p, s_tile0, tile + nwarps, lane, nxt);
+        const int size = T.size;
 
         // ---- stage 1: aggregate filter -------------------------------------
         GW af = ~GW(0), ou = GW(0);
-        if (active) {
-            for (int j = 0; j < size; j += 4) {
+        if (T.active) {
+#pragma unroll
+            for (int h = 0; h < PF; h += 4) {
+                if (h >= size || (af | ou) == GW(0)) break;
+                AggEntry<GW> e[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) e[u] = ld_agg(p.agg + (cur[h + u] < 0 ? -cur[h + u] : cur[h + u]));
+#pragma unroll
+                for (int u = 0; u < 4; ++u) step<GW>(af, ou, cur[h + u] < 0 ? e[u].t : e[u].f, e[u].u);
+            }
+            for (int j = PF; j < size && (af | ou) != GW(0); j += 4) {
                 int32_t l[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) l[u] = (j + u < size) ? ld_lit(lp + (j + u) * STRIDE) : p.sentinel;
+                for (int u = 0; u < 4; ++u) l[u] = (j + u < size) ? __ldg(T.lp + (j + u) * STRIDE) : p.sentinel;
+                AggEntry<GW> e[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int32_t lit = l[u];
-                    const AggEntry<GW> e = ld_agg(p.agg + (lit < 0 ? -lit : lit));
-                    step<GW>(af, ou, lit < 0 ? e.t : e.f, e.u);
-                }
-                if ((af | ou) == GW(0)) break;
+                for (int u = 0; u < 4; ++u) e[u] = ld_agg(p.agg + (l[u] < 0 ? -l[u] : l[u]));
+#pragma unroll
+                for (int u = 0; u < 4; ++u) step<GW>(af, ou, l[u] < 0 ? e[u].t : e[u].f, e[u].u);
             }
         }
-        const GW word = active ? ((af | ou) & p.group_mask) : GW(0);
+        const GW word = T.active ? ((af | ou) & p.group_mask) : GW(0);
 
-        // ---- stage 2: exact lane test per positive group --------------------
-        int n_emit = 0;
-        uint64_t emit = 0;
-        if (word) {
-            pos_acc += __popcll((unsigned long long)word);
-            double act = 0.0;
-            bool touched = false;
-            int last_tid = INT_MIN;
-            GW left = word;
-            while (left) {
-                const int g = __ffsll((long long)(unsigned long long)left) - 1;
-                left &= left - GW(1);
-                LW lf = ~LW(0), lo2 = LW(0);
-                for (int j = 0; j < size; j += 4) {
-                    int32_t l[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) l[u] = (j + u < size) ? ld_lit(lp + (j + u) * STRIDE) : p.sentinel;
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int32_t lit = l[u];
-                        const int64_t v = lit < 0 ? -lit : lit;
-                        const LaneEntry<LW> e = ld_lane(p.lane + v * p.G + g);
-                        const LW isf = lit < 0 ? (e.s & e.t) : (e.s & ~e.t);
-                        step<LW>(lf, lo2, isf, ~e.s);
-                    }
-                    if ((lf | lo2) == LW(0)) break;
-                }
-                const LW mask = (lf | lo2) & p.lane_mask[g];
-                if (!mask) continue;
-                const int hits = __popcll((unsigned long long)mask);
-                trig_acc += hits;
-                if (!p.emit_only) {
-                    if (!touched) { act = bd->acts[slot]; touched = true; }
-                    act = __dadd_rn(act, __dmul_rn(p.inc, (double)hits));
-                }
-                const int tid = p.tid[g];
-                if (tid != last_tid) {  // first triggering group of this thread (engine.py:462)
-                    last_tid = tid;
-                    bool dup = false;
-                    if (tid == p.carry_in_tid)
-                        dup = p.carry[bd->tile0 * STRIDE + slot] == (p.stamp_base | (uint32_t)tid);
-                    if (!dup) {
-                        emit |= 1ull << g;
-                        masks[g] = mask;
-                        ++n_emit;
-                    }
-                }
-            }
-            if (touched) bd->acts[slot] = act;
-            if (p.carry_out_tid >= 0 && last_tid == p.carry_out_tid)
-                p.carry[bd->tile0 * STRIDE + slot] = p.stamp_base | (uint32_t)last_tid;
-        }
-
-        // ---- K4: report emission, one atomic per warp ------------------------
-        int incl = n_emit;
+        // ---- report slot reservation: one atomic per warp --------------------
+        const int ub = __popcll((unsigned long long)word);
+        int incl = ub;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
             int o = __shfl_up_sync(0xffffffffu, incl, d);
@@ -241,43 +297,96 @@ __global__ void __launch_bounds__(256) k_test(const __grid_constant__ TestParams
             unsigned long long base = 0;
             if (lane == 31) base = atomicAdd(p.ctr, (unsigned long long)total);
             base = __shfl_sync(0xffffffffu, base, 31);
-            int64_t pos = (int64_t)base + incl - n_emit;
-            if (emit) {
-                const int64_t eid = bd->ids[slot];
-                while (emit) {
-                    const int g = __ffsll((long long)emit) - 1;
-                    emit &= emit - 1;
-                    if (pos < p.out_cap) {
-                        tsg_report r;
-                        r.engine_id = eid;
-                        r.lane_mask = (uint64_t)masks[g];
-                        r.group = p.g0 + g;
-                        r.bucket = bd->rank;
-                        r.slot = slot;
-                        p.out[pos] = r;
+            int64_t pos = (int64_t)base + incl - ub;
+            const int64_t end = pos + ub;
+
+            // ---- stage 2: exact lane test per positive group ----------------
+            if (word) {
+                pos_acc += ub;
+                const int64_t gslot = T.bd->tile0 * STRIDE + T.slot;
+                double act = 0.0;
+                if (!p.emit_only) act = T.bd->acts[T.slot];
+                bool touched = false;
+                int last_tid = INT_MIN;
+                const int64_t eid = T.bd->ids[T.slot];
+                GW left = word;
+                while (left) {
+                    const int g = __ffsll((long long)(unsigned long long)left) - 1;
+                    left &= left - GW(1);
+                    const LaneEntry<LW>* lt = p.lane + (int64_t)g * p.vstride;
+                    LW lf = ~LW(0), lo2 = LW(0);
+#pragma unroll
+                    for (int h = 0; h < PF; h += 4) {
+                        if (h >= size || (lf | lo2) == LW(0)) break;
+                        LaneEntry<LW> e[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) e[u] = ld_lane(lt + (cur[h + u] < 0 ? -cur[h + u] : cur[h + u]));
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            step<LW>(lf, lo2, cur[h + u] < 0 ? (e[u].s & e[u].t) : (e[u].s & ~e[u].t), ~e[u].s);
                     }
-                    ++pos;
+                    for (int j = PF; j < size && (lf | lo2) != LW(0); j += 4) {
+                        int32_t l[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) l[u] = (j + u < size) ? __ldg(T.lp + (j + u) * STRIDE) : p.sentinel;
+                        LaneEntry<LW> e[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) e[u] = ld_lane(lt + (l[u] < 0 ? -l[u] : l[u]));
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            step<LW>(lf, lo2, l[u] < 0 ? (e[u].s & e[u].t) : (e[u].s & ~e[u].t), ~e[u].s);
+                    }
+                    const LW mask = (lf | lo2) & p.lane_mask[g];
+                    if (!mask) continue;
+                    const int hits = __popcll((unsigned long long)mask);
+                    trig_acc += hits;
+                    if (!p.emit_only) {
+                        act = __dadd_rn(act, __dmul_rn(p.inc, (double)hits));
+                        touched = true;
+                    }
+                    const int tid = p.tid[g];
+                    if (tid != last_tid) {  // first triggering group of this thread (engine.py:462)
+                        last_tid = tid;
+                        bool dup = false;
+                        if (tid == p.carry_in_tid) dup = p.carry[gslot] == (p.stamp_base | (uint32_t)tid);
+                        if (!dup) {
+                            if (pos < p.out_cap) st_report(p.out + pos, eid, (uint64_t)mask, p.g0 + g, T.bd->rank, T.slot);
+                            ++pos;
+                            ++rep_acc;
+                        }
+                    }
                 }
+                if (touched) T.bd->acts[T.slot] = act;
+                if (p.carry_out_tid >= 0 && last_tid == p.carry_out_tid)
+                    p.carry[gslot] = p.stamp_base | (uint32_t)last_tid;
+                for (; pos < end; ++pos)  // padding for reserved-but-unused slots
+                    if (pos < p.out_cap) st_report(p.out + pos, -1, 0, -1, -1, -1);
             }
         }
+
+        T = N;
+#pragma unroll
+        for (int u = 0; u < PF; ++u) cur[u] = nxt[u];
     }
 
-    if (p.emit_only) return;
     // counters: warp reduce, then block reduce, one atomic per block
-    __shared__ unsigned long long s_pos[32], s_trig[32];
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
         pos_acc += __shfl_down_sync(0xffffffffu, pos_acc, d);
         trig_acc += __shfl_down_sync(0xffffffffu, trig_acc, d);
+        rep_acc += __shfl_down_sync(0xffffffffu, rep_acc, d);
     }
     const int w = threadIdx.x >> 5;
-    if (lane == 0) { s_pos[w] = pos_acc; s_trig[w] = trig_acc; }
+    if (lane == 0) { s_acc[0][w] = pos_acc; s_acc[1][w] = trig_acc; s_acc[2][w] = rep_acc; }
     __syncthreads();
     if (threadIdx.x == 0) {
-        unsigned long long a = 0, b = 0;
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { a += s_pos[i]; b += s_trig[i]; }
-        if (a) atomicAdd(p.ctr + 1, a);
-        if (b) atomicAdd(p.ctr + 2, b);
+        unsigned long long a = 0, b = 0, r = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { a += s_acc[0][i]; b += s_acc[1][i]; r += s_acc[2][i]; }
+        if (r) atomicAdd(p.ctr + 3, r);
+        if (!p.emit_only) {
+            if (a) atomicAdd(p.ctr + 1, a);
+            if (b) atomicAdd(p.ctr + 2, b);
+        }
     }
 }
 

@@ -60,6 +60,13 @@ def clause_buckets(n: int, num_vars: int, rng: np.random.Generator, size_lo=2, s
         if s == 0:
             out[s] = np.zeros((c, 0), np.int32)
             continue
+        if s * s > num_vars // 4:  # dense: rejection would rarely succeed
+            if s > num_vars:
+                raise ValueError(f"clause size {s} exceeds {num_vars} variables")
+            vs = np.stack([rng.choice(num_vars, s, replace=False) + 1 for _ in range(c)]).astype(np.int64)
+            sign = rng.integers(0, 2, (c, s), dtype=np.int64) * 2 - 1
+            out[s] = (vs * sign).astype(np.int32)
+            continue
         vs = rng.integers(1, num_vars + 1, (c, s), dtype=np.int64)
         while True:
             srt = np.sort(vs, axis=1)
