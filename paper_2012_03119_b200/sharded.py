@@ -1,0 +1,188 @@
+"""Multi-GPU sharding of the clause store (one process per GPU).
+
+Clauses are tested independently, so the store shards by
+clause: every rank owns a disjoint set of clauses in its own HBM store.  One
+round (engine.py:369-467) becomes
+
+    rank 0: group + stage + encode the round's snapshots (K1/K2)
+    all   : broadcast the packed tables over NVLink (NCCL)      <- the only data-path collective
+    all   : test the local shard (K3/K4/K5)
+    all   : gather the report records to rank 0, merge in the reference order
+
+Rank 0 owns the solver-facing API (add_clause / submit_assignment /
+drain_reports, the reference's producer side, engine.py:305-343); the other
+ranks run `worker_loop`.  Global reduce_store (engine.py:469-505) is exact:
+the doomed set is "the `target` smallest (activity, engine_id) keys among
+eligible clauses", so rank 0 finds the target-th smallest key over all
+shards and every rank removes exactly its keys <= that threshold.
+
+The helpers below (shard assignment, record merge, threshold selection,
+array collectives) are pure host logic; tests/test_sharded_gloo.py runs them
+with world_size 2 on the gloo backend.
+"""
+from __future__ import annotations
+
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from ._lib import REPORT_DTYPE
+
+
+# ---------------------------------------------------------------------------
+# pure host logic
+
+def assign_shards(sizes: Sequence[int], world: int, load: Optional[Dict[Tuple[int, int], int]] = None
+                  ) -> np.ndarray:
+    """Rank of every incoming clause: the rank holding the fewest clauses of
+    that size so far (ties -> lowest rank), so every size bucket -- and with
+    it the literal bytes -- is balanced across shards.
+    `load[(size, rank)]` is updated in place."""
+    load = {} if load is None else load
+    out = np.empty(len(sizes), dtype=np.int32)
+    for i, s in enumerate(sizes):
+        s = int(s)
+        best, best_n = 0, None
+        for r in range(world):
+            n = load.get((s, r), 0)
+            if best_n is None or n < best_n:
+                best, best_n = r, n
+        out[i] = best
+        load[(s, best)] = best_n + 1
+    return out
+
+
+def order_keys(recs: np.ndarray, group_width: int, bucket_rank_of: Dict[int, int],
+               size_of_eid: Dict[int, int]) -> Tuple[np.ndarray, ...]:
+    """Sort keys reproducing the reference's report order across shards.
+
+    Within a bucket, slot order equals engine-id order (clauses are appended
+    in id order and compaction preserves order, engine.py:150-163,184-200),
+    so (chunk, global bucket rank, engine_id, group) is the unsharded order
+    (engine.py:403-464)."""
+    grp = recs["group"].astype(np.int64)
+    eid = recs["engine_id"].astype(np.int64)
+    brank = np.fromiter((bucket_rank_of[size_of_eid[int(e)]] for e in eid), dtype=np.int64, count=len(eid))
+    return grp, eid, brank, grp // group_width
+
+
+def merge_reports(parts: Sequence[np.ndarray], group_width: int, bucket_rank_of: Dict[int, int],
+                  size_of_eid: Dict[int, int]) -> np.ndarray:
+    recs = np.concatenate([p for p in parts if len(p)]) if any(len(p) for p in parts) else \
+        np.zeros(0, REPORT_DTYPE)
+    if len(recs) == 0:
+        return recs
+    grp, eid, brank, chunk = order_keys(recs, group_width, bucket_rank_of, size_of_eid)
+    return recs[np.lexsort((grp, eid, brank, chunk))]
+
+
+def kth_key(key_parts: Sequence[Tuple[np.ndarray, np.ndarray]], k: int) -> Optional[Tuple[float, int]]:
+    """The k-th smallest (activity, engine_id) over all shards (1-based), or
+    None if fewer than k keys exist (then everything eligible goes)."""
+    acts = np.concatenate([a for a, _ in key_parts]) if key_parts else np.zeros(0)
+    ids = np.concatenate([i for _, i in key_parts]) if key_parts else np.zeros(0, np.int64)
+    if k <= 0:
+        return None
+    if k > len(ids):
+        return None
+    order = np.lexsort((ids, acts))
+    j = order[k - 1]
+    return float(acts[j]), int(ids[j])
+
+
+def count_le(acts: np.ndarray, ids: np.ndarray, key: Optional[Tuple[float, int]]) -> int:
+    """How many local keys are <= the global threshold key."""
+    if key is None:
+        return len(ids)
+    a, i = key
+    return int(np.count_nonzero((acts < a) | ((acts == a) & (ids <= i))))
+
+
+# ---------------------------------------------------------------------------
+# array collectives over torch.distributed (NCCL on GPUs, gloo on CPU)
+
+def _device(dist):
+    import torch
+    return torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
+
+
+def bcast_array(dist, arr: Optional[np.ndarray], src: int, dtype) -> np.ndarray:
+    import torch
+    dev = _device(dist)
+    n = torch.tensor([0 if arr is None else arr.size], dtype=torch.int64, device=dev)
+    dist.broadcast(n, src)
+    buf = torch.empty(int(n.item()), dtype=getattr(torch, np.dtype(dtype).name), device=dev)
+    if dist.get_rank() == src and buf.numel():
+        buf.copy_(torch.from_numpy(np.ascontiguousarray(arr, dtype=dtype).reshape(-1)).to(dev))
+    if buf.numel():
+        dist.broadcast(buf, src)
+    return buf.cpu().numpy()
+
+
+def gather_records(dist, recs: np.ndarray, dst: int = 0) -> Optional[List[np.ndarray]]:
+    """Gather variable-length report record arrays to `dst` (padded all_gather
+    of the byte view, sizes first)."""
+    import torch
+    dev = _device(dist)
+    world = dist.get_world_size()
+    raw = np.ascontiguousarray(recs).view(np.uint8)
+    n = torch.tensor([raw.size], dtype=torch.int64, device=dev)
+    sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(sizes, n)
+    m = max(int(s.item()) for s in sizes)
+    if m == 0:
+        return [np.zeros(0, REPORT_DTYPE) for _ in range(world)] if dist.get_rank() == dst else None
+    buf = torch.zeros(m, dtype=torch.uint8, device=dev)
+    if raw.size:
+        buf[:raw.size] = torch.from_numpy(raw).to(dev)
+    bufs = [torch.zeros(m, dtype=torch.uint8, device=dev) for _ in range(world)]
+    dist.all_gather(bufs, buf)
+    if dist.get_rank() != dst:
+        return None
+    return [b[:int(s.item())].cpu().numpy().view(REPORT_DTYPE) for b, s in zip(bufs, sizes)]
+
+
+def broadcast_tables(dist, engine, src: int = 0, stream=None) -> None:
+    """Broadcast the round's packed tables (tsg_round_tables) from `src` to
+    every rank, in place, over NCCL (NVLink on one node)."""
+    import torch
+    ptr, nbytes = engine.tables()
+
+    class _CAI:
+        __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                    "version": 3, "stream": None}
+
+    t = torch.as_tensor(_CAI(), device=torch.device("cuda", torch.cuda.current_device()))
+    if stream is not None:
+        with torch.cuda.stream(stream):
+            dist.broadcast(t, src)
+    else:
+        dist.broadcast(t, src)
+
+
+# ---------------------------------------------------------------------------
+# the sharded round over NativeEngine shards
+
+class ShardedRound:
+    """One rank's side of a sharded exchange round (used by bench.py and by
+    the distributed engine front end)."""
+
+    def __init__(self, dist, engine, group_width: int = 32):
+        import torch
+        self.dist, self.eng, self.gw = dist, engine, group_width
+        self.rank = dist.get_rank()
+        self.stream = torch.cuda.ExternalStream(engine.stream())
+
+    def run(self, group_lanes, group_tid, activity_inc: float, rows: Optional[np.ndarray] = None):
+        """Rank 0 passes the round's grouped rows; every rank passes the same
+        group_lanes / group_tid (broadcast by the caller)."""
+        self.eng.prepare(group_lanes, group_tid)
+        if self.rank == 0:
+            if rows is not None:
+                self.eng.stage(rows)
+            self.eng.encode()
+        self.eng.sync()
+        broadcast_tables(self.dist, self.eng, 0, self.stream)
+        res = self.eng.test(activity_inc)
+        recs = self.eng.fetch(res.reports)
+        return res, gather_records(self.dist, recs, 0)
