@@ -302,7 +302,7 @@ def main():
     if world == 1:
         from paper_2012_03119_b200 import _lib
         import ctypes as C
-        rec_buf = torch.empty((8 << 20) * 32, dtype=torch.uint8).pin_memory()
+        rec_buf = torch.empty((8 << 20) * 16, dtype=torch.uint8).pin_memory()
         L = eng.L
 
         def e2e_step():
@@ -321,7 +321,7 @@ def main():
         d2h = 0
         for _ in range(e2e_steps):
             r = e2e_step()
-            d2h += r.reports * 32 + 24
+            d2h += r.reports * 16 + 32
         with torch.cuda.stream(stream):
             e1.record(stream)
         eng.sync()

@@ -66,18 +66,24 @@ typedef struct tsg_round_result {
     double test_ms;                   /* device time of the trigger kernels       */
 } tsg_round_result;
 
-/* One report record (engine.py:90-102 Report minus the literals, which the
- * host keeps).  `group` is the global group index in round order
- * (engine.py:390-399); the destination thread is the group's tid.  Sorting
- * by (group / group_width, bucket, slot, group) reproduces the reference's
- * emission order (engine.py:403-464). */
+/* One report record, 16 bytes (engine.py:90-102 Report minus the literals,
+ * which the host keeps): key = engine_id << 16 | group, where `group` is the
+ * global group index in round order (engine.py:390-399) and the destination
+ * thread is that group's tid.  Engine ids must fit in 48 bits and a round
+ * holds at most 65535 groups.
+ *
+ * Order: inside a size bucket, slot order equals engine-id order (clauses
+ * are appended in id order and compaction preserves order, engine.py:150-163,
+ * 184-200), so sorting records by (group / group_width, creation rank of the
+ * clause's size bucket, engine_id, group) reproduces the reference's emission
+ * order (engine.py:403-464). */
 typedef struct tsg_report {
-    int64_t engine_id;
+    uint64_t key;
     uint64_t lane_mask;
-    int32_t group;
-    int32_t bucket; /* bucket creation rank (dict insertion order)             */
-    int64_t slot;   /* slot inside the bucket                                  */
 } tsg_report;
+#define TSG_REPORT_ENGINE_ID(r) ((int64_t)((r).key >> 16))
+#define TSG_REPORT_GROUP(r) ((int32_t)((r).key & 0xFFFFu))
+#define TSG_MAX_GROUPS 65535
 
 const char* tsg_last_error(void);
 int tsg_abi_version(void);

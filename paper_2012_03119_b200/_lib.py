@@ -40,9 +40,7 @@ class tsg_round_result(C.Structure):
                 ("encode_ms", C.c_double), ("test_ms", C.c_double)]
 
 
-REPORT_DTYPE = np.dtype([("engine_id", "<i8"), ("lane_mask", "<u8"), ("group", "<i4"),
-                         ("bucket", "<i4"), ("slot", "<i8")])
-assert REPORT_DTYPE.itemsize == 32
+from .reports import RECORD_DTYPE as REPORT_DTYPE  # noqa: E402  (tsg_report, 16 bytes)
 
 # every symbol include/tsg.h declares (checked by tests/test_abi.py)
 EXPORTS = (

@@ -103,6 +103,7 @@ struct tsg_engine {
     tsg_report* out2 = nullptr;             // compaction target for fetch
     int64_t out2_cap = 0;
     bool compacted = true;
+    bool oob = false;  // a stored literal may exceed num_vars (checked before testing)
     unsigned long long* ctr = nullptr;      // device [0..7]: [0..3] round counters, [4] maintenance scratch
     unsigned long long* h_ctr = nullptr;    // pinned [8]
     int64_t* carry = nullptr;
@@ -243,14 +244,16 @@ int launch_test(tsg_engine* h, int c, double inc, int emit_only) {
         p.lane_mask[g] = width_mask<LW>(h->glanes[g0 + g]);
     }
     if (h->n_tiles == 0) return TSG_OK;
+    const size_t smem = test_smem_bytes<GW>();
     if (!h->test_grid) {
+        CK(cudaFuncSetAttribute(k_test<LW, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_test<LW, GW>, 256, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_test<LW, GW>, TEST_THREADS, smem);
         h->test_grid = std::max(1, per_sm) * h->nsm;
     }
-    int64_t want = (h->n_tiles + 7) / 8;
+    int64_t want = (h->n_tiles + TEST_THREADS / 32 - 1) / (TEST_THREADS / 32);
     int grid = (int)std::min<int64_t>(want, h->test_grid);
-    k_test<LW, GW><<<grid, 256, 0, h->st>>>(p);
+    k_test<LW, GW><<<grid, TEST_THREADS, smem, h->st>>>(p);
     CK(cudaGetLastError());
     return TSG_OK;
 }
@@ -338,7 +341,7 @@ int compact_all(tsg_engine* h, const uint8_t* keep, const std::vector<int64_t>& 
 }
 
 struct ValidReport {
-    __host__ __device__ bool operator()(const tsg_report& r) const { return r.engine_id >= 0; }
+    __host__ __device__ bool operator()(const tsg_report& r) const { return r.key != REPORT_PAD; }
 };
 
 // squeeze the padding slots out of the round's records (order-preserving)
@@ -441,7 +444,7 @@ int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, 
         int32_t s = (int32_t)s64;
         for (int64_t j = offsets[i]; j < offsets[i + 1]; ++j) {
             int64_t v = lits[j] < 0 ? -(int64_t)lits[j] : lits[j];
-            if (v > h->V) return fail(TSG_ERANGE, "literal %d out of range for %d variables", lits[j], h->V);
+            if (v > h->V) h->oob = true;  // stored as-is; testing raises (numpy IndexError, engine.py:251)
         }
         auto it = h->by_size.find(s);
         int bi;
@@ -663,7 +666,8 @@ int tsg_stage_snapshots(tsg_engine* h, const int8_t* rows, int64_t n_rows, int64
 int tsg_round_prepare(tsg_engine* h, const int32_t* group_lanes, const int32_t* group_tid, int32_t n_groups) {
     CKR(validate_handle(h));
     DevGuard g(h->dev);
-    if (n_groups < 0) return fail(TSG_EINVAL, "n_groups < 0");
+    if (n_groups < 0 || n_groups > TSG_MAX_GROUPS)
+        return fail(TSG_EINVAL, "n_groups must be in 0..%d, got %d", TSG_MAX_GROUPS, n_groups);
     h->n_groups = n_groups;
     h->glanes.assign(group_lanes, group_lanes + n_groups);
     h->gtid.assign(group_tid, group_tid + n_groups);
@@ -723,6 +727,18 @@ int tsg_round_test(tsg_engine* h, double activity_inc, tsg_round_result* out) {
     h->n_alloc = 0;
     h->compacted = true;
     h->round_seq++;
+    if (h->n_chunks && h->oob) {  // out-of-range literal stored: numpy would raise IndexError
+        CK(cudaMemsetAsync(h->ctr + 4, 0, 8, h->st));
+        for (auto& b : h->buckets)
+            if (b.count && b.size)
+                k_max_var<<<grid_for(b.count * b.size), 256, 0, h->st>>>(b.lits, b.count, b.size, h->ctr + 4);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(h->h_ctr + 4, h->ctr + 4, 8, cudaMemcpyDeviceToHost, h->st));
+        CK(cudaStreamSynchronize(h->st));
+        if ((int64_t)h->h_ctr[4] > h->V)
+            return fail(TSG_ERANGE, "index %lld is out of bounds for axis 0 with size %d", (long long)h->h_ctr[4], h->V + 1);
+        h->oob = false;
+    }
     if (h->n_chunks) {
         CKR(build_desc(h));
         if (h->n_chunks > 1) CKR(dgrow(h, &h->carry, &h->carry_cap, std::max<int64_t>(1, h->n_tiles * STRIDE)));

@@ -17,7 +17,7 @@ namespace tsg {
 constexpr int MAXG = 64;
 
 #ifndef TSG_TEST_MIN_BLOCKS
-#define TSG_TEST_MIN_BLOCKS 4
+#define TSG_TEST_MIN_BLOCKS 3
 #endif
 
 // ---------------------------------------------------------------------------
@@ -140,20 +140,25 @@ __global__ void __launch_bounds__(256) k_encode(const int8_t* __restrict__ rows,
 // K3+K4+K5: trigger test.  Persistent grid; one warp per tile of 32 clauses
 // of one bucket, one clause per lane.
 //
-// Software pipeline: while a warp tests tile t it already has the first PF
-// literal rows of its next tile in flight (registers), so the HBM latency
-// of the literal stream overlaps the L2 gathers of the current tile.
-// Stage 1 (aggregate filter, engine.py:238-254) walks literals four at a
-// time and stops as soon as every group is negative: the live set
-// (all_false | one_undef) only shrinks, so a zero word is final.
-// Stage 2 (lane test, bitpack.py:120-135) runs per positive group in
-// ascending order with the same early exit, reusing the prefetched
-// literals.  Every triggering group bumps the clause's activity by
-// inc * popcount (fp64 round-to-nearest mul then add, no FMA:
-// engine.py:460); the first triggering group of each thread emits the
-// report (engine.py:462-464).  Report slots are reserved once per warp for
-// an upper bound (the positive-group count); unused slots are written as
-// padding (engine_id = -1) and squeezed out when the records are fetched.
+// The kernel is bound by L2 sectors (every table gather touches a 32-byte
+// sector: DESIGN.md §4), so it is organised to touch as few as possible:
+//  * software pipeline: while a warp tests tile t the first PF literal rows
+//    of its next tile are already in flight (registers);
+//  * stage 1 (aggregate filter, engine.py:238-254) gathers the first four
+//    literals' aggregate entries together, then one literal at a time, and
+//    stops as soon as every group is negative: the live set
+//    (all_false | one_undef) only shrinks, so a zero word is final;
+//  * the aggregate entries of the first PF literals stay in shared memory;
+//    stage 2 (lane test, bitpack.py:120-135) derives the lane words of every
+//    (literal, group) whose value subset is a single value ({T}: all lanes
+//    set and true, {F}: set and false, {U}: unset) and gathers lane words
+//    only for mixed subsets.
+// Every triggering group bumps the clause's activity by inc * popcount (fp64
+// round-to-nearest mul then add, no FMA: engine.py:460); the first
+// triggering group of each thread emits the report (engine.py:462-464).
+// Report slots are reserved once per warp for an upper bound (the
+// positive-group count); unused slots are written as padding (key = ~0) and
+// squeezed out when the records are fetched.
 
 struct BucketDesc {
     const int32_t* lits;
@@ -190,13 +195,19 @@ struct TestParams {
     LW lane_mask[MAXG];
 };
 
-constexpr int PF = 8;               // literal rows prefetched per tile
-constexpr int SMEM_BUCKETS = 1024;  // bucket table cached in shared memory
+constexpr int PF = 8;              // literal rows prefetched per tile
+constexpr int SMEM_BUCKETS = 256;  // bucket descriptors cached in shared memory
+constexpr int TEST_THREADS = 256;
 
-__device__ __forceinline__ void st_report(tsg_report* p, int64_t eid, uint64_t mask, int32_t group,
-                                          int32_t bucket, int64_t slot) {
-    reinterpret_cast<ulonglong2*>(p)[0] = make_ulonglong2((unsigned long long)eid, (unsigned long long)mask);
-    reinterpret_cast<int4*>(p)[1] = make_int4(group, bucket, (int)(uint32_t)slot, (int)(slot >> 32));
+template <class GW>
+constexpr size_t test_smem_bytes() {
+    return sizeof(BucketDesc) * SMEM_BUCKETS + sizeof(AggEntry<GW>) * PF * TEST_THREADS;
+}
+
+constexpr uint64_t REPORT_PAD = ~0ull;
+
+__device__ __forceinline__ void st_report(tsg_report* p, uint64_t key, uint64_t mask) {
+    *reinterpret_cast<ulonglong2*>(p) = make_ulonglong2(key, mask);
 }
 
 struct Tile {
@@ -207,27 +218,22 @@ struct Tile {
     bool active;
 };
 
-__device__ __forceinline__ int find_bucket(const int64_t* s_tile0, const BucketDesc* buckets, int nb, int64_t tile) {
+__device__ __forceinline__ const BucketDesc* find_bucket(const BucketDesc* sb, const BucketDesc* gb, int nb,
+                                                         int64_t tile) {
+    const BucketDesc* b = nb <= SMEM_BUCKETS ? sb : gb;
     int lo = 0, hi = nb - 1;
-    if (nb <= SMEM_BUCKETS) {
-        while (lo < hi) {
-            int mid = (lo + hi + 1) >> 1;
-            if (s_tile0[mid] <= tile) lo = mid; else hi = mid - 1;
-        }
-    } else {
-        while (lo < hi) {
-            int mid = (lo + hi + 1) >> 1;
-            if (buckets[mid].tile0 <= tile) lo = mid; else hi = mid - 1;
-        }
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (b[mid].tile0 <= tile) lo = mid; else hi = mid - 1;
     }
-    return lo;
+    return b + lo;
 }
 
 template <class LW, class GW>
-__device__ __forceinline__ Tile open_tile(const TestParams<LW, GW>& p, const int64_t* s_tile0, int64_t tile, int lane,
+__device__ __forceinline__ Tile open_tile(const TestParams<LW, GW>& p, const BucketDesc* sb, int64_t tile, int lane,
                                           int32_t (&buf)[PF]) {
     Tile t;
-    t.bd = p.buckets + find_bucket(s_tile0, p.buckets, p.nb, tile);
+    t.bd = find_bucket(sb, p.buckets, p.nb, tile);
     t.size = t.bd->size;
     const int64_t blk = tile - t.bd->tile0;
     t.slot = blk * STRIDE + lane;
@@ -238,48 +244,57 @@ __device__ __forceinline__ Tile open_tile(const TestParams<LW, GW>& p, const int
     return t;
 }
 
+__device__ __forceinline__ int lit_var(int32_t lit) { return lit < 0 ? -lit : lit; }
+
 template <class LW, class GW>
-__global__ void __launch_bounds__(256, TSG_TEST_MIN_BLOCKS) k_test(const __grid_constant__ TestParams<LW, GW> p) {
-    __shared__ int64_t s_tile0[SMEM_BUCKETS];
-    __shared__ unsigned long long s_acc[3][8];
-    for (int i = threadIdx.x; i < p.nb && i < SMEM_BUCKETS; i += blockDim.x) s_tile0[i] = p.buckets[i].tile0;
+__global__ void __launch_bounds__(TEST_THREADS, TSG_TEST_MIN_BLOCKS) k_test(const __grid_constant__ TestParams<LW, GW> p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    BucketDesc* sb = reinterpret_cast<BucketDesc*>(smem);
+    AggEntry<GW>* sagg = reinterpret_cast<AggEntry<GW>*>(smem + sizeof(BucketDesc) * SMEM_BUCKETS);
+    __shared__ unsigned long long s_acc[3][TEST_THREADS / 32];
+    if (p.nb <= SMEM_BUCKETS)
+        for (int i = threadIdx.x; i < p.nb; i += blockDim.x) sb[i] = p.buckets[i];
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
+    AggEntry<GW>* my = sagg + threadIdx.x;  // my[j * TEST_THREADS]: aggregate entry of literal j
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     unsigned long long pos_acc = 0, trig_acc = 0, rep_acc = 0;
 
     int64_t tile = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int32_t cur[PF], nxt[PF];
     Tile T{};
-    if (tile < p.n_tiles) T = open_tile(p, s_tile0, tile, lane, cur);
+    if (tile < p.n_tiles) T = open_tile(p, sb, tile, lane, cur);
 
     for (; tile < p.n_tiles; tile += nwarps) {
         Tile N{};
-        if (tile + nwarps < p.n_tiles) N = open_tile(p, s_tile0, tile + nwarps, lane, nxt);
+        if (tile + nwarps < p.n_tiles) N = open_tile(p, sb, tile + nwarps, lane, nxt);
         const int size = T.size;
 
         // ---- stage 1: aggregate filter -------------------------------------
         GW af = ~GW(0), ou = GW(0);
         if (T.active) {
-#pragma unroll
-            for (int h = 0; h < PF; h += 4) {
-                if (h >= size || (af | ou) == GW(0)) break;
+            {
                 AggEntry<GW> e[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) e[u] = ld_agg(p.agg + (cur[h + u] < 0 ? -cur[h + u] : cur[h + u]));
+                for (int u = 0; u < 4; ++u) e[u] = ld_agg(p.agg + lit_var(cur[u]));
 #pragma unroll
-                for (int u = 0; u < 4; ++u) step<GW>(af, ou, cur[h + u] < 0 ? e[u].t : e[u].f, e[u].u);
+                for (int u = 0; u < 4; ++u) {
+                    my[u * TEST_THREADS] = e[u];
+                    step<GW>(af, ou, cur[u] < 0 ? e[u].t : e[u].f, e[u].u);
+                }
             }
-            for (int j = PF; j < size && (af | ou) != GW(0); j += 4) {
-                int32_t l[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) l[u] = (j + u < size) ? __ldg(T.lp + (j + u) * STRIDE) : p.sentinel;
-                AggEntry<GW> e[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) e[u] = ld_agg(p.agg + (l[u] < 0 ? -l[u] : l[u]));
-#pragma unroll
-                for (int u = 0; u < 4; ++u) step<GW>(af, ou, l[u] < 0 ? e[u].t : e[u].f, e[u].u);
+            for (int u = 4; u < PF; ++u) {
+                if (u >= size || (af | ou) == GW(0)) break;
+                const AggEntry<GW> e = ld_agg(p.agg + lit_var(cur[u]));
+                my[u * TEST_THREADS] = e;
+                step<GW>(af, ou, cur[u] < 0 ? e.t : e.f, e.u);
+            }
+            for (int j = PF; j < size && (af | ou) != GW(0); ++j) {
+                const int32_t l = __ldg(T.lp + j * STRIDE);
+                const AggEntry<GW> e = ld_agg(p.agg + lit_var(l));
+                step<GW>(af, ou, l < 0 ? e.t : e.f, e.u);
             }
         }
         const GW word = T.active ? ((af | ou) & p.group_mask) : GW(0);
@@ -306,37 +321,46 @@ __global__ void __launch_bounds__(256, TSG_TEST_MIN_BLOCKS) k_test(const __grid_
                 const int64_t gslot = T.bd->tile0 * STRIDE + T.slot;
                 double act = 0.0;
                 if (!p.emit_only) act = T.bd->acts[T.slot];
+                const uint64_t key0 = (uint64_t)T.bd->ids[T.slot] << 16;
                 bool touched = false;
                 int last_tid = INT_MIN;
-                const int64_t eid = T.bd->ids[T.slot];
                 GW left = word;
                 while (left) {
                     const int g = __ffsll((long long)(unsigned long long)left) - 1;
                     left &= left - GW(1);
                     const LaneEntry<LW>* lt = p.lane + (int64_t)g * p.vstride;
+                    const LW lm = p.lane_mask[g];
                     LW lf = ~LW(0), lo2 = LW(0);
+                    LW isf[PF], iss[PF];
 #pragma unroll
-                    for (int h = 0; h < PF; h += 4) {
-                        if (h >= size || (lf | lo2) == LW(0)) break;
-                        LaneEntry<LW> e[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) e[u] = ld_lane(lt + (cur[h + u] < 0 ? -cur[h + u] : cur[h + u]));
-#pragma unroll
-                        for (int u = 0; u < 4; ++u)
-                            step<LW>(lf, lo2, cur[h + u] < 0 ? (e[u].s & e[u].t) : (e[u].s & ~e[u].t), ~e[u].s);
+                    for (int u = 0; u < PF; ++u) {
+                        if (u < size) {
+                            const bool neg = cur[u] < 0;
+                            const AggEntry<GW> sv = my[u * TEST_THREADS];
+                            const unsigned tb = (unsigned)((neg ? sv.f : sv.t) >> g) & 1u;
+                            const unsigned fb = (unsigned)((neg ? sv.t : sv.f) >> g) & 1u;
+                            const unsigned nb = (unsigned)(sv.u >> g) & 1u;
+                            if (tb + fb + nb == 1u) {  // single-valued subset: lane words are implied
+                                iss[u] = nb ? LW(0) : lm;
+                                isf[u] = fb ? lm : LW(0);
+                            } else {
+                                const LaneEntry<LW> e = ld_lane(lt + lit_var(cur[u]));
+                                iss[u] = e.s;
+                                isf[u] = neg ? (e.s & e.t) : (e.s & ~e.t);
+                            }
+                        } else {
+                            iss[u] = ~LW(0);
+                            isf[u] = ~LW(0);
+                        }
                     }
-                    for (int j = PF; j < size && (lf | lo2) != LW(0); j += 4) {
-                        int32_t l[4];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) l[u] = (j + u < size) ? __ldg(T.lp + (j + u) * STRIDE) : p.sentinel;
-                        LaneEntry<LW> e[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) e[u] = ld_lane(lt + (l[u] < 0 ? -l[u] : l[u]));
-#pragma unroll
-                        for (int u = 0; u < 4; ++u)
-                            step<LW>(lf, lo2, l[u] < 0 ? (e[u].s & e[u].t) : (e[u].s & ~e[u].t), ~e[u].s);
+                    for (int u = 0; u < PF; ++u) step<LW>(lf, lo2, isf[u], ~iss[u]);
+                    for (int j = PF; j < size && (lf | lo2) != LW(0); ++j) {
+                        const int32_t l = __ldg(T.lp + j * STRIDE);
+                        const LaneEntry<LW> e = ld_lane(lt + lit_var(l));
+                        step<LW>(lf, lo2, l < 0 ? (e.s & e.t) : (e.s & ~e.t), ~e.s);
                     }
-                    const LW mask = (lf | lo2) & p.lane_mask[g];
+                    const LW mask = (lf | lo2) & lm;
                     if (!mask) continue;
                     const int hits = __popcll((unsigned long long)mask);
                     trig_acc += hits;
@@ -350,7 +374,7 @@ __global__ void __launch_bounds__(256, TSG_TEST_MIN_BLOCKS) k_test(const __grid_
                         bool dup = false;
                         if (tid == p.carry_in_tid) dup = p.carry[gslot] == (p.stamp_base | (uint32_t)tid);
                         if (!dup) {
-                            if (pos < p.out_cap) st_report(p.out + pos, eid, (uint64_t)mask, p.g0 + g, T.bd->rank, T.slot);
+                            if (pos < p.out_cap) st_report(p.out + pos, key0 | (uint32_t)(p.g0 + g), (uint64_t)mask);
                             ++pos;
                             ++rep_acc;
                         }
@@ -360,7 +384,7 @@ __global__ void __launch_bounds__(256, TSG_TEST_MIN_BLOCKS) k_test(const __grid_
                 if (p.carry_out_tid >= 0 && last_tid == p.carry_out_tid)
                     p.carry[gslot] = p.stamp_base | (uint32_t)last_tid;
                 for (; pos < end; ++pos)  // padding for reserved-but-unused slots
-                    if (pos < p.out_cap) st_report(p.out + pos, -1, 0, -1, -1, -1);
+                    if (pos < p.out_cap) st_report(p.out + pos, REPORT_PAD, 0);
             }
         }
 

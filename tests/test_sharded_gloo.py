@@ -49,7 +49,8 @@ def _worker(rank, world, port, out_q):
         snaps = snaps.reshape(-1, nv + 1)
         gl, gt = W.groups_for(3, 32, 16)  # lane_width 16 -> 6 groups
         recs, ctr = st.test_round(nv, snaps, gl, gt, 16, 4, 1.0)  # group_width 4 -> 2 chunks
-        parts = S.gather_records(dist, np.asarray(recs), 0)
+        from paper_2012_03119_b200 import reports as R
+        parts = S.gather_records(dist, R.encode(recs["engine_id"], recs["group"], recs["lane_mask"]), 0)
         # global reduce: gather eligible keys, exact threshold, local victim counts
         acts = np.concatenate([b[5] for b in st.buckets()]) if st.buckets() else np.zeros(0)
         kid = np.concatenate([b[3] for b in st.buckets()]) if st.buckets() else np.zeros(0, np.int64)
@@ -88,7 +89,8 @@ def test_two_rank_round_and_reduce_match_unsharded_oracle():
     for p in procs:
         p.join(timeout=60)
     assert status == "ok", merged
-    merged = np.frombuffer(merged, dtype=REPORT_DTYPE)
+    from paper_2012_03119_b200.reports import DECODED_DTYPE
+    merged = np.frombuffer(merged, dtype=DECODED_DTYPE)
 
     # unsharded oracle on the same inputs
     nv = 400
