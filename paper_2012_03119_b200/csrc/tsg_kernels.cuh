@@ -17,7 +17,7 @@ namespace tsg {
 constexpr int MAXG = 64;
 
 #ifndef TSG_TEST_MIN_BLOCKS
-#define TSG_TEST_MIN_BLOCKS 3
+#define TSG_TEST_MIN_BLOCKS 4
 #endif
 
 // ---------------------------------------------------------------------------
@@ -86,21 +86,26 @@ __global__ void __launch_bounds__(256) k_encode(const int8_t* __restrict__ rows,
         LW tw[4] = {0, 0, 0, 0}, sw[4] = {0, 0, 0, 0};
         if (v0 <= V) {
             const int8_t* base = rows + c.row0[g] * c.pitch + v0;
-            for (int r0 = 0; r0 < n; r0 += 8) {
-                uint32_t w[8];
+            for (int r0 = 0; r0 < n; r0 += 16) {  // 16 row loads in flight per thread
+                uint32_t w[16];
 #pragma unroll
-                for (int k = 0; k < 8; ++k)
+                for (int k = 0; k < 16; ++k)
                     w[k] = (r0 + k < n) ? __ldg(reinterpret_cast<const uint32_t*>(base + (int64_t)(r0 + k) * c.pitch)) : 0u;
-                uint32_t aT = 0, aS = 0;
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {  // row r0+k ends at bit k of each byte
-                    aT = ((aT >> 1) & 0x7F7F7F7Fu) | eq1_msb(w[k]);
-                    aS = ((aS >> 1) & 0x7F7F7F7Fu) | nz_msb(w[k]);
-                }
+                for (int h = 0; h < 16; h += 8) {
+                    uint32_t aT = 0, aS = 0;
 #pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    tw[b] |= (LW)((aT >> (8 * b)) & 0xFFu) << r0;
-                    sw[b] |= (LW)((aS >> (8 * b)) & 0xFFu) << r0;
+                    for (int k = 0; k < 8; ++k) {  // row r0+h+k ends at bit k of each byte
+                        aT = ((aT >> 1) & 0x7F7F7F7Fu) | eq1_msb(w[h + k]);
+                        aS = ((aS >> 1) & 0x7F7F7F7Fu) | nz_msb(w[h + k]);
+                    }
+                    if (r0 + h < (int)(sizeof(LW) * 8)) {
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) {
+                            tw[b] |= (LW)((aT >> (8 * b)) & 0xFFu) << (r0 + h);
+                            sw[b] |= (LW)((aS >> (8 * b)) & 0xFFu) << (r0 + h);
+                        }
+                    }
                 }
             }
         }
@@ -141,13 +146,14 @@ __global__ void __launch_bounds__(256) k_encode(const int8_t* __restrict__ rows,
 // of one bucket, one clause per lane.
 //
 // The kernel is bound by L2 sectors (every table gather touches a 32-byte
-// sector: DESIGN.md §4), so it is organised to touch as few as possible:
-//  * software pipeline: while a warp tests tile t the first PF literal rows
-//    of its next tile are already in flight (registers);
-//  * stage 1 (aggregate filter, engine.py:238-254) gathers the first four
-//    literals' aggregate entries together, then one literal at a time, and
-//    stops as soon as every group is negative: the live set
-//    (all_false | one_undef) only shrinks, so a zero word is final;
+// sector: DESIGN.md §4) and by the latency of the gather chains, so:
+//  * the first PF literal rows of a warp's next tile are copied into shared
+//    memory with cp.async while the current tile is tested (double buffer,
+//    no registers held by the prefetch);
+//  * stage 1 (aggregate filter, engine.py:238-254) gathers four literals'
+//    aggregate entries at a time and stops as soon as every group is
+//    negative: the live set (all_false | one_undef) only shrinks, so a zero
+//    word is final;
 //  * the aggregate entries of the first PF literals stay in shared memory;
 //    stage 2 (lane test, bitpack.py:120-135) derives the lane words of every
 //    (literal, group) whose value subset is a single value ({T}: all lanes
@@ -195,13 +201,16 @@ struct TestParams {
     LW lane_mask[MAXG];
 };
 
-constexpr int PF = 8;              // literal rows prefetched per tile
-constexpr int SMEM_BUCKETS = 256;  // bucket descriptors cached in shared memory
+constexpr int PF = 8;             // literal rows prefetched per tile
+constexpr int SMEM_BUCKETS = 64;  // bucket descriptors cached in shared memory
 constexpr int TEST_THREADS = 256;
+constexpr int TEST_WARPS = TEST_THREADS / 32;
 
 template <class GW>
 constexpr size_t test_smem_bytes() {
-    return sizeof(BucketDesc) * SMEM_BUCKETS + sizeof(AggEntry<GW>) * PF * TEST_THREADS;
+    return sizeof(BucketDesc) * SMEM_BUCKETS           // bucket table
+           + sizeof(AggEntry<GW>) * PF * TEST_THREADS  // stage-1 entries kept for stage 2
+           + sizeof(int32_t) * 2 * PF * TEST_THREADS;  // literal-row double buffer
 }
 
 constexpr uint64_t REPORT_PAD = ~0ull;
@@ -209,6 +218,16 @@ constexpr uint64_t REPORT_PAD = ~0ull;
 __device__ __forceinline__ void st_report(tsg_report* p, uint64_t key, uint64_t mask) {
     *reinterpret_cast<ulonglong2*>(p) = make_ulonglong2(key, mask);
 }
+
+__device__ __forceinline__ void cp_async4(int32_t* dst, const int32_t* src, bool pred) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p cp.async.ca.shared.global [%0], [%1], 4;\n}\n" ::"r"(s),
+        "l"(src), "r"((int)pred)
+        : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
 struct Tile {
     const BucketDesc* bd;
@@ -229,9 +248,10 @@ __device__ __forceinline__ const BucketDesc* find_bucket(const BucketDesc* sb, c
     return b + lo;
 }
 
+// open a tile and start copying its first PF literal rows into `buf` (this lane's column)
 template <class LW, class GW>
 __device__ __forceinline__ Tile open_tile(const TestParams<LW, GW>& p, const BucketDesc* sb, int64_t tile, int lane,
-                                          int32_t (&buf)[PF]) {
+                                          int32_t* buf) {
     Tile t;
     t.bd = find_bucket(sb, p.buckets, p.nb, tile);
     t.size = t.bd->size;
@@ -240,7 +260,7 @@ __device__ __forceinline__ Tile open_tile(const TestParams<LW, GW>& p, const Buc
     t.active = t.slot < t.bd->count;
     t.lp = t.bd->lits + blk * (int64_t)t.size * STRIDE + lane;
 #pragma unroll
-    for (int u = 0; u < PF; ++u) buf[u] = (t.active && u < t.size) ? __ldg(t.lp + u * STRIDE) : p.sentinel;
+    for (int u = 0; u < PF; ++u) cp_async4(buf + u * 32, t.lp + u * STRIDE, t.active && u < t.size);
     return t;
 }
 
@@ -251,50 +271,62 @@ __global__ void __launch_bounds__(TEST_THREADS, TSG_TEST_MIN_BLOCKS) k_test(cons
     extern __shared__ __align__(16) unsigned char smem[];
     BucketDesc* sb = reinterpret_cast<BucketDesc*>(smem);
     AggEntry<GW>* sagg = reinterpret_cast<AggEntry<GW>*>(smem + sizeof(BucketDesc) * SMEM_BUCKETS);
-    __shared__ unsigned long long s_acc[3][TEST_THREADS / 32];
+    int32_t* slit = reinterpret_cast<int32_t*>(smem + sizeof(BucketDesc) * SMEM_BUCKETS +
+                                               sizeof(AggEntry<GW>) * PF * TEST_THREADS);
+    __shared__ unsigned long long s_acc[3][TEST_WARPS];
     if (p.nb <= SMEM_BUCKETS)
         for (int i = threadIdx.x; i < p.nb; i += blockDim.x) sb[i] = p.buckets[i];
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
-    AggEntry<GW>* my = sagg + threadIdx.x;  // my[j * TEST_THREADS]: aggregate entry of literal j
+    const int warp = threadIdx.x >> 5;
+    AggEntry<GW>* my = sagg + threadIdx.x;               // my[j * TEST_THREADS]: aggregate entry of literal j
+    int32_t* lbuf = slit + warp * (2 * PF * 32) + lane;  // lbuf[(b * PF + u) * 32]: literal row u, buffer b
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     unsigned long long pos_acc = 0, trig_acc = 0, rep_acc = 0;
 
     int64_t tile = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int32_t cur[PF], nxt[PF];
+    int b = 0;
     Tile T{};
-    if (tile < p.n_tiles) T = open_tile(p, sb, tile, lane, cur);
+    if (tile < p.n_tiles) T = open_tile(p, sb, tile, lane, lbuf);
+    cp_async_commit();
 
-    for (; tile < p.n_tiles; tile += nwarps) {
+    for (; tile < p.n_tiles; tile += nwarps, b ^= 1) {
         Tile N{};
-        if (tile + nwarps < p.n_tiles) N = open_tile(p, sb, tile + nwarps, lane, nxt);
+        if (tile + nwarps < p.n_tiles) N = open_tile(p, sb, tile + nwarps, lane, lbuf + (b ^ 1) * PF * 32);
+        cp_async_commit();
+        cp_async_wait1();  // this lane's rows of the current tile have landed
+        const int32_t* cur = lbuf + b * PF * 32;
         const int size = T.size;
+#define LIT(u) ((u) < size ? cur[(u) * 32] : p.sentinel)
 
         // ---- stage 1: aggregate filter -------------------------------------
         GW af = ~GW(0), ou = GW(0);
         if (T.active) {
-            {
+#pragma unroll
+            for (int h = 0; h < PF; h += 4) {
+                if (h >= size || (af | ou) == GW(0)) break;
+                int32_t l[4];
                 AggEntry<GW> e[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) e[u] = ld_agg(p.agg + lit_var(cur[u]));
+                for (int u = 0; u < 4; ++u) l[u] = LIT(h + u);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) e[u] = ld_agg(p.agg + lit_var(l[u]));
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    my[u * TEST_THREADS] = e[u];
-                    step<GW>(af, ou, cur[u] < 0 ? e[u].t : e[u].f, e[u].u);
+                    my[(h + u) * TEST_THREADS] = e[u];
+                    step<GW>(af, ou, l[u] < 0 ? e[u].t : e[u].f, e[u].u);
                 }
             }
+            for (int j = PF; j < size && (af | ou) != GW(0); j += 4) {
+                int32_t l[4];
+                AggEntry<GW> e[4];
 #pragma unroll
-            for (int u = 4; u < PF; ++u) {
-                if (u >= size || (af | ou) == GW(0)) break;
-                const AggEntry<GW> e = ld_agg(p.agg + lit_var(cur[u]));
-                my[u * TEST_THREADS] = e;
-                step<GW>(af, ou, cur[u] < 0 ? e.t : e.f, e.u);
-            }
-            for (int j = PF; j < size && (af | ou) != GW(0); ++j) {
-                const int32_t l = __ldg(T.lp + j * STRIDE);
-                const AggEntry<GW> e = ld_agg(p.agg + lit_var(l));
-                step<GW>(af, ou, l < 0 ? e.t : e.f, e.u);
+                for (int u = 0; u < 4; ++u) l[u] = (j + u < size) ? __ldg(T.lp + (j + u) * STRIDE) : p.sentinel;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) e[u] = ld_agg(p.agg + lit_var(l[u]));
+#pragma unroll
+                for (int u = 0; u < 4; ++u) step<GW>(af, ou, l[u] < 0 ? e[u].t : e[u].f, e[u].u);
             }
         }
         const GW word = T.active ? ((af | ou) & p.group_mask) : GW(0);
@@ -335,7 +367,8 @@ __global__ void __launch_bounds__(TEST_THREADS, TSG_TEST_MIN_BLOCKS) k_test(cons
 #pragma unroll
                     for (int u = 0; u < PF; ++u) {
                         if (u < size) {
-                            const bool neg = cur[u] < 0;
+                            const int32_t l = cur[u * 32];
+                            const bool neg = l < 0;
                             const AggEntry<GW> sv = my[u * TEST_THREADS];
                             const unsigned tb = (unsigned)((neg ? sv.f : sv.t) >> g) & 1u;
                             const unsigned fb = (unsigned)((neg ? sv.t : sv.f) >> g) & 1u;
@@ -344,7 +377,7 @@ __global__ void __launch_bounds__(TEST_THREADS, TSG_TEST_MIN_BLOCKS) k_test(cons
                                 iss[u] = nb ? LW(0) : lm;
                                 isf[u] = fb ? lm : LW(0);
                             } else {
-                                const LaneEntry<LW> e = ld_lane(lt + lit_var(cur[u]));
+                                const LaneEntry<LW> e = ld_lane(lt + lit_var(l));
                                 iss[u] = e.s;
                                 isf[u] = neg ? (e.s & e.t) : (e.s & ~e.t);
                             }
@@ -387,10 +420,8 @@ __global__ void __launch_bounds__(TEST_THREADS, TSG_TEST_MIN_BLOCKS) k_test(cons
                     if (pos < p.out_cap) st_report(p.out + pos, REPORT_PAD, 0);
             }
         }
-
+#undef LIT
         T = N;
-#pragma unroll
-        for (int u = 0; u < PF; ++u) cur[u] = nxt[u];
     }
 
     // counters: warp reduce, then block reduce, one atomic per block
@@ -400,16 +431,15 @@ __global__ void __launch_bounds__(TEST_THREADS, TSG_TEST_MIN_BLOCKS) k_test(cons
         trig_acc += __shfl_down_sync(0xffffffffu, trig_acc, d);
         rep_acc += __shfl_down_sync(0xffffffffu, rep_acc, d);
     }
-    const int w = threadIdx.x >> 5;
-    if (lane == 0) { s_acc[0][w] = pos_acc; s_acc[1][w] = trig_acc; s_acc[2][w] = rep_acc; }
+    if (lane == 0) { s_acc[0][warp] = pos_acc; s_acc[1][warp] = trig_acc; s_acc[2][warp] = rep_acc; }
     __syncthreads();
     if (threadIdx.x == 0) {
-        unsigned long long a = 0, b = 0, r = 0;
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { a += s_acc[0][i]; b += s_acc[1][i]; r += s_acc[2][i]; }
+        unsigned long long a = 0, bb = 0, r = 0;
+        for (int i = 0; i < TEST_WARPS; ++i) { a += s_acc[0][i]; bb += s_acc[1][i]; r += s_acc[2][i]; }
         if (r) atomicAdd(p.ctr + 3, r);
         if (!p.emit_only) {
             if (a) atomicAdd(p.ctr + 1, a);
-            if (b) atomicAdd(p.ctr + 2, b);
+            if (bb) atomicAdd(p.ctr + 2, bb);
         }
     }
 }

@@ -118,8 +118,13 @@ def test_raw_counters_and_empty_round(P):
 
 
 def test_literal_out_of_range_raises(P):
+    # the reference stores any literal and only fails when a round tests it
+    # (numpy IndexError in the gather, engine.py:251)
     e = P.Engine(3, 1)
     e.add_clause((1, 7), origin=0)
+    e.run_round()
+    assert len(e.store) == 1
+    e.submit_assignment(snap(P, 0, 0, 3, {1: -1}))
     with pytest.raises(IndexError):
         e.run_round()
 
