@@ -17,7 +17,10 @@ namespace tsg {
 constexpr int MAXG = 64;
 
 #ifndef TSG_TEST_MIN_BLOCKS
-#define TSG_TEST_MIN_BLOCKS 4
+#define TSG_TEST_MIN_BLOCKS 3
+#endif
+#ifndef TSG_TAIL  // stage-1 gather batch after the first four literals
+#define TSG_TAIL 4
 #endif
 
 // ---------------------------------------------------------------------------
@@ -147,9 +150,8 @@ __global__ void __launch_bounds__(256) k_encode(const int8_t* __restrict__ rows,
 //
 // The kernel is bound by L2 sectors (every table gather touches a 32-byte
 // sector: DESIGN.md §4) and by the latency of the gather chains, so:
-//  * the first PF literal rows of a warp's next tile are copied into shared
-//    memory with cp.async while the current tile is tested (double buffer,
-//    no registers held by the prefetch);
+//  * the first PF literal rows of a warp's next tile are loaded into
+//    registers while the current tile is tested (software pipeline);
 //  * stage 1 (aggregate filter, engine.py:238-254) gathers four literals'
 //    aggregate entries at a time and stops as soon as every group is
 //    negative: the live set (all_false | one_undef) only shrinks, so a zero
@@ -201,16 +203,13 @@ struct TestParams {
     LW lane_mask[MAXG];
 };
 
-constexpr int PF = 8;             // literal rows prefetched per tile
-constexpr int SMEM_BUCKETS = 64;  // bucket descriptors cached in shared memory
+constexpr int PF = 8;  // literal rows prefetched per tile
 constexpr int TEST_THREADS = 256;
 constexpr int TEST_WARPS = TEST_THREADS / 32;
 
 template <class GW>
 constexpr size_t test_smem_bytes() {
-    return sizeof(BucketDesc) * SMEM_BUCKETS           // bucket table
-           + sizeof(AggEntry<GW>) * PF * TEST_THREADS  // stage-1 entries kept for stage 2
-           + sizeof(int32_t) * 2 * PF * TEST_THREADS;  // literal-row double buffer
+    return sizeof(AggEntry<GW>) * PF * TEST_THREADS;  // stage-1 entries kept for stage 2
 }
 
 constexpr uint64_t REPORT_PAD = ~0ull;
@@ -218,16 +217,6 @@ constexpr uint64_t REPORT_PAD = ~0ull;
 __device__ __forceinline__ void st_report(tsg_report* p, uint64_t key, uint64_t mask) {
     *reinterpret_cast<ulonglong2*>(p) = make_ulonglong2(key, mask);
 }
-
-__device__ __forceinline__ void cp_async4(int32_t* dst, const int32_t* src, bool pred) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile(
-        "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p cp.async.ca.shared.global [%0], [%1], 4;\n}\n" ::"r"(s),
-        "l"(src), "r"((int)pred)
-        : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
 struct Tile {
     const BucketDesc* bd;
@@ -237,30 +226,29 @@ struct Tile {
     bool active;
 };
 
-__device__ __forceinline__ const BucketDesc* find_bucket(const BucketDesc* sb, const BucketDesc* gb, int nb,
-                                                         int64_t tile) {
-    const BucketDesc* b = nb <= SMEM_BUCKETS ? sb : gb;
-    int lo = 0, hi = nb - 1;
-    while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        if (b[mid].tile0 <= tile) lo = mid; else hi = mid - 1;
+// Tiles of a warp increase monotonically, so the warp walks the bucket table
+// forward: `bi` is the current bucket, `nt0` the first tile of the next one.
+__device__ __forceinline__ void seek_bucket(const BucketDesc* b, int nb, int64_t tile, int& bi, int64_t& nt0) {
+    while (tile >= nt0) {
+        ++bi;
+        nt0 = bi + 1 < nb ? b[bi + 1].tile0 : INT64_MAX;
     }
-    return b + lo;
 }
 
-// open a tile and start copying its first PF literal rows into `buf` (this lane's column)
+// open a tile and load its first PF literal rows (this lane's column) into registers
 template <class LW, class GW>
-__device__ __forceinline__ Tile open_tile(const TestParams<LW, GW>& p, const BucketDesc* sb, int64_t tile, int lane,
-                                          int32_t* buf) {
+__device__ __forceinline__ Tile open_tile(const TestParams<LW, GW>& p, int64_t tile, int lane, int& bi, int64_t& nt0,
+                                          int32_t (&buf)[PF]) {
+    seek_bucket(p.buckets, p.nb, tile, bi, nt0);
     Tile t;
-    t.bd = find_bucket(sb, p.buckets, p.nb, tile);
+    t.bd = p.buckets + bi;
     t.size = t.bd->size;
     const int64_t blk = tile - t.bd->tile0;
     t.slot = blk * STRIDE + lane;
     t.active = t.slot < t.bd->count;
     t.lp = t.bd->lits + blk * (int64_t)t.size * STRIDE + lane;
 #pragma unroll
-    for (int u = 0; u < PF; ++u) cp_async4(buf + u * 32, t.lp + u * STRIDE, t.active && u < t.size);
+    for (int u = 0; u < PF; ++u) buf[u] = (t.active && u < t.size) ? __ldg(t.lp + u * STRIDE) : p.sentinel;
     return t;
 }
 
@@ -269,53 +257,60 @@ __device__ __forceinline__ int lit_var(int32_t lit) { return lit < 0 ? -lit : li
 template <class LW, class GW>
 __global__ void __launch_bounds__(TEST_THREADS, TSG_TEST_MIN_BLOCKS) k_test(const __grid_constant__ TestParams<LW, GW> p) {
     extern __shared__ __align__(16) unsigned char smem[];
-    BucketDesc* sb = reinterpret_cast<BucketDesc*>(smem);
-    AggEntry<GW>* sagg = reinterpret_cast<AggEntry<GW>*>(smem + sizeof(BucketDesc) * SMEM_BUCKETS);
-    int32_t* slit = reinterpret_cast<int32_t*>(smem + sizeof(BucketDesc) * SMEM_BUCKETS +
-                                               sizeof(AggEntry<GW>) * PF * TEST_THREADS);
+    AggEntry<GW>* sagg = reinterpret_cast<AggEntry<GW>*>(smem);
     __shared__ unsigned long long s_acc[3][TEST_WARPS];
-    if (p.nb <= SMEM_BUCKETS)
-        for (int i = threadIdx.x; i < p.nb; i += blockDim.x) sb[i] = p.buckets[i];
-    __syncthreads();
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    AggEntry<GW>* my = sagg + threadIdx.x;               // my[j * TEST_THREADS]: aggregate entry of literal j
-    int32_t* lbuf = slit + warp * (2 * PF * 32) + lane;  // lbuf[(b * PF + u) * 32]: literal row u, buffer b
+    AggEntry<GW>* my = sagg + threadIdx.x;  // my[j * TEST_THREADS]: aggregate entry of literal j
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     unsigned long long pos_acc = 0, trig_acc = 0, rep_acc = 0;
 
     int64_t tile = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int b = 0;
+    int bi = 0;
+    int64_t nt0 = 0;
+    if (tile < p.n_tiles) {  // first bucket by binary search, then walk forward
+        int lo = 0, hi = p.nb - 1;
+        while (lo < hi) {
+            int mid = (lo + hi + 1) >> 1;
+            if (p.buckets[mid].tile0 <= tile) lo = mid; else hi = mid - 1;
+        }
+        bi = lo;
+        nt0 = bi + 1 < p.nb ? p.buckets[bi + 1].tile0 : INT64_MAX;
+    }
+    int32_t cur[PF], nxt[PF];
     Tile T{};
-    if (tile < p.n_tiles) T = open_tile(p, sb, tile, lane, lbuf);
-    cp_async_commit();
+    if (tile < p.n_tiles) T = open_tile(p, tile, lane, bi, nt0, cur);
 
-    for (; tile < p.n_tiles; tile += nwarps, b ^= 1) {
+    for (; tile < p.n_tiles; tile += nwarps) {
         Tile N{};
-        if (tile + nwarps < p.n_tiles) N = open_tile(p, sb, tile + nwarps, lane, lbuf + (b ^ 1) * PF * 32);
-        cp_async_commit();
-        cp_async_wait1();  // this lane's rows of the current tile have landed
-        const int32_t* cur = lbuf + b * PF * 32;
+        if (tile + nwarps < p.n_tiles) N = open_tile(p, tile + nwarps, lane, bi, nt0, nxt);
         const int size = T.size;
-#define LIT(u) ((u) < size ? cur[(u) * 32] : p.sentinel)
+#define LIT(u) (cur[u])
 
         // ---- stage 1: aggregate filter -------------------------------------
         GW af = ~GW(0), ou = GW(0);
         if (T.active) {
-#pragma unroll
-            for (int h = 0; h < PF; h += 4) {
-                if (h >= size || (af | ou) == GW(0)) break;
-                int32_t l[4];
+            {  // literals 0..3 together: nearly every clause needs them
                 AggEntry<GW> e[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) l[u] = LIT(h + u);
-#pragma unroll
-                for (int u = 0; u < 4; ++u) e[u] = ld_agg(p.agg + lit_var(l[u]));
+                for (int u = 0; u < 4; ++u) e[u] = ld_agg(p.agg + lit_var(LIT(u)));
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
+                    my[u * TEST_THREADS] = e[u];
+                    step<GW>(af, ou, LIT(u) < 0 ? e[u].t : e[u].f, e[u].u);
+                }
+            }
+#pragma unroll
+            for (int h = 4; h < PF; h += TSG_TAIL) {  // the rest in batches of TSG_TAIL
+                if (h >= size || (af | ou) == GW(0)) break;
+                AggEntry<GW> e[TSG_TAIL];
+#pragma unroll
+                for (int u = 0; u < TSG_TAIL; ++u) e[u] = ld_agg(p.agg + lit_var(LIT(h + u)));
+#pragma unroll
+                for (int u = 0; u < TSG_TAIL; ++u) {
                     my[(h + u) * TEST_THREADS] = e[u];
-                    step<GW>(af, ou, l[u] < 0 ? e[u].t : e[u].f, e[u].u);
+                    step<GW>(af, ou, LIT(h + u) < 0 ? e[u].t : e[u].f, e[u].u);
                 }
             }
             for (int j = PF; j < size && (af | ou) != GW(0); j += 4) {
@@ -367,7 +362,7 @@ __global__ void __launch_bounds__(TEST_THREADS, TSG_TEST_MIN_BLOCKS) k_test(cons
 #pragma unroll
                     for (int u = 0; u < PF; ++u) {
                         if (u < size) {
-                            const int32_t l = cur[u * 32];
+                            const int32_t l = cur[u];
                             const bool neg = l < 0;
                             const AggEntry<GW> sv = my[u * TEST_THREADS];
                             const unsigned tb = (unsigned)((neg ? sv.f : sv.t) >> g) & 1u;
@@ -422,6 +417,8 @@ __global__ void __launch_bounds__(TEST_THREADS, TSG_TEST_MIN_BLOCKS) k_test(cons
         }
 #undef LIT
         T = N;
+#pragma unroll
+        for (int u = 0; u < PF; ++u) cur[u] = nxt[u];
     }
 
     // counters: warp reduce, then block reduce, one atomic per block
