@@ -110,7 +110,11 @@ struct tsg_engine {
     int64_t carry_cap = 0;
     int64_t round_seq = 0;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-    int test_grid = 0;
+    int64_t grid[16] = {0};       // persistent grid per k_test variant
+    int64_t grid_smem[16] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
+    bool smem_table = true;       // shared-memory code table when it fits (TSG_SMEM_TABLE=0 disables)
+    uint8_t* codes = nullptr;     // literal-code table of the current chunk
+    int64_t codes_cap = 0;
 };
 
 namespace {
@@ -215,6 +219,25 @@ int do_encode(tsg_engine* h) {
     return TSG_OK;
 }
 
+template <class LW, class GW, class TAB, int THREADS, int MINB>
+int launch_kernel(tsg_engine* h, const TestParams<LW, GW>& p, int64_t codes_bytes, int variant) {
+    auto* fn = k_test<LW, GW, TAB, THREADS, MINB>;
+    const size_t smem = test_smem_bytes<GW, TAB, THREADS>(codes_bytes);
+    const int key = (int)(sizeof(LW) / 8) * 8 + (int)(sizeof(GW) / 8) * 4 + variant;
+    if (h->grid_smem[key] != (int64_t)smem) {  // occupancy per kernel variant and smem size
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, THREADS, smem));
+        h->grid[key] = std::max(1, per_sm) * h->nsm;
+        h->grid_smem[key] = (int64_t)smem;
+    }
+    int64_t want = (h->n_tiles + THREADS / 32 - 1) / (THREADS / 32);
+    int grid = (int)std::min<int64_t>(want, h->grid[key]);
+    fn<<<grid, THREADS, smem, h->st>>>(p);
+    CK(cudaGetLastError());
+    return TSG_OK;
+}
+
 template <class LW, class GW>
 int launch_test(tsg_engine* h, int c, double inc, int emit_only) {
     TestParams<LW, GW> p{};
@@ -244,18 +267,28 @@ int launch_test(tsg_engine* h, int c, double inc, int emit_only) {
         p.lane_mask[g] = width_mask<LW>(h->glanes[g0 + g]);
     }
     if (h->n_tiles == 0) return TSG_OK;
-    const size_t smem = test_smem_bytes<GW>();
-    if (!h->test_grid) {
-        CK(cudaFuncSetAttribute(k_test<LW, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_test<LW, GW>, TEST_THREADS, smem);
-        h->test_grid = std::max(1, per_sm) * h->nsm;
+    // shared-memory literal-code table when 2 * (V + 2) codes fit (G <= 32)
+    const int ew = G <= 8 ? 2 : (G <= 16 ? 4 : 8);
+    const int64_t codes_bytes = round_up(2 * ((int64_t)h->V + 2) * ew, 16);
+    if constexpr (sizeof(GW) == 4) {
+        if (h->smem_table && codes_bytes <= SMEM_TABLE_MAX) {
+            CKR(dgrow(h, &h->codes, &h->codes_cap, codes_bytes));
+            p.codes = h->codes;
+            p.codes_bytes = codes_bytes;
+            const auto* agg = reinterpret_cast<const AggEntry<uint32_t>*>(p.agg);
+            if (ew == 2) {
+                k_codes<uint16_t><<<grid_for(h->V + 2), 256, 0, h->st>>>(agg, h->V + 2, (uint16_t*)h->codes);
+                return launch_kernel<LW, GW, SmemTable<GW, uint16_t>, TEST_THREADS_SMEM, 1>(h, p, codes_bytes, 1);
+            }
+            if (ew == 4) {
+                k_codes<uint32_t><<<grid_for(h->V + 2), 256, 0, h->st>>>(agg, h->V + 2, (uint32_t*)h->codes);
+                return launch_kernel<LW, GW, SmemTable<GW, uint32_t>, TEST_THREADS_SMEM, 1>(h, p, codes_bytes, 2);
+            }
+            k_codes<uint64_t><<<grid_for(h->V + 2), 256, 0, h->st>>>(agg, h->V + 2, (uint64_t*)h->codes);
+            return launch_kernel<LW, GW, SmemTable<GW, uint64_t>, TEST_THREADS_SMEM, 1>(h, p, codes_bytes, 3);
+        }
     }
-    int64_t want = (h->n_tiles + TEST_THREADS / 32 - 1) / (TEST_THREADS / 32);
-    int grid = (int)std::min<int64_t>(want, h->test_grid);
-    k_test<LW, GW><<<grid, TEST_THREADS, smem, h->st>>>(p);
-    CK(cudaGetLastError());
-    return TSG_OK;
+    return launch_kernel<LW, GW, GlobalTable<GW>, TEST_THREADS, TSG_TEST_MIN_BLOCKS>(h, p, 0, 0);
 }
 
 int run_tests(tsg_engine* h, double inc, int emit_only) {
@@ -394,6 +427,7 @@ int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
     h->dev = cfg->device;
     h->cfg = *cfg;
     h->V = num_vars;
+    if (const char* e = getenv("TSG_SMEM_TABLE")) h->smem_table = atoi(e) != 0;
     DevGuard g(h->dev);
     cudaDeviceProp prop;
     if (cudaGetDeviceProperties(&prop, h->dev) != cudaSuccess) { delete h; return fail(TSG_ECUDA, "device properties"); }
@@ -419,7 +453,7 @@ int tsg_destroy(tsg_engine* h) {
     cudaStreamSynchronize(h->st);
     for (auto& b : h->buckets) { dfree(h, b.lits); dfree(h, b.acts); dfree(h, b.ids); dfree(h, b.origins); }
     dfree(h, h->rows_own); dfree(h, h->tables); dfree(h, h->d_desc); dfree(h, h->out);
-    dfree(h, h->ctr); dfree(h, h->carry); dfree(h, h->out2);
+    dfree(h, h->ctr); dfree(h, h->carry); dfree(h, h->out2); dfree(h, h->codes);
     cudaStreamSynchronize(h->st);
     if (h->h_ctr) cudaFreeHost(h->h_ctr);
     for (auto& e : h->ev) if (e) cudaEventDestroy(e);

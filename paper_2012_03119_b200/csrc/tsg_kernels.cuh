@@ -20,7 +20,15 @@ constexpr int MAXG = 64;
 #define TSG_TEST_MIN_BLOCKS 3
 #endif
 #ifndef TSG_TAIL  // stage-1 gather batch after the first four literals
-#define TSG_TAIL 4
+#define TSG_TAIL 2
+#endif
+#ifdef TSG_LIT_L1  // literal rows through L1 (default: streamed past L1, keeping it for the tables)
+#define LD_LIT(p) __ldg(p)
+#else
+#define LD_LIT(p) ld_lit(p)
+#endif
+#ifndef TSG_DERIVE  // stage 2 derives lane words of single-valued subsets from saved aggregates
+#define TSG_DERIVE 0  // measured: saving the entries costs more than the gathers it saves
 #endif
 
 // ---------------------------------------------------------------------------
@@ -185,6 +193,8 @@ struct TestParams {
     int32_t G;                 // groups in this chunk
     int64_t n_tiles;
     const AggEntry<GW>* agg;
+    const void* codes;         // per-literal-code table (shared-memory variant), codes_bytes long
+    int64_t codes_bytes;
     const LaneEntry<LW>* lane; // [G][vstride]
     int64_t vstride;
     int32_t sentinel;          // num_vars + 1
@@ -204,18 +214,65 @@ struct TestParams {
 };
 
 constexpr int PF = 8;  // literal rows prefetched per tile
-constexpr int TEST_THREADS = 256;
-constexpr int TEST_WARPS = TEST_THREADS / 32;
-
-template <class GW>
-constexpr size_t test_smem_bytes() {
-    return sizeof(AggEntry<GW>) * PF * TEST_THREADS;  // stage-1 entries kept for stage 2
-}
+constexpr int TEST_THREADS = 256;       // block of the L2-table variant
+constexpr int TEST_THREADS_SMEM = 768;  // block of the shared-memory-table variant (one per SM)
+constexpr int64_t SMEM_TABLE_MAX = 200 * 1024;
 
 constexpr uint64_t REPORT_PAD = ~0ull;
 
 __device__ __forceinline__ void st_report(tsg_report* p, uint64_t key, uint64_t mask) {
     *reinterpret_cast<ulonglong2*>(p) = make_ulonglong2(key, mask);
+}
+
+__device__ __forceinline__ int lit_var(int32_t lit) { return lit < 0 ? -lit : lit; }
+
+// Polarity-adjusted value subset of a literal in every group of the chunk:
+// bit g of t / f / u says that some lane of group g makes the literal True /
+// False / leaves it Undef (bitpack.py:138-182 seen through a literal,
+// bitpack.py:263-268).
+template <class GW>
+struct Subset {
+    GW t, f, u;
+};
+
+// Aggregates gathered from the L2-resident table AggEntry[num_vars + 2]:
+// one 32-byte sector per lookup; works for any num_vars.
+template <class GW>
+struct GlobalTable {
+    static constexpr bool kSmem = false;
+    const AggEntry<GW>* agg;
+    __device__ __forceinline__ Subset<GW> get(int32_t lit) const {
+        const AggEntry<GW> e = ld_agg(agg + lit_var(lit));
+        return lit < 0 ? Subset<GW>{e.f, e.t, e.u} : Subset<GW>{e.t, e.f, e.u};
+    }
+};
+
+// Per-literal-code words {can_be_false | can_be_undef << H} in shared memory
+// (code = 2 * var + negative): used when 2 * (num_vars + 2) codes fit, i.e.
+// small num_vars x groups; stage 1 then needs no L2 gathers at all.
+template <class GW, class EW>
+struct SmemTable {
+    static constexpr bool kSmem = true;
+    static constexpr int H = sizeof(EW) * 4;
+    const EW* code;
+    __device__ __forceinline__ Subset<GW> get(int32_t lit) const {
+        const int c = 2 * lit_var(lit) + (lit < 0);
+        const EW a = code[c], b = code[c ^ 1];
+        const EW m = (EW)((EW(1) << H) - 1);
+        return Subset<GW>{(GW)(b & m), (GW)(a & m), (GW)(a >> H)};  // True for lit = False for ~lit
+    }
+};
+
+template <class EW>
+__global__ void k_codes(const AggEntry<uint32_t>* __restrict__ agg, int64_t nv2, EW* __restrict__ code) {
+    constexpr int H = sizeof(EW) * 4;
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; v < nv2; v += (int64_t)gridDim.x * blockDim.x) {
+        const AggEntry<uint32_t> e = agg[v];
+        const EW m = (EW)((EW(1) << H) - 1);
+        code[2 * v] = (EW)((EW)(e.f & m) | (EW)((EW)(e.u & m) << H));      // +v is False where v is False
+        code[2 * v + 1] = (EW)((EW)(e.t & m) | (EW)((EW)(e.u & m) << H));  // -v is False where v is True
+    }
 }
 
 struct Tile {
@@ -248,21 +305,35 @@ __device__ __forceinline__ Tile open_tile(const TestParams<LW, GW>& p, int64_t t
     t.active = t.slot < t.bd->count;
     t.lp = t.bd->lits + blk * (int64_t)t.size * STRIDE + lane;
 #pragma unroll
-    for (int u = 0; u < PF; ++u) buf[u] = (t.active && u < t.size) ? __ldg(t.lp + u * STRIDE) : p.sentinel;
+    for (int u = 0; u < PF; ++u) buf[u] = (t.active && u < t.size) ? LD_LIT(t.lp + u * STRIDE) : p.sentinel;
     return t;
 }
 
-__device__ __forceinline__ int lit_var(int32_t lit) { return lit < 0 ? -lit : lit; }
+template <class GW, class TAB, int THREADS>
+constexpr size_t test_smem_bytes(int64_t codes_bytes) {
+    return TAB::kSmem ? (size_t)codes_bytes : (TSG_DERIVE ? sizeof(AggEntry<GW>) * PF * THREADS : 16);
+}
 
-template <class LW, class GW>
-__global__ void __launch_bounds__(TEST_THREADS, TSG_TEST_MIN_BLOCKS) k_test(const __grid_constant__ TestParams<LW, GW> p) {
+template <class LW, class GW, class TAB, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) k_test(const __grid_constant__ TestParams<LW, GW> p) {
+    constexpr int WARPS = THREADS / 32;
+    constexpr bool SAVE = !TAB::kSmem && TSG_DERIVE;  // keep stage-1 subsets for stage 2
     extern __shared__ __align__(16) unsigned char smem[];
-    AggEntry<GW>* sagg = reinterpret_cast<AggEntry<GW>*>(smem);
-    __shared__ unsigned long long s_acc[3][TEST_WARPS];
+    __shared__ unsigned long long s_acc[3][WARPS];
+    TAB tab;
+    if constexpr (TAB::kSmem) {  // per-block copy of the literal-code table
+        const uint4* src = reinterpret_cast<const uint4*>(p.codes);
+        uint4* dst = reinterpret_cast<uint4*>(smem);
+        for (int64_t i = threadIdx.x; i < p.codes_bytes / 16; i += THREADS) dst[i] = __ldg(src + i);
+        __syncthreads();
+        tab.code = reinterpret_cast<decltype(tab.code)>(smem);
+    } else {
+        tab.agg = p.agg;
+    }
+    AggEntry<GW>* my = reinterpret_cast<AggEntry<GW>*>(smem) + threadIdx.x;  // my[j * THREADS]: literal j
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    AggEntry<GW>* my = sagg + threadIdx.x;  // my[j * TEST_THREADS]: aggregate entry of literal j
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     unsigned long long pos_acc = 0, trig_acc = 0, rep_acc = 0;
 
@@ -286,42 +357,41 @@ __global__ void __launch_bounds__(TEST_THREADS, TSG_TEST_MIN_BLOCKS) k_test(cons
         Tile N{};
         if (tile + nwarps < p.n_tiles) N = open_tile(p, tile + nwarps, lane, bi, nt0, nxt);
         const int size = T.size;
-#define LIT(u) (cur[u])
 
         // ---- stage 1: aggregate filter -------------------------------------
         GW af = ~GW(0), ou = GW(0);
         if (T.active) {
             {  // literals 0..3 together: nearly every clause needs them
-                AggEntry<GW> e[4];
+                Subset<GW> s[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) e[u] = ld_agg(p.agg + lit_var(LIT(u)));
+                for (int u = 0; u < 4; ++u) s[u] = tab.get(cur[u]);
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    my[u * TEST_THREADS] = e[u];
-                    step<GW>(af, ou, LIT(u) < 0 ? e[u].t : e[u].f, e[u].u);
+                    if (SAVE) my[u * THREADS] = AggEntry<GW>{s[u].t, s[u].f, s[u].u, GW(0)};
+                    step<GW>(af, ou, s[u].f, s[u].u);
                 }
             }
 #pragma unroll
             for (int h = 4; h < PF; h += TSG_TAIL) {  // the rest in batches of TSG_TAIL
                 if (h >= size || (af | ou) == GW(0)) break;
-                AggEntry<GW> e[TSG_TAIL];
+                Subset<GW> s[TSG_TAIL];
 #pragma unroll
-                for (int u = 0; u < TSG_TAIL; ++u) e[u] = ld_agg(p.agg + lit_var(LIT(h + u)));
+                for (int u = 0; u < TSG_TAIL; ++u) s[u] = tab.get(cur[h + u]);
 #pragma unroll
                 for (int u = 0; u < TSG_TAIL; ++u) {
-                    my[(h + u) * TEST_THREADS] = e[u];
-                    step<GW>(af, ou, LIT(h + u) < 0 ? e[u].t : e[u].f, e[u].u);
+                    if (SAVE) my[(h + u) * THREADS] = AggEntry<GW>{s[u].t, s[u].f, s[u].u, GW(0)};
+                    step<GW>(af, ou, s[u].f, s[u].u);
                 }
             }
             for (int j = PF; j < size && (af | ou) != GW(0); j += 4) {
                 int32_t l[4];
-                AggEntry<GW> e[4];
+                Subset<GW> s[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) l[u] = (j + u < size) ? __ldg(T.lp + (j + u) * STRIDE) : p.sentinel;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) e[u] = ld_agg(p.agg + lit_var(l[u]));
+                for (int u = 0; u < 4; ++u) s[u] = tab.get(l[u]);
 #pragma unroll
-                for (int u = 0; u < 4; ++u) step<GW>(af, ou, l[u] < 0 ? e[u].t : e[u].f, e[u].u);
+                for (int u = 0; u < 4; ++u) step<GW>(af, ou, s[u].f, s[u].u);
             }
         }
         const GW word = T.active ? ((af | ou) & p.group_mask) : GW(0);
@@ -363,18 +433,26 @@ __global__ void __launch_bounds__(TEST_THREADS, TSG_TEST_MIN_BLOCKS) k_test(cons
                     for (int u = 0; u < PF; ++u) {
                         if (u < size) {
                             const int32_t l = cur[u];
-                            const bool neg = l < 0;
-                            const AggEntry<GW> sv = my[u * TEST_THREADS];
-                            const unsigned tb = (unsigned)((neg ? sv.f : sv.t) >> g) & 1u;
-                            const unsigned fb = (unsigned)((neg ? sv.t : sv.f) >> g) & 1u;
-                            const unsigned nb = (unsigned)(sv.u >> g) & 1u;
+                            unsigned tb = 1u, fb = 1u, nb = 1u;
+                            if (TAB::kSmem || TSG_DERIVE) {
+                                Subset<GW> sv;
+                                if constexpr (TAB::kSmem) {
+                                    sv = tab.get(l);
+                                } else {
+                                    const AggEntry<GW> a = my[u * THREADS];
+                                    sv = Subset<GW>{a.t, a.f, a.u};
+                                }
+                                tb = (unsigned)(sv.t >> g) & 1u;
+                                fb = (unsigned)(sv.f >> g) & 1u;
+                                nb = (unsigned)(sv.u >> g) & 1u;
+                            }
                             if (tb + fb + nb == 1u) {  // single-valued subset: lane words are implied
                                 iss[u] = nb ? LW(0) : lm;
                                 isf[u] = fb ? lm : LW(0);
                             } else {
                                 const LaneEntry<LW> e = ld_lane(lt + lit_var(l));
                                 iss[u] = e.s;
-                                isf[u] = neg ? (e.s & e.t) : (e.s & ~e.t);
+                                isf[u] = l < 0 ? (e.s & e.t) : (e.s & ~e.t);
                             }
                         } else {
                             iss[u] = ~LW(0);
@@ -415,7 +493,6 @@ __global__ void __launch_bounds__(TEST_THREADS, TSG_TEST_MIN_BLOCKS) k_test(cons
                     if (pos < p.out_cap) st_report(p.out + pos, REPORT_PAD, 0);
             }
         }
-#undef LIT
         T = N;
 #pragma unroll
         for (int u = 0; u < PF; ++u) cur[u] = nxt[u];
@@ -432,7 +509,7 @@ __global__ void __launch_bounds__(TEST_THREADS, TSG_TEST_MIN_BLOCKS) k_test(cons
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long a = 0, bb = 0, r = 0;
-        for (int i = 0; i < TEST_WARPS; ++i) { a += s_acc[0][i]; bb += s_acc[1][i]; r += s_acc[2][i]; }
+        for (int i = 0; i < WARPS; ++i) { a += s_acc[0][i]; bb += s_acc[1][i]; r += s_acc[2][i]; }
         if (r) atomicAdd(p.ctr + 3, r);
         if (!p.emit_only) {
             if (a) atomicAdd(p.ctr + 1, a);

@@ -179,11 +179,22 @@ def test_c1_parity_vs_oracle(P):
     assert res.reports > 0 and res.lane_triggers > 0
 
 
+@pytest.mark.parametrize("table", ["smem", "l2"])
 @pytest.mark.parametrize("lw,gw,threads,lanes", [(32, 32, 3, 40), (64, 64, 2, 64), (64, 8, 5, 70),
                                                  (7, 3, 4, 20), (1, 64, 3, 30), (32, 16, 40, 32)])
-def test_widths_and_multichunk_parity(P, lw, gw, threads, lanes):
+def test_widths_and_multichunk_parity(P, monkeypatch, table, lw, gw, threads, lanes):
+    # small num_vars: the shared-memory code table applies (G <= 32); "l2"
+    # forces the L2-gather table path on the same inputs
+    monkeypatch.setenv("TSG_SMEM_TABLE", "1" if table == "smem" else "0")
     run_both(P, n=20_000, threads=threads, lanes=lanes, nv=300, lane_width=lw, group_width=gw,
              seed=lw * 100 + gw, rounds=2, size_lo=0, size_hi=12)
+
+
+@pytest.mark.parametrize("table", ["smem", "l2"])
+def test_c2_shape_parity(P, monkeypatch, table):
+    # C2's 50k vars x 8 groups is the largest code table that fits shared memory
+    monkeypatch.setenv("TSG_SMEM_TABLE", "1" if table == "smem" else "0")
+    run_both(P, n=60_000, threads=8, lanes=32, nv=50_000, seed=22)
 
 
 def test_long_clauses_parity(P):
