@@ -219,6 +219,9 @@ constexpr int TEST_THREADS_SMEM = 768;  // block of the shared-memory-table vari
 constexpr int64_t SMEM_TABLE_MAX = 200 * 1024;
 
 constexpr uint64_t REPORT_PAD = ~0ull;
+#ifndef REPORT_CHUNK  // report slots a warp reserves per atomic
+#define REPORT_CHUNK 128ull
+#endif
 
 __device__ __forceinline__ void st_report(tsg_report* p, uint64_t key, uint64_t mask) {
     *reinterpret_cast<ulonglong2*>(p) = make_ulonglong2(key, mask);
@@ -352,6 +355,9 @@ __global__ void __launch_bounds__(THREADS, MINB) k_test(const __grid_constant__ 
     int32_t cur[PF], nxt[PF];
     Tile T{};
     if (tile < p.n_tiles) T = open_tile(p, tile, lane, bi, nt0, cur);
+    // report slots come from a warp-private chunk [cpos, cend) of the record
+    // buffer, refilled with one atomic every REPORT_CHUNK slots
+    int64_t cpos = 0, cend = 0;
 
     for (; tile < p.n_tiles; tile += nwarps) {
         Tile N{};
@@ -396,7 +402,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_test(const __grid_constant__ 
         }
         const GW word = T.active ? ((af | ou) & p.group_mask) : GW(0);
 
-        // ---- report slot reservation: one atomic per warp --------------------
+        // ---- report slot reservation from the warp's chunk ------------------
         const int ub = __popcll((unsigned long long)word);
         int incl = ub;
 #pragma unroll
@@ -406,11 +412,18 @@ __global__ void __launch_bounds__(THREADS, MINB) k_test(const __grid_constant__ 
         }
         const int total = __shfl_sync(0xffffffffu, incl, 31);
         if (total) {
-            unsigned long long base = 0;
-            if (lane == 31) base = atomicAdd(p.ctr, (unsigned long long)total);
-            base = __shfl_sync(0xffffffffu, base, 31);
-            int64_t pos = (int64_t)base + incl - ub;
+            if (cpos + total > cend) {  // chunk exhausted: pad its tail, take a new one
+                for (int64_t q = cpos + lane; q < cend; q += 32)
+                    if (q < p.out_cap) st_report(p.out + q, REPORT_PAD, 0);
+                const unsigned long long want = total > REPORT_CHUNK ? (unsigned long long)total : REPORT_CHUNK;
+                unsigned long long base = 0;
+                if (lane == 31) base = atomicAdd(p.ctr, want);
+                cpos = (int64_t)__shfl_sync(0xffffffffu, base, 31);
+                cend = cpos + (int64_t)want;
+            }
+            int64_t pos = cpos + incl - ub;
             const int64_t end = pos + ub;
+            cpos += total;
 
             // ---- stage 2: exact lane test per positive group ----------------
             if (word) {
@@ -497,6 +510,9 @@ __global__ void __launch_bounds__(THREADS, MINB) k_test(const __grid_constant__ 
 #pragma unroll
         for (int u = 0; u < PF; ++u) cur[u] = nxt[u];
     }
+
+    for (int64_t q = cpos + lane; q < cend; q += 32)  // pad the tail of the warp's last chunk
+        if (q < p.out_cap) st_report(p.out + q, REPORT_PAD, 0);
 
     // counters: warp reduce, then block reduce, one atomic per block
 #pragma unroll

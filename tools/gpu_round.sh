@@ -1,9 +1,7 @@
 #!/bin/bash
-# one GPU call: tests, bench, variant timing, ncu of both hot kernels
-set -x
-timeout 1200 python -m pytest tests -m gpu -x -q --timeout 300 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
+# one GPU call: tests, bench, timing, ncu of both hot kernels, launch list
+timeout 900 python -m pytest tests -m gpu -x -q --timeout 300 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
 python tools/profile_round.py C3 3 > gpurun_out/prof_plain.log 2>&1
-TSG_LIB=$PWD/paper_2012_03119_b200/libtsg_mb3.so python tools/profile_round.py C3 3 > gpurun_out/prof_mb3.log 2>&1
 python tools/profile_round.py C2 3 > gpurun_out/prof_c2.log 2>&1
 timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_test -s 1 -c 1 -o gpurun_out/prof_test python tools/profile_round.py C3 2 > gpurun_out/ncu_test.log 2>&1
