@@ -278,16 +278,9 @@ __global__ void k_codes(const AggEntry<uint32_t>* __restrict__ agg, int64_t nv2,
     }
 }
 
-struct Tile {
-    const BucketDesc* bd;
-    const int32_t* lp;  // this lane's literal 0 (row stride STRIDE)
-    int64_t slot;
-    int size;
-    bool active;
-};
 
 // Tiles of a warp increase monotonically, so the warp walks the bucket table
-// forward: `bi` is the current bucket, `nt0` the first tile of the next one.
+// forward: `bi` is the tile's bucket, `nt0` the first tile of bucket bi + 1.
 __device__ __forceinline__ void seek_bucket(const BucketDesc* b, int nb, int64_t tile, int& bi, int64_t& nt0) {
     while (tile >= nt0) {
         ++bi;
@@ -295,34 +288,49 @@ __device__ __forceinline__ void seek_bucket(const BucketDesc* b, int nb, int64_t
     }
 }
 
-// open a tile and load its first PF literal rows (this lane's column) into registers
-template <class LW, class GW>
-__device__ __forceinline__ Tile open_tile(const TestParams<LW, GW>& p, int64_t tile, int lane, int& bi, int64_t& nt0,
+// this lane's literal 0 in `tile` of bucket `bd` (literal j at + j * STRIDE)
+__device__ __forceinline__ const int32_t* lane_lits(const BucketDesc* bd, int64_t tile, int lane) {
+    return bd->lits + (tile - bd->tile0) * (int64_t)bd->size * STRIDE + lane;
+}
+
+__device__ __forceinline__ bool lane_active(const BucketDesc* bd, int64_t tile, int lane) {
+    return (tile - bd->tile0) * STRIDE + lane < bd->count;
+}
+
+// load the first PF literal rows of a tile (this lane's column)
+__device__ __forceinline__ void load_rows(const BucketDesc* bd, int64_t tile, int lane, int32_t sentinel,
                                           int32_t (&buf)[PF]) {
-    seek_bucket(p.buckets, p.nb, tile, bi, nt0);
-    Tile t;
-    t.bd = p.buckets + bi;
-    t.size = t.bd->size;
-    const int64_t blk = tile - t.bd->tile0;
-    t.slot = blk * STRIDE + lane;
-    t.active = t.slot < t.bd->count;
-    t.lp = t.bd->lits + blk * (int64_t)t.size * STRIDE + lane;
+    const int32_t* lp = lane_lits(bd, tile, lane);
+    const bool act = lane_active(bd, tile, lane);
+    const int size = bd->size;
 #pragma unroll
-    for (int u = 0; u < PF; ++u) buf[u] = (t.active && u < t.size) ? LD_LIT(t.lp + u * STRIDE) : p.sentinel;
-    return t;
+    for (int u = 0; u < PF; ++u) buf[u] = (act && u < size) ? LD_LIT(lp + u * STRIDE) : sentinel;
 }
 
 template <class GW, class TAB, int THREADS>
 constexpr size_t test_smem_bytes(int64_t codes_bytes) {
-    return TAB::kSmem ? (size_t)codes_bytes : (TSG_DERIVE ? sizeof(AggEntry<GW>) * PF * THREADS : 16);
+    return TAB::kSmem ? (size_t)codes_bytes : 16;
+}
+
+// one batch of stage-2 literals (lane words of group g for literals cur[h..h+3])
+template <class LW>
+__device__ __forceinline__ void lane_batch(const LaneEntry<LW>* lt, const int32_t* cur, int h, int size, LW& lf,
+                                           LW& lo) {
+    LaneEntry<LW> e[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+        if (h + u < size) e[u] = ld_lane(lt + lit_var(cur[h + u]));
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+        if (h + u < size)
+            step<LW>(lf, lo, cur[h + u] < 0 ? (e[u].s & e[u].t) : (e[u].s & ~e[u].t), ~e[u].s);
 }
 
 template <class LW, class GW, class TAB, int THREADS, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB) k_test(const __grid_constant__ TestParams<LW, GW> p) {
     constexpr int WARPS = THREADS / 32;
-    constexpr bool SAVE = !TAB::kSmem && TSG_DERIVE;  // keep stage-1 subsets for stage 2
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ unsigned long long s_acc[3][WARPS];
+    __shared__ unsigned int s_acc[3][WARPS];
     TAB tab;
     if constexpr (TAB::kSmem) {  // per-block copy of the literal-code table
         const uint4* src = reinterpret_cast<const uint4*>(p.codes);
@@ -333,12 +341,11 @@ __global__ void __launch_bounds__(THREADS, MINB) k_test(const __grid_constant__ 
     } else {
         tab.agg = p.agg;
     }
-    AggEntry<GW>* my = reinterpret_cast<AggEntry<GW>*>(smem) + threadIdx.x;  // my[j * THREADS]: literal j
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    unsigned long long pos_acc = 0, trig_acc = 0, rep_acc = 0;
+    unsigned int pos_acc = 0, trig_acc = 0, rep_acc = 0;
 
     int64_t tile = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int bi = 0;
@@ -353,54 +360,55 @@ __global__ void __launch_bounds__(THREADS, MINB) k_test(const __grid_constant__ 
         nt0 = bi + 1 < p.nb ? p.buckets[bi + 1].tile0 : INT64_MAX;
     }
     int32_t cur[PF], nxt[PF];
-    Tile T{};
-    if (tile < p.n_tiles) T = open_tile(p, tile, lane, bi, nt0, cur);
+    if (tile < p.n_tiles) load_rows(p.buckets + bi, tile, lane, p.sentinel, cur);
     // report slots come from a warp-private chunk [cpos, cend) of the record
     // buffer, refilled with one atomic every REPORT_CHUNK slots
     int64_t cpos = 0, cend = 0;
 
     for (; tile < p.n_tiles; tile += nwarps) {
-        Tile N{};
-        if (tile + nwarps < p.n_tiles) N = open_tile(p, tile + nwarps, lane, bi, nt0, nxt);
-        const int size = T.size;
+        const BucketDesc* bd = p.buckets + bi;
+        // software pipeline: the next tile's first rows are in flight while this one is tested
+        if (tile + nwarps < p.n_tiles) {
+            seek_bucket(p.buckets, p.nb, tile + nwarps, bi, nt0);
+            load_rows(p.buckets + bi, tile + nwarps, lane, p.sentinel, nxt);
+        }
+        const int size = bd->size;
+        const bool active = lane_active(bd, tile, lane);
 
-        // ---- stage 1: aggregate filter -------------------------------------
+        // ---- stage 1: aggregate filter (engine.py:238-254) -----------------
         GW af = ~GW(0), ou = GW(0);
-        if (T.active) {
+        if (active) {
             {  // literals 0..3 together: nearly every clause needs them
                 Subset<GW> s[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) s[u] = tab.get(cur[u]);
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    if (SAVE) my[u * THREADS] = AggEntry<GW>{s[u].t, s[u].f, s[u].u, GW(0)};
-                    step<GW>(af, ou, s[u].f, s[u].u);
-                }
+                for (int u = 0; u < 4; ++u) step<GW>(af, ou, s[u].f, s[u].u);
             }
 #pragma unroll
-            for (int h = 4; h < PF; h += TSG_TAIL) {  // the rest in batches of TSG_TAIL
+            for (int h = 4; h < PF; h += TSG_TAIL) {  // then batches of TSG_TAIL while any group is live
                 if (h >= size || (af | ou) == GW(0)) break;
                 Subset<GW> s[TSG_TAIL];
 #pragma unroll
                 for (int u = 0; u < TSG_TAIL; ++u) s[u] = tab.get(cur[h + u]);
 #pragma unroll
-                for (int u = 0; u < TSG_TAIL; ++u) {
-                    if (SAVE) my[(h + u) * THREADS] = AggEntry<GW>{s[u].t, s[u].f, s[u].u, GW(0)};
-                    step<GW>(af, ou, s[u].f, s[u].u);
+                for (int u = 0; u < TSG_TAIL; ++u) step<GW>(af, ou, s[u].f, s[u].u);
+            }
+            if (size > PF && (af | ou) != GW(0)) {
+                const int32_t* lp = lane_lits(bd, tile, lane);
+                for (int j = PF; j < size && (af | ou) != GW(0); j += 4) {
+                    int32_t l[4];
+                    Subset<GW> s[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) l[u] = (j + u < size) ? __ldg(lp + (j + u) * STRIDE) : p.sentinel;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) s[u] = tab.get(l[u]);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) step<GW>(af, ou, s[u].f, s[u].u);
                 }
             }
-            for (int j = PF; j < size && (af | ou) != GW(0); j += 4) {
-                int32_t l[4];
-                Subset<GW> s[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) l[u] = (j + u < size) ? __ldg(T.lp + (j + u) * STRIDE) : p.sentinel;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) s[u] = tab.get(l[u]);
-#pragma unroll
-                for (int u = 0; u < 4; ++u) step<GW>(af, ou, s[u].f, s[u].u);
-            }
         }
-        const GW word = T.active ? ((af | ou) & p.group_mask) : GW(0);
+        const GW word = active ? ((af | ou) & p.group_mask) : GW(0);
 
         // ---- report slot reservation from the warp's chunk ------------------
         const int ub = __popcll((unsigned long long)word);
@@ -425,13 +433,12 @@ __global__ void __launch_bounds__(THREADS, MINB) k_test(const __grid_constant__ 
             const int64_t end = pos + ub;
             cpos += total;
 
-            // ---- stage 2: exact lane test per positive group ----------------
+            // ---- stage 2: exact lane test per positive group (bitpack.py:120-135)
             if (word) {
                 pos_acc += ub;
-                const int64_t gslot = T.bd->tile0 * STRIDE + T.slot;
+                const int64_t slot = (tile - bd->tile0) * STRIDE + lane;
                 double act = 0.0;
-                if (!p.emit_only) act = T.bd->acts[T.slot];
-                const uint64_t key0 = (uint64_t)T.bd->ids[T.slot] << 16;
+                if (!p.emit_only) act = bd->acts[slot];
                 bool touched = false;
                 int last_tid = INT_MIN;
                 GW left = word;
@@ -439,51 +446,22 @@ __global__ void __launch_bounds__(THREADS, MINB) k_test(const __grid_constant__ 
                     const int g = __ffsll((long long)(unsigned long long)left) - 1;
                     left &= left - GW(1);
                     const LaneEntry<LW>* lt = p.lane + (int64_t)g * p.vstride;
-                    const LW lm = p.lane_mask[g];
                     LW lf = ~LW(0), lo2 = LW(0);
-                    LW isf[PF], iss[PF];
-#pragma unroll
-                    for (int u = 0; u < PF; ++u) {
-                        if (u < size) {
-                            const int32_t l = cur[u];
-                            unsigned tb = 1u, fb = 1u, nb = 1u;
-                            if (TAB::kSmem || TSG_DERIVE) {
-                                Subset<GW> sv;
-                                if constexpr (TAB::kSmem) {
-                                    sv = tab.get(l);
-                                } else {
-                                    const AggEntry<GW> a = my[u * THREADS];
-                                    sv = Subset<GW>{a.t, a.f, a.u};
-                                }
-                                tb = (unsigned)(sv.t >> g) & 1u;
-                                fb = (unsigned)(sv.f >> g) & 1u;
-                                nb = (unsigned)(sv.u >> g) & 1u;
-                            }
-                            if (tb + fb + nb == 1u) {  // single-valued subset: lane words are implied
-                                iss[u] = nb ? LW(0) : lm;
-                                isf[u] = fb ? lm : LW(0);
-                            } else {
-                                const LaneEntry<LW> e = ld_lane(lt + lit_var(l));
-                                iss[u] = e.s;
-                                isf[u] = l < 0 ? (e.s & e.t) : (e.s & ~e.t);
-                            }
-                        } else {
-                            iss[u] = ~LW(0);
-                            isf[u] = ~LW(0);
+                    lane_batch<LW>(lt, cur, 0, size, lf, lo2);
+                    if (size > 4 && (lf | lo2) != LW(0)) lane_batch<LW>(lt, cur, 4, size, lf, lo2);
+                    if (size > PF && (lf | lo2) != LW(0)) {
+                        const int32_t* lp = lane_lits(bd, tile, lane);
+                        for (int j = PF; j < size && (lf | lo2) != LW(0); ++j) {
+                            const int32_t l = __ldg(lp + j * STRIDE);
+                            const LaneEntry<LW> e = ld_lane(lt + lit_var(l));
+                            step<LW>(lf, lo2, l < 0 ? (e.s & e.t) : (e.s & ~e.t), ~e.s);
                         }
                     }
-#pragma unroll
-                    for (int u = 0; u < PF; ++u) step<LW>(lf, lo2, isf[u], ~iss[u]);
-                    for (int j = PF; j < size && (lf | lo2) != LW(0); ++j) {
-                        const int32_t l = __ldg(T.lp + j * STRIDE);
-                        const LaneEntry<LW> e = ld_lane(lt + lit_var(l));
-                        step<LW>(lf, lo2, l < 0 ? (e.s & e.t) : (e.s & ~e.t), ~e.s);
-                    }
-                    const LW mask = (lf | lo2) & lm;
+                    const LW mask = (lf | lo2) & p.lane_mask[g];
                     if (!mask) continue;
                     const int hits = __popcll((unsigned long long)mask);
                     trig_acc += hits;
-                    if (!p.emit_only) {
+                    if (!p.emit_only) {  // engine.py:460, rounded like the reference (no FMA)
                         act = __dadd_rn(act, __dmul_rn(p.inc, (double)hits));
                         touched = true;
                     }
@@ -491,26 +469,27 @@ __global__ void __launch_bounds__(THREADS, MINB) k_test(const __grid_constant__ 
                     if (tid != last_tid) {  // first triggering group of this thread (engine.py:462)
                         last_tid = tid;
                         bool dup = false;
-                        if (tid == p.carry_in_tid) dup = p.carry[gslot] == (p.stamp_base | (uint32_t)tid);
+                        if (tid == p.carry_in_tid)
+                            dup = p.carry[bd->tile0 * STRIDE + slot] == (p.stamp_base | (uint32_t)tid);
                         if (!dup) {
-                            if (pos < p.out_cap) st_report(p.out + pos, key0 | (uint32_t)(p.g0 + g), (uint64_t)mask);
+                            if (pos < p.out_cap)
+                                st_report(p.out + pos, ((uint64_t)bd->ids[slot] << 16) | (uint32_t)(p.g0 + g),
+                                          (uint64_t)mask);
                             ++pos;
                             ++rep_acc;
                         }
                     }
                 }
-                if (touched) T.bd->acts[T.slot] = act;
+                if (touched) bd->acts[slot] = act;
                 if (p.carry_out_tid >= 0 && last_tid == p.carry_out_tid)
-                    p.carry[gslot] = p.stamp_base | (uint32_t)last_tid;
+                    p.carry[bd->tile0 * STRIDE + slot] = p.stamp_base | (uint32_t)last_tid;
                 for (; pos < end; ++pos)  // padding for reserved-but-unused slots
                     if (pos < p.out_cap) st_report(p.out + pos, REPORT_PAD, 0);
             }
         }
-        T = N;
 #pragma unroll
         for (int u = 0; u < PF; ++u) cur[u] = nxt[u];
     }
-
     for (int64_t q = cpos + lane; q < cend; q += 32)  // pad the tail of the warp's last chunk
         if (q < p.out_cap) st_report(p.out + q, REPORT_PAD, 0);
 
