@@ -60,13 +60,29 @@ int grid_for(int64_t n, int threads = 256, int cap = 148 * 16) {
     return (int)b;
 }
 
-struct Bucket {
-    int32_t size = 0, rank = 0;
+// One physical interleaved array: the clauses of one size bucket whose hot
+// slab is `slab`.  Slot order inside a part is append order,
+// i.e. engine-id order; a logical bucket is the id-ordered merge of its parts.
+struct Part {
+    int32_t slab = 0;
     int64_t count = 0, cap = 0;  // cap: multiple of STRIDE
-    int32_t* lits = nullptr;
+    int32_t* lits = nullptr;     // hot-prefix order (see hmask)
     double* acts = nullptr;
     int64_t* ids = nullptr;
     int32_t* origins = nullptr;
+    uint64_t* hmask = nullptr;   // original positions (< 64) of the hot prefix
+};
+
+// A size bucket of the reference store (engine.py:122-163), split into one
+// part per variable slab.
+struct Bucket {
+    int32_t size = 0, rank = 0;
+    std::vector<Part> parts;
+    int64_t count() const {
+        int64_t n = 0;
+        for (auto& p : parts) n += p.count;
+        return n;
+    }
 };
 
 }  // namespace
@@ -110,11 +126,19 @@ struct tsg_engine {
     int64_t carry_cap = 0;
     int64_t round_seq = 0;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-    int64_t grid[16] = {0};       // persistent grid per k_test variant
-    int64_t grid_smem[16] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
+    int64_t grid[32] = {0};       // persistent grid per k_test variant
+    int64_t grid_smem[32];        // shared-memory size the grid was computed for (-1: none)
     bool smem_table = true;       // shared-memory code table when it fits (TSG_SMEM_TABLE=0 disables)
     uint8_t* codes = nullptr;     // literal-code table of the current chunk
     int64_t codes_cap = 0;
+
+    // variable slabs: [s * slab_w, (s + 1) * slab_w) for s < n_slabs, covering 0..V+1
+    int32_t n_slabs = 1, slab_w = 0;
+    bool slab_test = true;               // slab kernel when n_slabs > 1 (TSG_SLABS=0 disables)
+    std::vector<int64_t> slab_load;      // clauses per slab (placement tie-break)
+    std::vector<int64_t> h_slab_tile0;   // first tile of each slab (+ end)
+    int64_t* d_slab_tile0 = nullptr;
+    int64_t slab_tile0_cap = 0;
 };
 
 namespace {
@@ -157,29 +181,48 @@ int dgrow(tsg_engine* h, T** p, int64_t* cap, int64_t need, bool keep = false, i
     return TSG_OK;
 }
 
-int bucket_reserve(tsg_engine* h, Bucket& b, int64_t need) {
+void part_free(tsg_engine* h, Part& p) {
+    dfree(h, p.lits); dfree(h, p.acts); dfree(h, p.ids); dfree(h, p.origins); dfree(h, p.hmask);
+    p.lits = nullptr; p.acts = nullptr; p.ids = nullptr; p.origins = nullptr; p.hmask = nullptr;
+}
+
+int part_alloc(tsg_engine* h, Part& p, int32_t size, int64_t cap) {
+    CKR(dalloc(h, (void**)&p.lits, cap * (int64_t)std::max(size, 1) * 4));
+    CKR(dalloc(h, (void**)&p.acts, cap * 8));
+    CKR(dalloc(h, (void**)&p.ids, cap * 8));
+    CKR(dalloc(h, (void**)&p.origins, cap * 4));
+    CKR(dalloc(h, (void**)&p.hmask, cap * 8));
+    p.cap = cap;
+    return TSG_OK;
+}
+
+int part_reserve(tsg_engine* h, Part& b, int32_t size, int64_t need) {
     if (need <= b.cap) return TSG_OK;
     // _SizeBucket._grow doubles with a floor of 4 blocks (engine.py:141-148)
     int64_t nc = std::max<int64_t>(b.cap ? b.cap : 4 * STRIDE, 4 * STRIDE);
     while (nc < need) nc *= 2;
-    int32_t *lits = nullptr, *org = nullptr;
-    double* acts = nullptr;
-    int64_t* ids = nullptr;
-    CKR(dalloc(h, (void**)&lits, nc * (int64_t)std::max(b.size, 1) * 4));
-    CKR(dalloc(h, (void**)&acts, nc * 8));
-    CKR(dalloc(h, (void**)&ids, nc * 8));
-    CKR(dalloc(h, (void**)&org, nc * 4));
+    Part n;
+    n.slab = b.slab;
+    n.count = b.count;
+    CKR(part_alloc(h, n, size, nc));
     if (b.count) {
         int64_t used = round_up(b.count, STRIDE);
-        if (b.size) CK(cudaMemcpyAsync(lits, b.lits, used * b.size * 4, cudaMemcpyDeviceToDevice, h->st));
-        CK(cudaMemcpyAsync(acts, b.acts, b.count * 8, cudaMemcpyDeviceToDevice, h->st));
-        CK(cudaMemcpyAsync(ids, b.ids, b.count * 8, cudaMemcpyDeviceToDevice, h->st));
-        CK(cudaMemcpyAsync(org, b.origins, b.count * 4, cudaMemcpyDeviceToDevice, h->st));
+        if (size) CK(cudaMemcpyAsync(n.lits, b.lits, used * size * 4, cudaMemcpyDeviceToDevice, h->st));
+        CK(cudaMemcpyAsync(n.acts, b.acts, b.count * 8, cudaMemcpyDeviceToDevice, h->st));
+        CK(cudaMemcpyAsync(n.ids, b.ids, b.count * 8, cudaMemcpyDeviceToDevice, h->st));
+        CK(cudaMemcpyAsync(n.origins, b.origins, b.count * 4, cudaMemcpyDeviceToDevice, h->st));
+        CK(cudaMemcpyAsync(n.hmask, b.hmask, b.count * 8, cudaMemcpyDeviceToDevice, h->st));
     }
-    dfree(h, b.lits); dfree(h, b.acts); dfree(h, b.ids); dfree(h, b.origins);
-    b.lits = lits; b.acts = acts; b.ids = ids; b.origins = org;
-    b.cap = nc;
+    part_free(h, b);
+    b = n;
     return TSG_OK;
+}
+
+// every physical part, bucket-major then slab (the order of reduce/remove keep flags)
+template <class F>
+void for_parts(tsg_engine* h, F&& f) {
+    for (auto& b : h->buckets)
+        for (auto& p : b.parts) f(b, p);
 }
 
 bool wide_lane(const tsg_engine* h) { return h->cfg.lane_width > 32; }
@@ -239,6 +282,26 @@ int launch_kernel(tsg_engine* h, const TestParams<LW, GW>& p, int64_t codes_byte
 }
 
 template <class LW, class GW>
+int launch_slab(tsg_engine* h, const TestParams<LW, GW>& p) {
+    auto* fn = k_test_slab<LW, GW, TEST_THREADS_SLAB>;
+    const size_t smem = (size_t)3 * h->slab_w * sizeof(GW);
+    const int key = 16 + (int)(sizeof(LW) / 8) * 2 + (int)(sizeof(GW) / 8);
+    if (h->grid_smem[key] != (int64_t)smem) {
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, TEST_THREADS_SLAB, smem));
+        if (per_sm < 1) return fail(TSG_ECUDA, "slab kernel does not fit an SM (%zu B shared)", smem);
+        h->grid[key] = (int64_t)per_sm * h->nsm;
+        h->grid_smem[key] = (int64_t)smem;
+    }
+    const int64_t per_cta = 64;  // keep >= 64 tiles per CTA so each slab load is amortised
+    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->grid[key], (h->n_tiles + per_cta - 1) / per_cta));
+    fn<<<grid, TEST_THREADS_SLAB, smem, h->st>>>(p);
+    CK(cudaGetLastError());
+    return TSG_OK;
+}
+
+template <class LW, class GW>
 int launch_test(tsg_engine* h, int c, double inc, int emit_only) {
     TestParams<LW, GW> p{};
     int32_t g0 = c * h->cfg.group_width;
@@ -262,6 +325,8 @@ int launch_test(tsg_engine* h, int c, double inc, int emit_only) {
     p.carry_in_tid = (c > 0 && h->gtid[g0] == h->gtid[g0 - 1]) ? h->gtid[g0] : -1;
     p.carry_out_tid = (g0 + G < h->n_groups && h->gtid[g0 + G - 1] == h->gtid[g0 + G]) ? h->gtid[g0 + G - 1] : -1;
     p.emit_only = emit_only;
+    p.slab_tile0 = h->d_slab_tile0;
+    p.slab_w = h->slab_w;
     for (int g = 0; g < G; ++g) {
         p.tid[g] = h->gtid[g0 + g];
         p.lane_mask[g] = width_mask<LW>(h->glanes[g0 + g]);
@@ -288,6 +353,7 @@ int launch_test(tsg_engine* h, int c, double inc, int emit_only) {
             return launch_kernel<LW, GW, SmemTable<GW, uint64_t>, TEST_THREADS_SMEM, 1>(h, p, codes_bytes, 3);
         }
     }
+    if (h->slab_test && h->n_slabs > 1) return launch_slab<LW, GW>(h, p);
     return launch_kernel<LW, GW, GlobalTable<GW>, TEST_THREADS, TSG_TEST_MIN_BLOCKS>(h, p, 0, 0);
 }
 
@@ -303,26 +369,39 @@ int run_tests(tsg_engine* h, double inc, int emit_only) {
 
 int64_t store_size(const tsg_engine* h) {
     int64_t n = 0;
-    for (auto& b : h->buckets) n += b.count;
+    for (auto& b : h->buckets) n += b.count();
     return n;
 }
 
+// Tile table of the round: parts ordered slab-major (then bucket creation
+// order), so every slab's tiles are contiguous and a CTA of the slab kernel
+// loads each slab's table once.  Report order does not depend on it (the
+// host orders records by engine id, reports.py).
 int build_desc(tsg_engine* h) {
     h->h_desc.clear();
+    h->h_slab_tile0.assign(h->n_slabs + 1, 0);
     int64_t tiles = 0;
-    for (auto& b : h->buckets) {
-        if (!b.count) continue;
-        BucketDesc d{};
-        d.lits = b.lits; d.acts = b.acts; d.ids = b.ids;
-        d.size = b.size; d.rank = b.rank; d.count = b.count; d.tile0 = tiles;
-        tiles += (b.count + STRIDE - 1) / STRIDE;
-        h->h_desc.push_back(d);
+    for (int32_t s = 0; s < h->n_slabs; ++s) {
+        h->h_slab_tile0[s] = tiles;
+        for (auto& b : h->buckets) {
+            const Part& p = b.parts[s];
+            if (!p.count) continue;
+            BucketDesc d{};
+            d.lits = p.lits; d.acts = p.acts; d.ids = p.ids;
+            d.size = b.size; d.rank = b.rank; d.count = p.count; d.tile0 = tiles;
+            tiles += (p.count + STRIDE - 1) / STRIDE;
+            h->h_desc.push_back(d);
+        }
     }
+    h->h_slab_tile0[h->n_slabs] = tiles;
     h->n_tiles = tiles;
     CKR(dgrow(h, &h->d_desc, &h->desc_cap, std::max<int64_t>(1, (int64_t)h->h_desc.size())));
     if (!h->h_desc.empty())
         CK(cudaMemcpyAsync(h->d_desc, h->h_desc.data(), h->h_desc.size() * sizeof(BucketDesc),
                            cudaMemcpyHostToDevice, h->st));
+    CKR(dgrow(h, &h->d_slab_tile0, &h->slab_tile0_cap, (int64_t)h->h_slab_tile0.size()));
+    CK(cudaMemcpyAsync(h->d_slab_tile0, h->h_slab_tile0.data(), h->h_slab_tile0.size() * 8,
+                       cudaMemcpyHostToDevice, h->st));
     return TSG_OK;
 }
 
@@ -331,12 +410,12 @@ int validate_handle(tsg_engine* h) {
     return TSG_OK;
 }
 
-// compact every bucket by keep flags laid out in global (bucket order) index
+// compact every part by keep flags laid out in for_parts order
 int compact_all(tsg_engine* h, const uint8_t* keep, const std::vector<int64_t>& base) {
     int64_t* sel = nullptr;
     int64_t* nsel = nullptr;
     int64_t maxc = 0;
-    for (auto& b : h->buckets) maxc = std::max(maxc, b.count);
+    for_parts(h, [&](Bucket&, Part& p) { maxc = std::max(maxc, p.count); });
     if (!maxc) return TSG_OK;
     CKR(dalloc(h, (void**)&sel, maxc * 8));
     CKR(dalloc(h, (void**)&nsel, 8));
@@ -345,32 +424,81 @@ int compact_all(tsg_engine* h, const uint8_t* keep, const std::vector<int64_t>& 
     cub::DeviceSelect::Flagged(nullptr, tmp_bytes, cnt, keep, sel, nsel, maxc, h->st);
     void* tmp = nullptr;
     CKR(dalloc(h, &tmp, (int64_t)tmp_bytes + 16));
-    for (size_t bi = 0; bi < h->buckets.size(); ++bi) {
-        Bucket& b = h->buckets[bi];
-        if (!b.count) continue;
-        CK(cub::DeviceSelect::Flagged(tmp, tmp_bytes, cnt, keep + base[bi], sel, nsel, b.count, h->st));
-        int64_t kept = 0;
-        CK(cudaMemcpyAsync(&kept, nsel, 8, cudaMemcpyDeviceToHost, h->st));
-        CK(cudaStreamSynchronize(h->st));
-        if (kept == b.count) continue;
-        Bucket nb = b;
-        nb.lits = nullptr; nb.acts = nullptr; nb.ids = nullptr; nb.origins = nullptr;
-        nb.cap = b.cap;  // keep capacity (the reference never shrinks, engine.py:184-200)
-        CKR(dalloc(h, (void**)&nb.lits, nb.cap * (int64_t)std::max(b.size, 1) * 4));
-        CKR(dalloc(h, (void**)&nb.acts, nb.cap * 8));
-        CKR(dalloc(h, (void**)&nb.ids, nb.cap * 8));
-        CKR(dalloc(h, (void**)&nb.origins, nb.cap * 4));
-        if (kept) {
-            k_compact<<<grid_for(kept), 256, 0, h->st>>>(sel, kept, b.size, b.lits, b.acts, b.ids, b.origins,
-                                                         nb.lits, nb.acts, nb.ids, nb.origins);
-            CK(cudaGetLastError());
+    size_t pi = 0;
+    for (auto& b : h->buckets) {
+        for (auto& p : b.parts) {
+            const int64_t pb = base[pi++];
+            if (!p.count) continue;
+            CK(cub::DeviceSelect::Flagged(tmp, tmp_bytes, cnt, keep + pb, sel, nsel, p.count, h->st));
+            int64_t kept = 0;
+            CK(cudaMemcpyAsync(&kept, nsel, 8, cudaMemcpyDeviceToHost, h->st));
+            CK(cudaStreamSynchronize(h->st));
+            if (kept == p.count) continue;
+            Part np;
+            np.slab = p.slab;
+            // keep capacity (the reference never shrinks, engine.py:184-200)
+            CKR(part_alloc(h, np, b.size, p.cap));
+            if (kept) {
+                k_compact<<<grid_for(kept), 256, 0, h->st>>>(sel, kept, b.size, p.lits, p.acts, p.ids, p.origins,
+                                                             p.hmask, np.lits, np.acts, np.ids, np.origins,
+                                                             np.hmask);
+                CK(cudaGetLastError());
+            }
+            part_free(h, p);
+            np.count = kept;
+            p = np;
         }
-        dfree(h, b.lits); dfree(h, b.acts); dfree(h, b.ids); dfree(h, b.origins);
-        nb.count = kept;
-        b = nb;
     }
     dfree(h, tmp); dfree(h, sel); dfree(h, nsel);
     return TSG_OK;
+}
+
+// per-part offsets into one flat keep-flag array (for_parts order)
+std::vector<int64_t> part_bases(tsg_engine* h, int64_t* total) {
+    std::vector<int64_t> base;
+    int64_t acc = 0;
+    for_parts(h, [&](Bucket&, Part& p) { base.push_back(acc); acc += p.count; });
+    *total = acc;
+    return base;
+}
+
+int32_t slab_of(const tsg_engine* h, int32_t lit) {
+    int64_t v = lit < 0 ? -(int64_t)lit : lit;
+    return (int32_t)std::min<int64_t>(v / h->slab_w, h->n_slabs - 1);
+}
+
+// Placement of one clause: the slab holding most of its
+// literals among the first 64 positions (ties: the least-loaded slab); those
+// literals move to the front, in order, and hmask records their original
+// positions so readback restores the reference's literal order.
+int32_t place_clause(tsg_engine* h, const int32_t* lits, int32_t size, std::vector<int32_t>& cnt,
+                     int32_t* out, uint64_t* hmask) {
+    const int32_t lim = std::min(size, 64);
+    int32_t slab = 0;
+    if (h->n_slabs > 1 && size > 0) {
+        for (int32_t j = 0; j < lim; ++j) cnt[slab_of(h, lits[j])]++;
+        int32_t best = -1;
+        for (int32_t j = 0; j < lim; ++j) {
+            int32_t s = slab_of(h, lits[j]);
+            if (best < 0 || cnt[s] > cnt[best] || (cnt[s] == cnt[best] && h->slab_load[s] < h->slab_load[best]))
+                best = s;
+        }
+        for (int32_t j = 0; j < lim; ++j) cnt[slab_of(h, lits[j])] = 0;
+        slab = best;
+    }
+    uint64_t m = 0;
+    int32_t o = 0;
+    for (int32_t j = 0; j < lim; ++j) {
+        if (slab_of(h, lits[j]) == slab) {
+            m |= 1ull << j;
+            out[o++] = lits[j];
+        }
+    }
+    for (int32_t j = 0; j < size; ++j)
+        if (j >= 64 || !((m >> j) & 1)) out[o++] = lits[j];
+    *hmask = m;
+    h->slab_load[slab]++;
+    return slab;
 }
 
 struct ValidReport {
@@ -424,10 +552,26 @@ int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(TSG_ECUDA, "no CUDA device");
     if (cfg->device < 0 || cfg->device >= ndev) return fail(TSG_EINVAL, "device %d out of range (%d)", cfg->device, ndev);
     auto* h = new tsg_engine();
+    for (auto& x : h->grid_smem) x = -1;
     h->dev = cfg->device;
     h->cfg = *cfg;
     h->V = num_vars;
     if (const char* e = getenv("TSG_SMEM_TABLE")) h->smem_table = atoi(e) != 0;
+    // variable slabs sized so one slab's aggregate words fit a CTA's shared memory
+    {
+        const int64_t per_var = 3 * (h->cfg.group_width > 32 ? 8 : 4);
+        const int64_t nv2 = (int64_t)num_vars + 2;
+        const int64_t max_w = std::max<int64_t>(32, (SLAB_SMEM_BYTES / per_var) / 32 * 32);
+        int64_t ns = (nv2 + max_w - 1) / max_w;
+        if (const char* e = getenv("TSG_SLABS")) {
+            if (atoi(e) == 0) h->slab_test = false;
+            else if (atoi(e) > 0) ns = std::max<int64_t>(ns, atoi(e));  // force more slabs (tests)
+        }
+        int64_t w = round_up((nv2 + ns - 1) / ns, 32);
+        h->n_slabs = (int32_t)((nv2 + w - 1) / w);
+        h->slab_w = (int32_t)w;
+        h->slab_load.assign(h->n_slabs, 0);
+    }
     DevGuard g(h->dev);
     cudaDeviceProp prop;
     if (cudaGetDeviceProperties(&prop, h->dev) != cudaSuccess) { delete h; return fail(TSG_ECUDA, "device properties"); }
@@ -451,7 +595,8 @@ int tsg_destroy(tsg_engine* h) {
     if (!h) return TSG_OK;
     DevGuard g(h->dev);
     cudaStreamSynchronize(h->st);
-    for (auto& b : h->buckets) { dfree(h, b.lits); dfree(h, b.acts); dfree(h, b.ids); dfree(h, b.origins); }
+    for_parts(h, [&](Bucket&, Part& p) { part_free(h, p); });
+    dfree(h, h->d_slab_tile0);
     dfree(h, h->rows_own); dfree(h, h->tables); dfree(h, h->d_desc); dfree(h, h->out);
     dfree(h, h->ctr); dfree(h, h->carry); dfree(h, h->out2); dfree(h, h->codes);
     cudaStreamSynchronize(h->st);
@@ -471,7 +616,6 @@ int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, 
     // group clauses by size, preserving arrival order; new sizes create buckets
     // in first-seen order (dict insertion order of ClauseStore.buckets)
     std::vector<int> bucket_of(n);
-    std::vector<int64_t> per_bucket_n;
     for (int64_t i = 0; i < n; ++i) {
         int64_t s64 = offsets[i + 1] - offsets[i];
         if (s64 < 0 || s64 > (1 << 24)) return fail(TSG_EINVAL, "bad clause size");
@@ -487,46 +631,61 @@ int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, 
             Bucket b;
             b.size = s;
             b.rank = bi;
+            b.parts.resize(h->n_slabs);
+            for (int32_t q = 0; q < h->n_slabs; ++q) b.parts[q].slab = q;
             h->buckets.push_back(b);
             h->by_size[s] = bi;
         } else {
             bi = it->second;
         }
         bucket_of[i] = bi;
-        if ((int64_t)per_bucket_n.size() <= bi) per_bucket_n.resize(bi + 1, 0);
-        per_bucket_n[bi]++;
     }
-    // per bucket: gather clause-major literals + metadata on the host, one H2D each
-    std::vector<std::vector<int64_t>> members(h->buckets.size());
-    for (int64_t i = 0; i < n; ++i) members[bucket_of[i]].push_back(i);
-    for (size_t bi = 0; bi < members.size(); ++bi) {
-        auto& mem = members[bi];
+    // place every clause in a slab part (hot literals first), then one H2D +
+    // scatter per (bucket, slab) part
+    const int32_t P = h->n_slabs;
+    std::vector<int32_t> cnt(P, 0);
+    std::vector<int32_t> placed((size_t)std::max<int64_t>(offsets[n] - offsets[0], 1));
+    std::vector<uint64_t> hm(n);
+    std::vector<int32_t> slab_of_clause(n);
+    std::vector<std::vector<int64_t>> members(h->buckets.size() * P);
+    for (int64_t i = 0; i < n; ++i) {
+        const int32_t s = (int32_t)(offsets[i + 1] - offsets[i]);
+        slab_of_clause[i] = place_clause(h, lits + offsets[i], s, cnt, placed.data() + (offsets[i] - offsets[0]),
+                                         &hm[i]);
+        members[(size_t)bucket_of[i] * P + slab_of_clause[i]].push_back(i);
+    }
+    for (size_t mi = 0; mi < members.size(); ++mi) {
+        auto& mem = members[mi];
         if (mem.empty()) continue;
-        Bucket& b = h->buckets[bi];
+        Bucket& b = h->buckets[mi / P];
+        Part& p = b.parts[mi % P];
         int64_t k = (int64_t)mem.size();
-        CKR(bucket_reserve(h, b, b.count + k));
+        CKR(part_reserve(h, p, b.size, p.count + k));
         std::vector<int32_t> hl((size_t)(k * b.size));
         std::vector<int64_t> hid(k);
         std::vector<int32_t> hor(k);
+        std::vector<uint64_t> hmk(k);
         for (int64_t c = 0; c < k; ++c) {
             int64_t i = mem[c];
-            if (b.size) memcpy(&hl[c * b.size], lits + offsets[i], b.size * 4);
+            if (b.size) memcpy(&hl[c * b.size], placed.data() + (offsets[i] - offsets[0]), b.size * 4);
             hid[c] = ids[i];
             hor[c] = origins[i];
+            hmk[c] = hm[i];
         }
         if (b.size) {
             int32_t* tmp = nullptr;
             CKR(dalloc(h, (void**)&tmp, k * b.size * 4));
             CK(cudaMemcpyAsync(tmp, hl.data(), k * b.size * 4, cudaMemcpyHostToDevice, h->st));
-            k_append<<<grid_for(k * b.size), 256, 0, h->st>>>(tmp, k, b.size, b.count, b.lits);
+            k_append<<<grid_for(k * b.size), 256, 0, h->st>>>(tmp, k, b.size, p.count, p.lits);
             CK(cudaGetLastError());
             dfree(h, tmp);
         }
-        CK(cudaMemcpyAsync(b.ids + b.count, hid.data(), k * 8, cudaMemcpyHostToDevice, h->st));
-        CK(cudaMemcpyAsync(b.origins + b.count, hor.data(), k * 4, cudaMemcpyHostToDevice, h->st));
-        k_fill_f64<<<grid_for(k), 256, 0, h->st>>>(b.acts + b.count, k, activity);
+        CK(cudaMemcpyAsync(p.ids + p.count, hid.data(), k * 8, cudaMemcpyHostToDevice, h->st));
+        CK(cudaMemcpyAsync(p.origins + p.count, hor.data(), k * 4, cudaMemcpyHostToDevice, h->st));
+        CK(cudaMemcpyAsync(p.hmask + p.count, hmk.data(), k * 8, cudaMemcpyHostToDevice, h->st));
+        k_fill_f64<<<grid_for(k), 256, 0, h->st>>>(p.acts + p.count, k, activity);
         CK(cudaGetLastError());
-        b.count += k;
+        p.count += k;
         CK(cudaStreamSynchronize(h->st));  // host vectors go out of scope
     }
     return TSG_OK;
@@ -548,7 +707,7 @@ int tsg_bucket_info(tsg_engine* h, int32_t b, int32_t* size, int64_t* count) {
     CKR(validate_handle(h));
     if (b < 0 || b >= (int32_t)h->buckets.size()) return fail(TSG_ERANGE, "bucket %d out of range", b);
     *size = h->buckets[b].size;
-    *count = h->buckets[b].count;
+    *count = h->buckets[b].count();
     return TSG_OK;
 }
 
@@ -557,27 +716,50 @@ int tsg_bucket_read(tsg_engine* h, int32_t bi, int32_t* lits, int64_t* ids, int3
     if (bi < 0 || bi >= (int32_t)h->buckets.size()) return fail(TSG_ERANGE, "bucket %d out of range", bi);
     DevGuard g(h->dev);
     Bucket& b = h->buckets[bi];
-    if (!b.count) return TSG_OK;
-    if (lits && b.size) {
-        int32_t* tmp = nullptr;
-        CKR(dalloc(h, (void**)&tmp, b.count * b.size * 4));
-        k_deinterleave<<<grid_for(b.count * b.size), 256, 0, h->st>>>(b.lits, b.count, b.size, tmp);
-        CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(lits, tmp, b.count * b.size * 4, cudaMemcpyDeviceToHost, h->st));
-        dfree(h, tmp);
+    const int64_t total = b.count();
+    if (!total) return TSG_OK;
+    // every part in its own slot order (original literal order restored), then
+    // merged by engine id = the reference's slot order (reports.py)
+    std::vector<int32_t> hl(lits && b.size ? total * b.size : 0);
+    std::vector<int64_t> hid(total);
+    std::vector<int32_t> hor(origins ? total : 0);
+    std::vector<double> hac(acts ? total : 0);
+    int64_t off = 0;
+    for (auto& p : b.parts) {
+        if (!p.count) continue;
+        if (lits && b.size) {
+            int32_t* tmp = nullptr;
+            CKR(dalloc(h, (void**)&tmp, p.count * b.size * 4));
+            k_deinterleave<<<grid_for(p.count), 256, 0, h->st>>>(p.lits, p.hmask, p.count, b.size, tmp);
+            CK(cudaGetLastError());
+            CK(cudaMemcpyAsync(hl.data() + off * b.size, tmp, p.count * b.size * 4, cudaMemcpyDeviceToHost, h->st));
+            dfree(h, tmp);
+        }
+        CK(cudaMemcpyAsync(hid.data() + off, p.ids, p.count * 8, cudaMemcpyDeviceToHost, h->st));
+        if (origins) CK(cudaMemcpyAsync(hor.data() + off, p.origins, p.count * 4, cudaMemcpyDeviceToHost, h->st));
+        if (acts) CK(cudaMemcpyAsync(hac.data() + off, p.acts, p.count * 8, cudaMemcpyDeviceToHost, h->st));
+        off += p.count;
     }
-    if (ids) CK(cudaMemcpyAsync(ids, b.ids, b.count * 8, cudaMemcpyDeviceToHost, h->st));
-    if (origins) CK(cudaMemcpyAsync(origins, b.origins, b.count * 4, cudaMemcpyDeviceToHost, h->st));
-    if (acts) CK(cudaMemcpyAsync(acts, b.acts, b.count * 8, cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
+    std::vector<int64_t> ord(total);
+    for (int64_t i = 0; i < total; ++i) ord[i] = i;
+    std::stable_sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) { return hid[x] < hid[y]; });
+    for (int64_t k = 0; k < total; ++k) {
+        const int64_t i = ord[k];
+        if (ids) ids[k] = hid[i];
+        if (origins) origins[k] = hor[i];
+        if (acts) acts[k] = hac[i];
+        if (lits && b.size) memcpy(lits + k * b.size, hl.data() + i * b.size, b.size * 4);
+    }
     return TSG_OK;
 }
 
 int tsg_scale_activities(tsg_engine* h, double factor) {
     CKR(validate_handle(h));
     DevGuard g(h->dev);
-    for (auto& b : h->buckets)
-        if (b.count) k_scale_f64<<<grid_for(b.count), 256, 0, h->st>>>(b.acts, b.count, factor);
+    for_parts(h, [&](Bucket&, Part& p) {
+        if (p.count) k_scale_f64<<<grid_for(p.count), 256, 0, h->st>>>(p.acts, p.count, factor);
+    });
     CK(cudaGetLastError());
     return TSG_OK;
 }
@@ -586,11 +768,9 @@ int tsg_reduce(tsg_engine* h, int64_t eligible_below, int64_t target, int64_t* r
     CKR(validate_handle(h));
     DevGuard g(h->dev);
     *removed = 0;
-    int64_t total = store_size(h);
+    int64_t total = 0;
+    std::vector<int64_t> base = part_bases(h, &total);
     if (total == 0 || target <= 0) return TSG_OK;
-    std::vector<int64_t> base(h->buckets.size());
-    int64_t acc = 0;
-    for (size_t i = 0; i < h->buckets.size(); ++i) { base[i] = acc; acc += h->buckets[i].count; }
     uint64_t *ka = nullptr, *ki = nullptr, *ka2 = nullptr, *ki2 = nullptr;
     int64_t *ix = nullptr, *ix2 = nullptr, *doomed_ids = nullptr;
     uint8_t* keep = nullptr;
@@ -599,11 +779,14 @@ int tsg_reduce(tsg_engine* h, int64_t eligible_below, int64_t target, int64_t* r
     CKR(dalloc(h, (void**)&ix, total * 8)); CKR(dalloc(h, (void**)&ix2, total * 8));
     CKR(dalloc(h, (void**)&keep, total));
     CK(cudaMemsetAsync(h->ctr + 4, 0, 8, h->st));
-    for (size_t i = 0; i < h->buckets.size(); ++i) {
-        Bucket& b = h->buckets[i];
-        if (!b.count) continue;
-        k_reduce_keys<<<grid_for(b.count), 256, 0, h->st>>>(b.acts, b.ids, b.count, base[i], eligible_below,
-                                                            ka, ki, ix, h->ctr + 4);
+    {
+        size_t pi = 0;
+        for_parts(h, [&](Bucket&, Part& p) {
+            const int64_t pb = base[pi++];
+            if (p.count)
+                k_reduce_keys<<<grid_for(p.count), 256, 0, h->st>>>(p.acts, p.ids, p.count, pb, eligible_below,
+                                                                    ka, ki, ix, h->ctr + 4);
+        });
     }
     CK(cudaGetLastError());
     // stable LSD: sort by id, then stably by activity bits => (activity, id) order (engine.py:488)
@@ -639,23 +822,24 @@ int tsg_remove_clauses(tsg_engine* h, const int64_t* ids, int64_t n, int64_t* re
     CKR(validate_handle(h));
     DevGuard g(h->dev);
     *removed = 0;
-    int64_t total = store_size(h);
+    int64_t total = 0;
+    std::vector<int64_t> base = part_bases(h, &total);
     if (total == 0 || n <= 0) return TSG_OK;
     std::vector<int64_t> del(ids, ids + n);
     std::sort(del.begin(), del.end());
-    std::vector<int64_t> base(h->buckets.size());
-    int64_t acc = 0;
-    for (size_t i = 0; i < h->buckets.size(); ++i) { base[i] = acc; acc += h->buckets[i].count; }
     int64_t* d_del = nullptr;
     uint8_t* keep = nullptr;
     CKR(dalloc(h, (void**)&d_del, n * 8));
     CKR(dalloc(h, (void**)&keep, total));
     CK(cudaMemcpyAsync(d_del, del.data(), n * 8, cudaMemcpyHostToDevice, h->st));
     CK(cudaMemsetAsync(h->ctr + 4, 0, 8, h->st));
-    for (size_t i = 0; i < h->buckets.size(); ++i) {
-        Bucket& b = h->buckets[i];
-        if (!b.count) continue;
-        k_mark_deleted<<<grid_for(b.count), 256, 0, h->st>>>(b.ids, b.count, base[i], d_del, n, keep, h->ctr + 4);
+    {
+        size_t pi = 0;
+        for_parts(h, [&](Bucket&, Part& p) {
+            const int64_t pb = base[pi++];
+            if (p.count)
+                k_mark_deleted<<<grid_for(p.count), 256, 0, h->st>>>(p.ids, p.count, pb, d_del, n, keep, h->ctr + 4);
+        });
     }
     CK(cudaGetLastError());
     unsigned long long gone = 0;
@@ -763,9 +947,10 @@ int tsg_round_test(tsg_engine* h, double activity_inc, tsg_round_result* out) {
     h->round_seq++;
     if (h->n_chunks && h->oob) {  // out-of-range literal stored: numpy would raise IndexError
         CK(cudaMemsetAsync(h->ctr + 4, 0, 8, h->st));
-        for (auto& b : h->buckets)
-            if (b.count && b.size)
-                k_max_var<<<grid_for(b.count * b.size), 256, 0, h->st>>>(b.lits, b.count, b.size, h->ctr + 4);
+        for_parts(h, [&](Bucket& b, Part& p) {
+            if (p.count && b.size)
+                k_max_var<<<grid_for(p.count * b.size), 256, 0, h->st>>>(p.lits, p.count, b.size, h->ctr + 4);
+        });
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(h->h_ctr + 4, h->ctr + 4, 8, cudaMemcpyDeviceToHost, h->st));
         CK(cudaStreamSynchronize(h->st));

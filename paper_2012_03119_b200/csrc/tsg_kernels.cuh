@@ -209,6 +209,8 @@ struct TestParams {
     int32_t carry_in_tid;      // first tid of the chunk if it continues from the previous chunk, else -1
     int32_t carry_out_tid;     // last tid of the chunk if it continues into the next chunk, else -1
     int32_t emit_only;         // replay after report-buffer overflow: no activity / counter side effects
+    const int64_t* slab_tile0; // slab kernel: first tile of each slab (+ end)
+    int32_t slab_w;            // slab kernel: variables per slab
     int32_t tid[MAXG];
     LW lane_mask[MAXG];
 };
@@ -217,6 +219,11 @@ constexpr int PF = 8;  // literal rows prefetched per tile
 constexpr int TEST_THREADS = 256;       // block of the L2-table variant
 constexpr int TEST_THREADS_SMEM = 768;  // block of the shared-memory-table variant (one per SM)
 constexpr int64_t SMEM_TABLE_MAX = 200 * 1024;
+#ifndef TSG_SLAB_THREADS
+#define TSG_SLAB_THREADS 1024
+#endif
+constexpr int TEST_THREADS_SLAB = TSG_SLAB_THREADS;  // block of the slab variant (one per SM)
+constexpr int64_t SLAB_SMEM_BYTES = 224 * 1024;     // one slab's words (227 KB per CTA minus statics)
 
 constexpr uint64_t REPORT_PAD = ~0ull;
 #ifndef REPORT_CHUNK  // report slots a warp reserves per atomic
@@ -243,6 +250,7 @@ struct Subset {
 template <class GW>
 struct GlobalTable {
     static constexpr bool kSmem = false;
+    static constexpr bool kSlab = false;
     const AggEntry<GW>* agg;
     __device__ __forceinline__ Subset<GW> get(int32_t lit) const {
         const AggEntry<GW> e = ld_agg(agg + lit_var(lit));
@@ -256,6 +264,7 @@ struct GlobalTable {
 template <class GW, class EW>
 struct SmemTable {
     static constexpr bool kSmem = true;
+    static constexpr bool kSlab = false;
     static constexpr int H = sizeof(EW) * 4;
     const EW* code;
     __device__ __forceinline__ Subset<GW> get(int32_t lit) const {
@@ -263,6 +272,31 @@ struct SmemTable {
         const EW a = code[c], b = code[c ^ 1];
         const EW m = (EW)((EW(1) << H) - 1);
         return Subset<GW>{(GW)(b & m), (GW)(a & m), (GW)(a >> H)};  // True for lit = False for ~lit
+    }
+};
+
+// One variable slab [lo, lo + w) in shared memory (slab kernel): the
+// can-be-False word of each literal code and the can-be-Undef word of each
+// variable; literals outside the slab are gathered from the L2 table.
+template <class GW>
+struct SlabTable {
+    static constexpr bool kSmem = true;
+    static constexpr bool kSlab = true;
+    const GW* fc;  // [2 * w]: code 2i = +(lo+i), 2i+1 = -(lo+i)
+    const GW* u;   // [w]
+    const AggEntry<GW>* agg;
+    int32_t lo, w;
+    __device__ __forceinline__ bool hot(int32_t lit) const {
+        return (uint32_t)(lit_var(lit) - lo) < (uint32_t)w;
+    }
+    __device__ __forceinline__ void get_hot(int32_t lit, GW& f, GW& uu) const {
+        const int i = lit_var(lit) - lo;
+        f = fc[2 * i + (lit < 0)];
+        uu = u[i];
+    }
+    __device__ __forceinline__ Subset<GW> get(int32_t lit) const {
+        const AggEntry<GW> e = ld_agg(agg + lit_var(lit));
+        return lit < 0 ? Subset<GW>{e.f, e.t, e.u} : Subset<GW>{e.t, e.f, e.u};
     }
 };
 
@@ -326,31 +360,72 @@ __device__ __forceinline__ void lane_batch(const LaneEntry<LW>* lt, const int32_
             step<LW>(lf, lo, cur[h + u] < 0 ? (e[u].s & e[u].t) : (e[u].s & ~e[u].t), ~e[u].s);
 }
 
-template <class LW, class GW, class TAB, int THREADS, int MINB>
-__global__ void __launch_bounds__(THREADS, MINB) k_test(const __grid_constant__ TestParams<LW, GW> p) {
-    constexpr int WARPS = THREADS / 32;
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ unsigned int s_acc[3][WARPS];
-    TAB tab;
-    if constexpr (TAB::kSmem) {  // per-block copy of the literal-code table
-        const uint4* src = reinterpret_cast<const uint4*>(p.codes);
-        uint4* dst = reinterpret_cast<uint4*>(smem);
-        for (int64_t i = threadIdx.x; i < p.codes_bytes / 16; i += THREADS) dst[i] = __ldg(src + i);
-        __syncthreads();
-        tab.code = reinterpret_cast<decltype(tab.code)>(smem);
-    } else {
-        tab.agg = p.agg;
+// Per-warp running state of the tile loop: the warp's report-slot chunk
+// [cpos, cend) and its counter accumulators.
+struct WarpAcc {
+    int64_t cpos = 0, cend = 0;
+    unsigned int pos = 0, trig = 0, rep = 0;
+};
+
+// Stage 1 of the slab kernel for one clause: the hot prefix (literals whose
+// variable lies in the CTA's slab, stored first) is looked up in shared
+// memory; the cold rest is gathered from the L2-resident table two literals
+// at a time while any group is live.
+template <class LW, class GW>
+__device__ __forceinline__ void stage1_slab(const TestParams<LW, GW>& p, const SlabTable<GW>& tab,
+                                            const int32_t (&cur)[PF], const int32_t* lp, int size, GW& af, GW& ou) {
+    int hp = 0;  // hot prefix length
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+        if (hp == u && u < size && tab.hot(cur[u])) {
+            GW f, uu;
+            tab.get_hot(cur[u], f, uu);
+            step<GW>(af, ou, f, uu);
+            hp = u + 1;
+        }
     }
+    if (hp == PF && size > PF) {  // long hot prefix (long clauses)
+        for (; hp < size; ++hp) {
+            const int32_t l = __ldg(lp + hp * STRIDE);
+            if (!tab.hot(l)) break;
+            GW f, uu;
+            tab.get_hot(l, f, uu);
+            step<GW>(af, ou, f, uu);
+        }
+    }
+#pragma unroll
+    for (int b0 = 0; b0 < PF; b0 += 2) {  // cold literals held in registers
+        if (b0 >= size || (af | ou) == GW(0)) break;
+        if (b0 + 2 <= hp) continue;
+        const bool n0 = b0 >= hp, n1 = b0 + 1 >= hp && b0 + 1 < size;
+        Subset<GW> s0{GW(0), ~GW(0), GW(0)}, s1{GW(0), ~GW(0), GW(0)};
+        if (n0) s0 = tab.get(cur[b0]);
+        if (n1) s1 = tab.get(cur[b0 + 1]);
+        step<GW>(af, ou, s0.f, s0.u);
+        step<GW>(af, ou, s1.f, s1.u);
+    }
+    if (size > PF && (af | ou) != GW(0)) {  // cold literals beyond the prefetched rows
+        for (int j = hp > PF ? hp : PF; j < size && (af | ou) != GW(0); j += 4) {
+            int32_t l[4];
+            Subset<GW> s[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) l[u] = (j + u < size) ? __ldg(lp + (j + u) * STRIDE) : p.sentinel;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) s[u] = tab.get(l[u]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) step<GW>(af, ou, s[u].f, s[u].u);
+        }
+    }
+}
 
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    unsigned int pos_acc = 0, trig_acc = 0, rep_acc = 0;
-
-    int64_t tile = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+// The tile loop shared by every k_test variant: the warp tests tiles
+// tile, tile + step, ... < end (one clause per lane).
+template <class LW, class GW, class TAB>
+__device__ __forceinline__ void test_tiles(const TestParams<LW, GW>& p, const TAB& tab, int64_t tile, int64_t end,
+                                           int64_t step_tiles, int lane, WarpAcc& acc) {
     int bi = 0;
     int64_t nt0 = 0;
-    if (tile < p.n_tiles) {  // first bucket by binary search, then walk forward
+    if (tile < end) {  // first bucket by binary search, then walk forward
         int lo = 0, hi = p.nb - 1;
         while (lo < hi) {
             int mid = (lo + hi + 1) >> 1;
@@ -360,17 +435,14 @@ __global__ void __launch_bounds__(THREADS, MINB) k_test(const __grid_constant__ 
         nt0 = bi + 1 < p.nb ? p.buckets[bi + 1].tile0 : INT64_MAX;
     }
     int32_t cur[PF], nxt[PF];
-    if (tile < p.n_tiles) load_rows(p.buckets + bi, tile, lane, p.sentinel, cur);
-    // report slots come from a warp-private chunk [cpos, cend) of the record
-    // buffer, refilled with one atomic every REPORT_CHUNK slots
-    int64_t cpos = 0, cend = 0;
+    if (tile < end) load_rows(p.buckets + bi, tile, lane, p.sentinel, cur);
 
-    for (; tile < p.n_tiles; tile += nwarps) {
+    for (; tile < end; tile += step_tiles) {
         const BucketDesc* bd = p.buckets + bi;
         // software pipeline: the next tile's first rows are in flight while this one is tested
-        if (tile + nwarps < p.n_tiles) {
-            seek_bucket(p.buckets, p.nb, tile + nwarps, bi, nt0);
-            load_rows(p.buckets + bi, tile + nwarps, lane, p.sentinel, nxt);
+        if (tile + step_tiles < end) {
+            seek_bucket(p.buckets, p.nb, tile + step_tiles, bi, nt0);
+            load_rows(p.buckets + bi, tile + step_tiles, lane, p.sentinel, nxt);
         }
         const int size = bd->size;
         const bool active = lane_active(bd, tile, lane);
@@ -378,33 +450,37 @@ __global__ void __launch_bounds__(THREADS, MINB) k_test(const __grid_constant__ 
         // ---- stage 1: aggregate filter (engine.py:238-254) -----------------
         GW af = ~GW(0), ou = GW(0);
         if (active) {
-            {  // literals 0..3 together: nearly every clause needs them
-                Subset<GW> s[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) s[u] = tab.get(cur[u]);
-#pragma unroll
-                for (int u = 0; u < 4; ++u) step<GW>(af, ou, s[u].f, s[u].u);
-            }
-#pragma unroll
-            for (int h = 4; h < PF; h += TSG_TAIL) {  // then batches of TSG_TAIL while any group is live
-                if (h >= size || (af | ou) == GW(0)) break;
-                Subset<GW> s[TSG_TAIL];
-#pragma unroll
-                for (int u = 0; u < TSG_TAIL; ++u) s[u] = tab.get(cur[h + u]);
-#pragma unroll
-                for (int u = 0; u < TSG_TAIL; ++u) step<GW>(af, ou, s[u].f, s[u].u);
-            }
-            if (size > PF && (af | ou) != GW(0)) {
-                const int32_t* lp = lane_lits(bd, tile, lane);
-                for (int j = PF; j < size && (af | ou) != GW(0); j += 4) {
-                    int32_t l[4];
+            if constexpr (TAB::kSlab) {
+                stage1_slab<LW, GW>(p, tab, cur, lane_lits(bd, tile, lane), size, af, ou);
+            } else {
+                {  // literals 0..3 together: nearly every clause needs them
                     Subset<GW> s[4];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) l[u] = (j + u < size) ? __ldg(lp + (j + u) * STRIDE) : p.sentinel;
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) s[u] = tab.get(l[u]);
+                    for (int u = 0; u < 4; ++u) s[u] = tab.get(cur[u]);
 #pragma unroll
                     for (int u = 0; u < 4; ++u) step<GW>(af, ou, s[u].f, s[u].u);
+                }
+#pragma unroll
+                for (int h = 4; h < PF; h += TSG_TAIL) {  // then batches of TSG_TAIL while any group is live
+                    if (h >= size || (af | ou) == GW(0)) break;
+                    Subset<GW> s[TSG_TAIL];
+#pragma unroll
+                    for (int u = 0; u < TSG_TAIL; ++u) s[u] = tab.get(cur[h + u]);
+#pragma unroll
+                    for (int u = 0; u < TSG_TAIL; ++u) step<GW>(af, ou, s[u].f, s[u].u);
+                }
+                if (size > PF && (af | ou) != GW(0)) {
+                    const int32_t* lp = lane_lits(bd, tile, lane);
+                    for (int j = PF; j < size && (af | ou) != GW(0); j += 4) {
+                        int32_t l[4];
+                        Subset<GW> s[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) l[u] = (j + u < size) ? __ldg(lp + (j + u) * STRIDE) : p.sentinel;
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) s[u] = tab.get(l[u]);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) step<GW>(af, ou, s[u].f, s[u].u);
+                    }
                 }
             }
         }
@@ -420,22 +496,22 @@ __global__ void __launch_bounds__(THREADS, MINB) k_test(const __grid_constant__ 
         }
         const int total = __shfl_sync(0xffffffffu, incl, 31);
         if (total) {
-            if (cpos + total > cend) {  // chunk exhausted: pad its tail, take a new one
-                for (int64_t q = cpos + lane; q < cend; q += 32)
+            if (acc.cpos + total > acc.cend) {  // chunk exhausted: pad its tail, take a new one
+                for (int64_t q = acc.cpos + lane; q < acc.cend; q += 32)
                     if (q < p.out_cap) st_report(p.out + q, REPORT_PAD, 0);
                 const unsigned long long want = total > REPORT_CHUNK ? (unsigned long long)total : REPORT_CHUNK;
                 unsigned long long base = 0;
                 if (lane == 31) base = atomicAdd(p.ctr, want);
-                cpos = (int64_t)__shfl_sync(0xffffffffu, base, 31);
-                cend = cpos + (int64_t)want;
+                acc.cpos = (int64_t)__shfl_sync(0xffffffffu, base, 31);
+                acc.cend = acc.cpos + (int64_t)want;
             }
-            int64_t pos = cpos + incl - ub;
-            const int64_t end = pos + ub;
-            cpos += total;
+            int64_t pos = acc.cpos + incl - ub;
+            const int64_t pend = pos + ub;
+            acc.cpos += total;
 
             // ---- stage 2: exact lane test per positive group (bitpack.py:120-135)
             if (word) {
-                pos_acc += ub;
+                acc.pos += ub;
                 const int64_t slot = (tile - bd->tile0) * STRIDE + lane;
                 double act = 0.0;
                 if (!p.emit_only) act = bd->acts[slot];
@@ -460,7 +536,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_test(const __grid_constant__ 
                     const LW mask = (lf | lo2) & p.lane_mask[g];
                     if (!mask) continue;
                     const int hits = __popcll((unsigned long long)mask);
-                    trig_acc += hits;
+                    acc.trig += hits;
                     if (!p.emit_only) {  // engine.py:460, rounded like the reference (no FMA)
                         act = __dadd_rn(act, __dmul_rn(p.inc, (double)hits));
                         touched = true;
@@ -476,31 +552,35 @@ __global__ void __launch_bounds__(THREADS, MINB) k_test(const __grid_constant__ 
                                 st_report(p.out + pos, ((uint64_t)bd->ids[slot] << 16) | (uint32_t)(p.g0 + g),
                                           (uint64_t)mask);
                             ++pos;
-                            ++rep_acc;
+                            ++acc.rep;
                         }
                     }
                 }
                 if (touched) bd->acts[slot] = act;
                 if (p.carry_out_tid >= 0 && last_tid == p.carry_out_tid)
                     p.carry[bd->tile0 * STRIDE + slot] = p.stamp_base | (uint32_t)last_tid;
-                for (; pos < end; ++pos)  // padding for reserved-but-unused slots
+                for (; pos < pend; ++pos)  // padding for reserved-but-unused slots
                     if (pos < p.out_cap) st_report(p.out + pos, REPORT_PAD, 0);
             }
         }
 #pragma unroll
         for (int u = 0; u < PF; ++u) cur[u] = nxt[u];
     }
-    for (int64_t q = cpos + lane; q < cend; q += 32)  // pad the tail of the warp's last chunk
-        if (q < p.out_cap) st_report(p.out + q, REPORT_PAD, 0);
+}
 
-    // counters: warp reduce, then block reduce, one atomic per block
+// pad the warp's last chunk; counters: warp reduce, block reduce, one atomic per block
+template <class LW, class GW, int WARPS>
+__device__ __forceinline__ void finish_block(const TestParams<LW, GW>& p, WarpAcc& acc, int lane, int warp,
+                                             unsigned int (&s_acc)[3][WARPS]) {
+    for (int64_t q = acc.cpos + lane; q < acc.cend; q += 32)
+        if (q < p.out_cap) st_report(p.out + q, REPORT_PAD, 0);
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
-        pos_acc += __shfl_down_sync(0xffffffffu, pos_acc, d);
-        trig_acc += __shfl_down_sync(0xffffffffu, trig_acc, d);
-        rep_acc += __shfl_down_sync(0xffffffffu, rep_acc, d);
+        acc.pos += __shfl_down_sync(0xffffffffu, acc.pos, d);
+        acc.trig += __shfl_down_sync(0xffffffffu, acc.trig, d);
+        acc.rep += __shfl_down_sync(0xffffffffu, acc.rep, d);
     }
-    if (lane == 0) { s_acc[0][warp] = pos_acc; s_acc[1][warp] = trig_acc; s_acc[2][warp] = rep_acc; }
+    if (lane == 0) { s_acc[0][warp] = acc.pos; s_acc[1][warp] = acc.trig; s_acc[2][warp] = acc.rep; }
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long a = 0, bb = 0, r = 0;
@@ -511,6 +591,76 @@ __global__ void __launch_bounds__(THREADS, MINB) k_test(const __grid_constant__ 
             if (bb) atomicAdd(p.ctr + 2, bb);
         }
     }
+}
+
+// Grid-stride variant: persistent warps over all tiles; the aggregate table
+// is gathered from L2 (GlobalTable) or held whole in shared memory (SmemTable).
+template <class LW, class GW, class TAB, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) k_test(const __grid_constant__ TestParams<LW, GW> p) {
+    constexpr int WARPS = THREADS / 32;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ unsigned int s_acc[3][WARPS];
+    TAB tab;
+    if constexpr (TAB::kSmem) {  // per-block copy of the literal-code table
+        const uint4* src = reinterpret_cast<const uint4*>(p.codes);
+        uint4* dst = reinterpret_cast<uint4*>(smem);
+        for (int64_t i = threadIdx.x; i < p.codes_bytes / 16; i += THREADS) dst[i] = __ldg(src + i);
+        __syncthreads();
+        tab.code = reinterpret_cast<decltype(tab.code)>(smem);
+    } else {
+        tab.agg = p.agg;
+    }
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    WarpAcc acc;
+    test_tiles<LW, GW, TAB>(p, tab, ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, p.n_tiles, nwarps, lane,
+                            acc);
+    finish_block<LW, GW, WARPS>(p, acc, lane, warp, s_acc);
+}
+
+// Slab variant: one CTA per SM owns a contiguous range of
+// tiles; tiles are ordered slab-major, so the CTA walks at most a few slabs.
+// For each it stages the slab's aggregate words in shared memory (F-capable
+// word per literal code, U word per variable) and tests the slab's tiles
+// with stage1_slab.
+template <class LW, class GW, int THREADS>
+__global__ void __launch_bounds__(THREADS, 1) k_test_slab(const __grid_constant__ TestParams<LW, GW> p) {
+    constexpr int WARPS = THREADS / 32;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ unsigned int s_acc[3][WARPS];
+    SlabTable<GW> tab;
+    tab.fc = reinterpret_cast<GW*>(smem);
+    tab.u = tab.fc + 2 * (int64_t)p.slab_w;
+    tab.agg = p.agg;
+    tab.w = p.slab_w;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    WarpAcc acc;
+    const int64_t t_end = p.n_tiles * (int64_t)(blockIdx.x + 1) / gridDim.x;
+    int64_t t = p.n_tiles * (int64_t)blockIdx.x / gridDim.x;
+    int s = 0;
+    while (t < t_end) {
+        while (p.slab_tile0[s + 1] <= t) ++s;
+        const int64_t seg_end = t_end < p.slab_tile0[s + 1] ? t_end : p.slab_tile0[s + 1];
+        const int64_t lo = (int64_t)s * p.slab_w;
+        __syncthreads();  // every warp is done with the previous slab
+        GW* fc = const_cast<GW*>(tab.fc);
+        GW* us = const_cast<GW*>(tab.u);
+        for (int i = threadIdx.x; i < p.slab_w; i += THREADS) {
+            const int64_t v = lo + i;
+            AggEntry<GW> e{~GW(0), ~GW(0), GW(0), GW(0)};
+            if (v <= p.sentinel) e = ld_agg(p.agg + v);
+            fc[2 * i] = e.f;      // +v is False where v can be False
+            fc[2 * i + 1] = e.t;  // -v is False where v can be True
+            us[i] = e.u;
+        }
+        __syncthreads();
+        tab.lo = (int32_t)lo;
+        test_tiles<LW, GW, SlabTable<GW>>(p, tab, t + warp, seg_end, WARPS, lane, acc);
+        t = seg_end;
+    }
+    finish_block<LW, GW, WARPS>(p, acc, lane, warp, s_acc);
 }
 
 }  // namespace tsg

@@ -34,15 +34,21 @@ __global__ void k_scale_f64(double* p, int64_t n, double f) {
     for (; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = __dmul_rn(p[i], f);
 }
 
-// interleaved -> clause-major (lits_at / literal_columns, engine.py:165-182)
-__global__ void k_deinterleave(const int32_t* __restrict__ src, int64_t n, int32_t size,
-                               int32_t* __restrict__ dst) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int64_t total = n * size;
-    for (; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t c = i / size;
-        int32_t j = (int32_t)(i - c * size);
-        dst[i] = src[(c / STRIDE) * size * STRIDE + (int64_t)j * STRIDE + (c % STRIDE)];
+// interleaved -> clause-major in the clause's original literal order
+// (lits_at / literal_columns, engine.py:165-182).  A stored clause holds its
+// hot prefix first; hmask bit j marks original position j (< 64) as hot.
+__global__ void k_deinterleave(const int32_t* __restrict__ src, const uint64_t* __restrict__ hmask, int64_t n,
+                               int32_t size, int32_t* __restrict__ dst) {
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t* s = src + (c / STRIDE) * size * STRIDE + (c % STRIDE);
+        const uint64_t m = hmask[c];
+        int32_t hot = 0, cold = __popcll(m);
+        for (int32_t j = 0; j < size; ++j) {
+            const bool is_hot = j < 64 && ((m >> j) & 1);
+            const int32_t k = is_hot ? hot++ : cold++;
+            dst[c * size + j] = s[(int64_t)k * STRIDE];
+        }
     }
 }
 
@@ -107,14 +113,17 @@ __global__ void k_mark_deleted(const int64_t* __restrict__ ids, int64_t n, int64
 __global__ void k_compact(const int64_t* __restrict__ src_slot, int64_t kept, int32_t size,
                           const int32_t* __restrict__ lits_in, const double* __restrict__ acts_in,
                           const int64_t* __restrict__ ids_in, const int32_t* __restrict__ org_in,
+                          const uint64_t* __restrict__ hm_in,
                           int32_t* __restrict__ lits_out, double* __restrict__ acts_out,
-                          int64_t* __restrict__ ids_out, int32_t* __restrict__ org_out) {
+                          int64_t* __restrict__ ids_out, int32_t* __restrict__ org_out,
+                          uint64_t* __restrict__ hm_out) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     for (; k < kept; k += (int64_t)gridDim.x * blockDim.x) {
         int64_t o = src_slot[k];
         acts_out[k] = acts_in[o];
         ids_out[k] = ids_in[o];
         org_out[k] = org_in[o];
+        hm_out[k] = hm_in[o];
         const int32_t* s = lits_in + (o / STRIDE) * size * STRIDE + (o % STRIDE);
         int32_t* d = lits_out + (k / STRIDE) * size * STRIDE + (k % STRIDE);
         for (int j = 0; j < size; ++j) d[(int64_t)j * STRIDE] = s[(int64_t)j * STRIDE];

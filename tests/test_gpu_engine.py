@@ -131,6 +131,22 @@ def test_literal_out_of_range_raises(P):
 
 # ---- config-scale parity vs the CPU oracle ---------------------------------
 
+# stage-1 table variants, selected per engine at tsg_create:
+#   smem       whole literal-code table in shared memory (small num_vars x groups)
+#   l2         aggregate table gathered from L2, unpartitioned store
+#   slab       store partitioned into 4 variable slabs, hot prefix from shared memory
+#   smem_slab  partitioned store (hot-prefix literal order) tested by the smem kernel
+TABLES = {"smem": {"TSG_SMEM_TABLE": "1", "TSG_SLABS": "0"},
+          "l2": {"TSG_SMEM_TABLE": "0", "TSG_SLABS": "0"},
+          "slab": {"TSG_SMEM_TABLE": "0", "TSG_SLABS": "4"},
+          "smem_slab": {"TSG_SMEM_TABLE": "1", "TSG_SLABS": "4"}}
+
+
+def use_table(monkeypatch, table):
+    for k, v in TABLES[table].items():
+        monkeypatch.setenv(k, v)
+
+
 def run_both(P, cfg_name=None, n=None, threads=None, lanes=None, nv=None, lane_width=32, group_width=32,
              seed=0, inc=1.0, rounds=1, size_lo=2, size_hi=30):
     from paper_2012_03119_b200 import workload as W
@@ -174,34 +190,52 @@ def run_both(P, cfg_name=None, n=None, threads=None, lanes=None, nv=None, lane_w
     return res
 
 
-def test_c1_parity_vs_oracle(P):
+@pytest.mark.parametrize("table", ["smem", "slab"])
+def test_c1_parity_vs_oracle(P, monkeypatch, table):
+    use_table(monkeypatch, table)
     res = run_both(P, "C1", rounds=2)
     assert res.reports > 0 and res.lane_triggers > 0
 
 
-@pytest.mark.parametrize("table", ["smem", "l2"])
+@pytest.mark.parametrize("table", ["smem", "l2", "slab", "smem_slab"])
 @pytest.mark.parametrize("lw,gw,threads,lanes", [(32, 32, 3, 40), (64, 64, 2, 64), (64, 8, 5, 70),
                                                  (7, 3, 4, 20), (1, 64, 3, 30), (32, 16, 40, 32)])
 def test_widths_and_multichunk_parity(P, monkeypatch, table, lw, gw, threads, lanes):
-    # small num_vars: the shared-memory code table applies (G <= 32); "l2"
-    # forces the L2-gather table path on the same inputs
-    monkeypatch.setenv("TSG_SMEM_TABLE", "1" if table == "smem" else "0")
+    # small num_vars: every table variant applies to the same inputs
+    use_table(monkeypatch, table)
     run_both(P, n=20_000, threads=threads, lanes=lanes, nv=300, lane_width=lw, group_width=gw,
              seed=lw * 100 + gw, rounds=2, size_lo=0, size_hi=12)
 
 
-@pytest.mark.parametrize("table", ["smem", "l2"])
+@pytest.mark.parametrize("table", ["smem", "l2", "slab"])
 def test_c2_shape_parity(P, monkeypatch, table):
-    # C2's 50k vars x 8 groups is the largest code table that fits shared memory
-    monkeypatch.setenv("TSG_SMEM_TABLE", "1" if table == "smem" else "0")
+    # C2's 50k vars x 8 groups is the largest code table that fits shared memory;
+    # with it disabled the store's 3 natural slabs drive the slab kernel
+    use_table(monkeypatch, table)
+    if table == "slab":
+        monkeypatch.delenv("TSG_SLABS")
     run_both(P, n=60_000, threads=8, lanes=32, nv=50_000, seed=22)
 
 
-def test_long_clauses_parity(P):
+@pytest.mark.parametrize("table", ["l2", "slab"])
+def test_c3_shape_parity(P, monkeypatch, table):
+    # C3's 200k vars x 32 groups: 11 natural slabs (the benchmark's kernel)
+    use_table(monkeypatch, table)
+    if table == "slab":
+        monkeypatch.delenv("TSG_SLABS")
+    run_both(P, n=150_000, threads=32, lanes=32, nv=200_000, seed=23)
+
+
+@pytest.mark.parametrize("table", ["smem", "slab"])
+def test_long_clauses_parity(P, monkeypatch, table):
+    # hot prefixes longer than the prefetched rows, hot literals past position 64
+    use_table(monkeypatch, table)
     run_both(P, n=3000, threads=4, lanes=32, nv=2000, seed=9, size_lo=100, size_hi=400)
 
 
-def test_reduce_and_remove_parity(P):
+@pytest.mark.parametrize("table", ["smem", "slab"])
+def test_reduce_and_remove_parity(P, monkeypatch, table):
+    use_table(monkeypatch, table)
     from paper_2012_03119_b200 import workload as W
     from paper_2012_03119_b200.native import NativeEngine
     rng = np.random.default_rng(3)
@@ -244,7 +278,11 @@ def test_reduce_and_remove_parity(P):
     assert res.reports == len(recs) and res.lane_triggers == ctr["lane_triggers"]
 
 
-def test_report_buffer_overflow_replay(P):
+@pytest.mark.parametrize("table", ["smem", "slab"])
+def test_report_buffer_overflow_replay(P, monkeypatch, table):
+    use_table(monkeypatch, table)
+    if table == "slab":
+        monkeypatch.setenv("TSG_SLABS", "2")
     from paper_2012_03119_b200 import workload as W
     from paper_2012_03119_b200.native import NativeEngine
     rng = np.random.default_rng(11)
