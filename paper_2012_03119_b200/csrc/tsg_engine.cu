@@ -137,8 +137,10 @@ struct tsg_engine {
     bool slab_test = true;               // slab kernel when n_slabs > 1 (TSG_SLABS=0 disables)
     std::vector<int64_t> slab_load;      // clauses per slab (placement tie-break)
     std::vector<int64_t> h_slab_tile0;   // first tile of each slab (+ end)
-    int64_t* d_slab_tile0 = nullptr;
+    std::vector<int32_t> h_slab_desc0;   // first descriptor of each slab (+ end)
+    int64_t* d_slab_tile0 = nullptr;     // [n_slabs + 1] tile0, then [n_slabs + 1] desc0 (int32), then schedule
     int64_t slab_tile0_cap = 0;
+    std::vector<uint64_t> h_sched;
 };
 
 namespace {
@@ -294,8 +296,8 @@ int launch_slab(tsg_engine* h, const TestParams<LW, GW>& p) {
         h->grid[key] = (int64_t)per_sm * h->nsm;
         h->grid_smem[key] = (int64_t)smem;
     }
-    const int64_t per_cta = 64;  // keep >= 64 tiles per CTA so each slab load is amortised
-    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->grid[key], (h->n_tiles + per_cta - 1) / per_cta));
+    if (h->h_sched.empty()) return TSG_OK;
+    int grid = (int)std::min<int64_t>(h->grid[key], (int64_t)h->h_sched.size());
     fn<<<grid, TEST_THREADS_SLAB, smem, h->st>>>(p);
     CK(cudaGetLastError());
     return TSG_OK;
@@ -326,6 +328,9 @@ int launch_test(tsg_engine* h, int c, double inc, int emit_only) {
     p.carry_out_tid = (g0 + G < h->n_groups && h->gtid[g0 + G - 1] == h->gtid[g0 + G]) ? h->gtid[g0 + G - 1] : -1;
     p.emit_only = emit_only;
     p.slab_tile0 = h->d_slab_tile0;
+    p.slab_desc0 = reinterpret_cast<const int32_t*>(h->d_slab_tile0 + (h->n_slabs + 1));
+    p.sched = reinterpret_cast<const uint64_t*>(h->d_slab_tile0 + 2 * (h->n_slabs + 1));
+    p.n_sched = (int32_t)h->h_sched.size();
     p.slab_w = h->slab_w;
     for (int g = 0; g < G; ++g) {
         p.tid[g] = h->gtid[g0 + g];
@@ -380,9 +385,11 @@ int64_t store_size(const tsg_engine* h) {
 int build_desc(tsg_engine* h) {
     h->h_desc.clear();
     h->h_slab_tile0.assign(h->n_slabs + 1, 0);
+    h->h_slab_desc0.assign(h->n_slabs + 1, 0);
     int64_t tiles = 0;
     for (int32_t s = 0; s < h->n_slabs; ++s) {
         h->h_slab_tile0[s] = tiles;
+        h->h_slab_desc0[s] = (int32_t)h->h_desc.size();
         for (auto& b : h->buckets) {
             const Part& p = b.parts[s];
             if (!p.count) continue;
@@ -394,14 +401,51 @@ int build_desc(tsg_engine* h) {
         }
     }
     h->h_slab_tile0[h->n_slabs] = tiles;
+    h->h_slab_desc0[h->n_slabs] = (int32_t)h->h_desc.size();
     h->n_tiles = tiles;
     CKR(dgrow(h, &h->d_desc, &h->desc_cap, std::max<int64_t>(1, (int64_t)h->h_desc.size())));
     if (!h->h_desc.empty())
         CK(cudaMemcpyAsync(h->d_desc, h->h_desc.data(), h->h_desc.size() * sizeof(BucketDesc),
                            cudaMemcpyHostToDevice, h->st));
-    CKR(dgrow(h, &h->d_slab_tile0, &h->slab_tile0_cap, (int64_t)h->h_slab_tile0.size()));
+    // slab schedule for a grid of one CTA per SM: each slab gets CTAs in
+    // proportion to its tiles (largest remainder, at least one if it has any)
+    h->h_sched.clear();
+    {
+        const int64_t grid = h->nsm;
+        std::vector<int64_t> n(h->n_slabs, 0);
+        std::vector<std::pair<double, int>> rem;
+        int64_t used = 0, nonempty = 0;
+        for (int32_t s = 0; s < h->n_slabs; ++s) {
+            const int64_t t = h->h_slab_tile0[s + 1] - h->h_slab_tile0[s];
+            if (!t) continue;
+            ++nonempty;
+            const double share = tiles ? (double)grid * t / tiles : 0.0;
+            n[s] = std::max<int64_t>(1, (int64_t)share);
+            n[s] = std::min<int64_t>(n[s], std::max<int64_t>(1, (t + 7) / 8));  // >= 8 tiles per CTA
+            used += n[s];
+            rem.push_back({share - (double)n[s], s});
+        }
+        std::sort(rem.begin(), rem.end(), [](auto& x, auto& y) { return x.first > y.first || (x.first == y.first && x.second < y.second); });
+        for (auto& r : rem) {
+            if (used >= grid) break;
+            const int64_t t = h->h_slab_tile0[r.second + 1] - h->h_slab_tile0[r.second];
+            if (r.first > 0 && n[r.second] < std::max<int64_t>(1, (t + 7) / 8)) { n[r.second]++; used++; }
+        }
+        (void)nonempty;
+        for (int32_t s = 0; s < h->n_slabs; ++s)
+            for (int64_t k = 0; k < n[s]; ++k)
+                h->h_sched.push_back((uint64_t)s << 32 | (uint64_t)k << 16 | (uint64_t)n[s]);
+    }
+    const int64_t words = 2 * (int64_t)(h->n_slabs + 1) + (int64_t)h->h_sched.size() + 1;
+    CKR(dgrow(h, &h->d_slab_tile0, &h->slab_tile0_cap, words));
     CK(cudaMemcpyAsync(h->d_slab_tile0, h->h_slab_tile0.data(), h->h_slab_tile0.size() * 8,
                        cudaMemcpyHostToDevice, h->st));
+    CK(cudaMemcpyAsync(h->d_slab_tile0 + (h->n_slabs + 1), h->h_slab_desc0.data(), h->h_slab_desc0.size() * 4,
+                       cudaMemcpyHostToDevice, h->st));
+    if (!h->h_sched.empty())
+        CK(cudaMemcpyAsync(h->d_slab_tile0 + 2 * (h->n_slabs + 1), h->h_sched.data(), h->h_sched.size() * 8,
+                           cudaMemcpyHostToDevice, h->st));
+    CK(cudaStreamSynchronize(h->st));  // host vectors are rebuilt next round
     return TSG_OK;
 }
 
@@ -557,16 +601,22 @@ int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
     h->cfg = *cfg;
     h->V = num_vars;
     if (const char* e = getenv("TSG_SMEM_TABLE")) h->smem_table = atoi(e) != 0;
-    // variable slabs sized so one slab's aggregate words fit a CTA's shared memory
+    // Variable slabs, opt-in: TSG_SLABS=1 partitions the store
+    // into as many slabs as one CTA's shared memory needs for the aggregate
+    // words, TSG_SLABS=n>1 into at least n.  Default: one slab (unpartitioned
+    // store, global-table kernel), the faster layout measured on B200.
     {
         const int64_t per_var = 3 * (h->cfg.group_width > 32 ? 8 : 4);
         const int64_t nv2 = (int64_t)num_vars + 2;
-        const int64_t max_w = std::max<int64_t>(32, (SLAB_SMEM_BYTES / per_var) / 32 * 32);
-        int64_t ns = (nv2 + max_w - 1) / max_w;
+        int64_t slab_bytes = SLAB_SMEM_BYTES;
+        if (const char* e = getenv("TSG_SLAB_BYTES")) slab_bytes = std::min<int64_t>(SLAB_SMEM_BYTES, atol(e));
+        const int64_t max_w = std::max<int64_t>(32, (slab_bytes / per_var) / 32 * 32);
+        int64_t ns = 1;
         if (const char* e = getenv("TSG_SLABS")) {
-            if (atoi(e) == 0) h->slab_test = false;
-            else if (atoi(e) > 0) ns = std::max<int64_t>(ns, atoi(e));  // force more slabs (tests)
+            const int req = atoi(e);
+            if (req >= 1) ns = std::max<int64_t>((nv2 + max_w - 1) / max_w, req);
         }
+        if (ns <= 1) h->slab_test = false;
         int64_t w = round_up((nv2 + ns - 1) / ns, 32);
         h->n_slabs = (int32_t)((nv2 + w - 1) / w);
         h->slab_w = (int32_t)w;
@@ -972,18 +1022,21 @@ int tsg_round_test(tsg_engine* h, double activity_inc, tsg_round_result* out) {
         int64_t positives = (int64_t)h->h_ctr[1];
         res.lane_triggers = (int64_t)h->h_ctr[2];
         int64_t n_rec = (int64_t)h->h_ctr[3];
-        if (n_slots > h->out_cap) {  // overflow: grow, replay emission only (no side effects)
+        // overflow: grow, replay emission only (no activity / counter side
+        // effects).  Slot reservation depends on which warp tests which tile
+        // (dynamic in the slab kernel), so a replay may need a different count.
+        while (n_slots > h->out_cap) {
             dfree(h, h->out);
             h->out = nullptr;
-            h->out_cap = n_slots + n_slots / 4 + 1024;
+            h->out_cap = n_slots + n_slots / 4 + 1024 + (int64_t)h->nsm * 64 * (int64_t)REPORT_CHUNK;
             CKR(dalloc(h, (void**)&h->out, h->out_cap * (int64_t)sizeof(tsg_report)));
             CK(cudaMemsetAsync(h->ctr, 0, 4 * sizeof(unsigned long long), h->st));
             CKR(run_tests(h, activity_inc, 1));
             CK(cudaMemcpyAsync(h->h_ctr, h->ctr, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
             CK(cudaStreamSynchronize(h->st));
-            if ((int64_t)h->h_ctr[3] != n_rec || (int64_t)h->h_ctr[0] != n_slots)
-                return fail(TSG_ECUDA, "report replay mismatch");
-            res.reruns = 1;
+            if ((int64_t)h->h_ctr[3] != n_rec) return fail(TSG_ECUDA, "report replay mismatch");
+            n_slots = (int64_t)h->h_ctr[0];
+            res.reruns++;
         }
         h->n_out = n_rec;
         h->n_alloc = n_slots;

@@ -210,20 +210,27 @@ struct TestParams {
     int32_t carry_out_tid;     // last tid of the chunk if it continues into the next chunk, else -1
     int32_t emit_only;         // replay after report-buffer overflow: no activity / counter side effects
     const int64_t* slab_tile0; // slab kernel: first tile of each slab (+ end)
+    const int32_t* slab_desc0; // slab kernel: first descriptor of each slab (+ end)
+    const uint64_t* sched;     // slab kernel: per CTA slab << 32 | rank << 16 | CTAs on the slab
+    int32_t n_sched;
     int32_t slab_w;            // slab kernel: variables per slab
     int32_t tid[MAXG];
     LW lane_mask[MAXG];
 };
 
 constexpr int PF = 8;  // literal rows prefetched per tile
-constexpr int TEST_THREADS = 256;       // block of the L2-table variant
+#ifndef TSG_TEST_THREADS
+#define TSG_TEST_THREADS 256
+#endif
+constexpr int TEST_THREADS = TSG_TEST_THREADS;  // block of the L2-table variant
 constexpr int TEST_THREADS_SMEM = 768;  // block of the shared-memory-table variant (one per SM)
 constexpr int64_t SMEM_TABLE_MAX = 200 * 1024;
 #ifndef TSG_SLAB_THREADS
-#define TSG_SLAB_THREADS 1024
+#define TSG_SLAB_THREADS 768
 #endif
 constexpr int TEST_THREADS_SLAB = TSG_SLAB_THREADS;  // block of the slab variant (one per SM)
-constexpr int64_t SLAB_SMEM_BYTES = 224 * 1024;     // one slab's words (227 KB per CTA minus statics)
+constexpr int64_t SLAB_SMEM_BYTES = 132 * 1024;     // one slab's words: keeps the CTA under the 164 KB carveout,
+                                                    // leaving ~92 KB of L1 for in-flight gathers (measured cliff below ~60 KB)
 
 constexpr uint64_t REPORT_PAD = ~0ull;
 #ifndef REPORT_CHUNK  // report slots a warp reserves per atomic
@@ -346,18 +353,45 @@ constexpr size_t test_smem_bytes(int64_t codes_bytes) {
     return TAB::kSmem ? (size_t)codes_bytes : 16;
 }
 
-// one batch of stage-2 literals (lane words of group g for literals cur[h..h+3])
-template <class LW>
-__device__ __forceinline__ void lane_batch(const LaneEntry<LW>* lt, const int32_t* cur, int h, int size, LW& lf,
+// The current tile's first PF literal rows of this lane's clause.
+// RegRows keeps them in registers (indexed with compile-time positions);
+// SmemRows keeps them in a per-warp shared-memory buffer [PF][32] so the slab
+// kernel can index them with lane-dependent positions (one LDS, no select
+// chains, no local memory).
+struct RegRows {
+    int32_t r[PF];
+    __device__ __forceinline__ int32_t get(int j) const { return r[j]; }
+    __device__ __forceinline__ void take(const int32_t (&nxt)[PF]) {
+#pragma unroll
+        for (int u = 0; u < PF; ++u) r[u] = nxt[u];
+    }
+};
+struct SmemRows {
+    int32_t* buf;  // this warp's [PF][32] buffer, offset by lane
+    __device__ __forceinline__ int32_t get(int j) const { return buf[j * 32]; }
+    __device__ __forceinline__ void take(const int32_t (&nxt)[PF]) {
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < PF; ++u) buf[u * 32] = nxt[u];
+        __syncwarp();
+    }
+};
+
+// one batch of stage-2 literals (lane words of group g for literals h..h+3)
+template <class LW, class ROWS>
+__device__ __forceinline__ void lane_batch(const LaneEntry<LW>* lt, const ROWS& rows, int h, int size, LW& lf,
                                            LW& lo) {
     LaneEntry<LW> e[4];
+    int32_t l[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) l[u] = rows.get(h + u);
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-        if (h + u < size) e[u] = ld_lane(lt + lit_var(cur[h + u]));
+        if (h + u < size) e[u] = ld_lane(lt + lit_var(l[u]));
 #pragma unroll
     for (int u = 0; u < 4; ++u)
         if (h + u < size)
-            step<LW>(lf, lo, cur[h + u] < 0 ? (e[u].s & e[u].t) : (e[u].s & ~e[u].t), ~e[u].s);
+            step<LW>(lf, lo, l[u] < 0 ? (e[u].s & e[u].t) : (e[u].s & ~e[u].t), ~e[u].s);
 }
 
 // Per-warp running state of the tile loop: the warp's report-slot chunk
@@ -367,82 +401,93 @@ struct WarpAcc {
     unsigned int pos = 0, trig = 0, rep = 0;
 };
 
+#ifndef TSG_COLD0  // literals in the first cold gather batch of the slab kernel
+#define TSG_COLD0 3
+#endif
+
 // Stage 1 of the slab kernel for one clause: the hot prefix (literals whose
 // variable lies in the CTA's slab, stored first) is looked up in shared
-// memory; the cold rest is gathered from the L2-resident table two literals
-// at a time while any group is live.
+// memory; the cold rest is gathered from the L2-resident table in batches
+// aligned to each lane's own first cold position (TSG_COLD0 literals, then
+// 2 at a time) while any group is live, so a warp needs only as many L2
+// round trips as its lanes' longest chain.
 template <class LW, class GW>
 __device__ __forceinline__ void stage1_slab(const TestParams<LW, GW>& p, const SlabTable<GW>& tab,
-                                            const int32_t (&cur)[PF], const int32_t* lp, int size, GW& af, GW& ou) {
+                                            const SmemRows& rows, const int32_t* lp, int size, GW& af, GW& ou) {
+    auto lit_at = [&](int i) -> int32_t {
+        if (i >= size) return p.sentinel;
+        return i < PF ? rows.get(i) : __ldg(lp + i * STRIDE);
+    };
     int hp = 0;  // hot prefix length
-#pragma unroll
-    for (int u = 0; u < PF; ++u) {
-        if (hp == u && u < size && tab.hot(cur[u])) {
-            GW f, uu;
-            tab.get_hot(cur[u], f, uu);
-            step<GW>(af, ou, f, uu);
-            hp = u + 1;
-        }
+    while (hp < size) {
+        const int32_t l = lit_at(hp);
+        if (!tab.hot(l)) break;
+        GW f, uu;
+        tab.get_hot(l, f, uu);
+        step<GW>(af, ou, f, uu);
+        ++hp;
     }
-    if (hp == PF && size > PF) {  // long hot prefix (long clauses)
-        for (; hp < size; ++hp) {
-            const int32_t l = __ldg(lp + hp * STRIDE);
-            if (!tab.hot(l)) break;
-            GW f, uu;
-            tab.get_hot(l, f, uu);
-            step<GW>(af, ou, f, uu);
-        }
-    }
+    int j = hp;  // next cold position of this lane
+    if (j < size && (af | ou) != GW(0)) {
+        int32_t l[TSG_COLD0];
 #pragma unroll
-    for (int b0 = 0; b0 < PF; b0 += 2) {  // cold literals held in registers
-        if (b0 >= size || (af | ou) == GW(0)) break;
-        if (b0 + 2 <= hp) continue;
-        const bool n0 = b0 >= hp, n1 = b0 + 1 >= hp && b0 + 1 < size;
-        Subset<GW> s0{GW(0), ~GW(0), GW(0)}, s1{GW(0), ~GW(0), GW(0)};
-        if (n0) s0 = tab.get(cur[b0]);
-        if (n1) s1 = tab.get(cur[b0 + 1]);
-        step<GW>(af, ou, s0.f, s0.u);
-        step<GW>(af, ou, s1.f, s1.u);
-    }
-    if (size > PF && (af | ou) != GW(0)) {  // cold literals beyond the prefetched rows
-        for (int j = hp > PF ? hp : PF; j < size && (af | ou) != GW(0); j += 4) {
-            int32_t l[4];
-            Subset<GW> s[4];
+        for (int k = 0; k < TSG_COLD0; ++k) l[k] = lit_at(j + k);
+        Subset<GW> sb[TSG_COLD0];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) l[u] = (j + u < size) ? __ldg(lp + (j + u) * STRIDE) : p.sentinel;
+        for (int k = 0; k < TSG_COLD0; ++k) sb[k] = tab.get(l[k]);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) s[u] = tab.get(l[u]);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) step<GW>(af, ou, s[u].f, s[u].u);
+        for (int k = 0; k < TSG_COLD0; ++k) step<GW>(af, ou, sb[k].f, sb[k].u);
+        j += TSG_COLD0;
+        while (j < size && (af | ou) != GW(0)) {
+            const int32_t l0 = lit_at(j), l1 = lit_at(j + 1);
+            const Subset<GW> s0 = tab.get(l0), s1 = tab.get(l1);
+            step<GW>(af, ou, s0.f, s0.u);
+            step<GW>(af, ou, s1.f, s1.u);
+            j += 2;
         }
     }
 }
 
-// The tile loop shared by every k_test variant: the warp tests tiles
-// tile, tile + step, ... < end (one clause per lane).
-template <class LW, class GW, class TAB>
-__device__ __forceinline__ void test_tiles(const TestParams<LW, GW>& p, const TAB& tab, int64_t tile, int64_t end,
-                                           int64_t step_tiles, int lane, WarpAcc& acc) {
+// Tile sources (warp-uniform, strictly increasing per warp; -1 = done).
+struct StrideTiles {  // tiles t, t + step, ... < end
+    int64_t t, step, end;
+    bool started = false;
+    __device__ __forceinline__ int64_t next(int) {
+        if (started) t += step;
+        started = true;
+        return t < end ? t : -1;
+    }
+};
+// The tile loop shared by every k_test variant (one clause per lane).
+// `descs[0, nb)` covers every tile the source hands out (global memory, or
+// the slab's share staged in shared memory).
+template <class LW, class GW, class TAB, class SRC, class ROWS>
+__device__ __forceinline__ void test_tiles(const TestParams<LW, GW>& p, const TAB& tab, const BucketDesc* descs,
+                                           int nb, SRC& src, ROWS& cur, int lane, WarpAcc& acc) {
+    int64_t tile = src.next(lane);
+    if (tile < 0) return;
     int bi = 0;
     int64_t nt0 = 0;
-    if (tile < end) {  // first bucket by binary search, then walk forward
-        int lo = 0, hi = p.nb - 1;
+    {  // first bucket by binary search, then walk forward
+        int lo = 0, hi = nb - 1;
         while (lo < hi) {
             int mid = (lo + hi + 1) >> 1;
-            if (p.buckets[mid].tile0 <= tile) lo = mid; else hi = mid - 1;
+            if (descs[mid].tile0 <= tile) lo = mid; else hi = mid - 1;
         }
         bi = lo;
-        nt0 = bi + 1 < p.nb ? p.buckets[bi + 1].tile0 : INT64_MAX;
+        nt0 = bi + 1 < nb ? descs[bi + 1].tile0 : INT64_MAX;
     }
-    int32_t cur[PF], nxt[PF];
-    if (tile < end) load_rows(p.buckets + bi, tile, lane, p.sentinel, cur);
+    int32_t nxt[PF];
+    load_rows(descs + bi, tile, lane, p.sentinel, nxt);
+    cur.take(nxt);
 
-    for (; tile < end; tile += step_tiles) {
-        const BucketDesc* bd = p.buckets + bi;
+    while (tile >= 0) {
+        const BucketDesc* bd = descs + bi;
         // software pipeline: the next tile's first rows are in flight while this one is tested
-        if (tile + step_tiles < end) {
-            seek_bucket(p.buckets, p.nb, tile + step_tiles, bi, nt0);
-            load_rows(p.buckets + bi, tile + step_tiles, lane, p.sentinel, nxt);
+        const int64_t ntile = src.next(lane);
+        if (ntile >= 0) {
+            seek_bucket(descs, nb, ntile, bi, nt0);
+            load_rows(descs + bi, ntile, lane, p.sentinel, nxt);
         }
         const int size = bd->size;
         const bool active = lane_active(bd, tile, lane);
@@ -456,7 +501,7 @@ __device__ __forceinline__ void test_tiles(const TestParams<LW, GW>& p, const TA
                 {  // literals 0..3 together: nearly every clause needs them
                     Subset<GW> s[4];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) s[u] = tab.get(cur[u]);
+                    for (int u = 0; u < 4; ++u) s[u] = tab.get(cur.get(u));
 #pragma unroll
                     for (int u = 0; u < 4; ++u) step<GW>(af, ou, s[u].f, s[u].u);
                 }
@@ -465,7 +510,7 @@ __device__ __forceinline__ void test_tiles(const TestParams<LW, GW>& p, const TA
                     if (h >= size || (af | ou) == GW(0)) break;
                     Subset<GW> s[TSG_TAIL];
 #pragma unroll
-                    for (int u = 0; u < TSG_TAIL; ++u) s[u] = tab.get(cur[h + u]);
+                    for (int u = 0; u < TSG_TAIL; ++u) s[u] = tab.get(cur.get(h + u));
 #pragma unroll
                     for (int u = 0; u < TSG_TAIL; ++u) step<GW>(af, ou, s[u].f, s[u].u);
                 }
@@ -563,8 +608,8 @@ __device__ __forceinline__ void test_tiles(const TestParams<LW, GW>& p, const TA
                     if (pos < p.out_cap) st_report(p.out + pos, REPORT_PAD, 0);
             }
         }
-#pragma unroll
-        for (int u = 0; u < PF; ++u) cur[u] = nxt[u];
+        if (ntile >= 0) cur.take(nxt);
+        tile = ntile;
     }
 }
 
@@ -614,21 +659,30 @@ __global__ void __launch_bounds__(THREADS, MINB) k_test(const __grid_constant__ 
     const int warp = threadIdx.x >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     WarpAcc acc;
-    test_tiles<LW, GW, TAB>(p, tab, ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, p.n_tiles, nwarps, lane,
-                            acc);
+    StrideTiles src{((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps, p.n_tiles};
+    RegRows rows;
+    test_tiles<LW, GW, TAB>(p, tab, p.buckets, p.nb, src, rows, lane, acc);
     finish_block<LW, GW, WARPS>(p, acc, lane, warp, s_acc);
 }
 
-// Slab variant: one CTA per SM owns a contiguous range of
-// tiles; tiles are ordered slab-major, so the CTA walks at most a few slabs.
-// For each it stages the slab's aggregate words in shared memory (F-capable
-// word per literal code, U word per variable) and tests the slab's tiles
-// with stage1_slab.
+// Slab variant: one CTA per SM.  The host schedule gives
+// every CTA one slab and its rank among the n CTAs sharing that slab (n
+// proportional to the slab's tiles).  The CTA stages the slab's aggregate
+// words in shared memory (can-be-False word per literal code, can-be-Undef
+// word per variable) plus the slab's tile descriptors, then its warps walk
+// the slab's tiles interleaved with the other CTAs of the slab
+// (tile = first + rank * WARPS + warp + k * n * WARPS), which mixes short-
+// and long-clause tiles evenly over the CTAs.  sched[c] = slab << 32 |
+// rank << 16 | n; a CTA index beyond the schedule picks up entries c + grid...
+constexpr int SLAB_DESC_MAX = 80;  // descriptors staged in shared memory (else read from global)
+
 template <class LW, class GW, int THREADS>
 __global__ void __launch_bounds__(THREADS, 1) k_test_slab(const __grid_constant__ TestParams<LW, GW> p) {
     constexpr int WARPS = THREADS / 32;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ unsigned int s_acc[3][WARPS];
+    __shared__ BucketDesc s_desc[SLAB_DESC_MAX];
+    __shared__ int32_t s_rows[WARPS][PF][32];
     SlabTable<GW> tab;
     tab.fc = reinterpret_cast<GW*>(smem);
     tab.u = tab.fc + 2 * (int64_t)p.slab_w;
@@ -637,28 +691,30 @@ __global__ void __launch_bounds__(THREADS, 1) k_test_slab(const __grid_constant_
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     WarpAcc acc;
-    const int64_t t_end = p.n_tiles * (int64_t)(blockIdx.x + 1) / gridDim.x;
-    int64_t t = p.n_tiles * (int64_t)blockIdx.x / gridDim.x;
-    int s = 0;
-    while (t < t_end) {
-        while (p.slab_tile0[s + 1] <= t) ++s;
-        const int64_t seg_end = t_end < p.slab_tile0[s + 1] ? t_end : p.slab_tile0[s + 1];
+    for (int c = blockIdx.x; c < p.n_sched; c += gridDim.x) {
+        const uint64_t e = p.sched[c];
+        const int s = (int)(e >> 32), rank = (int)((e >> 16) & 0xFFFF), n = (int)(e & 0xFFFF);
         const int64_t lo = (int64_t)s * p.slab_w;
-        __syncthreads();  // every warp is done with the previous slab
+        const int d0 = p.slab_desc0[s], nd = p.slab_desc0[s + 1] - d0;
+        __syncthreads();  // the previous entry's table and descriptors are no longer read
         GW* fc = const_cast<GW*>(tab.fc);
         GW* us = const_cast<GW*>(tab.u);
         for (int i = threadIdx.x; i < p.slab_w; i += THREADS) {
             const int64_t v = lo + i;
-            AggEntry<GW> e{~GW(0), ~GW(0), GW(0), GW(0)};
-            if (v <= p.sentinel) e = ld_agg(p.agg + v);
-            fc[2 * i] = e.f;      // +v is False where v can be False
-            fc[2 * i + 1] = e.t;  // -v is False where v can be True
-            us[i] = e.u;
+            AggEntry<GW> ae{~GW(0), ~GW(0), GW(0), GW(0)};
+            if (v <= p.sentinel) ae = ld_agg(p.agg + v);
+            fc[2 * i] = ae.f;      // +v is False where v can be False
+            fc[2 * i + 1] = ae.t;  // -v is False where v can be True
+            us[i] = ae.u;
         }
+        const bool staged = nd <= SLAB_DESC_MAX;
+        if (staged)
+            for (int i = threadIdx.x; i < nd; i += THREADS) s_desc[i] = p.buckets[d0 + i];
         __syncthreads();
         tab.lo = (int32_t)lo;
-        test_tiles<LW, GW, SlabTable<GW>>(p, tab, t + warp, seg_end, WARPS, lane, acc);
-        t = seg_end;
+        StrideTiles src{p.slab_tile0[s] + (int64_t)rank * WARPS + warp, (int64_t)n * WARPS, p.slab_tile0[s + 1]};
+        SmemRows rows{&s_rows[warp][0][lane]};
+        test_tiles<LW, GW, SlabTable<GW>>(p, tab, staged ? s_desc : p.buckets + d0, nd, src, rows, lane, acc);
     }
     finish_block<LW, GW, WARPS>(p, acc, lane, warp, s_acc);
 }

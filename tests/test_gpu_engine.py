@@ -134,7 +134,7 @@ def test_literal_out_of_range_raises(P):
 # stage-1 table variants, selected per engine at tsg_create:
 #   smem       whole literal-code table in shared memory (small num_vars x groups)
 #   l2         aggregate table gathered from L2, unpartitioned store
-#   slab       store partitioned into 4 variable slabs, hot prefix from shared memory
+#   slab       store partitioned into variable slabs (opt-in layout), hot prefix from shared memory
 #   smem_slab  partitioned store (hot-prefix literal order) tested by the smem kernel
 TABLES = {"smem": {"TSG_SMEM_TABLE": "1", "TSG_SLABS": "0"},
           "l2": {"TSG_SMEM_TABLE": "0", "TSG_SLABS": "0"},
@@ -213,7 +213,7 @@ def test_c2_shape_parity(P, monkeypatch, table):
     # with it disabled the store's 3 natural slabs drive the slab kernel
     use_table(monkeypatch, table)
     if table == "slab":
-        monkeypatch.delenv("TSG_SLABS")
+        monkeypatch.setenv("TSG_SLABS", "1")
     run_both(P, n=60_000, threads=8, lanes=32, nv=50_000, seed=22)
 
 
@@ -222,7 +222,7 @@ def test_c3_shape_parity(P, monkeypatch, table):
     # C3's 200k vars x 32 groups: 11 natural slabs (the benchmark's kernel)
     use_table(monkeypatch, table)
     if table == "slab":
-        monkeypatch.delenv("TSG_SLABS")
+        monkeypatch.setenv("TSG_SLABS", "1")
     run_both(P, n=150_000, threads=32, lanes=32, nv=200_000, seed=23)
 
 
