@@ -137,6 +137,20 @@ int tsg_stage_snapshots(tsg_engine* h, const int8_t* rows, int64_t n_rows,
                         int64_t row_pitch, int32_t on_device);
 int tsg_round(tsg_engine* h, const int32_t* group_lanes, const int32_t* group_tid,
               int32_t n_groups, double activity_inc, tsg_round_result* out);
+/* Packed snapshot rows (snapshot ingress): 2 bits per
+ * variable, a quarter of the int8 bytes.  u64 word k of a row covers
+ * variables 32k..32k+31: bit i of the low half = (value == 1), bit i of the
+ * high half = (value != 0) -- the same is_true / is_set the encoder derives
+ * from int8 rows (bitpack.py:104-111).  A row has tsg_packed_words(num_vars)
+ * words.  tsg_pack_rows is host code (no device, thread-safe: solver threads
+ * pack their own snapshots); tsg_stage_packed replaces tsg_stage_snapshots
+ * for the next round (on_device=1: `rows` is device memory, 32-byte aligned,
+ * pitch a multiple of 4 words, used in place). */
+int tsg_packed_words(int32_t num_vars, int64_t* words);
+int tsg_pack_rows(const int8_t* rows, int64_t n_rows, int64_t row_pitch, int32_t num_vars,
+                  uint64_t* out, int64_t out_pitch_words);
+int tsg_stage_packed(tsg_engine* h, const uint64_t* rows, int64_t n_rows,
+                     int64_t pitch_words, int32_t on_device);
 int tsg_round_prepare(tsg_engine* h, const int32_t* group_lanes,
                       const int32_t* group_tid, int32_t n_groups);
 int tsg_round_encode(tsg_engine* h);

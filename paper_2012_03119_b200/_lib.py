@@ -49,7 +49,7 @@ EXPORTS = (
     "tsg_scale_activities", "tsg_reduce", "tsg_remove_clauses", "tsg_stage_snapshots", "tsg_round",
     "tsg_round_prepare", "tsg_round_encode", "tsg_round_tables", "tsg_round_test", "tsg_fetch_reports",
     "tsg_reports_device", "tsg_sync", "tsg_stream", "tsg_pack", "tsg_aggregate", "tsg_lane_trigger",
-    "tsg_aggregate_trigger",
+    "tsg_aggregate_trigger", "tsg_packed_words", "tsg_pack_rows", "tsg_stage_packed",
 )
 
 _lib = None
@@ -74,6 +74,9 @@ def _declare(L):
         "tsg_reduce": ([P, I64, I64, pI64, P], C.c_int),
         "tsg_remove_clauses": ([P, P, I64, pI64], C.c_int),
         "tsg_stage_snapshots": ([P, P, I64, I64, I32], C.c_int),
+        "tsg_packed_words": ([I32, P], C.c_int),
+        "tsg_pack_rows": ([P, I64, I64, I32, P, I64], C.c_int),
+        "tsg_stage_packed": ([P, P, I64, I64, I32], C.c_int),
         "tsg_round": ([P, P, P, I32, D, C.POINTER(tsg_round_result)], C.c_int),
         "tsg_round_prepare": ([P, P, P, I32], C.c_int),
         "tsg_round_encode": ([P], C.c_int),

@@ -4,6 +4,7 @@
 // kernel launches on one CUDA stream per handle, report-buffer management,
 // store maintenance with CUB sort/select for the rare reduce path.
 #include <cuda_runtime.h>
+#include <immintrin.h>
 
 #include <algorithm>
 #include <cstdarg>
@@ -100,6 +101,11 @@ struct tsg_engine {
     const int8_t* rows = nullptr;  // device rows used by the encoder (owned or aliased)
     int8_t* rows_own = nullptr;
     int64_t rows_cap = 0, pitch = 0, n_rows = 0;
+    // packed rows (2 bits per variable, tsg_pack_rows) when `packed`
+    bool packed = false;
+    const uint64_t* prows = nullptr;
+    uint64_t* prows_own = nullptr;
+    int64_t prows_cap = 0, ppitch = 0;
 
     // round description
     int32_t n_groups = 0, n_chunks = 0;
@@ -249,10 +255,23 @@ int launch_encode(tsg_engine* h, int c) {
     auto* agg = reinterpret_cast<AggEntry<GW>*>(h->tables + h->chunk_off[c]);
     auto* lane = reinterpret_cast<LaneEntry<LW>*>(h->tables + h->chunk_off[c] + agg_bytes(h));
     dim3 grid((unsigned)((h->V + 2 + 127) / 128)), block(32, 8);
-    k_encode<LW, GW><<<grid, block, 0, h->st>>>(h->rows, ec, lane, agg);
+    if (h->packed) {
+        EncodePackedChunk pc{};
+        pc.G = ec.G;
+        pc.num_vars = h->V;
+        pc.pitch_words = h->ppitch;
+        pc.vstride = ec.vstride;
+        for (int g = 0; g < ec.G; ++g) { pc.row0[g] = ec.row0[g]; pc.lanes[g] = ec.lanes[g]; }
+        k_encode_packed<LW, GW><<<grid, block, 0, h->st>>>(h->prows, pc, lane, agg);
+    } else {
+        k_encode<LW, GW><<<grid, block, 0, h->st>>>(h->rows, ec, lane, agg);
+    }
     CK(cudaGetLastError());
     return TSG_OK;
 }
+
+// u64 words of one packed row: every 128-variable encoder block reads 4 words
+int64_t packed_words(int32_t V) { return round_up(((int64_t)V + 2 + 31) / 32, 4); }
 
 int do_encode(tsg_engine* h) {
     for (int c = 0; c < h->n_chunks; ++c) {
@@ -647,7 +666,7 @@ int tsg_destroy(tsg_engine* h) {
     cudaStreamSynchronize(h->st);
     for_parts(h, [&](Bucket&, Part& p) { part_free(h, p); });
     dfree(h, h->d_slab_tile0);
-    dfree(h, h->rows_own); dfree(h, h->tables); dfree(h, h->d_desc); dfree(h, h->out);
+    dfree(h, h->rows_own); dfree(h, h->prows_own); dfree(h, h->tables); dfree(h, h->d_desc); dfree(h, h->out);
     dfree(h, h->ctr); dfree(h, h->carry); dfree(h, h->out2); dfree(h, h->codes);
     cudaStreamSynchronize(h->st);
     if (h->h_ctr) cudaFreeHost(h->h_ctr);
@@ -908,6 +927,7 @@ int tsg_stage_snapshots(tsg_engine* h, const int8_t* rows, int64_t n_rows, int64
     if (n_rows < 0) return fail(TSG_EINVAL, "n_rows < 0");
     if (n_rows > 0 && row_pitch < h->V + 1) return fail(TSG_EINVAL, "row pitch %lld < num_vars+1", (long long)row_pitch);
     h->n_rows = n_rows;
+    h->packed = false;
     if (n_rows == 0) return TSG_OK;
     if (on_device && row_pitch % 4 == 0) {  // encode straight from the caller's HBM rows
         h->rows = rows;
@@ -928,6 +948,94 @@ int tsg_stage_snapshots(tsg_engine* h, const int8_t* rows, int64_t n_rows, int64
                          on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDefault, h->st));
     h->rows = h->rows_own;
     h->pitch = pitch;
+    return TSG_OK;
+}
+
+int tsg_packed_words(int32_t num_vars, int64_t* words) {
+    if (num_vars < 0) return fail(TSG_EINVAL, "num_vars < 0");
+    *words = packed_words(num_vars);
+    return TSG_OK;
+}
+
+// SWAR pack of one row into 2-bit words (AVX2 when the host has it)
+__attribute__((target("avx2"))) static void pack_row_avx2(const int8_t* r, int64_t nv1, uint64_t* out, int64_t words) {
+    const __m256i one = _mm256_set1_epi8(1), zero = _mm256_setzero_si256();
+    int64_t k = 0;
+    for (; 32 * k + 32 <= nv1; ++k) {
+        const __m256i x = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(r + 32 * k));
+        const uint32_t t = (uint32_t)_mm256_movemask_epi8(_mm256_cmpeq_epi8(x, one));
+        const uint32_t z = (uint32_t)_mm256_movemask_epi8(_mm256_cmpeq_epi8(x, zero));
+        out[k] = (uint64_t)t | ((uint64_t)~z << 32);
+    }
+    for (; k < words; ++k) {
+        uint32_t t = 0, st = 0;
+        for (int64_t i = 32 * k; i < 32 * k + 32 && i < nv1; ++i) {
+            t |= (uint32_t)(r[i] == 1) << (i - 32 * k);
+            st |= (uint32_t)(r[i] != 0) << (i - 32 * k);
+        }
+        out[k] = (uint64_t)t | ((uint64_t)st << 32);
+    }
+}
+
+static void pack_row_scalar(const int8_t* r, int64_t nv1, uint64_t* out, int64_t words) {
+    for (int64_t k = 0; k < words; ++k) {
+        uint32_t t = 0, st = 0;
+        for (int64_t i = 32 * k; i < 32 * k + 32 && i < nv1; ++i) {
+            t |= (uint32_t)(r[i] == 1) << (i - 32 * k);
+            st |= (uint32_t)(r[i] != 0) << (i - 32 * k);
+        }
+        out[k] = (uint64_t)t | ((uint64_t)st << 32);
+    }
+}
+
+int tsg_pack_rows(const int8_t* rows, int64_t n_rows, int64_t row_pitch, int32_t num_vars, uint64_t* out,
+                  int64_t out_pitch_words) {
+    if (n_rows < 0 || num_vars < 0) return fail(TSG_EINVAL, "negative size");
+    const int64_t words = packed_words(num_vars);
+    if (n_rows > 0 && (!rows || !out)) return fail(TSG_EINVAL, "null argument");
+    if (n_rows > 0 && row_pitch < (int64_t)num_vars + 1)
+        return fail(TSG_EINVAL, "row pitch %lld < num_vars+1", (long long)row_pitch);
+    if (out_pitch_words < words) return fail(TSG_EINVAL, "out pitch %lld < %lld words", (long long)out_pitch_words, (long long)words);
+    static const bool avx2 = __builtin_cpu_supports("avx2");
+    for (int64_t r = 0; r < n_rows; ++r) {
+        uint64_t* o = out + r * out_pitch_words;
+        if (avx2) pack_row_avx2(rows + r * row_pitch, (int64_t)num_vars + 1, o, words);
+        else pack_row_scalar(rows + r * row_pitch, (int64_t)num_vars + 1, o, words);
+        for (int64_t k = words; k < out_pitch_words; ++k) o[k] = 0;
+    }
+    return TSG_OK;
+}
+
+int tsg_stage_packed(tsg_engine* h, const uint64_t* rows, int64_t n_rows, int64_t pitch_words, int32_t on_device) {
+    CKR(validate_handle(h));
+    DevGuard g(h->dev);
+    const int64_t words = packed_words(h->V);
+    if (n_rows < 0) return fail(TSG_EINVAL, "n_rows < 0");
+    if (n_rows > 0 && pitch_words < words)
+        return fail(TSG_EINVAL, "packed pitch %lld < %lld words", (long long)pitch_words, (long long)words);
+    h->n_rows = n_rows;
+    h->packed = true;
+    if (n_rows == 0) return TSG_OK;
+    if (on_device && pitch_words % 4 == 0 && ((uintptr_t)rows % 32) == 0) {
+        h->prows = rows;
+        h->ppitch = pitch_words;
+        return TSG_OK;
+    }
+    const int64_t need = words * n_rows;
+    if (need > h->prows_cap) {
+        dfree(h, h->prows_own);
+        h->prows_own = nullptr;
+        const int64_t cap = std::max(need, h->prows_cap * 2);
+        CKR(dalloc(h, (void**)&h->prows_own, cap * 8));
+        h->prows_cap = cap;
+    }
+    if (pitch_words == words)
+        CK(cudaMemcpyAsync(h->prows_own, rows, need * 8, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDefault, h->st));
+    else
+        CK(cudaMemcpy2DAsync(h->prows_own, words * 8, rows, pitch_words * 8, words * 8, n_rows,
+                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDefault, h->st));
+    h->prows = h->prows_own;
+    h->ppitch = words;
     return TSG_OK;
 }
 

@@ -153,6 +153,95 @@ __global__ void __launch_bounds__(256) k_encode(const int8_t* __restrict__ rows,
 }
 
 // ---------------------------------------------------------------------------
+// K1+K2 from packed rows: every snapshot row arrives as
+// 2 bits per variable -- u64 word k holds variables 32k..32k+31, low half
+// "== TRUE", high half "!= UNDEF" (tsg_pack_rows) -- a quarter of the int8
+// bytes.  Block = 32 x 8 threads covers 128 variables (4 words per row);
+// warp y takes groups y, y+8, ...  Lane r loads row r of the group (32
+// contiguous bytes), and a 5-step shuffle transpose turns the 32 rows x 32
+// variables bit matrix into one lane word per variable, so lane v ends up
+// with is_true / is_set of variable v exactly as k_encode produces them.
+
+// 32x32 bit transpose across the warp: afterwards bit j of lane i's word is
+// bit i of lane j's word before.
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
+#pragma unroll
+    for (int sft = 16; sft >= 1; sft >>= 1) {
+        const uint32_t m = sft == 16 ? 0x0000FFFFu : sft == 8 ? 0x00FF00FFu : sft == 4 ? 0x0F0F0F0Fu
+                         : sft == 2 ? 0x33333333u : 0x55555555u;
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, sft);
+        x = (lane & sft) ? ((x & ~m) | ((y & ~m) >> sft)) : ((x & m) | ((y & m) << sft));
+    }
+    return x;
+}
+
+struct EncodePackedChunk {
+    int32_t G;
+    int32_t num_vars;
+    int64_t pitch_words;  // u64 words between rows (multiple of 4)
+    int64_t vstride;
+    int64_t row0[MAXG];
+    int32_t lanes[MAXG];
+};
+
+template <class LW, class GW>
+__global__ void __launch_bounds__(256) k_encode_packed(const uint64_t* __restrict__ rows,
+                                                       const __grid_constant__ EncodePackedChunk c,
+                                                       LaneEntry<LW>* __restrict__ lane_tab,
+                                                       AggEntry<GW>* __restrict__ agg) {
+    __shared__ GW sT[128], sF[128], sU[128];
+    const int lane = threadIdx.x, y = threadIdx.y, t = y * 32 + lane;
+    if (t < 128) { sT[t] = 0; sF[t] = 0; sU[t] = 0; }
+    __syncthreads();
+    const int64_t vbase = (int64_t)blockIdx.x * 128;
+    const int64_t V = c.num_vars;
+    const int64_t w0 = (int64_t)blockIdx.x * 4;  // first word of the block in every row
+    for (int g = y; g < c.G; g += 8) {
+        const int n = c.lanes[g];
+        LW tw[4] = {0, 0, 0, 0}, sw[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int half = 0; half < (int)(sizeof(LW) / 4); ++half) {
+            if (half * 32 >= n) break;
+            const int r = half * 32 + lane;
+            uint4 a = make_uint4(0, 0, 0, 0), b = make_uint4(0, 0, 0, 0);
+            if (r < n) {
+                const uint4* src = reinterpret_cast<const uint4*>(rows + (c.row0[g] + r) * c.pitch_words + w0);
+                a = __ldg(src);
+                b = __ldg(src + 1);
+            }
+            const uint32_t tv[4] = {a.x, a.z, b.x, b.z}, sv[4] = {a.y, a.w, b.y, b.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                tw[k] |= (LW)warp_transpose32(tv[k], lane) << (32 * half);
+                sw[k] |= (LW)warp_transpose32(sv[k], lane) << (32 * half);
+            }
+        }
+        const LW lm = width_mask<LW>(n);
+        const GW bit = GW(1) << g;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t v = vbase + 32 * k + lane;
+            LW tk = tw[k], sk = sw[k];
+            if (v == 0) { tk = 0; sk = 0; }  // slot 0 is never set (bitpack.py:110-111)
+            LaneEntry<LW>* dst = lane_tab + (int64_t)g * c.vstride + v;
+            if (v <= V) *dst = LaneEntry<LW>{tk, sk};
+            else if (v == V + 1) *dst = LaneEntry<LW>{LW(0), ~LW(0)};  // sentinel: always False
+            if (v >= 1 && v <= V) {  // AggregateAssignment.from_packed, bitpack.py:156-166
+                if (tk != 0) or_shared(&sT[32 * k + lane], bit);
+                if ((sk & ~tk) != 0) or_shared(&sF[32 * k + lane], bit);
+                if (n == 0 || (~sk & lm) != 0) or_shared(&sU[32 * k + lane], bit);
+            }
+        }
+    }
+    __syncthreads();
+    if (t < 128) {
+        const int64_t v = vbase + t;
+        if (v <= V) agg[v] = AggEntry<GW>{sT[t], sF[t], sU[t], GW(0)};
+        else if (v == V + 1) agg[v] = AggEntry<GW>{~GW(0), ~GW(0), GW(0), GW(0)};
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K3+K4+K5: trigger test.  Persistent grid; one warp per tile of 32 clauses
 // of one bucket, one clause per lane.
 //

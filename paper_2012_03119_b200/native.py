@@ -15,6 +15,41 @@ from . import _lib, reports
 from ._lib import REPORT_DTYPE, check, ptr
 
 
+def packed_words(num_vars: int) -> int:
+    """u64 words per packed snapshot row (include/tsg.h tsg_packed_words)."""
+    w = C.c_int64(0)
+    check(_lib.load().tsg_packed_words(num_vars, C.byref(w)))
+    return w.value
+
+
+def pack_rows(rows: np.ndarray, num_vars: int, out: Optional[np.ndarray] = None, threads: int = 1) -> np.ndarray:
+    """int8 snapshot rows [n, >= num_vars+1] -> packed rows uint64[n, packed_words]
+    (2 bits per variable; tsg_pack_rows).  The C call releases the GIL, so
+    `threads` > 1 packs row chunks in parallel -- the way solver threads pack
+    their own snapshots."""
+    rows = np.ascontiguousarray(rows, np.int8)
+    n = rows.shape[0]
+    w = packed_words(num_vars)
+    if out is None:
+        out = np.empty((n, w), np.uint64)
+    L = _lib.load()
+
+    def run(a, b):
+        if b > a:
+            check(L.tsg_pack_rows(C.c_void_p(rows.ctypes.data + a * rows.strides[0]), b - a, rows.strides[0],
+                                  num_vars, C.c_void_p(out.ctypes.data + a * out.strides[0]),
+                                  out.strides[0] // 8))
+
+    if threads <= 1 or n < 2 * threads:
+        run(0, n)
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+        cuts = [n * i // threads for i in range(threads + 1)]
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(lambda i: run(cuts[i], cuts[i + 1]), range(threads)))
+    return out
+
+
 class NativeEngine:
     def __init__(self, num_vars: int, lane_width: int = 32, group_width: int = 32, device: int = 0,
                  timing: bool = False, report_capacity: int = 0):
@@ -96,6 +131,14 @@ class NativeEngine:
 
     def stage_device(self, dptr: int, n_rows: int, pitch: int) -> None:
         check(self.L.tsg_stage_snapshots(self.h, C.c_void_p(dptr), n_rows, pitch, 1))
+
+    def stage_packed(self, packed: np.ndarray) -> None:
+        """Packed rows (pack_rows) from host memory (pinned memory copies fastest)."""
+        check(self.L.tsg_stage_packed(self.h, C.c_void_p(packed.ctypes.data), packed.shape[0],
+                                      packed.strides[0] // 8, 0))
+
+    def stage_packed_ptr(self, ptr_: int, n_rows: int, pitch_words: int, on_device: bool) -> None:
+        check(self.L.tsg_stage_packed(self.h, C.c_void_p(ptr_), n_rows, pitch_words, 1 if on_device else 0))
 
     def prepare(self, group_lanes, group_tid) -> None:
         self._gl = np.ascontiguousarray(group_lanes, np.int32)

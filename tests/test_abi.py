@@ -4,6 +4,7 @@ product fails loudly instead of falling back to a CPU path."""
 import os
 import re
 
+import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -53,3 +54,23 @@ def test_host_side_validation_matches_reference():
         P.pack_assignments([[0, 0]] * 3, 1, lane_width=2)
     with pytest.raises(ValueError):
         P.pack_assignments([], 1, lane_width=65)
+
+
+@pytest.mark.parametrize("num_vars", [0, 1, 30, 31, 32, 63, 95, 1000, 4097])
+def test_pack_rows_host_encoding(num_vars):
+    # tsg_pack_rows is host code (snapshot ingress): 2 bits per variable,
+    # low half (value == 1), high half (value != 0) -- bitpack.py:104-111
+    from paper_2012_03119_b200.native import pack_rows, packed_words
+    rng = np.random.default_rng(num_vars)
+    rows = rng.choice(np.array([1, -1, 0, 0, 1, 5, -7], np.int8), size=(9, num_vars + 1 + 3))
+    got = pack_rows(rows[:, :num_vars + 1], num_vars, threads=3)
+    w = packed_words(num_vars)
+    assert got.shape == (9, w) and w % 4 == 0 and 32 * w >= num_vars + 2
+    t = np.zeros((9, 32 * w), bool)
+    s = np.zeros((9, 32 * w), bool)
+    t[:, :num_vars + 1] = rows[:, :num_vars + 1] == 1
+    s[:, :num_vars + 1] = rows[:, :num_vars + 1] != 0
+    bit = np.uint64(1) << np.arange(32, dtype=np.uint64)
+    want = (t.reshape(9, w, 32) * bit).sum(2).astype(np.uint64) | \
+        ((s.reshape(9, w, 32) * bit).sum(2).astype(np.uint64) << np.uint64(32))
+    assert np.array_equal(got, want)

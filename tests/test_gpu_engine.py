@@ -309,3 +309,66 @@ def test_report_buffer_overflow_replay(P, monkeypatch, table):
     acts_dev = np.concatenate([b[4] for b in dev.buckets()])
     acts_ora = np.concatenate([b[5] for b in ora.buckets()])
     assert np.array_equal(acts_dev.view(np.uint64), acts_ora.view(np.uint64))
+
+
+def _tables(eng):
+    import torch
+    ptr_, nbytes = eng.tables()
+
+    class _CAI:
+        __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr_, False), "version": 3}
+    eng.sync()
+    return torch.as_tensor(_CAI(), device="cuda").cpu().numpy().copy()
+
+
+def _defined_tables(raw, nv, lw, gw, gl):
+    """The written entries of the round tables (tsg_engine.cu layout: per chunk
+    agg[V+2] then lane[G][vstride], each region 256-byte aligned)."""
+    def up(x, m):
+        return (x + m - 1) // m * m
+    aeb = 32 if gw > 32 else 16
+    leb = 16 if lw > 32 else 8
+    vstride = up(nv + 2, 4)
+    parts, off = [], 0
+    for c in range(0, len(gl), gw):
+        G = min(gw, len(gl) - c)
+        parts.append(raw[off:off + (nv + 2) * aeb].reshape(nv + 2, aeb)[:, :3 * aeb // 4])  # t, f, u
+        off += up((nv + 2) * aeb, 256)
+        lane = raw[off:off + vstride * G * leb].reshape(G, vstride, leb)[:, :nv + 2]
+        parts.append(lane.reshape(-1))
+        off += up(vstride * G * leb, 256)
+    return np.concatenate([x.reshape(-1) for x in parts])
+
+
+@pytest.mark.parametrize("lw,gw,threads,lanes,nv", [(32, 32, 3, 40, 1000), (64, 64, 2, 100, 333),
+                                                    (64, 8, 5, 70, 4095), (7, 3, 4, 20, 31), (32, 32, 32, 32, 20_000)])
+def test_packed_rows_encode_identically(P, lw, gw, threads, lanes, nv):
+    # snapshot ingress in 2-bit packed rows: the packed encoder must build
+    # byte-identical lane/aggregate tables, and the round identical results
+    from paper_2012_03119_b200 import workload as W
+    from paper_2012_03119_b200.native import NativeEngine, pack_rows
+    rng = np.random.default_rng(nv)
+    buckets = W.clause_buckets(5000, nv, rng, 1, 10)
+    flat, offs, ids = W.flatten(buckets)
+    snaps = W.snapshots(threads, lanes, nv, rng)
+    snaps[:, 0] = rng.integers(-1, 2, snaps.shape[0])  # slot 0 must be ignored
+    snaps[::7, 5 % (nv + 1)] = 9                       # non-{1,-1,0} values read as False
+    gl, gt = W.groups_for(threads, lanes, lw)
+    out = []
+    for packed in (False, True):
+        e = NativeEngine(nv, lw, gw)
+        e.add_clauses(flat, offs, ids)
+        if packed:
+            e.stage_packed(pack_rows(snaps, nv, threads=2))
+        else:
+            e.stage(snaps)
+        e.prepare(gl, gt)
+        e.encode()
+        tab = _defined_tables(_tables(e), nv, lw, gw, gl)
+        res = e.test(1.0)
+        recs = np.sort(e.fetch(res.reports), order=["engine_id", "group"])
+        out.append((tab, res.lane_triggers, res.aggregate_tests_negative, recs))
+        e.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][1:3] == out[1][1:3]
+    assert np.array_equal(out[0][3], out[1][3])
