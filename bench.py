@@ -233,12 +233,15 @@ def main():
     build_s = time.perf_counter() - t_build
 
     stream = torch.cuda.ExternalStream(eng.stream(), device=torch.device("cuda", local))
-    # device-resident snapshots (pitch multiple of 16) for the `value` leg
-    pitch = (cfg.num_vars + 1 + 15) // 16 * 16
-    d_snaps = torch.zeros((A, pitch), dtype=torch.int8, device=f"cuda:{local}")
-    d_snaps[:, :cfg.num_vars + 1] = torch.from_numpy(snaps).to(d_snaps.device)
+    # device-resident snapshots for the `value` leg, in the ingress format the
+    # solver threads hand over: packed rows, 2 bits per variable (tsg_pack_rows)
+    from paper_2012_03119_b200.native import pack_rows, packed_words
+    pw = packed_words(cfg.num_vars)
+    host_threads = os.cpu_count() or 1
+    d_packed = torch.from_numpy(pack_rows(snaps, cfg.num_vars, threads=host_threads).view(np.int64)).to(
+        f"cuda:{local}")
     torch.cuda.synchronize()
-    eng.stage_device(d_snaps.data_ptr(), A, pitch)
+    eng.stage_packed_ptr(d_packed.data_ptr(), A, pw, on_device=True)
     eng.prepare(gl, gt)
 
     tables_t = None
@@ -295,41 +298,63 @@ def main():
     value = tests_per_step / (ms_per_step * 1e-3)
 
     # ---- e2e: host buffers through the C ABI -------------------------------
+    # Primary: the step's input is the round's snapshots as packed 2-bit rows in
+    # pinned host memory -- the ingress format solver threads produce when they
+    # submit (tsg_pack_rows replaces the int8 values.copy() the reference solver
+    # makes per snapshot, solver.py:280-282) -- copied H2D (tsg_stage_packed),
+    # the round, and the report records copied D2H (tsg_fetch_reports), every
+    # step, wall clock.  Also measured: the host packing itself and the same
+    # step from raw int8 rows (205 MB H2D).
     e2e = None
-    h_snaps = torch.from_numpy(snaps).pin_memory()
-    rec_buf = None
     e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
     if world == 1:
         from paper_2012_03119_b200 import _lib
         import ctypes as C
         rec_buf = torch.empty((8 << 20) * 16, dtype=torch.uint8).pin_memory()
+        h_packed_t = torch.empty((A, pw), dtype=torch.int64).pin_memory()
+        h_packed = h_packed_t.numpy().view(np.uint64)
+        h_int8_t = torch.from_numpy(snaps).pin_memory()
         L = eng.L
 
-        def e2e_step():
-            _lib.check(L.tsg_stage_snapshots(eng.h, C.c_void_p(h_snaps.data_ptr()), A, cfg.num_vars + 1, 0))
-            r = eng.round(gl, gt, 1.0)
+        def finish(r):
             got = C.c_int64(0)
             n = min(r.reports, (8 << 20))
             _lib.check(L.tsg_fetch_reports(eng.h, C.c_void_p(rec_buf.data_ptr()), n, C.byref(got)))
             return r
-        for _ in range(2):
-            e2e_step()
-        eng.sync()
-        w0 = time.perf_counter()
-        with torch.cuda.stream(stream):
-            e0.record(stream)
-        d2h = 0
-        for _ in range(e2e_steps):
-            r = e2e_step()
-            d2h += r.reports * 16 + 32
-        with torch.cuda.stream(stream):
-            e1.record(stream)
-        eng.sync()
-        wall = time.perf_counter() - w0
-        e2e_ms = e0.elapsed_time(e1) / e2e_steps
-        e2e = {"value": r.lane_tests / (e2e_ms * 1e-3), "unit": "clause_assignment_tests/s",
-               "h2d_bytes_per_step": int(A * (cfg.num_vars + 1)), "d2h_bytes_per_step": int(d2h / e2e_steps),
-               "ms_per_step": e2e_ms, "wall_ms_per_step": wall / e2e_steps * 1e3}
+
+        def step_packed():
+            _lib.check(L.tsg_stage_packed(eng.h, C.c_void_p(h_packed_t.data_ptr()), A, pw, 0))
+            return finish(eng.round(gl, gt, 1.0))
+
+        def step_int8():
+            _lib.check(L.tsg_stage_snapshots(eng.h, C.c_void_p(h_int8_t.data_ptr()), A, cfg.num_vars + 1, 0))
+            return finish(eng.round(gl, gt, 1.0))
+
+        def timed(fn, k):
+            for _ in range(2):
+                fn()
+            eng.sync()
+            w0 = time.perf_counter()
+            d2h = 0
+            for _ in range(k):
+                r = fn()
+                d2h += r.reports * 16 + 32
+            eng.sync()
+            return (time.perf_counter() - w0) / k * 1e3, r, d2h // k
+
+        pack_rows(snaps, cfg.num_vars, out=h_packed, threads=host_threads)
+        p0 = time.perf_counter()
+        for _ in range(3):
+            pack_rows(snaps, cfg.num_vars, out=h_packed, threads=host_threads)
+        pack_ms = (time.perf_counter() - p0) / 3 * 1e3
+        ms, r, d2h = timed(step_packed, e2e_steps)
+        ms8, r8, _ = timed(step_int8, max(3, e2e_steps // 2))
+        e2e = {"value": r.lane_tests / (ms * 1e-3), "unit": "clause_assignment_tests/s",
+               "h2d_bytes_per_step": int(A * pw * 8), "d2h_bytes_per_step": int(d2h), "ms_per_step": ms,
+               "input": "packed 2-bit snapshot rows in pinned host memory (solver-side ingress format)",
+               "host_pack_ms_per_round": pack_ms, "host_pack_threads": host_threads,
+               "int8_rows": {"value": r8.lane_tests / (ms8 * 1e-3), "ms_per_step": ms8,
+                             "h2d_bytes_per_step": int(A * (cfg.num_vars + 1))}}
 
     # ---- roofline of the trigger kernel --------------------------------------
     peak, peak_kind = load_peaks()

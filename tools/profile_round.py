@@ -24,11 +24,17 @@ eng = NativeEngine(cfg.num_vars, timing=True, report_capacity=8 << 20)
 eng.add_clauses(flat, offs, ids)
 snaps = W.snapshots(cfg.threads, cfg.lanes, cfg.num_vars, np.random.default_rng(cfg.seed + 999))
 gl, gt = W.groups_for(cfg.threads, cfg.lanes)
-pitch = (cfg.num_vars + 1 + 15) // 16 * 16
-d = torch.zeros((snaps.shape[0], pitch), dtype=torch.int8, device="cuda")
-d[:, :cfg.num_vars + 1] = torch.from_numpy(snaps).cuda()
-torch.cuda.synchronize()
-eng.stage_device(d.data_ptr(), snaps.shape[0], pitch)
+if os.environ.get("TSG_INT8_ROWS"):  # int8 snapshot rows
+    pitch = (cfg.num_vars + 1 + 15) // 16 * 16
+    d = torch.zeros((snaps.shape[0], pitch), dtype=torch.int8, device="cuda")
+    d[:, :cfg.num_vars + 1] = torch.from_numpy(snaps).cuda()
+    torch.cuda.synchronize()
+    eng.stage_device(d.data_ptr(), snaps.shape[0], pitch)
+else:  # packed rows (the ingress format)
+    from paper_2012_03119_b200.native import pack_rows, packed_words
+    d = torch.from_numpy(pack_rows(snaps, cfg.num_vars, threads=8).view(np.int64)).cuda()
+    torch.cuda.synchronize()
+    eng.stage_packed_ptr(d.data_ptr(), snaps.shape[0], packed_words(cfg.num_vars), on_device=True)
 eng.prepare(gl, gt)
 for r in range(rounds):
     eng.encode()
