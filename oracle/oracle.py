@@ -284,6 +284,13 @@ class OracleEngine:
         q.clear()
         return out
 
+    def remove_clauses(self, ids):  # explicit delete (C4): _SizeBucket.compact with a keep mask
+        ids = [int(i) for i in ids]
+        removed = self.store.remove(ids)
+        for i in ids:
+            self.lits.pop(i, None)
+        return removed
+
     def reduce_store(self):  # engine.py:469-505
         total = len(self.store)
         if total == 0:

@@ -190,6 +190,9 @@ class Engine:
         h = C.c_void_p()
         check(self._L.tsg_create(num_vars, C.byref(cfg), C.byref(h)))
         self._h = h
+        w = C.c_int64(0)
+        check(self._L.tsg_packed_words(num_vars, C.byref(w)))
+        self._packed_words = w.value
         self.store = DeviceClauseStore(self)
         self._lits: Dict[int, tuple] = {}
         self._size_rank: Dict[int, int] = {}
@@ -237,15 +240,33 @@ class Engine:
         return engine_id
 
     def submit_assignment(self, snapshot) -> bool:
+        """engine.py:319-333.  The snapshot is packed to 2 bits per variable
+        here, in the submitting solver thread (tsg_pack_rows releases the GIL),
+        where the reference keeps the int8 array; a wrong length is reported
+        by run_round, as in the reference (bitpack.py:92-103)."""
         cap = self.config.assignment_queue_capacity
         with self._queue_lock:
             q = self._snapshots.setdefault(snapshot.thread_id, deque())
             if len(q) >= cap:
                 self.counters["snapshots_dropped"] += 1
                 return False
-            q.append(snapshot)
+        packed = self._pack(snapshot.values)
+        with self._queue_lock:
+            q = self._snapshots.setdefault(snapshot.thread_id, deque())
+            if len(q) >= cap:  # filled up while this thread was packing
+                self.counters["snapshots_dropped"] += 1
+                return False
+            q.append((snapshot, packed))
             self.counters["snapshots_accepted"] += 1
             return True
+
+    def _pack(self, values):
+        vals = np.ascontiguousarray(np.asarray(values, dtype=np.int8))
+        if vals.ndim != 1 or vals.shape[0] != self.num_vars + 1:
+            return vals.shape[0] if vals.ndim == 1 else -1  # length error, raised by run_round
+        out = np.empty((1, self._packed_words), dtype=np.uint64)
+        check(self._L.tsg_pack_rows(ptr(vals), 1, vals.shape[0], self.num_vars, ptr(out), self._packed_words))
+        return out
 
     def drain_reports(self, thread_id: int) -> List[Report]:
         with self._queue_lock:
@@ -331,19 +352,17 @@ class Engine:
             snaps = pending[tid]
             for i in range(0, len(snaps), lane_width):
                 chunk = snaps[i:i + lane_width]
-                for j, s in enumerate(chunk):
-                    vals = np.asarray(s.values, dtype=np.int8)
-                    if vals.shape[0] != self.num_vars + 1:
-                        raise ValueError(f"assignment {j} has {vals.shape[0]} slots, "
-                                         f"expected {self.num_vars + 1}")
-                    rows.append(vals)
+                for j, (_, packed) in enumerate(chunk):
+                    if not isinstance(packed, np.ndarray):
+                        raise ValueError(f"assignment {j} has {packed} slots, expected {self.num_vars + 1}")
+                    rows.append(packed)
                 lanes.append(len(chunk))
                 tids.append(tid)
 
         reports: List[Report] = []
         if lanes:
-            block = np.ascontiguousarray(np.stack(rows))
-            check(self._L.tsg_stage_snapshots(self._h, ptr(block), block.shape[0], block.shape[1], 0))
+            block = np.concatenate(rows)
+            check(self._L.tsg_stage_packed(self._h, ptr(block), block.shape[0], block.shape[1], 0))
             gl = np.asarray(lanes, dtype=np.int32)
             gt = np.asarray(tids, dtype=np.int32)
             res = _lib.tsg_round_result()
@@ -385,7 +404,7 @@ class Engine:
         if self.config.trace:
             self.trace.append(RoundTrace(
                 snapshots=[(s.thread_id, np.array(s.values, copy=True))
-                           for snaps in pending.values() for s in snaps],
+                           for snaps in pending.values() for s, _ in snaps],
                 store=store_snapshot, reports=list(reports)))
 
         self.counters["rounds"] += 1
