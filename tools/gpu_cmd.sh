@@ -1,2 +1,2 @@
-timeout 600 python -m pytest tests/test_gpu_streaming.py -m gpu -x -q --timeout 200 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_exchange.py -m gpu -x -q --timeout 300 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
 tail -15 gpurun_out/pytest_gpu.log
