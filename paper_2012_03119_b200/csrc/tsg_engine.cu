@@ -147,6 +147,8 @@ struct tsg_engine {
     int64_t* d_slab_tile0 = nullptr;     // [n_slabs + 1] tile0, then [n_slabs + 1] desc0 (int32), then schedule
     int64_t slab_tile0_cap = 0;
     std::vector<uint64_t> h_sched;
+    bool l2_persist = true;             // persisting L2 window over the round tables (TSG_L2_PERSIST=0 disables)
+    const void* persist_base = nullptr;
 };
 
 namespace {
@@ -620,6 +622,7 @@ int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
     h->cfg = *cfg;
     h->V = num_vars;
     if (const char* e = getenv("TSG_SMEM_TABLE")) h->smem_table = atoi(e) != 0;
+    if (const char* e = getenv("TSG_L2_PERSIST")) h->l2_persist = atoi(e) != 0;
     // Variable slabs, opt-in: TSG_SLABS=1 partitions the store
     // into as many slabs as one CTA's shared memory needs for the aggregate
     // words, TSG_SLABS=n>1 into at least n.  Default: one slab (unpartitioned
@@ -1070,6 +1073,25 @@ int tsg_round_prepare(tsg_engine* h, const int32_t* group_lanes, const int32_t* 
         h->tables = nullptr;
         CKR(dalloc(h, (void**)&h->tables, off));
         h->tables_cap = off;
+    }
+    if (h->l2_persist && off > 0 && h->persist_base != h->tables) {
+        // keep the round tables L2-resident while the clause stream and the
+        // report records flow through (access-policy window, persisting hits)
+        int max_persist = 0, max_window = 0;
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, h->dev);
+        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, h->dev);
+        const size_t win = (size_t)std::min<int64_t>(off, max_window);
+        if (max_persist > 0 && win > 0) {
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(win, (size_t)max_persist));
+            cudaStreamAttrValue attr{};
+            attr.accessPolicyWindow.base_ptr = h->tables;
+            attr.accessPolicyWindow.num_bytes = win;
+            attr.accessPolicyWindow.hitRatio = std::min(1.0f, (float)max_persist / (float)win);
+            attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+            attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+            CK(cudaStreamSetAttribute(h->st, cudaStreamAttributeAccessPolicyWindow, &attr));
+            h->persist_base = h->tables;
+        }
     }
     return TSG_OK;
 }
