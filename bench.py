@@ -211,11 +211,20 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TSG_BENCH_BACKEND=gloo runs the multi-rank path with every rank on the
+    # visible GPUs round-robin (a harness check of the N>1 logic on one GPU);
+    # the measured configuration is NCCL, one rank per GPU.
+    backend = os.environ.get("TSG_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     from paper_2012_03119_b200.native import NativeEngine
 
@@ -289,6 +298,15 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
     elapsed_ms = e0.elapsed_time(e1)
+    if dist is not None:  # the broadcast tables must be identical on every rank
+        with torch.cuda.stream(stream):
+            cs = torch.stack([tables_t.to(torch.int64).sum(), (tables_t.to(torch.int64) * 131).remainder(
+                1000003).sum()])
+        lo, hi = cs.clone(), cs.clone()
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+        dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+        if not torch.equal(lo, hi):
+            raise RuntimeError("round tables differ across ranks after the broadcast")
     if dist is not None:
         t = torch.tensor([elapsed_ms], device=f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -158,6 +158,9 @@ struct DevGuard {
     explicit DevGuard(int dev) {
         cudaGetDevice(&prev);
         if (prev != dev) cudaSetDevice(dev);
+        // a non-sticky error left by another library in this thread (torch,
+        // NCCL, gloo) must not be reported by our own launch checks
+        cudaGetLastError();
     }
     ~DevGuard() {
         int cur = -1;
@@ -1081,15 +1084,22 @@ int tsg_round_prepare(tsg_engine* h, const int32_t* group_lanes, const int32_t* 
         cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, h->dev);
         cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, h->dev);
         const size_t win = (size_t)std::min<int64_t>(off, max_window);
+        // best effort: another context may hold the device-wide persisting
+        // carve-out; then the round runs without the window
+        if (max_persist > 0 && win > 0 &&
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(win, (size_t)max_persist)) != cudaSuccess) {
+            cudaGetLastError();
+            max_persist = 0;
+        }
         if (max_persist > 0 && win > 0) {
-            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(win, (size_t)max_persist));
             cudaStreamAttrValue attr{};
             attr.accessPolicyWindow.base_ptr = h->tables;
             attr.accessPolicyWindow.num_bytes = win;
             attr.accessPolicyWindow.hitRatio = std::min(1.0f, (float)max_persist / (float)win);
             attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
             attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-            CK(cudaStreamSetAttribute(h->st, cudaStreamAttributeAccessPolicyWindow, &attr));
+            if (cudaStreamSetAttribute(h->st, cudaStreamAttributeAccessPolicyWindow, &attr) != cudaSuccess)
+                cudaGetLastError();
             h->persist_base = h->tables;
         }
     }
