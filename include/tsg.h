@@ -157,6 +157,14 @@ int tsg_round_encode(tsg_engine* h);
 int tsg_round_tables(tsg_engine* h, void** device_ptr, int64_t* bytes);
 int tsg_round_test(tsg_engine* h, double activity_inc, tsg_round_result* out);
 int tsg_fetch_reports(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n);
+/* Pipelined egress: compact the round's records and start their copy into
+ * `out` (pinned host memory) on the handle's egress stream, returning the
+ * record count at once.  The next round writes the other of two record
+ * buffers, so its ingress and test overlap this copy (PCIe is full duplex);
+ * a round never overwrites a buffer whose copy-out is still running.  `out`
+ * must stay untouched until tsg_fetch_wait returns. */
+int tsg_fetch_reports_async(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n);
+int tsg_fetch_wait(tsg_engine* h);
 /* device pointer + count of the round's records (for device-side consumers) */
 int tsg_reports_device(tsg_engine* h, void** device_ptr, int64_t* n);
 int tsg_sync(tsg_engine* h);

@@ -125,6 +125,19 @@ struct tsg_engine {
     tsg_report* out2 = nullptr;             // compaction target for fetch
     int64_t out2_cap = 0;
     bool compacted = true;
+    // report egress (tsg_fetch_reports_async): the record buffers above are one
+    // of two slots; `alt` is the other.  A round whose records are being copied
+    // out on the egress stream hands its slot over, and the next round writes
+    // the other one; a slot is rewritten only after its copy-out event.
+    struct Slot {
+        tsg_report *out = nullptr, *out2 = nullptr;
+        int64_t out_cap = 0, out2_cap = 0;
+        cudaEvent_t ev = nullptr;   // copy-out of this slot's records done
+    } alt;
+    cudaEvent_t ev_cur = nullptr;   // egress event of the current slot
+    bool cur_pending = false;
+    cudaStream_t egress = nullptr;
+    cudaEvent_t ev_ready = nullptr; // compacted records ready for copy-out
     bool oob = false;  // a stored literal may exceed num_vars (checked before testing)
     unsigned long long* ctr = nullptr;      // device [0..7]: [0..3] round counters, [4] maintenance scratch
     unsigned long long* h_ctr = nullptr;    // pinned [8]
@@ -658,6 +671,10 @@ int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     for (auto& e : h->ev) cudaEventCreate(&e);
+    cudaStreamCreateWithFlags(&h->egress, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&h->ev_cur, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&h->alt.ev, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&h->ev_ready, cudaEventDisableTiming);
     if (cudaMallocHost(&h->h_ctr, 8 * sizeof(unsigned long long)) != cudaSuccess) { delete h; return fail(TSG_ECUDA, "pinned alloc"); }
     if (dalloc(h, (void**)&h->ctr, 8 * sizeof(unsigned long long))) { delete h; return TSG_ENOMEM; }
     h->out_cap = cfg->report_capacity > 0 ? cfg->report_capacity : (1 << 16);
@@ -674,9 +691,13 @@ int tsg_destroy(tsg_engine* h) {
     dfree(h, h->d_slab_tile0);
     dfree(h, h->rows_own); dfree(h, h->prows_own); dfree(h, h->tables); dfree(h, h->d_desc); dfree(h, h->out);
     dfree(h, h->ctr); dfree(h, h->carry); dfree(h, h->out2); dfree(h, h->codes);
+    if (h->egress) cudaStreamSynchronize(h->egress);
+    dfree(h, h->alt.out); dfree(h, h->alt.out2);
     cudaStreamSynchronize(h->st);
     if (h->h_ctr) cudaFreeHost(h->h_ctr);
     for (auto& e : h->ev) if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : {h->ev_cur, h->alt.ev, h->ev_ready}) if (e) cudaEventDestroy(e);
+    if (h->egress) cudaStreamDestroy(h->egress);
     cudaStreamDestroy(h->st);
     delete h;
     return TSG_OK;
@@ -1131,6 +1152,19 @@ int tsg_round_test(tsg_engine* h, double activity_inc, tsg_round_result* out) {
     DevGuard g(h->dev);
     tsg_round_result res{};
     res.n_chunks = h->n_chunks;
+    if (h->cur_pending) {  // the last round's records are still being copied out: switch slots
+        std::swap(h->out, h->alt.out); std::swap(h->out2, h->alt.out2);
+        std::swap(h->out_cap, h->alt.out_cap); std::swap(h->out2_cap, h->alt.out2_cap);
+        std::swap(h->ev_cur, h->alt.ev);
+        h->cur_pending = false;
+        if (!h->out) {
+            h->out_cap = h->alt.out_cap;
+            CKR(dalloc(h, (void**)&h->out, h->out_cap * (int64_t)sizeof(tsg_report)));
+        }
+    }
+    // the slot about to be written may have been handed to the egress stream
+    // two rounds ago: its copy-out must finish first (no-op if never recorded)
+    CK(cudaStreamWaitEvent(h->st, h->ev_cur, 0));
     h->n_out = 0;
     h->n_alloc = 0;
     h->compacted = true;
@@ -1222,6 +1256,28 @@ int tsg_fetch_reports(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n) {
         CK(cudaStreamSynchronize(h->st));
     }
     *n = k;
+    return TSG_OK;
+}
+
+int tsg_fetch_reports_async(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n) {
+    CKR(validate_handle(h));
+    DevGuard g(h->dev);
+    CKR(compact_reports(h));
+    const int64_t k = std::min(cap, h->n_out);
+    *n = k;
+    if (k <= 0) return TSG_OK;
+    CK(cudaEventRecord(h->ev_ready, h->st));
+    CK(cudaStreamWaitEvent(h->egress, h->ev_ready, 0));
+    CK(cudaMemcpyAsync(out, h->out, k * sizeof(tsg_report), cudaMemcpyDeviceToHost, h->egress));
+    CK(cudaEventRecord(h->ev_cur, h->egress));
+    h->cur_pending = true;
+    return TSG_OK;
+}
+
+int tsg_fetch_wait(tsg_engine* h) {
+    CKR(validate_handle(h));
+    DevGuard g(h->dev);
+    CK(cudaStreamSynchronize(h->egress));
     return TSG_OK;
 }
 

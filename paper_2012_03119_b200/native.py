@@ -174,6 +174,16 @@ class NativeEngine:
             check(self.L.tsg_fetch_reports(self.h, ptr(out), n, C.byref(got)))
         return out[:got.value]
 
+    def fetch_async(self, out: np.ndarray) -> int:
+        """Start copying the round's records into `out` (pinned, REPORT_DTYPE);
+        returns the count.  Valid after wait()."""
+        got = C.c_int64(0)
+        check(self.L.tsg_fetch_reports_async(self.h, ptr(out), len(out), C.byref(got)))
+        return got.value
+
+    def wait(self) -> None:
+        check(self.L.tsg_fetch_wait(self.h))
+
     def fetch(self, n: int) -> np.ndarray:
         """Decoded records: (engine_id, group, lane_mask), unordered."""
         return reports.decode(self.fetch_raw(n))
