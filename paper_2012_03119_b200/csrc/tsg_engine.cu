@@ -160,6 +160,7 @@ struct tsg_engine {
     int64_t* d_slab_tile0 = nullptr;     // [n_slabs + 1] tile0, then [n_slabs + 1] desc0 (int32), then schedule
     int64_t slab_tile0_cap = 0;
     std::vector<uint64_t> h_sched;
+    bool desc_dirty = true;             // store changed since the tile table was built
     bool l2_persist = true;             // persisting L2 window over the round tables (TSG_L2_PERSIST=0 disables)
     const void* persist_base = nullptr;
 };
@@ -420,6 +421,7 @@ int64_t store_size(const tsg_engine* h) {
 // loads each slab's table once.  Report order does not depend on it (the
 // host orders records by engine id, reports.py).
 int build_desc(tsg_engine* h) {
+    if (!h->desc_dirty) return TSG_OK;  // store unchanged since the last round
     h->h_desc.clear();
     h->h_slab_tile0.assign(h->n_slabs + 1, 0);
     h->h_slab_desc0.assign(h->n_slabs + 1, 0);
@@ -482,7 +484,8 @@ int build_desc(tsg_engine* h) {
     if (!h->h_sched.empty())
         CK(cudaMemcpyAsync(h->d_slab_tile0 + 2 * (h->n_slabs + 1), h->h_sched.data(), h->h_sched.size() * 8,
                            cudaMemcpyHostToDevice, h->st));
-    CK(cudaStreamSynchronize(h->st));  // host vectors are rebuilt next round
+    // (pageable sources: the copies above have consumed the host vectors on return)
+    h->desc_dirty = false;
     return TSG_OK;
 }
 
@@ -706,6 +709,7 @@ int tsg_destroy(tsg_engine* h) {
 int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, int64_t n,
                     const int64_t* ids, const int32_t* origins, double activity) {
     CKR(validate_handle(h));
+    h->desc_dirty = true;
     if (n <= 0) return TSG_OK;
     if (!offsets || !ids || !origins) return fail(TSG_EINVAL, "null argument");
     DevGuard g(h->dev);
@@ -862,6 +866,7 @@ int tsg_scale_activities(tsg_engine* h, double factor) {
 
 int tsg_reduce(tsg_engine* h, int64_t eligible_below, int64_t target, int64_t* removed, int64_t* removed_ids) {
     CKR(validate_handle(h));
+    h->desc_dirty = true;
     DevGuard g(h->dev);
     *removed = 0;
     int64_t total = 0;
@@ -916,6 +921,7 @@ int tsg_reduce(tsg_engine* h, int64_t eligible_below, int64_t target, int64_t* r
 
 int tsg_remove_clauses(tsg_engine* h, const int64_t* ids, int64_t n, int64_t* removed) {
     CKR(validate_handle(h));
+    h->desc_dirty = true;
     DevGuard g(h->dev);
     *removed = 0;
     int64_t total = 0;
