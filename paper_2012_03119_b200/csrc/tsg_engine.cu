@@ -161,6 +161,7 @@ struct tsg_engine {
     int64_t slab_tile0_cap = 0;
     std::vector<uint64_t> h_sched;
     bool desc_dirty = true;             // store changed since the tile table was built
+    bool pivot = true;                  // pivot-first clause layout (TSG_PIVOT=0 disables)
     bool l2_persist = true;             // persisting L2 window over the round tables (TSG_L2_PERSIST=0 disables)
     const void* persist_base = nullptr;
 };
@@ -572,10 +573,23 @@ int32_t place_clause(tsg_engine* h, const int32_t* lits, int32_t size, std::vect
     }
     uint64_t m = 0;
     int32_t o = 0;
-    for (int32_t j = 0; j < lim; ++j) {
-        if (slab_of(h, lits[j]) == slab) {
-            m |= 1ull << j;
-            out[o++] = lits[j];
+    if (h->n_slabs == 1) {
+        // unpartitioned store: the pivot -- the literal with the smallest
+        // variable among the first 64 -- goes first; add_clauses orders each
+        // batch by pivot, so a warp's first-literal gathers share table lines
+        if (h->pivot && lim > 0) {
+            int32_t jp = 0;
+            for (int32_t j = 1; j < lim; ++j)
+                if (std::llabs((long long)lits[j]) < std::llabs((long long)lits[jp])) jp = j;
+            m = 1ull << jp;
+            out[o++] = lits[jp];
+        }
+    } else {
+        for (int32_t j = 0; j < lim; ++j) {
+            if (slab_of(h, lits[j]) == slab) {
+                m |= 1ull << j;
+                out[o++] = lits[j];
+            }
         }
     }
     for (int32_t j = 0; j < size; ++j)
@@ -642,6 +656,7 @@ int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
     h->V = num_vars;
     if (const char* e = getenv("TSG_SMEM_TABLE")) h->smem_table = atoi(e) != 0;
     if (const char* e = getenv("TSG_L2_PERSIST")) h->l2_persist = atoi(e) != 0;
+    if (const char* e = getenv("TSG_PIVOT")) h->pivot = atoi(e) != 0;
     // Variable slabs, opt-in: TSG_SLABS=1 partitions the store
     // into as many slabs as one CTA's shared memory needs for the aggregate
     // words, TSG_SLABS=n>1 into at least n.  Default: one slab (unpartitioned
@@ -753,6 +768,15 @@ int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, 
         slab_of_clause[i] = place_clause(h, lits + offsets[i], s, cnt, placed.data() + (offsets[i] - offsets[0]),
                                          &hm[i]);
         members[(size_t)bucket_of[i] * P + slab_of_clause[i]].push_back(i);
+    }
+    if (h->pivot && P == 1) {  // each part's new clauses in pivot-variable order (stable)
+        for (auto& mem : members)
+            std::stable_sort(mem.begin(), mem.end(), [&](int64_t x, int64_t y) {
+                const int64_t sx = offsets[x + 1] - offsets[x], sy = offsets[y + 1] - offsets[y];
+                const int64_t vx = sx ? std::llabs((long long)placed[offsets[x] - offsets[0]]) : 0;
+                const int64_t vy = sy ? std::llabs((long long)placed[offsets[y] - offsets[0]]) : 0;
+                return vx < vy;
+            });
     }
     for (size_t mi = 0; mi < members.size(); ++mi) {
         auto& mem = members[mi];
