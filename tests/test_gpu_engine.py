@@ -411,3 +411,40 @@ def test_async_report_egress_double_buffered(P):
         assert np.array_equal(g, w)
     a.close()
     b.close()
+
+
+def test_c3_full_size_parity(P):
+    # the benchmark's own workload (bench.py C3: 10M clauses x 1024 assignments,
+    # 200k vars, same seeds) through the benchmark's ingress path (packed rows):
+    # every record, counter and fp64 activity bit-exact against the oracle
+    import os
+    from paper_2012_03119_b200 import workload as W
+    from paper_2012_03119_b200.native import NativeEngine, pack_rows
+    cfg = W.CONFIGS["C3"]
+    rng = np.random.default_rng(cfg.seed)
+    buckets = W.clause_buckets(cfg.n_clauses, cfg.num_vars, rng, cfg.size_lo, cfg.size_hi)
+    flat, offs, ids = W.flatten(buckets)
+    snaps = W.snapshots(cfg.threads, cfg.lanes, cfg.num_vars, np.random.default_rng(cfg.seed + 999))
+    gl, gt = W.groups_for(cfg.threads, cfg.lanes)
+    dev = NativeEngine(cfg.num_vars, report_capacity=8 << 20)
+    dev.add_clauses(flat, offs, ids)
+    dev.stage_packed(pack_rows(snaps, cfg.num_vars, threads=os.cpu_count() or 1))
+    res = dev.round(gl, gt, 1.0)
+    recs = np.sort(dev.fetch(res.reports), order=["engine_id", "group"])
+    ora = O.OracleStore()
+    ora.insert_flat(flat, offs, ids)
+    del flat
+    orecs, octr = ora.test_round(cfg.num_vars, snaps, gl, gt, 32, 32, 1.0, nthreads=os.cpu_count() or 1)
+    assert res.reports == len(orecs) == len(recs) > 1_000_000
+    o = np.zeros(len(orecs), recs.dtype)
+    for f in ("engine_id", "group", "lane_mask"):
+        o[f] = orecs[f]
+    o = np.sort(o, order=["engine_id", "group"])
+    for f in ("engine_id", "group", "lane_mask"):
+        assert np.array_equal(recs[f], o[f]), f
+    for k in ("clauses_tested", "aggregate_tests", "aggregate_tests_negative", "lane_tests", "lane_triggers"):
+        assert getattr(res, k) == octr[k], k
+    for (s, lits, i1, o1, a1), (s2, n2, lits2, i2, o2, a2) in zip(dev.buckets(), ora.buckets()):
+        assert s == s2 and np.array_equal(i1, i2)
+        assert np.array_equal(a1.view(np.uint64), a2.view(np.uint64))
+    dev.close()
