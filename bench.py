@@ -272,8 +272,23 @@ def main():
                 dist.broadcast(tables_t, src=0)
         return eng.test(1.0)
 
-    for _ in range(args.warmup):
-        res = step()
+    def run_steps(n, record):
+        """n rounds.  One GPU: device rounds back to back -- round i+1 is
+        encoded (into the other table slot) before round i is collected
+        (tsg_round_launch / tsg_round_collect), so the GPU does not idle on
+        the host between rounds.  N GPUs: encode, NCCL broadcast, test."""
+        if dist is not None:
+            for _ in range(n):
+                record(step())
+            return
+        for i in range(n):
+            eng.encode()
+            if i:
+                record(eng.collect())
+            eng.launch(1.0)
+        record(eng.collect())
+
+    run_steps(args.warmup, lambda r: None)
     eng.sync()
     if dist is not None:
         dist.barrier()
@@ -286,11 +301,16 @@ def main():
     with ClockSampler(local) as clk:
         with torch.cuda.stream(stream):
             e0.record(stream)
-        for _ in range(args.steps):
-            res = step()
-            test_ms.append(res.test_ms)
-            enc_ms.append(res.encode_ms)
-            reports.append(res.reports)
+        last = []
+
+        def record(r):
+            test_ms.append(r.test_ms)
+            enc_ms.append(r.encode_ms)
+            reports.append(r.reports)
+            last[:] = [r]
+
+        run_steps(args.steps, record)
+        res = last[0]
         with torch.cuda.stream(stream):
             e1.record(stream)
         eng.sync()
@@ -346,21 +366,35 @@ def main():
             _lib.check(L.tsg_stage_packed(eng.h, C.c_void_p(h_packed_t.data_ptr()), A, pw, 0))
             return finish(eng.round(gl, gt, 1.0))
 
-        def step_pipelined():
-            # same transfers; the record copy-out of round k runs on the egress
-            # stream while round k+1's rows go in (tsg_fetch_reports_async)
-            _lib.check(L.tsg_stage_packed(eng.h, C.c_void_p(h_packed_t.data_ptr()), A, pw, 0))
-            r = eng.round(gl, gt, 1.0)
+        def fetch_async(r):
             got = C.c_int64(0)
             buf = rec_bufs[k_step[0] % 2]
             k_step[0] += 1
             _lib.check(L.tsg_fetch_reports_async(eng.h, C.c_void_p(buf.data_ptr()), min(r.reports, 8 << 20),
                                                  C.byref(got)))
+
+        def loop_pipelined(k):
+            # same transfers per round, pipelined: round i-1's records copy out
+            # on the egress stream while round i's rows go in and round i is
+            # tested (tsg_fetch_reports_async; measured faster than also
+            # overlapping the encode via tsg_round_launch/collect, which queues
+            # the copy-out behind the next round's rows)
+            r = None
+            for _ in range(k):
+                _lib.check(L.tsg_stage_packed(eng.h, C.c_void_p(h_packed_t.data_ptr()), A, pw, 0))
+                r = eng.round(gl, gt, 1.0)
+                fetch_async(r)
             return r
 
-        def step_int8():
-            _lib.check(L.tsg_stage_snapshots(eng.h, C.c_void_p(h_int8_t.data_ptr()), A, cfg.num_vars + 1, 0))
-            return finish(eng.round(gl, gt, 1.0))
+        def timed_loop(fn, k):
+            fn(2)
+            eng.sync()
+            _lib.check(L.tsg_fetch_wait(eng.h))
+            w0 = time.perf_counter()
+            r = fn(k)
+            eng.sync()
+            _lib.check(L.tsg_fetch_wait(eng.h))
+            return (time.perf_counter() - w0) / k * 1e3, r, r.reports * 16 + 32
 
         def timed(fn, k):
             for _ in range(2):
@@ -381,13 +415,14 @@ def main():
         for _ in range(3):
             pack_rows(snaps, cfg.num_vars, out=h_packed, threads=host_threads)
         pack_ms = (time.perf_counter() - p0) / 3 * 1e3
-        ms, r, d2h = timed(step_pipelined, e2e_steps)
+        ms, r, d2h = timed_loop(loop_pipelined, e2e_steps)
         ms_seq, _, _ = timed(step_packed, max(3, e2e_steps // 2))
         ms8, r8, _ = timed(step_int8, max(3, e2e_steps // 2))
         e2e = {"value": r.lane_tests / (ms * 1e-3), "unit": "clause_assignment_tests/s",
                "h2d_bytes_per_step": int(A * pw * 8), "d2h_bytes_per_step": int(d2h), "ms_per_step": ms,
                "input": "packed 2-bit snapshot rows in pinned host memory (solver-side ingress format)",
-               "egress": "report copy-out of round k overlapped with round k+1 (tsg_fetch_reports_async)",
+               "pipeline": "round i-1's records copy out on the egress stream while round i's rows go in "
+                           "and round i is tested",
                "sequential_ms_per_step": ms_seq,
                "host_pack_ms_per_round": pack_ms, "host_pack_threads": host_threads,
                "int8_rows": {"value": r8.lane_tests / (ms8 * 1e-3), "ms_per_step": ms8,

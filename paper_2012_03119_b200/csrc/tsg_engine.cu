@@ -88,6 +88,16 @@ struct Bucket {
 
 }  // namespace
 
+// The group description of one round (tsg_round_prepare), kept per round
+// so a launched round can be collected -- and its report emission replayed --
+// after the next round has been prepared and encoded.
+struct RoundDesc {
+    int32_t n_groups = 0, n_chunks = 0;
+    std::vector<int32_t> glanes, gtid;
+    std::vector<int64_t> grow0;
+    std::vector<int64_t> chunk_off;  // byte offset of each chunk's tables within a table slot
+};
+
 struct tsg_engine {
     int dev = 0;
     int nsm = 148;
@@ -107,13 +117,20 @@ struct tsg_engine {
     uint64_t* prows_own = nullptr;
     int64_t prows_cap = 0, ppitch = 0;
 
-    // round description
-    int32_t n_groups = 0, n_chunks = 0;
-    std::vector<int32_t> glanes, gtid;
-    std::vector<int64_t> grow0;
-    std::vector<int64_t> chunk_off;  // byte offset of each chunk's tables
+    // round description: `rd` as prepared, `fl` of the launched round
+    RoundDesc rd, fl;
+    // round tables: two slots of tables_bytes each (slot stride slot_bytes);
+    // encode writes slot `tslot`; tsg_round_launch flips it, so the next
+    // round encodes while the launched one still owns its tables
     int8_t* tables = nullptr;
-    int64_t tables_cap = 0, tables_bytes = 0;
+    int64_t tables_cap = 0, tables_bytes = 0, slot_bytes = 0;
+    int tslot = 0;
+    bool inflight = false;       // launched, not collected
+    int fl_slot = 0;
+    double fl_inc = 0.0;
+    cudaEvent_t ev_done = nullptr;        // counters of the launched round are on the host
+    cudaEvent_t ev_enc[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // per table slot: encode start/end
+    cudaEvent_t ev_tst[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // per table slot: test start/end
 
     BucketDesc* d_desc = nullptr;
     int64_t desc_cap = 0;
@@ -162,7 +179,7 @@ struct tsg_engine {
     std::vector<uint64_t> h_sched;
     bool desc_dirty = true;             // store changed since the tile table was built
     bool pivot = true;                  // pivot-first clause layout (TSG_PIVOT=0 disables)
-    bool l2_persist = true;             // persisting L2 window over the round tables (TSG_L2_PERSIST=0 disables)
+    bool l2_persist = false;            // persisting L2 window over the round tables (TSG_L2_PERSIST=1; measured slower)
     const void* persist_base = nullptr;
 };
 
@@ -263,17 +280,19 @@ int64_t lane_entry_bytes(const tsg_engine* h) { return wide_lane(h) ? 16 : 8; }
 template <class LW, class GW>
 int launch_encode(tsg_engine* h, int c) {
     EncodeChunk ec{};
+    const RoundDesc& rd = h->rd;
     int32_t g0 = c * h->cfg.group_width;
-    ec.G = std::min(h->cfg.group_width, h->n_groups - g0);
+    ec.G = std::min(h->cfg.group_width, rd.n_groups - g0);
     ec.num_vars = h->V;
     ec.pitch = h->pitch;
     ec.vstride = vstride(h);
     for (int g = 0; g < ec.G; ++g) {
-        ec.row0[g] = h->grow0[g0 + g];
-        ec.lanes[g] = h->glanes[g0 + g];
+        ec.row0[g] = rd.grow0[g0 + g];
+        ec.lanes[g] = rd.glanes[g0 + g];
     }
-    auto* agg = reinterpret_cast<AggEntry<GW>*>(h->tables + h->chunk_off[c]);
-    auto* lane = reinterpret_cast<LaneEntry<LW>*>(h->tables + h->chunk_off[c] + agg_bytes(h));
+    int8_t* tab = h->tables + h->tslot * h->slot_bytes;
+    auto* agg = reinterpret_cast<AggEntry<GW>*>(tab + rd.chunk_off[c]);
+    auto* lane = reinterpret_cast<LaneEntry<LW>*>(tab + rd.chunk_off[c] + agg_bytes(h));
     dim3 grid((unsigned)((h->V + 2 + 127) / 128)), block(32, 8);
     if (h->packed) {
         EncodePackedChunk pc{};
@@ -294,7 +313,7 @@ int launch_encode(tsg_engine* h, int c) {
 int64_t packed_words(int32_t V) { return round_up(((int64_t)V + 2 + 31) / 32, 4); }
 
 int do_encode(tsg_engine* h) {
-    for (int c = 0; c < h->n_chunks; ++c) {
+    for (int c = 0; c < h->rd.n_chunks; ++c) {
         int r;
         if (wide_lane(h)) r = wide_group(h) ? launch_encode<uint64_t, uint64_t>(h, c) : launch_encode<uint64_t, uint32_t>(h, c);
         else r = wide_group(h) ? launch_encode<uint32_t, uint64_t>(h, c) : launch_encode<uint32_t, uint32_t>(h, c);
@@ -343,16 +362,17 @@ int launch_slab(tsg_engine* h, const TestParams<LW, GW>& p) {
 }
 
 template <class LW, class GW>
-int launch_test(tsg_engine* h, int c, double inc, int emit_only) {
+int launch_test(tsg_engine* h, const RoundDesc& rd, int slot, int c, double inc, int emit_only) {
     TestParams<LW, GW> p{};
     int32_t g0 = c * h->cfg.group_width;
-    int32_t G = std::min(h->cfg.group_width, h->n_groups - g0);
+    int32_t G = std::min(h->cfg.group_width, rd.n_groups - g0);
+    const int8_t* tab = h->tables + slot * h->slot_bytes;
     p.buckets = h->d_desc;
     p.nb = (int32_t)h->h_desc.size();
     p.G = G;
     p.n_tiles = h->n_tiles;
-    p.agg = reinterpret_cast<const AggEntry<GW>*>(h->tables + h->chunk_off[c]);
-    p.lane = reinterpret_cast<const LaneEntry<LW>*>(h->tables + h->chunk_off[c] + agg_bytes(h));
+    p.agg = reinterpret_cast<const AggEntry<GW>*>(tab + rd.chunk_off[c]);
+    p.lane = reinterpret_cast<const LaneEntry<LW>*>(tab + rd.chunk_off[c] + agg_bytes(h));
     p.vstride = vstride(h);
     p.sentinel = h->V + 1;
     p.g0 = g0;
@@ -363,8 +383,8 @@ int launch_test(tsg_engine* h, int c, double inc, int emit_only) {
     p.out_cap = h->out_cap;
     p.carry = h->carry;
     p.stamp_base = (h->round_seq & 0x7fffffff) << 32;
-    p.carry_in_tid = (c > 0 && h->gtid[g0] == h->gtid[g0 - 1]) ? h->gtid[g0] : -1;
-    p.carry_out_tid = (g0 + G < h->n_groups && h->gtid[g0 + G - 1] == h->gtid[g0 + G]) ? h->gtid[g0 + G - 1] : -1;
+    p.carry_in_tid = (c > 0 && rd.gtid[g0] == rd.gtid[g0 - 1]) ? rd.gtid[g0] : -1;
+    p.carry_out_tid = (g0 + G < rd.n_groups && rd.gtid[g0 + G - 1] == rd.gtid[g0 + G]) ? rd.gtid[g0 + G - 1] : -1;
     p.emit_only = emit_only;
     p.slab_tile0 = h->d_slab_tile0;
     p.slab_desc0 = reinterpret_cast<const int32_t*>(h->d_slab_tile0 + (h->n_slabs + 1));
@@ -372,8 +392,8 @@ int launch_test(tsg_engine* h, int c, double inc, int emit_only) {
     p.n_sched = (int32_t)h->h_sched.size();
     p.slab_w = h->slab_w;
     for (int g = 0; g < G; ++g) {
-        p.tid[g] = h->gtid[g0 + g];
-        p.lane_mask[g] = width_mask<LW>(h->glanes[g0 + g]);
+        p.tid[g] = rd.gtid[g0 + g];
+        p.lane_mask[g] = width_mask<LW>(rd.glanes[g0 + g]);
     }
     if (h->n_tiles == 0) return TSG_OK;
     // shared-memory literal-code table when 2 * (V + 2) codes fit (G <= 32)
@@ -401,11 +421,11 @@ int launch_test(tsg_engine* h, int c, double inc, int emit_only) {
     return launch_kernel<LW, GW, GlobalTable<GW>, TEST_THREADS, TSG_TEST_MIN_BLOCKS>(h, p, 0, 0);
 }
 
-int run_tests(tsg_engine* h, double inc, int emit_only) {
-    for (int c = 0; c < h->n_chunks; ++c) {
+int run_tests(tsg_engine* h, const RoundDesc& rd, int slot, double inc, int emit_only) {
+    for (int c = 0; c < rd.n_chunks; ++c) {
         int r;
-        if (wide_lane(h)) r = wide_group(h) ? launch_test<uint64_t, uint64_t>(h, c, inc, emit_only) : launch_test<uint64_t, uint32_t>(h, c, inc, emit_only);
-        else r = wide_group(h) ? launch_test<uint32_t, uint64_t>(h, c, inc, emit_only) : launch_test<uint32_t, uint32_t>(h, c, inc, emit_only);
+        if (wide_lane(h)) r = wide_group(h) ? launch_test<uint64_t, uint64_t>(h, rd, slot, c, inc, emit_only) : launch_test<uint64_t, uint32_t>(h, rd, slot, c, inc, emit_only);
+        else r = wide_group(h) ? launch_test<uint32_t, uint64_t>(h, rd, slot, c, inc, emit_only) : launch_test<uint32_t, uint32_t>(h, rd, slot, c, inc, emit_only);
         if (r) return r;
     }
     return TSG_OK;
@@ -693,6 +713,9 @@ int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
     cudaEventCreateWithFlags(&h->ev_cur, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&h->alt.ev, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&h->ev_ready, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&h->ev_done, cudaEventDisableTiming);
+    for (int sl = 0; sl < 2; ++sl)
+        for (int k = 0; k < 2; ++k) { cudaEventCreate(&h->ev_enc[sl][k]); cudaEventCreate(&h->ev_tst[sl][k]); }
     if (cudaMallocHost(&h->h_ctr, 8 * sizeof(unsigned long long)) != cudaSuccess) { delete h; return fail(TSG_ECUDA, "pinned alloc"); }
     if (dalloc(h, (void**)&h->ctr, 8 * sizeof(unsigned long long))) { delete h; return TSG_ENOMEM; }
     h->out_cap = cfg->report_capacity > 0 ? cfg->report_capacity : (1 << 16);
@@ -714,7 +737,12 @@ int tsg_destroy(tsg_engine* h) {
     cudaStreamSynchronize(h->st);
     if (h->h_ctr) cudaFreeHost(h->h_ctr);
     for (auto& e : h->ev) if (e) cudaEventDestroy(e);
-    for (cudaEvent_t e : {h->ev_cur, h->alt.ev, h->ev_ready}) if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : {h->ev_cur, h->alt.ev, h->ev_ready, h->ev_done}) if (e) cudaEventDestroy(e);
+    for (int sl = 0; sl < 2; ++sl)
+        for (int k = 0; k < 2; ++k) {
+            if (h->ev_enc[sl][k]) cudaEventDestroy(h->ev_enc[sl][k]);
+            if (h->ev_tst[sl][k]) cudaEventDestroy(h->ev_tst[sl][k]);
+        }
     if (h->egress) cudaStreamDestroy(h->egress);
     cudaStreamDestroy(h->st);
     delete h;
@@ -724,6 +752,7 @@ int tsg_destroy(tsg_engine* h) {
 int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, int64_t n,
                     const int64_t* ids, const int32_t* origins, double activity) {
     CKR(validate_handle(h));
+    if (h->inflight) return fail(TSG_EINVAL, "the store cannot change while a launched round is not collected");
     h->desc_dirty = true;
     if (n <= 0) return TSG_OK;
     if (!offsets || !ids || !origins) return fail(TSG_EINVAL, "null argument");
@@ -880,6 +909,7 @@ int tsg_bucket_read(tsg_engine* h, int32_t bi, int32_t* lits, int64_t* ids, int3
 
 int tsg_scale_activities(tsg_engine* h, double factor) {
     CKR(validate_handle(h));
+    if (h->inflight) return fail(TSG_EINVAL, "the store cannot change while a launched round is not collected");
     DevGuard g(h->dev);
     for_parts(h, [&](Bucket&, Part& p) {
         if (p.count) k_scale_f64<<<grid_for(p.count), 256, 0, h->st>>>(p.acts, p.count, factor);
@@ -890,6 +920,7 @@ int tsg_scale_activities(tsg_engine* h, double factor) {
 
 int tsg_reduce(tsg_engine* h, int64_t eligible_below, int64_t target, int64_t* removed, int64_t* removed_ids) {
     CKR(validate_handle(h));
+    if (h->inflight) return fail(TSG_EINVAL, "the store cannot change while a launched round is not collected");
     h->desc_dirty = true;
     DevGuard g(h->dev);
     *removed = 0;
@@ -945,6 +976,7 @@ int tsg_reduce(tsg_engine* h, int64_t eligible_below, int64_t target, int64_t* r
 
 int tsg_remove_clauses(tsg_engine* h, const int64_t* ids, int64_t n, int64_t* removed) {
     CKR(validate_handle(h));
+    if (h->inflight) return fail(TSG_EINVAL, "the store cannot change while a launched round is not collected");
     h->desc_dirty = true;
     DevGuard g(h->dev);
     *removed = 0;
@@ -1096,93 +1128,86 @@ int tsg_stage_packed(tsg_engine* h, const uint64_t* rows, int64_t n_rows, int64_
     return TSG_OK;
 }
 
+void persist_tables(tsg_engine* h);
+
 int tsg_round_prepare(tsg_engine* h, const int32_t* group_lanes, const int32_t* group_tid, int32_t n_groups) {
     CKR(validate_handle(h));
     DevGuard g(h->dev);
     if (n_groups < 0 || n_groups > TSG_MAX_GROUPS)
         return fail(TSG_EINVAL, "n_groups must be in 0..%d, got %d", TSG_MAX_GROUPS, n_groups);
-    h->n_groups = n_groups;
-    h->glanes.assign(group_lanes, group_lanes + n_groups);
-    h->gtid.assign(group_tid, group_tid + n_groups);
-    h->grow0.resize(n_groups);
+    RoundDesc rd;
+    rd.n_groups = n_groups;
+    rd.glanes.assign(group_lanes, group_lanes + n_groups);
+    rd.gtid.assign(group_tid, group_tid + n_groups);
+    rd.grow0.resize(n_groups);
     int64_t r = 0;
     for (int i = 0; i < n_groups; ++i) {
-        if (h->glanes[i] < 0 || h->glanes[i] > h->cfg.lane_width)
-            return fail(TSG_ECAPACITY, "%d assignments exceed lane width %d", h->glanes[i], h->cfg.lane_width);
-        h->grow0[i] = r;
-        r += h->glanes[i];
+        if (rd.glanes[i] < 0 || rd.glanes[i] > h->cfg.lane_width)
+            return fail(TSG_ECAPACITY, "%d assignments exceed lane width %d", rd.glanes[i], h->cfg.lane_width);
+        rd.grow0[i] = r;
+        r += rd.glanes[i];
     }
-    h->n_chunks = (n_groups + h->cfg.group_width - 1) / h->cfg.group_width;
-    h->chunk_off.resize(h->n_chunks);
+    rd.n_chunks = (n_groups + h->cfg.group_width - 1) / h->cfg.group_width;
+    rd.chunk_off.resize(rd.n_chunks);
     int64_t off = 0;
-    for (int c = 0; c < h->n_chunks; ++c) {
+    for (int c = 0; c < rd.n_chunks; ++c) {
         int G = std::min(h->cfg.group_width, n_groups - c * h->cfg.group_width);
-        h->chunk_off[c] = off;
+        rd.chunk_off[c] = off;
         off += agg_bytes(h);
         off += round_up(vstride(h) * G * lane_entry_bytes(h), 256);
     }
-    h->tables_bytes = off;
-    if (off > h->tables_cap) {
+    // table slots never shrink and hold at least one full chunk, so rounds of
+    // up to group_width groups can be prepared while another is in flight
+    const int64_t one_chunk = agg_bytes(h) + round_up(vstride(h) * h->cfg.group_width * lane_entry_bytes(h), 256);
+    const int64_t slot = std::max(h->slot_bytes, round_up(std::max(off, one_chunk), 4096));
+    if (slot != h->slot_bytes) {
+        if (h->inflight) return fail(TSG_EINVAL, "collect the launched round before preparing a larger one");
         dfree(h, h->tables);
         h->tables = nullptr;
-        CKR(dalloc(h, (void**)&h->tables, off));
-        h->tables_cap = off;
+        CKR(dalloc(h, (void**)&h->tables, 2 * slot));
+        h->tables_cap = 2 * slot;
+        h->slot_bytes = slot;
+        h->persist_base = nullptr;
     }
-    if (h->l2_persist && off > 0 && h->persist_base != h->tables) {
-        // keep the round tables L2-resident while the clause stream and the
-        // report records flow through (access-policy window, persisting hits)
-        int max_persist = 0, max_window = 0;
-        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, h->dev);
-        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, h->dev);
-        const size_t win = (size_t)std::min<int64_t>(off, max_window);
-        // best effort: another context may hold the device-wide persisting
-        // carve-out; then the round runs without the window
-        if (max_persist > 0 && win > 0 &&
-            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(win, (size_t)max_persist)) != cudaSuccess) {
-            cudaGetLastError();
-            max_persist = 0;
-        }
-        if (max_persist > 0 && win > 0) {
-            cudaStreamAttrValue attr{};
-            attr.accessPolicyWindow.base_ptr = h->tables;
-            attr.accessPolicyWindow.num_bytes = win;
-            attr.accessPolicyWindow.hitRatio = std::min(1.0f, (float)max_persist / (float)win);
-            attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-            attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-            if (cudaStreamSetAttribute(h->st, cudaStreamAttributeAccessPolicyWindow, &attr) != cudaSuccess)
-                cudaGetLastError();
-            h->persist_base = h->tables;
-        }
+    h->tables_bytes = off;
+    h->rd = std::move(rd);
+    persist_tables(h);
+    return TSG_OK;
+}
+
+// Persisting L2 window over both table slots, so the 640 MB clause stream
+// and the report records cannot evict the tables.  Set once per table
+// allocation: changing the device-wide persisting limit stalls the device,
+// so it must stay off the per-round path.  Best effort: another context may
+// hold the device-wide persisting carve-out.
+void persist_tables(tsg_engine* h) {
+    const void* base = h->tables;
+    if (!h->l2_persist || h->tables_bytes <= 0 || h->persist_base == base) return;
+    h->persist_base = base;
+    int max_persist = 0, max_window = 0;
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, h->dev);
+    cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, h->dev);
+    const size_t win = (size_t)std::min<int64_t>(h->slot_bytes + h->tables_bytes, max_window);
+    if (max_persist <= 0 || win == 0 ||
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(win, (size_t)max_persist)) != cudaSuccess) {
+        cudaGetLastError();
+        return;
     }
-    return TSG_OK;
+    cudaStreamAttrValue attr{};
+    attr.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+    attr.accessPolicyWindow.num_bytes = win;
+    attr.accessPolicyWindow.hitRatio = std::min(1.0f, (float)max_persist / (float)win);
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    if (cudaStreamSetAttribute(h->st, cudaStreamAttributeAccessPolicyWindow, &attr) != cudaSuccess)
+        cudaGetLastError();
 }
 
-int tsg_round_encode(tsg_engine* h) {
-    CKR(validate_handle(h));
-    DevGuard g(h->dev);
-    int64_t need_rows = h->n_groups ? h->grow0.back() + h->glanes.back() : 0;
-    if (need_rows > h->n_rows) return fail(TSG_EINVAL, "groups need %lld rows, %lld staged", (long long)need_rows, (long long)h->n_rows);
-    if (!h->n_chunks) return TSG_OK;
-    bool timing = h->cfg.flags & TSG_F_TIMING;
-    if (timing) CK(cudaEventRecord(h->ev[0], h->st));
-    CKR(do_encode(h));
-    if (timing) CK(cudaEventRecord(h->ev[1], h->st));
-    return TSG_OK;
-}
-
-int tsg_round_tables(tsg_engine* h, void** device_ptr, int64_t* bytes) {
-    CKR(validate_handle(h));
-    *device_ptr = h->tables;
-    *bytes = h->tables_bytes;
-    return TSG_OK;
-}
-
-int tsg_round_test(tsg_engine* h, double activity_inc, tsg_round_result* out) {
-    CKR(validate_handle(h));
-    DevGuard g(h->dev);
-    tsg_round_result res{};
-    res.n_chunks = h->n_chunks;
-    if (h->cur_pending) {  // the last round's records are still being copied out: switch slots
+// Launch the test of the prepared, encoded round (table slot h->tslot): the
+// kernels and the counter copy-out are queued, nothing waits.
+int round_launch(tsg_engine* h, double inc, bool flip) {
+    if (h->inflight) return fail(TSG_EINVAL, "a launched round has not been collected");
+    if (h->cur_pending) {  // the last round's records are still being copied out: switch record slots
         std::swap(h->out, h->alt.out); std::swap(h->out2, h->alt.out2);
         std::swap(h->out_cap, h->alt.out_cap); std::swap(h->out2_cap, h->alt.out2_cap);
         std::swap(h->ev_cur, h->alt.ev);
@@ -1192,14 +1217,17 @@ int tsg_round_test(tsg_engine* h, double activity_inc, tsg_round_result* out) {
             CKR(dalloc(h, (void**)&h->out, h->out_cap * (int64_t)sizeof(tsg_report)));
         }
     }
-    // the slot about to be written may have been handed to the egress stream
-    // two rounds ago: its copy-out must finish first (no-op if never recorded)
+    // the record slot about to be written may have been handed to the egress
+    // stream two rounds ago: its copy-out must finish first (no-op if never recorded)
     CK(cudaStreamWaitEvent(h->st, h->ev_cur, 0));
     h->n_out = 0;
     h->n_alloc = 0;
     h->compacted = true;
     h->round_seq++;
-    if (h->n_chunks && h->oob) {  // out-of-range literal stored: numpy would raise IndexError
+    h->fl = h->rd;
+    h->fl_slot = h->tslot;
+    h->fl_inc = inc;
+    if (h->fl.n_chunks && h->oob) {  // out-of-range literal stored: numpy would raise IndexError
         CK(cudaMemsetAsync(h->ctr + 4, 0, 8, h->st));
         for_parts(h, [&](Bucket& b, Part& p) {
             if (p.count && b.size)
@@ -1212,30 +1240,46 @@ int tsg_round_test(tsg_engine* h, double activity_inc, tsg_round_result* out) {
             return fail(TSG_ERANGE, "index %lld is out of bounds for axis 0 with size %d", (long long)h->h_ctr[4], h->V + 1);
         h->oob = false;
     }
-    if (h->n_chunks) {
+    if (h->fl.n_chunks) {
         CKR(build_desc(h));
-        if (h->n_chunks > 1) CKR(dgrow(h, &h->carry, &h->carry_cap, std::max<int64_t>(1, h->n_tiles * STRIDE)));
+        if (h->fl.n_chunks > 1) CKR(dgrow(h, &h->carry, &h->carry_cap, std::max<int64_t>(1, h->n_tiles * STRIDE)));
         CK(cudaMemsetAsync(h->ctr, 0, 4 * sizeof(unsigned long long), h->st));
-        bool timing = h->cfg.flags & TSG_F_TIMING;
-        if (timing) CK(cudaEventRecord(h->ev[2], h->st));
-        CKR(run_tests(h, activity_inc, 0));
-        if (timing) CK(cudaEventRecord(h->ev[3], h->st));
+        const bool timing = h->cfg.flags & TSG_F_TIMING;
+        if (timing) CK(cudaEventRecord(h->ev_tst[h->fl_slot][0], h->st));
+        CKR(run_tests(h, h->fl, h->fl_slot, inc, 0));
+        if (timing) CK(cudaEventRecord(h->ev_tst[h->fl_slot][1], h->st));
         CK(cudaMemcpyAsync(h->h_ctr, h->ctr, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
-        CK(cudaStreamSynchronize(h->st));
+        CK(cudaEventRecord(h->ev_done, h->st));
+    }
+    h->inflight = true;
+    if (flip) h->tslot ^= 1;
+    return TSG_OK;
+}
+
+// Wait for the launched round's counters; grow the record buffer and replay
+// emission if it overflowed; fill the round's figures.
+int round_collect(tsg_engine* h, tsg_round_result* out) {
+    if (!h->inflight) return fail(TSG_EINVAL, "no launched round to collect");
+    h->inflight = false;
+    const RoundDesc& rd = h->fl;
+    tsg_round_result res{};
+    res.n_chunks = rd.n_chunks;
+    if (rd.n_chunks) {
+        CK(cudaEventSynchronize(h->ev_done));
         int64_t n_slots = (int64_t)h->h_ctr[0];
         int64_t positives = (int64_t)h->h_ctr[1];
         res.lane_triggers = (int64_t)h->h_ctr[2];
         int64_t n_rec = (int64_t)h->h_ctr[3];
         // overflow: grow, replay emission only (no activity / counter side
-        // effects).  Slot reservation depends on which warp tests which tile
-        // (dynamic in the slab kernel), so a replay may need a different count.
+        // effects) from the round's own table slot.  Slot reservation depends
+        // on which warp tests which tile, so a replay may need a different count.
         while (n_slots > h->out_cap) {
             dfree(h, h->out);
             h->out = nullptr;
             h->out_cap = n_slots + n_slots / 4 + 1024 + (int64_t)h->nsm * 64 * (int64_t)REPORT_CHUNK;
             CKR(dalloc(h, (void**)&h->out, h->out_cap * (int64_t)sizeof(tsg_report)));
             CK(cudaMemsetAsync(h->ctr, 0, 4 * sizeof(unsigned long long), h->st));
-            CKR(run_tests(h, activity_inc, 1));
+            CKR(run_tests(h, rd, h->fl_slot, h->fl_inc, 1));
             CK(cudaMemcpyAsync(h->h_ctr, h->ctr, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
             CK(cudaStreamSynchronize(h->st));
             if ((int64_t)h->h_ctr[3] != n_rec) return fail(TSG_ECUDA, "report replay mismatch");
@@ -1247,26 +1291,67 @@ int tsg_round_test(tsg_engine* h, double activity_inc, tsg_round_result* out) {
         h->compacted = n_slots == n_rec;
         int64_t n = store_size(h);
         int64_t lanes_total = 0;
-        for (int c = 0; c < h->n_chunks; ++c) {
+        for (int c = 0; c < rd.n_chunks; ++c) {
             int32_t g0 = c * h->cfg.group_width;
-            int G = std::min(h->cfg.group_width, h->n_groups - g0);
+            int G = std::min(h->cfg.group_width, rd.n_groups - g0);
             int64_t lanes = 0;
-            for (int gg = 0; gg < G; ++gg) lanes += h->glanes[g0 + gg];
+            for (int gg = 0; gg < G; ++gg) lanes += rd.glanes[g0 + gg];
             res.aggregate_tests += n * G;
             lanes_total += lanes;
         }
-        res.clauses_tested = n * h->n_chunks;
+        res.clauses_tested = n * rd.n_chunks;
         res.lane_tests = n * lanes_total;
         res.aggregate_tests_negative = res.aggregate_tests - positives;
         res.reports = n_rec;
-        if (timing) {
+        if (h->cfg.flags & TSG_F_TIMING) {
             float ms = 0;
-            if (cudaEventElapsedTime(&ms, h->ev[0], h->ev[1]) == cudaSuccess) res.encode_ms = ms;
-            if (cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]) == cudaSuccess) res.test_ms = ms;
+            if (cudaEventElapsedTime(&ms, h->ev_enc[h->fl_slot][0], h->ev_enc[h->fl_slot][1]) == cudaSuccess) res.encode_ms = ms;
+            else cudaGetLastError();
+            if (cudaEventElapsedTime(&ms, h->ev_tst[h->fl_slot][0], h->ev_tst[h->fl_slot][1]) == cudaSuccess) res.test_ms = ms;
+            else cudaGetLastError();
         }
     }
     if (out) *out = res;
     return TSG_OK;
+}
+
+int tsg_round_encode(tsg_engine* h) {
+    CKR(validate_handle(h));
+    DevGuard g(h->dev);
+    int64_t need_rows = h->rd.n_groups ? h->rd.grow0.back() + h->rd.glanes.back() : 0;
+    if (need_rows > h->n_rows) return fail(TSG_EINVAL, "groups need %lld rows, %lld staged", (long long)need_rows, (long long)h->n_rows);
+    if (!h->rd.n_chunks) return TSG_OK;
+    const bool timing = h->cfg.flags & TSG_F_TIMING;
+    if (timing) CK(cudaEventRecord(h->ev_enc[h->tslot][0], h->st));
+    CKR(do_encode(h));
+    if (timing) CK(cudaEventRecord(h->ev_enc[h->tslot][1], h->st));
+    return TSG_OK;
+}
+
+int tsg_round_tables(tsg_engine* h, void** device_ptr, int64_t* bytes) {
+    CKR(validate_handle(h));
+    *device_ptr = h->tables + h->tslot * h->slot_bytes;
+    *bytes = h->tables_bytes;
+    return TSG_OK;
+}
+
+int tsg_round_test(tsg_engine* h, double activity_inc, tsg_round_result* out) {
+    CKR(validate_handle(h));
+    DevGuard g(h->dev);
+    CKR(round_launch(h, activity_inc, false));
+    return round_collect(h, out);
+}
+
+int tsg_round_launch(tsg_engine* h, double activity_inc) {
+    CKR(validate_handle(h));
+    DevGuard g(h->dev);
+    return round_launch(h, activity_inc, true);
+}
+
+int tsg_round_collect(tsg_engine* h, tsg_round_result* out) {
+    CKR(validate_handle(h));
+    DevGuard g(h->dev);
+    return round_collect(h, out);
 }
 
 int tsg_round(tsg_engine* h, const int32_t* group_lanes, const int32_t* group_tid, int32_t n_groups,

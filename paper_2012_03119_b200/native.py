@@ -158,6 +158,16 @@ class NativeEngine:
         check(self.L.tsg_round_test(self.h, activity_inc, C.byref(res)))
         return res
 
+    def launch(self, activity_inc: float = 1.0) -> None:
+        """Queue the test of the prepared, encoded round (tsg_round_launch)."""
+        check(self.L.tsg_round_launch(self.h, activity_inc))
+
+    def collect(self) -> _lib.tsg_round_result:
+        """Figures of the launched round (tsg_round_collect)."""
+        res = _lib.tsg_round_result()
+        check(self.L.tsg_round_collect(self.h, C.byref(res)))
+        return res
+
     def round(self, group_lanes, group_tid, activity_inc: float = 1.0) -> _lib.tsg_round_result:
         gl = np.ascontiguousarray(group_lanes, np.int32)
         gt = np.ascontiguousarray(group_tid, np.int32)

@@ -448,3 +448,53 @@ def test_c3_full_size_parity(P):
         assert s == s2 and np.array_equal(i1, i2)
         assert np.array_equal(a1.view(np.uint64), a2.view(np.uint64))
     dev.close()
+
+
+@pytest.mark.parametrize("cap", [1 << 20, 64])  # 64: every round overflows and replays after the next encode
+def test_async_rounds_match_sync_rounds(P, cap):
+    # launch(k); stage/prepare/encode(k+1); collect(k): identical figures,
+    # records and activities to synchronous rounds, overflow replays included
+    from paper_2012_03119_b200 import workload as W
+    from paper_2012_03119_b200.native import NativeEngine, pack_rows
+    rng = np.random.default_rng(17)
+    nv = 2000
+    buckets = W.clause_buckets(30_000, nv, rng, 1, 9)
+    flat, offs, ids = W.flatten(buckets)
+    rounds = []
+    for k in range(5):
+        threads = 2 + k % 3
+        snaps = W.snapshots(threads, 32, nv, rng)
+        rounds.append((snaps, *W.groups_for(threads, 32)))
+    a, b = NativeEngine(nv, report_capacity=cap), NativeEngine(nv)
+    a.add_clauses(flat, offs, ids)
+    b.add_clauses(flat, offs, ids)
+    fields = ("reports", "clauses_tested", "aggregate_tests", "aggregate_tests_negative", "lane_tests",
+              "lane_triggers")
+    want = []
+    for k, (snaps, gl, gt) in enumerate(rounds):
+        b.stage(snaps)
+        r = b.round(gl, gt, 1.0 + k)
+        want.append(([getattr(r, f) for f in fields], np.sort(b.fetch(r.reports), order=["engine_id", "group"])))
+    got = []
+    for k, (snaps, gl, gt) in enumerate(rounds):
+        a.stage_packed(pack_rows(snaps, nv))
+        a.prepare(gl, gt)
+        a.encode()
+        if k:
+            r = a.collect()
+            got.append(([getattr(r, f) for f in fields], np.sort(a.fetch(r.reports), order=["engine_id", "group"])))
+        a.launch(1.0 + k)
+    r = a.collect()
+    got.append(([getattr(r, f) for f in fields], np.sort(a.fetch(r.reports), order=["engine_id", "group"])))
+    for (gf, gr), (wf, wr) in zip(got, want):
+        assert gf == wf
+        assert np.array_equal(gr, wr)
+    for x, y in zip(a.buckets(), b.buckets()):
+        assert np.array_equal(x[4].view(np.uint64), y[4].view(np.uint64))
+    with pytest.raises(ValueError):  # one launched round at a time
+        a.prepare(*rounds[0][1:])
+        a.encode()
+        a.launch(1.0)
+        a.launch(1.0)
+    a.close()
+    b.close()

@@ -1,2 +1,3 @@
-timeout 900 python -m pytest tests/test_gpu_engine.py -m gpu -x -q --timeout 600 -k "full_size" -p no:cacheprovider --durations=3 > gpurun_out/pytest_gpu.log 2>&1
-tail -6 gpurun_out/pytest_gpu.log
+timeout 700 python -m pytest tests -m gpu -x -q --timeout 300 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
+tail -2 gpurun_out/pytest_gpu.log
+timeout 400 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.log 2>&1; tail -1 gpurun_out/bench.log
