@@ -386,6 +386,10 @@ def main():
                 fetch_async(r)
             return r
 
+        def step_int8():
+            _lib.check(L.tsg_stage_snapshots(eng.h, C.c_void_p(h_int8_t.data_ptr()), A, cfg.num_vars + 1, 0))
+            return finish(eng.round(gl, gt, 1.0))
+
         def timed_loop(fn, k):
             fn(2)
             eng.sync()
@@ -410,23 +414,32 @@ def main():
             _lib.check(L.tsg_fetch_wait(eng.h))
             return (time.perf_counter() - w0) / k * 1e3, r, d2h // k
 
-        pack_rows(snaps, cfg.num_vars, out=h_packed, threads=host_threads)
-        p0 = time.perf_counter()
-        for _ in range(3):
+        try:
             pack_rows(snaps, cfg.num_vars, out=h_packed, threads=host_threads)
-        pack_ms = (time.perf_counter() - p0) / 3 * 1e3
-        ms, r, d2h = timed_loop(loop_pipelined, e2e_steps)
-        ms_seq, _, _ = timed(step_packed, max(3, e2e_steps // 2))
-        ms8, r8, _ = timed(step_int8, max(3, e2e_steps // 2))
-        e2e = {"value": r.lane_tests / (ms * 1e-3), "unit": "clause_assignment_tests/s",
-               "h2d_bytes_per_step": int(A * pw * 8), "d2h_bytes_per_step": int(d2h), "ms_per_step": ms,
-               "input": "packed 2-bit snapshot rows in pinned host memory (solver-side ingress format)",
-               "pipeline": "round i-1's records copy out on the egress stream while round i's rows go in "
-                           "and round i is tested",
-               "sequential_ms_per_step": ms_seq,
-               "host_pack_ms_per_round": pack_ms, "host_pack_threads": host_threads,
-               "int8_rows": {"value": r8.lane_tests / (ms8 * 1e-3), "ms_per_step": ms8,
-                             "h2d_bytes_per_step": int(A * (cfg.num_vars + 1))}}
+            p0 = time.perf_counter()
+            for _ in range(3):
+                pack_rows(snaps, cfg.num_vars, out=h_packed, threads=host_threads)
+            pack_ms = (time.perf_counter() - p0) / 3 * 1e3
+            ms, r, d2h = timed_loop(loop_pipelined, e2e_steps)
+            ms_seq, _, _ = timed(step_packed, max(3, e2e_steps // 2))
+            ms8, r8, _ = timed(step_int8, max(3, e2e_steps // 2))
+            # two operating modes of the same API, both measured; the engine's
+            # faster mode on this box is the headline (the other is reported)
+            mode = "pipelined" if ms <= ms_seq else "sequential"
+            best = min(ms, ms_seq)
+            e2e = {"value": r.lane_tests / (best * 1e-3), "unit": "clause_assignment_tests/s",
+                   "h2d_bytes_per_step": int(A * pw * 8), "d2h_bytes_per_step": int(d2h), "ms_per_step": best,
+                   "input": "packed 2-bit snapshot rows in pinned host memory (solver-side ingress format)",
+                   "mode": mode,
+                   "pipelined_ms_per_step": ms,
+                   "pipelined": "round i-1's records copy out on the egress stream while round i's rows go in "
+                                "and round i is tested",
+                   "sequential_ms_per_step": ms_seq,
+                   "host_pack_ms_per_round": pack_ms, "host_pack_threads": host_threads,
+                   "int8_rows": {"value": r8.lane_tests / (ms8 * 1e-3), "ms_per_step": ms8,
+                                 "h2d_bytes_per_step": int(A * (cfg.num_vars + 1))}}
+        except Exception as exc:  # reported in the line, never fatal to it
+            e2e = {"value": None, "error": repr(exc)}
 
     # ---- roofline of the trigger kernel --------------------------------------
     peak, peak_kind = load_peaks()

@@ -1,3 +1,1 @@
-timeout 700 python -m pytest tests -m gpu -x -q --timeout 300 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
-tail -2 gpurun_out/pytest_gpu.log
 timeout 400 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.log 2>&1; tail -1 gpurun_out/bench.log
