@@ -718,7 +718,7 @@ int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
         for (int k = 0; k < 2; ++k) { cudaEventCreate(&h->ev_enc[sl][k]); cudaEventCreate(&h->ev_tst[sl][k]); }
     if (cudaMallocHost(&h->h_ctr, 8 * sizeof(unsigned long long)) != cudaSuccess) { delete h; return fail(TSG_ECUDA, "pinned alloc"); }
     if (dalloc(h, (void**)&h->ctr, 8 * sizeof(unsigned long long))) { delete h; return TSG_ENOMEM; }
-    h->out_cap = cfg->report_capacity > 0 ? cfg->report_capacity : (1 << 16);
+    h->out_cap = cfg->report_capacity > 0 ? std::min<int64_t>(cfg->report_capacity, INT32_MAX / 2) : (1 << 16);
     if (dalloc(h, (void**)&h->out, h->out_cap * (int64_t)sizeof(tsg_report))) { delete h; return TSG_ENOMEM; }
     *out = h;
     return TSG_OK;
@@ -1242,6 +1242,8 @@ int round_launch(tsg_engine* h, double inc, bool flip) {
     }
     if (h->fl.n_chunks) {
         CKR(build_desc(h));
+        if (h->n_tiles >= (int64_t)INT32_MAX / 2)  // the kernels index tiles with 32-bit integers
+            return fail(TSG_ECAPACITY, "store of %lld tiles exceeds the 32-bit tile index", (long long)h->n_tiles);
         if (h->fl.n_chunks > 1) CKR(dgrow(h, &h->carry, &h->carry_cap, std::max<int64_t>(1, h->n_tiles * STRIDE)));
         CK(cudaMemsetAsync(h->ctr, 0, 4 * sizeof(unsigned long long), h->st));
         const bool timing = h->cfg.flags & TSG_F_TIMING;
@@ -1277,6 +1279,8 @@ int round_collect(tsg_engine* h, tsg_round_result* out) {
             dfree(h, h->out);
             h->out = nullptr;
             h->out_cap = n_slots + n_slots / 4 + 1024 + (int64_t)h->nsm * 64 * (int64_t)REPORT_CHUNK;
+            if (h->out_cap >= (int64_t)INT32_MAX)  // report slots are 32-bit in the kernels
+                return fail(TSG_ECAPACITY, "%lld report slots exceed the 32-bit record index", (long long)n_slots);
             CKR(dalloc(h, (void**)&h->out, h->out_cap * (int64_t)sizeof(tsg_report)));
             CK(cudaMemsetAsync(h->ctr, 0, 4 * sizeof(unsigned long long), h->st));
             CKR(run_tests(h, rd, h->fl_slot, h->fl_inc, 1));

@@ -411,24 +411,24 @@ __global__ void k_codes(const AggEntry<uint32_t>* __restrict__ agg, int64_t nv2,
 
 // Tiles of a warp increase monotonically, so the warp walks the bucket table
 // forward: `bi` is the tile's bucket, `nt0` the first tile of bucket bi + 1.
-__device__ __forceinline__ void seek_bucket(const BucketDesc* b, int nb, int64_t tile, int& bi, int64_t& nt0) {
+__device__ __forceinline__ void seek_bucket(const BucketDesc* b, int nb, int tile, int& bi, int& nt0) {
     while (tile >= nt0) {
         ++bi;
-        nt0 = bi + 1 < nb ? b[bi + 1].tile0 : INT64_MAX;
+        nt0 = bi + 1 < nb ? (int)b[bi + 1].tile0 : INT_MAX;
     }
 }
 
 // this lane's literal 0 in `tile` of bucket `bd` (literal j at + j * STRIDE)
-__device__ __forceinline__ const int32_t* lane_lits(const BucketDesc* bd, int64_t tile, int lane) {
-    return bd->lits + (tile - bd->tile0) * (int64_t)bd->size * STRIDE + lane;
+__device__ __forceinline__ const int32_t* lane_lits(const BucketDesc* bd, int tile, int lane) {
+    return bd->lits + (int64_t)(tile - (int)bd->tile0) * bd->size * STRIDE + lane;
 }
 
-__device__ __forceinline__ bool lane_active(const BucketDesc* bd, int64_t tile, int lane) {
+__device__ __forceinline__ bool lane_active(const BucketDesc* bd, int tile, int lane) {
     return (tile - bd->tile0) * STRIDE + lane < bd->count;
 }
 
 // load the first PF literal rows of a tile (this lane's column)
-__device__ __forceinline__ void load_rows(const BucketDesc* bd, int64_t tile, int lane, int32_t sentinel,
+__device__ __forceinline__ void load_rows(const BucketDesc* bd, int tile, int lane, int32_t sentinel,
                                           int32_t (&buf)[PF]) {
     const int32_t* lp = lane_lits(bd, tile, lane);
     const bool act = lane_active(bd, tile, lane);
@@ -486,7 +486,7 @@ __device__ __forceinline__ void lane_batch(const LaneEntry<LW>* lt, const ROWS& 
 // Per-warp running state of the tile loop: the warp's report-slot chunk
 // [cpos, cend) and its counter accumulators.
 struct WarpAcc {
-    int64_t cpos = 0, cend = 0;
+    int cpos = 0, cend = 0;  // report slots (the host keeps out_cap < 2^31)
     unsigned int pos = 0, trig = 0, rep = 0;
 };
 
@@ -539,9 +539,9 @@ __device__ __forceinline__ void stage1_slab(const TestParams<LW, GW>& p, const S
 
 // Tile sources (warp-uniform, strictly increasing per warp; -1 = done).
 struct StrideTiles {  // tiles t, t + step, ... < end
-    int64_t t, step, end;
+    int t, step, end;  // tile indices (the host keeps n_tiles < 2^31)
     bool started = false;
-    __device__ __forceinline__ int64_t next(int) {
+    __device__ __forceinline__ int next(int) {
         if (started) t += step;
         started = true;
         return t < end ? t : -1;
@@ -553,10 +553,10 @@ struct StrideTiles {  // tiles t, t + step, ... < end
 template <class LW, class GW, class TAB, class SRC, class ROWS>
 __device__ __forceinline__ void test_tiles(const TestParams<LW, GW>& p, const TAB& tab, const BucketDesc* descs,
                                            int nb, SRC& src, ROWS& cur, int lane, WarpAcc& acc) {
-    int64_t tile = src.next(lane);
+    int tile = src.next(lane);
     if (tile < 0) return;
     int bi = 0;
-    int64_t nt0 = 0;
+    int nt0 = 0;
     {  // first bucket by binary search, then walk forward
         int lo = 0, hi = nb - 1;
         while (lo < hi) {
@@ -564,7 +564,7 @@ __device__ __forceinline__ void test_tiles(const TestParams<LW, GW>& p, const TA
             if (descs[mid].tile0 <= tile) lo = mid; else hi = mid - 1;
         }
         bi = lo;
-        nt0 = bi + 1 < nb ? descs[bi + 1].tile0 : INT64_MAX;
+        nt0 = bi + 1 < nb ? (int)descs[bi + 1].tile0 : INT_MAX;
     }
     int32_t nxt[PF];
     load_rows(descs + bi, tile, lane, p.sentinel, nxt);
@@ -573,7 +573,7 @@ __device__ __forceinline__ void test_tiles(const TestParams<LW, GW>& p, const TA
     while (tile >= 0) {
         const BucketDesc* bd = descs + bi;
         // software pipeline: the next tile's first rows are in flight while this one is tested
-        const int64_t ntile = src.next(lane);
+        const int ntile = src.next(lane);
         if (ntile >= 0) {
             seek_bucket(descs, nb, ntile, bi, nt0);
             load_rows(descs + bi, ntile, lane, p.sentinel, nxt);
@@ -631,22 +631,22 @@ __device__ __forceinline__ void test_tiles(const TestParams<LW, GW>& p, const TA
         const int total = __shfl_sync(0xffffffffu, incl, 31);
         if (total) {
             if (acc.cpos + total > acc.cend) {  // chunk exhausted: pad its tail, take a new one
-                for (int64_t q = acc.cpos + lane; q < acc.cend; q += 32)
+                for (int q = acc.cpos + lane; q < acc.cend; q += 32)
                     if (q < p.out_cap) st_report(p.out + q, REPORT_PAD, 0);
                 const unsigned long long want = total > REPORT_CHUNK ? (unsigned long long)total : REPORT_CHUNK;
                 unsigned long long base = 0;
                 if (lane == 31) base = atomicAdd(p.ctr, want);
-                acc.cpos = (int64_t)__shfl_sync(0xffffffffu, base, 31);
-                acc.cend = acc.cpos + (int64_t)want;
+                acc.cpos = (int)__shfl_sync(0xffffffffu, base, 31);
+                acc.cend = acc.cpos + (int)want;
             }
-            int64_t pos = acc.cpos + incl - ub;
-            const int64_t pend = pos + ub;
+            int pos = acc.cpos + incl - ub;
+            const int pend = pos + ub;
             acc.cpos += total;
 
             // ---- stage 2: exact lane test per positive group (bitpack.py:120-135)
             if (word) {
                 acc.pos += ub;
-                const int64_t slot = (tile - bd->tile0) * STRIDE + lane;
+                const int slot = (tile - (int)bd->tile0) * STRIDE + lane;
                 double act = 0.0;
                 if (!p.emit_only) act = bd->acts[slot];
                 bool touched = false;
@@ -706,7 +706,7 @@ __device__ __forceinline__ void test_tiles(const TestParams<LW, GW>& p, const TA
 template <class LW, class GW, int WARPS>
 __device__ __forceinline__ void finish_block(const TestParams<LW, GW>& p, WarpAcc& acc, int lane, int warp,
                                              unsigned int (&s_acc)[3][WARPS]) {
-    for (int64_t q = acc.cpos + lane; q < acc.cend; q += 32)
+    for (int q = acc.cpos + lane; q < acc.cend; q += 32)
         if (q < p.out_cap) st_report(p.out + q, REPORT_PAD, 0);
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
@@ -746,9 +746,9 @@ __global__ void __launch_bounds__(THREADS, MINB) k_test(const __grid_constant__ 
     }
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int nwarps = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
     WarpAcc acc;
-    StrideTiles src{((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps, p.n_tiles};
+    StrideTiles src{(int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5), nwarps, (int)p.n_tiles};
     RegRows rows;
     test_tiles<LW, GW, TAB>(p, tab, p.buckets, p.nb, src, rows, lane, acc);
     finish_block<LW, GW, WARPS>(p, acc, lane, warp, s_acc);
@@ -801,7 +801,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_test_slab(const __grid_constant_
             for (int i = threadIdx.x; i < nd; i += THREADS) s_desc[i] = p.buckets[d0 + i];
         __syncthreads();
         tab.lo = (int32_t)lo;
-        StrideTiles src{p.slab_tile0[s] + (int64_t)rank * WARPS + warp, (int64_t)n * WARPS, p.slab_tile0[s + 1]};
+        StrideTiles src{(int)p.slab_tile0[s] + rank * WARPS + warp, n * WARPS, (int)p.slab_tile0[s + 1]};
         SmemRows rows{&s_rows[warp][0][lane]};
         test_tiles<LW, GW, SlabTable<GW>>(p, tab, staged ? s_desc : p.buckets + d0, nd, src, rows, lane, acc);
     }
