@@ -649,16 +649,35 @@ __device__ __forceinline__ void test_tiles(const TestParams<LW, GW>& p, const TA
                 const int slot = (tile - (int)bd->tile0) * STRIDE + lane;
                 double act = 0.0;
                 if (!p.emit_only) act = bd->acts[slot];
+                const uint64_t key_hi = (uint64_t)bd->ids[slot] << 16;  // issued early: off the report's path
                 bool touched = false;
                 int last_tid = INT_MIN;
                 GW left = word;
-                while (left) {
-                    const int g = __ffsll((long long)(unsigned long long)left) - 1;
-                    left &= left - GW(1);
-                    const LaneEntry<LW>* lt = p.lane + (int64_t)g * p.vstride;
-                    LW lf = ~LW(0), lo2 = LW(0);
-                    lane_batch<LW>(lt, cur, 0, size, lf, lo2);
-                    if (size > 4 && (lf | lo2) != LW(0)) lane_batch<LW>(lt, cur, 4, size, lf, lo2);
+                // the first triggering group of each thread emits the report
+                // (engine.py:462); every triggering group bumps the activity
+                // in group order (engine.py:460, fp64 mul then add, no FMA)
+                auto settle = [&](int g, LW mask) {
+                    if (!mask) return;
+                    const int hits = __popcll((unsigned long long)mask);
+                    acc.trig += hits;
+                    if (!p.emit_only) {
+                        act = __dadd_rn(act, __dmul_rn(p.inc, (double)hits));
+                        touched = true;
+                    }
+                    const int tid = p.tid[g];
+                    if (tid != last_tid) {
+                        last_tid = tid;
+                        bool dup = false;
+                        if (tid == p.carry_in_tid)
+                            dup = p.carry[bd->tile0 * STRIDE + slot] == (p.stamp_base | (uint32_t)tid);
+                        if (!dup) {
+                            if (pos < p.out_cap) st_report(p.out + pos, key_hi | (uint32_t)(p.g0 + g), (uint64_t)mask);
+                            ++pos;
+                            ++acc.rep;
+                        }
+                    }
+                };
+                auto lane_tail = [&](const LaneEntry<LW>* lt, LW& lf, LW& lo2) {
                     if (size > PF && (lf | lo2) != LW(0)) {
                         const int32_t* lp = lane_lits(bd, tile, lane);
                         for (int j = PF; j < size && (lf | lo2) != LW(0); ++j) {
@@ -667,28 +686,16 @@ __device__ __forceinline__ void test_tiles(const TestParams<LW, GW>& p, const TA
                             step<LW>(lf, lo2, l < 0 ? (e.s & e.t) : (e.s & ~e.t), ~e.s);
                         }
                     }
-                    const LW mask = (lf | lo2) & p.lane_mask[g];
-                    if (!mask) continue;
-                    const int hits = __popcll((unsigned long long)mask);
-                    acc.trig += hits;
-                    if (!p.emit_only) {  // engine.py:460, rounded like the reference (no FMA)
-                        act = __dadd_rn(act, __dmul_rn(p.inc, (double)hits));
-                        touched = true;
-                    }
-                    const int tid = p.tid[g];
-                    if (tid != last_tid) {  // first triggering group of this thread (engine.py:462)
-                        last_tid = tid;
-                        bool dup = false;
-                        if (tid == p.carry_in_tid)
-                            dup = p.carry[bd->tile0 * STRIDE + slot] == (p.stamp_base | (uint32_t)tid);
-                        if (!dup) {
-                            if (pos < p.out_cap)
-                                st_report(p.out + pos, ((uint64_t)bd->ids[slot] << 16) | (uint32_t)(p.g0 + g),
-                                          (uint64_t)mask);
-                            ++pos;
-                            ++acc.rep;
-                        }
-                    }
+                };
+                while (left) {
+                    const int g = __ffsll((long long)(unsigned long long)left) - 1;
+                    left &= left - GW(1);
+                    const LaneEntry<LW>* lt = p.lane + (int64_t)g * p.vstride;
+                    LW lf = ~LW(0), lo2 = LW(0);
+                    lane_batch<LW>(lt, cur, 0, size, lf, lo2);
+                    if (size > 4 && (lf | lo2) != LW(0)) lane_batch<LW>(lt, cur, 4, size, lf, lo2);
+                    lane_tail(lt, lf, lo2);
+                    settle(g, (lf | lo2) & p.lane_mask[g]);
                 }
                 if (touched) bd->acts[slot] = act;
                 if (p.carry_out_tid >= 0 && last_tid == p.carry_out_tid)
