@@ -85,3 +85,24 @@ def test_exchange_loop_reports_are_imported(X):
     assert check_trace(engines[0], formula.num_vars) > 0
     for e in engines:
         e.close()
+
+
+def test_reference_cli_with_gpu_engine(X, tmp_path):
+    # the reference's CLI end to end (DIMACS, answer line, exit code,
+    # --stats-json schema of instrumentation.py) with the GPU engine inside
+    import io
+    import json
+    import contextlib
+    from paper_2012_03119_b200.__main__ import main
+    f = X.random_3cnf(150, 4.26, 1)  # UNSAT (checked against the reference engine above)
+    cnf = tmp_path / "f.cnf"
+    cnf.write_text(f"p cnf {f.num_vars} {len(f.clauses)}\n" +
+                   "".join(" ".join(map(str, c)) + " 0\n" for c in f.clauses))
+    stats = tmp_path / "stats.jsonl"
+    out = io.StringIO()
+    with contextlib.redirect_stdout(out):
+        rc = main([str(cnf), "--threads", "4", "--timeout", "120", "--stats-json", str(stats)])
+    assert rc == 20 and "s UNSATISFIABLE" in out.getvalue()
+    rows = [json.loads(line) for line in stats.read_text().splitlines() if line.strip()]
+    keys = set().union(*rows)
+    assert any("imports_per_assignment" in str(r) for r in rows), keys
