@@ -163,14 +163,20 @@ __global__ void __launch_bounds__(256) k_encode(const int8_t* __restrict__ rows,
 // with is_true / is_set of variable v exactly as k_encode produces them.
 
 // 32x32 bit transpose across the warp: afterwards bit j of lane i's word is
-// bit i of lane j's word before.
+// bit i of lane j's word before.  Stage s exchanges s-blocks with lane^s: a
+// per-lane rotate (left by s, or right by s when lane bit s is set) brings the
+// partner's block into place and one LOP3 merges it under the stage mask --
+// SHFL + SHF + LOP3 per stage (the wrapped-around bits fall outside the mask).
 __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
 #pragma unroll
     for (int sft = 16; sft >= 1; sft >>= 1) {
         const uint32_t m = sft == 16 ? 0x0000FFFFu : sft == 8 ? 0x00FF00FFu : sft == 4 ? 0x0F0F0F0Fu
                          : sft == 2 ? 0x33333333u : 0x55555555u;
+        const bool up = lane & sft;
+        const uint32_t keep = up ? ~m : m;
         const uint32_t y = __shfl_xor_sync(0xffffffffu, x, sft);
-        x = (lane & sft) ? ((x & ~m) | ((y & ~m) >> sft)) : ((x & m) | ((y & m) << sft));
+        const uint32_t yy = __funnelshift_l(y, y, up ? 32 - sft : sft);  // rotate
+        x = (x & keep) | (yy & ~keep);
     }
     return x;
 }
@@ -196,18 +202,32 @@ __global__ void __launch_bounds__(256) k_encode_packed(const uint64_t* __restric
     const int64_t vbase = (int64_t)blockIdx.x * 128;
     const int64_t V = c.num_vars;
     const int64_t w0 = (int64_t)blockIdx.x * 4;  // first word of the block in every row
+    // this lane's 32 bytes of row `half * 32 + lane` of group g (zeros past the group)
+    auto load_row = [&](int g, int half, uint4& a, uint4& b) {
+        const int r = half * 32 + lane;
+        a = make_uint4(0, 0, 0, 0);
+        b = make_uint4(0, 0, 0, 0);
+        if (g < c.G && r < c.lanes[g]) {
+            const uint4* src = reinterpret_cast<const uint4*>(rows + (c.row0[g] + r) * c.pitch_words + w0);
+            a = __ldg(src);
+            b = __ldg(src + 1);
+        }
+    };
+    uint4 na, nb;  // <= 32 lanes: the warp's next group is loaded while this one is transposed
+    if constexpr (sizeof(LW) == 4) load_row(y, 0, na, nb);
     for (int g = y; g < c.G; g += 8) {
         const int n = c.lanes[g];
         LW tw[4] = {0, 0, 0, 0}, sw[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int half = 0; half < (int)(sizeof(LW) / 4); ++half) {
             if (half * 32 >= n) break;
-            const int r = half * 32 + lane;
-            uint4 a = make_uint4(0, 0, 0, 0), b = make_uint4(0, 0, 0, 0);
-            if (r < n) {
-                const uint4* src = reinterpret_cast<const uint4*>(rows + (c.row0[g] + r) * c.pitch_words + w0);
-                a = __ldg(src);
-                b = __ldg(src + 1);
+            uint4 a, b;
+            if constexpr (sizeof(LW) == 4) {
+                a = na;
+                b = nb;
+                load_row(g + 8, 0, na, nb);
+            } else {
+                load_row(g, half, a, b);
             }
             const uint32_t tv[4] = {a.x, a.z, b.x, b.z}, sv[4] = {a.y, a.w, b.y, b.w};
 #pragma unroll
@@ -215,6 +235,9 @@ __global__ void __launch_bounds__(256) k_encode_packed(const uint64_t* __restric
                 tw[k] |= (LW)warp_transpose32(tv[k], lane) << (32 * half);
                 sw[k] |= (LW)warp_transpose32(sv[k], lane) << (32 * half);
             }
+        }
+        if constexpr (sizeof(LW) == 4) {
+            if (n == 0) load_row(g + 8, 0, na, nb);  // the half loop did not run
         }
         const LW lm = width_mask<LW>(n);
         const GW bit = GW(1) << g;
