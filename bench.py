@@ -19,9 +19,11 @@ busy_seconds, instrumentation.py:248-250).
   box's host cores, rank 0 only, on a bounded slice of the same workload.
 
 Multi-GPU (torchrun): every rank holds its own C3-sized clause shard
-(weak scaling); rank 0 stages and encodes the round, the packed tables are
-broadcast over NVLink with NCCL, every rank tests its shard, and the time is
-the max over ranks.
+(weak scaling) and the round's packed rows (the host sends each GPU its copy
+over that GPU's own PCIe link); every rank encodes the round's tables and
+tests its shard -- no data-path collective -- and the time is the max over
+ranks.  `--tables bcast`: rank 0 encodes and NCCL broadcasts the tables over
+NVLink instead.
 """
 from __future__ import annotations
 
@@ -200,6 +202,9 @@ def main():
     ap.add_argument("--config", default="C3", choices=sorted(W.CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--tables", default="replicated", choices=["replicated", "bcast"],
+                    help="N>1: every rank encodes the round's tables from its own copy of the rows "
+                         "(default; no data-path collective), or rank 0 encodes and NCCL broadcasts them")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = W.CONFIGS[args.config]
@@ -254,7 +259,7 @@ def main():
     eng.prepare(gl, gt)
 
     tables_t = None
-    if dist is not None:
+    if dist is not None and args.tables == "bcast":
         ptr, nbytes = eng.tables()
 
         class _CAI:
@@ -277,7 +282,7 @@ def main():
         encoded (into the other table slot) before round i is collected
         (tsg_round_launch / tsg_round_collect), so the GPU does not idle on
         the host between rounds.  N GPUs: encode, NCCL broadcast, test."""
-        if dist is not None:
+        if tables_t is not None:
             for _ in range(n):
                 record(step())
             return
@@ -318,7 +323,7 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
     elapsed_ms = e0.elapsed_time(e1)
-    if dist is not None:  # the broadcast tables must be identical on every rank
+    if tables_t is not None:  # the broadcast tables must be identical on every rank
         with torch.cuda.stream(stream):
             cs = torch.stack([tables_t.to(torch.int64).sum(), (tables_t.to(torch.int64) * 131).remainder(
                 1000003).sum()])
@@ -472,7 +477,10 @@ def main():
                        "clauses_per_gpu": cfg.n_clauses, "assignments": A, "groups": G, "num_vars": cfg.num_vars,
                        "sum_literals_per_gpu": sum_lits, "reports_per_step": P,
                        "l2": "inputs larger than L2 (640 MB clause DB + 205 MB snapshots per GPU vs 126 MB L2)",
-                       "parallelism": f"clause shards x{world}, tables broadcast (NCCL)" if world > 1 else "1 GPU"},
+                       "parallelism": "1 GPU" if world == 1 else (
+                           f"clause shards x{world}; tables broadcast from rank 0 (NCCL)" if args.tables == "bcast"
+                           else f"clause shards x{world}; every rank encodes the round's tables from its copy of "
+                                f"the packed rows (no data-path collective)")},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,
             "build_seconds": build_s,
