@@ -161,7 +161,6 @@ struct tsg_engine {
     int64_t* carry = nullptr;
     int64_t carry_cap = 0;
     int64_t round_seq = 0;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     int64_t grid[32] = {0};       // persistent grid per k_test variant
     int64_t grid_smem[32];        // shared-memory size the grid was computed for (-1: none)
     bool smem_table = true;       // shared-memory code table when it fits (TSG_SMEM_TABLE=0 disables)
@@ -708,7 +707,6 @@ int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
         uint64_t thr = UINT64_MAX;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
-    for (auto& e : h->ev) cudaEventCreate(&e);
     cudaStreamCreateWithFlags(&h->egress, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&h->ev_cur, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&h->alt.ev, cudaEventDisableTiming);
@@ -736,7 +734,6 @@ int tsg_destroy(tsg_engine* h) {
     dfree(h, h->alt.out); dfree(h, h->alt.out2);
     cudaStreamSynchronize(h->st);
     if (h->h_ctr) cudaFreeHost(h->h_ctr);
-    for (auto& e : h->ev) if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : {h->ev_cur, h->alt.ev, h->ev_ready, h->ev_done}) if (e) cudaEventDestroy(e);
     for (int sl = 0; sl < 2; ++sl)
         for (int k = 0; k < 2; ++k) {
