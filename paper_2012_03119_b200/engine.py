@@ -17,6 +17,7 @@ CUDA device raises.
 from __future__ import annotations
 
 import ctypes as C
+import itertools
 import threading
 import time
 from collections import deque
@@ -80,6 +81,15 @@ class Report:
     lits: tuple
     engine_id: int
     lane_mask: int
+
+
+@dataclass
+class _ReportBatch:
+    """One round's reports for one destination, in emission order."""
+
+    lits: list
+    eids: list
+    masks: list
 
 
 @dataclass
@@ -196,6 +206,8 @@ class Engine:
         self.store = DeviceClauseStore(self)
         self._lits: Dict[int, tuple] = {}
         self._size_rank: Dict[int, int] = {}
+        self._rank_of_size = np.zeros(64, dtype=np.int64)   # bucket creation rank by clause size
+        self._size_of = np.zeros(1024, dtype=np.int32)      # clause size by engine id
 
         self._id_lock = threading.Lock()
         self._next_id = 0
@@ -204,6 +216,7 @@ class Engine:
         self._queue_lock = threading.Lock()
         self._snapshots: Dict[int, deque] = {t: deque() for t in range(thread_count)}
         self._reports: Dict[int, deque] = {t: deque() for t in range(thread_count)}
+        self._pending_reports: Dict[int, int] = {}
 
         self._activity_inc = 1.0
         self._reduce_watermark = 0
@@ -269,13 +282,23 @@ class Engine:
         return out
 
     def drain_reports(self, thread_id: int) -> List[Report]:
+        """engine.py:335-343.  A round queues each destination's reports as
+        one batch (literals captured at round time); the Report objects are
+        built here, in the draining solver thread, off the engine worker."""
         with self._queue_lock:
             q = self._reports.get(thread_id)
             if not q:
                 return []
-            out = list(q)
+            items = list(q)
             q.clear()
-            return out
+            self._pending_reports[thread_id] = 0
+        out: List[Report] = []
+        for it in items:
+            if isinstance(it, _ReportBatch):
+                out.extend(map(Report, itertools.repeat(thread_id, len(it.eids)), it.lits, it.eids, it.masks))
+            else:
+                out.append(it)
+        return out
 
     # ------------------------------------------------------------------
     # engine worker side
@@ -286,21 +309,33 @@ class Engine:
         if not batch:
             return
         n = len(batch)
+        lens = np.fromiter((len(b[1]) for b in batch), dtype=np.int64, count=n)
         offs = np.zeros(n + 1, dtype=np.int64)
-        for i, (_, lits, _) in enumerate(batch):
-            offs[i + 1] = offs[i] + len(lits)
-        flat = np.zeros(max(int(offs[-1]), 1), dtype=np.int32)
-        for i, (_, lits, _) in enumerate(batch):
-            if lits:
-                flat[offs[i]:offs[i + 1]] = lits
+        np.cumsum(lens, out=offs[1:])
+        total = int(offs[-1])
+        flat = np.fromiter(itertools.chain.from_iterable(b[1] for b in batch), dtype=np.int32, count=total) \
+            if total else np.zeros(1, dtype=np.int32)
         ids = np.fromiter((b[0] for b in batch), dtype=np.int64, count=n)
         org = np.fromiter((b[2] for b in batch), dtype=np.int32, count=n)
         check(self._L.tsg_add_clauses(self._h, ptr(flat), ptr(offs), n, ptr(ids), ptr(org),
                                       self._activity_inc))
-        for eid, lits, _ in batch:
-            self._lits[eid] = lits
-            if len(lits) not in self._size_rank:  # bucket creation order (dict insertion order)
-                self._size_rank[len(lits)] = len(self._size_rank)
+        self._lits.update((b[0], b[1]) for b in batch)
+        # bucket creation order (dict insertion order): new sizes in first-seen order
+        sizes, first = np.unique(lens, return_index=True)
+        for size in sizes[np.argsort(first, kind="stable")].tolist():
+            if size not in self._size_rank:
+                self._size_rank[size] = len(self._size_rank)
+                if size >= len(self._rank_of_size):
+                    grown = np.zeros(max(size + 1, 2 * len(self._rank_of_size)), dtype=np.int64)
+                    grown[:len(self._rank_of_size)] = self._rank_of_size
+                    self._rank_of_size = grown
+                self._rank_of_size[size] = self._size_rank[size]
+        top = int(ids.max()) + 1
+        if top > len(self._size_of):
+            grown = np.zeros(max(top, 2 * len(self._size_of)), dtype=np.int32)
+            grown[:len(self._size_of)] = self._size_of
+            self._size_of = grown
+        self._size_of[ids] = lens
         self.counters["clauses_added"] += n
 
     def _integrate_exports(self) -> None:
@@ -359,7 +394,7 @@ class Engine:
                 lanes.append(len(chunk))
                 tids.append(tid)
 
-        reports: List[Report] = []
+        n_rep = 0
         if lanes:
             block = np.concatenate(rows)
             check(self._L.tsg_stage_packed(self._h, ptr(block), block.shape[0], block.shape[1], 0))
@@ -376,21 +411,32 @@ class Engine:
             result.aggregate_tests_negative = res.aggregate_tests_negative
             recs = _reports.decode(self._fetch(res.reports))
             if len(recs):
-                lits_of = self._lits
-                rank = self._size_rank
-                brank = np.fromiter((rank[len(lits_of[e])] for e in recs["engine_id"].tolist()),
-                                    dtype=np.int64, count=len(recs))
+                brank = self._rank_of_size[self._size_of[recs["engine_id"]]]
                 recs = recs[_reports.reference_order(recs, self.config.group_width, brank)]
-                for eid, mask, g in zip(recs["engine_id"].tolist(), recs["lane_mask"].tolist(),
-                                        recs["group"].tolist()):
-                    reports.append(Report(tids[g], lits_of[eid], eid, mask))
+                dest = np.asarray(tids, dtype=np.int64)[recs["group"]]
+                order = np.argsort(dest, kind="stable")  # per destination, in emission order
+                eids = recs["engine_id"][order].tolist()
+                lits_of = self._lits
+                lits = [lits_of[e] for e in eids]  # captured now: a later reduce may drop the clause
+                masks = recs["lane_mask"][order].tolist()
+                dsorted = dest[order]
+                cuts = np.flatnonzero(np.diff(dsorted)) + 1
+                bounds = [0] + cuts.tolist() + [len(eids)]
+                batches = [(int(dsorted[a]), _ReportBatch(lits[a:b], eids[a:b], masks[a:b]))
+                           for a, b in zip(bounds[:-1], bounds[1:])]
+                n_rep = len(eids)
+                if self.config.trace:  # the trace keeps Report objects in emission order
+                    emitted = [None] * n_rep
+                    for k, i in enumerate(order.tolist()):
+                        emitted[i] = Report(int(dsorted[k]), lits[k], eids[k], masks[k])
 
-        if reports:
+        if n_rep:
             with self._queue_lock:
-                for rep in reports:
-                    self._reports.setdefault(rep.destination, deque()).append(rep)
-            self.counters["reports_delivered"] += len(reports)
-            result.reports_emitted = len(reports)
+                for d, batch in batches:
+                    self._reports.setdefault(d, deque()).append(batch)
+                    self._pending_reports[d] = self._pending_reports.get(d, 0) + len(batch.eids)
+            self.counters["reports_delivered"] += n_rep
+            result.reports_emitted = n_rep
 
         if result.assignments_consumed:  # engine.py:416-420
             self._activity_inc /= self.config.activity_decay
@@ -405,7 +451,7 @@ class Engine:
             self.trace.append(RoundTrace(
                 snapshots=[(s.thread_id, np.array(s.values, copy=True))
                            for snaps in pending.values() for s, _ in snaps],
-                store=store_snapshot, reports=list(reports)))
+                store=store_snapshot, reports=emitted if n_rep else []))
 
         self.counters["rounds"] += 1
         self.counters["busy_seconds"] += time.perf_counter() - started
@@ -463,6 +509,6 @@ class Engine:
         with self._id_lock:
             out["staged_pending"] = len(self._staged)
         with self._queue_lock:
-            out["reports_pending"] = sum(len(q) for q in self._reports.values())
+            out["reports_pending"] = sum(self._pending_reports.values())
             out["snapshots_pending"] = sum(len(q) for q in self._snapshots.values())
         return out
