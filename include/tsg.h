@@ -97,7 +97,11 @@ int tsg_destroy(tsg_engine* h);
  * _integrate_exports / ClauseStore.insert (engine.py:348-358, 213-219):
  * append n clauses in order.  Clause i has literals lits[offsets[i] ..
  * offsets[i+1]), engine id ids[i], origin origins[i]; all start at
- * `activity`.  Buckets are created in first-seen size order. */
+ * `activity`.  Buckets are created in first-seen size order.  Engine ids
+ * must increase with insertion order (the reference assigns them that way,
+ * engine.py:305-317): the store orders clauses by id wherever the
+ * reference's slot order is visible (reports, bucket reads), because the
+ * device layout inside a bucket is pivot-ordered. */
 int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets,
                     int64_t n, const int64_t* ids, const int32_t* origins,
                     double activity);
