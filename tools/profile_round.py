@@ -17,11 +17,13 @@ from paper_2012_03119_b200.native import NativeEngine  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "C3"
 rounds = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 cfg = W.CONFIGS[name]
+n_clauses = int(os.environ.get("TSG_N_CLAUSES", cfg.n_clauses))  # scale the store (capacity runs)
 rng = np.random.default_rng(cfg.seed)
-b = W.clause_buckets(cfg.n_clauses, cfg.num_vars, rng)
+b = W.clause_buckets(n_clauses, cfg.num_vars, rng)
 flat, offs, ids = W.flatten(b)
 eng = NativeEngine(cfg.num_vars, timing=True, report_capacity=8 << 20)
 eng.add_clauses(flat, offs, ids)
+del flat, b
 snaps = W.snapshots(cfg.threads, cfg.lanes, cfg.num_vars, np.random.default_rng(cfg.seed + 999))
 gl, gt = W.groups_for(cfg.threads, cfg.lanes)
 if os.environ.get("TSG_INT8_ROWS"):  # int8 snapshot rows
@@ -39,5 +41,6 @@ eng.prepare(gl, gt)
 for r in range(rounds):
     eng.encode()
     res = eng.test(1.0)
-    print(f"round {r}: encode {res.encode_ms:.3f} ms test {res.test_ms:.3f} ms reports {res.reports} "
+    print(f"round {r}: clauses {n_clauses} encode {res.encode_ms:.3f} ms test {res.test_ms:.3f} ms "
+          f"({res.lane_tests / (res.test_ms * 1e-3):.3e} tests/s) reports {res.reports} "
           f"lane_triggers {res.lane_triggers} neg {res.aggregate_tests_negative}/{res.aggregate_tests}", flush=True)
