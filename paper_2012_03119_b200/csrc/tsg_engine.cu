@@ -676,7 +676,7 @@ int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
     if (const char* e = getenv("TSG_SMEM_TABLE")) h->smem_table = atoi(e) != 0;
     if (const char* e = getenv("TSG_L2_PERSIST")) h->l2_persist = atoi(e) != 0;
     if (const char* e = getenv("TSG_PIVOT")) h->pivot = atoi(e) != 0;
-    // Variable slabs (DESIGN.md §4.2), opt-in: TSG_SLABS=1 partitions the store
+    // Variable slabs (DESIGN.md §4.3), opt-in: TSG_SLABS=1 partitions the store
     // into as many slabs as one CTA's shared memory needs for the aggregate
     // words, TSG_SLABS=n>1 into at least n.  Default: one slab (unpartitioned
     // store, global-table kernel), the faster layout measured on B200.
