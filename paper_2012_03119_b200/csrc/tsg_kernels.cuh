@@ -27,9 +27,6 @@ constexpr int MAXG = 64;
 #else
 #define LD_LIT(p) ld_lit(p)
 #endif
-#ifndef TSG_DERIVE  // stage 2 derives lane words of single-valued subsets from saved aggregates
-#define TSG_DERIVE 0  // measured: saving the entries costs more than the gathers it saves
-#endif
 
 // ---------------------------------------------------------------------------
 // K1+K2: encoder.
@@ -272,21 +269,22 @@ __global__ void __launch_bounds__(256) k_encode_packed(const uint64_t* __restric
 // sector: DESIGN.md §4) and by the latency of the gather chains, so:
 //  * the first PF literal rows of a warp's next tile are loaded into
 //    registers while the current tile is tested (software pipeline);
-//  * stage 1 (aggregate filter, engine.py:238-254) gathers four literals'
-//    aggregate entries at a time and stops as soon as every group is
+//  * stage 1 (aggregate filter, engine.py:238-254) gathers the aggregate
+//    entries of literals 0-3 together -- literal 0 is the clause's pivot,
+//    shared by the pivot-ordered tile, so that gather costs the warp a few
+//    sectors -- then two at a time, and stops as soon as every group is
 //    negative: the live set (all_false | one_undef) only shrinks, so a zero
 //    word is final;
-//  * the aggregate entries of the first PF literals stay in shared memory;
-//    stage 2 (lane test, bitpack.py:120-135) derives the lane words of every
-//    (literal, group) whose value subset is a single value ({T}: all lanes
-//    set and true, {F}: set and false, {U}: unset) and gathers lane words
-//    only for mixed subsets.
+//  * stage 2 (lane test, bitpack.py:120-135) runs per positive group with
+//    the same early exit; the clause's activity and engine id are loaded at
+//    stage-2 entry, off the report path.
 // Every triggering group bumps the clause's activity by inc * popcount (fp64
 // round-to-nearest mul then add, no FMA: engine.py:460); the first
 // triggering group of each thread emits the report (engine.py:462-464).
-// Report slots are reserved once per warp for an upper bound (the
-// positive-group count); unused slots are written as padding (key = ~0) and
-// squeezed out when the records are fetched.
+// Report slots come from a warp-private chunk refilled by one atomic per
+// REPORT_CHUNK slots, reserved for an upper bound (the positive-group
+// count); unused slots are written as padding (key = ~0) and squeezed out
+// when the records are fetched.
 
 struct BucketDesc {
     const int32_t* lits;
