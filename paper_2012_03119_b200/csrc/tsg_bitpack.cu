@@ -158,6 +158,7 @@ int tsg_pack(int32_t device, const int8_t* rows, int64_t n, int64_t row_pitch, i
     c.num_vars = num_vars;
     c.pitch = pitch;
     c.vstride = vstride;
+    c.polarity = nullptr;
     c.row0[0] = 0;
     c.lanes[0] = (int32_t)n;
     auto* lane = (LaneEntry<uint64_t>*)d_lane.p;

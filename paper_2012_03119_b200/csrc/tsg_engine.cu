@@ -67,11 +67,11 @@ int grid_for(int64_t n, int threads = 256, int cap = 148 * 16) {
 struct Part {
     int32_t slab = 0;
     int64_t count = 0, cap = 0;  // cap: multiple of STRIDE
-    int32_t* lits = nullptr;     // hot-prefix order (see hmask)
+    int32_t* lits = nullptr;     // placement order (see `order`)
     double* acts = nullptr;
     int64_t* ids = nullptr;
     int32_t* origins = nullptr;
-    uint64_t* hmask = nullptr;   // original positions (< 64) of the hot prefix
+    uint64_t* order = nullptr;   // where the stored literal order came from (tsg_store.cuh order_word)
 };
 
 // A size bucket of the reference store (engine.py:122-163), split into one
@@ -178,6 +178,12 @@ struct tsg_engine {
     std::vector<uint64_t> h_sched;
     bool desc_dirty = true;             // store changed since the tile table was built
     bool pivot = true;                  // pivot-first clause layout (TSG_PIVOT=0 disables)
+    // literal polarity placed right after the pivot (+1 / -1 / 0 none).  Prior
+    // before any round: +1 -- in the paper's measured value subsets
+    // a variable can be True in a window more often
+    // (.208) than False (.153), so positive literals are non-False more often
+    int prefer = 1;
+    bool prefer_fixed = false;          // TSG_PREFER fixes it; else set from each round's statistics
     bool l2_persist = false;            // persisting L2 window over the round tables (TSG_L2_PERSIST=1; measured slower)
     const void* persist_base = nullptr;
 };
@@ -226,8 +232,8 @@ int dgrow(tsg_engine* h, T** p, int64_t* cap, int64_t need, bool keep = false, i
 }
 
 void part_free(tsg_engine* h, Part& p) {
-    dfree(h, p.lits); dfree(h, p.acts); dfree(h, p.ids); dfree(h, p.origins); dfree(h, p.hmask);
-    p.lits = nullptr; p.acts = nullptr; p.ids = nullptr; p.origins = nullptr; p.hmask = nullptr;
+    dfree(h, p.lits); dfree(h, p.acts); dfree(h, p.ids); dfree(h, p.origins); dfree(h, p.order);
+    p.lits = nullptr; p.acts = nullptr; p.ids = nullptr; p.origins = nullptr; p.order = nullptr;
 }
 
 int part_alloc(tsg_engine* h, Part& p, int32_t size, int64_t cap) {
@@ -235,7 +241,7 @@ int part_alloc(tsg_engine* h, Part& p, int32_t size, int64_t cap) {
     CKR(dalloc(h, (void**)&p.acts, cap * 8));
     CKR(dalloc(h, (void**)&p.ids, cap * 8));
     CKR(dalloc(h, (void**)&p.origins, cap * 4));
-    CKR(dalloc(h, (void**)&p.hmask, cap * 8));
+    CKR(dalloc(h, (void**)&p.order, cap * 8));
     p.cap = cap;
     return TSG_OK;
 }
@@ -255,7 +261,7 @@ int part_reserve(tsg_engine* h, Part& b, int32_t size, int64_t need) {
         CK(cudaMemcpyAsync(n.acts, b.acts, b.count * 8, cudaMemcpyDeviceToDevice, h->st));
         CK(cudaMemcpyAsync(n.ids, b.ids, b.count * 8, cudaMemcpyDeviceToDevice, h->st));
         CK(cudaMemcpyAsync(n.origins, b.origins, b.count * 4, cudaMemcpyDeviceToDevice, h->st));
-        CK(cudaMemcpyAsync(n.hmask, b.hmask, b.count * 8, cudaMemcpyDeviceToDevice, h->st));
+        CK(cudaMemcpyAsync(n.order, b.order, b.count * 8, cudaMemcpyDeviceToDevice, h->st));
     }
     part_free(h, b);
     b = n;
@@ -289,6 +295,7 @@ int launch_encode(tsg_engine* h, int c) {
         ec.row0[g] = rd.grow0[g0 + g];
         ec.lanes[g] = rd.glanes[g0 + g];
     }
+    ec.polarity = h->ctr + 6;
     int8_t* tab = h->tables + h->tslot * h->slot_bytes;
     auto* agg = reinterpret_cast<AggEntry<GW>*>(tab + rd.chunk_off[c]);
     auto* lane = reinterpret_cast<LaneEntry<LW>*>(tab + rd.chunk_off[c] + agg_bytes(h));
@@ -300,6 +307,7 @@ int launch_encode(tsg_engine* h, int c) {
         pc.pitch_words = h->ppitch;
         pc.vstride = ec.vstride;
         for (int g = 0; g < ec.G; ++g) { pc.row0[g] = ec.row0[g]; pc.lanes[g] = ec.lanes[g]; }
+        pc.polarity = ec.polarity;
         k_encode_packed<LW, GW><<<grid, block, 0, h->st>>>(h->prows, pc, lane, agg);
     } else {
         k_encode<LW, GW><<<grid, block, 0, h->st>>>(h->rows, ec, lane, agg);
@@ -544,8 +552,8 @@ int compact_all(tsg_engine* h, const uint8_t* keep, const std::vector<int64_t>& 
             CKR(part_alloc(h, np, b.size, p.cap));
             if (kept) {
                 k_compact<<<grid_for(kept), 256, 0, h->st>>>(sel, kept, b.size, p.lits, p.acts, p.ids, p.origins,
-                                                             p.hmask, np.lits, np.acts, np.ids, np.origins,
-                                                             np.hmask);
+                                                             p.order, np.lits, np.acts, np.ids, np.origins,
+                                                             np.order);
                 CK(cudaGetLastError());
             }
             part_free(h, p);
@@ -571,14 +579,19 @@ int32_t slab_of(const tsg_engine* h, int32_t lit) {
     return (int32_t)std::min<int64_t>(v / h->slab_w, h->n_slabs - 1);
 }
 
-// Placement of one clause: the slab holding most of its
-// literals among the first 64 positions (ties: the least-loaded slab); those
-// literals move to the front, in order, and hmask records their original
-// positions so readback restores the reference's literal order.
+// Placement of one clause.  Unpartitioned store: the pivot
+// -- the literal with the smallest variable among the first 58 -- goes first
+// (add_clauses orders each batch by pivot, so a warp's first gathers share
+// table lines), then the literals of the preferred polarity (those more
+// likely to be non-False under the recent rounds' assignments: they end the
+// early-exit recurrence sooner), then the rest.  Slab-partitioned store: the
+// literals of the chosen slab (the one holding most of them) go first.  The
+// order word lets readback restore the reference's literal order.
 int32_t place_clause(tsg_engine* h, const int32_t* lits, int32_t size, std::vector<int32_t>& cnt,
-                     int32_t* out, uint64_t* hmask) {
-    const int32_t lim = std::min(size, 64);
-    int32_t slab = 0;
+                     int32_t* out, uint64_t* order) {
+    const int32_t lim = std::min(size, ORDER_MASK_BITS);
+    int32_t slab = 0, jp = -1;
+    uint64_t m = 0;
     if (h->n_slabs > 1 && size > 0) {
         for (int32_t j = 0; j < lim; ++j) cnt[slab_of(h, lits[j])]++;
         int32_t best = -1;
@@ -589,31 +602,23 @@ int32_t place_clause(tsg_engine* h, const int32_t* lits, int32_t size, std::vect
         }
         for (int32_t j = 0; j < lim; ++j) cnt[slab_of(h, lits[j])] = 0;
         slab = best;
+        for (int32_t j = 0; j < lim; ++j)
+            if (slab_of(h, lits[j]) == slab) m |= 1ull << j;
+    } else if (h->pivot && lim > 0) {
+        jp = 0;
+        for (int32_t j = 1; j < lim; ++j)
+            if (std::llabs((long long)lits[j]) < std::llabs((long long)lits[jp])) jp = j;
+        if (h->prefer != 0)
+            for (int32_t j = 0; j < lim; ++j)
+                if (j != jp && (lits[j] > 0) == (h->prefer > 0)) m |= 1ull << j;
     }
-    uint64_t m = 0;
     int32_t o = 0;
-    if (h->n_slabs == 1) {
-        // unpartitioned store: the pivot -- the literal with the smallest
-        // variable among the first 64 -- goes first; add_clauses orders each
-        // batch by pivot, so a warp's first-literal gathers share table lines
-        if (h->pivot && lim > 0) {
-            int32_t jp = 0;
-            for (int32_t j = 1; j < lim; ++j)
-                if (std::llabs((long long)lits[j]) < std::llabs((long long)lits[jp])) jp = j;
-            m = 1ull << jp;
-            out[o++] = lits[jp];
-        }
-    } else {
-        for (int32_t j = 0; j < lim; ++j) {
-            if (slab_of(h, lits[j]) == slab) {
-                m |= 1ull << j;
-                out[o++] = lits[j];
-            }
-        }
-    }
+    if (jp >= 0) out[o++] = lits[jp];
+    for (int32_t j = 0; j < lim; ++j)
+        if ((m >> j) & 1) out[o++] = lits[j];
     for (int32_t j = 0; j < size; ++j)
-        if (j >= 64 || !((m >> j) & 1)) out[o++] = lits[j];
-    *hmask = m;
+        if (j != jp && (j >= lim || !((m >> j) & 1))) out[o++] = lits[j];
+    *order = order_word(jp, m);
     h->slab_load[slab]++;
     return slab;
 }
@@ -676,6 +681,7 @@ int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
     if (const char* e = getenv("TSG_SMEM_TABLE")) h->smem_table = atoi(e) != 0;
     if (const char* e = getenv("TSG_L2_PERSIST")) h->l2_persist = atoi(e) != 0;
     if (const char* e = getenv("TSG_PIVOT")) h->pivot = atoi(e) != 0;
+    if (const char* e = getenv("TSG_PREFER")) { h->prefer = atoi(e); h->prefer_fixed = true; }
     // Variable slabs, opt-in: TSG_SLABS=1 partitions the store
     // into as many slabs as one CTA's shared memory needs for the aggregate
     // words, TSG_SLABS=n>1 into at least n.  Default: one slab (unpartitioned
@@ -832,7 +838,7 @@ int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, 
         }
         CK(cudaMemcpyAsync(p.ids + p.count, hid.data(), k * 8, cudaMemcpyHostToDevice, h->st));
         CK(cudaMemcpyAsync(p.origins + p.count, hor.data(), k * 4, cudaMemcpyHostToDevice, h->st));
-        CK(cudaMemcpyAsync(p.hmask + p.count, hmk.data(), k * 8, cudaMemcpyHostToDevice, h->st));
+        CK(cudaMemcpyAsync(p.order + p.count, hmk.data(), k * 8, cudaMemcpyHostToDevice, h->st));
         k_fill_f64<<<grid_for(k), 256, 0, h->st>>>(p.acts + p.count, k, activity);
         CK(cudaGetLastError());
         p.count += k;
@@ -880,7 +886,7 @@ int tsg_bucket_read(tsg_engine* h, int32_t bi, int32_t* lits, int64_t* ids, int3
         if (lits && b.size) {
             int32_t* tmp = nullptr;
             CKR(dalloc(h, (void**)&tmp, p.count * b.size * 4));
-            k_deinterleave<<<grid_for(p.count), 256, 0, h->st>>>(p.lits, p.hmask, p.count, b.size, tmp);
+            k_deinterleave<<<grid_for(p.count), 256, 0, h->st>>>(p.lits, p.order, p.count, b.size, tmp);
             CK(cudaGetLastError());
             CK(cudaMemcpyAsync(hl.data() + off * b.size, tmp, p.count * b.size * 4, cudaMemcpyDeviceToHost, h->st));
             dfree(h, tmp);
@@ -1248,6 +1254,7 @@ int round_launch(tsg_engine* h, double inc, bool flip) {
         CKR(run_tests(h, h->fl, h->fl_slot, inc, 0));
         if (timing) CK(cudaEventRecord(h->ev_tst[h->fl_slot][1], h->st));
         CK(cudaMemcpyAsync(h->h_ctr, h->ctr, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
+        CK(cudaMemcpyAsync(h->h_ctr + 6, h->ctr + 6, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
         CK(cudaEventRecord(h->ev_done, h->st));
     }
     h->inflight = true;
@@ -1265,6 +1272,11 @@ int round_collect(tsg_engine* h, tsg_round_result* out) {
     res.n_chunks = rd.n_chunks;
     if (rd.n_chunks) {
         CK(cudaEventSynchronize(h->ev_done));
+        // literal placement for the next inserts: the polarity that is
+        // non-False more often under this round's assignments goes right
+        // after the pivot (ends the early-exit recurrence sooner)
+        if (!h->prefer_fixed && h->h_ctr[6] + h->h_ctr[7] > 0)
+            h->prefer = h->h_ctr[7] < h->h_ctr[6] ? 1 : (h->h_ctr[7] > h->h_ctr[6] ? -1 : 0);
         int64_t n_slots = (int64_t)h->h_ctr[0];
         int64_t positives = (int64_t)h->h_ctr[1];
         res.lane_triggers = (int64_t)h->h_ctr[2];
@@ -1324,6 +1336,7 @@ int tsg_round_encode(tsg_engine* h) {
     if (!h->rd.n_chunks) return TSG_OK;
     const bool timing = h->cfg.flags & TSG_F_TIMING;
     if (timing) CK(cudaEventRecord(h->ev_enc[h->tslot][0], h->st));
+    CK(cudaMemsetAsync(h->ctr + 6, 0, 2 * sizeof(unsigned long long), h->st));
     CKR(do_encode(h));
     if (timing) CK(cudaEventRecord(h->ev_enc[h->tslot][1], h->st));
     return TSG_OK;

@@ -49,6 +49,7 @@ struct EncodeChunk {
     int64_t vstride;      // lane-table row length (num_vars + 2)
     int64_t row0[MAXG];   // first row of each group
     int32_t lanes[MAXG];  // rows (lanes) of each group
+    unsigned long long* polarity;  // [2] += (var, group) pairs that can be True / can be False
 };
 
 // 0x80 in every byte of w that is != 0
@@ -146,6 +147,15 @@ __global__ void __launch_bounds__(256) k_encode(const int8_t* __restrict__ rows,
         const int64_t v = vbase + t;
         if (v <= V) agg[v] = AggEntry<GW>{sT[t], sF[t], sU[t], GW(0)};
         else if (v == V + 1) agg[v] = AggEntry<GW>{~GW(0), ~GW(0), GW(0), GW(0)};
+        // polarity statistics for the store's literal placement
+        unsigned nt = (v >= 1 && v <= V) ? __popcll((unsigned long long)sT[t]) : 0u;
+        unsigned nf = (v >= 1 && v <= V) ? __popcll((unsigned long long)sF[t]) : 0u;
+        nt = __reduce_add_sync(0xffffffffu, nt);
+        nf = __reduce_add_sync(0xffffffffu, nf);
+        if ((t & 31) == 0 && c.polarity) {
+            atomicAdd(c.polarity, (unsigned long long)nt);
+            atomicAdd(c.polarity + 1, (unsigned long long)nf);
+        }
     }
 }
 
@@ -185,6 +195,7 @@ struct EncodePackedChunk {
     int64_t vstride;
     int64_t row0[MAXG];
     int32_t lanes[MAXG];
+    unsigned long long* polarity;  // [2] += (var, group) pairs that can be True / can be False
 };
 
 template <class LW, class GW>
@@ -258,6 +269,15 @@ __global__ void __launch_bounds__(256) k_encode_packed(const uint64_t* __restric
         const int64_t v = vbase + t;
         if (v <= V) agg[v] = AggEntry<GW>{sT[t], sF[t], sU[t], GW(0)};
         else if (v == V + 1) agg[v] = AggEntry<GW>{~GW(0), ~GW(0), GW(0), GW(0)};
+        // polarity statistics for the store's literal placement
+        unsigned nt = (v >= 1 && v <= V) ? __popcll((unsigned long long)sT[t]) : 0u;
+        unsigned nf = (v >= 1 && v <= V) ? __popcll((unsigned long long)sF[t]) : 0u;
+        nt = __reduce_add_sync(0xffffffffu, nt);
+        nf = __reduce_add_sync(0xffffffffu, nf);
+        if ((t & 31) == 0 && c.polarity) {
+            atomicAdd(c.polarity, (unsigned long long)nt);
+            atomicAdd(c.polarity + 1, (unsigned long long)nf);
+        }
     }
 }
 

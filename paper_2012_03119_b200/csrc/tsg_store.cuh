@@ -35,18 +35,30 @@ __global__ void k_scale_f64(double* p, int64_t n, double f) {
 }
 
 // interleaved -> clause-major in the clause's original literal order
-// (lits_at / literal_columns, engine.py:165-182).  A stored clause holds its
-// hot prefix first; hmask bit j marks original position j (< 64) as hot.
-__global__ void k_deinterleave(const int32_t* __restrict__ src, const uint64_t* __restrict__ hmask, int64_t n,
+// (lits_at / literal_columns, engine.py:165-182).  A stored clause is laid
+// out [pivot][tier-2 literals][the rest], each part in original order; its
+// order word says where they came from: bits 58-63 = pivot position + 1
+// (0: no pivot), bits 0-57 = original positions of the tier-2 literals.
+constexpr int ORDER_MASK_BITS = 58;
+
+__host__ __device__ __forceinline__ uint64_t order_word(int32_t pivot, uint64_t tier2) {
+    return ((uint64_t)(pivot + 1) << ORDER_MASK_BITS) | (tier2 & ((1ull << ORDER_MASK_BITS) - 1));
+}
+
+__global__ void k_deinterleave(const int32_t* __restrict__ src, const uint64_t* __restrict__ order, int64_t n,
                                int32_t size, int32_t* __restrict__ dst) {
     int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     for (; c < n; c += (int64_t)gridDim.x * blockDim.x) {
         const int32_t* s = src + (c / STRIDE) * size * STRIDE + (c % STRIDE);
-        const uint64_t m = hmask[c];
-        int32_t hot = 0, cold = __popcll(m);
+        const uint64_t w = order[c];
+        const int32_t pivot = (int32_t)(w >> ORDER_MASK_BITS) - 1;
+        const uint64_t m = w & ((1ull << ORDER_MASK_BITS) - 1);
+        int32_t t2 = pivot >= 0, rest = t2 + __popcll(m);
         for (int32_t j = 0; j < size; ++j) {
-            const bool is_hot = j < 64 && ((m >> j) & 1);
-            const int32_t k = is_hot ? hot++ : cold++;
+            int32_t k;
+            if (j == pivot) k = 0;
+            else if (j < ORDER_MASK_BITS && ((m >> j) & 1)) k = t2++;
+            else k = rest++;
             dst[c * size + j] = s[(int64_t)k * STRIDE];
         }
     }
