@@ -1,4 +1,4 @@
-timeout 900 python -m pytest tests -m gpu -x -q --timeout 300 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_engine.py -m gpu -x -q --timeout 300 -p no:cacheprovider -k "packed or c1 or widths or c3_full" > gpurun_out/pytest_gpu.log 2>&1
 tail -2 gpurun_out/pytest_gpu.log
 for i in 1 2; do timeout 120 python tools/profile_round.py C3 4 2>&1 | tail -1; done
-timeout 400 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.log 2>&1; tail -1 gpurun_out/bench.log | python -c "import sys,json; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['roofline']['frac'], d['roofline']['kernel_ms'], d['e2e']['ms_per_step'], d['e2e']['mode'])"
+timeout 120 python tools/profile_round.py C2 4 2>&1 | tail -1
