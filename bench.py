@@ -150,9 +150,41 @@ def cpu_baseline(cfg: W.Config, snaps, gl, gt, slice_clauses=2_000_000, repeats=
         dt = time.perf_counter() - t0
         rate = ctr["lane_tests"] / dt
         best = rate if best is None else max(best, rate)
-    return {"value": best, "unit": "clause_assignment_tests/s", "cores": threads, "kind": "port",
-            "sample": f"{slice_clauses} clauses of the {cfg.name} generator x {snaps.shape[0]} assignments, "
-                      f"one round, oracle/tsg_oracle.c with {threads} pthreads"}
+    out = {"value": best, "unit": "clause_assignment_tests/s", "cores": threads, "kind": "port",
+           "sample": f"{slice_clauses} clauses of the {cfg.name} generator x {snaps.shape[0]} assignments, "
+                     f"one round, oracle/tsg_oracle.c with {threads} pthreads"}
+    try:
+        out["reference_python"] = reference_python_rate(cfg, snaps)
+    except Exception as exc:  # optional side figure
+        out["reference_python"] = {"value": None, "error": repr(exc)}
+    return out
+
+
+def reference_python_rate(cfg: W.Config, snaps, n_clauses=200_000):
+    """The reference engine itself (triggersat.engine, pure Python + numpy,
+    single worker thread; baseline/_ref) on a small slice of the workload:
+    one run_round over n_clauses x the round's assignments, its own
+    lane_tests / busy_seconds (instrumentation.py:248-250).  Side figure."""
+    from paper_2012_03119_b200 import exchange as X
+    ts = X.import_reference()
+    if ts is None:
+        return {"value": None, "unavailable": "baseline/_ref not installed"}
+    from triggersat.engine import AssignmentSnapshot, Engine, EngineConfig
+    rng = np.random.default_rng(cfg.seed + 555)
+    eng = Engine(cfg.num_vars, cfg.threads, EngineConfig(lane_width=32, group_width=32,
+                                                         assignment_queue_capacity=cfg.lanes))
+    for s_, arr in W.clause_buckets(n_clauses, cfg.num_vars, rng, cfg.size_lo, cfg.size_hi).items():
+        for row in arr:
+            eng.add_clause(tuple(int(x) for x in row), origin=0)
+    eng.run_round()  # integrate the clauses (not timed)
+    for i in range(snaps.shape[0]):
+        eng.submit_assignment(AssignmentSnapshot(i // cfg.lanes, snaps[i], i))
+    t0 = time.perf_counter()
+    eng.run_round()
+    dt = time.perf_counter() - t0
+    return {"value": eng.counters["lane_tests"] / dt, "unit": "clause_assignment_tests/s", "cores": 1,
+            "kind": "reference", "sample": f"triggersat.engine.Engine.run_round, {n_clauses} clauses x "
+                                            f"{snaps.shape[0]} assignments, one round ({dt:.2f} s)"}
 
 
 def run_reference(args, cfg):
