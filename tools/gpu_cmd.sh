@@ -1,2 +1,5 @@
-for lib in libtsg.so libtsg_lock.so; do echo $lib; for i in 1 2; do TSG_LIB=$PWD/paper_2012_03119_b200/$lib timeout 120 python tools/profile_round.py C3 4 2>&1 | tail -1; done; TSG_LIB=$PWD/paper_2012_03119_b200/$lib timeout 120 python tools/profile_round.py C2 4 2>&1 | tail -1; done
-TSG_LIB=$PWD/paper_2012_03119_b200/libtsg_lock.so timeout 600 python -m pytest tests/test_gpu_engine.py -m gpu -x -q --timeout 300 -p no:cacheprovider -k "c1 or widths or multichunk or long" 2>&1 | tail -1
+timeout 900 python -m pytest tests -m gpu -x -q --timeout 300 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
+tail -1 gpurun_out/pytest_gpu.log
+START=$(date +%s); timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo "bench wall $(( $(date +%s) - START )) s"
+tail -1 gpurun_out/bench.log | python -c "import sys,json; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['roofline']['frac'], d['e2e']['ms_per_step'], d['cpu_baseline'])"
+timeout 300 python bench.py --impl reference --steps 3 --warmup 1 2>&1 | tail -1 | cut -c1-300
