@@ -498,3 +498,37 @@ def test_async_rounds_match_sync_rounds(P, cap):
         a.launch(1.0)
     a.close()
     b.close()
+
+
+def test_abi_error_paths(P):
+    # errors surface as the reference's exception types (bitpack.py:30-36,
+    # 92-103; engine.py:64-74), never as silent fallbacks
+    from paper_2012_03119_b200 import workload as W
+    from paper_2012_03119_b200.native import NativeEngine, pack_rows, packed_words
+    from paper_2012_03119_b200._lib import CapacityError
+    nv = 1000
+    e = NativeEngine(nv, 8, 4)
+    flat, offs, ids = W.flatten(W.clause_buckets(500, nv, np.random.default_rng(1), 1, 5))
+    e.add_clauses(flat, offs, ids)
+    snaps = W.snapshots(2, 8, nv, np.random.default_rng(2))
+    with pytest.raises(ValueError):  # packed pitch shorter than a row
+        e.stage_packed(np.ascontiguousarray(pack_rows(snaps, nv)[:, :packed_words(nv) - 4]))
+    with pytest.raises(CapacityError):  # more lanes than lane_width
+        e.prepare(np.array([9], np.int32), np.array([0], np.int32))
+    with pytest.raises(ValueError):  # groups need more rows than staged
+        e.stage(snaps[:4])
+        e.prepare(*W.groups_for(2, 8, 8))
+        e.encode()
+    e.stage(snaps)
+    e.prepare(*W.groups_for(2, 8, 8))
+    e.encode()
+    e.launch(1.0)
+    with pytest.raises(ValueError):  # the store is frozen while a round is in flight
+        e.add_clauses(flat[:3], np.array([0, 3], np.int64), np.array([10 ** 6], np.int64))
+    with pytest.raises(ValueError):
+        e.remove(np.array([0]))
+    r = e.collect()
+    assert r.reports == len(e.fetch(r.reports))
+    with pytest.raises(ValueError):  # nothing in flight
+        e.collect()
+    e.close()
