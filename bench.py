@@ -385,6 +385,8 @@ def main():
     if True:  # every rank, over its own PCIe link; time = max over ranks
         from paper_2012_03119_b200 import _lib
         import ctypes as C
+        eng.set_record_bytes(12)  # 12-byte egress records (lane_width 32)
+        rec_bytes = 12
         rec_buf = torch.empty((8 << 20) * 16, dtype=torch.uint8).pin_memory()
         rec_bufs = [torch.empty((8 << 20) * 16, dtype=torch.uint8).pin_memory() for _ in range(2)]
         k_step = [0]
@@ -435,7 +437,7 @@ def main():
             r = fn(k)
             eng.sync()
             _lib.check(L.tsg_fetch_wait(eng.h))
-            return (time.perf_counter() - w0) / k * 1e3, r, r.reports * 16 + 32
+            return (time.perf_counter() - w0) / k * 1e3, r, r.reports * rec_bytes + 48
 
         def timed(fn, k):
             for _ in range(2):
@@ -446,7 +448,7 @@ def main():
             d2h = 0
             for _ in range(k):
                 r = fn()
-                d2h += r.reports * 16 + 32
+                d2h += r.reports * rec_bytes + 48
             eng.sync()
             _lib.check(L.tsg_fetch_wait(eng.h))
             return (time.perf_counter() - w0) / k * 1e3, r, d2h // k

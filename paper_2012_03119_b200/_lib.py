@@ -51,6 +51,7 @@ EXPORTS = (
     "tsg_reports_device", "tsg_sync", "tsg_stream", "tsg_pack", "tsg_aggregate", "tsg_lane_trigger",
     "tsg_aggregate_trigger", "tsg_packed_words", "tsg_pack_rows", "tsg_stage_packed",
     "tsg_fetch_reports_async", "tsg_fetch_wait", "tsg_round_launch", "tsg_round_collect",
+    "tsg_set_record_bytes",
 )
 
 _lib = None
@@ -86,6 +87,7 @@ def _declare(L):
         "tsg_fetch_reports": ([P, P, I64, pI64], C.c_int),
         "tsg_fetch_reports_async": ([P, P, I64, pI64], C.c_int),
         "tsg_fetch_wait": ([P], C.c_int),
+        "tsg_set_record_bytes": ([P, I32], C.c_int),
         "tsg_round_launch": ([P, D], C.c_int),
         "tsg_round_collect": ([P, C.POINTER(tsg_round_result)], C.c_int),
         "tsg_reports_device": ([P, C.POINTER(P), pI64], C.c_int),

@@ -149,12 +149,17 @@ struct tsg_engine {
     struct Slot {
         tsg_report *out = nullptr, *out2 = nullptr;
         int64_t out_cap = 0, out2_cap = 0;
+        uint8_t* out12 = nullptr;
+        int64_t out12_cap = 0;
         cudaEvent_t ev = nullptr;   // copy-out of this slot's records done
     } alt;
     cudaEvent_t ev_cur = nullptr;   // egress event of the current slot
     bool cur_pending = false;
     cudaStream_t egress = nullptr;
     cudaEvent_t ev_ready = nullptr; // compacted records ready for copy-out
+    int32_t record_bytes = 16;      // egress record format (tsg_set_record_bytes)
+    uint8_t* out12 = nullptr;       // 12-byte egress records of the current slot
+    int64_t out12_cap = 0;
     bool oob = false;  // a stored literal may exceed num_vars (checked before testing)
     unsigned long long* ctr = nullptr;      // device [0..7]: [0..3] round counters, [4] maintenance scratch
     unsigned long long* h_ctr = nullptr;    // pinned [8]
@@ -737,7 +742,7 @@ int tsg_destroy(tsg_engine* h) {
     dfree(h, h->rows_own); dfree(h, h->prows_own); dfree(h, h->tables); dfree(h, h->d_desc); dfree(h, h->out);
     dfree(h, h->ctr); dfree(h, h->carry); dfree(h, h->out2); dfree(h, h->codes);
     if (h->egress) cudaStreamSynchronize(h->egress);
-    dfree(h, h->alt.out); dfree(h, h->alt.out2);
+    dfree(h, h->alt.out); dfree(h, h->alt.out2); dfree(h, h->alt.out12); dfree(h, h->out12);
     cudaStreamSynchronize(h->st);
     if (h->h_ctr) cudaFreeHost(h->h_ctr);
     for (cudaEvent_t e : {h->ev_cur, h->alt.ev, h->ev_ready, h->ev_done}) if (e) cudaEventDestroy(e);
@@ -1213,6 +1218,7 @@ int round_launch(tsg_engine* h, double inc, bool flip) {
     if (h->cur_pending) {  // the last round's records are still being copied out: switch record slots
         std::swap(h->out, h->alt.out); std::swap(h->out2, h->alt.out2);
         std::swap(h->out_cap, h->alt.out_cap); std::swap(h->out2_cap, h->alt.out2_cap);
+        std::swap(h->out12, h->alt.out12); std::swap(h->out12_cap, h->alt.out12_cap);
         std::swap(h->ev_cur, h->alt.ev);
         h->cur_pending = false;
         if (!h->out) {
@@ -1375,16 +1381,43 @@ int tsg_round(tsg_engine* h, const int32_t* group_lanes, const int32_t* group_ti
     return tsg_round_test(h, activity_inc, out);
 }
 
+// the source and size of the round's first k records in the egress format
+int egress_view(tsg_engine* h, int64_t k, const void** src, int64_t* bytes) {
+    if (h->record_bytes == 16 || k <= 0) {
+        *src = h->out;
+        *bytes = k * (int64_t)sizeof(tsg_report);
+        return TSG_OK;
+    }
+    CKR(dgrow(h, &h->out12, &h->out12_cap, k * 12));
+    k_pack_records12<<<grid_for(k), 256, 0, h->st>>>(h->out, k, h->out12);
+    CK(cudaGetLastError());
+    *src = h->out12;
+    *bytes = k * 12;
+    return TSG_OK;
+}
+
 int tsg_fetch_reports(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n) {
     CKR(validate_handle(h));
     DevGuard g(h->dev);
     CKR(compact_reports(h));
     int64_t k = std::min(cap, h->n_out);
     if (k > 0) {
-        CK(cudaMemcpyAsync(out, h->out, k * sizeof(tsg_report), cudaMemcpyDeviceToHost, h->st));
+        const void* src = nullptr;
+        int64_t bytes = 0;
+        CKR(egress_view(h, k, &src, &bytes));
+        CK(cudaMemcpyAsync(out, src, bytes, cudaMemcpyDeviceToHost, h->st));
         CK(cudaStreamSynchronize(h->st));
     }
     *n = k;
+    return TSG_OK;
+}
+
+int tsg_set_record_bytes(tsg_engine* h, int32_t bytes) {
+    CKR(validate_handle(h));
+    if (bytes != 16 && bytes != 12) return fail(TSG_EINVAL, "record bytes must be 16 or 12, got %d", bytes);
+    if (bytes == 12 && h->cfg.lane_width > 32)
+        return fail(TSG_EINVAL, "12-byte records carry a 32-bit lane mask: lane_width %d > 32", h->cfg.lane_width);
+    h->record_bytes = bytes;
     return TSG_OK;
 }
 
@@ -1395,9 +1428,12 @@ int tsg_fetch_reports_async(tsg_engine* h, tsg_report* out, int64_t cap, int64_t
     const int64_t k = std::min(cap, h->n_out);
     *n = k;
     if (k <= 0) return TSG_OK;
+    const void* src = nullptr;
+    int64_t bytes = 0;
+    CKR(egress_view(h, k, &src, &bytes));
     CK(cudaEventRecord(h->ev_ready, h->st));
     CK(cudaStreamWaitEvent(h->egress, h->ev_ready, 0));
-    CK(cudaMemcpyAsync(out, h->out, k * sizeof(tsg_report), cudaMemcpyDeviceToHost, h->egress));
+    CK(cudaMemcpyAsync(out, src, bytes, cudaMemcpyDeviceToHost, h->egress));
     CK(cudaEventRecord(h->ev_cur, h->egress));
     h->cur_pending = true;
     return TSG_OK;

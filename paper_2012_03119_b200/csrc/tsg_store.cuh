@@ -6,6 +6,7 @@
 #include <cstdint>
 
 #include "tsg_device.cuh"
+#include "../../include/tsg.h"
 
 namespace tsg {
 
@@ -61,6 +62,19 @@ __global__ void k_deinterleave(const int32_t* __restrict__ src, const uint64_t* 
             else k = rest++;
             dst[c * size + j] = s[(int64_t)k * STRIDE];
         }
+    }
+}
+
+// 16-byte report records -> 12-byte egress records {key, 32-bit lane mask}
+// (lane_width <= 32), three 4-byte words each
+__global__ void k_pack_records12(const tsg_report* __restrict__ in, int64_t n, uint8_t* __restrict__ out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const tsg_report r = in[i];
+        uint32_t* o = reinterpret_cast<uint32_t*>(out + i * 12);
+        o[0] = (uint32_t)r.key;
+        o[1] = (uint32_t)(r.key >> 32);
+        o[2] = (uint32_t)r.lane_mask;
     }
 }
 

@@ -203,6 +203,10 @@ class Engine:
         w = C.c_int64(0)
         check(self._L.tsg_packed_words(num_vars, C.byref(w)))
         self._packed_words = w.value
+        self._rec_dtype = REPORT_DTYPE
+        if self.config.lane_width <= 32:  # 12-byte egress records: a quarter fewer bytes D2H
+            check(self._L.tsg_set_record_bytes(self._h, 12))
+            self._rec_dtype = _reports.RECORD12_DTYPE
         self.store = DeviceClauseStore(self)
         self._lits: Dict[int, tuple] = {}
         self._size_rank: Dict[int, int] = {}
@@ -458,7 +462,7 @@ class Engine:
         return result
 
     def _fetch(self, n: int) -> np.ndarray:
-        recs = np.zeros(n, dtype=REPORT_DTYPE)
+        recs = np.zeros(n, dtype=self._rec_dtype)
         if n:
             got = C.c_int64(0)
             check(self._L.tsg_fetch_reports(self._h, ptr(recs), n, C.byref(got)))

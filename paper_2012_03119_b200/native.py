@@ -175,10 +175,17 @@ class NativeEngine:
         check(self.L.tsg_round(self.h, ptr(gl), ptr(gt), len(gl), activity_inc, C.byref(res)))
         return res
 
+    record_bytes = 16
+
+    def set_record_bytes(self, nbytes: int) -> None:
+        """Egress record format: 16 (tsg_report) or 12 (lane_width <= 32)."""
+        check(self.L.tsg_set_record_bytes(self.h, nbytes))
+        self.record_bytes = nbytes
+
     def fetch_raw(self, n: int, out: Optional[np.ndarray] = None) -> np.ndarray:
-        """The round's 16-byte records (include/tsg.h tsg_report)."""
+        """The round's records in the egress format (tsg_report, or 12-byte)."""
         if out is None or len(out) < n:
-            out = np.zeros(max(n, 1), REPORT_DTYPE)
+            out = np.zeros(max(n, 1), REPORT_DTYPE if self.record_bytes == 16 else reports.RECORD12_DTYPE)
         got = C.c_int64(0)
         if n:
             check(self.L.tsg_fetch_reports(self.h, ptr(out), n, C.byref(got)))

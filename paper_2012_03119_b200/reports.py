@@ -14,6 +14,9 @@ from typing import Dict, Mapping
 import numpy as np
 
 RECORD_DTYPE = np.dtype([("key", "<u8"), ("lane_mask", "<u8")])
+# 12-byte egress records (tsg_set_record_bytes(h, 12), lane_width <= 32)
+RECORD12_DTYPE = np.dtype({"names": ["key", "lane_mask"], "formats": ["<u8", "<u4"], "offsets": [0, 8],
+                           "itemsize": 12})
 PAD_KEY = np.uint64(0xFFFFFFFFFFFFFFFF)
 DECODED_DTYPE = np.dtype([("engine_id", "<i8"), ("group", "<i4"), ("lane_mask", "<u8")])
 

@@ -532,3 +532,37 @@ def test_abi_error_paths(P):
     with pytest.raises(ValueError):  # nothing in flight
         e.collect()
     e.close()
+
+
+def test_twelve_byte_egress_records(P):
+    # 12-byte egress records carry the same (engine id, group, lane mask) as
+    # the 16-byte tsg_report, sync and async; lane_width 64 refuses them
+    from paper_2012_03119_b200 import reports as R
+    from paper_2012_03119_b200 import workload as W
+    from paper_2012_03119_b200.native import NativeEngine
+    rng = np.random.default_rng(21)
+    nv = 2000
+    flat, offs, ids = W.flatten(W.clause_buckets(30_000, nv, rng, 1, 8))
+    snaps = W.snapshots(3, 32, nv, rng)
+    gl, gt = W.groups_for(3, 32)
+    out = []
+    for nbytes in (16, 12):
+        e = NativeEngine(nv)
+        e.set_record_bytes(nbytes)
+        e.add_clauses(flat, offs, ids)
+        e.stage(snaps)
+        r = e.round(gl, gt, 1.0)
+        sync = np.sort(R.decode(e.fetch_raw(r.reports)), order=["engine_id", "group"])
+        buf = np.zeros(r.reports, R.RECORD12_DTYPE if nbytes == 12 else R.RECORD_DTYPE)
+        assert e.fetch_async(buf) == r.reports
+        e.wait()
+        out.append((sync, np.sort(R.decode(buf), order=["engine_id", "group"])))
+        e.close()
+    assert len(out[0][0]) > 100
+    for a in out:
+        for b in out:
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    w = NativeEngine(nv, 64, 32)
+    with pytest.raises(ValueError):
+        w.set_record_bytes(12)
+    w.close()

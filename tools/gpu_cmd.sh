@@ -1,1 +1,4 @@
-timeout 600 python -m pytest tests/test_gpu_engine.py -m gpu -x -q --timeout 300 -p no:cacheprovider -k "error_paths or async" 2>&1 | tail -15
+timeout 900 python -m pytest tests -m gpu -x -q --timeout 300 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
+tail -1 gpurun_out/pytest_gpu.log
+timeout 600 python bench.py > gpurun_out/bench.log 2>&1
+tail -1 gpurun_out/bench.log | python -c "import sys,json; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['roofline']['frac'], json.dumps(d['e2e']))"
