@@ -1,4 +1,1 @@
-timeout 900 python -m pytest tests -m gpu -x -q --timeout 300 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
-tail -1 gpurun_out/pytest_gpu.log
-timeout 600 python bench.py > gpurun_out/bench.log 2>&1
-tail -1 gpurun_out/bench.log | python -c "import sys,json; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['roofline']['frac'], json.dumps(d['e2e']))"
+for lib in paper_2012_03119_b200/libtsg*.so; do echo "== $lib"; for i in 1 2; do TSG_LIB=$PWD/$lib timeout 120 python tools/profile_round.py C3 4 2>&1 | tail -1 | cut -c1-110; done; done
