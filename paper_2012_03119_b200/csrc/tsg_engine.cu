@@ -1259,8 +1259,9 @@ int round_launch(tsg_engine* h, double inc, bool flip) {
         if (timing) CK(cudaEventRecord(h->ev_tst[h->fl_slot][0], h->st));
         CKR(run_tests(h, h->fl, h->fl_slot, inc, 0));
         if (timing) CK(cudaEventRecord(h->ev_tst[h->fl_slot][1], h->st));
-        CK(cudaMemcpyAsync(h->h_ctr, h->ctr, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
-        CK(cudaMemcpyAsync(h->h_ctr + 6, h->ctr + 6, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
+        // round counters [0..3] and polarity counts [6..7] in one copy ([4..5]
+        // are maintenance scratch, idle during a round)
+        CK(cudaMemcpyAsync(h->h_ctr, h->ctr, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
         CK(cudaEventRecord(h->ev_done, h->st));
     }
     h->inflight = true;
