@@ -525,7 +525,11 @@ def main():
                                    f"seed {cfg.seed}",
                        "clauses_per_gpu": cfg.n_clauses, "assignments": A, "groups": G, "num_vars": cfg.num_vars,
                        "sum_literals_per_gpu": sum_lits, "reports_per_step": P,
-                       "l2": "inputs larger than L2 (640 MB clause DB + 205 MB snapshots per GPU vs 126 MB L2)",
+                       "l2": (f"inputs larger than L2 ({4 * sum_lits / 1e6:.0f} MB clause literals + "
+                              f"{A * pw * 8 / 1e6:.0f} MB packed snapshot rows per GPU vs 126 MB L2)"
+                              if 4 * sum_lits + A * pw * 8 > 126e6 else
+                              f"inputs fit in L2 ({4 * sum_lits / 1e6:.0f} MB + {A * pw * 8 / 1e6:.0f} MB): "
+                              f"a parity config, not the headline workload (C3)"),
                        "parallelism": "1 GPU" if world == 1 else (
                            f"clause shards x{world}; tables broadcast from rank 0 (NCCL)" if args.tables == "bcast"
                            else f"clause shards x{world}; every rank encodes the round's tables from its copy of "
