@@ -310,20 +310,21 @@ def main():
         return eng.test(1.0)
 
     def run_steps(n, record):
-        """n rounds.  One GPU: device rounds back to back -- round i+1 is
-        encoded (into the other table slot) before round i is collected
-        (tsg_round_launch / tsg_round_collect), so the GPU does not idle on
-        the host between rounds.  N GPUs: encode, NCCL broadcast, test."""
+        """n rounds.  Device rounds back to back with two in flight: round
+        i is encoded and launched (tsg_round_launch) before round i-1 is
+        collected (tsg_round_collect), so the GPU always has the next round
+        queued.  --tables bcast: encode, NCCL broadcast, test."""
         if tables_t is not None:
             for _ in range(n):
                 record(step())
             return
-        for i in range(n):
+        for i in range(n):  # two rounds in flight
+            if i >= 2:
+                record(eng.collect())  # round i-2 owns the table slot round i encodes into
             eng.encode()
-            if i:
-                record(eng.collect())
             eng.launch(1.0)
-        record(eng.collect())
+        for _ in range(min(n, 2)):
+            record(eng.collect())
 
     run_steps(args.warmup, lambda r: None)
     eng.sync()

@@ -162,10 +162,13 @@ int tsg_round_tables(tsg_engine* h, void** device_ptr, int64_t* bytes);
 int tsg_round_test(tsg_engine* h, double activity_inc, tsg_round_result* out);
 /* Asynchronous test (device rounds back to back): tsg_round_launch queues
  * the test of the prepared, encoded round and returns; the next round may
- * then be staged, prepared and encoded (into the other of two table slots)
- * before tsg_round_collect waits for the launched round's figures -- so the
- * GPU never idles on the host between rounds.  One launched round at a
- * time; the store must not change until it is collected (TSG_EINVAL). */
+ * then be staged, prepared, encoded (into the other of two table slots) and
+ * launched before tsg_round_collect waits for the OLDEST launched round's
+ * figures -- so the GPU always has the next round queued.  Up to two rounds
+ * in flight, each with its own table slot, counters and record buffers; a
+ * round must be collected before its table slot is encoded again, and the
+ * store must not change while any round is in flight (TSG_EINVAL).  The
+ * fetch calls read the records of the last collected round. */
 int tsg_round_launch(tsg_engine* h, double activity_inc);
 int tsg_round_collect(tsg_engine* h, tsg_round_result* out);
 int tsg_fetch_reports(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n);

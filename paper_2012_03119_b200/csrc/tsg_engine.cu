@@ -117,20 +117,39 @@ struct tsg_engine {
     uint64_t* prows_own = nullptr;
     int64_t prows_cap = 0, ppitch = 0;
 
-    // round description: `rd` as prepared, `fl` of the launched round
-    RoundDesc rd, fl;
+    // round description as prepared
+    RoundDesc rd;
     // round tables: two slots of tables_bytes each (slot stride slot_bytes);
     // encode writes slot `tslot`; tsg_round_launch flips it, so the next
     // round encodes while the launched one still owns its tables
     int8_t* tables = nullptr;
     int64_t tables_cap = 0, tables_bytes = 0, slot_bytes = 0;
     int tslot = 0;
-    bool inflight = false;       // launched, not collected
-    int fl_slot = 0;
-    double fl_inc = 0.0;
-    cudaEvent_t ev_done = nullptr;        // counters of the launched round are on the host
     cudaEvent_t ev_enc[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // per table slot: encode start/end
-    cudaEvent_t ev_tst[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // per table slot: test start/end
+
+    // Two round states alternate: a launched round keeps its
+    // group description, table slot, counters, carry stamps and record
+    // buffers until it is collected, so up to two rounds are in flight and
+    // the next round is queued before the previous one is collected.
+    struct RoundState {
+        RoundDesc fl;
+        int slot = 0;                         // table slot it tests
+        double inc = 0.0;
+        int64_t seq = 0;                      // launch sequence: carry stamps, collect order
+        int32_t run = 0;                      // 0: the round's test; 1, 2, ...: emission replays
+        bool inflight = false;                // launched, not collected
+        unsigned long long* ctr = nullptr;    // device [8]: [0..3] round counters, [6..7] polarity counts
+        unsigned long long* h_ctr = nullptr;  // pinned [8]
+        cudaEvent_t ev_done = nullptr;        // its counters are on the host
+        cudaEvent_t ev_tst[2] = {nullptr, nullptr};
+        int64_t* carry = nullptr;             // per-clause (round, tid) stamps of multi-chunk rounds
+        int64_t carry_cap = 0;
+    } rs[2];
+    int next_rs = 0;                      // state of the next launch
+    int fetch_rs = 0;                     // state the fetch calls read (the last collected)
+    int report_rs = 0;                    // state whose record buffers are in the fields below
+    unsigned long long* mctr = nullptr;   // device [8]: maintenance scratch (reduce, remove, range check)
+    unsigned long long* h_mctr = nullptr; // pinned [8]
 
     BucketDesc* d_desc = nullptr;
     int64_t desc_cap = 0;
@@ -142,29 +161,25 @@ struct tsg_engine {
     tsg_report* out2 = nullptr;             // compaction target for fetch
     int64_t out2_cap = 0;
     bool compacted = true;
-    // report egress (tsg_fetch_reports_async): the record buffers above are one
-    // of two slots; `alt` is the other.  A round whose records are being copied
-    // out on the egress stream hands its slot over, and the next round writes
-    // the other one; a slot is rewritten only after its copy-out event.
+    // record buffers: the fields above belong to round state `report_rs`,
+    // `alt` to the other one (use_reports swaps them); a state's buffers are
+    // rewritten only after their copy-out event (tsg_fetch_reports_async).
     struct Slot {
         tsg_report *out = nullptr, *out2 = nullptr;
         int64_t out_cap = 0, out2_cap = 0;
         uint8_t* out12 = nullptr;
         int64_t out12_cap = 0;
-        cudaEvent_t ev = nullptr;   // copy-out of this slot's records done
+        cudaEvent_t ev = nullptr;   // copy-out of these records done
+        int64_t n_out = 0, n_alloc = 0;
+        bool compacted = true;
     } alt;
-    cudaEvent_t ev_cur = nullptr;   // egress event of the current slot
-    bool cur_pending = false;
+    cudaEvent_t ev_cur = nullptr;   // copy-out of the current buffers done
     cudaStream_t egress = nullptr;
     cudaEvent_t ev_ready = nullptr; // compacted records ready for copy-out
     int32_t record_bytes = 16;      // egress record format (tsg_set_record_bytes)
     uint8_t* out12 = nullptr;       // 12-byte egress records of the current slot
     int64_t out12_cap = 0;
     bool oob = false;  // a stored literal may exceed num_vars (checked before testing)
-    unsigned long long* ctr = nullptr;      // device [0..7]: [0..3] round counters, [4] maintenance scratch
-    unsigned long long* h_ctr = nullptr;    // pinned [8]
-    int64_t* carry = nullptr;
-    int64_t carry_cap = 0;
     int64_t round_seq = 0;
     int64_t grid[32] = {0};       // persistent grid per k_test variant
     int64_t grid_smem[32];        // shared-memory size the grid was computed for (-1: none)
@@ -210,6 +225,8 @@ struct DevGuard {
         if (prev >= 0 && cur != prev) cudaSetDevice(prev);
     }
 };
+
+bool any_inflight(const tsg_engine* h) { return h->rs[0].inflight || h->rs[1].inflight; }
 
 int dalloc(tsg_engine* h, void** p, int64_t bytes) {
     *p = nullptr;
@@ -300,7 +317,7 @@ int launch_encode(tsg_engine* h, int c) {
         ec.row0[g] = rd.grow0[g0 + g];
         ec.lanes[g] = rd.glanes[g0 + g];
     }
-    ec.polarity = h->ctr + 6;
+    ec.polarity = h->rs[h->next_rs].ctr + 6;  // counted for the round this encode feeds
     int8_t* tab = h->tables + h->tslot * h->slot_bytes;
     auto* agg = reinterpret_cast<AggEntry<GW>*>(tab + rd.chunk_off[c]);
     auto* lane = reinterpret_cast<LaneEntry<LW>*>(tab + rd.chunk_off[c] + agg_bytes(h));
@@ -374,7 +391,10 @@ int launch_slab(tsg_engine* h, const TestParams<LW, GW>& p) {
 }
 
 template <class LW, class GW>
-int launch_test(tsg_engine* h, const RoundDesc& rd, int slot, int c, double inc, int emit_only) {
+int launch_test(tsg_engine* h, int k, int c, double inc, int emit_only) {
+    const auto& R = h->rs[k];
+    const RoundDesc& rd = R.fl;
+    const int slot = R.slot;
     TestParams<LW, GW> p{};
     int32_t g0 = c * h->cfg.group_width;
     int32_t G = std::min(h->cfg.group_width, rd.n_groups - g0);
@@ -391,10 +411,12 @@ int launch_test(tsg_engine* h, const RoundDesc& rd, int slot, int c, double inc,
     p.group_mask = width_mask<GW>(G);
     p.inc = inc;
     p.out = h->out;
-    p.ctr = h->ctr;
+    p.ctr = R.ctr;
     p.out_cap = h->out_cap;
-    p.carry = h->carry;
-    p.stamp_base = (h->round_seq & 0x7fffffff) << 32;
+    p.carry = R.carry;
+    // carry stamps are unique per (round, run): a replay must not see the
+    // stamps its own round's first run left behind
+    p.stamp_base = (((R.seq << 6) | (R.run & 63)) & 0x7fffffff) << 32;
     p.carry_in_tid = (c > 0 && rd.gtid[g0] == rd.gtid[g0 - 1]) ? rd.gtid[g0] : -1;
     p.carry_out_tid = (g0 + G < rd.n_groups && rd.gtid[g0 + G - 1] == rd.gtid[g0 + G]) ? rd.gtid[g0 + G - 1] : -1;
     p.emit_only = emit_only;
@@ -433,11 +455,12 @@ int launch_test(tsg_engine* h, const RoundDesc& rd, int slot, int c, double inc,
     return launch_kernel<LW, GW, GlobalTable<GW>, TEST_THREADS, TSG_TEST_MIN_BLOCKS>(h, p, 0, 0);
 }
 
-int run_tests(tsg_engine* h, const RoundDesc& rd, int slot, double inc, int emit_only) {
-    for (int c = 0; c < rd.n_chunks; ++c) {
+// the round of state k (its record buffers must be the active ones)
+int run_tests(tsg_engine* h, int k, double inc, int emit_only) {
+    for (int c = 0; c < h->rs[k].fl.n_chunks; ++c) {
         int r;
-        if (wide_lane(h)) r = wide_group(h) ? launch_test<uint64_t, uint64_t>(h, rd, slot, c, inc, emit_only) : launch_test<uint64_t, uint32_t>(h, rd, slot, c, inc, emit_only);
-        else r = wide_group(h) ? launch_test<uint32_t, uint64_t>(h, rd, slot, c, inc, emit_only) : launch_test<uint32_t, uint32_t>(h, rd, slot, c, inc, emit_only);
+        if (wide_lane(h)) r = wide_group(h) ? launch_test<uint64_t, uint64_t>(h, k, c, inc, emit_only) : launch_test<uint64_t, uint32_t>(h, k, c, inc, emit_only);
+        else r = wide_group(h) ? launch_test<uint32_t, uint64_t>(h, k, c, inc, emit_only) : launch_test<uint32_t, uint32_t>(h, k, c, inc, emit_only);
         if (r) return r;
     }
     return TSG_OK;
@@ -635,7 +658,9 @@ struct ValidReport {
 // squeeze the padding slots out of the round's records (order-preserving)
 int compact_reports(tsg_engine* h) {
     if (h->compacted) return TSG_OK;
-    CKR(dgrow(h, &h->out2, &h->out2_cap, std::max<int64_t>(h->n_out, 1)));
+    // the compacted buffer becomes the round state's record buffer: it must
+    // not shrink below the current capacity, or the next round overflows
+    CKR(dgrow(h, &h->out2, &h->out2_cap, std::max<int64_t>(h->out_cap, 1)));
     int64_t* nsel = nullptr;
     CKR(dalloc(h, (void**)&nsel, 8));
     size_t tb = 0;
@@ -722,11 +747,16 @@ int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
     cudaEventCreateWithFlags(&h->ev_cur, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&h->alt.ev, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&h->ev_ready, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&h->ev_done, cudaEventDisableTiming);
     for (int sl = 0; sl < 2; ++sl)
-        for (int k = 0; k < 2; ++k) { cudaEventCreate(&h->ev_enc[sl][k]); cudaEventCreate(&h->ev_tst[sl][k]); }
-    if (cudaMallocHost(&h->h_ctr, 8 * sizeof(unsigned long long)) != cudaSuccess) { delete h; return fail(TSG_ECUDA, "pinned alloc"); }
-    if (dalloc(h, (void**)&h->ctr, 8 * sizeof(unsigned long long))) { delete h; return TSG_ENOMEM; }
+        for (int k = 0; k < 2; ++k) cudaEventCreate(&h->ev_enc[sl][k]);
+    for (auto& R : h->rs) {
+        cudaEventCreateWithFlags(&R.ev_done, cudaEventDisableTiming);
+        for (auto& e : R.ev_tst) cudaEventCreate(&e);
+        if (cudaMallocHost(&R.h_ctr, 8 * sizeof(unsigned long long)) != cudaSuccess) { delete h; return fail(TSG_ECUDA, "pinned alloc"); }
+        if (dalloc(h, (void**)&R.ctr, 8 * sizeof(unsigned long long))) { delete h; return TSG_ENOMEM; }
+    }
+    if (cudaMallocHost(&h->h_mctr, 8 * sizeof(unsigned long long)) != cudaSuccess) { delete h; return fail(TSG_ECUDA, "pinned alloc"); }
+    if (dalloc(h, (void**)&h->mctr, 8 * sizeof(unsigned long long))) { delete h; return TSG_ENOMEM; }
     h->out_cap = cfg->report_capacity > 0 ? std::min<int64_t>(cfg->report_capacity, INT32_MAX / 2) : (1 << 16);
     if (dalloc(h, (void**)&h->out, h->out_cap * (int64_t)sizeof(tsg_report))) { delete h; return TSG_ENOMEM; }
     *out = h;
@@ -740,17 +770,21 @@ int tsg_destroy(tsg_engine* h) {
     for_parts(h, [&](Bucket&, Part& p) { part_free(h, p); });
     dfree(h, h->d_slab_tile0);
     dfree(h, h->rows_own); dfree(h, h->prows_own); dfree(h, h->tables); dfree(h, h->d_desc); dfree(h, h->out);
-    dfree(h, h->ctr); dfree(h, h->carry); dfree(h, h->out2); dfree(h, h->codes);
+    dfree(h, h->mctr); dfree(h, h->out2); dfree(h, h->codes);
+    for (auto& R : h->rs) { dfree(h, R.ctr); dfree(h, R.carry); }
     if (h->egress) cudaStreamSynchronize(h->egress);
     dfree(h, h->alt.out); dfree(h, h->alt.out2); dfree(h, h->alt.out12); dfree(h, h->out12);
     cudaStreamSynchronize(h->st);
-    if (h->h_ctr) cudaFreeHost(h->h_ctr);
-    for (cudaEvent_t e : {h->ev_cur, h->alt.ev, h->ev_ready, h->ev_done}) if (e) cudaEventDestroy(e);
+    if (h->h_mctr) cudaFreeHost(h->h_mctr);
+    for (cudaEvent_t e : {h->ev_cur, h->alt.ev, h->ev_ready}) if (e) cudaEventDestroy(e);
+    for (auto& R : h->rs) {
+        if (R.h_ctr) cudaFreeHost(R.h_ctr);
+        if (R.ev_done) cudaEventDestroy(R.ev_done);
+        for (auto& e : R.ev_tst) if (e) cudaEventDestroy(e);
+    }
     for (int sl = 0; sl < 2; ++sl)
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < 2; ++k)
             if (h->ev_enc[sl][k]) cudaEventDestroy(h->ev_enc[sl][k]);
-            if (h->ev_tst[sl][k]) cudaEventDestroy(h->ev_tst[sl][k]);
-        }
     if (h->egress) cudaStreamDestroy(h->egress);
     cudaStreamDestroy(h->st);
     delete h;
@@ -760,7 +794,7 @@ int tsg_destroy(tsg_engine* h) {
 int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, int64_t n,
                     const int64_t* ids, const int32_t* origins, double activity) {
     CKR(validate_handle(h));
-    if (h->inflight) return fail(TSG_EINVAL, "the store cannot change while a launched round is not collected");
+    if (any_inflight(h)) return fail(TSG_EINVAL, "the store cannot change while a launched round is not collected");
     h->desc_dirty = true;
     if (n <= 0) return TSG_OK;
     if (!offsets || !ids || !origins) return fail(TSG_EINVAL, "null argument");
@@ -917,7 +951,7 @@ int tsg_bucket_read(tsg_engine* h, int32_t bi, int32_t* lits, int64_t* ids, int3
 
 int tsg_scale_activities(tsg_engine* h, double factor) {
     CKR(validate_handle(h));
-    if (h->inflight) return fail(TSG_EINVAL, "the store cannot change while a launched round is not collected");
+    if (any_inflight(h)) return fail(TSG_EINVAL, "the store cannot change while a launched round is not collected");
     DevGuard g(h->dev);
     for_parts(h, [&](Bucket&, Part& p) {
         if (p.count) k_scale_f64<<<grid_for(p.count), 256, 0, h->st>>>(p.acts, p.count, factor);
@@ -928,7 +962,7 @@ int tsg_scale_activities(tsg_engine* h, double factor) {
 
 int tsg_reduce(tsg_engine* h, int64_t eligible_below, int64_t target, int64_t* removed, int64_t* removed_ids) {
     CKR(validate_handle(h));
-    if (h->inflight) return fail(TSG_EINVAL, "the store cannot change while a launched round is not collected");
+    if (any_inflight(h)) return fail(TSG_EINVAL, "the store cannot change while a launched round is not collected");
     h->desc_dirty = true;
     DevGuard g(h->dev);
     *removed = 0;
@@ -942,14 +976,14 @@ int tsg_reduce(tsg_engine* h, int64_t eligible_below, int64_t target, int64_t* r
     CKR(dalloc(h, (void**)&ka2, total * 8)); CKR(dalloc(h, (void**)&ki2, total * 8));
     CKR(dalloc(h, (void**)&ix, total * 8)); CKR(dalloc(h, (void**)&ix2, total * 8));
     CKR(dalloc(h, (void**)&keep, total));
-    CK(cudaMemsetAsync(h->ctr + 4, 0, 8, h->st));
+    CK(cudaMemsetAsync(h->mctr + 4, 0, 8, h->st));
     {
         size_t pi = 0;
         for_parts(h, [&](Bucket&, Part& p) {
             const int64_t pb = base[pi++];
             if (p.count)
                 k_reduce_keys<<<grid_for(p.count), 256, 0, h->st>>>(p.acts, p.ids, p.count, pb, eligible_below,
-                                                                    ka, ki, ix, h->ctr + 4);
+                                                                    ka, ki, ix, h->mctr + 4);
         });
     }
     CK(cudaGetLastError());
@@ -964,7 +998,7 @@ int tsg_reduce(tsg_engine* h, int64_t eligible_below, int64_t target, int64_t* r
     CK(cudaGetLastError());
     CK(cub::DeviceRadixSort::SortPairs(tmp, tb, ka2, ka, ix2, ix, total, 0, 64, h->st));
     unsigned long long n_el = 0;
-    CK(cudaMemcpyAsync(&n_el, h->ctr + 4, 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaMemcpyAsync(&n_el, h->mctr + 4, 8, cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
     int64_t rem = std::min<int64_t>(target, (int64_t)n_el);
     if (rem > 0) {
@@ -984,7 +1018,7 @@ int tsg_reduce(tsg_engine* h, int64_t eligible_below, int64_t target, int64_t* r
 
 int tsg_remove_clauses(tsg_engine* h, const int64_t* ids, int64_t n, int64_t* removed) {
     CKR(validate_handle(h));
-    if (h->inflight) return fail(TSG_EINVAL, "the store cannot change while a launched round is not collected");
+    if (any_inflight(h)) return fail(TSG_EINVAL, "the store cannot change while a launched round is not collected");
     h->desc_dirty = true;
     DevGuard g(h->dev);
     *removed = 0;
@@ -998,18 +1032,18 @@ int tsg_remove_clauses(tsg_engine* h, const int64_t* ids, int64_t n, int64_t* re
     CKR(dalloc(h, (void**)&d_del, n * 8));
     CKR(dalloc(h, (void**)&keep, total));
     CK(cudaMemcpyAsync(d_del, del.data(), n * 8, cudaMemcpyHostToDevice, h->st));
-    CK(cudaMemsetAsync(h->ctr + 4, 0, 8, h->st));
+    CK(cudaMemsetAsync(h->mctr + 4, 0, 8, h->st));
     {
         size_t pi = 0;
         for_parts(h, [&](Bucket&, Part& p) {
             const int64_t pb = base[pi++];
             if (p.count)
-                k_mark_deleted<<<grid_for(p.count), 256, 0, h->st>>>(p.ids, p.count, pb, d_del, n, keep, h->ctr + 4);
+                k_mark_deleted<<<grid_for(p.count), 256, 0, h->st>>>(p.ids, p.count, pb, d_del, n, keep, h->mctr + 4);
         });
     }
     CK(cudaGetLastError());
     unsigned long long gone = 0;
-    CK(cudaMemcpyAsync(&gone, h->ctr + 4, 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaMemcpyAsync(&gone, h->mctr + 4, 8, cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
     if (gone) CKR(compact_all(h, keep, base));
     dfree(h, d_del); dfree(h, keep);
@@ -1169,10 +1203,16 @@ int tsg_round_prepare(tsg_engine* h, const int32_t* group_lanes, const int32_t* 
     const int64_t one_chunk = agg_bytes(h) + round_up(vstride(h) * h->cfg.group_width * lane_entry_bytes(h), 256);
     const int64_t slot = std::max(h->slot_bytes, round_up(std::max(off, one_chunk), 4096));
     if (slot != h->slot_bytes) {
-        if (h->inflight) return fail(TSG_EINVAL, "collect the launched round before preparing a larger one");
+        // grow both slots; stream order keeps in-flight rounds valid: their
+        // kernels precede the copy, and a later replay reads the moved slot
+        int8_t* nt = nullptr;
+        CKR(dalloc(h, (void**)&nt, 2 * slot));
+        if (h->tables && any_inflight(h))
+            for (int i = 0; i < 2; ++i)
+                CK(cudaMemcpyAsync(nt + i * slot, h->tables + i * h->slot_bytes, h->slot_bytes,
+                                   cudaMemcpyDeviceToDevice, h->st));
         dfree(h, h->tables);
-        h->tables = nullptr;
-        CKR(dalloc(h, (void**)&h->tables, 2 * slot));
+        h->tables = nt;
         h->tables_cap = 2 * slot;
         h->slot_bytes = slot;
         h->persist_base = nullptr;
@@ -1211,86 +1251,108 @@ void persist_tables(tsg_engine* h) {
         cudaGetLastError();
 }
 
-// Launch the test of the prepared, encoded round (table slot h->tslot): the
-// kernels and the counter copy-out are queued, nothing waits.
+// Make round state k's record buffers the active ones (the fields of
+// tsg_engine); the other state's buffers wait in `alt`.
+void use_reports(tsg_engine* h, int k) {
+    if (h->report_rs == k) return;
+    std::swap(h->out, h->alt.out); std::swap(h->out2, h->alt.out2);
+    std::swap(h->out_cap, h->alt.out_cap); std::swap(h->out2_cap, h->alt.out2_cap);
+    std::swap(h->out12, h->alt.out12); std::swap(h->out12_cap, h->alt.out12_cap);
+    std::swap(h->ev_cur, h->alt.ev);
+    std::swap(h->n_out, h->alt.n_out); std::swap(h->n_alloc, h->alt.n_alloc);
+    std::swap(h->compacted, h->alt.compacted);
+    h->report_rs = k;
+}
+
+// Launch the test of the prepared, encoded round (table slot h->tslot) in
+// the next round state: kernels, counter copy-out and its event are queued,
+// nothing waits.  At most two rounds are in flight.
 int round_launch(tsg_engine* h, double inc, bool flip) {
-    if (h->inflight) return fail(TSG_EINVAL, "a launched round has not been collected");
-    if (h->cur_pending) {  // the last round's records are still being copied out: switch record slots
-        std::swap(h->out, h->alt.out); std::swap(h->out2, h->alt.out2);
-        std::swap(h->out_cap, h->alt.out_cap); std::swap(h->out2_cap, h->alt.out2_cap);
-        std::swap(h->out12, h->alt.out12); std::swap(h->out12_cap, h->alt.out12_cap);
-        std::swap(h->ev_cur, h->alt.ev);
-        h->cur_pending = false;
-        if (!h->out) {
-            h->out_cap = h->alt.out_cap;
-            CKR(dalloc(h, (void**)&h->out, h->out_cap * (int64_t)sizeof(tsg_report)));
-        }
+    const int k = h->next_rs;
+    auto& R = h->rs[k];
+    if (R.inflight) return fail(TSG_EINVAL, "two rounds are in flight: collect one first");
+    for (const auto& Q : h->rs)
+        if (Q.inflight && Q.slot == h->tslot)
+            return fail(TSG_EINVAL, "table slot %d still belongs to an uncollected round", h->tslot);
+    use_reports(h, k);
+    if (!h->out) {
+        h->out_cap = std::max<int64_t>(h->alt.out_cap, 1 << 16);
+        CKR(dalloc(h, (void**)&h->out, h->out_cap * (int64_t)sizeof(tsg_report)));
     }
-    // the record slot about to be written may have been handed to the egress
-    // stream two rounds ago: its copy-out must finish first (no-op if never recorded)
+    // this state's buffers may still be copying out from two rounds ago
+    // (no-op if never recorded)
     CK(cudaStreamWaitEvent(h->st, h->ev_cur, 0));
     h->n_out = 0;
     h->n_alloc = 0;
     h->compacted = true;
-    h->round_seq++;
-    h->fl = h->rd;
-    h->fl_slot = h->tslot;
-    h->fl_inc = inc;
-    if (h->fl.n_chunks && h->oob) {  // out-of-range literal stored: numpy would raise IndexError
-        CK(cudaMemsetAsync(h->ctr + 4, 0, 8, h->st));
+    R.fl = h->rd;
+    R.slot = h->tslot;
+    R.inc = inc;
+    R.seq = ++h->round_seq;
+    R.run = 0;
+    if (R.fl.n_chunks && h->oob) {  // out-of-range literal stored: numpy would raise IndexError
+        CK(cudaMemsetAsync(h->mctr + 4, 0, 8, h->st));
         for_parts(h, [&](Bucket& b, Part& p) {
             if (p.count && b.size)
-                k_max_var<<<grid_for(p.count * b.size), 256, 0, h->st>>>(p.lits, p.count, b.size, h->ctr + 4);
+                k_max_var<<<grid_for(p.count * b.size), 256, 0, h->st>>>(p.lits, p.count, b.size, h->mctr + 4);
         });
         CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(h->h_ctr + 4, h->ctr + 4, 8, cudaMemcpyDeviceToHost, h->st));
+        CK(cudaMemcpyAsync(h->h_mctr + 4, h->mctr + 4, 8, cudaMemcpyDeviceToHost, h->st));
         CK(cudaStreamSynchronize(h->st));
-        if ((int64_t)h->h_ctr[4] > h->V)
-            return fail(TSG_ERANGE, "index %lld is out of bounds for axis 0 with size %d", (long long)h->h_ctr[4], h->V + 1);
+        if ((int64_t)h->h_mctr[4] > h->V)
+            return fail(TSG_ERANGE, "index %lld is out of bounds for axis 0 with size %d", (long long)h->h_mctr[4], h->V + 1);
         h->oob = false;
     }
-    if (h->fl.n_chunks) {
+    if (R.fl.n_chunks) {
         CKR(build_desc(h));
         if (h->n_tiles >= (int64_t)INT32_MAX / 2)  // the kernels index tiles with 32-bit integers
             return fail(TSG_ECAPACITY, "store of %lld tiles exceeds the 32-bit tile index", (long long)h->n_tiles);
-        if (h->fl.n_chunks > 1) CKR(dgrow(h, &h->carry, &h->carry_cap, std::max<int64_t>(1, h->n_tiles * STRIDE)));
-        CK(cudaMemsetAsync(h->ctr, 0, 4 * sizeof(unsigned long long), h->st));
+        if (R.fl.n_chunks > 1) CKR(dgrow(h, &R.carry, &R.carry_cap, std::max<int64_t>(1, h->n_tiles * STRIDE)));
+        CK(cudaMemsetAsync(R.ctr, 0, 4 * sizeof(unsigned long long), h->st));
         const bool timing = h->cfg.flags & TSG_F_TIMING;
-        if (timing) CK(cudaEventRecord(h->ev_tst[h->fl_slot][0], h->st));
-        CKR(run_tests(h, h->fl, h->fl_slot, inc, 0));
-        if (timing) CK(cudaEventRecord(h->ev_tst[h->fl_slot][1], h->st));
-        // round counters [0..3] and polarity counts [6..7] in one copy ([4..5]
-        // are maintenance scratch, idle during a round)
-        CK(cudaMemcpyAsync(h->h_ctr, h->ctr, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
-        CK(cudaEventRecord(h->ev_done, h->st));
+        if (timing) CK(cudaEventRecord(R.ev_tst[0], h->st));
+        CKR(run_tests(h, k, inc, 0));
+        if (timing) CK(cudaEventRecord(R.ev_tst[1], h->st));
+        // round counters [0..3] and polarity counts [6..7] in one copy
+        CK(cudaMemcpyAsync(R.h_ctr, R.ctr, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
+        CK(cudaEventRecord(R.ev_done, h->st));
     }
-    h->inflight = true;
+    R.inflight = true;
+    h->next_rs ^= 1;
     if (flip) h->tslot ^= 1;
     return TSG_OK;
 }
 
-// Wait for the launched round's counters; grow the record buffer and replay
-// emission if it overflowed; fill the round's figures.
+// Collect the oldest launched round: wait for its counters; grow its record
+// buffer and replay emission if it overflowed (its table slot and carry
+// stamps are its own, so the replay is exact even with the next round in
+// flight); fill its figures.  The fetch calls then read its records.
 int round_collect(tsg_engine* h, tsg_round_result* out) {
-    if (!h->inflight) return fail(TSG_EINVAL, "no launched round to collect");
-    h->inflight = false;
-    const RoundDesc& rd = h->fl;
+    int k = -1;
+    for (int j = 0; j < 2; ++j)
+        if (h->rs[j].inflight && (k < 0 || h->rs[j].seq < h->rs[k].seq)) k = j;
+    if (k < 0) return fail(TSG_EINVAL, "no launched round to collect");
+    auto& R = h->rs[k];
+    R.inflight = false;
+    use_reports(h, k);
+    h->fetch_rs = k;
+    const RoundDesc& rd = R.fl;
     tsg_round_result res{};
     res.n_chunks = rd.n_chunks;
     if (rd.n_chunks) {
-        CK(cudaEventSynchronize(h->ev_done));
+        CK(cudaEventSynchronize(R.ev_done));
         // literal placement for the next inserts: the polarity that is
         // non-False more often under this round's assignments goes right
         // after the pivot (ends the early-exit recurrence sooner)
-        if (!h->prefer_fixed && h->h_ctr[6] + h->h_ctr[7] > 0)
-            h->prefer = h->h_ctr[7] < h->h_ctr[6] ? 1 : (h->h_ctr[7] > h->h_ctr[6] ? -1 : 0);
-        int64_t n_slots = (int64_t)h->h_ctr[0];
-        int64_t positives = (int64_t)h->h_ctr[1];
-        res.lane_triggers = (int64_t)h->h_ctr[2];
-        int64_t n_rec = (int64_t)h->h_ctr[3];
+        if (!h->prefer_fixed && R.h_ctr[6] + R.h_ctr[7] > 0)
+            h->prefer = R.h_ctr[7] < R.h_ctr[6] ? 1 : (R.h_ctr[7] > R.h_ctr[6] ? -1 : 0);
+        int64_t n_slots = (int64_t)R.h_ctr[0];
+        int64_t positives = (int64_t)R.h_ctr[1];
+        res.lane_triggers = (int64_t)R.h_ctr[2];
+        int64_t n_rec = (int64_t)R.h_ctr[3];
         // overflow: grow, replay emission only (no activity / counter side
-        // effects) from the round's own table slot.  Slot reservation depends
-        // on which warp tests which tile, so a replay may need a different count.
+        // effects).  Slot reservation depends on which warp tests which tile,
+        // so a replay may need a different count.
         while (n_slots > h->out_cap) {
             dfree(h, h->out);
             h->out = nullptr;
@@ -1298,12 +1360,13 @@ int round_collect(tsg_engine* h, tsg_round_result* out) {
             if (h->out_cap >= (int64_t)INT32_MAX)  // report slots are 32-bit in the kernels
                 return fail(TSG_ECAPACITY, "%lld report slots exceed the 32-bit record index", (long long)n_slots);
             CKR(dalloc(h, (void**)&h->out, h->out_cap * (int64_t)sizeof(tsg_report)));
-            CK(cudaMemsetAsync(h->ctr, 0, 4 * sizeof(unsigned long long), h->st));
-            CKR(run_tests(h, rd, h->fl_slot, h->fl_inc, 1));
-            CK(cudaMemcpyAsync(h->h_ctr, h->ctr, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
+            CK(cudaMemsetAsync(R.ctr, 0, 4 * sizeof(unsigned long long), h->st));
+            R.run++;
+            CKR(run_tests(h, k, R.inc, 1));
+            CK(cudaMemcpyAsync(R.h_ctr, R.ctr, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
             CK(cudaStreamSynchronize(h->st));
-            if ((int64_t)h->h_ctr[3] != n_rec) return fail(TSG_ECUDA, "report replay mismatch");
-            n_slots = (int64_t)h->h_ctr[0];
+            if ((int64_t)R.h_ctr[3] != n_rec) return fail(TSG_ECUDA, "report replay mismatch");
+            n_slots = (int64_t)R.h_ctr[0];
             res.reruns++;
         }
         h->n_out = n_rec;
@@ -1325,9 +1388,9 @@ int round_collect(tsg_engine* h, tsg_round_result* out) {
         res.reports = n_rec;
         if (h->cfg.flags & TSG_F_TIMING) {
             float ms = 0;
-            if (cudaEventElapsedTime(&ms, h->ev_enc[h->fl_slot][0], h->ev_enc[h->fl_slot][1]) == cudaSuccess) res.encode_ms = ms;
+            if (cudaEventElapsedTime(&ms, h->ev_enc[R.slot][0], h->ev_enc[R.slot][1]) == cudaSuccess) res.encode_ms = ms;
             else cudaGetLastError();
-            if (cudaEventElapsedTime(&ms, h->ev_tst[h->fl_slot][0], h->ev_tst[h->fl_slot][1]) == cudaSuccess) res.test_ms = ms;
+            if (cudaEventElapsedTime(&ms, R.ev_tst[0], R.ev_tst[1]) == cudaSuccess) res.test_ms = ms;
             else cudaGetLastError();
         }
     }
@@ -1343,7 +1406,10 @@ int tsg_round_encode(tsg_engine* h) {
     if (!h->rd.n_chunks) return TSG_OK;
     const bool timing = h->cfg.flags & TSG_F_TIMING;
     if (timing) CK(cudaEventRecord(h->ev_enc[h->tslot][0], h->st));
-    CK(cudaMemsetAsync(h->ctr + 6, 0, 2 * sizeof(unsigned long long), h->st));
+    for (const auto& Q : h->rs)
+        if (Q.inflight && Q.slot == h->tslot)
+            return fail(TSG_EINVAL, "table slot %d still belongs to an uncollected round", h->tslot);
+    CK(cudaMemsetAsync(h->rs[h->next_rs].ctr + 6, 0, 2 * sizeof(unsigned long long), h->st));
     CKR(do_encode(h));
     if (timing) CK(cudaEventRecord(h->ev_enc[h->tslot][1], h->st));
     return TSG_OK;
@@ -1400,6 +1466,7 @@ int egress_view(tsg_engine* h, int64_t k, const void** src, int64_t* bytes) {
 int tsg_fetch_reports(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n) {
     CKR(validate_handle(h));
     DevGuard g(h->dev);
+    use_reports(h, h->fetch_rs);
     CKR(compact_reports(h));
     int64_t k = std::min(cap, h->n_out);
     if (k > 0) {
@@ -1425,6 +1492,7 @@ int tsg_set_record_bytes(tsg_engine* h, int32_t bytes) {
 int tsg_fetch_reports_async(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n) {
     CKR(validate_handle(h));
     DevGuard g(h->dev);
+    use_reports(h, h->fetch_rs);
     CKR(compact_reports(h));
     const int64_t k = std::min(cap, h->n_out);
     *n = k;
@@ -1436,7 +1504,6 @@ int tsg_fetch_reports_async(tsg_engine* h, tsg_report* out, int64_t cap, int64_t
     CK(cudaStreamWaitEvent(h->egress, h->ev_ready, 0));
     CK(cudaMemcpyAsync(out, src, bytes, cudaMemcpyDeviceToHost, h->egress));
     CK(cudaEventRecord(h->ev_cur, h->egress));
-    h->cur_pending = true;
     return TSG_OK;
 }
 
@@ -1450,6 +1517,7 @@ int tsg_fetch_wait(tsg_engine* h) {
 int tsg_reports_device(tsg_engine* h, void** device_ptr, int64_t* n) {
     CKR(validate_handle(h));
     DevGuard g(h->dev);
+    use_reports(h, h->fetch_rs);
     CKR(compact_reports(h));
     *device_ptr = h->out;
     *n = h->n_out;

@@ -450,10 +450,11 @@ def test_c3_full_size_parity(P):
     dev.close()
 
 
-@pytest.mark.parametrize("cap", [1 << 20, 64])  # 64: every round overflows and replays after the next encode
-def test_async_rounds_match_sync_rounds(P, cap):
-    # launch(k); stage/prepare/encode(k+1); collect(k): identical figures,
-    # records and activities to synchronous rounds, overflow replays included
+@pytest.mark.parametrize("cap", [1 << 20, 64])  # 64: every round overflows and replays with the next in flight
+@pytest.mark.parametrize("gw", [32, 1])  # gw 1: multi-chunk rounds (carry stamps per round state)
+def test_async_rounds_match_sync_rounds(P, cap, gw):
+    # two rounds in flight: launch(k-1), launch(k), collect(k-1) ...: identical
+    # figures, records and activities to synchronous rounds, overflow replays included
     from paper_2012_03119_b200 import workload as W
     from paper_2012_03119_b200.native import NativeEngine, pack_rows
     rng = np.random.default_rng(17)
@@ -465,7 +466,7 @@ def test_async_rounds_match_sync_rounds(P, cap):
         threads = 2 + k % 3
         snaps = W.snapshots(threads, 32, nv, rng)
         rounds.append((snaps, *W.groups_for(threads, 32)))
-    a, b = NativeEngine(nv, report_capacity=cap), NativeEngine(nv)
+    a, b = NativeEngine(nv, 32, gw, report_capacity=cap), NativeEngine(nv, 32, gw)
     a.add_clauses(flat, offs, ids)
     b.add_clauses(flat, offs, ids)
     fields = ("reports", "clauses_tested", "aggregate_tests", "aggregate_tests_negative", "lane_tests",
@@ -476,24 +477,29 @@ def test_async_rounds_match_sync_rounds(P, cap):
         r = b.round(gl, gt, 1.0 + k)
         want.append(([getattr(r, f) for f in fields], np.sort(b.fetch(r.reports), order=["engine_id", "group"])))
     got = []
-    for k, (snaps, gl, gt) in enumerate(rounds):
+
+    def take():
+        r = a.collect()  # the oldest launched round
+        got.append(([getattr(r, f) for f in fields], np.sort(a.fetch(r.reports), order=["engine_id", "group"])))
+
+    for k, (snaps, gl, gt) in enumerate(rounds):  # two rounds in flight
+        if k >= 2:
+            take()  # round k-2 owns the table slot round k encodes into
         a.stage_packed(pack_rows(snaps, nv))
         a.prepare(gl, gt)
         a.encode()
-        if k:
-            r = a.collect()
-            got.append(([getattr(r, f) for f in fields], np.sort(a.fetch(r.reports), order=["engine_id", "group"])))
         a.launch(1.0 + k)
-    r = a.collect()
-    got.append(([getattr(r, f) for f in fields], np.sort(a.fetch(r.reports), order=["engine_id", "group"])))
+    take()
+    take()
     for (gf, gr), (wf, wr) in zip(got, want):
         assert gf == wf
         assert np.array_equal(gr, wr)
     for x, y in zip(a.buckets(), b.buckets()):
         assert np.array_equal(x[4].view(np.uint64), y[4].view(np.uint64))
-    with pytest.raises(ValueError):  # one launched round at a time
+    with pytest.raises(ValueError):  # at most two rounds in flight
         a.prepare(*rounds[0][1:])
         a.encode()
+        a.launch(1.0)
         a.launch(1.0)
         a.launch(1.0)
     a.close()

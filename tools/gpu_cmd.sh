@@ -1,1 +1,5 @@
-for c in C1 C2; do timeout 300 python bench.py --config $c --steps 10 --warmup 3 > gpurun_out/bench_$c.log 2>&1; tail -1 gpurun_out/bench_$c.log | python -c "import sys,json; d=json.loads(sys.stdin.read()); print(d['config']['workload'][:40], d['value'], d['ms_per_step'], d['roofline']['frac'], d['e2e']['ms_per_step'] if d['e2e'] else None)"; done
+timeout 900 python -m pytest tests -m gpu -x -q --timeout 300 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
+tail -1 gpurun_out/pytest_gpu.log
+grep -E "^FAILED|^E " gpurun_out/pytest_gpu.log | head -5
+timeout 600 python bench.py > gpurun_out/bench.log 2>&1
+tail -1 gpurun_out/bench.log | python -c "import sys,json; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['roofline']['frac'], d['roofline']['kernel_ms'], d['roofline']['encode_ms'], d['e2e']['ms_per_step'], d['e2e']['mode'])"
