@@ -138,8 +138,12 @@ struct tsg_engine {
         int64_t seq = 0;                      // launch sequence: carry stamps, collect order
         int32_t run = 0;                      // 0: the round's test; 1, 2, ...: emission replays
         bool inflight = false;                // launched, not collected
-        unsigned long long* ctr = nullptr;    // device [8]: [0..3] round counters, [6..7] polarity counts
-        unsigned long long* h_ctr = nullptr;  // pinned [8]
+        // device [8]: [0..3] round counters, [5] CTAs done, [6..7] polarity
+        // counts; zero between rounds (the round's last CTA publishes them
+        // to h_ctr and re-zeroes them, so no memset or copy is queued)
+        unsigned long long* ctr = nullptr;
+        unsigned long long* h_ctr = nullptr;  // pinned [8], written by the kernel
+        bool pol_pending = false;             // an encode counted into ctr[6..7] since the last launch
         cudaEvent_t ev_done = nullptr;        // its counters are on the host
         cudaEvent_t ev_tst[2] = {nullptr, nullptr};
         int64_t* carry = nullptr;             // per-clause (round, tid) stamps of multi-chunk rounds
@@ -420,6 +424,7 @@ int launch_test(tsg_engine* h, int k, int c, double inc, int emit_only) {
     p.carry_in_tid = (c > 0 && rd.gtid[g0] == rd.gtid[g0 - 1]) ? rd.gtid[g0] : -1;
     p.carry_out_tid = (g0 + G < rd.n_groups && rd.gtid[g0 + G - 1] == rd.gtid[g0 + G]) ? rd.gtid[g0 + G - 1] : -1;
     p.emit_only = emit_only;
+    p.pub = (!emit_only && c == rd.n_chunks - 1) ? R.h_ctr : nullptr;
     p.slab_tile0 = h->d_slab_tile0;
     p.slab_desc0 = reinterpret_cast<const int32_t*>(h->d_slab_tile0 + (h->n_slabs + 1));
     p.sched = reinterpret_cast<const uint64_t*>(h->d_slab_tile0 + 2 * (h->n_slabs + 1));
@@ -754,6 +759,7 @@ int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
         for (auto& e : R.ev_tst) cudaEventCreate(&e);
         if (cudaMallocHost(&R.h_ctr, 8 * sizeof(unsigned long long)) != cudaSuccess) { delete h; return fail(TSG_ECUDA, "pinned alloc"); }
         if (dalloc(h, (void**)&R.ctr, 8 * sizeof(unsigned long long))) { delete h; return TSG_ENOMEM; }
+        if (cudaMemsetAsync(R.ctr, 0, 8 * sizeof(unsigned long long), h->st) != cudaSuccess) { delete h; return fail(TSG_ECUDA, "memset"); }
     }
     if (cudaMallocHost(&h->h_mctr, 8 * sizeof(unsigned long long)) != cudaSuccess) { delete h; return fail(TSG_ECUDA, "pinned alloc"); }
     if (dalloc(h, (void**)&h->mctr, 8 * sizeof(unsigned long long))) { delete h; return TSG_ENOMEM; }
@@ -1308,16 +1314,18 @@ int round_launch(tsg_engine* h, double inc, bool flip) {
         if (h->n_tiles >= (int64_t)INT32_MAX / 2)  // the kernels index tiles with 32-bit integers
             return fail(TSG_ECAPACITY, "store of %lld tiles exceeds the 32-bit tile index", (long long)h->n_tiles);
         if (R.fl.n_chunks > 1) CKR(dgrow(h, &R.carry, &R.carry_cap, std::max<int64_t>(1, h->n_tiles * STRIDE)));
-        CK(cudaMemsetAsync(R.ctr, 0, 4 * sizeof(unsigned long long), h->st));
         const bool timing = h->cfg.flags & TSG_F_TIMING;
         if (timing) CK(cudaEventRecord(R.ev_tst[0], h->st));
         CKR(run_tests(h, k, inc, 0));
         if (timing) CK(cudaEventRecord(R.ev_tst[1], h->st));
-        // round counters [0..3] and polarity counts [6..7] in one copy
-        CK(cudaMemcpyAsync(R.h_ctr, R.ctr, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
+        if (h->n_tiles == 0) {  // no kernel ran to publish the counters
+            CK(cudaMemcpyAsync(R.h_ctr, R.ctr, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
+            CK(cudaMemsetAsync(R.ctr, 0, 8 * sizeof(unsigned long long), h->st));
+        }
         CK(cudaEventRecord(R.ev_done, h->st));
     }
     R.inflight = true;
+    R.pol_pending = false;
     h->next_rs ^= 1;
     if (flip) h->tslot ^= 1;
     return TSG_OK;
@@ -1369,6 +1377,7 @@ int round_collect(tsg_engine* h, tsg_round_result* out) {
             n_slots = (int64_t)R.h_ctr[0];
             res.reruns++;
         }
+        if (res.reruns) CK(cudaMemsetAsync(R.ctr, 0, 4 * sizeof(unsigned long long), h->st));
         h->n_out = n_rec;
         h->n_alloc = n_slots;
         h->compacted = n_slots == n_rec;
@@ -1409,7 +1418,10 @@ int tsg_round_encode(tsg_engine* h) {
     for (const auto& Q : h->rs)
         if (Q.inflight && Q.slot == h->tslot)
             return fail(TSG_EINVAL, "table slot %d still belongs to an uncollected round", h->tslot);
-    CK(cudaMemsetAsync(h->rs[h->next_rs].ctr + 6, 0, 2 * sizeof(unsigned long long), h->st));
+    auto& Rn = h->rs[h->next_rs];
+    if (Rn.pol_pending)  // re-encoded without a launch: count this encode only
+        CK(cudaMemsetAsync(Rn.ctr + 6, 0, 2 * sizeof(unsigned long long), h->st));
+    Rn.pol_pending = true;
     CKR(do_encode(h));
     if (timing) CK(cudaEventRecord(h->ev_enc[h->tslot][1], h->st));
     return TSG_OK;

@@ -339,6 +339,7 @@ struct TestParams {
     int32_t carry_in_tid;      // first tid of the chunk if it continues from the previous chunk, else -1
     int32_t carry_out_tid;     // last tid of the chunk if it continues into the next chunk, else -1
     int32_t emit_only;         // replay after report-buffer overflow: no activity / counter side effects
+    unsigned long long* pub;   // last launch of a round: host-mapped [8] the last CTA publishes ctr to
     const int64_t* slab_tile0; // slab kernel: first tile of each slab (+ end)
     const int32_t* slab_desc0; // slab kernel: first descriptor of each slab (+ end)
     const uint64_t* sched;     // slab kernel: per CTA slab << 32 | rank << 16 | CTAs on the slab
@@ -771,6 +772,15 @@ __device__ __forceinline__ void finish_block(const TestParams<LW, GW>& p, WarpAc
         if (!p.emit_only) {
             if (a) atomicAdd(p.ctr + 1, a);
             if (bb) atomicAdd(p.ctr + 2, bb);
+        }
+        if (p.pub) {  // the round's last CTA hands the counters to the host and re-zeroes them
+            __threadfence();
+            if (atomicAdd(p.ctr + 5, 1ull) == gridDim.x - 1) {
+                __threadfence();
+#pragma unroll
+                for (int i = 0; i < 8; ++i) p.pub[i] = atomicExch(p.ctr + i, 0ull);
+                __threadfence_system();
+            }
         }
     }
 }
