@@ -414,16 +414,25 @@ def main():
                                                  C.byref(got)))
 
         def loop_pipelined(k):
-            # same transfers per round, pipelined: round i-1's records copy out
-            # on the egress stream while round i's rows go in and round i is
-            # tested (tsg_fetch_reports_async; measured faster than also
-            # overlapping the encode via tsg_round_launch/collect, which queues
-            # the copy-out behind the next round's rows)
-            r = None
+            # same transfers per round, pipelined over three engines of the
+            # link: round i+1's rows copy in on the ingress stream (two staging
+            # buffers) while round i is encoded and tested and round i-1's
+            # records copy out on the egress stream (tsg_fetch_reports_async)
+            r, pending = None, 0
+            eng.prepare(gl, gt)
             for _ in range(k):
                 _lib.check(L.tsg_stage_packed(eng.h, C.c_void_p(h_packed_t.data_ptr()), A, pw, 0))
-                r = eng.round(gl, gt, 1.0)
+                if pending:
+                    r = eng.collect()
+                    fetch_async(r)
+                    pending -= 1
+                eng.encode()
+                eng.launch(1.0)
+                pending += 1
+            while pending:
+                r = eng.collect()
                 fetch_async(r)
+                pending -= 1
             return r
 
         def step_int8():
@@ -487,8 +496,8 @@ def main():
                    "input": "packed 2-bit snapshot rows in pinned host memory (solver-side ingress format)",
                    "mode": mode,
                    "pipelined_ms_per_step": ms,
-                   "pipelined": "round i-1's records copy out on the egress stream while round i's rows go in "
-                                "and round i is tested",
+                   "pipelined": "round i+1's rows copy in (ingress stream) while round i is encoded and tested "
+                                "and round i-1's records copy out (egress stream)",
                    "sequential_ms_per_step": ms_seq,
                    "host_pack_ms_per_round": pack_ms, "host_pack_threads": host_threads,
                    "int8_rows": {"value": r8.lane_tests * world / (ms8 * 1e-3), "ms_per_step": ms8,

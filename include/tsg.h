@@ -149,7 +149,12 @@ int tsg_round(tsg_engine* h, const int32_t* group_lanes, const int32_t* group_ti
  * words.  tsg_pack_rows is host code (no device, thread-safe: solver threads
  * pack their own snapshots); tsg_stage_packed replaces tsg_stage_snapshots
  * for the next round (on_device=1: `rows` is device memory, 32-byte aligned,
- * pitch a multiple of 4 words, used in place). */
+ * pitch a multiple of 4 words, used in place).  Host rows are copied on the
+ * library's ingress stream into one of two staging buffers, so the next
+ * round's rows go in while the current round is tested: the call returns
+ * before a copy from pinned memory has finished, and pinned rows must stay
+ * unchanged until the round encoded from them is collected (pageable rows
+ * are consumed before the call returns). */
 int tsg_packed_words(int32_t num_vars, int64_t* words);
 int tsg_pack_rows(const int8_t* rows, int64_t n_rows, int64_t row_pitch, int32_t num_vars,
                   uint64_t* out, int64_t out_pitch_words);

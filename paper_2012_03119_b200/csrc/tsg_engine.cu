@@ -114,8 +114,16 @@ struct tsg_engine {
     // packed rows (2 bits per variable, tsg_pack_rows) when `packed`
     bool packed = false;
     const uint64_t* prows = nullptr;
-    uint64_t* prows_own = nullptr;
-    int64_t prows_cap = 0, ppitch = 0;
+    int64_t ppitch = 0;
+    // two staging buffers filled on the ingress stream: the rows of round
+    // i+1 copy in while round i is encoded and tested
+    uint64_t* pbuf[2] = {nullptr, nullptr};
+    int64_t pbuf_cap[2] = {0, 0};
+    int pk = 1;                           // buffer of the last stage
+    bool pstaged = false;                 // prows is pbuf[pk], copied on the ingress stream
+    cudaStream_t ingress = nullptr;
+    cudaEvent_t ev_staged[2] = {nullptr, nullptr};  // copy into pbuf[b] done
+    cudaEvent_t ev_read[2] = {nullptr, nullptr};    // encoder done reading pbuf[b]
 
     // round description as prepared
     RoundDesc rd;
@@ -749,6 +757,11 @@ int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     cudaStreamCreateWithFlags(&h->egress, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&h->ingress, cudaStreamNonBlocking);
+    for (int b = 0; b < 2; ++b) {
+        cudaEventCreateWithFlags(&h->ev_staged[b], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&h->ev_read[b], cudaEventDisableTiming);
+    }
     cudaEventCreateWithFlags(&h->ev_cur, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&h->alt.ev, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&h->ev_ready, cudaEventDisableTiming);
@@ -775,7 +788,8 @@ int tsg_destroy(tsg_engine* h) {
     cudaStreamSynchronize(h->st);
     for_parts(h, [&](Bucket&, Part& p) { part_free(h, p); });
     dfree(h, h->d_slab_tile0);
-    dfree(h, h->rows_own); dfree(h, h->prows_own); dfree(h, h->tables); dfree(h, h->d_desc); dfree(h, h->out);
+    if (h->ingress) cudaStreamSynchronize(h->ingress);
+    dfree(h, h->rows_own); dfree(h, h->pbuf[0]); dfree(h, h->pbuf[1]); dfree(h, h->tables); dfree(h, h->d_desc); dfree(h, h->out);
     dfree(h, h->mctr); dfree(h, h->out2); dfree(h, h->codes);
     for (auto& R : h->rs) { dfree(h, R.ctr); dfree(h, R.carry); }
     if (h->egress) cudaStreamSynchronize(h->egress);
@@ -792,6 +806,11 @@ int tsg_destroy(tsg_engine* h) {
         for (int k = 0; k < 2; ++k)
             if (h->ev_enc[sl][k]) cudaEventDestroy(h->ev_enc[sl][k]);
     if (h->egress) cudaStreamDestroy(h->egress);
+    for (int b = 0; b < 2; ++b) {
+        if (h->ev_staged[b]) cudaEventDestroy(h->ev_staged[b]);
+        if (h->ev_read[b]) cudaEventDestroy(h->ev_read[b]);
+    }
+    if (h->ingress) cudaStreamDestroy(h->ingress);
     cudaStreamDestroy(h->st);
     delete h;
     return TSG_OK;
@@ -1152,26 +1171,41 @@ int tsg_stage_packed(tsg_engine* h, const uint64_t* rows, int64_t n_rows, int64_
         return fail(TSG_EINVAL, "packed pitch %lld < %lld words", (long long)pitch_words, (long long)words);
     h->n_rows = n_rows;
     h->packed = true;
+    h->pstaged = false;
     if (n_rows == 0) return TSG_OK;
     if (on_device && pitch_words % 4 == 0 && ((uintptr_t)rows % 32) == 0) {
         h->prows = rows;
         h->ppitch = pitch_words;
         return TSG_OK;
     }
+    // copy into the staging buffer the previous stage did not use, on the
+    // ingress stream, once the encoder that read it last is done (ev_read,
+    // recorded by tsg_round_encode) -- not behind the rounds in flight
+    const int b = h->pk ^ 1;
     const int64_t need = words * n_rows;
-    if (need > h->prows_cap) {
-        dfree(h, h->prows_own);
-        h->prows_own = nullptr;
-        const int64_t cap = std::max(need, h->prows_cap * 2);
-        CKR(dalloc(h, (void**)&h->prows_own, cap * 8));
-        h->prows_cap = cap;
+    CK(cudaStreamWaitEvent(h->ingress, h->ev_read[b], 0));
+    if (need > h->pbuf_cap[b] || on_device) {
+        if (need > h->pbuf_cap[b]) {
+            dfree(h, h->pbuf[b]);  // stream-ordered after its last reader on h->st
+            h->pbuf[b] = nullptr;
+            const int64_t cap = std::max(need, h->pbuf_cap[b] * 2);
+            CKR(dalloc(h, (void**)&h->pbuf[b], cap * 8));
+            h->pbuf_cap[b] = cap;
+        }
+        // the allocation, and device-side sources written on h->st, come first
+        CK(cudaEventRecord(h->ev_staged[b], h->st));
+        CK(cudaStreamWaitEvent(h->ingress, h->ev_staged[b], 0));
     }
     if (pitch_words == words)
-        CK(cudaMemcpyAsync(h->prows_own, rows, need * 8, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDefault, h->st));
+        CK(cudaMemcpyAsync(h->pbuf[b], rows, need * 8, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDefault,
+                           h->ingress));
     else
-        CK(cudaMemcpy2DAsync(h->prows_own, words * 8, rows, pitch_words * 8, words * 8, n_rows,
-                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDefault, h->st));
-    h->prows = h->prows_own;
+        CK(cudaMemcpy2DAsync(h->pbuf[b], words * 8, rows, pitch_words * 8, words * 8, n_rows,
+                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDefault, h->ingress));
+    CK(cudaEventRecord(h->ev_staged[b], h->ingress));
+    h->pk = b;
+    h->pstaged = true;
+    h->prows = h->pbuf[b];
     h->ppitch = words;
     return TSG_OK;
 }
@@ -1413,16 +1447,18 @@ int tsg_round_encode(tsg_engine* h) {
     int64_t need_rows = h->rd.n_groups ? h->rd.grow0.back() + h->rd.glanes.back() : 0;
     if (need_rows > h->n_rows) return fail(TSG_EINVAL, "groups need %lld rows, %lld staged", (long long)need_rows, (long long)h->n_rows);
     if (!h->rd.n_chunks) return TSG_OK;
-    const bool timing = h->cfg.flags & TSG_F_TIMING;
-    if (timing) CK(cudaEventRecord(h->ev_enc[h->tslot][0], h->st));
     for (const auto& Q : h->rs)
         if (Q.inflight && Q.slot == h->tslot)
             return fail(TSG_EINVAL, "table slot %d still belongs to an uncollected round", h->tslot);
+    if (h->packed && h->pstaged) CK(cudaStreamWaitEvent(h->st, h->ev_staged[h->pk], 0));  // rows copied in
+    const bool timing = h->cfg.flags & TSG_F_TIMING;
+    if (timing) CK(cudaEventRecord(h->ev_enc[h->tslot][0], h->st));
     auto& Rn = h->rs[h->next_rs];
     if (Rn.pol_pending)  // re-encoded without a launch: count this encode only
         CK(cudaMemsetAsync(Rn.ctr + 6, 0, 2 * sizeof(unsigned long long), h->st));
     Rn.pol_pending = true;
     CKR(do_encode(h));
+    if (h->packed && h->pstaged) CK(cudaEventRecord(h->ev_read[h->pk], h->st));
     if (timing) CK(cudaEventRecord(h->ev_enc[h->tslot][1], h->st));
     return TSG_OK;
 }
