@@ -193,6 +193,7 @@ struct tsg_engine {
     int64_t out12_cap = 0;
     bool oob = false;  // a stored literal may exceed num_vars (checked before testing)
     int64_t round_seq = 0;
+    int enc_attr = 0;             // k_encode_packed32 shared-memory attribute set, per GW
     int64_t grid[32] = {0};       // persistent grid per k_test variant
     int64_t grid_smem[32];        // shared-memory size the grid was computed for (-1: none)
     bool smem_table = true;       // shared-memory code table when it fits (TSG_SMEM_TABLE=0 disables)
@@ -342,7 +343,23 @@ int launch_encode(tsg_engine* h, int c) {
         pc.vstride = ec.vstride;
         for (int g = 0; g < ec.G; ++g) { pc.row0[g] = ec.row0[g]; pc.lanes[g] = ec.lanes[g]; }
         pc.polarity = ec.polarity;
-        k_encode_packed<LW, GW><<<grid, block, 0, h->st>>>(h->prows, pc, lane, agg);
+        static const bool enc_stage = !getenv("TSG_ENC_STAGE") || atoi(getenv("TSG_ENC_STAGE")) != 0;
+        if (sizeof(LW) == 4 && enc_stage) {
+            const int need = (ec.G + 7) / 8;  // groups per warp
+            const int gpw = need <= 1 ? 1 : need <= 2 ? 2 : need <= 4 ? 4 : 8;
+            const size_t smem = (size_t)8 * gpw * 32 * 32;
+            auto* lt = reinterpret_cast<LaneEntry<uint32_t>*>(lane);
+            auto* fn = gpw == 1 ? k_encode_packed32<GW, 1> : gpw == 2 ? k_encode_packed32<GW, 2>
+                     : gpw == 4 ? k_encode_packed32<GW, 4> : k_encode_packed32<GW, 8>;
+            const int bit = 1 << (gpw + 8 * (int)(sizeof(GW) / 8));
+            if (!(h->enc_attr & bit)) {  // 64 KB of row stage at 8 groups per warp
+                CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                h->enc_attr |= bit;
+            }
+            fn<<<grid, block, smem, h->st>>>(h->prows, pc, lt, agg);
+        } else {
+            k_encode_packed<LW, GW><<<grid, block, 0, h->st>>>(h->prows, pc, lane, agg);
+        }
     } else {
         k_encode<LW, GW><<<grid, block, 0, h->st>>>(h->rows, ec, lane, agg);
     }

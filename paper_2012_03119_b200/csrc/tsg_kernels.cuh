@@ -281,6 +281,188 @@ __global__ void __launch_bounds__(256) k_encode_packed(const uint64_t* __restric
     }
 }
 
+// Lane width <= 32 (one row per lane): every warp first queues ALL its
+// groups' rows (32 bytes per row) as 16-byte cp.async copies into its own
+// shared-memory stage, one commit group per group, then transposes group j
+// as soon as its copies land (cp.async.wait_group) -- up to 64 KB per SM in
+// flight instead of one group per warp, so the encoder streams the rows at
+// HBM rate rather than waiting on each group's load.  A lane reads back only
+// the row it copied, so no warp barrier is needed; the two 16-byte halves
+// are swapped on every other 4-lane quad (conflict-free 128-bit reads).
+constexpr int ENC_MAX_GPW = 8;
+#ifndef TSG_ENC_PAIR
+#define TSG_ENC_PAIR 0
+#endif  // groups per warp (G <= 64, 8 warps)
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_upto(int pending) {  // wait until <= pending groups are in flight
+    switch (pending) {
+        case 0: asm volatile("cp.async.wait_group 0;\n" ::: "memory"); break;
+        case 1: asm volatile("cp.async.wait_group 1;\n" ::: "memory"); break;
+        case 2: asm volatile("cp.async.wait_group 2;\n" ::: "memory"); break;
+        case 3: asm volatile("cp.async.wait_group 3;\n" ::: "memory"); break;
+        case 4: asm volatile("cp.async.wait_group 4;\n" ::: "memory"); break;
+        case 5: asm volatile("cp.async.wait_group 5;\n" ::: "memory"); break;
+        case 6: asm volatile("cp.async.wait_group 6;\n" ::: "memory"); break;
+        default: asm volatile("cp.async.wait_group 7;\n" ::: "memory"); break;
+    }
+}
+
+// Lane-dependent constants of warp_transpose32, computed once per thread.
+struct Transpose32 {
+    uint32_t keep[5], amt[5];
+    uint32_t sel[2];  // byte stages (16, 8): one PRMT takes the partner's bytes in place
+    __device__ __forceinline__ explicit Transpose32(int lane) {
+        sel[0] = (lane & 16) ? 0x3276u : 0x5410u;
+        sel[1] = (lane & 8) ? 0x3715u : 0x6240u;
+        asm volatile("" : "+r"(sel[0]), "+r"(sel[1]));
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+            const int sft = 16 >> i;
+            const uint32_t m = i == 0 ? 0x0000FFFFu : i == 1 ? 0x00FF00FFu : i == 2 ? 0x0F0F0F0Fu
+                             : i == 3 ? 0x33333333u : 0x55555555u;
+            const bool up = lane & sft;
+            keep[i] = up ? ~m : m;
+            amt[i] = up ? 32 - sft : sft;
+            // opaque from here on: one register each, so a stage is SHFL +
+            // SHF + one LOP3 select instead of the masks being refolded
+            asm volatile("" : "+r"(keep[i]), "+r"(amt[i]));
+        }
+    }
+    __device__ __forceinline__ uint32_t operator()(uint32_t x) const {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) x = __byte_perm(x, __shfl_xor_sync(0xffffffffu, x, 16 >> i), sel[i]);
+#pragma unroll
+        for (int i = 2; i < 5; ++i) {
+            const uint32_t y = __shfl_xor_sync(0xffffffffu, x, 16 >> i);
+            const uint32_t yy = __funnelshift_l(y, y, amt[i]);  // rotate the partner's block into place
+            uint32_t r;
+            asm("lop3.b32 %0, %1, %2, %3, 0xE2;" : "=r"(r) : "r"(x), "r"(keep[i]), "r"(yy));  // keep ? x : yy
+            x = r;
+        }
+        return x;
+    }
+    // Two transposes, one shuffle per stage: a lane only ever uses the half
+    // of its partner's word the partner discards (the ~keep blocks), so A's
+    // discarded blocks and B's, rotated into the keep blocks, share one word.
+    __device__ __forceinline__ void pair(uint32_t& a, uint32_t& b) const {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {  // byte stages: shuffle + PRMT each
+            a = __byte_perm(a, __shfl_xor_sync(0xffffffffu, a, 16 >> i), sel[i]);
+            b = __byte_perm(b, __shfl_xor_sync(0xffffffffu, b, 16 >> i), sel[i]);
+        }
+#pragma unroll
+        for (int i = 2; i < 5; ++i) {
+            const uint32_t br = __funnelshift_r(b, b, amt[i]);  // B's ~keep blocks onto the keep blocks
+            uint32_t p, na, nb;
+            asm("lop3.b32 %0, %1, %2, %3, 0xE2;" : "=r"(p) : "r"(br), "r"(keep[i]), "r"(a));  // keep ? br : a
+            const uint32_t q = __shfl_xor_sync(0xffffffffu, p, 16 >> i);
+            const uint32_t qa = __funnelshift_l(q, q, amt[i]);  // partner's A blocks into place
+            asm("lop3.b32 %0, %1, %2, %3, 0xE2;" : "=r"(na) : "r"(a), "r"(keep[i]), "r"(qa));  // keep ? a : qa
+            asm("lop3.b32 %0, %1, %2, %3, 0xE2;" : "=r"(nb) : "r"(b), "r"(keep[i]), "r"(q));   // keep ? b : q
+            a = na;
+            b = nb;
+        }
+    }
+};
+
+template <class GW, int GPW>
+__global__ void __launch_bounds__(256) k_encode_packed32(const uint64_t* __restrict__ rows,
+                                                         const __grid_constant__ EncodePackedChunk c,
+                                                         LaneEntry<uint32_t>* __restrict__ lane_tab,
+                                                         AggEntry<GW>* __restrict__ agg) {
+    extern __shared__ uint4 stage[];  // [8 warps][GPW groups][32 rows][2 halves]
+    // per-warp aggregate bits: bit j of part[plane][warp][var] = group warp + 8j
+    __shared__ uint8_t part[3][8][128];
+    const int lane = threadIdx.x, y = threadIdx.y, t = y * 32 + lane;
+    const int64_t vbase = (int64_t)blockIdx.x * 128;
+    const int64_t V = c.num_vars;
+    const int64_t w0 = (int64_t)blockIdx.x * 4;  // first word of the block in every row
+    const int sw = (lane >> 2) & 1;              // half swap of this lane's quad
+    uint4* mine = stage + (size_t)y * GPW * 64 + lane * 2;
+#pragma unroll
+    for (int j = 0; j < GPW; ++j) {
+        const int g = y + 8 * j;
+        const bool ok = g < c.G && lane < c.lanes[g];
+        const uint64_t* src = ok ? rows + (c.row0[g] + lane) * c.pitch_words + w0 : rows;
+        cp_async16(mine + j * 64 + sw, src, ok ? 16 : 0);  // zero-filled past the group
+        cp_async16(mine + j * 64 + (sw ^ 1), src + 2, ok ? 16 : 0);
+        cp_async_commit();
+    }
+    const Transpose32 xp(lane);
+    uint32_t nT[4] = {0, 0, 0, 0}, nF[4] = {0, 0, 0, 0}, nU[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < GPW; ++j) {
+        const int g = y + 8 * j;
+        cp_async_wait_upto(GPW - 1 - j);
+        // no branch around the shuffles (they must stay provably converged):
+        // groups past G transpose zero-filled rows and store nothing
+        const bool live = g < c.G;
+        const int n = live ? c.lanes[g] : 0;
+        const uint4 a = mine[j * 64 + sw], b = mine[j * 64 + (sw ^ 1)];
+        const uint32_t tv[4] = {a.x, a.z, b.x, b.z}, sv[4] = {a.y, a.w, b.y, b.w};
+        const uint32_t lm = width_mask<uint32_t>(n);
+        uint32_t T[4], S[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { T[k] = tv[k]; S[k] = sv[k]; }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {  // eight independent shuffle chains (paired in the bit stages)
+            if (TSG_ENC_PAIR) xp.pair(T[k], S[k]);
+            else { T[k] = xp(T[k]); S[k] = xp(S[k]); }
+        }
+        LaneEntry<uint32_t>* dst = lane_tab + (int64_t)g * c.vstride + vbase + lane;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int v = (int)vbase + 32 * k + lane;  // num_vars < 2^30
+            if (v == 0) { T[k] = 0; S[k] = 0; }  // slot 0 is never set (bitpack.py:110-111)
+            const bool sentinel = v == (int)V + 1;   // always False
+            if (live && v <= (int)V + 1)
+                dst[32 * k] = sentinel ? LaneEntry<uint32_t>{0u, ~0u} : LaneEntry<uint32_t>{T[k], S[k]};
+            // AggregateAssignment.from_packed, bitpack.py:156-166 (slot 0 / past V masked below)
+            if (T[k] != 0) nT[k] |= 1u << j;
+            if ((S[k] & ~T[k]) != 0) nF[k] |= 1u << j;
+            if (live && (n == 0 || (~S[k] & lm) != 0)) nU[k] |= 1u << j;
+        }
+    }
+    cp_async_wait_upto(0);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        part[0][y][32 * k + lane] = (uint8_t)nT[k];
+        part[1][y][32 * k + lane] = (uint8_t)nF[k];
+        part[2][y][32 * k + lane] = (uint8_t)nU[k];
+    }
+    __syncthreads();
+    if (t < 128) {
+        const int64_t v = vbase + t;
+        GW aT = 0, aF = 0, aU = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w)
+#pragma unroll
+            for (int j = 0; j < GPW; ++j) {
+                const GW bit = GW(1) << (w + 8 * j);  // groups past G never set a bit
+                if (part[0][w][t] >> j & 1) aT |= bit;
+                if (part[1][w][t] >> j & 1) aF |= bit;
+                if (part[2][w][t] >> j & 1) aU |= bit;
+            }
+        if (v >= 1 && v <= V) agg[v] = AggEntry<GW>{aT, aF, aU, GW(0)};
+        else if (v == 0) agg[v] = AggEntry<GW>{GW(0), GW(0), GW(0), GW(0)};
+        else if (v == V + 1) agg[v] = AggEntry<GW>{~GW(0), ~GW(0), GW(0), GW(0)};
+        // polarity statistics for the store's literal placement
+        unsigned nt = (v >= 1 && v <= V) ? __popcll((unsigned long long)aT) : 0u;
+        unsigned nf = (v >= 1 && v <= V) ? __popcll((unsigned long long)aF) : 0u;
+        nt = __reduce_add_sync(0xffffffffu, nt);
+        nf = __reduce_add_sync(0xffffffffu, nf);
+        if ((t & 31) == 0 && c.polarity) {
+            atomicAdd(c.polarity, (unsigned long long)nt);
+            atomicAdd(c.polarity + 1, (unsigned long long)nf);
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K3+K4+K5: trigger test.  Persistent grid; one warp per tile of 32 clauses
 // of one bucket, one clause per lane.

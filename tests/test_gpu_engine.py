@@ -452,7 +452,8 @@ def test_c3_full_size_parity(P):
 
 @pytest.mark.parametrize("cap", [1 << 20, 64])  # 64: every round overflows and replays with the next in flight
 @pytest.mark.parametrize("gw", [32, 1])  # gw 1: multi-chunk rounds (carry stamps per round state)
-def test_async_rounds_match_sync_rounds(P, cap, gw):
+@pytest.mark.parametrize("pinned", [False, True])  # pinned: rows copy in asynchronously on the ingress stream
+def test_async_rounds_match_sync_rounds(P, cap, gw, pinned):
     # two rounds in flight: launch(k-1), launch(k), collect(k-1) ...: identical
     # figures, records and activities to synchronous rounds, overflow replays included
     from paper_2012_03119_b200 import workload as W
@@ -476,7 +477,7 @@ def test_async_rounds_match_sync_rounds(P, cap, gw):
         b.stage(snaps)
         r = b.round(gl, gt, 1.0 + k)
         want.append(([getattr(r, f) for f in fields], np.sort(b.fetch(r.reports), order=["engine_id", "group"])))
-    got = []
+    got, keep = [], []
 
     def take():
         r = a.collect()  # the oldest launched round
@@ -485,7 +486,13 @@ def test_async_rounds_match_sync_rounds(P, cap, gw):
     for k, (snaps, gl, gt) in enumerate(rounds):  # two rounds in flight
         if k >= 2:
             take()  # round k-2 owns the table slot round k encodes into
-        a.stage_packed(pack_rows(snaps, nv))
+        rows = pack_rows(snaps, nv)
+        if pinned:  # one pinned buffer per round: unchanged until its round is collected
+            import torch
+            buf = torch.empty(rows.shape, dtype=torch.int64).pin_memory()
+            keep.append(buf)
+            rows = np.copyto(buf.numpy().view(np.uint64), rows) or buf.numpy().view(np.uint64)
+        a.stage_packed(rows)
         a.prepare(gl, gt)
         a.encode()
         a.launch(1.0 + k)
