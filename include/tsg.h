@@ -187,7 +187,10 @@ int tsg_fetch_reports_async(tsg_engine* h, tsg_report* out, int64_t cap, int64_t
 int tsg_fetch_wait(tsg_engine* h);
 /* Egress record format of tsg_fetch_reports / tsg_fetch_reports_async: 16
  * (tsg_report, default) or 12 bytes -- {uint64 key, uint32 lane_mask},
- * packed, for lane_width <= 32 -- a quarter fewer bytes over PCIe. */
+ * packed, for lane_width <= 32 -- a quarter fewer bytes over PCIe -- or 8
+ * bytes, one uint64 engine_id << 37 | group << 32 | lane_mask, half the
+ * bytes, when every engine id ever added is < 2^27 and the round has <= 32
+ * groups (a fetch that does not fit fails with TSG_ECAPACITY). */
 int tsg_set_record_bytes(tsg_engine* h, int32_t bytes);
 /* device pointer + count of the round's records (for device-side consumers) */
 int tsg_reports_device(tsg_engine* h, void** device_ptr, int64_t* n);

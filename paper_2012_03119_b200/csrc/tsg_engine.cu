@@ -189,6 +189,7 @@ struct tsg_engine {
     cudaStream_t egress = nullptr;
     cudaEvent_t ev_ready = nullptr; // compacted records ready for copy-out
     int32_t record_bytes = 16;      // egress record format (tsg_set_record_bytes)
+    int64_t max_id = -1;            // largest engine id ever added (8-byte records need < 2^27)
     uint8_t* out12 = nullptr;       // 12-byte egress records of the current slot
     int64_t out12_cap = 0;
     bool oob = false;  // a stored literal may exceed num_vars (checked before testing)
@@ -852,6 +853,7 @@ int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, 
             int64_t v = lits[j] < 0 ? -(int64_t)lits[j] : lits[j];
             if (v > h->V) h->oob = true;  // stored as-is; testing raises (numpy IndexError, engine.py:251)
         }
+        if (ids[i] < 0 || ids[i] > h->max_id) h->max_id = std::max<int64_t>(h->max_id, ids[i] < 0 ? INT64_MAX : ids[i]);
         auto it = h->by_size.find(s);
         int bi;
         if (it == h->by_size.end()) {
@@ -1520,6 +1522,17 @@ int egress_view(tsg_engine* h, int64_t k, const void** src, int64_t* bytes) {
         *bytes = k * (int64_t)sizeof(tsg_report);
         return TSG_OK;
     }
+    if (h->record_bytes == 8) {
+        if (h->max_id >= (int64_t(1) << 27) || h->rs[h->fetch_rs].fl.n_groups > 32)
+            return fail(TSG_ECAPACITY, "8-byte records need engine ids < 2^27 and <= 32 groups (largest id %lld, "
+                        "%d groups): use 12-byte records", (long long)h->max_id, h->rs[h->fetch_rs].fl.n_groups);
+        CKR(dgrow(h, &h->out12, &h->out12_cap, k * 8));
+        k_pack_records8<<<grid_for(k), 256, 0, h->st>>>(h->out, k, reinterpret_cast<uint64_t*>(h->out12));
+        CK(cudaGetLastError());
+        *src = h->out12;
+        *bytes = k * 8;
+        return TSG_OK;
+    }
     CKR(dgrow(h, &h->out12, &h->out12_cap, k * 12));
     k_pack_records12<<<grid_for(k), 256, 0, h->st>>>(h->out, k, h->out12);
     CK(cudaGetLastError());
@@ -1547,9 +1560,10 @@ int tsg_fetch_reports(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n) {
 
 int tsg_set_record_bytes(tsg_engine* h, int32_t bytes) {
     CKR(validate_handle(h));
-    if (bytes != 16 && bytes != 12) return fail(TSG_EINVAL, "record bytes must be 16 or 12, got %d", bytes);
-    if (bytes == 12 && h->cfg.lane_width > 32)
-        return fail(TSG_EINVAL, "12-byte records carry a 32-bit lane mask: lane_width %d > 32", h->cfg.lane_width);
+    if (bytes != 16 && bytes != 12 && bytes != 8)
+        return fail(TSG_EINVAL, "record bytes must be 16, 12 or 8, got %d", bytes);
+    if (bytes != 16 && h->cfg.lane_width > 32)
+        return fail(TSG_EINVAL, "%d-byte records carry a 32-bit lane mask: lane_width %d > 32", bytes, h->cfg.lane_width);
     h->record_bytes = bytes;
     return TSG_OK;
 }

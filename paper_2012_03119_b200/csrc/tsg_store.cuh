@@ -78,6 +78,16 @@ __global__ void k_pack_records12(const tsg_report* __restrict__ in, int64_t n, u
     }
 }
 
+// 8-byte egress records: engine_id << 37 | group << 32 | lane_mask (engine
+// ids < 2^27, groups < 32, lane width <= 32; checked by the host).
+__global__ void k_pack_records8(const tsg_report* __restrict__ in, int64_t n, uint64_t* __restrict__ out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const tsg_report r = in[i];
+        out[i] = ((r.key >> 16) << 37) | ((r.key & 0x1F) << 32) | (uint32_t)r.lane_mask;
+    }
+}
+
 // K7: reduce keys over the whole store.  Eligible clauses (id < watermark,
 // engine.py:486) get their activity bits as key (non-negative doubles order
 // like their IEEE bit patterns); ineligible ones sort last.

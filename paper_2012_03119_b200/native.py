@@ -178,14 +178,16 @@ class NativeEngine:
     record_bytes = 16
 
     def set_record_bytes(self, nbytes: int) -> None:
-        """Egress record format: 16 (tsg_report) or 12 (lane_width <= 32)."""
+        """Egress record format: 16 (tsg_report), 12 (lane_width <= 32) or 8
+        (also engine ids < 2^27 and <= 32 groups)."""
         check(self.L.tsg_set_record_bytes(self.h, nbytes))
         self.record_bytes = nbytes
 
     def fetch_raw(self, n: int, out: Optional[np.ndarray] = None) -> np.ndarray:
         """The round's records in the egress format (tsg_report, or 12-byte)."""
         if out is None or len(out) < n:
-            out = np.zeros(max(n, 1), REPORT_DTYPE if self.record_bytes == 16 else reports.RECORD12_DTYPE)
+            out = np.zeros(max(n, 1), {16: REPORT_DTYPE, 12: reports.RECORD12_DTYPE,
+                                       8: reports.RECORD8_DTYPE}[self.record_bytes])
         got = C.c_int64(0)
         if n:
             check(self.L.tsg_fetch_reports(self.h, ptr(out), n, C.byref(got)))

@@ -548,8 +548,8 @@ def test_abi_error_paths(P):
 
 
 def test_twelve_byte_egress_records(P):
-    # 12-byte egress records carry the same (engine id, group, lane mask) as
-    # the 16-byte tsg_report, sync and async; lane_width 64 refuses them
+    # 12- and 8-byte egress records carry the same (engine id, group, lane
+    # mask) as the 16-byte tsg_report, sync and async; lane_width 64 refuses them
     from paper_2012_03119_b200 import reports as R
     from paper_2012_03119_b200 import workload as W
     from paper_2012_03119_b200.native import NativeEngine
@@ -559,14 +559,14 @@ def test_twelve_byte_egress_records(P):
     snaps = W.snapshots(3, 32, nv, rng)
     gl, gt = W.groups_for(3, 32)
     out = []
-    for nbytes in (16, 12):
+    for nbytes in (16, 12, 8):
         e = NativeEngine(nv)
         e.set_record_bytes(nbytes)
         e.add_clauses(flat, offs, ids)
         e.stage(snaps)
         r = e.round(gl, gt, 1.0)
         sync = np.sort(R.decode(e.fetch_raw(r.reports)), order=["engine_id", "group"])
-        buf = np.zeros(r.reports, R.RECORD12_DTYPE if nbytes == 12 else R.RECORD_DTYPE)
+        buf = np.zeros(r.reports, {16: R.RECORD_DTYPE, 12: R.RECORD12_DTYPE, 8: R.RECORD8_DTYPE}[nbytes])
         assert e.fetch_async(buf) == r.reports
         e.wait()
         out.append((sync, np.sort(R.decode(buf), order=["engine_id", "group"])))
@@ -576,6 +576,20 @@ def test_twelve_byte_egress_records(P):
         for b in out:
             assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
     w = NativeEngine(nv, 64, 32)
-    with pytest.raises(ValueError):
-        w.set_record_bytes(12)
+    for nbytes in (12, 8):
+        with pytest.raises(ValueError):
+            w.set_record_bytes(nbytes)
     w.close()
+    # 8-byte records refuse engine ids >= 2^27 and rounds of more than 32 groups
+    from paper_2012_03119_b200._lib import CapacityError
+    for big_id, threads in ((True, 3), (False, 33)):
+        e = NativeEngine(nv)
+        e.set_record_bytes(8)
+        e.add_clauses(flat, offs, ids + ((1 << 27) if big_id else 0))
+        sn = W.snapshots(threads, 32, nv, rng)
+        e.stage(sn)
+        r = e.round(*W.groups_for(threads, 32), 1.0)
+        assert r.reports > 0
+        with pytest.raises(CapacityError):
+            e.fetch_raw(r.reports)
+        e.close()

@@ -36,17 +36,25 @@ def t(name, fn):
     return r
 
 
-for i in range(12):
+eng.set_record_bytes(8)
+eng.prepare(gl, gt)
+pending = 0
+w0 = time.perf_counter()
+for i in range(24):
     t("stage", lambda: _lib.check(L.tsg_stage_packed(eng.h, C.c_void_p(hp.data_ptr()), A, pw, 0)))
-    t("prepare", lambda: eng.prepare(gl, gt))
-    t("encode", lambda: eng.encode())
-    if i:
+    if pending:
         r = t("collect", lambda: eng.collect())
         got = C.c_int64(0)
         t("fetch_async", lambda: _lib.check(L.tsg_fetch_reports_async(
             eng.h, C.c_void_p(bufs[i % 2].data_ptr()), r.reports, C.byref(got))))
+        pending -= 1
+    t("encode", lambda: eng.encode())
     t("launch", lambda: eng.launch(1.0))
+    pending += 1
+    if i == 3:
+        w0 = time.perf_counter()
 t("collect", lambda: eng.collect())
 t("wait", lambda: eng.wait())
+print(f"steady ms/step {(time.perf_counter() - w0) / 20 * 1e3:.3f}")
 for k, v in T.items():
     print(f"{k:12s} median {np.median(v):8.3f} ms  max {max(v):8.3f}")
