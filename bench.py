@@ -52,6 +52,9 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
+L2_GATHER_CEILING = 0.99  # measured sectors/clk/SM
+
+
 def load_traffic(config):
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
@@ -530,6 +533,22 @@ def main():
 
     if rank == 0:
         clocks = clk.summary()
+        # the bound that actually limits k_test: L2 sectors (literal rows +
+        # random table gathers, from the committed ncu capture) per SM clock,
+        # against the measured random-gather ceiling
+        try:
+            sectors = load_traffic(cfg.name + "_l2_read_sectors")
+            nsm = torch.cuda.get_device_properties(local).multi_processor_count
+            mhz = float(clocks.get("sm_mhz") or 0) if isinstance(clocks, dict) else 0.0
+            if sectors and mhz > 0:
+                per_clk = sectors / (test_ms_avg * 1e-3 * mhz * 1e6 * nsm)
+                roofline["l2_gather"] = {
+                    "sectors_per_launch": sectors, "achieved_sectors_per_clk_per_sm": per_clk,
+                    "ceiling_sectors_per_clk_per_sm": L2_GATHER_CEILING, "frac": per_clk / L2_GATHER_CEILING,
+                    "ceiling_source": "tools/microbench/gather_modes.cu: random 16-byte gathers from an "
+                                      "L2-resident table as divergent LDGs, B200"}
+        except Exception:
+            pass
         line = {
             "metric": "clause_assignment_tests_per_second", "value": value, "unit": "clause_assignment_tests/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,

@@ -152,6 +152,7 @@ struct tsg_engine {
         unsigned long long* ctr = nullptr;
         unsigned long long* h_ctr = nullptr;  // pinned [8], written by the kernel
         bool pol_pending = false;             // an encode counted into ctr[6..7] since the last launch
+        unsigned long long* tiles = nullptr;  // device DynTiles counters, zero between launches
         cudaEvent_t ev_done = nullptr;        // its counters are on the host
         cudaEvent_t ev_tst[2] = {nullptr, nullptr};
         int64_t* carry = nullptr;             // per-clause (round, tid) stamps of multi-chunk rounds
@@ -451,6 +452,11 @@ int launch_test(tsg_engine* h, int k, int c, double inc, int emit_only) {
     p.carry_out_tid = (g0 + G < rd.n_groups && rd.gtid[g0 + G - 1] == rd.gtid[g0 + G]) ? rd.gtid[g0 + G - 1] : -1;
     p.emit_only = emit_only;
     p.pub = (!emit_only && c == rd.n_chunks - 1) ? R.h_ctr : nullptr;
+    // dynamic tile counters balance the SMs (±5 % active cycles with the
+    // static stride) but measured no faster: off unless TSG_DYN_TILES=1
+    static const bool dyn = getenv("TSG_DYN_TILES") && atoi(getenv("TSG_DYN_TILES")) != 0;
+    p.dyn_tiles = dyn ? 1 : 0;
+    p.tiles = R.tiles;
     p.slab_tile0 = h->d_slab_tile0;
     p.slab_desc0 = reinterpret_cast<const int32_t*>(h->d_slab_tile0 + (h->n_slabs + 1));
     p.sched = reinterpret_cast<const uint64_t*>(h->d_slab_tile0 + 2 * (h->n_slabs + 1));
@@ -791,6 +797,9 @@ int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
         if (cudaMallocHost(&R.h_ctr, 8 * sizeof(unsigned long long)) != cudaSuccess) { delete h; return fail(TSG_ECUDA, "pinned alloc"); }
         if (dalloc(h, (void**)&R.ctr, 8 * sizeof(unsigned long long))) { delete h; return TSG_ENOMEM; }
         if (cudaMemsetAsync(R.ctr, 0, 8 * sizeof(unsigned long long), h->st) != cudaSuccess) { delete h; return fail(TSG_ECUDA, "memset"); }
+        const int64_t tb = (int64_t)TSG_DYN_NC * DYN_STRIDE * sizeof(unsigned long long);
+        if (dalloc(h, (void**)&R.tiles, tb)) { delete h; return TSG_ENOMEM; }
+        if (cudaMemsetAsync(R.tiles, 0, tb, h->st) != cudaSuccess) { delete h; return fail(TSG_ECUDA, "memset"); }
     }
     if (cudaMallocHost(&h->h_mctr, 8 * sizeof(unsigned long long)) != cudaSuccess) { delete h; return fail(TSG_ECUDA, "pinned alloc"); }
     if (dalloc(h, (void**)&h->mctr, 8 * sizeof(unsigned long long))) { delete h; return TSG_ENOMEM; }
@@ -809,7 +818,7 @@ int tsg_destroy(tsg_engine* h) {
     if (h->ingress) cudaStreamSynchronize(h->ingress);
     dfree(h, h->rows_own); dfree(h, h->pbuf[0]); dfree(h, h->pbuf[1]); dfree(h, h->tables); dfree(h, h->d_desc); dfree(h, h->out);
     dfree(h, h->mctr); dfree(h, h->out2); dfree(h, h->codes);
-    for (auto& R : h->rs) { dfree(h, R.ctr); dfree(h, R.carry); }
+    for (auto& R : h->rs) { dfree(h, R.ctr); dfree(h, R.carry); dfree(h, R.tiles); }
     if (h->egress) cudaStreamSynchronize(h->egress);
     dfree(h, h->alt.out); dfree(h, h->alt.out2); dfree(h, h->alt.out12); dfree(h, h->out12);
     cudaStreamSynchronize(h->st);

@@ -522,6 +522,8 @@ struct TestParams {
     int32_t carry_out_tid;     // last tid of the chunk if it continues into the next chunk, else -1
     int32_t emit_only;         // replay after report-buffer overflow: no activity / counter side effects
     unsigned long long* pub;   // last launch of a round: host-mapped [8] the last CTA publishes ctr to
+    int32_t dyn_tiles;         // tiles from the counters `tiles` (DynTiles) instead of a static stride
+    unsigned long long* tiles; // [TSG_DYN_NC * DYN_STRIDE] per-launch tile counters (zero between launches)
     const int64_t* slab_tile0; // slab kernel: first tile of each slab (+ end)
     const int32_t* slab_desc0; // slab kernel: first descriptor of each slab (+ end)
     const uint64_t* sched;     // slab kernel: per CTA slab << 32 | rank << 16 | CTAs on the slab
@@ -762,6 +764,34 @@ __device__ __forceinline__ void stage1_slab(const TestParams<LW, GW>& p, const S
 }
 
 // Tile sources (warp-uniform, strictly increasing per warp; -1 = done).
+// Warps take tiles one at a time from TSG_DYN_NC per-launch counters
+// (counter c hands out tiles c, c + NC, c + 2 NC, ...; warp w uses counter
+// w % NC), so SMs that run faster -- the two dies' L2 distances differ --
+// take more tiles instead of idling at the end of a static share.  The
+// atomic for the tile after next is issued when `next` returns, so its
+// latency overlaps a whole tile.
+#ifndef TSG_DYN_NC
+#define TSG_DYN_NC 8
+#endif
+constexpr int DYN_STRIDE = 32;  // u64 words between counters (separate L2 lines)
+struct DynTiles {
+    unsigned long long* ctr;  // this warp's counter
+    int c, end;
+    unsigned long long ahead = 0;  // lane 0: the next k, in flight
+    bool primed = false;
+    __device__ __forceinline__ int next(int lane) {
+        if (!primed) {
+            primed = true;
+            if (lane == 0) ahead = atomicAdd(ctr, 1ull);
+        }
+        const unsigned long long k = __shfl_sync(0xffffffffu, ahead, 0);
+        const long long t = (long long)c + (long long)TSG_DYN_NC * (long long)k;
+        if (t >= end) return -1;
+        if (lane == 0) ahead = atomicAdd(ctr, 1ull);
+        return (int)t;
+    }
+};
+
 struct StrideTiles {  // tiles t, t + step, ... < end
     int t, step, end;  // tile indices (the host keeps n_tiles < 2^31)
     bool started = false;
@@ -955,13 +985,20 @@ __device__ __forceinline__ void finish_block(const TestParams<LW, GW>& p, WarpAc
             if (a) atomicAdd(p.ctr + 1, a);
             if (bb) atomicAdd(p.ctr + 2, bb);
         }
-        if (p.pub) {  // the round's last CTA hands the counters to the host and re-zeroes them
+        // the launch's last CTA re-zeroes the tile counters and the CTA count
+        // [5]; on a round's last launch it also hands the counters to the
+        // host and re-zeroes them
+        __threadfence();
+        if (atomicAdd(p.ctr + 5, 1ull) == gridDim.x - 1) {
             __threadfence();
-            if (atomicAdd(p.ctr + 5, 1ull) == gridDim.x - 1) {
-                __threadfence();
+            if (p.tiles)
+                for (int c = 0; c < TSG_DYN_NC; ++c) atomicExch(p.tiles + c * DYN_STRIDE, 0ull);
+            if (p.pub) {
 #pragma unroll
                 for (int i = 0; i < 8; ++i) p.pub[i] = atomicExch(p.ctr + i, 0ull);
                 __threadfence_system();
+            } else {
+                atomicExch(p.ctr + 5, 0ull);
             }
         }
     }
@@ -988,9 +1025,16 @@ __global__ void __launch_bounds__(THREADS, MINB) k_test(const __grid_constant__ 
     const int warp = threadIdx.x >> 5;
     const int nwarps = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
     WarpAcc acc;
-    StrideTiles src{(int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5), nwarps, (int)p.n_tiles};
     RegRows rows;
-    test_tiles<LW, GW, TAB>(p, tab, p.buckets, p.nb, src, rows, lane, acc);
+    if (p.dyn_tiles) {
+        const int gw = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+        const int c = gw % TSG_DYN_NC;
+        DynTiles src{p.tiles + c * DYN_STRIDE, c, (int)p.n_tiles};
+        test_tiles<LW, GW, TAB>(p, tab, p.buckets, p.nb, src, rows, lane, acc);
+    } else {
+        StrideTiles src{(int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5), nwarps, (int)p.n_tiles};
+        test_tiles<LW, GW, TAB>(p, tab, p.buckets, p.nb, src, rows, lane, acc);
+    }
     finish_block<LW, GW, WARPS>(p, acc, lane, warp, s_acc);
 }
 

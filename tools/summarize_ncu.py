@@ -104,6 +104,9 @@ def main():
             wr = got.get("dram__bytes_write.sum")
             if rd and wr:
                 traffic[config] = to_bytes(rd[1], rd[2]) + to_bytes(wr[1], wr[2])
+            sec = got.get("lts__t_sectors_srcunit_tex_op_read.sum")
+            if sec:  # L2 sectors the launch read (the gather-bound roofline in bench.py)
+                traffic[config + "_l2_read_sectors"] = float(sec[1])
     with open(traffic_path, "w") as fh:
         json.dump(traffic, fh, indent=1)
     if launches:
