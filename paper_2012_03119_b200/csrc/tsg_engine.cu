@@ -199,6 +199,9 @@ struct tsg_engine {
     int64_t grid[32] = {0};       // persistent grid per k_test variant
     int64_t grid_smem[32];        // shared-memory size the grid was computed for (-1: none)
     bool smem_table = true;       // shared-memory code table when it fits (TSG_SMEM_TABLE=0 disables)
+    // dynamic tile counters in k_test balance the SMs (±5 % active cycles
+    // with the static stride) but measured no faster: opt-in, TSG_DYN_TILES=1
+    bool dyn_tiles = false;
     uint8_t* codes = nullptr;     // literal-code table of the current chunk
     int64_t codes_cap = 0;
 
@@ -452,10 +455,7 @@ int launch_test(tsg_engine* h, int k, int c, double inc, int emit_only) {
     p.carry_out_tid = (g0 + G < rd.n_groups && rd.gtid[g0 + G - 1] == rd.gtid[g0 + G]) ? rd.gtid[g0 + G - 1] : -1;
     p.emit_only = emit_only;
     p.pub = (!emit_only && c == rd.n_chunks - 1) ? R.h_ctr : nullptr;
-    // dynamic tile counters balance the SMs (±5 % active cycles with the
-    // static stride) but measured no faster: off unless TSG_DYN_TILES=1
-    static const bool dyn = getenv("TSG_DYN_TILES") && atoi(getenv("TSG_DYN_TILES")) != 0;
-    p.dyn_tiles = dyn ? 1 : 0;
+    p.dyn_tiles = h->dyn_tiles ? 1 : 0;
     p.tiles = R.tiles;
     p.slab_tile0 = h->d_slab_tile0;
     p.slab_desc0 = reinterpret_cast<const int32_t*>(h->d_slab_tile0 + (h->n_slabs + 1));
@@ -746,6 +746,7 @@ int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
     h->cfg = *cfg;
     h->V = num_vars;
     if (const char* e = getenv("TSG_SMEM_TABLE")) h->smem_table = atoi(e) != 0;
+    if (const char* e = getenv("TSG_DYN_TILES")) h->dyn_tiles = atoi(e) != 0;
     if (const char* e = getenv("TSG_L2_PERSIST")) h->l2_persist = atoi(e) != 0;
     if (const char* e = getenv("TSG_PIVOT")) h->pivot = atoi(e) != 0;
     if (const char* e = getenv("TSG_PREFER")) { h->prefer = atoi(e); h->prefer_fixed = true; }

@@ -136,10 +136,12 @@ def test_literal_out_of_range_raises(P):
 #   l2         aggregate table gathered from L2, unpartitioned store
 #   slab       store partitioned into variable slabs (opt-in layout), hot prefix from shared memory
 #   smem_slab  partitioned store (hot-prefix literal order) tested by the smem kernel
-TABLES = {"smem": {"TSG_SMEM_TABLE": "1", "TSG_SLABS": "0"},
-          "l2": {"TSG_SMEM_TABLE": "0", "TSG_SLABS": "0"},
-          "slab": {"TSG_SMEM_TABLE": "0", "TSG_SLABS": "4"},
-          "smem_slab": {"TSG_SMEM_TABLE": "1", "TSG_SLABS": "4"}}
+#   l2_dyn     l2 with dynamic tile counters (opt-in scheduling)
+TABLES = {"smem": {"TSG_SMEM_TABLE": "1", "TSG_SLABS": "0", "TSG_DYN_TILES": "0"},
+          "l2": {"TSG_SMEM_TABLE": "0", "TSG_SLABS": "0", "TSG_DYN_TILES": "0"},
+          "l2_dyn": {"TSG_SMEM_TABLE": "0", "TSG_SLABS": "0", "TSG_DYN_TILES": "1"},
+          "slab": {"TSG_SMEM_TABLE": "0", "TSG_SLABS": "4", "TSG_DYN_TILES": "0"},
+          "smem_slab": {"TSG_SMEM_TABLE": "1", "TSG_SLABS": "4", "TSG_DYN_TILES": "0"}}
 
 
 def use_table(monkeypatch, table):
@@ -197,7 +199,7 @@ def test_c1_parity_vs_oracle(P, monkeypatch, table):
     assert res.reports > 0 and res.lane_triggers > 0
 
 
-@pytest.mark.parametrize("table", ["smem", "l2", "slab", "smem_slab"])
+@pytest.mark.parametrize("table", ["smem", "l2", "l2_dyn", "slab", "smem_slab"])
 @pytest.mark.parametrize("lw,gw,threads,lanes", [(32, 32, 3, 40), (64, 64, 2, 64), (64, 8, 5, 70),
                                                  (7, 3, 4, 20), (1, 64, 3, 30), (32, 16, 40, 32)])
 def test_widths_and_multichunk_parity(P, monkeypatch, table, lw, gw, threads, lanes):
@@ -207,7 +209,7 @@ def test_widths_and_multichunk_parity(P, monkeypatch, table, lw, gw, threads, la
              seed=lw * 100 + gw, rounds=2, size_lo=0, size_hi=12)
 
 
-@pytest.mark.parametrize("table", ["smem", "l2", "slab"])
+@pytest.mark.parametrize("table", ["smem", "l2", "l2_dyn", "slab"])
 def test_c2_shape_parity(P, monkeypatch, table):
     # C2's 50k vars x 8 groups is the largest code table that fits shared memory;
     # with it disabled the store's 3 natural slabs drive the slab kernel
