@@ -863,7 +863,7 @@ __device__ __forceinline__ void test_tiles(const TestParams<LW, GW>& p, const TA
                         int32_t l[4];
                         Subset<GW> s[4];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) l[u] = (j + u < size) ? __ldg(lp + (j + u) * STRIDE) : p.sentinel;
+                        for (int u = 0; u < 4; ++u) l[u] = (j + u < size) ? ld_lit_tail(lp + (j + u) * STRIDE) : p.sentinel;
 #pragma unroll
                         for (int u = 0; u < 4; ++u) s[u] = tab.get(l[u]);
 #pragma unroll
@@ -935,7 +935,7 @@ __device__ __forceinline__ void test_tiles(const TestParams<LW, GW>& p, const TA
                     if (size > PF && (lf | lo2) != LW(0)) {
                         const int32_t* lp = lane_lits(bd, tile, lane);
                         for (int j = PF; j < size && (lf | lo2) != LW(0); ++j) {
-                            const int32_t l = __ldg(lp + j * STRIDE);
+                            const int32_t l = ld_lit_tail(lp + j * STRIDE);
                             const LaneEntry<LW> e = ld_lane(lt + lit_var(l));
                             step<LW>(lf, lo2, l < 0 ? (e.s & e.t) : (e.s & ~e.t), ~e.s);
                         }
