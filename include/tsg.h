@@ -66,6 +66,24 @@ typedef struct tsg_round_result {
     double test_ms;                   /* device time of the trigger kernels       */
 } tsg_round_result;
 
+/* Cumulative figures of an engine (tsg_counters): the reference's counter
+ * dict (engine.py:284-299) as far as the device sees it -- snapshot and
+ * drop counts stay with the host side that owns the queues. */
+typedef struct tsg_counters_t {
+    int64_t rounds;                   /* rounds collected                         */
+    int64_t reports;                  /* records emitted                          */
+    int64_t clauses_tested;
+    int64_t aggregate_tests;
+    int64_t aggregate_tests_negative;
+    int64_t lane_tests;
+    int64_t lane_triggers;
+    int64_t reruns;                   /* report-buffer overflow replays           */
+    int64_t clauses_added;
+    int64_t clauses_removed;          /* by tsg_reduce (engine.py:469-505)        */
+    int64_t clauses_deleted;          /* by tsg_remove_clauses                    */
+    int64_t reduces;
+} tsg_counters_t;
+
 /* One report record, 16 bytes (engine.py:90-102 Report minus the literals,
  * which the host keeps): key = engine_id << 16 | group, where `group` is the
  * global group index in round order (engine.py:390-399) and the destination
@@ -113,6 +131,16 @@ int tsg_bucket_info(tsg_engine* h, int32_t b, int32_t* size, int64_t* count);
 int tsg_bucket_read(tsg_engine* h, int32_t b, int32_t* lits, int64_t* ids,
                     int32_t* origins, double* acts);
 /* ClauseStore.scale_activities (engine.py:233-235) */
+/* Literals of stored clauses by engine id, original literal order
+ * (engine.py:165-169 lits_at; Report.lits, engine.py:409-414), so a host
+ * that keeps no literal copy can resolve report records.  sizes[i] = size
+ * of clause ids[i] or -1 if it is not stored; the found clauses' literals
+ * are concatenated in request order into lits (*n_lits of them; with
+ * lits == NULL only sizes and *n_lits are filled; TSG_ECAPACITY if they do
+ * not fit lits_cap). */
+int tsg_get_clauses(tsg_engine* h, const int64_t* ids, int64_t n, int32_t* sizes, int32_t* lits,
+                    int64_t lits_cap, int64_t* n_lits);
+int tsg_counters(tsg_engine* h, tsg_counters_t* out);
 int tsg_scale_activities(tsg_engine* h, double factor);
 /* reduce_store selection + compaction (engine.py:476-500): remove the
  * `target` smallest (activity, engine_id) among clauses with id <

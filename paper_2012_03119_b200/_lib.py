@@ -40,6 +40,12 @@ class tsg_round_result(C.Structure):
                 ("encode_ms", C.c_double), ("test_ms", C.c_double)]
 
 
+class tsg_counters_t(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in (
+        "rounds", "reports", "clauses_tested", "aggregate_tests", "aggregate_tests_negative", "lane_tests",
+        "lane_triggers", "reruns", "clauses_added", "clauses_removed", "clauses_deleted", "reduces")]
+
+
 from .reports import RECORD_DTYPE as REPORT_DTYPE  # noqa: E402  (tsg_report, 16 bytes)
 
 # every symbol include/tsg.h declares (checked by tests/test_abi.py)
@@ -51,7 +57,7 @@ EXPORTS = (
     "tsg_reports_device", "tsg_sync", "tsg_stream", "tsg_pack", "tsg_aggregate", "tsg_lane_trigger",
     "tsg_aggregate_trigger", "tsg_packed_words", "tsg_pack_rows", "tsg_stage_packed",
     "tsg_fetch_reports_async", "tsg_fetch_wait", "tsg_round_launch", "tsg_round_collect",
-    "tsg_set_record_bytes",
+    "tsg_set_record_bytes", "tsg_get_clauses", "tsg_counters",
 )
 
 _lib = None
@@ -73,6 +79,8 @@ def _declare(L):
         "tsg_bucket_info": ([P, I32, C.POINTER(C.c_int32), pI64], C.c_int),
         "tsg_bucket_read": ([P, I32, P, P, P, P], C.c_int),
         "tsg_scale_activities": ([P, D], C.c_int),
+        "tsg_get_clauses": ([P, P, I64, P, P, I64, pI64], C.c_int),
+        "tsg_counters": ([P, P], C.c_int),
         "tsg_reduce": ([P, I64, I64, pI64, P], C.c_int),
         "tsg_remove_clauses": ([P, P, I64, pI64], C.c_int),
         "tsg_stage_snapshots": ([P, P, I64, I64, I32], C.c_int),

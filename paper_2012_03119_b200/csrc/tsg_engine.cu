@@ -196,6 +196,7 @@ struct tsg_engine {
     bool oob = false;  // a stored literal may exceed num_vars (checked before testing)
     int64_t round_seq = 0;
     int enc_attr = 0;             // k_encode_packed32 shared-memory attribute set, per GW
+    tsg_counters_t totals{};      // cumulative figures (tsg_counters)
     int64_t grid[32] = {0};       // persistent grid per k_test variant
     int64_t grid_smem[32];        // shared-memory size the grid was computed for (-1: none)
     bool smem_table = true;       // shared-memory code table when it fits (TSG_SMEM_TABLE=0 disables)
@@ -937,6 +938,7 @@ int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, 
         p.count += k;
         CK(cudaStreamSynchronize(h->st));  // host vectors go out of scope
     }
+    h->totals.clauses_added += n;
     return TSG_OK;
 }
 
@@ -1000,6 +1002,87 @@ int tsg_bucket_read(tsg_engine* h, int32_t bi, int32_t* lits, int64_t* ids, int3
         if (acts) acts[k] = hac[i];
         if (lits && b.size) memcpy(lits + k * b.size, hl.data() + i * b.size, b.size * 4);
     }
+    return TSG_OK;
+}
+
+// Literals of stored clauses by engine id, in their original order (the
+// reference's `lits_at` / Report.lits, engine.py:165-169, 409-414): a C host
+// that keeps no literal copy of its own resolves report records with this.
+int tsg_get_clauses(tsg_engine* h, const int64_t* ids, int64_t n, int32_t* sizes, int32_t* lits, int64_t lits_cap,
+                    int64_t* n_lits) {
+    CKR(validate_handle(h));
+    if (n < 0 || (n > 0 && (!ids || !sizes || !n_lits))) return fail(TSG_EINVAL, "bad arguments");
+    if (n_lits) *n_lits = 0;
+    if (n == 0) return TSG_OK;
+    DevGuard g(h->dev);
+    std::vector<int64_t> qi(n);
+    for (int64_t i = 0; i < n; ++i) qi[i] = i;
+    std::sort(qi.begin(), qi.end(), [&](int64_t a, int64_t b) { return ids[a] < ids[b]; });
+    std::vector<int64_t> q(n);
+    for (int64_t i = 0; i < n; ++i) q[i] = ids[qi[i]];
+    // parts in a flat list: part index -> (bucket, part)
+    std::vector<std::pair<int, int>> parts;
+    for (int bi = 0; bi < (int)h->buckets.size(); ++bi)
+        for (int pi = 0; pi < (int)h->buckets[bi].parts.size(); ++pi)
+            if (h->buckets[bi].parts[pi].count) parts.push_back({bi, pi});
+    int64_t* d = nullptr;  // [q | qidx | loc]
+    CKR(dalloc(h, (void**)&d, 3 * n * 8));
+    CK(cudaMemcpyAsync(d, q.data(), n * 8, cudaMemcpyHostToDevice, h->st));
+    CK(cudaMemcpyAsync(d + n, qi.data(), n * 8, cudaMemcpyHostToDevice, h->st));
+    CK(cudaMemsetAsync(d + 2 * n, 0xFF, n * 8, h->st));
+    for (int64_t k = 0; k < (int64_t)parts.size(); ++k) {
+        const Part& p = h->buckets[parts[k].first].parts[parts[k].second];
+        k_find_ids<<<grid_for(p.count), 256, 0, h->st>>>(p.ids, p.count, d, d + n, n, k, d + 2 * n);
+    }
+    CK(cudaGetLastError());
+    std::vector<int64_t> loc(n);
+    CK(cudaMemcpyAsync(loc.data(), d + 2 * n, n * 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    dfree(h, d);
+    int64_t total = 0;
+    std::vector<int64_t> off(n);
+    for (int64_t i = 0; i < n; ++i) {
+        if (loc[i] < 0) { sizes[i] = -1; off[i] = total; continue; }
+        sizes[i] = h->buckets[parts[loc[i] >> 40].first].size;
+        off[i] = total;
+        total += sizes[i];
+    }
+    *n_lits = total;
+    if (!lits || total == 0) return TSG_OK;
+    if (total > lits_cap) return fail(TSG_ECAPACITY, "%lld literals do not fit %lld", (long long)total, (long long)lits_cap);
+    // per part: gather its hits' literals, then place them in request order
+    std::vector<std::vector<int64_t>> hit(parts.size());
+    for (int64_t i = 0; i < n; ++i)
+        if (loc[i] >= 0) hit[loc[i] >> 40].push_back(i);
+    for (size_t k = 0; k < parts.size(); ++k) {
+        if (hit[k].empty()) continue;
+        const Bucket& b = h->buckets[parts[k].first];
+        const Part& p = b.parts[parts[k].second];
+        const int64_t m = (int64_t)hit[k].size();
+        if (b.size == 0) continue;
+        std::vector<int64_t> slots(m);
+        for (int64_t j = 0; j < m; ++j) slots[j] = loc[hit[k][j]] & ((int64_t(1) << 40) - 1);
+        int64_t* ds = nullptr;
+        int32_t* dl = nullptr;
+        CKR(dalloc(h, (void**)&ds, m * 8));
+        CKR(dalloc(h, (void**)&dl, m * b.size * 4));
+        CK(cudaMemcpyAsync(ds, slots.data(), m * 8, cudaMemcpyHostToDevice, h->st));
+        k_deinterleave_sel<<<grid_for(m), 256, 0, h->st>>>(p.lits, p.order, ds, m, b.size, dl);
+        CK(cudaGetLastError());
+        std::vector<int32_t> hl(m * b.size);
+        CK(cudaMemcpyAsync(hl.data(), dl, m * b.size * 4, cudaMemcpyDeviceToHost, h->st));
+        CK(cudaStreamSynchronize(h->st));
+        dfree(h, ds);
+        dfree(h, dl);
+        for (int64_t j = 0; j < m; ++j) memcpy(lits + off[hit[k][j]], hl.data() + j * b.size, b.size * 4);
+    }
+    return TSG_OK;
+}
+
+int tsg_counters(tsg_engine* h, tsg_counters_t* out) {
+    CKR(validate_handle(h));
+    if (!out) return fail(TSG_EINVAL, "null argument");
+    *out = h->totals;
     return TSG_OK;
 }
 
@@ -1067,6 +1150,8 @@ int tsg_reduce(tsg_engine* h, int64_t eligible_below, int64_t target, int64_t* r
     dfree(h, keep); dfree(h, doomed_ids);
     CK(cudaStreamSynchronize(h->st));
     *removed = rem;
+    h->totals.reduces += 1;
+    h->totals.clauses_removed += rem;
     return TSG_OK;
 }
 
@@ -1103,6 +1188,7 @@ int tsg_remove_clauses(tsg_engine* h, const int64_t* ids, int64_t n, int64_t* re
     dfree(h, d_del); dfree(h, keep);
     CK(cudaStreamSynchronize(h->st));
     *removed = (int64_t)gone;
+    h->totals.clauses_deleted += (int64_t)gone;
     return TSG_OK;
 }
 
@@ -1466,6 +1552,15 @@ int round_collect(tsg_engine* h, tsg_round_result* out) {
             else cudaGetLastError();
         }
     }
+    auto& T = h->totals;
+    T.rounds += 1;
+    T.reports += res.reports;
+    T.clauses_tested += res.clauses_tested;
+    T.aggregate_tests += res.aggregate_tests;
+    T.aggregate_tests_negative += res.aggregate_tests_negative;
+    T.lane_tests += res.lane_tests;
+    T.lane_triggers += res.lane_triggers;
+    T.reruns += res.reruns;
     if (out) *out = res;
     return TSG_OK;
 }

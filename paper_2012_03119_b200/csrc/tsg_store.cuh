@@ -78,6 +78,44 @@ __global__ void k_pack_records12(const tsg_report* __restrict__ in, int64_t n, u
     }
 }
 
+// Clause lookup by engine id (tsg_get_clauses): every stored slot binary-
+// searches the sorted query ids; a hit records (part, slot) for its query.
+__global__ void k_find_ids(const int64_t* __restrict__ ids, int64_t n, const int64_t* __restrict__ q,
+                           const int64_t* __restrict__ qidx, int64_t nq, int64_t part, int64_t* __restrict__ loc) {
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; c < n; c += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t id = ids[c];
+        int64_t lo = 0, hi = nq;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (q[mid] < id) lo = mid + 1; else hi = mid;
+        }
+        for (; lo < nq && q[lo] == id; ++lo) loc[qidx[lo]] = (part << 40) | c;
+    }
+}
+
+// literals of the selected slots in their original order (k_deinterleave for a slot list)
+__global__ void k_deinterleave_sel(const int32_t* __restrict__ src, const uint64_t* __restrict__ order,
+                                   const int64_t* __restrict__ slots, int64_t n, int32_t size,
+                                   int32_t* __restrict__ dst) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = slots[i];
+        const int32_t* s = src + (c / STRIDE) * size * STRIDE + (c % STRIDE);
+        const uint64_t w = order[c];
+        const int32_t pivot = (int32_t)(w >> ORDER_MASK_BITS) - 1;
+        const uint64_t m = w & ((1ull << ORDER_MASK_BITS) - 1);
+        int32_t t2 = pivot >= 0, rest = t2 + __popcll(m);
+        for (int32_t j = 0; j < size; ++j) {
+            int32_t k;
+            if (j == pivot) k = 0;
+            else if (j < ORDER_MASK_BITS && ((m >> j) & 1)) k = t2++;
+            else k = rest++;
+            dst[i * size + j] = s[(int64_t)k * STRIDE];
+        }
+    }
+}
+
 // 8-byte egress records: engine_id << 37 | group << 32 | lane_mask (engine
 // ids < 2^27, groups < 32, lane width <= 32; checked by the host).
 __global__ void k_pack_records8(const tsg_report* __restrict__ in, int64_t n, uint64_t* __restrict__ out) {

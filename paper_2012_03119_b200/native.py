@@ -121,6 +121,33 @@ class NativeEngine:
                                         C.byref(removed)))
         return removed.value
 
+    def get_clauses(self, ids) -> list:
+        """Literal tuples of the stored clauses `ids` (None where not stored), in
+        their original order (tsg_get_clauses; engine.py:165-169)."""
+        q = np.ascontiguousarray(ids, np.int64)
+        n = len(q)
+        if n == 0:
+            return []
+        sizes = np.zeros(n, np.int32)
+        tot = C.c_int64(0)
+        check(self.L.tsg_get_clauses(self.h, ptr(q), n, ptr(sizes), None, 0, C.byref(tot)))
+        lits = np.zeros(max(tot.value, 1), np.int32)
+        check(self.L.tsg_get_clauses(self.h, ptr(q), n, ptr(sizes), ptr(lits), len(lits), C.byref(tot)))
+        out, o = [], 0
+        for s in sizes.tolist():
+            if s < 0:
+                out.append(None)
+            else:
+                out.append(tuple(lits[o:o + s].tolist()))
+                o += s
+        return out
+
+    def counters(self) -> dict:
+        """Cumulative figures (tsg_counters)."""
+        c = _lib.tsg_counters_t()
+        check(self.L.tsg_counters(self.h, C.byref(c)))
+        return {n: getattr(c, n) for n, _ in c._fields_}
+
     def scale(self, factor: float) -> None:
         check(self.L.tsg_scale_activities(self.h, factor))
 

@@ -595,3 +595,36 @@ def test_twelve_byte_egress_records(P):
         with pytest.raises(CapacityError):
             e.fetch_raw(r.reports)
         e.close()
+
+
+def test_get_clauses_and_counters(P):
+    # tsg_get_clauses returns stored clauses by engine id in their original
+    # literal order (engine.py:165-169) despite the pivot / polarity layout,
+    # None once removed; tsg_counters accumulates the round figures
+    from paper_2012_03119_b200 import workload as W
+    from paper_2012_03119_b200.native import NativeEngine
+    rng = np.random.default_rng(5)
+    nv = 3000
+    flat, offs, ids = W.flatten(W.clause_buckets(50_000, nv, rng, 0, 30))
+    e = NativeEngine(nv)
+    e.add_clauses(flat, offs, ids)
+    want = {int(ids[i]): tuple(flat[offs[i]:offs[i + 1]].tolist()) for i in range(len(ids))}
+    pick = rng.choice(ids, 2000, replace=False)
+    q = np.concatenate([pick, [ids.max() + 1, -5], pick[:3]])  # missing ids and repeats
+    got = e.get_clauses(q)
+    assert got[:2000] == [want[int(i)] for i in pick]
+    assert got[2000:2002] == [None, None] and got[2002:] == [want[int(i)] for i in pick[:3]]
+    figs = []
+    for k in range(3):
+        e.stage(W.snapshots(2, 32, nv, rng))
+        r = e.round(*W.groups_for(2, 32), 1.0)
+        figs.append(r)
+    gone = e.remove(pick[:100])
+    assert gone == 100 and e.get_clauses(pick[:100]) == [None] * 100
+    assert e.get_clauses(pick[100:200]) == [want[int(i)] for i in pick[100:200]]
+    c = e.counters()
+    assert c["rounds"] == 3 and c["clauses_added"] == len(ids) and c["clauses_deleted"] == 100
+    for f in ("reports", "clauses_tested", "aggregate_tests", "aggregate_tests_negative", "lane_tests",
+              "lane_triggers"):
+        assert c[f] == sum(getattr(r, f) for r in figs), f
+    e.close()
