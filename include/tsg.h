@@ -62,7 +62,7 @@ typedef struct tsg_round_result {
     int64_t lane_triggers;            /* engine.py:461                            */
     int32_t n_chunks;                 /* ceil(n_groups / group_width)             */
     int32_t reruns;                   /* report-buffer overflow replays           */
-    double encode_ms;                 /* device time, TSG_F_TIMING only           */
+    double encode_ms;                 /* device time, TSG_F_TIMING (-1: not sampled, tsg_set_timing) */
     double test_ms;                   /* device time of the trigger kernels       */
 } tsg_round_result;
 
@@ -141,6 +141,11 @@ int tsg_bucket_read(tsg_engine* h, int32_t b, int32_t* lits, int64_t* ids,
 int tsg_get_clauses(tsg_engine* h, const int64_t* ids, int64_t n, int32_t* sizes, int32_t* lits,
                     int64_t lits_cap, int64_t* n_lits);
 int tsg_counters(tsg_engine* h, tsg_counters_t* out);
+/* With TSG_F_TIMING: bracket only rounds whose launch sequence number is a
+ * multiple of `every` with timing events (0 = none; default 1 = all) --
+ * each event stalls the stream front end for a few microseconds.  Unsampled
+ * rounds report encode_ms = test_ms = -1. */
+int tsg_set_timing(tsg_engine* h, int32_t every);
 int tsg_scale_activities(tsg_engine* h, double factor);
 /* reduce_store selection + compaction (engine.py:476-500): remove the
  * `target` smallest (activity, engine_id) among clauses with id <

@@ -152,6 +152,7 @@ struct tsg_engine {
         unsigned long long* ctr = nullptr;
         unsigned long long* h_ctr = nullptr;  // pinned [8], written by the kernel
         bool pol_pending = false;             // an encode counted into ctr[6..7] since the last launch
+        bool timed = false;                   // its encode / test are bracketed by timing events
         unsigned long long* tiles = nullptr;  // device DynTiles counters, zero between launches
         cudaEvent_t ev_done = nullptr;        // its counters are on the host
         cudaEvent_t ev_tst[2] = {nullptr, nullptr};
@@ -197,6 +198,7 @@ struct tsg_engine {
     int64_t round_seq = 0;
     int enc_attr = 0;             // k_encode_packed32 shared-memory attribute set, per GW
     tsg_counters_t totals{};      // cumulative figures (tsg_counters)
+    int32_t timing_every = 1;     // TSG_F_TIMING: events on rounds whose sequence is a multiple (tsg_set_timing)
     int64_t grid[32] = {0};       // persistent grid per k_test variant
     int64_t grid_smem[32];        // shared-memory size the grid was computed for (-1: none)
     bool smem_table = true;       // shared-memory code table when it fits (TSG_SMEM_TABLE=0 disables)
@@ -246,6 +248,12 @@ struct DevGuard {
 };
 
 bool any_inflight(const tsg_engine* h) { return h->rs[0].inflight || h->rs[1].inflight; }
+
+// Timing events stall the stream front end (≈2.5 µs each between dependent
+// kernels), so they can be limited to every n-th round (tsg_set_timing).
+bool timed_round(const tsg_engine* h, int64_t seq) {
+    return (h->cfg.flags & TSG_F_TIMING) && h->timing_every > 0 && seq % h->timing_every == 0;
+}
 
 int dalloc(tsg_engine* h, void** p, int64_t bytes) {
     *p = nullptr;
@@ -1079,6 +1087,13 @@ int tsg_get_clauses(tsg_engine* h, const int64_t* ids, int64_t n, int32_t* sizes
     return TSG_OK;
 }
 
+int tsg_set_timing(tsg_engine* h, int32_t every) {
+    CKR(validate_handle(h));
+    if (every < 0) return fail(TSG_EINVAL, "timing stride must be >= 0, got %d", every);
+    h->timing_every = every;
+    return TSG_OK;
+}
+
 int tsg_counters(tsg_engine* h, tsg_counters_t* out) {
     CKR(validate_handle(h));
     if (!out) return fail(TSG_EINVAL, "null argument");
@@ -1463,7 +1478,8 @@ int round_launch(tsg_engine* h, double inc, bool flip) {
         if (h->n_tiles >= (int64_t)INT32_MAX / 2)  // the kernels index tiles with 32-bit integers
             return fail(TSG_ECAPACITY, "store of %lld tiles exceeds the 32-bit tile index", (long long)h->n_tiles);
         if (R.fl.n_chunks > 1) CKR(dgrow(h, &R.carry, &R.carry_cap, std::max<int64_t>(1, h->n_tiles * STRIDE)));
-        const bool timing = h->cfg.flags & TSG_F_TIMING;
+        const bool timing = timed_round(h, R.seq);
+        R.timed = timing;
         if (timing) CK(cudaEventRecord(R.ev_tst[0], h->st));
         CKR(run_tests(h, k, inc, 0));
         if (timing) CK(cudaEventRecord(R.ev_tst[1], h->st));
@@ -1544,7 +1560,8 @@ int round_collect(tsg_engine* h, tsg_round_result* out) {
         res.lane_tests = n * lanes_total;
         res.aggregate_tests_negative = res.aggregate_tests - positives;
         res.reports = n_rec;
-        if (h->cfg.flags & TSG_F_TIMING) {
+        res.encode_ms = res.test_ms = -1.0;  // not sampled
+        if (R.timed) {
             float ms = 0;
             if (cudaEventElapsedTime(&ms, h->ev_enc[R.slot][0], h->ev_enc[R.slot][1]) == cudaSuccess) res.encode_ms = ms;
             else cudaGetLastError();
@@ -1575,7 +1592,7 @@ int tsg_round_encode(tsg_engine* h) {
         if (Q.inflight && Q.slot == h->tslot)
             return fail(TSG_EINVAL, "table slot %d still belongs to an uncollected round", h->tslot);
     if (h->packed && h->pstaged) CK(cudaStreamWaitEvent(h->st, h->ev_staged[h->pk], 0));  // rows copied in
-    const bool timing = h->cfg.flags & TSG_F_TIMING;
+    const bool timing = timed_round(h, h->round_seq + 1);  // the round this encode feeds
     if (timing) CK(cudaEventRecord(h->ev_enc[h->tslot][0], h->st));
     auto& Rn = h->rs[h->next_rs];
     if (Rn.pol_pending)  // re-encoded without a launch: count this encode only

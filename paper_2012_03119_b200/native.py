@@ -142,6 +142,10 @@ class NativeEngine:
                 o += s
         return out
 
+    def set_timing(self, every: int) -> None:
+        """With timing=True: events on every `every`-th round only (tsg_set_timing)."""
+        check(self.L.tsg_set_timing(self.h, every))
+
     def counters(self) -> dict:
         """Cumulative figures (tsg_counters)."""
         c = _lib.tsg_counters_t()
