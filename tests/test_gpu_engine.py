@@ -628,3 +628,31 @@ def test_get_clauses_and_counters(P):
               "lane_triggers"):
         assert c[f] == sum(getattr(r, f) for r in figs), f
     e.close()
+
+
+def test_timing_sampling(P):
+    # tsg_set_timing(n): only rounds whose launch sequence is a multiple of n
+    # carry event timings; the others report -1 (figures unaffected)
+    from paper_2012_03119_b200 import workload as W
+    from paper_2012_03119_b200.native import NativeEngine
+    rng = np.random.default_rng(9)
+    nv = 2000
+    flat, offs, ids = W.flatten(W.clause_buckets(20_000, nv, rng, 1, 9))
+    e = NativeEngine(nv, timing=True)
+    e.add_clauses(flat, offs, ids)
+    e.set_timing(2)
+    snaps = W.snapshots(2, 32, nv, rng)
+    gl, gt = W.groups_for(2, 32)
+    got = []
+    for _ in range(4):
+        e.stage(snaps)
+        got.append(e.round(gl, gt, 1.0))
+    assert [r.test_ms >= 0 for r in got] == [False, True, False, True]
+    assert all((r.encode_ms >= 0) == (r.test_ms >= 0) for r in got)
+    assert len({r.reports for r in got}) == 1
+    e.set_timing(0)
+    e.stage(snaps)
+    assert e.round(gl, gt, 1.0).test_ms == -1
+    with pytest.raises(ValueError):
+        e.set_timing(-1)
+    e.close()
