@@ -290,6 +290,9 @@ __global__ void __launch_bounds__(256) k_encode_packed(const uint64_t* __restric
 // the row it copied, so no warp barrier is needed; the two 16-byte halves
 // are swapped on every other 4-lane quad (conflict-free 128-bit reads).
 constexpr int ENC_MAX_GPW = 8;
+#ifndef TSG_ENC_WAIT_ALL
+#define TSG_ENC_WAIT_ALL 0
+#endif
 #ifndef TSG_ENC_PAIR
 #define TSG_ENC_PAIR 0
 #endif  // groups per warp (G <= 64, 8 warps)
@@ -394,11 +397,12 @@ __global__ void __launch_bounds__(256) k_encode_packed32(const uint64_t* __restr
         cp_async_commit();
     }
     const Transpose32 xp(lane);
+    if (TSG_ENC_WAIT_ALL) cp_async_wait_upto(0);  // all groups landed: the compiler may interleave them
     uint32_t nT[4] = {0, 0, 0, 0}, nF[4] = {0, 0, 0, 0}, nU[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int j = 0; j < GPW; ++j) {
         const int g = y + 8 * j;
-        cp_async_wait_upto(GPW - 1 - j);
+        if (!TSG_ENC_WAIT_ALL) cp_async_wait_upto(GPW - 1 - j);
         // no branch around the shuffles (they must stay provably converged):
         // groups past G transpose zero-filled rows and store nothing
         const bool live = g < c.G;
