@@ -197,6 +197,17 @@ int tsg_round_prepare(tsg_engine* h, const int32_t* group_lanes,
                       const int32_t* group_tid, int32_t n_groups);
 int tsg_round_encode(tsg_engine* h);
 int tsg_round_tables(tsg_engine* h, void** device_ptr, int64_t* bytes);
+/* Split snapshot ingress across GPUs: each rank stages the
+ * packed rows of groups [g_begin, g_end) only and encodes them; lane entries
+ * of the other groups are left for an all-gather, aggregate words carry only
+ * these groups' bits (disjoint across ranks, so a sum all-reduce ORs them);
+ * exactly one rank passes sentinel = 1.  One chunk, lane_width <= 32.
+ * tsg_round_layout gives the byte offsets inside tsg_round_tables' region:
+ * aggregate table [agg_off, agg_off + agg_len), group g's lane entries at
+ * lane_off + g * group_bytes. */
+int tsg_round_encode_groups(tsg_engine* h, int32_t g_begin, int32_t g_end, int32_t sentinel);
+int tsg_round_layout(tsg_engine* h, int64_t* agg_off, int64_t* agg_len, int64_t* lane_off,
+                     int64_t* group_bytes);
 int tsg_round_test(tsg_engine* h, double activity_inc, tsg_round_result* out);
 /* Asynchronous test (device rounds back to back): tsg_round_launch queues
  * the test of the prepared, encoded round and returns; the next round may

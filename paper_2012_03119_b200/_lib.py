@@ -57,7 +57,8 @@ EXPORTS = (
     "tsg_reports_device", "tsg_sync", "tsg_stream", "tsg_pack", "tsg_aggregate", "tsg_lane_trigger",
     "tsg_aggregate_trigger", "tsg_packed_words", "tsg_pack_rows", "tsg_stage_packed",
     "tsg_fetch_reports_async", "tsg_fetch_wait", "tsg_round_launch", "tsg_round_collect",
-    "tsg_set_record_bytes", "tsg_get_clauses", "tsg_counters", "tsg_set_timing",
+    "tsg_set_record_bytes", "tsg_get_clauses", "tsg_counters", "tsg_set_timing", "tsg_round_encode_groups",
+    "tsg_round_layout",
 )
 
 _lib = None
@@ -82,6 +83,8 @@ def _declare(L):
         "tsg_get_clauses": ([P, P, I64, P, P, I64, pI64], C.c_int),
         "tsg_counters": ([P, P], C.c_int),
         "tsg_set_timing": ([P, I32], C.c_int),
+        "tsg_round_encode_groups": ([P, I32, I32, I32], C.c_int),
+        "tsg_round_layout": ([P, pI64, pI64, pI64, pI64], C.c_int),
         "tsg_reduce": ([P, I64, I64, pI64, P], C.c_int),
         "tsg_remove_clauses": ([P, P, I64, pI64], C.c_int),
         "tsg_stage_snapshots": ([P, P, I64, I64, I32], C.c_int),

@@ -197,6 +197,9 @@ struct tsg_engine {
     bool oob = false;  // a stored literal may exceed num_vars (checked before testing)
     int64_t round_seq = 0;
     int enc_attr = 0;             // k_encode_packed32 shared-memory attribute set, per GW
+    // tsg_round_encode_groups: encode groups [enc_g0, enc_g1) only (enc_g1 < 0: all)
+    int32_t enc_g0 = 0, enc_g1 = -1;
+    bool enc_sentinel = true;
     tsg_counters_t totals{};      // cumulative figures (tsg_counters)
     int32_t timing_every = 1;     // TSG_F_TIMING: events on rounds whose sequence is a multiple (tsg_set_timing)
     int64_t grid[32] = {0};       // persistent grid per k_test variant
@@ -355,9 +358,16 @@ int launch_encode(tsg_engine* h, int c) {
         pc.num_vars = h->V;
         pc.pitch_words = h->ppitch;
         pc.vstride = ec.vstride;
-        for (int g = 0; g < ec.G; ++g) { pc.row0[g] = ec.row0[g]; pc.lanes[g] = ec.lanes[g]; }
+        // a group range (tsg_round_encode_groups): rows hold only its groups
+        const int64_t row_base = h->enc_g1 >= 0 ? rd.grow0[h->enc_g0] : 0;
+        for (int g = 0; g < ec.G; ++g) { pc.row0[g] = ec.row0[g] - row_base; pc.lanes[g] = ec.lanes[g]; }
         pc.polarity = ec.polarity;
+        pc.gbeg = h->enc_g1 >= 0 ? std::max(0, h->enc_g0 - g0) : 0;
+        pc.gend = h->enc_g1 >= 0 ? std::min(ec.G, h->enc_g1 - g0) : ec.G;
+        pc.sentinel = h->enc_sentinel ? 1 : 0;
         static const bool enc_stage = !getenv("TSG_ENC_STAGE") || atoi(getenv("TSG_ENC_STAGE")) != 0;
+        if (h->enc_g1 >= 0 && !(sizeof(LW) == 4 && enc_stage))
+            return fail(TSG_EINVAL, "group-range encode needs the staged encoder (k_encode_packed32)");
         if (sizeof(LW) == 4 && enc_stage) {
             const int need = (ec.G + 7) / 8;  // groups per warp
             const int gpw = need <= 1 ? 1 : need <= 2 ? 2 : need <= 4 ? 4 : 8;
@@ -1601,6 +1611,47 @@ int tsg_round_encode(tsg_engine* h) {
     CKR(do_encode(h));
     if (h->packed && h->pstaged) CK(cudaEventRecord(h->ev_read[h->pk], h->st));
     if (timing) CK(cudaEventRecord(h->ev_enc[h->tslot][1], h->st));
+    return TSG_OK;
+}
+
+// One rank's share of a round's encode when the snapshot ingress is split
+// across GPUs: the staged packed rows hold exactly groups
+// [g_begin, g_end); their lane entries are written, the other groups' are
+// left for the all-gather, and the aggregate words carry only these groups'
+// bits, so a sum all-reduce over the ranks ORs them (the bits are disjoint).
+// `sentinel`: this rank writes the always-False entry (exactly one rank).
+int tsg_round_encode_groups(tsg_engine* h, int32_t g_begin, int32_t g_end, int32_t sentinel) {
+    CKR(validate_handle(h));
+    const RoundDesc& rd = h->rd;
+    if (rd.n_chunks != 1 || wide_lane(h) || !h->packed)
+        return fail(TSG_EINVAL, "group-range encode needs one chunk, lane_width <= 32 and packed rows");
+    if (g_begin < 0 || g_end > rd.n_groups || g_begin >= g_end)
+        return fail(TSG_EINVAL, "group range [%d, %d) outside 0..%d", g_begin, g_end, rd.n_groups);
+    const int64_t need = rd.grow0[g_end - 1] + rd.glanes[g_end - 1] - rd.grow0[g_begin];
+    if (need > h->n_rows) return fail(TSG_EINVAL, "groups need %lld rows, %lld staged", (long long)need, (long long)h->n_rows);
+    h->enc_g0 = g_begin;
+    h->enc_g1 = g_end;
+    h->enc_sentinel = sentinel != 0;
+    const int64_t keep_rows = h->n_rows;
+    h->n_rows = std::max<int64_t>(h->n_rows, rd.n_groups ? rd.grow0.back() + rd.glanes.back() : 0);  // row check of the full round
+    const int rc = tsg_round_encode(h);
+    h->n_rows = keep_rows;
+    h->enc_g0 = 0;
+    h->enc_g1 = -1;
+    h->enc_sentinel = true;
+    return rc;
+}
+
+// Byte layout of the prepared round's tables (one chunk): the aggregate
+// table at agg_off (agg_bytes), then group g's lane entries at lane_off +
+// g * group_bytes -- the regions tsg_round_encode_groups ranks combine.
+int tsg_round_layout(tsg_engine* h, int64_t* agg_off, int64_t* agg_len, int64_t* lane_off, int64_t* group_bytes) {
+    CKR(validate_handle(h));
+    if (h->rd.n_chunks < 1) return fail(TSG_EINVAL, "no prepared round");
+    *agg_off = h->rd.chunk_off[0];
+    *agg_len = (int64_t)(h->V + 2) * agg_entry_bytes(h);
+    *lane_off = h->rd.chunk_off[0] + agg_bytes(h);
+    *group_bytes = vstride(h) * lane_entry_bytes(h);
     return TSG_OK;
 }
 

@@ -196,6 +196,11 @@ struct EncodePackedChunk {
     int64_t row0[MAXG];
     int32_t lanes[MAXG];
     unsigned long long* polarity;  // [2] += (var, group) pairs that can be True / can be False
+    // k_encode_packed32 only: encode groups [gbeg, gend) of the chunk (the
+    // others' lane entries are left alone and their aggregate bits are 0,
+    // so the ranks' tables combine by all-gather + sum); `sentinel` writes
+    // the always-False entry of variable num_vars + 1 (exactly one rank)
+    int32_t gbeg, gend, sentinel;
 };
 
 template <class LW, class GW>
@@ -390,7 +395,7 @@ __global__ void __launch_bounds__(256) k_encode_packed32(const uint64_t* __restr
 #pragma unroll
     for (int j = 0; j < GPW; ++j) {
         const int g = y + 8 * j;
-        const bool ok = g < c.G && lane < c.lanes[g];
+        const bool ok = g >= c.gbeg && g < c.gend && lane < c.lanes[g];
         const uint64_t* src = ok ? rows + (c.row0[g] + lane) * c.pitch_words + w0 : rows;
         cp_async16(mine + j * 64 + sw, src, ok ? 16 : 0);  // zero-filled past the group
         cp_async16(mine + j * 64 + (sw ^ 1), src + 2, ok ? 16 : 0);
@@ -405,7 +410,7 @@ __global__ void __launch_bounds__(256) k_encode_packed32(const uint64_t* __restr
         if (!TSG_ENC_WAIT_ALL) cp_async_wait_upto(GPW - 1 - j);
         // no branch around the shuffles (they must stay provably converged):
         // groups past G transpose zero-filled rows and store nothing
-        const bool live = g < c.G;
+        const bool live = g >= c.gbeg && g < c.gend;
         const int n = live ? c.lanes[g] : 0;
         const uint4 a = mine[j * 64 + sw], b = mine[j * 64 + (sw ^ 1)];
         const uint32_t tv[4] = {a.x, a.z, b.x, b.z}, sv[4] = {a.y, a.w, b.y, b.w};
@@ -454,7 +459,8 @@ __global__ void __launch_bounds__(256) k_encode_packed32(const uint64_t* __restr
             }
         if (v >= 1 && v <= V) agg[v] = AggEntry<GW>{aT, aF, aU, GW(0)};
         else if (v == 0) agg[v] = AggEntry<GW>{GW(0), GW(0), GW(0), GW(0)};
-        else if (v == V + 1) agg[v] = AggEntry<GW>{~GW(0), ~GW(0), GW(0), GW(0)};
+        else if (v == V + 1)
+            agg[v] = c.sentinel ? AggEntry<GW>{~GW(0), ~GW(0), GW(0), GW(0)} : AggEntry<GW>{GW(0), GW(0), GW(0), GW(0)};
         // polarity statistics for the store's literal placement
         unsigned nt = (v >= 1 && v <= V) ? __popcll((unsigned long long)aT) : 0u;
         unsigned nf = (v >= 1 && v <= V) ? __popcll((unsigned long long)aF) : 0u;

@@ -179,6 +179,17 @@ class NativeEngine:
     def encode(self) -> None:
         check(self.L.tsg_round_encode(self.h))
 
+    def encode_groups(self, g_begin: int, g_end: int, sentinel: bool) -> None:
+        """Encode groups [g_begin, g_end) from rows holding only those groups
+        (tsg_round_encode_groups; split ingress across GPUs)."""
+        check(self.L.tsg_round_encode_groups(self.h, g_begin, g_end, 1 if sentinel else 0))
+
+    def layout(self) -> Tuple[int, int, int, int]:
+        """(agg_off, agg_len, lane_off, group_bytes) inside tables() (tsg_round_layout)."""
+        v = [C.c_int64(0) for _ in range(4)]
+        check(self.L.tsg_round_layout(self.h, *[C.byref(x) for x in v]))
+        return tuple(x.value for x in v)
+
     def tables(self) -> Tuple[int, int]:
         p, n = C.c_void_p(), C.c_int64(0)
         check(self.L.tsg_round_tables(self.h, C.byref(p), C.byref(n)))

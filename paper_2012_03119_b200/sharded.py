@@ -6,6 +6,9 @@ round (engine.py:369-467) becomes
 
     rank 0: group + stage + encode the round's snapshots (K1/K2)
     all   : broadcast the packed tables over NVLink (NCCL)      <- the only data-path collective
+or, with the snapshot ingress split (`run_split`):
+    rank r: stage + encode the rows of its 1/N of the groups only (its own PCIe link)
+    all   : all-gather the lane entries + sum-all-reduce the aggregate words
     all   : test the local shard (K3/K4/K5)
     all   : gather the report records to rank 0, merge in the reference order
 
@@ -154,6 +157,46 @@ def broadcast_tables(dist, engine, src: int = 0, stream=None) -> None:
         dist.broadcast(t, src)
 
 
+def split_groups(n_groups: int, world: int, rank: int) -> Optional[Tuple[int, int]]:
+    """This rank's contiguous group range when the snapshot ingress is split
+    (equal shares, so the lane tables all-gather in place); None if the
+    groups do not divide evenly."""
+    if world <= 1 or n_groups % world:
+        return None
+    per = n_groups // world
+    return rank * per, (rank + 1) * per
+
+
+def combine_tables(dist, engine, n_groups: int, stream=None) -> None:
+    """After every rank encoded its group range (tsg_round_encode_groups):
+    all-gather the lane entries (group-major, equal contiguous shares) and
+    sum-all-reduce the aggregate words (each rank set only its groups' bits,
+    so the sum is their OR) -- SURVEY.md §8(e)'s split ingress, in place on
+    the round's table slot."""
+    import torch
+    ptr, nbytes = engine.tables()
+    agg_off, agg_len, lane_off, gbytes = engine.layout()
+    world, rank = dist.get_world_size(), dist.get_rank()
+
+    class _CAI:
+        __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                    "version": 3, "stream": None}
+
+    t = torch.as_tensor(_CAI(), device=torch.device("cuda", torch.cuda.current_device()))
+    per = n_groups // world * gbytes
+    lane = t[lane_off:lane_off + world * per]
+    agg = t[agg_off:agg_off + agg_len].view(torch.int32)
+    ctx = torch.cuda.stream(stream) if stream is not None else torch.cuda.stream(torch.cuda.current_stream())
+    with ctx:
+        mine = lane[rank * per:(rank + 1) * per]
+        if dist.get_backend() == "nccl":
+            dist.all_gather_into_tensor(lane, mine.clone())
+        else:
+            parts = [lane[r * per:(r + 1) * per] for r in range(world)]
+            dist.all_gather(parts, mine.clone())
+        dist.all_reduce(agg, op=dist.ReduceOp.SUM)
+
+
 # ---------------------------------------------------------------------------
 # the sharded round over NativeEngine shards
 
@@ -166,6 +209,22 @@ class ShardedRound:
         self.dist, self.eng, self.gw = dist, engine, group_width
         self.rank = dist.get_rank()
         self.stream = torch.cuda.ExternalStream(engine.stream())
+
+    def run_split(self, group_lanes, group_tid, activity_inc: float, packed_rows: np.ndarray):
+        """Split ingress: every rank passes the packed rows of its own group
+        range only (split_groups), encodes them, and the tables are combined
+        over the collective before every rank tests its shard."""
+        n_groups = len(group_lanes)
+        gb, ge = split_groups(n_groups, self.dist.get_world_size(), self.rank)
+        self.eng.prepare(group_lanes, group_tid)
+        self.eng.stage_packed(packed_rows)
+        self.eng.encode_groups(gb, ge, self.rank == 0)
+        self.eng.sync()
+        combine_tables(self.dist, self.eng, n_groups, self.stream)
+        self.stream.synchronize()
+        res = self.eng.test(activity_inc)
+        recs = self.eng.fetch_raw(res.reports)
+        return res, gather_records(self.dist, recs, 0)
 
     def run(self, group_lanes, group_tid, activity_inc: float, rows: Optional[np.ndarray] = None):
         """Rank 0 passes the round's grouped rows; every rank passes the same

@@ -94,3 +94,77 @@ def test_sharded_round_on_gpu_matches_unsharded_oracle():
     assert len(want) > 1000 and len(merged) == len(want)
     for fld in ("engine_id", "lane_mask", "group"):
         assert np.array_equal(merged[fld], want[fld]), fld
+
+
+def _split_worker(rank, world, port, out_q):
+    # split ingress: every rank stages + encodes only its
+    # groups' rows; tables combined by all-gather + sum all-reduce
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    from paper_2012_03119_b200 import sharded as S
+    from paper_2012_03119_b200 import workload as W
+    from paper_2012_03119_b200.native import NativeEngine, pack_rows
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(SEED + 1)
+        buckets = W.clause_buckets(N, NV, rng, 1, 12)
+        flat, offs, ids = W.flatten(buckets)
+        snaps = W.snapshots(4, 32, NV, rng)
+        gl, gt = W.groups_for(4, 32)
+        sizes = np.diff(offs)
+        owner = S.assign_shards(sizes, world)
+        mine = np.nonzero(owner == rank)[0]
+        f = np.concatenate([flat[offs[i]:offs[i + 1]] for i in mine])
+        o = np.concatenate([[0], np.cumsum(sizes[mine])]).astype(np.int64)
+        eng = NativeEngine(NV, 32, 32, device=0)
+        eng.add_clauses(f, o, ids[mine])
+        gb, ge = S.split_groups(len(gl), world, rank)
+        rows = pack_rows(snaps[gb * 32:ge * 32], NV)
+        res, parts = S.ShardedRound(dist, eng, 32).run_split(gl, gt, 1.0, rows)
+        if rank == 0:
+            size_of = {int(ids[i]): int(sizes[i]) for i in range(len(ids))}
+            brank = {s: k for k, s in enumerate(buckets.keys())}
+            merged = S.merge_reports(parts, 32, brank, size_of)
+            out_q.put(("ok", merged.tobytes()))
+        eng.close()
+    except Exception:
+        import traceback
+        out_q.put(("err", traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_split_ingress_round_on_gpu_matches_unsharded_oracle():
+    from gpu_util import require_device
+    require_device()
+    from oracle import oracle as O
+    from paper_2012_03119_b200 import workload as W
+    from paper_2012_03119_b200.reports import DECODED_DTYPE
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_split_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    status, payload = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+    assert status == "ok", payload
+    merged = np.frombuffer(payload, dtype=DECODED_DTYPE)
+
+    rng = np.random.default_rng(SEED + 1)
+    buckets = W.clause_buckets(N, NV, rng, 1, 12)
+    flat, offs, ids = W.flatten(buckets)
+    snaps = W.snapshots(4, 32, NV, rng)
+    gl, gt = W.groups_for(4, 32)
+    st = O.OracleStore()
+    st.insert_flat(flat, offs, ids)
+    want, _ = st.test_round(NV, snaps, gl, gt, 32, 32, 1.0)
+    assert len(want) > 1000 and len(merged) == len(want)
+    for fld in ("engine_id", "lane_mask", "group"):
+        assert np.array_equal(merged[fld], want[fld]), fld
