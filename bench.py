@@ -23,7 +23,9 @@ Multi-GPU (torchrun): every rank holds its own C3-sized clause shard
 over that GPU's own PCIe link); every rank encodes the round's tables and
 tests its shard -- no data-path collective -- and the time is the max over
 ranks.  `--tables bcast`: rank 0 encodes and NCCL broadcasts the tables over
-NVLink instead.
+NVLink instead.  `--e2e-ingress split`: in the e2e leg each rank copies in
+only the rows of its 1/N of the groups and the encoded tables are combined
+by an all-gather + sum all-reduce (sharded.combine_tables).
 """
 from __future__ import annotations
 
@@ -241,6 +243,10 @@ def main():
     ap.add_argument("--tables", default="replicated", choices=["replicated", "bcast"],
                     help="N>1: every rank encodes the round's tables from its own copy of the rows "
                          "(default; no data-path collective), or rank 0 encodes and NCCL broadcasts them")
+    ap.add_argument("--e2e-ingress", default="replicated", choices=["split", "replicated"],
+                    help="N>1 e2e: every rank copies in all rows (default, no collective), or each rank "
+                         "copies in only its share of the round's groups and the encoded tables are combined "
+                         "over the process group (split; SURVEY.md §8(e))")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = W.CONFIGS[args.config]
@@ -412,6 +418,17 @@ def main():
             _lib.check(L.tsg_fetch_reports(eng.h, C.c_void_p(rec_buf.data_ptr()), n, C.byref(got)))
             return r
 
+        # N>1: split ingress -- rank r copies in only the rows
+        # of its 1/N of the groups over its own PCIe link, encodes them, and
+        # the tables are combined over NCCL before every rank tests its shard
+        from paper_2012_03119_b200 import sharded as S
+        split = (S.split_groups(G, world, rank) if (dist is not None and args.e2e_ingress == "split")
+                 else None)
+        split_row0, split_rows = 0, A
+        if split is not None:
+            split_row0 = int(sum(gl[:split[0]]))
+            split_rows = int(sum(gl[split[0]:split[1]]))
+
         def step_packed():
             _lib.check(L.tsg_stage_packed(eng.h, C.c_void_p(h_packed_t.data_ptr()), A, pw, 0))
             return finish(eng.round(gl, gt, 1.0))
@@ -436,12 +453,17 @@ def main():
             for i in range(warm + k):
                 if i == warm:
                     w0 = time.perf_counter()
-                _lib.check(L.tsg_stage_packed(eng.h, C.c_void_p(h_packed_t.data_ptr()), A, pw, 0))
+                _lib.check(L.tsg_stage_packed(eng.h, C.c_void_p(h_packed_t.data_ptr() + split_row0 * pw * 8),
+                                              split_rows, pw, 0))
                 if pending:
                     r = eng.collect()
                     fetch_async(r)
                     pending -= 1
-                eng.encode()
+                if split is not None:  # this rank's groups, then all-gather / all-reduce the tables
+                    eng.encode_groups(split[0], split[1], rank == 0)
+                    S.combine_tables(dist, eng, G, stream)
+                else:
+                    eng.encode()
                 eng.launch(1.0)
                 pending += 1
             while pending:
@@ -504,8 +526,12 @@ def main():
             mode = "pipelined" if ms <= ms_seq else "sequential"
             best = min(ms, ms_seq)
             e2e = {"value": r.lane_tests * world / (best * 1e-3), "unit": "clause_assignment_tests/s",
-                   "h2d_bytes_per_step": int(A * pw * 8) * world, "d2h_bytes_per_step": int(d2h) * world,
+                   "h2d_bytes_per_step": int((split_rows if mode == "pipelined" else A) * pw * 8) * world,
+                   "d2h_bytes_per_step": int(d2h) * world,
                    "ms_per_step": best,
+                   "ingress": ("split: each rank copies in its 1/N of the groups' rows; tables combined by NCCL "
+                               "all-gather + all-reduce" if (split is not None and mode == "pipelined")
+                               else "every rank copies in all rows"),
                    "input": "packed 2-bit snapshot rows in pinned host memory (solver-side ingress format)",
                    "mode": mode,
                    "pipelined_ms_per_step": ms,
