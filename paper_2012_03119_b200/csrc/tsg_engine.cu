@@ -153,6 +153,7 @@ struct tsg_engine {
         unsigned long long* h_ctr = nullptr;  // pinned [8], written by the kernel
         bool pol_pending = false;             // an encode counted into ctr[6..7] since the last launch
         bool timed = false;                   // its encode / test are bracketed by timing events
+        bool rec8 = false;                    // its records are 8-byte u64 (tsg_set_record_bytes(8) and they fit)
         unsigned long long* tiles = nullptr;  // device DynTiles counters, zero between launches
         cudaEvent_t ev_done = nullptr;        // its counters are on the host
         cudaEvent_t ev_tst[2] = {nullptr, nullptr};
@@ -475,6 +476,7 @@ int launch_test(tsg_engine* h, int k, int c, double inc, int emit_only) {
     p.emit_only = emit_only;
     p.pub = (!emit_only && c == rd.n_chunks - 1) ? R.h_ctr : nullptr;
     p.dyn_tiles = h->dyn_tiles ? 1 : 0;
+    p.rec8 = R.rec8 ? 1 : 0;
     p.tiles = R.tiles;
     p.slab_tile0 = h->d_slab_tile0;
     p.slab_desc0 = reinterpret_cast<const int32_t*>(h->d_slab_tile0 + (h->n_slabs + 1));
@@ -710,6 +712,9 @@ int32_t place_clause(tsg_engine* h, const int32_t* lits, int32_t size, std::vect
 struct ValidReport {
     __host__ __device__ bool operator()(const tsg_report& r) const { return r.key != REPORT_PAD; }
 };
+struct ValidRecord8 {
+    __host__ __device__ bool operator()(const uint64_t& r) const { return r != REPORT_PAD; }
+};
 
 // squeeze the padding slots out of the round's records (order-preserving)
 int compact_reports(tsg_engine* h) {
@@ -720,10 +725,15 @@ int compact_reports(tsg_engine* h) {
     int64_t* nsel = nullptr;
     CKR(dalloc(h, (void**)&nsel, 8));
     size_t tb = 0;
-    cub::DeviceSelect::If(nullptr, tb, h->out, h->out2, nsel, h->n_alloc, ValidReport(), h->st);
+    const bool rec8 = h->rs[h->report_rs].rec8;
+    auto* o8 = reinterpret_cast<uint64_t*>(h->out);
+    auto* t8 = reinterpret_cast<uint64_t*>(h->out2);
+    if (rec8) cub::DeviceSelect::If(nullptr, tb, o8, t8, nsel, h->n_alloc, ValidRecord8(), h->st);
+    else cub::DeviceSelect::If(nullptr, tb, h->out, h->out2, nsel, h->n_alloc, ValidReport(), h->st);
     void* tmp = nullptr;
     CKR(dalloc(h, &tmp, (int64_t)tb + 16));
-    CK(cub::DeviceSelect::If(tmp, tb, h->out, h->out2, nsel, h->n_alloc, ValidReport(), h->st));
+    if (rec8) CK(cub::DeviceSelect::If(tmp, tb, o8, t8, nsel, h->n_alloc, ValidRecord8(), h->st));
+    else CK(cub::DeviceSelect::If(tmp, tb, h->out, h->out2, nsel, h->n_alloc, ValidReport(), h->st));
     dfree(h, tmp);
     dfree(h, nsel);
     std::swap(h->out, h->out2);
@@ -1470,6 +1480,9 @@ int round_launch(tsg_engine* h, double inc, bool flip) {
     R.inc = inc;
     R.seq = ++h->round_seq;
     R.run = 0;
+    // 8-byte egress: the kernel writes the packed u64 records itself when
+    // they fit (ids < 2^27, <= 32 groups, 32-bit lane masks)
+    R.rec8 = h->record_bytes == 8 && !wide_lane(h) && h->max_id < (int64_t(1) << 27) && h->rd.n_groups <= 32;
     if (R.fl.n_chunks && h->oob) {  // out-of-range literal stored: numpy would raise IndexError
         CK(cudaMemsetAsync(h->mctr + 4, 0, 8, h->st));
         for_parts(h, [&](Bucket& b, Part& p) {
@@ -1690,6 +1703,13 @@ int tsg_round(tsg_engine* h, const int32_t* group_lanes, const int32_t* group_ti
 
 // the source and size of the round's first k records in the egress format
 int egress_view(tsg_engine* h, int64_t k, const void** src, int64_t* bytes) {
+    if (h->rs[h->fetch_rs].rec8) {  // written as 8-byte records by the kernel
+        if (h->record_bytes != 8)
+            return fail(TSG_EINVAL, "the round was launched with 8-byte records; fetch it before changing the format");
+        *src = h->out;
+        *bytes = k * 8;
+        return TSG_OK;
+    }
     if (h->record_bytes == 16 || k <= 0) {
         *src = h->out;
         *bytes = k * (int64_t)sizeof(tsg_report);
@@ -1770,6 +1790,8 @@ int tsg_reports_device(tsg_engine* h, void** device_ptr, int64_t* n) {
     CKR(validate_handle(h));
     DevGuard g(h->dev);
     use_reports(h, h->fetch_rs);
+    if (h->rs[h->fetch_rs].rec8)
+        return fail(TSG_EINVAL, "the round's records are 8-byte u64 (tsg_set_record_bytes(8)), not tsg_report");
     CKR(compact_reports(h));
     *device_ptr = h->out;
     *n = h->n_out;

@@ -533,6 +533,7 @@ struct TestParams {
     int32_t emit_only;         // replay after report-buffer overflow: no activity / counter side effects
     unsigned long long* pub;   // last launch of a round: host-mapped [8] the last CTA publishes ctr to
     int32_t dyn_tiles;         // tiles from the counters `tiles` (DynTiles) instead of a static stride
+    int32_t rec8;              // records as 8-byte u64 (st_record)
     unsigned long long* tiles; // [TSG_DYN_NC * DYN_STRIDE] per-launch tile counters (zero between launches)
     const int64_t* slab_tile0; // slab kernel: first tile of each slab (+ end)
     const int32_t* slab_desc0; // slab kernel: first descriptor of each slab (+ end)
@@ -564,6 +565,19 @@ constexpr uint64_t REPORT_PAD = ~0ull;
 
 __device__ __forceinline__ void st_report(tsg_report* p, uint64_t key, uint64_t mask) {
     *reinterpret_cast<ulonglong2*>(p) = make_ulonglong2(key, mask);
+}
+// Record i of the round: 16-byte tsg_report, or -- rounds launched for
+// 8-byte egress (TestParams::rec8) -- one u64 engine_id << 37 | group << 32 |
+// lane_mask written straight from the kernel (half the bytes, no pack pass).
+// `hi` is the engine id already shifted for the format.
+__device__ __forceinline__ void st_record(tsg_report* out, int rec8, int pos, uint64_t hi, uint32_t group,
+                                          uint64_t mask) {
+    if (rec8) reinterpret_cast<uint64_t*>(out)[pos] = hi | ((uint64_t)group << 32) | (uint32_t)mask;
+    else st_report(out + pos, hi | group, mask);
+}
+__device__ __forceinline__ void st_pad(tsg_report* out, int rec8, int pos) {
+    if (rec8) reinterpret_cast<uint64_t*>(out)[pos] = REPORT_PAD;
+    else st_report(out + pos, REPORT_PAD, 0);
 }
 
 __device__ __forceinline__ int lit_var(int32_t lit) { return lit < 0 ? -lit : lit; }
@@ -896,7 +910,7 @@ __device__ __forceinline__ void test_tiles(const TestParams<LW, GW>& p, const TA
         if (total) {
             if (acc.cpos + total > acc.cend) {  // chunk exhausted: pad its tail, take a new one
                 for (int q = acc.cpos + lane; q < acc.cend; q += 32)
-                    if (q < p.out_cap) st_report(p.out + q, REPORT_PAD, 0);
+                    if (q < p.out_cap) st_pad(p.out, p.rec8, q);
                 const unsigned long long want = total > REPORT_CHUNK ? (unsigned long long)total : REPORT_CHUNK;
                 unsigned long long base = 0;
                 if (lane == 31) base = atomicAdd(p.ctr, want);
@@ -913,7 +927,7 @@ __device__ __forceinline__ void test_tiles(const TestParams<LW, GW>& p, const TA
                 const int slot = (tile - (int)bd->tile0) * STRIDE + lane;
                 double act = 0.0;
                 if (!p.emit_only) act = bd->acts[slot];
-                const uint64_t key_hi = (uint64_t)bd->ids[slot] << 16;  // issued early: off the report's path
+                const uint64_t key_hi = (uint64_t)bd->ids[slot] << (p.rec8 ? 37 : 16);  // issued early: off the report's path
                 bool touched = false;
                 int last_tid = INT_MIN;
                 GW left = word;
@@ -935,7 +949,7 @@ __device__ __forceinline__ void test_tiles(const TestParams<LW, GW>& p, const TA
                         if (tid == p.carry_in_tid)
                             dup = p.carry[bd->tile0 * STRIDE + slot] == (p.stamp_base | (uint32_t)tid);
                         if (!dup) {
-                            if (pos < p.out_cap) st_report(p.out + pos, key_hi | (uint32_t)(p.g0 + g), (uint64_t)mask);
+                            if (pos < p.out_cap) st_record(p.out, p.rec8, pos, key_hi, (uint32_t)(p.g0 + g), (uint64_t)mask);
                             ++pos;
                             ++acc.rep;
                         }
@@ -965,7 +979,7 @@ __device__ __forceinline__ void test_tiles(const TestParams<LW, GW>& p, const TA
                 if (p.carry_out_tid >= 0 && last_tid == p.carry_out_tid)
                     p.carry[bd->tile0 * STRIDE + slot] = p.stamp_base | (uint32_t)last_tid;
                 for (; pos < pend; ++pos)  // padding for reserved-but-unused slots
-                    if (pos < p.out_cap) st_report(p.out + pos, REPORT_PAD, 0);
+                    if (pos < p.out_cap) st_pad(p.out, p.rec8, pos);
             }
         }
         if (ntile >= 0) cur.take(nxt);
@@ -978,7 +992,7 @@ template <class LW, class GW, int WARPS>
 __device__ __forceinline__ void finish_block(const TestParams<LW, GW>& p, WarpAcc& acc, int lane, int warp,
                                              unsigned int (&s_acc)[3][WARPS]) {
     for (int q = acc.cpos + lane; q < acc.cend; q += 32)
-        if (q < p.out_cap) st_report(p.out + q, REPORT_PAD, 0);
+        if (q < p.out_cap) st_pad(p.out, p.rec8, q);
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
         acc.pos += __shfl_down_sync(0xffffffffu, acc.pos, d);
