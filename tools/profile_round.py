@@ -22,6 +22,7 @@ rng = np.random.default_rng(cfg.seed)
 b = W.clause_buckets(n_clauses, cfg.num_vars, rng)
 flat, offs, ids = W.flatten(b)
 eng = NativeEngine(cfg.num_vars, timing=True, report_capacity=8 << 20)
+eng.set_record_bytes(int(os.environ.get("TSG_RECORD_BYTES", "8")))  # as bench.py: the kernel writes 8-byte records
 eng.add_clauses(flat, offs, ids)
 del flat, b
 snaps = W.snapshots(cfg.threads, cfg.lanes, cfg.num_vars, np.random.default_rng(cfg.seed + 999))
