@@ -127,3 +127,14 @@ def test_kth_key_and_count_le_are_exact():
         thr = kth_key(list(zip(acts, ids)), k)
         assert sum(count_le(a, i, thr) for a, i in zip(acts, ids)) == k
     assert kth_key(list(zip(acts, ids)), 500) is None
+
+
+def test_split_groups_equal_contiguous_shares():
+    # split ingress (sharded.combine_tables) needs equal contiguous group
+    # shares so the group-major lane entries all-gather in place
+    from paper_2012_03119_b200 import sharded as S
+    assert S.split_groups(32, 1, 0) is None
+    assert S.split_groups(30, 4, 0) is None
+    got = [S.split_groups(32, 8, r) for r in range(8)]
+    assert got[0] == (0, 4) and got[7] == (28, 32)
+    assert all(a[1] == b[0] for a, b in zip(got, got[1:]))
