@@ -204,9 +204,11 @@ class Engine:
         check(self._L.tsg_packed_words(num_vars, C.byref(w)))
         self._packed_words = w.value
         self._rec_dtype = REPORT_DTYPE
+        self._rec_bytes = 16
         if self.config.lane_width <= 32:  # 12-byte egress records: a quarter fewer bytes D2H
             check(self._L.tsg_set_record_bytes(self._h, 12))
             self._rec_dtype = _reports.RECORD12_DTYPE
+            self._rec_bytes = 12
         self.store = DeviceClauseStore(self)
         self._lits: Dict[int, tuple] = {}
         self._size_rank: Dict[int, int] = {}
@@ -404,6 +406,14 @@ class Engine:
             check(self._L.tsg_stage_packed(self._h, ptr(block), block.shape[0], block.shape[1], 0))
             gl = np.asarray(lanes, dtype=np.int32)
             gt = np.asarray(tids, dtype=np.int32)
+            if self.config.lane_width <= 32:
+                # 8-byte records written by the kernel when ids and groups fit,
+                # else the 12-byte form (include/tsg.h tsg_set_record_bytes)
+                nb = 8 if (self._next_id <= (1 << 27) and len(lanes) <= 32) else 12
+                if nb != self._rec_bytes:
+                    check(self._L.tsg_set_record_bytes(self._h, nb))
+                    self._rec_bytes = nb
+                    self._rec_dtype = _reports.RECORD8_DTYPE if nb == 8 else _reports.RECORD12_DTYPE
             res = _lib.tsg_round_result()
             check(self._L.tsg_round(self._h, ptr(gl), ptr(gt), len(lanes), self._activity_inc, C.byref(res)))
             self.last_round = res
