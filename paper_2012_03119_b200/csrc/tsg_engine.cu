@@ -205,7 +205,10 @@ struct tsg_engine {
     int32_t timing_every = 1;     // TSG_F_TIMING: events on rounds whose sequence is a multiple (tsg_set_timing)
     int64_t grid[32] = {0};       // persistent grid per k_test variant
     int64_t grid_smem[32];        // shared-memory size the grid was computed for (-1: none)
-    bool smem_table = true;       // shared-memory code table when it fits (TSG_SMEM_TABLE=0 disables)
+    // shared-memory code table when it fits: measured slower than the L2
+    // table on B200 even at C1 / C2 (0.026 / 0.047 vs 0.022 / 0.043 ms per
+    // round), so opt-in (TSG_SMEM_TABLE=1)
+    bool smem_table = false;
     // dynamic tile counters in k_test balance the SMs (±5 % active cycles
     // with the static stride) but measured no faster: opt-in, TSG_DYN_TILES=1
     bool dyn_tiles = false;
