@@ -122,6 +122,16 @@ struct tsg_engine {
     int pk = 1;                           // buffer of the last stage
     bool pstaged = false;                 // prows is pbuf[pk], copied on the ingress stream
     cudaStream_t ingress = nullptr;
+    // encoder stream (TSG_ASYNC_ENCODE=1, opt-in): round i+1's encode runs
+    // beside round i's trigger test, filling the SMs its CTAs leave at the
+    // end; the compute stream waits for ev_encoded before the next test.
+    // Measured 0.298 vs 0.293 ms per C3 step (the encode can only start as
+    // k_test's CTAs retire, and the next test then waits for all of it).
+    cudaStream_t enc_st = nullptr;
+    cudaStream_t est = nullptr;           // stream the encoder kernels go to (enc_st or st)
+    bool async_encode = false;
+    bool enc_wait_main = true;            // the encoder's inputs were last written on st (tables, int8 rows)
+    cudaEvent_t ev_main = nullptr, ev_encoded = nullptr;
     cudaEvent_t ev_staged[2] = {nullptr, nullptr};  // copy into pbuf[b] done
     cudaEvent_t ev_read[2] = {nullptr, nullptr};    // encoder done reading pbuf[b]
 
@@ -384,12 +394,12 @@ int launch_encode(tsg_engine* h, int c) {
                 CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
                 h->enc_attr |= bit;
             }
-            fn<<<grid, block, smem, h->st>>>(h->prows, pc, lt, agg);
+            fn<<<grid, block, smem, h->est>>>(h->prows, pc, lt, agg);
         } else {
-            k_encode_packed<LW, GW><<<grid, block, 0, h->st>>>(h->prows, pc, lane, agg);
+            k_encode_packed<LW, GW><<<grid, block, 0, h->est>>>(h->prows, pc, lane, agg);
         }
     } else {
-        k_encode<LW, GW><<<grid, block, 0, h->st>>>(h->rows, ec, lane, agg);
+        k_encode<LW, GW><<<grid, block, 0, h->est>>>(h->rows, ec, lane, agg);
     }
     CK(cudaGetLastError());
     return TSG_OK;
@@ -779,6 +789,7 @@ int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
     h->V = num_vars;
     if (const char* e = getenv("TSG_SMEM_TABLE")) h->smem_table = atoi(e) != 0;
     if (const char* e = getenv("TSG_DYN_TILES")) h->dyn_tiles = atoi(e) != 0;
+    if (const char* e = getenv("TSG_ASYNC_ENCODE")) h->async_encode = atoi(e) != 0;
     if (const char* e = getenv("TSG_L2_PERSIST")) h->l2_persist = atoi(e) != 0;
     if (const char* e = getenv("TSG_PIVOT")) h->pivot = atoi(e) != 0;
     if (const char* e = getenv("TSG_PREFER")) { h->prefer = atoi(e); h->prefer_fixed = true; }
@@ -815,6 +826,10 @@ int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
     }
     cudaStreamCreateWithFlags(&h->egress, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&h->ingress, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&h->enc_st, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&h->ev_main, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&h->ev_encoded, cudaEventDisableTiming);
+    h->est = h->st;
     for (int b = 0; b < 2; ++b) {
         cudaEventCreateWithFlags(&h->ev_staged[b], cudaEventDisableTiming);
         cudaEventCreateWithFlags(&h->ev_read[b], cudaEventDisableTiming);
@@ -845,6 +860,7 @@ int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
 int tsg_destroy(tsg_engine* h) {
     if (!h) return TSG_OK;
     DevGuard g(h->dev);
+    if (h->enc_st) cudaStreamSynchronize(h->enc_st);
     cudaStreamSynchronize(h->st);
     for_parts(h, [&](Bucket&, Part& p) { part_free(h, p); });
     dfree(h, h->d_slab_tile0);
@@ -871,6 +887,8 @@ int tsg_destroy(tsg_engine* h) {
         if (h->ev_read[b]) cudaEventDestroy(h->ev_read[b]);
     }
     if (h->ingress) cudaStreamDestroy(h->ingress);
+    if (h->enc_st) cudaStreamDestroy(h->enc_st);
+    for (cudaEvent_t e : {h->ev_main, h->ev_encoded}) if (e) cudaEventDestroy(e);
     cudaStreamDestroy(h->st);
     delete h;
     return TSG_OK;
@@ -1245,6 +1263,8 @@ int tsg_stage_snapshots(tsg_engine* h, const int8_t* rows, int64_t n_rows, int64
     }
     int64_t pitch = round_up(h->V + 1, 16);
     int64_t need = pitch * n_rows;
+    CK(cudaStreamWaitEvent(h->st, h->ev_encoded, 0));  // the last encode on the encoder stream read rows_own
+    h->enc_wait_main = true;                             // the next encode reads what st copies in
     if (need > h->rows_cap) {
         dfree(h, h->rows_own);
         h->rows_own = nullptr;
@@ -1339,7 +1359,8 @@ int tsg_stage_packed(tsg_engine* h, const uint64_t* rows, int64_t n_rows, int64_
     CK(cudaStreamWaitEvent(h->ingress, h->ev_read[b], 0));
     if (need > h->pbuf_cap[b] || on_device) {
         if (need > h->pbuf_cap[b]) {
-            dfree(h, h->pbuf[b]);  // stream-ordered after its last reader on h->st
+            CK(cudaStreamWaitEvent(h->st, h->ev_read[b], 0));  // its last reader may be on the encoder stream
+            dfree(h, h->pbuf[b]);  // stream-ordered after its last reader
             h->pbuf[b] = nullptr;
             const int64_t cap = std::max(need, h->pbuf_cap[b] * 2);
             CKR(dalloc(h, (void**)&h->pbuf[b], cap * 8));
@@ -1399,6 +1420,8 @@ int tsg_round_prepare(tsg_engine* h, const int32_t* group_lanes, const int32_t* 
         // grow both slots; stream order keeps in-flight rounds valid: their
         // kernels precede the copy, and a later replay reads the moved slot
         int8_t* nt = nullptr;
+        CK(cudaStreamWaitEvent(h->st, h->ev_encoded, 0));  // an encode may still write the old slots
+        h->enc_wait_main = true;                             // the next encode writes the new buffer
         CKR(dalloc(h, (void**)&nt, 2 * slot));
         if (h->tables && any_inflight(h))
             for (int i = 0; i < 2; ++i)
@@ -1617,17 +1640,31 @@ int tsg_round_encode(tsg_engine* h) {
     for (const auto& Q : h->rs)
         if (Q.inflight && Q.slot == h->tslot)
             return fail(TSG_EINVAL, "table slot %d still belongs to an uncollected round", h->tslot);
-    if (h->packed && h->pstaged) CK(cudaStreamWaitEvent(h->st, h->ev_staged[h->pk], 0));  // rows copied in
+    // The encoder's inputs: rows (ingress stream, or st for int8 / device
+    // copies), the table slot (free once its round was collected -- the host
+    // waited for it), the state's polarity counters (zeroed by that round).
+    h->est = h->async_encode ? h->enc_st : h->st;
+    if (h->est != h->st && h->enc_wait_main) {
+        CK(cudaEventRecord(h->ev_main, h->st));
+        CK(cudaStreamWaitEvent(h->est, h->ev_main, 0));
+        h->enc_wait_main = false;
+    }
+    if (h->packed && h->pstaged) CK(cudaStreamWaitEvent(h->est, h->ev_staged[h->pk], 0));  // rows copied in
     const bool timing = timed_round(h, h->round_seq + 1);  // the round this encode feeds
-    if (timing) CK(cudaEventRecord(h->ev_enc[h->tslot][0], h->st));
+    if (timing) CK(cudaEventRecord(h->ev_enc[h->tslot][0], h->est));
     auto& Rn = h->rs[h->next_rs];
     if (Rn.pol_pending)  // re-encoded without a launch: count this encode only
-        CK(cudaMemsetAsync(Rn.ctr + 6, 0, 2 * sizeof(unsigned long long), h->st));
+        CK(cudaMemsetAsync(Rn.ctr + 6, 0, 2 * sizeof(unsigned long long), h->est));
     Rn.pol_pending = true;
-    CKR(do_encode(h));
-    if (h->packed && h->pstaged) CK(cudaEventRecord(h->ev_read[h->pk], h->st));
-    if (timing) CK(cudaEventRecord(h->ev_enc[h->tslot][1], h->st));
-    return TSG_OK;
+    const int rc = do_encode(h);
+    if (h->packed && h->pstaged) CK(cudaEventRecord(h->ev_read[h->pk], h->est));
+    if (timing) CK(cudaEventRecord(h->ev_enc[h->tslot][1], h->est));
+    if (h->est != h->st) {  // everything after this on st (test, broadcast) sees the tables
+        CK(cudaEventRecord(h->ev_encoded, h->est));
+        CK(cudaStreamWaitEvent(h->st, h->ev_encoded, 0));
+    }
+    h->est = h->st;
+    return rc;
 }
 
 // One rank's share of a round's encode when the snapshot ingress is split

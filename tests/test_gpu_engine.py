@@ -454,9 +454,10 @@ def test_c3_full_size_parity(P):
 
 @pytest.mark.parametrize("cap", [1 << 20, 64])  # 64: every round overflows and replays with the next in flight
 @pytest.mark.parametrize("gw", [32, 1])  # gw 1: multi-chunk rounds (carry stamps per round state)
-# pinned: rows copy in asynchronously on the ingress stream; rec 8: the kernel writes 8-byte records
-@pytest.mark.parametrize("pinned,rec", [(False, 16), (True, 16), (False, 8)])
-def test_async_rounds_match_sync_rounds(P, cap, gw, pinned, rec):
+# pinned: rows copy in asynchronously on the ingress stream; rec 8: the kernel writes 8-byte records;
+# aenc: the encoder runs on its own stream (TSG_ASYNC_ENCODE)
+@pytest.mark.parametrize("pinned,rec,aenc", [(False, 16, 0), (True, 16, 0), (False, 8, 0), (True, 8, 1)])
+def test_async_rounds_match_sync_rounds(P, monkeypatch, cap, gw, pinned, rec, aenc):
     # two rounds in flight: launch(k-1), launch(k), collect(k-1) ...: identical
     # figures, records and activities to synchronous rounds, overflow replays included
     from paper_2012_03119_b200 import workload as W
@@ -470,7 +471,10 @@ def test_async_rounds_match_sync_rounds(P, cap, gw, pinned, rec):
         threads = 2 + k % 3
         snaps = W.snapshots(threads, 32, nv, rng)
         rounds.append((snaps, *W.groups_for(threads, 32)))
-    a, b = NativeEngine(nv, 32, gw, report_capacity=cap), NativeEngine(nv, 32, gw)
+    monkeypatch.setenv("TSG_ASYNC_ENCODE", str(aenc))
+    a = NativeEngine(nv, 32, gw, report_capacity=cap)
+    monkeypatch.setenv("TSG_ASYNC_ENCODE", "0")
+    b = NativeEngine(nv, 32, gw)
     if rec == 8:
         a.set_record_bytes(8)
     a.add_clauses(flat, offs, ids)
