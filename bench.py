@@ -202,7 +202,8 @@ def run_reference(args, cfg):
     snaps = W.snapshots(cfg.threads, cfg.lanes, cfg.num_vars, rng)
     gl, gt = W.groups_for(cfg.threads, cfg.lanes)
     from oracle import oracle as O
-    b = W.clause_buckets(1_000_000, cfg.num_vars, np.random.default_rng(cfg.seed + 777), cfg.size_lo, cfg.size_hi)
+    n_sample = min(2_000_000, cfg.n_clauses)  # the same bounded slice as the cpu_baseline leg
+    b = W.clause_buckets(n_sample, cfg.num_vars, np.random.default_rng(cfg.seed + 777), cfg.size_lo, cfg.size_hi)
     flat, offs, ids = W.flatten(b)
     st = O.OracleStore()
     st.insert_flat(flat, offs, ids)
@@ -216,7 +217,7 @@ def run_reference(args, cfg):
         tests += ctr["lane_tests"]
     dt = time.perf_counter() - t0
     v = tests / dt
-    sample = (f"1000000 clauses of the {cfg.name} generator x {snaps.shape[0]} assignments per step, "
+    sample = (f"{n_sample} clauses of the {cfg.name} generator x {snaps.shape[0]} assignments per step, "
               f"oracle/tsg_oracle.c (C port of engine.py:238-467) with {threads} pthreads")
     print(json.dumps({
         "impl": "reference", "metric": "clause_assignment_tests_per_second", "value": v,

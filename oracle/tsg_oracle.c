@@ -40,31 +40,67 @@ int ora_pack(const int8_t* values, int64_t n, int64_t pitch, int32_t num_vars,
 
 /* AggregateAssignment.from_packed (bitpack.py:152-167) folded into
  * build_aggregate_batch (bitpack.py:211-244). */
+/* variables [v_lo, v_hi) of the aggregate (the threads of ora_test_round
+ * split the variables; the result does not depend on the split) */
+static void aggregate_range(const uint64_t* is_true, const uint64_t* is_set, const int32_t* lane_counts,
+                            int32_t n_groups, size_t nv, size_t v_lo, size_t v_hi,
+                            uint64_t* cbt, uint64_t* cbf, uint64_t* cbu) {
+    memset(cbt + v_lo, 0, sizeof(uint64_t) * (v_hi - v_lo));
+    memset(cbf + v_lo, 0, sizeof(uint64_t) * (v_hi - v_lo));
+    memset(cbu + v_lo, 0, sizeof(uint64_t) * (v_hi - v_lo));
+    if (v_lo < 1) v_lo = 1; /* slot 0 stays False, :166 */
+    for (int32_t g = 0; g < n_groups; ++g) {
+        const uint64_t* t = is_true + (size_t)g * nv;
+        const uint64_t* s = is_set + (size_t)g * nv;
+        uint64_t bit = 1ULL << g;
+        if (lane_counts[g] == 0) { /* empty group reads as all-Undef, :156-161 */
+            for (size_t v = v_lo; v < v_hi; ++v) cbu[v] |= bit;
+            continue;
+        }
+        uint64_t mask = width_mask(lane_counts[g]);
+        for (size_t v = v_lo; v < v_hi; ++v) {
+            if (t[v] != 0) cbt[v] |= bit;
+            if ((s[v] & ~t[v]) != 0) cbf[v] |= bit;
+            if ((~s[v] & mask) != 0) cbu[v] |= bit;
+        }
+    }
+}
+
 int ora_aggregate(const uint64_t* is_true, const uint64_t* is_set,
                   const int32_t* lane_counts, int32_t n_groups, int32_t num_vars,
                   int32_t group_width, uint64_t* cbt, uint64_t* cbf, uint64_t* cbu) {
     if (group_width < 1 || group_width > WORD_BITS) return -1;
     if (n_groups > group_width) return -2;
     size_t nv = (size_t)num_vars + 1;
-    memset(cbt, 0, sizeof(uint64_t) * nv);
-    memset(cbf, 0, sizeof(uint64_t) * nv);
-    memset(cbu, 0, sizeof(uint64_t) * nv);
-    for (int32_t g = 0; g < n_groups; ++g) {
-        const uint64_t* t = is_true + (size_t)g * nv;
-        const uint64_t* s = is_set + (size_t)g * nv;
-        uint64_t bit = 1ULL << g;
-        if (lane_counts[g] == 0) { /* empty group reads as all-Undef, :156-161 */
-            for (size_t v = 1; v < nv; ++v) cbu[v] |= bit;
-            continue;
-        }
-        uint64_t mask = width_mask(lane_counts[g]);
-        for (size_t v = 1; v < nv; ++v) { /* slot 0 stays False, :166 */
-            if (t[v] != 0) cbt[v] |= bit;
-            if ((s[v] & ~t[v]) != 0) cbf[v] |= bit;
-            if ((~s[v] & mask) != 0) cbu[v] |= bit;
-        }
-    }
+    aggregate_range(is_true, is_set, lane_counts, n_groups, nv, 0, nv, cbt, cbf, cbu);
     return 0;
+}
+
+/* ora_test_round's table build, split over threads: thread w packs groups
+ * w, w + nw, ... and then aggregates its share of the variables. */
+typedef struct build_job {
+    pthread_t th;
+    int32_t w, nw, phase;
+    const int8_t* snaps;
+    const int64_t* row0;
+    const int32_t* group_lanes;
+    int64_t pitch;
+    int32_t g0, ng, num_vars, lane_width;
+    uint64_t *pt, *ps, *lm, *cb;
+} build_job;
+
+static void* run_build(void* arg) {
+    build_job* j = (build_job*)arg;
+    size_t nv = (size_t)j->num_vars + 1;
+    if (j->phase == 0) {
+        for (int32_t i = j->w; i < j->ng; i += j->nw)
+            ora_pack(j->snaps + j->row0[j->g0 + i] * j->pitch, j->group_lanes[j->g0 + i], j->pitch, j->num_vars,
+                     j->lane_width, j->pt + (size_t)i * nv, j->ps + (size_t)i * nv, &j->lm[i]);
+    } else {
+        size_t lo = nv * (size_t)j->w / (size_t)j->nw, hi = nv * (size_t)(j->w + 1) / (size_t)j->nw;
+        aggregate_range(j->pt, j->ps, j->group_lanes + j->g0, j->ng, nv, lo, hi, j->cb, j->cb + nv, j->cb + 2 * nv);
+    }
+    return NULL;
 }
 
 /* bitpack.py:120-135 (literal_words :58-67) */
@@ -419,12 +455,21 @@ int ora_test_round(ora_store* s, int32_t num_vars, const int8_t* snaps,
     for (int32_t g0 = 0; g0 < n_groups; g0 += group_width) { /* :403-407 */
         int32_t ng = n_groups - g0 < group_width ? n_groups - g0 : group_width;
         int32_t lanes_total = 0;
-        for (int32_t i = 0; i < ng; ++i) {
-            ora_pack(snaps + row0[g0 + i] * pitch, group_lanes[g0 + i], pitch, num_vars,
-                     lane_width, pt + (size_t)i * nv, ps + (size_t)i * nv, &lm[i]);
-            lanes_total += group_lanes[g0 + i];
+        for (int32_t i = 0; i < ng; ++i) lanes_total += group_lanes[g0 + i];
+        /* pack the chunk's groups, then aggregate (bitpack.py:81-117, 152-167, 211-244) */
+        for (int32_t phase = 0; phase < 2; ++phase) {
+            build_job* jobs = (build_job*)calloc((size_t)nthreads, sizeof(build_job));
+            for (int32_t t = 0; t < nthreads; ++t) {
+                build_job jb = {0, t, nthreads, phase, snaps, row0, group_lanes, pitch, g0, ng, num_vars,
+                                lane_width, pt, ps, lm, cb};
+                jobs[t] = jb;
+                if (nthreads > 1) pthread_create(&jobs[t].th, NULL, run_build, &jobs[t]);
+                else run_build(&jobs[t]);
+            }
+            if (nthreads > 1)
+                for (int32_t t = 0; t < nthreads; ++t) pthread_join(jobs[t].th, NULL);
+            free(jobs);
         }
-        ora_aggregate(pt, ps, group_lanes + g0, ng, num_vars, group_width, cb, cb + nv, cb + 2 * nv);
         chunk_ctx c = {s, num_vars, lane_width, group_width, g0, ng, pt, ps, lm,
                        cb, cb + nv, cb + 2 * nv, group_tid, activity_inc};
         int64_t positives = 0;
