@@ -19,6 +19,9 @@ constexpr int MAXG = 64;
 #ifndef TSG_TEST_MIN_BLOCKS
 #define TSG_TEST_MIN_BLOCKS 3
 #endif
+#ifndef TSG_LANE_TAIL2  // stage-2 literals past the prefetched rows two at a time
+#define TSG_LANE_TAIL2 0
+#endif
 #ifndef TSG_TAIL  // stage-1 gather batch after the first four literals
 #define TSG_TAIL 2
 #endif
@@ -958,11 +961,21 @@ __device__ __forceinline__ void test_tiles(const TestParams<LW, GW>& p, const TA
                 auto lane_tail = [&](const LaneEntry<LW>* lt, LW& lf, LW& lo2) {
                     if (size > PF && (lf | lo2) != LW(0)) {
                         const int32_t* lp = lane_lits(bd, tile, lane);
+#if TSG_LANE_TAIL2
+                        for (int j = PF; j < size && (lf | lo2) != LW(0); j += 2) {  // two lane gathers in flight
+                            const int32_t l0 = ld_lit_tail(lp + j * STRIDE);
+                            const int32_t l1 = j + 1 < size ? ld_lit_tail(lp + (j + 1) * STRIDE) : p.sentinel;
+                            const LaneEntry<LW> e0 = ld_lane(lt + lit_var(l0)), e1 = ld_lane(lt + lit_var(l1));
+                            step<LW>(lf, lo2, l0 < 0 ? (e0.s & e0.t) : (e0.s & ~e0.t), ~e0.s);
+                            step<LW>(lf, lo2, l1 < 0 ? (e1.s & e1.t) : (e1.s & ~e1.t), ~e1.s);
+                        }
+#else
                         for (int j = PF; j < size && (lf | lo2) != LW(0); ++j) {
                             const int32_t l = ld_lit_tail(lp + j * STRIDE);
                             const LaneEntry<LW> e = ld_lane(lt + lit_var(l));
                             step<LW>(lf, lo2, l < 0 ? (e.s & e.t) : (e.s & ~e.t), ~e.s);
                         }
+#endif
                     }
                 };
                 while (left) {
