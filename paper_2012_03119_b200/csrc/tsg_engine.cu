@@ -1526,7 +1526,14 @@ int round_launch(tsg_engine* h, double inc, bool flip) {
         CKR(build_desc(h));
         if (h->n_tiles >= (int64_t)INT32_MAX / 2)  // the kernels index tiles with 32-bit integers
             return fail(TSG_ECAPACITY, "store of %lld tiles exceeds the 32-bit tile index", (long long)h->n_tiles);
-        if (R.fl.n_chunks > 1) CKR(dgrow(h, &R.carry, &R.carry_cap, std::max<int64_t>(1, h->n_tiles * STRIDE)));
+        if (R.fl.n_chunks > 1) {
+            // carry stamps are matched by value ((round, run) << 32 | tid): the
+            // buffer is cleared every multi-chunk round, so neither a recycled
+            // allocation (another engine's stamps) nor a round 2^25 launches ago
+            // can fake a "(engine id, tid) already reported"
+            CKR(dgrow(h, &R.carry, &R.carry_cap, std::max<int64_t>(1, h->n_tiles * STRIDE)));
+            CK(cudaMemsetAsync(R.carry, 0, (size_t)std::max<int64_t>(1, h->n_tiles * STRIDE) * sizeof(int64_t), h->st));
+        }
         const bool timing = timed_round(h, R.seq);
         R.timed = timing;
         if (timing) CK(cudaEventRecord(R.ev_tst[0], h->st));
@@ -1587,7 +1594,9 @@ int round_collect(tsg_engine* h, tsg_round_result* out) {
             CKR(run_tests(h, k, R.inc, 1));
             CK(cudaMemcpyAsync(R.h_ctr, R.ctr, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
             CK(cudaStreamSynchronize(h->st));
-            if ((int64_t)R.h_ctr[3] != n_rec) return fail(TSG_ECUDA, "report replay mismatch");
+            if ((int64_t)R.h_ctr[3] != n_rec)
+                return fail(TSG_ECUDA, "report replay mismatch: %lld records, %lld in the first run (replay %d, %d chunks)",
+                            (long long)R.h_ctr[3], (long long)n_rec, R.run, rd.n_chunks);
             n_slots = (int64_t)R.h_ctr[0];
             res.reruns++;
         }

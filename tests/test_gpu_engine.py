@@ -663,3 +663,31 @@ def test_timing_sampling(P):
     with pytest.raises(ValueError):
         e.set_timing(-1)
     e.close()
+
+
+def test_replay_with_threads_spanning_chunks_after_recycled_memory(P):
+    # regression: overflow replays of rounds whose threads span chunk
+    # boundaries, in a second engine of the process (its carry-stamp buffer
+    # recycled from the first engine's) -- every run must match the oracle
+    from paper_2012_03119_b200 import workload as W
+    from paper_2012_03119_b200.native import NativeEngine
+    nv = 300
+    for seed in (1, 5):
+        rng = np.random.default_rng(seed)
+        buckets = W.clause_buckets(60000, nv, rng, 0, 12)
+        flat, offs, ids = W.flatten(buckets)
+        snaps = W.snapshots(3, 58, nv, rng)
+        gl, gt = W.groups_for(3, 58, 16)  # 4 groups per thread, 3 per chunk
+        st = O.OracleStore()
+        st.insert_flat(flat, offs, ids)
+        want, _ = st.test_round(nv, snaps, gl, gt, 16, 3, 1.0, nthreads=8)
+        for cap in (0, 64, 0, 64):
+            e = NativeEngine(nv, 16, 3, report_capacity=cap)
+            e.add_clauses(flat, offs, ids)
+            e.stage(snaps)
+            r = e.round(gl, gt, 1.0)
+            assert r.reports == len(want)
+            recs = W.in_reference_order(e.fetch(r.reports), offs, ids, buckets, 3)
+            for f in ("engine_id", "lane_mask", "group"):
+                assert np.array_equal(recs[f], want[f]), f
+            e.close()

@@ -57,7 +57,11 @@ def test_randomised_parity_vs_oracle():
             snaps = W.snapshots(threads, lanes, nv, rng)
             gl, gt = W.groups_for(threads, lanes, lw)
             dev.stage(snaps)
-            res = dev.round(gl, gt, inc)
+            try:
+                res = dev.round(gl, gt, inc)
+            except Exception as exc:
+                raise AssertionError(f"case {cases} round {r}: lw {lw} gw {gw} nv {nv} n {n} sizes {lo}-{hi} "
+                                     f"threads {threads} lanes {lanes} store {len(dev)}: {exc}") from exc
             recs = dev.fetch(res.reports)
             orecs, octr = ora.test_round(nv, snaps, gl, gt, lw, gw, inc, nthreads=8)
             recs = W.in_reference_order(recs, offs, ids, buckets, gw)
