@@ -50,18 +50,19 @@ typedef struct tsg_config {
     int64_t report_capacity; /* initial device report buffer (records); 0=auto  */
 } tsg_config;
 
-#define TSG_F_TIMING 1 /* record CUDA events around encode/test (fills *_ms) */
+#define TSG_F_TIMING 1    /* record CUDA events around encode/test (fills *_ms)      */
+#define TSG_F_ALL_PAIRS 2 /* every triggering (clause, group), see tsg_set_all_pairs  */
 
 /* Per-round figures, the quantities engine.py:437-467 adds to its counters. */
 typedef struct tsg_round_result {
-    int64_t reports;                  /* records emitted after (eid, tid) dedup   */
+    int64_t reports;                  /* records emitted (after (eid, tid) dedup unless all-pairs) */
     int64_t clauses_tested;           /* engine.py:445 (once per chunk)           */
     int64_t aggregate_tests;          /* engine.py:446                            */
     int64_t aggregate_tests_negative; /* engine.py:465-467                        */
     int64_t lane_tests;               /* engine.py:447                            */
     int64_t lane_triggers;            /* engine.py:461                            */
     int32_t n_chunks;                 /* ceil(n_groups / group_width)             */
-    int32_t reruns;                   /* report-buffer overflow replays           */
+    int32_t reruns;                   /* record-buffer overflow replays (0 or 1)  */
     double encode_ms;                 /* device time, TSG_F_TIMING (-1: not sampled, tsg_set_timing) */
     double test_ms;                   /* device time of the trigger kernels       */
 } tsg_round_result;
@@ -141,6 +142,12 @@ int tsg_bucket_read(tsg_engine* h, int32_t b, int32_t* lits, int64_t* ids,
 int tsg_get_clauses(tsg_engine* h, const int64_t* ids, int64_t n, int32_t* sizes, int32_t* lits,
                     int64_t lits_cap, int64_t* n_lits);
 int tsg_counters(tsg_engine* h, tsg_counters_t* out);
+/* All-pairs mode (or TSG_F_ALL_PAIRS at create): rounds launched while it is
+ * on emit one record for EVERY triggering (clause, group) -- the pair set of
+ * multi_trigger (bitpack.py:282-300) -- instead of the reference's first
+ * triggering group per (clause, thread) (engine.py:462-464).  Activities and
+ * counters are unaffected; `reports` counts the records. */
+int tsg_set_all_pairs(tsg_engine* h, int32_t on);
 /* With TSG_F_TIMING: bracket only rounds whose launch sequence number is a
  * multiple of `every` with timing events (0 = none; default 1 = all) --
  * each event stalls the stream front end for a few microseconds.  Unsampled
@@ -149,10 +156,26 @@ int tsg_set_timing(tsg_engine* h, int32_t every);
 int tsg_scale_activities(tsg_engine* h, double factor);
 /* reduce_store selection + compaction (engine.py:476-500): remove the
  * `target` smallest (activity, engine_id) among clauses with id <
- * eligible_below; order-preserving compaction per bucket.  removed_ids (may be
- * NULL, else room for `target`) receives the removed ids in key order. */
+ * eligible_below (device radix select on the 128-bit key); order-preserving
+ * compaction per bucket.  removed_ids (may be NULL, else room for `target`)
+ * receives the removed ids in ascending order. */
 int tsg_reduce(tsg_engine* h, int64_t eligible_below, int64_t target,
                int64_t* removed, int64_t* removed_ids);
+/* The same selection split for clause shards (one store per GPU): begin
+ * builds the keys of the clauses with id < eligible_below and returns how
+ * many there are; hist fills hist[256] with the number of those keys whose
+ * top `bits` bits (a multiple of 8, < 128) equal the prefix (prefix_hi =
+ * key bits 127..64 = the activity's IEEE bits, prefix_lo = bits 63..0 = the
+ * engine id, both left-aligned, the rest zero), per value of the next 8
+ * bits; the caller sums the shards' histograms and extends the prefix
+ * until it pins the global target-th smallest key; commit removes every
+ * eligible key whose top `bits` bits are <= the prefix (bits = 0: none)
+ * and ends the selection (removed_ids: room for cap ids, ascending; may be
+ * NULL).  The store must not change between begin and commit. */
+int tsg_reduce_begin(tsg_engine* h, int64_t eligible_below, int64_t* n_eligible);
+int tsg_reduce_hist(tsg_engine* h, uint64_t prefix_hi, uint64_t prefix_lo, int32_t bits, uint64_t* hist);
+int tsg_reduce_commit(tsg_engine* h, uint64_t prefix_hi, uint64_t prefix_lo, int32_t bits, int64_t* removed,
+                      int64_t* removed_ids, int64_t cap);
 /* explicit delete (streaming config C4): remove the listed ids if present,
  * order-preserving (the compact(keep) of engine.py:184-200). */
 int tsg_remove_clauses(tsg_engine* h, const int64_t* ids, int64_t n, int64_t* removed);
@@ -164,9 +187,12 @@ int tsg_remove_clauses(tsg_engine* h, const int64_t* ids, int64_t n, int64_t* re
  *    False, like bitpack.py:108-109).  `row_pitch` is the byte distance between
  *    rows at `rows`; on_device=1 means `rows` is a device pointer.
  * 2. tsg_round: encode (K1/K2) and test (K3+K4+K5) every chunk of
- *    group_width groups against every bucket; bumps activities by
- *    activity_inc * hits (engine.py:460, fp64, no FMA).
- * 3. tsg_fetch_reports: copy the round's report records out.
+ *    group_width groups against every bucket in ONE trigger launch (rounds
+ *    of several chunks sweep a chunk-level aggregate first);
+ *    bumps activities by activity_inc * hits (engine.py:460, fp64, no FMA).
+ *    A thread's groups must be consecutive (TSG_EINVAL otherwise).
+ * 3. tsg_fetch_reports: copy the round's report records out (exactly
+ *    `reports` records, unordered: the host orders them, reports.py).
  * The split form (prepare / encode / tables / test) exists for multi-GPU:
  * rank 0 encodes, the packed tables are broadcast over NVLink, every rank
  * tests its own clause shard. */
@@ -197,6 +223,12 @@ int tsg_round_prepare(tsg_engine* h, const int32_t* group_lanes,
                       const int32_t* group_tid, int32_t n_groups);
 int tsg_round_encode(tsg_engine* h);
 int tsg_round_tables(tsg_engine* h, void** device_ptr, int64_t* bytes);
+/* One process driving several GPUs (one engine per device, each holding a
+ * clause shard): copy the encoded tables of src's prepared round into dst's
+ * table slot over NVLink (peer copy, ordered after src's encode; src's next
+ * encode waits for it).  Both engines must have prepared the same round;
+ * dst then launches without encoding. */
+int tsg_round_tables_copy(tsg_engine* dst, tsg_engine* src);
 /* Split snapshot ingress across GPUs: each rank stages the
  * packed rows of groups [g_begin, g_end) only and encodes them; lane entries
  * of the other groups are left for an all-gather, aggregate words carry only

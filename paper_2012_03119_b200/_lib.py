@@ -17,6 +17,7 @@ LIB_PATH = os.environ.get("TSG_LIB", os.path.join(HERE, "libtsg.so"))
 
 TSG_OK, TSG_EINVAL, TSG_ECAPACITY, TSG_ERANGE, TSG_ECUDA, TSG_ENOMEM = range(6)
 TSG_F_TIMING = 1
+TSG_F_ALL_PAIRS = 2
 
 
 class CapacityError(ValueError):
@@ -58,7 +59,8 @@ EXPORTS = (
     "tsg_aggregate_trigger", "tsg_packed_words", "tsg_pack_rows", "tsg_stage_packed",
     "tsg_fetch_reports_async", "tsg_fetch_wait", "tsg_round_launch", "tsg_round_collect",
     "tsg_set_record_bytes", "tsg_get_clauses", "tsg_counters", "tsg_set_timing", "tsg_round_encode_groups",
-    "tsg_round_layout",
+    "tsg_round_layout", "tsg_set_all_pairs", "tsg_round_tables_copy", "tsg_reduce_begin", "tsg_reduce_hist",
+    "tsg_reduce_commit",
 )
 
 _lib = None
@@ -83,9 +85,14 @@ def _declare(L):
         "tsg_get_clauses": ([P, P, I64, P, P, I64, pI64], C.c_int),
         "tsg_counters": ([P, P], C.c_int),
         "tsg_set_timing": ([P, I32], C.c_int),
+        "tsg_set_all_pairs": ([P, I32], C.c_int),
+        "tsg_round_tables_copy": ([P, P], C.c_int),
         "tsg_round_encode_groups": ([P, I32, I32, I32], C.c_int),
         "tsg_round_layout": ([P, pI64, pI64, pI64, pI64], C.c_int),
         "tsg_reduce": ([P, I64, I64, pI64, P], C.c_int),
+        "tsg_reduce_begin": ([P, I64, pI64], C.c_int),
+        "tsg_reduce_hist": ([P, C.c_uint64, C.c_uint64, I32, P], C.c_int),
+        "tsg_reduce_commit": ([P, C.c_uint64, C.c_uint64, I32, pI64, P, I64], C.c_int),
         "tsg_remove_clauses": ([P, P, I64, pI64], C.c_int),
         "tsg_stage_snapshots": ([P, P, I64, I64, I32], C.c_int),
         "tsg_packed_words": ([I32, P], C.c_int),

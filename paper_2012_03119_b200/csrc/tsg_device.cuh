@@ -33,72 +33,33 @@ __host__ __device__ __forceinline__ W width_mask(int w) {
     return w >= (int)(sizeof(W) * 8) ? ~W(0) : ((W(1) << w) - W(1));
 }
 
-// L2 eviction hints (TSG_L2_HINTS; measured slower, default off): 1 =
-// evict_last on the table gathers + evict_first on the literal stream
-// (k_test 0.288 vs 0.267 ms), 2 = evict_first on the stream only (0.269).
-#ifndef TSG_L2_HINTS
-#define TSG_L2_HINTS 0
-#endif
-__device__ __forceinline__ uint64_t l2_keep_policy() {
-    uint64_t pol;
-    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-__device__ __forceinline__ uint64_t l2_stream_policy() {
-    uint64_t pol;
-    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-
 __device__ __forceinline__ AggEntry<uint32_t> ld_agg(const AggEntry<uint32_t>* p) {
-#if TSG_L2_HINTS == 1
-    uint4 v;
-    asm("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
-        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(l2_keep_policy()));
-#else
-    uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
-#endif
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
     return {v.x, v.y, v.z, v.w};
 }
 __device__ __forceinline__ AggEntry<uint64_t> ld_agg(const AggEntry<uint64_t>* p) {
-    ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(p));
-    ulonglong2 b = __ldg(reinterpret_cast<const ulonglong2*>(p) + 1);
+    const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(p));
+    const ulonglong2 b = __ldg(reinterpret_cast<const ulonglong2*>(p) + 1);
     return {a.x, a.y, b.x, b.y};
 }
 __device__ __forceinline__ LaneEntry<uint32_t> ld_lane(const LaneEntry<uint32_t>* p) {
-#if TSG_L2_HINTS == 1
-    uint2 v;
-    asm("ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(l2_keep_policy()));
-#else
-    uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
-#endif
+    const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
     return {v.x, v.y};
 }
 __device__ __forceinline__ LaneEntry<uint64_t> ld_lane(const LaneEntry<uint64_t>* p) {
-    ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(p));
+    const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(p));
     return {v.x, v.y};
 }
 
-// Streaming literal load: the clause DB is read once per round.
+// Streaming literal load: the clause DB is read once per round, past L1
+// (which it would only evict the table lines from).
 __device__ __forceinline__ int32_t ld_lit(const int32_t* p) {
     int32_t r;
-#if TSG_L2_HINTS
-    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(l2_stream_policy()));
-#else
     asm("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(r) : "l"(p));
-#endif
     return r;
 }
-// literals past the prefetched rows: through L1 (stage 2 re-reads them), first out of L2
-__device__ __forceinline__ int32_t ld_lit_tail(const int32_t* p) {
-#if TSG_L2_HINTS
-    int32_t r;
-    asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(l2_stream_policy()));
-    return r;
-#else
-    return __ldg(p);
-#endif
-}
+// literals past the prefetched rows: through L1 (stage 2 re-reads them)
+__device__ __forceinline__ int32_t ld_lit_tail(const int32_t* p) { return __ldg(p); }
 
 __device__ __forceinline__ void or_shared(uint32_t* p, uint32_t v) { atomicOr(p, v); }
 __device__ __forceinline__ void or_shared(uint64_t* p, uint64_t v) {

@@ -1,8 +1,10 @@
 // tsg_engine.cu -- C ABI (include/tsg.h) over the sm_100a kernels.
 //
-// Host runtime of the device engine: bucket bookkeeping, staging, chunking,
-// kernel launches on one CUDA stream per handle, report-buffer management,
-// store maintenance with CUB sort/select for the rare reduce path.
+// Host runtime of the device engine: bucket bookkeeping, staging, the round
+// (encode, chunk-level aggregate, one trigger launch), record buffers and
+// egress, and store maintenance (radix-select reduce, order-preserving
+// compaction).  Every device kernel on these paths is in tsg_kernels.cuh /
+// tsg_store.cuh; no library kernels.
 #include <cuda_runtime.h>
 #include <immintrin.h>
 
@@ -12,10 +14,8 @@
 #include <cstring>
 #include <string>
 #include <unordered_map>
+#include <unordered_set>
 #include <vector>
-
-#include <cub/cub.cuh>
-#include <thrust/iterator/counting_iterator.h>
 
 #include "../../include/tsg.h"
 #include "tsg_kernels.cuh"
@@ -61,29 +61,17 @@ int grid_for(int64_t n, int threads = 256, int cap = 148 * 16) {
     return (int)b;
 }
 
-// One physical interleaved array: the clauses of one size bucket whose hot
-// slab is `slab`.  Slot order inside a part is append order,
-// i.e. engine-id order; a logical bucket is the id-ordered merge of its parts.
-struct Part {
-    int32_t slab = 0;
+// A size bucket of the reference store (engine.py:122-163): one interleaved
+// array, slots in placement order (pivot-sorted per insert batch, DESIGN.md
+// §3); the reference's slot order is engine-id order (reports.py).
+struct Bucket {
+    int32_t size = 0, rank = 0;
     int64_t count = 0, cap = 0;  // cap: multiple of STRIDE
-    int32_t* lits = nullptr;     // placement order (see `order`)
+    int32_t* lits = nullptr;
     double* acts = nullptr;
     int64_t* ids = nullptr;
     int32_t* origins = nullptr;
     uint64_t* order = nullptr;   // where the stored literal order came from (tsg_store.cuh order_word)
-};
-
-// A size bucket of the reference store (engine.py:122-163), split into one
-// part per variable slab.
-struct Bucket {
-    int32_t size = 0, rank = 0;
-    std::vector<Part> parts;
-    int64_t count() const {
-        int64_t n = 0;
-        for (auto& p : parts) n += p.count;
-        return n;
-    }
 };
 
 }  // namespace
@@ -95,7 +83,9 @@ struct RoundDesc {
     int32_t n_groups = 0, n_chunks = 0;
     std::vector<int32_t> glanes, gtid;
     std::vector<int64_t> grow0;
-    std::vector<int64_t> chunk_off;  // byte offset of each chunk's tables within a table slot
+    int64_t chunk_stride = 0;  // bytes between chunk tables inside a table slot
+    int64_t top_off = 0;       // chunk-level aggregate (n_chunks > 1)
+    int32_t per_bit = 1;       // chunks per bit of the chunk-level aggregate
 };
 
 struct tsg_engine {
@@ -122,128 +112,96 @@ struct tsg_engine {
     int pk = 1;                           // buffer of the last stage
     bool pstaged = false;                 // prows is pbuf[pk], copied on the ingress stream
     cudaStream_t ingress = nullptr;
-    // encoder stream (TSG_ASYNC_ENCODE=1, opt-in): round i+1's encode runs
-    // beside round i's trigger test, filling the SMs its CTAs leave at the
-    // end; the compute stream waits for ev_encoded before the next test.
-    // Measured 0.298 vs 0.293 ms per C3 step (the encode can only start as
-    // k_test's CTAs retire, and the next test then waits for all of it).
-    cudaStream_t enc_st = nullptr;
-    cudaStream_t est = nullptr;           // stream the encoder kernels go to (enc_st or st)
-    bool async_encode = false;
-    bool enc_wait_main = true;            // the encoder's inputs were last written on st (tables, int8 rows)
-    cudaEvent_t ev_main = nullptr, ev_encoded = nullptr;
     cudaEvent_t ev_staged[2] = {nullptr, nullptr};  // copy into pbuf[b] done
     cudaEvent_t ev_read[2] = {nullptr, nullptr};    // encoder done reading pbuf[b]
 
-    // round description as prepared
-    RoundDesc rd;
-    // round tables: two slots of tables_bytes each (slot stride slot_bytes);
-    // encode writes slot `tslot`; tsg_round_launch flips it, so the next
-    // round encodes while the launched one still owns its tables
+    RoundDesc rd;  // as prepared
+    // round tables: two slots (slot stride slot_bytes); encode writes slot
+    // `tslot`; tsg_round_launch flips it, so the next round encodes while the
+    // launched one still owns its tables
     int8_t* tables = nullptr;
-    int64_t tables_cap = 0, tables_bytes = 0, slot_bytes = 0;
+    int64_t tables_bytes = 0, slot_bytes = 0;
     int tslot = 0;
     cudaEvent_t ev_enc[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // per table slot: encode start/end
 
     // Two round states alternate: a launched round keeps its
-    // group description, table slot, counters, carry stamps and record
-    // buffers until it is collected, so up to two rounds are in flight and
-    // the next round is queued before the previous one is collected.
+    // group description, table slot, counters and record buffer until it is
+    // collected -- and the buffer until its records were copied out -- so up
+    // to two rounds are in flight.
     struct RoundState {
         RoundDesc fl;
         int slot = 0;                         // table slot it tests
         double inc = 0.0;
-        int64_t seq = 0;                      // launch sequence: carry stamps, collect order
-        int32_t run = 0;                      // 0: the round's test; 1, 2, ...: emission replays
+        int64_t seq = 0;                      // launch sequence: collect order
         bool inflight = false;                // launched, not collected
-        // device [8]: [0..3] round counters, [5] CTAs done, [6..7] polarity
-        // counts; zero between rounds (the round's last CTA publishes them
-        // to h_ctr and re-zeroes them, so no memset or copy is queued)
+        // device [8]: [0] records, [1] aggregate positives, [2] lane triggers,
+        // [5] CTAs done, [6..7] polarity counts; zero between rounds (the
+        // round's last CTA publishes them to h_ctr and re-zeroes them)
         unsigned long long* ctr = nullptr;
         unsigned long long* h_ctr = nullptr;  // pinned [8], written by the kernel
         bool pol_pending = false;             // an encode counted into ctr[6..7] since the last launch
         bool timed = false;                   // its encode / test are bracketed by timing events
-        bool rec8 = false;                    // its records are 8-byte u64 (tsg_set_record_bytes(8) and they fit)
-        unsigned long long* tiles = nullptr;  // device DynTiles counters, zero between launches
+        bool rec8 = false;                    // its records are 8-byte u64
+        bool all_pairs = false;
+        GroupDesc* d_groups = nullptr;        // the round's groups (device)
+        GroupDesc* h_groups = nullptr;        // pinned staging of the same
+        int64_t groups_cap = 0;
         cudaEvent_t ev_done = nullptr;        // its counters are on the host
         cudaEvent_t ev_tst[2] = {nullptr, nullptr};
-        int64_t* carry = nullptr;             // per-clause (round, tid) stamps of multi-chunk rounds
-        int64_t carry_cap = 0;
+        // records: exact count n_out in out (tsg_report or u64); egress
+        // repacking in out12; ev_copied = the last copy-out from them is done
+        tsg_report* out = nullptr;
+        int64_t out_cap = 0, n_out = 0;
+        uint8_t* out12 = nullptr;
+        int64_t out12_cap = 0;
+        cudaEvent_t ev_copied = nullptr;
     } rs[2];
     int next_rs = 0;                      // state of the next launch
     int fetch_rs = 0;                     // state the fetch calls read (the last collected)
-    int report_rs = 0;                    // state whose record buffers are in the fields below
-    unsigned long long* mctr = nullptr;   // device [8]: maintenance scratch (reduce, remove, range check)
+    unsigned long long* mctr = nullptr;   // device [8]: maintenance scratch
     unsigned long long* h_mctr = nullptr; // pinned [8]
+    cudaStream_t egress = nullptr;
+    cudaEvent_t ev_ready = nullptr;       // records ready for copy-out
+    cudaEvent_t ev_peer = nullptr;        // tsg_round_tables_copy: tables encoded / copied
 
     BucketDesc* d_desc = nullptr;
     int64_t desc_cap = 0;
     std::vector<BucketDesc> h_desc;
     int64_t n_tiles = 0;
+    bool desc_dirty = true;               // store changed since the tile table was built
 
-    tsg_report* out = nullptr;
-    int64_t out_cap = 0, n_out = 0, n_alloc = 0;
-    tsg_report* out2 = nullptr;             // compaction target for fetch
-    int64_t out2_cap = 0;
-    bool compacted = true;
-    // record buffers: the fields above belong to round state `report_rs`,
-    // `alt` to the other one (use_reports swaps them); a state's buffers are
-    // rewritten only after their copy-out event (tsg_fetch_reports_async).
-    struct Slot {
-        tsg_report *out = nullptr, *out2 = nullptr;
-        int64_t out_cap = 0, out2_cap = 0;
-        uint8_t* out12 = nullptr;
-        int64_t out12_cap = 0;
-        cudaEvent_t ev = nullptr;   // copy-out of these records done
-        int64_t n_out = 0, n_alloc = 0;
-        bool compacted = true;
-    } alt;
-    cudaEvent_t ev_cur = nullptr;   // copy-out of the current buffers done
-    cudaStream_t egress = nullptr;
-    cudaEvent_t ev_ready = nullptr; // compacted records ready for copy-out
     int32_t record_bytes = 16;      // egress record format (tsg_set_record_bytes)
+    bool all_pairs = false;         // tsg_set_all_pairs
     int64_t max_id = -1;            // largest engine id ever added (8-byte records need < 2^27)
-    uint8_t* out12 = nullptr;       // 12-byte egress records of the current slot
-    int64_t out12_cap = 0;
-    bool oob = false;  // a stored literal may exceed num_vars (checked before testing)
+    bool oob = false;               // a stored literal may exceed num_vars (checked before testing)
     int64_t round_seq = 0;
-    int enc_attr = 0;             // k_encode_packed32 shared-memory attribute set, per GW
+    int enc_attr = 0;               // k_encode_packed32 shared-memory attribute set, per (GPW, GW)
     // tsg_round_encode_groups: encode groups [enc_g0, enc_g1) only (enc_g1 < 0: all)
     int32_t enc_g0 = 0, enc_g1 = -1;
     bool enc_sentinel = true;
-    tsg_counters_t totals{};      // cumulative figures (tsg_counters)
-    int32_t timing_every = 1;     // TSG_F_TIMING: events on rounds whose sequence is a multiple (tsg_set_timing)
-    int64_t grid[32] = {0};       // persistent grid per k_test variant
-    int64_t grid_smem[32];        // shared-memory size the grid was computed for (-1: none)
-    // shared-memory code table when it fits: measured slower than the L2
-    // table on B200 even at C1 / C2 (0.026 / 0.047 vs 0.022 / 0.043 ms per
-    // round), so opt-in (TSG_SMEM_TABLE=1)
-    bool smem_table = false;
-    // dynamic tile counters in k_test balance the SMs (±5 % active cycles
-    // with the static stride) but measured no faster: opt-in, TSG_DYN_TILES=1
-    bool dyn_tiles = false;
-    uint8_t* codes = nullptr;     // literal-code table of the current chunk
-    int64_t codes_cap = 0;
+    tsg_counters_t totals{};        // cumulative figures (tsg_counters)
+    int32_t timing_every = 1;       // TSG_F_TIMING: events on rounds whose sequence is a multiple (tsg_set_timing)
+    int64_t grid[8] = {0};          // persistent grid per k_test variant (0: not computed)
 
-    // variable slabs: [s * slab_w, (s + 1) * slab_w) for s < n_slabs, covering 0..V+1
-    int32_t n_slabs = 1, slab_w = 0;
-    bool slab_test = true;               // slab kernel when n_slabs > 1 (TSG_SLABS=0 disables)
-    std::vector<int64_t> slab_load;      // clauses per slab (placement tie-break)
-    std::vector<int64_t> h_slab_tile0;   // first tile of each slab (+ end)
-    std::vector<int32_t> h_slab_desc0;   // first descriptor of each slab (+ end)
-    int64_t* d_slab_tile0 = nullptr;     // [n_slabs + 1] tile0, then [n_slabs + 1] desc0 (int32), then schedule
-    int64_t slab_tile0_cap = 0;
-    std::vector<uint64_t> h_sched;
-    bool desc_dirty = true;             // store changed since the tile table was built
-    bool pivot = true;                  // pivot-first clause layout (TSG_PIVOT=0 disables)
+    // a reduce selection in progress (tsg_reduce_begin .. tsg_reduce_commit):
+    // the flat key arrays over the store as it was at begin
+    struct Select {
+        bool open = false;
+        uint64_t *ka = nullptr, *ki = nullptr;
+        uint8_t* keep = nullptr;
+        unsigned long long* hist = nullptr;
+        std::vector<int64_t> base;
+        int64_t flat = 0, n_eligible = 0, store_seq = 0;
+    } sel;
+    int64_t store_seq = 0;          // bumped by every store change (a selection must not outlive one)
+
+    bool pivot = true;              // pivot-first clause layout (TSG_PIVOT=0 disables)
     // literal polarity placed right after the pivot (+1 / -1 / 0 none).  Prior
     // before any round: +1 -- in the paper's measured value subsets
     // a variable can be True in a window more often
     // (.208) than False (.153), so positive literals are non-False more often
     int prefer = 1;
-    bool prefer_fixed = false;          // TSG_PREFER fixes it; else set from each round's statistics
-    bool l2_persist = false;            // persisting L2 window over the round tables (TSG_L2_PERSIST=1; measured slower)
-    const void* persist_base = nullptr;
+    bool prefer_fixed = false;      // TSG_PREFER fixes it; else set from each round's statistics
 };
 
 namespace {
@@ -284,61 +242,51 @@ void dfree(tsg_engine* h, void* p) {
 }
 
 template <class T>
-int dgrow(tsg_engine* h, T** p, int64_t* cap, int64_t need, bool keep = false, int64_t keep_elems = 0) {
+int dgrow(tsg_engine* h, T** p, int64_t* cap, int64_t need) {
     if (need <= *cap) return TSG_OK;
     int64_t nc = std::max<int64_t>(need, *cap * 2);
     T* np = nullptr;
     CKR(dalloc(h, (void**)&np, nc * (int64_t)sizeof(T)));
-    if (keep && *p && keep_elems)
-        CK(cudaMemcpyAsync(np, *p, keep_elems * sizeof(T), cudaMemcpyDeviceToDevice, h->st));
     dfree(h, *p);
     *p = np;
     *cap = nc;
     return TSG_OK;
 }
 
-void part_free(tsg_engine* h, Part& p) {
-    dfree(h, p.lits); dfree(h, p.acts); dfree(h, p.ids); dfree(h, p.origins); dfree(h, p.order);
-    p.lits = nullptr; p.acts = nullptr; p.ids = nullptr; p.origins = nullptr; p.order = nullptr;
+void bucket_free(tsg_engine* h, Bucket& b) {
+    dfree(h, b.lits); dfree(h, b.acts); dfree(h, b.ids); dfree(h, b.origins); dfree(h, b.order);
+    b.lits = nullptr; b.acts = nullptr; b.ids = nullptr; b.origins = nullptr; b.order = nullptr;
 }
 
-int part_alloc(tsg_engine* h, Part& p, int32_t size, int64_t cap) {
-    CKR(dalloc(h, (void**)&p.lits, cap * (int64_t)std::max(size, 1) * 4));
-    CKR(dalloc(h, (void**)&p.acts, cap * 8));
-    CKR(dalloc(h, (void**)&p.ids, cap * 8));
-    CKR(dalloc(h, (void**)&p.origins, cap * 4));
-    CKR(dalloc(h, (void**)&p.order, cap * 8));
-    p.cap = cap;
+// arrays of a bucket with `cap` slots (count and bookkeeping unchanged)
+int bucket_alloc(tsg_engine* h, Bucket& b, int64_t cap) {
+    CKR(dalloc(h, (void**)&b.lits, cap * (int64_t)std::max(b.size, 1) * 4));
+    CKR(dalloc(h, (void**)&b.acts, cap * 8));
+    CKR(dalloc(h, (void**)&b.ids, cap * 8));
+    CKR(dalloc(h, (void**)&b.origins, cap * 4));
+    CKR(dalloc(h, (void**)&b.order, cap * 8));
+    b.cap = cap;
     return TSG_OK;
 }
 
-int part_reserve(tsg_engine* h, Part& b, int32_t size, int64_t need) {
+int bucket_reserve(tsg_engine* h, Bucket& b, int64_t need) {
     if (need <= b.cap) return TSG_OK;
     // _SizeBucket._grow doubles with a floor of 4 blocks (engine.py:141-148)
     int64_t nc = std::max<int64_t>(b.cap ? b.cap : 4 * STRIDE, 4 * STRIDE);
     while (nc < need) nc *= 2;
-    Part n;
-    n.slab = b.slab;
-    n.count = b.count;
-    CKR(part_alloc(h, n, size, nc));
+    Bucket n = b;
+    CKR(bucket_alloc(h, n, nc));
     if (b.count) {
-        int64_t used = round_up(b.count, STRIDE);
-        if (size) CK(cudaMemcpyAsync(n.lits, b.lits, used * size * 4, cudaMemcpyDeviceToDevice, h->st));
+        const int64_t used = round_up(b.count, STRIDE);
+        if (b.size) CK(cudaMemcpyAsync(n.lits, b.lits, used * b.size * 4, cudaMemcpyDeviceToDevice, h->st));
         CK(cudaMemcpyAsync(n.acts, b.acts, b.count * 8, cudaMemcpyDeviceToDevice, h->st));
         CK(cudaMemcpyAsync(n.ids, b.ids, b.count * 8, cudaMemcpyDeviceToDevice, h->st));
         CK(cudaMemcpyAsync(n.origins, b.origins, b.count * 4, cudaMemcpyDeviceToDevice, h->st));
         CK(cudaMemcpyAsync(n.order, b.order, b.count * 8, cudaMemcpyDeviceToDevice, h->st));
     }
-    part_free(h, b);
+    bucket_free(h, b);
     b = n;
     return TSG_OK;
-}
-
-// every physical part, bucket-major then slab (the order of reduce/remove keep flags)
-template <class F>
-void for_parts(tsg_engine* h, F&& f) {
-    for (auto& b : h->buckets)
-        for (auto& p : b.parts) f(b, p);
 }
 
 bool wide_lane(const tsg_engine* h) { return h->cfg.lane_width > 32; }
@@ -347,273 +295,170 @@ int64_t agg_entry_bytes(const tsg_engine* h) { return wide_group(h) ? 32 : 16; }
 int64_t vstride(const tsg_engine* h) { return round_up((int64_t)h->V + 2, 4); }
 int64_t agg_bytes(const tsg_engine* h) { return round_up((int64_t)(h->V + 2) * agg_entry_bytes(h), 256); }
 int64_t lane_entry_bytes(const tsg_engine* h) { return wide_lane(h) ? 16 : 8; }
+// one chunk's tables: its aggregate table, then its groups' lane tables
+int64_t chunk_bytes(const tsg_engine* h) {
+    return agg_bytes(h) + round_up(vstride(h) * h->cfg.group_width * lane_entry_bytes(h), 256);
+}
+int64_t top_bytes(const tsg_engine* h) { return round_up((int64_t)(h->V + 2) * 16, 256); }
+
+// u64 words of one packed row: every 128-variable encoder block reads 4 words
+int64_t packed_words(int32_t V) { return round_up(((int64_t)V + 2 + 31) / 32, 4); }
 
 template <class LW, class GW>
 int launch_encode(tsg_engine* h, int c) {
-    EncodeChunk ec{};
     const RoundDesc& rd = h->rd;
-    int32_t g0 = c * h->cfg.group_width;
-    ec.G = std::min(h->cfg.group_width, rd.n_groups - g0);
-    ec.num_vars = h->V;
-    ec.pitch = h->pitch;
-    ec.vstride = vstride(h);
-    for (int g = 0; g < ec.G; ++g) {
-        ec.row0[g] = rd.grow0[g0 + g];
-        ec.lanes[g] = rd.glanes[g0 + g];
-    }
-    ec.polarity = h->rs[h->next_rs].ctr + 6;  // counted for the round this encode feeds
-    int8_t* tab = h->tables + h->tslot * h->slot_bytes;
-    auto* agg = reinterpret_cast<AggEntry<GW>*>(tab + rd.chunk_off[c]);
-    auto* lane = reinterpret_cast<LaneEntry<LW>*>(tab + rd.chunk_off[c] + agg_bytes(h));
-    dim3 grid((unsigned)((h->V + 2 + 127) / 128)), block(32, 8);
-    if (h->packed) {
-        EncodePackedChunk pc{};
-        pc.G = ec.G;
-        pc.num_vars = h->V;
-        pc.pitch_words = h->ppitch;
-        pc.vstride = ec.vstride;
-        // a group range (tsg_round_encode_groups): rows hold only its groups
-        const int64_t row_base = h->enc_g1 >= 0 ? rd.grow0[h->enc_g0] : 0;
-        for (int g = 0; g < ec.G; ++g) { pc.row0[g] = ec.row0[g] - row_base; pc.lanes[g] = ec.lanes[g]; }
-        pc.polarity = ec.polarity;
-        pc.gbeg = h->enc_g1 >= 0 ? std::max(0, h->enc_g0 - g0) : 0;
-        pc.gend = h->enc_g1 >= 0 ? std::min(ec.G, h->enc_g1 - g0) : ec.G;
-        pc.sentinel = h->enc_sentinel ? 1 : 0;
-        static const bool enc_stage = !getenv("TSG_ENC_STAGE") || atoi(getenv("TSG_ENC_STAGE")) != 0;
-        if (h->enc_g1 >= 0 && !(sizeof(LW) == 4 && enc_stage))
-            return fail(TSG_EINVAL, "group-range encode needs the staged encoder (k_encode_packed32)");
-        if (sizeof(LW) == 4 && enc_stage) {
-            const int need = (ec.G + 7) / 8;  // groups per warp
-            const int gpw = need <= 1 ? 1 : need <= 2 ? 2 : need <= 4 ? 4 : 8;
-            const size_t smem = (size_t)8 * gpw * 32 * 32;
-            auto* lt = reinterpret_cast<LaneEntry<uint32_t>*>(lane);
-            auto* fn = gpw == 1 ? k_encode_packed32<GW, 1> : gpw == 2 ? k_encode_packed32<GW, 2>
-                     : gpw == 4 ? k_encode_packed32<GW, 4> : k_encode_packed32<GW, 8>;
-            const int bit = 1 << (gpw + 8 * (int)(sizeof(GW) / 8));
-            if (!(h->enc_attr & bit)) {  // 64 KB of row stage at 8 groups per warp
-                CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                h->enc_attr |= bit;
-            }
-            fn<<<grid, block, smem, h->est>>>(h->prows, pc, lt, agg);
-        } else {
-            k_encode_packed<LW, GW><<<grid, block, 0, h->est>>>(h->prows, pc, lane, agg);
+    const int32_t g0 = c * h->cfg.group_width;
+    const int32_t G = std::min(h->cfg.group_width, rd.n_groups - g0);
+    int8_t* tab = h->tables + h->tslot * h->slot_bytes + c * rd.chunk_stride;
+    auto* agg = reinterpret_cast<AggEntry<GW>*>(tab);
+    auto* lane = reinterpret_cast<LaneEntry<LW>*>(tab + agg_bytes(h));
+    unsigned long long* polarity = h->rs[h->next_rs].ctr + 6;  // counted for the round this encode feeds
+    const dim3 grid((unsigned)((h->V + 2 + 127) / 128)), block(32, 8);
+    if (!h->packed) {
+        EncodeChunk ec{};
+        ec.G = G;
+        ec.num_vars = h->V;
+        ec.pitch = h->pitch;
+        ec.vstride = vstride(h);
+        for (int g = 0; g < G; ++g) {
+            ec.row0[g] = rd.grow0[g0 + g];
+            ec.lanes[g] = rd.glanes[g0 + g];
         }
+        ec.polarity = polarity;
+        k_encode<LW, GW><<<grid, block, 0, h->st>>>(h->rows, ec, lane, agg);
+        CK(cudaGetLastError());
+        return TSG_OK;
+    }
+    EncodePackedChunk pc{};
+    pc.G = G;
+    pc.num_vars = h->V;
+    pc.pitch_words = h->ppitch;
+    pc.vstride = vstride(h);
+    // a group range (tsg_round_encode_groups): the rows hold only its groups
+    const int64_t row_base = h->enc_g1 >= 0 ? rd.grow0[h->enc_g0] : 0;
+    for (int g = 0; g < G; ++g) {
+        pc.row0[g] = rd.grow0[g0 + g] - row_base;
+        pc.lanes[g] = rd.glanes[g0 + g];
+    }
+    pc.polarity = polarity;
+    pc.gbeg = h->enc_g1 >= 0 ? std::max(0, h->enc_g0 - g0) : 0;
+    pc.gend = h->enc_g1 >= 0 ? std::min(G, h->enc_g1 - g0) : G;
+    pc.sentinel = h->enc_sentinel ? 1 : 0;
+    if constexpr (sizeof(LW) == 4) {
+        const int need = (G + 7) / 8;  // groups per warp
+        const int gpw = need <= 1 ? 1 : need <= 2 ? 2 : need <= 4 ? 4 : 8;
+        const size_t smem = (size_t)8 * gpw * 32 * 32;
+        auto* fn = gpw == 1 ? k_encode_packed32<GW, 1> : gpw == 2 ? k_encode_packed32<GW, 2>
+                 : gpw == 4 ? k_encode_packed32<GW, 4> : k_encode_packed32<GW, 8>;
+        const int bit = 1 << (gpw + 8 * (int)(sizeof(GW) / 8));
+        if (!(h->enc_attr & bit)) {  // 64 KB of row stage at 8 groups per warp
+            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            h->enc_attr |= bit;
+        }
+        fn<<<grid, block, smem, h->st>>>(h->prows, pc, lane, agg);
     } else {
-        k_encode<LW, GW><<<grid, block, 0, h->est>>>(h->rows, ec, lane, agg);
+        if (h->enc_g1 >= 0) return fail(TSG_EINVAL, "group-range encode needs lane_width <= 32");
+        k_encode_packed<LW, GW><<<grid, block, 0, h->st>>>(h->prows, pc, lane, agg);
     }
     CK(cudaGetLastError());
     return TSG_OK;
 }
 
-// u64 words of one packed row: every 128-variable encoder block reads 4 words
-int64_t packed_words(int32_t V) { return round_up(((int64_t)V + 2 + 31) / 32, 4); }
-
 int do_encode(tsg_engine* h) {
-    for (int c = 0; c < h->rd.n_chunks; ++c) {
+    const RoundDesc& rd = h->rd;
+    for (int c = 0; c < rd.n_chunks; ++c) {
         int r;
         if (wide_lane(h)) r = wide_group(h) ? launch_encode<uint64_t, uint64_t>(h, c) : launch_encode<uint64_t, uint32_t>(h, c);
         else r = wide_group(h) ? launch_encode<uint32_t, uint64_t>(h, c) : launch_encode<uint32_t, uint32_t>(h, c);
         if (r) return r;
     }
+    if (rd.n_chunks > 1) {  // chunk-level aggregate over the chunks' tables
+        const uint8_t* slot = reinterpret_cast<const uint8_t*>(h->tables + h->tslot * h->slot_bytes);
+        auto* top = reinterpret_cast<AggEntry<uint32_t>*>(h->tables + h->tslot * h->slot_bytes + rd.top_off);
+        const int64_t nv2 = (int64_t)h->V + 2;
+        if (wide_group(h)) k_top<uint64_t><<<grid_for(nv2), 256, 0, h->st>>>(slot, rd.chunk_stride, rd.n_chunks, rd.per_bit, nv2, top);
+        else k_top<uint32_t><<<grid_for(nv2), 256, 0, h->st>>>(slot, rd.chunk_stride, rd.n_chunks, rd.per_bit, nv2, top);
+        CK(cudaGetLastError());
+    }
     return TSG_OK;
 }
 
-template <class LW, class GW, class TAB, int THREADS, int MINB>
-int launch_kernel(tsg_engine* h, const TestParams<LW, GW>& p, int64_t codes_bytes, int variant) {
-    auto* fn = k_test<LW, GW, TAB, THREADS, MINB>;
-    const size_t smem = test_smem_bytes<GW, TAB, THREADS>(codes_bytes);
-    const int key = (int)(sizeof(LW) / 8) * 8 + (int)(sizeof(GW) / 8) * 4 + variant;
-    if (h->grid_smem[key] != (int64_t)smem) {  // occupancy per kernel variant and smem size
-        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, THREADS, smem));
-        h->grid[key] = std::max(1, per_sm) * h->nsm;
-        h->grid_smem[key] = (int64_t)smem;
+// Tile table of the round: buckets in creation order, tiles of 32 slots.
+int build_desc(tsg_engine* h) {
+    if (!h->desc_dirty) return TSG_OK;  // store unchanged since the last round
+    h->h_desc.clear();
+    int64_t tiles = 0;
+    for (auto& b : h->buckets) {
+        if (!b.count) continue;
+        BucketDesc d{};
+        d.lits = b.lits; d.acts = b.acts; d.ids = b.ids;
+        d.size = b.size; d.rank = b.rank; d.count = b.count; d.tile0 = tiles;
+        tiles += (b.count + STRIDE - 1) / STRIDE;
+        h->h_desc.push_back(d);
     }
-    int64_t want = (h->n_tiles + THREADS / 32 - 1) / (THREADS / 32);
-    int grid = (int)std::min<int64_t>(want, h->grid[key]);
-    fn<<<grid, THREADS, smem, h->st>>>(p);
-    CK(cudaGetLastError());
+    h->n_tiles = tiles;
+    CKR(dgrow(h, &h->d_desc, &h->desc_cap, std::max<int64_t>(1, (int64_t)h->h_desc.size())));
+    if (!h->h_desc.empty()) {
+        CK(cudaMemcpyAsync(h->d_desc, h->h_desc.data(), h->h_desc.size() * sizeof(BucketDesc),
+                           cudaMemcpyHostToDevice, h->st));
+        CK(cudaStreamSynchronize(h->st));  // pageable source
+    }
+    h->desc_dirty = false;
     return TSG_OK;
 }
 
 template <class LW, class GW>
-int launch_slab(tsg_engine* h, const TestParams<LW, GW>& p) {
-    auto* fn = k_test_slab<LW, GW, TEST_THREADS_SLAB>;
-    const size_t smem = (size_t)3 * h->slab_w * sizeof(GW);
-    const int key = 16 + (int)(sizeof(LW) / 8) * 2 + (int)(sizeof(GW) / 8);
-    if (h->grid_smem[key] != (int64_t)smem) {
-        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, TEST_THREADS_SLAB, smem));
-        if (per_sm < 1) return fail(TSG_ECUDA, "slab kernel does not fit an SM (%zu B shared)", smem);
-        h->grid[key] = (int64_t)per_sm * h->nsm;
-        h->grid_smem[key] = (int64_t)smem;
-    }
-    if (h->h_sched.empty()) return TSG_OK;
-    int grid = (int)std::min<int64_t>(h->grid[key], (int64_t)h->h_sched.size());
-    fn<<<grid, TEST_THREADS_SLAB, smem, h->st>>>(p);
-    CK(cudaGetLastError());
-    return TSG_OK;
-}
-
-template <class LW, class GW>
-int launch_test(tsg_engine* h, int k, int c, double inc, int emit_only) {
-    const auto& R = h->rs[k];
+int launch_test(tsg_engine* h, int k, int emit_only) {
+    auto& R = h->rs[k];
     const RoundDesc& rd = R.fl;
-    const int slot = R.slot;
     TestParams<LW, GW> p{};
-    int32_t g0 = c * h->cfg.group_width;
-    int32_t G = std::min(h->cfg.group_width, rd.n_groups - g0);
-    const int8_t* tab = h->tables + slot * h->slot_bytes;
     p.buckets = h->d_desc;
     p.nb = (int32_t)h->h_desc.size();
-    p.G = G;
-    p.n_tiles = h->n_tiles;
-    p.agg = reinterpret_cast<const AggEntry<GW>*>(tab + rd.chunk_off[c]);
-    p.lane = reinterpret_cast<const LaneEntry<LW>*>(tab + rd.chunk_off[c] + agg_bytes(h));
+    p.n_tiles = (int32_t)h->n_tiles;
+    p.tables = reinterpret_cast<const uint8_t*>(h->tables + R.slot * h->slot_bytes);
+    p.chunk_stride = rd.chunk_stride;
+    p.lane_off = agg_bytes(h);
     p.vstride = vstride(h);
+    p.top = reinterpret_cast<const AggEntry<uint32_t>*>(p.tables + rd.top_off);
+    p.n_chunks = rd.n_chunks;
+    p.group_width = h->cfg.group_width;
+    p.n_groups = rd.n_groups;
+    p.per_bit = rd.per_bit;
     p.sentinel = h->V + 1;
-    p.g0 = g0;
-    p.group_mask = width_mask<GW>(G);
-    p.inc = inc;
-    p.out = h->out;
+    p.groups = R.d_groups;
+    p.inc = R.inc;
+    p.out = R.out;
+    p.out_cap = (unsigned long long)R.out_cap;
     p.ctr = R.ctr;
-    p.out_cap = h->out_cap;
-    p.carry = R.carry;
-    // carry stamps are unique per (round, run): a replay must not see the
-    // stamps its own round's first run left behind
-    p.stamp_base = (((R.seq << 6) | (R.run & 63)) & 0x7fffffff) << 32;
-    p.carry_in_tid = (c > 0 && rd.gtid[g0] == rd.gtid[g0 - 1]) ? rd.gtid[g0] : -1;
-    p.carry_out_tid = (g0 + G < rd.n_groups && rd.gtid[g0 + G - 1] == rd.gtid[g0 + G]) ? rd.gtid[g0 + G - 1] : -1;
+    p.pub = emit_only ? nullptr : R.h_ctr;
     p.emit_only = emit_only;
-    p.pub = (!emit_only && c == rd.n_chunks - 1) ? R.h_ctr : nullptr;
-    p.dyn_tiles = h->dyn_tiles ? 1 : 0;
     p.rec8 = R.rec8 ? 1 : 0;
-    p.tiles = R.tiles;
-    p.slab_tile0 = h->d_slab_tile0;
-    p.slab_desc0 = reinterpret_cast<const int32_t*>(h->d_slab_tile0 + (h->n_slabs + 1));
-    p.sched = reinterpret_cast<const uint64_t*>(h->d_slab_tile0 + 2 * (h->n_slabs + 1));
-    p.n_sched = (int32_t)h->h_sched.size();
-    p.slab_w = h->slab_w;
-    for (int g = 0; g < G; ++g) {
-        p.tid[g] = rd.gtid[g0 + g];
-        p.lane_mask[g] = width_mask<LW>(rd.glanes[g0 + g]);
+    p.all_pairs = R.all_pairs ? 1 : 0;
+    const bool multi = rd.n_chunks > 1;
+    auto* fn = multi ? k_test<LW, GW, true> : k_test<LW, GW, false>;
+    const int key = (int)(sizeof(LW) / 8) * 4 + (int)(sizeof(GW) / 8) * 2 + (multi ? 1 : 0);
+    if (!h->grid[key]) {  // persistent grid: as many CTAs as fit on every SM
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, TEST_THREADS, 0));
+        h->grid[key] = (int64_t)std::max(1, per_sm) * h->nsm;
     }
-    if (h->n_tiles == 0) return TSG_OK;
-    // shared-memory literal-code table when 2 * (V + 2) codes fit (G <= 32)
-    const int ew = G <= 8 ? 2 : (G <= 16 ? 4 : 8);
-    const int64_t codes_bytes = round_up(2 * ((int64_t)h->V + 2) * ew, 16);
-    if constexpr (sizeof(GW) == 4) {
-        if (h->smem_table && codes_bytes <= SMEM_TABLE_MAX) {
-            CKR(dgrow(h, &h->codes, &h->codes_cap, codes_bytes));
-            p.codes = h->codes;
-            p.codes_bytes = codes_bytes;
-            const auto* agg = reinterpret_cast<const AggEntry<uint32_t>*>(p.agg);
-            if (ew == 2) {
-                k_codes<uint16_t><<<grid_for(h->V + 2), 256, 0, h->st>>>(agg, h->V + 2, (uint16_t*)h->codes);
-                return launch_kernel<LW, GW, SmemTable<GW, uint16_t>, TEST_THREADS_SMEM, 1>(h, p, codes_bytes, 1);
-            }
-            if (ew == 4) {
-                k_codes<uint32_t><<<grid_for(h->V + 2), 256, 0, h->st>>>(agg, h->V + 2, (uint32_t*)h->codes);
-                return launch_kernel<LW, GW, SmemTable<GW, uint32_t>, TEST_THREADS_SMEM, 1>(h, p, codes_bytes, 2);
-            }
-            k_codes<uint64_t><<<grid_for(h->V + 2), 256, 0, h->st>>>(agg, h->V + 2, (uint64_t*)h->codes);
-            return launch_kernel<LW, GW, SmemTable<GW, uint64_t>, TEST_THREADS_SMEM, 1>(h, p, codes_bytes, 3);
-        }
-    }
-    if (h->slab_test && h->n_slabs > 1) return launch_slab<LW, GW>(h, p);
-    return launch_kernel<LW, GW, GlobalTable<GW>, TEST_THREADS, TSG_TEST_MIN_BLOCKS>(h, p, 0, 0);
+    const int64_t want = (h->n_tiles + TEST_THREADS / 32 - 1) / (TEST_THREADS / 32);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, h->grid[key]));
+    fn<<<grid, TEST_THREADS, 0, h->st>>>(p);
+    CK(cudaGetLastError());
+    return TSG_OK;
 }
 
-// the round of state k (its record buffers must be the active ones)
-int run_tests(tsg_engine* h, int k, double inc, int emit_only) {
-    for (int c = 0; c < h->rs[k].fl.n_chunks; ++c) {
-        int r;
-        if (wide_lane(h)) r = wide_group(h) ? launch_test<uint64_t, uint64_t>(h, k, c, inc, emit_only) : launch_test<uint64_t, uint32_t>(h, k, c, inc, emit_only);
-        else r = wide_group(h) ? launch_test<uint32_t, uint64_t>(h, k, c, inc, emit_only) : launch_test<uint32_t, uint32_t>(h, k, c, inc, emit_only);
-        if (r) return r;
-    }
-    return TSG_OK;
+// the round of state k
+int run_test(tsg_engine* h, int k, int emit_only) {
+    if (wide_lane(h)) return wide_group(h) ? launch_test<uint64_t, uint64_t>(h, k, emit_only) : launch_test<uint64_t, uint32_t>(h, k, emit_only);
+    return wide_group(h) ? launch_test<uint32_t, uint64_t>(h, k, emit_only) : launch_test<uint32_t, uint32_t>(h, k, emit_only);
 }
 
 int64_t store_size(const tsg_engine* h) {
     int64_t n = 0;
-    for (auto& b : h->buckets) n += b.count();
+    for (auto& b : h->buckets) n += b.count;
     return n;
-}
-
-// Tile table of the round: parts ordered slab-major (then bucket creation
-// order), so every slab's tiles are contiguous and a CTA of the slab kernel
-// loads each slab's table once.  Report order does not depend on it (the
-// host orders records by engine id, reports.py).
-int build_desc(tsg_engine* h) {
-    if (!h->desc_dirty) return TSG_OK;  // store unchanged since the last round
-    h->h_desc.clear();
-    h->h_slab_tile0.assign(h->n_slabs + 1, 0);
-    h->h_slab_desc0.assign(h->n_slabs + 1, 0);
-    int64_t tiles = 0;
-    for (int32_t s = 0; s < h->n_slabs; ++s) {
-        h->h_slab_tile0[s] = tiles;
-        h->h_slab_desc0[s] = (int32_t)h->h_desc.size();
-        for (auto& b : h->buckets) {
-            const Part& p = b.parts[s];
-            if (!p.count) continue;
-            BucketDesc d{};
-            d.lits = p.lits; d.acts = p.acts; d.ids = p.ids;
-            d.size = b.size; d.rank = b.rank; d.count = p.count; d.tile0 = tiles;
-            tiles += (p.count + STRIDE - 1) / STRIDE;
-            h->h_desc.push_back(d);
-        }
-    }
-    h->h_slab_tile0[h->n_slabs] = tiles;
-    h->h_slab_desc0[h->n_slabs] = (int32_t)h->h_desc.size();
-    h->n_tiles = tiles;
-    CKR(dgrow(h, &h->d_desc, &h->desc_cap, std::max<int64_t>(1, (int64_t)h->h_desc.size())));
-    if (!h->h_desc.empty())
-        CK(cudaMemcpyAsync(h->d_desc, h->h_desc.data(), h->h_desc.size() * sizeof(BucketDesc),
-                           cudaMemcpyHostToDevice, h->st));
-    // slab schedule for a grid of one CTA per SM: each slab gets CTAs in
-    // proportion to its tiles (largest remainder, at least one if it has any)
-    h->h_sched.clear();
-    {
-        const int64_t grid = h->nsm;
-        std::vector<int64_t> n(h->n_slabs, 0);
-        std::vector<std::pair<double, int>> rem;
-        int64_t used = 0, nonempty = 0;
-        for (int32_t s = 0; s < h->n_slabs; ++s) {
-            const int64_t t = h->h_slab_tile0[s + 1] - h->h_slab_tile0[s];
-            if (!t) continue;
-            ++nonempty;
-            const double share = tiles ? (double)grid * t / tiles : 0.0;
-            n[s] = std::max<int64_t>(1, (int64_t)share);
-            n[s] = std::min<int64_t>(n[s], std::max<int64_t>(1, (t + 7) / 8));  // >= 8 tiles per CTA
-            used += n[s];
-            rem.push_back({share - (double)n[s], s});
-        }
-        std::sort(rem.begin(), rem.end(), [](auto& x, auto& y) { return x.first > y.first || (x.first == y.first && x.second < y.second); });
-        for (auto& r : rem) {
-            if (used >= grid) break;
-            const int64_t t = h->h_slab_tile0[r.second + 1] - h->h_slab_tile0[r.second];
-            if (r.first > 0 && n[r.second] < std::max<int64_t>(1, (t + 7) / 8)) { n[r.second]++; used++; }
-        }
-        (void)nonempty;
-        for (int32_t s = 0; s < h->n_slabs; ++s)
-            for (int64_t k = 0; k < n[s]; ++k)
-                h->h_sched.push_back((uint64_t)s << 32 | (uint64_t)k << 16 | (uint64_t)n[s]);
-    }
-    const int64_t words = 2 * (int64_t)(h->n_slabs + 1) + (int64_t)h->h_sched.size() + 1;
-    CKR(dgrow(h, &h->d_slab_tile0, &h->slab_tile0_cap, words));
-    CK(cudaMemcpyAsync(h->d_slab_tile0, h->h_slab_tile0.data(), h->h_slab_tile0.size() * 8,
-                       cudaMemcpyHostToDevice, h->st));
-    CK(cudaMemcpyAsync(h->d_slab_tile0 + (h->n_slabs + 1), h->h_slab_desc0.data(), h->h_slab_desc0.size() * 4,
-                       cudaMemcpyHostToDevice, h->st));
-    if (!h->h_sched.empty())
-        CK(cudaMemcpyAsync(h->d_slab_tile0 + 2 * (h->n_slabs + 1), h->h_sched.data(), h->h_sched.size() * 8,
-                           cudaMemcpyHostToDevice, h->st));
-    // (pageable sources: the copies above have consumed the host vectors on return)
-    h->desc_dirty = false;
-    return TSG_OK;
 }
 
 int validate_handle(tsg_engine* h) {
@@ -621,89 +466,82 @@ int validate_handle(tsg_engine* h) {
     return TSG_OK;
 }
 
-// compact every part by keep flags laid out in for_parts order
-int compact_all(tsg_engine* h, const uint8_t* keep, const std::vector<int64_t>& base) {
-    int64_t* sel = nullptr;
-    int64_t* nsel = nullptr;
-    int64_t maxc = 0;
-    for_parts(h, [&](Bucket&, Part& p) { maxc = std::max(maxc, p.count); });
-    if (!maxc) return TSG_OK;
-    CKR(dalloc(h, (void**)&sel, maxc * 8));
-    CKR(dalloc(h, (void**)&nsel, 8));
-    size_t tmp_bytes = 0;
-    thrust::counting_iterator<int64_t> cnt(0);
-    cub::DeviceSelect::Flagged(nullptr, tmp_bytes, cnt, keep, sel, nsel, maxc, h->st);
-    void* tmp = nullptr;
-    CKR(dalloc(h, &tmp, (int64_t)tmp_bytes + 16));
-    size_t pi = 0;
-    for (auto& b : h->buckets) {
-        for (auto& p : b.parts) {
-            const int64_t pb = base[pi++];
-            if (!p.count) continue;
-            CK(cub::DeviceSelect::Flagged(tmp, tmp_bytes, cnt, keep + pb, sel, nsel, p.count, h->st));
-            int64_t kept = 0;
-            CK(cudaMemcpyAsync(&kept, nsel, 8, cudaMemcpyDeviceToHost, h->st));
-            CK(cudaStreamSynchronize(h->st));
-            if (kept == p.count) continue;
-            Part np;
-            np.slab = p.slab;
-            // keep capacity (the reference never shrinks, engine.py:184-200)
-            CKR(part_alloc(h, np, b.size, p.cap));
-            if (kept) {
-                k_compact<<<grid_for(kept), 256, 0, h->st>>>(sel, kept, b.size, p.lits, p.acts, p.ids, p.origins,
-                                                             p.order, np.lits, np.acts, np.ids, np.origins,
-                                                             np.order);
-                CK(cudaGetLastError());
-            }
-            part_free(h, p);
-            np.count = kept;
-            p = np;
-        }
+// Order-preserving compaction of every bucket by the flat keep array
+// (bucket b's slots at base[b], each bucket padded to KEEP_BLOCK; padding
+// keeps 0): K8 through k_keep_count / k_keep_select / k_compact.
+int compact_all(tsg_engine* h, const uint8_t* keep, const std::vector<int64_t>& base, int64_t flat) {
+    const int64_t nblk = flat / KEEP_BLOCK;
+    h->store_seq++;
+    if (!nblk) return TSG_OK;
+    int32_t* cnt = nullptr;
+    int64_t *off = nullptr, *sel = nullptr;
+    CKR(dalloc(h, (void**)&cnt, nblk * 4));
+    CKR(dalloc(h, (void**)&off, nblk * 8));
+    CKR(dalloc(h, (void**)&sel, flat * 8));
+    k_keep_count<<<(unsigned)nblk, KEEP_BLOCK, 0, h->st>>>(keep, cnt);
+    CK(cudaGetLastError());
+    std::vector<int32_t> hc(nblk);
+    CK(cudaMemcpyAsync(hc.data(), cnt, nblk * 4, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    std::vector<int64_t> ho(nblk);
+    int64_t acc = 0;
+    for (int64_t i = 0; i < nblk; ++i) { ho[i] = acc; acc += hc[i]; }
+    CK(cudaMemcpyAsync(off, ho.data(), nblk * 8, cudaMemcpyHostToDevice, h->st));
+    k_keep_select<<<(unsigned)nblk, KEEP_BLOCK, 0, h->st>>>(keep, off, sel);
+    CK(cudaGetLastError());
+    for (size_t bi = 0; bi < h->buckets.size(); ++bi) {
+        Bucket& b = h->buckets[bi];
+        if (!b.count) continue;
+        const int64_t blk0 = base[bi] / KEEP_BLOCK, blk1 = blk0 + (b.count + KEEP_BLOCK - 1) / KEEP_BLOCK;
+        int64_t kept = 0;
+        for (int64_t i = blk0; i < blk1; ++i) kept += hc[i];
+        if (kept == b.count) continue;
+        Bucket n = b;
+        CKR(bucket_alloc(h, n, b.cap));  // keep capacity (the reference never shrinks, engine.py:184-200)
+        if (kept)
+            k_compact<<<grid_for(kept), 256, 0, h->st>>>(sel + ho[blk0], base[bi], kept, b.size, b.lits, b.acts,
+                                                         b.ids, b.origins, b.order, n.lits, n.acts, n.ids,
+                                                         n.origins, n.order);
+        CK(cudaGetLastError());
+        bucket_free(h, b);
+        n.count = kept;
+        b = n;
     }
-    dfree(h, tmp); dfree(h, sel); dfree(h, nsel);
+    CK(cudaStreamSynchronize(h->st));  // ho is pageable
+    dfree(h, cnt); dfree(h, off); dfree(h, sel);
     return TSG_OK;
 }
 
-// per-part offsets into one flat keep-flag array (for_parts order)
-std::vector<int64_t> part_bases(tsg_engine* h, int64_t* total) {
+// per-bucket offsets into the flat maintenance arrays (KEEP_BLOCK-aligned)
+std::vector<int64_t> bucket_bases(tsg_engine* h, int64_t* flat) {
     std::vector<int64_t> base;
     int64_t acc = 0;
-    for_parts(h, [&](Bucket&, Part& p) { base.push_back(acc); acc += p.count; });
-    *total = acc;
+    for (auto& b : h->buckets) {
+        base.push_back(acc);
+        acc += round_up(b.count, KEEP_BLOCK);
+    }
+    *flat = acc;
     return base;
 }
 
-int32_t slab_of(const tsg_engine* h, int32_t lit) {
-    int64_t v = lit < 0 ? -(int64_t)lit : lit;
-    return (int32_t)std::min<int64_t>(v / h->slab_w, h->n_slabs - 1);
+void select_free(tsg_engine* h) {
+    auto& S = h->sel;
+    dfree(h, S.ka); dfree(h, S.ki); dfree(h, S.keep); dfree(h, S.hist);
+    S = tsg_engine::Select{};
 }
 
-// Placement of one clause.  Unpartitioned store: the pivot
-// -- the literal with the smallest variable among the first 58 -- goes first
-// (add_clauses orders each batch by pivot, so a warp's first gathers share
-// table lines), then the literals of the preferred polarity (those more
-// likely to be non-False under the recent rounds' assignments: they end the
-// early-exit recurrence sooner), then the rest.  Slab-partitioned store: the
-// literals of the chosen slab (the one holding most of them) go first.  The
-// order word lets readback restore the reference's literal order.
-int32_t place_clause(tsg_engine* h, const int32_t* lits, int32_t size, std::vector<int32_t>& cnt,
-                     int32_t* out, uint64_t* order) {
+// Placement of one clause: the pivot -- the literal with the
+// smallest variable among the first 58 -- goes first (add_clauses orders
+// each batch by pivot, so a warp's first gathers share table lines), then
+// the literals of the preferred polarity (those more likely to be non-False
+// under the recent rounds' assignments: they end the early-exit recurrence
+// sooner), then the rest.  The order word lets readback restore the
+// reference's literal order.
+void place_clause(const tsg_engine* h, const int32_t* lits, int32_t size, int32_t* out, uint64_t* order) {
     const int32_t lim = std::min(size, ORDER_MASK_BITS);
-    int32_t slab = 0, jp = -1;
+    int32_t jp = -1;
     uint64_t m = 0;
-    if (h->n_slabs > 1 && size > 0) {
-        for (int32_t j = 0; j < lim; ++j) cnt[slab_of(h, lits[j])]++;
-        int32_t best = -1;
-        for (int32_t j = 0; j < lim; ++j) {
-            int32_t s = slab_of(h, lits[j]);
-            if (best < 0 || cnt[s] > cnt[best] || (cnt[s] == cnt[best] && h->slab_load[s] < h->slab_load[best]))
-                best = s;
-        }
-        for (int32_t j = 0; j < lim; ++j) cnt[slab_of(h, lits[j])] = 0;
-        slab = best;
-        for (int32_t j = 0; j < lim; ++j)
-            if (slab_of(h, lits[j]) == slab) m |= 1ull << j;
-    } else if (h->pivot && lim > 0) {
+    if (h->pivot && lim > 0) {
         jp = 0;
         for (int32_t j = 1; j < lim; ++j)
             if (std::llabs((long long)lits[j]) < std::llabs((long long)lits[jp])) jp = j;
@@ -718,42 +556,6 @@ int32_t place_clause(tsg_engine* h, const int32_t* lits, int32_t size, std::vect
     for (int32_t j = 0; j < size; ++j)
         if (j != jp && (j >= lim || !((m >> j) & 1))) out[o++] = lits[j];
     *order = order_word(jp, m);
-    h->slab_load[slab]++;
-    return slab;
-}
-
-struct ValidReport {
-    __host__ __device__ bool operator()(const tsg_report& r) const { return r.key != REPORT_PAD; }
-};
-struct ValidRecord8 {
-    __host__ __device__ bool operator()(const uint64_t& r) const { return r != REPORT_PAD; }
-};
-
-// squeeze the padding slots out of the round's records (order-preserving)
-int compact_reports(tsg_engine* h) {
-    if (h->compacted) return TSG_OK;
-    // the compacted buffer becomes the round state's record buffer: it must
-    // not shrink below the current capacity, or the next round overflows
-    CKR(dgrow(h, &h->out2, &h->out2_cap, std::max<int64_t>(h->out_cap, 1)));
-    int64_t* nsel = nullptr;
-    CKR(dalloc(h, (void**)&nsel, 8));
-    size_t tb = 0;
-    const bool rec8 = h->rs[h->report_rs].rec8;
-    auto* o8 = reinterpret_cast<uint64_t*>(h->out);
-    auto* t8 = reinterpret_cast<uint64_t*>(h->out2);
-    if (rec8) cub::DeviceSelect::If(nullptr, tb, o8, t8, nsel, h->n_alloc, ValidRecord8(), h->st);
-    else cub::DeviceSelect::If(nullptr, tb, h->out, h->out2, nsel, h->n_alloc, ValidReport(), h->st);
-    void* tmp = nullptr;
-    CKR(dalloc(h, &tmp, (int64_t)tb + 16));
-    if (rec8) CK(cub::DeviceSelect::If(tmp, tb, o8, t8, nsel, h->n_alloc, ValidRecord8(), h->st));
-    else CK(cub::DeviceSelect::If(tmp, tb, h->out, h->out2, nsel, h->n_alloc, ValidReport(), h->st));
-    dfree(h, tmp);
-    dfree(h, nsel);
-    std::swap(h->out, h->out2);
-    std::swap(h->out_cap, h->out2_cap);
-    h->n_alloc = h->n_out;
-    h->compacted = true;
-    return TSG_OK;
 }
 
 }  // namespace
@@ -773,6 +575,8 @@ int tsg_device_count(int32_t* n) {
     return TSG_OK;
 }
 
+int tsg_destroy(tsg_engine* h);
+
 int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
     if (!out || !cfg) return fail(TSG_EINVAL, "null argument");
     *out = nullptr;
@@ -783,37 +587,12 @@ int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(TSG_ECUDA, "no CUDA device");
     if (cfg->device < 0 || cfg->device >= ndev) return fail(TSG_EINVAL, "device %d out of range (%d)", cfg->device, ndev);
     auto* h = new tsg_engine();
-    for (auto& x : h->grid_smem) x = -1;
     h->dev = cfg->device;
     h->cfg = *cfg;
     h->V = num_vars;
-    if (const char* e = getenv("TSG_SMEM_TABLE")) h->smem_table = atoi(e) != 0;
-    if (const char* e = getenv("TSG_DYN_TILES")) h->dyn_tiles = atoi(e) != 0;
-    if (const char* e = getenv("TSG_ASYNC_ENCODE")) h->async_encode = atoi(e) != 0;
-    if (const char* e = getenv("TSG_L2_PERSIST")) h->l2_persist = atoi(e) != 0;
+    h->all_pairs = (cfg->flags & TSG_F_ALL_PAIRS) != 0;
     if (const char* e = getenv("TSG_PIVOT")) h->pivot = atoi(e) != 0;
     if (const char* e = getenv("TSG_PREFER")) { h->prefer = atoi(e); h->prefer_fixed = true; }
-    // Variable slabs, opt-in: TSG_SLABS=1 partitions the store
-    // into as many slabs as one CTA's shared memory needs for the aggregate
-    // words, TSG_SLABS=n>1 into at least n.  Default: one slab (unpartitioned
-    // store, global-table kernel), the faster layout measured on B200.
-    {
-        const int64_t per_var = 3 * (h->cfg.group_width > 32 ? 8 : 4);
-        const int64_t nv2 = (int64_t)num_vars + 2;
-        int64_t slab_bytes = SLAB_SMEM_BYTES;
-        if (const char* e = getenv("TSG_SLAB_BYTES")) slab_bytes = std::min<int64_t>(SLAB_SMEM_BYTES, atol(e));
-        const int64_t max_w = std::max<int64_t>(32, (slab_bytes / per_var) / 32 * 32);
-        int64_t ns = 1;
-        if (const char* e = getenv("TSG_SLABS")) {
-            const int req = atoi(e);
-            if (req >= 1) ns = std::max<int64_t>((nv2 + max_w - 1) / max_w, req);
-        }
-        if (ns <= 1) h->slab_test = false;
-        int64_t w = round_up((nv2 + ns - 1) / ns, 32);
-        h->n_slabs = (int32_t)((nv2 + w - 1) / w);
-        h->slab_w = (int32_t)w;
-        h->slab_load.assign(h->n_slabs, 0);
-    }
     DevGuard g(h->dev);
     cudaDeviceProp prop;
     if (cudaGetDeviceProperties(&prop, h->dev) != cudaSuccess) { delete h; return fail(TSG_ECUDA, "device properties"); }
@@ -824,35 +603,32 @@ int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
         uint64_t thr = UINT64_MAX;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
-    cudaStreamCreateWithFlags(&h->egress, cudaStreamNonBlocking);
-    cudaStreamCreateWithFlags(&h->ingress, cudaStreamNonBlocking);
-    cudaStreamCreateWithFlags(&h->enc_st, cudaStreamNonBlocking);
-    cudaEventCreateWithFlags(&h->ev_main, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&h->ev_encoded, cudaEventDisableTiming);
-    h->est = h->st;
-    for (int b = 0; b < 2; ++b) {
-        cudaEventCreateWithFlags(&h->ev_staged[b], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&h->ev_read[b], cudaEventDisableTiming);
-    }
-    cudaEventCreateWithFlags(&h->ev_cur, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&h->alt.ev, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&h->ev_ready, cudaEventDisableTiming);
+    bool ok = cudaStreamCreateWithFlags(&h->egress, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&h->ingress, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaEventCreateWithFlags(&h->ev_ready, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&h->ev_peer, cudaEventDisableTiming) == cudaSuccess;
+    for (int b = 0; b < 2; ++b)
+        ok = ok && cudaEventCreateWithFlags(&h->ev_staged[b], cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&h->ev_read[b], cudaEventDisableTiming) == cudaSuccess;
     for (int sl = 0; sl < 2; ++sl)
-        for (int k = 0; k < 2; ++k) cudaEventCreate(&h->ev_enc[sl][k]);
+        for (int k = 0; k < 2; ++k) ok = ok && cudaEventCreate(&h->ev_enc[sl][k]) == cudaSuccess;
+    const int64_t cap0 = cfg->report_capacity > 0 ? cfg->report_capacity : (1 << 16);
     for (auto& R : h->rs) {
-        cudaEventCreateWithFlags(&R.ev_done, cudaEventDisableTiming);
-        for (auto& e : R.ev_tst) cudaEventCreate(&e);
-        if (cudaMallocHost(&R.h_ctr, 8 * sizeof(unsigned long long)) != cudaSuccess) { delete h; return fail(TSG_ECUDA, "pinned alloc"); }
-        if (dalloc(h, (void**)&R.ctr, 8 * sizeof(unsigned long long))) { delete h; return TSG_ENOMEM; }
-        if (cudaMemsetAsync(R.ctr, 0, 8 * sizeof(unsigned long long), h->st) != cudaSuccess) { delete h; return fail(TSG_ECUDA, "memset"); }
-        const int64_t tb = (int64_t)TSG_DYN_NC * DYN_STRIDE * sizeof(unsigned long long);
-        if (dalloc(h, (void**)&R.tiles, tb)) { delete h; return TSG_ENOMEM; }
-        if (cudaMemsetAsync(R.tiles, 0, tb, h->st) != cudaSuccess) { delete h; return fail(TSG_ECUDA, "memset"); }
+        ok = ok && cudaEventCreateWithFlags(&R.ev_done, cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&R.ev_copied, cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreate(&R.ev_tst[0]) == cudaSuccess && cudaEventCreate(&R.ev_tst[1]) == cudaSuccess &&
+             cudaMallocHost(&R.h_ctr, 8 * sizeof(unsigned long long)) == cudaSuccess &&
+             dalloc(h, (void**)&R.ctr, 8 * sizeof(unsigned long long)) == TSG_OK &&
+             cudaMemsetAsync(R.ctr, 0, 8 * sizeof(unsigned long long), h->st) == cudaSuccess &&
+             dalloc(h, (void**)&R.out, cap0 * (int64_t)sizeof(tsg_report)) == TSG_OK;
+        R.out_cap = cap0;
     }
-    if (cudaMallocHost(&h->h_mctr, 8 * sizeof(unsigned long long)) != cudaSuccess) { delete h; return fail(TSG_ECUDA, "pinned alloc"); }
-    if (dalloc(h, (void**)&h->mctr, 8 * sizeof(unsigned long long))) { delete h; return TSG_ENOMEM; }
-    h->out_cap = cfg->report_capacity > 0 ? std::min<int64_t>(cfg->report_capacity, INT32_MAX / 2) : (1 << 16);
-    if (dalloc(h, (void**)&h->out, h->out_cap * (int64_t)sizeof(tsg_report))) { delete h; return TSG_ENOMEM; }
+    ok = ok && cudaMallocHost(&h->h_mctr, 8 * sizeof(unsigned long long)) == cudaSuccess &&
+         dalloc(h, (void**)&h->mctr, 8 * sizeof(unsigned long long)) == TSG_OK;
+    if (!ok) {
+        tsg_destroy(h);
+        return fail(TSG_ECUDA, "engine resources could not be created");
+    }
     *out = h;
     return TSG_OK;
 }
@@ -860,36 +636,34 @@ int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
 int tsg_destroy(tsg_engine* h) {
     if (!h) return TSG_OK;
     DevGuard g(h->dev);
-    if (h->enc_st) cudaStreamSynchronize(h->enc_st);
-    cudaStreamSynchronize(h->st);
-    for_parts(h, [&](Bucket&, Part& p) { part_free(h, p); });
-    dfree(h, h->d_slab_tile0);
+    if (h->st) select_free(h);
+    if (h->st) cudaStreamSynchronize(h->st);
     if (h->ingress) cudaStreamSynchronize(h->ingress);
-    dfree(h, h->rows_own); dfree(h, h->pbuf[0]); dfree(h, h->pbuf[1]); dfree(h, h->tables); dfree(h, h->d_desc); dfree(h, h->out);
-    dfree(h, h->mctr); dfree(h, h->out2); dfree(h, h->codes);
-    for (auto& R : h->rs) { dfree(h, R.ctr); dfree(h, R.carry); dfree(h, R.tiles); }
     if (h->egress) cudaStreamSynchronize(h->egress);
-    dfree(h, h->alt.out); dfree(h, h->alt.out2); dfree(h, h->alt.out12); dfree(h, h->out12);
-    cudaStreamSynchronize(h->st);
+    if (h->st) {
+        for (auto& b : h->buckets) bucket_free(h, b);
+        dfree(h, h->rows_own); dfree(h, h->pbuf[0]); dfree(h, h->pbuf[1]); dfree(h, h->tables); dfree(h, h->d_desc);
+        dfree(h, h->mctr);
+        for (auto& R : h->rs) { dfree(h, R.ctr); dfree(h, R.out); dfree(h, R.out12); dfree(h, R.d_groups); }
+        cudaStreamSynchronize(h->st);
+    }
     if (h->h_mctr) cudaFreeHost(h->h_mctr);
-    for (cudaEvent_t e : {h->ev_cur, h->alt.ev, h->ev_ready}) if (e) cudaEventDestroy(e);
     for (auto& R : h->rs) {
         if (R.h_ctr) cudaFreeHost(R.h_ctr);
-        if (R.ev_done) cudaEventDestroy(R.ev_done);
-        for (auto& e : R.ev_tst) if (e) cudaEventDestroy(e);
+        if (R.h_groups) cudaFreeHost(R.h_groups);
+        for (cudaEvent_t e : {R.ev_done, R.ev_copied, R.ev_tst[0], R.ev_tst[1]}) if (e) cudaEventDestroy(e);
     }
     for (int sl = 0; sl < 2; ++sl)
         for (int k = 0; k < 2; ++k)
             if (h->ev_enc[sl][k]) cudaEventDestroy(h->ev_enc[sl][k]);
-    if (h->egress) cudaStreamDestroy(h->egress);
     for (int b = 0; b < 2; ++b) {
         if (h->ev_staged[b]) cudaEventDestroy(h->ev_staged[b]);
         if (h->ev_read[b]) cudaEventDestroy(h->ev_read[b]);
     }
+    for (cudaEvent_t e : {h->ev_ready, h->ev_peer}) if (e) cudaEventDestroy(e);
+    if (h->egress) cudaStreamDestroy(h->egress);
     if (h->ingress) cudaStreamDestroy(h->ingress);
-    if (h->enc_st) cudaStreamDestroy(h->enc_st);
-    for (cudaEvent_t e : {h->ev_main, h->ev_encoded}) if (e) cudaEventDestroy(e);
-    cudaStreamDestroy(h->st);
+    if (h->st) cudaStreamDestroy(h->st);
     delete h;
     return TSG_OK;
 }
@@ -898,53 +672,49 @@ int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, 
                     const int64_t* ids, const int32_t* origins, double activity) {
     CKR(validate_handle(h));
     if (any_inflight(h)) return fail(TSG_EINVAL, "the store cannot change while a launched round is not collected");
-    h->desc_dirty = true;
     if (n <= 0) return TSG_OK;
     if (!offsets || !ids || !origins) return fail(TSG_EINVAL, "null argument");
+    // validate the whole batch before any state changes
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t s64 = offsets[i + 1] - offsets[i];
+        if (s64 < 0 || s64 > (1 << 24)) return fail(TSG_EINVAL, "bad clause size at clause %lld", (long long)i);
+    }
+    if (offsets[n] > offsets[0] && !lits) return fail(TSG_EINVAL, "null literals");
     DevGuard g(h->dev);
+    h->desc_dirty = true;
+    h->store_seq++;
     // group clauses by size, preserving arrival order; new sizes create buckets
     // in first-seen order (dict insertion order of ClauseStore.buckets)
     std::vector<int> bucket_of(n);
     for (int64_t i = 0; i < n; ++i) {
-        int64_t s64 = offsets[i + 1] - offsets[i];
-        if (s64 < 0 || s64 > (1 << 24)) return fail(TSG_EINVAL, "bad clause size");
-        int32_t s = (int32_t)s64;
+        const int32_t s = (int32_t)(offsets[i + 1] - offsets[i]);
         for (int64_t j = offsets[i]; j < offsets[i + 1]; ++j) {
-            int64_t v = lits[j] < 0 ? -(int64_t)lits[j] : lits[j];
+            const int64_t v = lits[j] < 0 ? -(int64_t)lits[j] : lits[j];
             if (v > h->V) h->oob = true;  // stored as-is; testing raises (numpy IndexError, engine.py:251)
         }
         if (ids[i] < 0 || ids[i] > h->max_id) h->max_id = std::max<int64_t>(h->max_id, ids[i] < 0 ? INT64_MAX : ids[i]);
         auto it = h->by_size.find(s);
-        int bi;
         if (it == h->by_size.end()) {
-            bi = (int)h->buckets.size();
             Bucket b;
             b.size = s;
-            b.rank = bi;
-            b.parts.resize(h->n_slabs);
-            for (int32_t q = 0; q < h->n_slabs; ++q) b.parts[q].slab = q;
+            b.rank = (int32_t)h->buckets.size();
+            h->by_size[s] = (int)h->buckets.size();
+            bucket_of[i] = (int)h->buckets.size();
             h->buckets.push_back(b);
-            h->by_size[s] = bi;
         } else {
-            bi = it->second;
+            bucket_of[i] = it->second;
         }
-        bucket_of[i] = bi;
     }
-    // place every clause in a slab part (hot literals first), then one H2D +
-    // scatter per (bucket, slab) part
-    const int32_t P = h->n_slabs;
-    std::vector<int32_t> cnt(P, 0);
+    // place every clause (pivot first), then one H2D + scatter per bucket
     std::vector<int32_t> placed((size_t)std::max<int64_t>(offsets[n] - offsets[0], 1));
     std::vector<uint64_t> hm(n);
-    std::vector<int32_t> slab_of_clause(n);
-    std::vector<std::vector<int64_t>> members(h->buckets.size() * P);
+    std::vector<std::vector<int64_t>> members(h->buckets.size());
     for (int64_t i = 0; i < n; ++i) {
         const int32_t s = (int32_t)(offsets[i + 1] - offsets[i]);
-        slab_of_clause[i] = place_clause(h, lits + offsets[i], s, cnt, placed.data() + (offsets[i] - offsets[0]),
-                                         &hm[i]);
-        members[(size_t)bucket_of[i] * P + slab_of_clause[i]].push_back(i);
+        place_clause(h, lits + offsets[i], s, placed.data() + (offsets[i] - offsets[0]), &hm[i]);
+        members[bucket_of[i]].push_back(i);
     }
-    if (h->pivot && P == 1) {  // each part's new clauses in pivot-variable order (stable)
+    if (h->pivot) {  // each bucket's new clauses in pivot-variable order (stable)
         for (auto& mem : members)
             std::stable_sort(mem.begin(), mem.end(), [&](int64_t x, int64_t y) {
                 const int64_t sx = offsets[x + 1] - offsets[x], sy = offsets[y + 1] - offsets[y];
@@ -953,19 +723,18 @@ int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, 
                 return vx < vy;
             });
     }
-    for (size_t mi = 0; mi < members.size(); ++mi) {
-        auto& mem = members[mi];
+    for (size_t bi = 0; bi < members.size(); ++bi) {
+        auto& mem = members[bi];
         if (mem.empty()) continue;
-        Bucket& b = h->buckets[mi / P];
-        Part& p = b.parts[mi % P];
-        int64_t k = (int64_t)mem.size();
-        CKR(part_reserve(h, p, b.size, p.count + k));
+        Bucket& b = h->buckets[bi];
+        const int64_t k = (int64_t)mem.size();
+        CKR(bucket_reserve(h, b, b.count + k));
         std::vector<int32_t> hl((size_t)(k * b.size));
         std::vector<int64_t> hid(k);
         std::vector<int32_t> hor(k);
         std::vector<uint64_t> hmk(k);
         for (int64_t c = 0; c < k; ++c) {
-            int64_t i = mem[c];
+            const int64_t i = mem[c];
             if (b.size) memcpy(&hl[c * b.size], placed.data() + (offsets[i] - offsets[0]), b.size * 4);
             hid[c] = ids[i];
             hor[c] = origins[i];
@@ -975,16 +744,16 @@ int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, 
             int32_t* tmp = nullptr;
             CKR(dalloc(h, (void**)&tmp, k * b.size * 4));
             CK(cudaMemcpyAsync(tmp, hl.data(), k * b.size * 4, cudaMemcpyHostToDevice, h->st));
-            k_append<<<grid_for(k * b.size), 256, 0, h->st>>>(tmp, k, b.size, p.count, p.lits);
+            k_append<<<grid_for(k * b.size), 256, 0, h->st>>>(tmp, k, b.size, b.count, b.lits);
             CK(cudaGetLastError());
             dfree(h, tmp);
         }
-        CK(cudaMemcpyAsync(p.ids + p.count, hid.data(), k * 8, cudaMemcpyHostToDevice, h->st));
-        CK(cudaMemcpyAsync(p.origins + p.count, hor.data(), k * 4, cudaMemcpyHostToDevice, h->st));
-        CK(cudaMemcpyAsync(p.order + p.count, hmk.data(), k * 8, cudaMemcpyHostToDevice, h->st));
-        k_fill_f64<<<grid_for(k), 256, 0, h->st>>>(p.acts + p.count, k, activity);
+        CK(cudaMemcpyAsync(b.ids + b.count, hid.data(), k * 8, cudaMemcpyHostToDevice, h->st));
+        CK(cudaMemcpyAsync(b.origins + b.count, hor.data(), k * 4, cudaMemcpyHostToDevice, h->st));
+        CK(cudaMemcpyAsync(b.order + b.count, hmk.data(), k * 8, cudaMemcpyHostToDevice, h->st));
+        k_fill_f64<<<grid_for(k), 256, 0, h->st>>>(b.acts + b.count, k, activity);
         CK(cudaGetLastError());
-        p.count += k;
+        b.count += k;
         CK(cudaStreamSynchronize(h->st));  // host vectors go out of scope
     }
     h->totals.clauses_added += n;
@@ -1007,7 +776,7 @@ int tsg_bucket_info(tsg_engine* h, int32_t b, int32_t* size, int64_t* count) {
     CKR(validate_handle(h));
     if (b < 0 || b >= (int32_t)h->buckets.size()) return fail(TSG_ERANGE, "bucket %d out of range", b);
     *size = h->buckets[b].size;
-    *count = h->buckets[b].count();
+    *count = h->buckets[b].count;
     return TSG_OK;
 }
 
@@ -1016,30 +785,25 @@ int tsg_bucket_read(tsg_engine* h, int32_t bi, int32_t* lits, int64_t* ids, int3
     if (bi < 0 || bi >= (int32_t)h->buckets.size()) return fail(TSG_ERANGE, "bucket %d out of range", bi);
     DevGuard g(h->dev);
     Bucket& b = h->buckets[bi];
-    const int64_t total = b.count();
+    const int64_t total = b.count;
     if (!total) return TSG_OK;
-    // every part in its own slot order (original literal order restored), then
-    // merged by engine id = the reference's slot order (reports.py)
+    // slot order (original literal order restored), then sorted by engine id
+    // = the reference's slot order (reports.py)
     std::vector<int32_t> hl(lits && b.size ? total * b.size : 0);
     std::vector<int64_t> hid(total);
     std::vector<int32_t> hor(origins ? total : 0);
     std::vector<double> hac(acts ? total : 0);
-    int64_t off = 0;
-    for (auto& p : b.parts) {
-        if (!p.count) continue;
-        if (lits && b.size) {
-            int32_t* tmp = nullptr;
-            CKR(dalloc(h, (void**)&tmp, p.count * b.size * 4));
-            k_deinterleave<<<grid_for(p.count), 256, 0, h->st>>>(p.lits, p.order, p.count, b.size, tmp);
-            CK(cudaGetLastError());
-            CK(cudaMemcpyAsync(hl.data() + off * b.size, tmp, p.count * b.size * 4, cudaMemcpyDeviceToHost, h->st));
-            dfree(h, tmp);
-        }
-        CK(cudaMemcpyAsync(hid.data() + off, p.ids, p.count * 8, cudaMemcpyDeviceToHost, h->st));
-        if (origins) CK(cudaMemcpyAsync(hor.data() + off, p.origins, p.count * 4, cudaMemcpyDeviceToHost, h->st));
-        if (acts) CK(cudaMemcpyAsync(hac.data() + off, p.acts, p.count * 8, cudaMemcpyDeviceToHost, h->st));
-        off += p.count;
+    if (lits && b.size) {
+        int32_t* tmp = nullptr;
+        CKR(dalloc(h, (void**)&tmp, total * b.size * 4));
+        k_deinterleave<<<grid_for(total), 256, 0, h->st>>>(b.lits, b.order, total, b.size, tmp);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(hl.data(), tmp, total * b.size * 4, cudaMemcpyDeviceToHost, h->st));
+        dfree(h, tmp);
     }
+    CK(cudaMemcpyAsync(hid.data(), b.ids, total * 8, cudaMemcpyDeviceToHost, h->st));
+    if (origins) CK(cudaMemcpyAsync(hor.data(), b.origins, total * 4, cudaMemcpyDeviceToHost, h->st));
+    if (acts) CK(cudaMemcpyAsync(hac.data(), b.acts, total * 8, cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
     std::vector<int64_t> ord(total);
     for (int64_t i = 0; i < total; ++i) ord[i] = i;
@@ -1069,19 +833,14 @@ int tsg_get_clauses(tsg_engine* h, const int64_t* ids, int64_t n, int32_t* sizes
     std::sort(qi.begin(), qi.end(), [&](int64_t a, int64_t b) { return ids[a] < ids[b]; });
     std::vector<int64_t> q(n);
     for (int64_t i = 0; i < n; ++i) q[i] = ids[qi[i]];
-    // parts in a flat list: part index -> (bucket, part)
-    std::vector<std::pair<int, int>> parts;
-    for (int bi = 0; bi < (int)h->buckets.size(); ++bi)
-        for (int pi = 0; pi < (int)h->buckets[bi].parts.size(); ++pi)
-            if (h->buckets[bi].parts[pi].count) parts.push_back({bi, pi});
     int64_t* d = nullptr;  // [q | qidx | loc]
     CKR(dalloc(h, (void**)&d, 3 * n * 8));
     CK(cudaMemcpyAsync(d, q.data(), n * 8, cudaMemcpyHostToDevice, h->st));
     CK(cudaMemcpyAsync(d + n, qi.data(), n * 8, cudaMemcpyHostToDevice, h->st));
     CK(cudaMemsetAsync(d + 2 * n, 0xFF, n * 8, h->st));
-    for (int64_t k = 0; k < (int64_t)parts.size(); ++k) {
-        const Part& p = h->buckets[parts[k].first].parts[parts[k].second];
-        k_find_ids<<<grid_for(p.count), 256, 0, h->st>>>(p.ids, p.count, d, d + n, n, k, d + 2 * n);
+    for (int64_t k = 0; k < (int64_t)h->buckets.size(); ++k) {
+        const Bucket& b = h->buckets[k];
+        if (b.count) k_find_ids<<<grid_for(b.count), 256, 0, h->st>>>(b.ids, b.count, d, d + n, n, k, d + 2 * n);
     }
     CK(cudaGetLastError());
     std::vector<int64_t> loc(n);
@@ -1091,24 +850,22 @@ int tsg_get_clauses(tsg_engine* h, const int64_t* ids, int64_t n, int32_t* sizes
     int64_t total = 0;
     std::vector<int64_t> off(n);
     for (int64_t i = 0; i < n; ++i) {
-        if (loc[i] < 0) { sizes[i] = -1; off[i] = total; continue; }
-        sizes[i] = h->buckets[parts[loc[i] >> 40].first].size;
         off[i] = total;
+        if (loc[i] < 0) { sizes[i] = -1; continue; }
+        sizes[i] = h->buckets[loc[i] >> 40].size;
         total += sizes[i];
     }
     *n_lits = total;
     if (!lits || total == 0) return TSG_OK;
     if (total > lits_cap) return fail(TSG_ECAPACITY, "%lld literals do not fit %lld", (long long)total, (long long)lits_cap);
-    // per part: gather its hits' literals, then place them in request order
-    std::vector<std::vector<int64_t>> hit(parts.size());
+    // per bucket: gather its hits' literals, then place them in request order
+    std::vector<std::vector<int64_t>> hit(h->buckets.size());
     for (int64_t i = 0; i < n; ++i)
         if (loc[i] >= 0) hit[loc[i] >> 40].push_back(i);
-    for (size_t k = 0; k < parts.size(); ++k) {
-        if (hit[k].empty()) continue;
-        const Bucket& b = h->buckets[parts[k].first];
-        const Part& p = b.parts[parts[k].second];
+    for (size_t k = 0; k < h->buckets.size(); ++k) {
+        const Bucket& b = h->buckets[k];
         const int64_t m = (int64_t)hit[k].size();
-        if (b.size == 0) continue;
+        if (!m || b.size == 0) continue;
         std::vector<int64_t> slots(m);
         for (int64_t j = 0; j < m; ++j) slots[j] = loc[hit[k][j]] & ((int64_t(1) << 40) - 1);
         int64_t* ds = nullptr;
@@ -1116,7 +873,7 @@ int tsg_get_clauses(tsg_engine* h, const int64_t* ids, int64_t n, int32_t* sizes
         CKR(dalloc(h, (void**)&ds, m * 8));
         CKR(dalloc(h, (void**)&dl, m * b.size * 4));
         CK(cudaMemcpyAsync(ds, slots.data(), m * 8, cudaMemcpyHostToDevice, h->st));
-        k_deinterleave_sel<<<grid_for(m), 256, 0, h->st>>>(p.lits, p.order, ds, m, b.size, dl);
+        k_deinterleave_sel<<<grid_for(m), 256, 0, h->st>>>(b.lits, b.order, ds, m, b.size, dl);
         CK(cudaGetLastError());
         std::vector<int32_t> hl(m * b.size);
         CK(cudaMemcpyAsync(hl.data(), dl, m * b.size * 4, cudaMemcpyDeviceToHost, h->st));
@@ -1135,6 +892,12 @@ int tsg_set_timing(tsg_engine* h, int32_t every) {
     return TSG_OK;
 }
 
+int tsg_set_all_pairs(tsg_engine* h, int32_t on) {
+    CKR(validate_handle(h));
+    h->all_pairs = on != 0;
+    return TSG_OK;
+}
+
 int tsg_counters(tsg_engine* h, tsg_counters_t* out) {
     CKR(validate_handle(h));
     if (!out) return fail(TSG_EINVAL, "null argument");
@@ -1146,64 +909,102 @@ int tsg_scale_activities(tsg_engine* h, double factor) {
     CKR(validate_handle(h));
     if (any_inflight(h)) return fail(TSG_EINVAL, "the store cannot change while a launched round is not collected");
     DevGuard g(h->dev);
-    for_parts(h, [&](Bucket&, Part& p) {
-        if (p.count) k_scale_f64<<<grid_for(p.count), 256, 0, h->st>>>(p.acts, p.count, factor);
-    });
+    for (auto& b : h->buckets)
+        if (b.count) k_scale_f64<<<grid_for(b.count), 256, 0, h->st>>>(b.acts, b.count, factor);
     CK(cudaGetLastError());
     return TSG_OK;
 }
 
-int tsg_reduce(tsg_engine* h, int64_t eligible_below, int64_t target, int64_t* removed, int64_t* removed_ids) {
+// reduce_store (engine.py:469-505) as a radix select on the 128-bit key
+// (activity bits, engine id), split so that several stores (clause shards
+// on several GPUs) can select their global `target` smallest keys exactly:
+// begin builds the keys of the eligible clauses (id < eligible_below,
+// engine.py:486); hist counts, per value of the next 8 key bits, the
+// eligible keys whose top `bits` bits equal the prefix -- the caller sums
+// the shards' histograms and steers the prefix; commit removes every
+// eligible key whose top `bits` bits are <= the prefix (order-preserving
+// compaction, engine.py:184-200).  tsg_reduce runs the loop for one store.
+int tsg_reduce_begin(tsg_engine* h, int64_t eligible_below, int64_t* n_eligible) {
     CKR(validate_handle(h));
+    if (!n_eligible) return fail(TSG_EINVAL, "null argument");
     if (any_inflight(h)) return fail(TSG_EINVAL, "the store cannot change while a launched round is not collected");
-    h->desc_dirty = true;
+    DevGuard g(h->dev);
+    select_free(h);
+    auto& S = h->sel;
+    S.base = bucket_bases(h, &S.flat);
+    *n_eligible = 0;
+    if (S.flat == 0) { S.open = true; S.store_seq = h->store_seq; return TSG_OK; }
+    CKR(dalloc(h, (void**)&S.ka, S.flat * 8));
+    CKR(dalloc(h, (void**)&S.ki, S.flat * 8));
+    CKR(dalloc(h, (void**)&S.keep, S.flat));
+    CKR(dalloc(h, (void**)&S.hist, 256 * 8));
+    CK(cudaMemsetAsync(S.ka, 0xFF, S.flat * 8, h->st));  // padding: NO_KEY
+    CK(cudaMemsetAsync(S.keep, 0, S.flat, h->st));
+    CK(cudaMemsetAsync(h->mctr + 4, 0, 8, h->st));
+    for (size_t bi = 0; bi < h->buckets.size(); ++bi) {
+        const Bucket& b = h->buckets[bi];
+        if (b.count)
+            k_reduce_keys<<<grid_for(b.count), 256, 0, h->st>>>(b.acts, b.ids, b.count, S.base[bi], eligible_below,
+                                                                S.ka, S.ki, S.keep, h->mctr + 4);
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h->h_mctr + 4, h->mctr + 4, 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    S.n_eligible = (int64_t)h->h_mctr[4];
+    S.open = true;
+    S.store_seq = h->store_seq;
+    *n_eligible = S.n_eligible;
+    return TSG_OK;
+}
+
+int tsg_reduce_hist(tsg_engine* h, uint64_t prefix_hi, uint64_t prefix_lo, int32_t bits, uint64_t* hist) {
+    CKR(validate_handle(h));
+    auto& S = h->sel;
+    if (!S.open || S.store_seq != h->store_seq) return fail(TSG_EINVAL, "no reduce selection open on this store");
+    if (bits < 0 || bits > 120 || bits % 8 || !hist) return fail(TSG_EINVAL, "bad prefix length %d", bits);
+    if (S.flat == 0) { memset(hist, 0, 256 * 8); return TSG_OK; }
+    DevGuard g(h->dev);
+    CK(cudaMemsetAsync(S.hist, 0, 256 * 8, h->st));
+    k_select_hist<<<grid_for(S.flat), 256, 0, h->st>>>(S.ka, S.ki, S.flat, prefix_hi, prefix_lo, bits, S.hist);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(hist, S.hist, 256 * 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    return TSG_OK;
+}
+
+int tsg_reduce_commit(tsg_engine* h, uint64_t prefix_hi, uint64_t prefix_lo, int32_t bits, int64_t* removed,
+                      int64_t* removed_ids, int64_t cap) {
+    CKR(validate_handle(h));
+    if (!removed) return fail(TSG_EINVAL, "null argument");
+    auto& S = h->sel;
+    if (!S.open || S.store_seq != h->store_seq) return fail(TSG_EINVAL, "no reduce selection open on this store");
+    if (bits < 0 || bits > 128 || bits % 8) return fail(TSG_EINVAL, "bad prefix length %d", bits);
     DevGuard g(h->dev);
     *removed = 0;
-    int64_t total = 0;
-    std::vector<int64_t> base = part_bases(h, &total);
-    if (total == 0 || target <= 0) return TSG_OK;
-    uint64_t *ka = nullptr, *ki = nullptr, *ka2 = nullptr, *ki2 = nullptr;
-    int64_t *ix = nullptr, *ix2 = nullptr, *doomed_ids = nullptr;
-    uint8_t* keep = nullptr;
-    CKR(dalloc(h, (void**)&ka, total * 8)); CKR(dalloc(h, (void**)&ki, total * 8));
-    CKR(dalloc(h, (void**)&ka2, total * 8)); CKR(dalloc(h, (void**)&ki2, total * 8));
-    CKR(dalloc(h, (void**)&ix, total * 8)); CKR(dalloc(h, (void**)&ix2, total * 8));
-    CKR(dalloc(h, (void**)&keep, total));
-    CK(cudaMemsetAsync(h->mctr + 4, 0, 8, h->st));
-    {
-        size_t pi = 0;
-        for_parts(h, [&](Bucket&, Part& p) {
-            const int64_t pb = base[pi++];
-            if (p.count)
-                k_reduce_keys<<<grid_for(p.count), 256, 0, h->st>>>(p.acts, p.ids, p.count, pb, eligible_below,
-                                                                    ka, ki, ix, h->mctr + 4);
-        });
-    }
-    CK(cudaGetLastError());
-    // stable LSD: sort by id, then stably by activity bits => (activity, id) order (engine.py:488)
-    size_t tb = 0, tb2 = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tb, ki, ki2, ix, ix2, total, 0, 64, h->st);
-    cub::DeviceRadixSort::SortPairs(nullptr, tb2, ka, ka2, ix, ix2, total, 0, 64, h->st);
-    void* tmp = nullptr;
-    CKR(dalloc(h, &tmp, (int64_t)std::max(tb, tb2) + 16));
-    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, ki, ki2, ix, ix2, total, 0, 64, h->st));
-    k_gather_u64<<<grid_for(total), 256, 0, h->st>>>(ka, ix2, total, ka2);  // act keys in id order
-    CK(cudaGetLastError());
-    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, ka2, ka, ix2, ix, total, 0, 64, h->st));
-    unsigned long long n_el = 0;
-    CK(cudaMemcpyAsync(&n_el, h->mctr + 4, 8, cudaMemcpyDeviceToHost, h->st));
-    CK(cudaStreamSynchronize(h->st));
-    int64_t rem = std::min<int64_t>(target, (int64_t)n_el);
-    if (rem > 0) {
-        CK(cudaMemsetAsync(keep, 1, total, h->st));
-        CKR(dalloc(h, (void**)&doomed_ids, rem * 8));
-        k_mark_doomed<<<grid_for(rem), 256, 0, h->st>>>(ix, rem, keep, ki, doomed_ids);
+    int64_t rem = 0;
+    if (S.flat && bits > 0) {
+        int64_t* doomed = nullptr;
+        CKR(dalloc(h, (void**)&doomed, std::max<int64_t>(S.n_eligible, 1) * 8));
+        CK(cudaMemsetAsync(h->mctr + 3, 0, 8, h->st));
+        k_select_mark<<<grid_for(S.flat), 256, 0, h->st>>>(S.ka, S.ki, S.flat, prefix_hi, prefix_lo, bits, S.keep,
+                                                           doomed, h->mctr + 3);
         CK(cudaGetLastError());
-        if (removed_ids) CK(cudaMemcpyAsync(removed_ids, doomed_ids, rem * 8, cudaMemcpyDeviceToHost, h->st));
-        CKR(compact_all(h, keep, base));
+        CK(cudaMemcpyAsync(h->h_mctr + 3, h->mctr + 3, 8, cudaMemcpyDeviceToHost, h->st));
+        CK(cudaStreamSynchronize(h->st));
+        rem = (int64_t)h->h_mctr[3];
+        if (removed_ids && rem > cap) { dfree(h, doomed); return fail(TSG_ECAPACITY, "%lld removed ids exceed %lld", (long long)rem, (long long)cap); }
+        if (removed_ids && rem) {  // ascending engine id
+            CK(cudaMemcpyAsync(removed_ids, doomed, rem * 8, cudaMemcpyDeviceToHost, h->st));
+            CK(cudaStreamSynchronize(h->st));
+            std::sort(removed_ids, removed_ids + rem);
+        }
+        if (rem) {
+            h->desc_dirty = true;
+            CKR(compact_all(h, S.keep, S.base, S.flat));
+        }
+        dfree(h, doomed);
     }
-    dfree(h, tmp); dfree(h, ka); dfree(h, ki); dfree(h, ka2); dfree(h, ki2); dfree(h, ix); dfree(h, ix2);
-    dfree(h, keep); dfree(h, doomed_ids);
+    select_free(h);
     CK(cudaStreamSynchronize(h->st));
     *removed = rem;
     h->totals.reduces += 1;
@@ -1211,40 +1012,73 @@ int tsg_reduce(tsg_engine* h, int64_t eligible_below, int64_t target, int64_t* r
     return TSG_OK;
 }
 
+int tsg_reduce(tsg_engine* h, int64_t eligible_below, int64_t target, int64_t* removed, int64_t* removed_ids) {
+    CKR(validate_handle(h));
+    if (!removed) return fail(TSG_EINVAL, "null argument");
+    *removed = 0;
+    if (store_size(h) == 0 || target <= 0) {  // nothing selected; still counts as a reduce
+        if (any_inflight(h)) return fail(TSG_EINVAL, "the store cannot change while a launched round is not collected");
+        h->totals.reduces += 1;
+        return TSG_OK;
+    }
+    int64_t n_el = 0;
+    CKR(tsg_reduce_begin(h, eligible_below, &n_el));
+    const int64_t rem = std::min(target, n_el);
+    // the prefix (ph, pl) of `bits` bits: rem - k keys lie strictly below it,
+    // and k of the keys with this prefix are still to be taken
+    uint64_t ph = 0, pl = 0;
+    int bits = 0;
+    int64_t k = rem;
+    uint64_t hh[256];
+    while (k > 0 && bits < 128) {
+        CKR(tsg_reduce_hist(h, ph, pl, bits, hh));
+        int d = 0;
+        for (; d < 256 && (int64_t)hh[d] < k; ++d) k -= (int64_t)hh[d];
+        if (d == 256) return fail(TSG_ECUDA, "reduce select lost %lld keys", (long long)k);
+        if (bits < 64) ph |= (uint64_t)d << (56 - bits);
+        else pl |= (uint64_t)d << (120 - bits);
+        bits += 8;
+        if ((int64_t)hh[d] == k) break;  // every key with this prefix goes
+    }
+    CKR(tsg_reduce_commit(h, ph, pl, rem > 0 ? bits : 0, removed, removed_ids, target));
+    if (*removed != rem)
+        return fail(TSG_ECUDA, "reduce select removed %lld of %lld keys", (long long)*removed, (long long)rem);
+    return TSG_OK;
+}
+
 int tsg_remove_clauses(tsg_engine* h, const int64_t* ids, int64_t n, int64_t* removed) {
     CKR(validate_handle(h));
+    if (!removed) return fail(TSG_EINVAL, "null argument");
     if (any_inflight(h)) return fail(TSG_EINVAL, "the store cannot change while a launched round is not collected");
-    h->desc_dirty = true;
     DevGuard g(h->dev);
     *removed = 0;
-    int64_t total = 0;
-    std::vector<int64_t> base = part_bases(h, &total);
-    if (total == 0 || n <= 0) return TSG_OK;
+    if (store_size(h) == 0 || n <= 0) return TSG_OK;
+    h->desc_dirty = true;
+    int64_t flat = 0;
+    const std::vector<int64_t> base = bucket_bases(h, &flat);
     std::vector<int64_t> del(ids, ids + n);
     std::sort(del.begin(), del.end());
     int64_t* d_del = nullptr;
     uint8_t* keep = nullptr;
     CKR(dalloc(h, (void**)&d_del, n * 8));
-    CKR(dalloc(h, (void**)&keep, total));
+    CKR(dalloc(h, (void**)&keep, flat));
     CK(cudaMemcpyAsync(d_del, del.data(), n * 8, cudaMemcpyHostToDevice, h->st));
+    CK(cudaMemsetAsync(keep, 0, flat, h->st));
     CK(cudaMemsetAsync(h->mctr + 4, 0, 8, h->st));
-    {
-        size_t pi = 0;
-        for_parts(h, [&](Bucket&, Part& p) {
-            const int64_t pb = base[pi++];
-            if (p.count)
-                k_mark_deleted<<<grid_for(p.count), 256, 0, h->st>>>(p.ids, p.count, pb, d_del, n, keep, h->mctr + 4);
-        });
+    for (size_t bi = 0; bi < h->buckets.size(); ++bi) {
+        const Bucket& b = h->buckets[bi];
+        if (b.count)
+            k_mark_deleted<<<grid_for(b.count), 256, 0, h->st>>>(b.ids, b.count, base[bi], d_del, n, keep, h->mctr + 4);
     }
     CK(cudaGetLastError());
-    unsigned long long gone = 0;
-    CK(cudaMemcpyAsync(&gone, h->mctr + 4, 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaMemcpyAsync(h->h_mctr + 4, h->mctr + 4, 8, cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
-    if (gone) CKR(compact_all(h, keep, base));
+    const int64_t gone = (int64_t)h->h_mctr[4];
+    if (gone) CKR(compact_all(h, keep, base, flat));
     dfree(h, d_del); dfree(h, keep);
     CK(cudaStreamSynchronize(h->st));
-    *removed = (int64_t)gone;
-    h->totals.clauses_deleted += (int64_t)gone;
+    *removed = gone;
+    h->totals.clauses_deleted += gone;
     return TSG_OK;
 }
 
@@ -1261,14 +1095,12 @@ int tsg_stage_snapshots(tsg_engine* h, const int8_t* rows, int64_t n_rows, int64
         h->pitch = row_pitch;
         return TSG_OK;
     }
-    int64_t pitch = round_up(h->V + 1, 16);
-    int64_t need = pitch * n_rows;
-    CK(cudaStreamWaitEvent(h->st, h->ev_encoded, 0));  // the last encode on the encoder stream read rows_own
-    h->enc_wait_main = true;                             // the next encode reads what st copies in
+    const int64_t pitch = round_up(h->V + 1, 16);
+    const int64_t need = pitch * n_rows;
     if (need > h->rows_cap) {
         dfree(h, h->rows_own);
         h->rows_own = nullptr;
-        int64_t cap = std::max(need, h->rows_cap * 2);
+        const int64_t cap = std::max(need, h->rows_cap * 2);
         CKR(dalloc(h, (void**)&h->rows_own, cap));
         CK(cudaMemsetAsync(h->rows_own, 0, cap, h->st));  // pad bytes stay zero (Undef)
         h->rows_cap = cap;
@@ -1359,8 +1191,7 @@ int tsg_stage_packed(tsg_engine* h, const uint64_t* rows, int64_t n_rows, int64_
     CK(cudaStreamWaitEvent(h->ingress, h->ev_read[b], 0));
     if (need > h->pbuf_cap[b] || on_device) {
         if (need > h->pbuf_cap[b]) {
-            CK(cudaStreamWaitEvent(h->st, h->ev_read[b], 0));  // its last reader may be on the encoder stream
-            dfree(h, h->pbuf[b]);  // stream-ordered after its last reader
+            dfree(h, h->pbuf[b]);  // stream-ordered after its last reader (the encoder runs on st)
             h->pbuf[b] = nullptr;
             const int64_t cap = std::max(need, h->pbuf_cap[b] * 2);
             CKR(dalloc(h, (void**)&h->pbuf[b], cap * 8));
@@ -1384,44 +1215,44 @@ int tsg_stage_packed(tsg_engine* h, const uint64_t* rows, int64_t n_rows, int64_
     return TSG_OK;
 }
 
-void persist_tables(tsg_engine* h);
-
 int tsg_round_prepare(tsg_engine* h, const int32_t* group_lanes, const int32_t* group_tid, int32_t n_groups) {
     CKR(validate_handle(h));
     DevGuard g(h->dev);
     if (n_groups < 0 || n_groups > TSG_MAX_GROUPS)
         return fail(TSG_EINVAL, "n_groups must be in 0..%d, got %d", TSG_MAX_GROUPS, n_groups);
+    if (n_groups > 0 && (!group_lanes || !group_tid)) return fail(TSG_EINVAL, "null argument");
     RoundDesc rd;
     rd.n_groups = n_groups;
     rd.glanes.assign(group_lanes, group_lanes + n_groups);
     rd.gtid.assign(group_tid, group_tid + n_groups);
     rd.grow0.resize(n_groups);
     int64_t r = 0;
+    std::unordered_set<int32_t> closed;  // threads whose run of groups has ended
     for (int i = 0; i < n_groups; ++i) {
         if (rd.glanes[i] < 0 || rd.glanes[i] > h->cfg.lane_width)
             return fail(TSG_ECAPACITY, "%d assignments exceed lane width %d", rd.glanes[i], h->cfg.lane_width);
+        // a thread's groups are consecutive (engine.py:390-399 groups per sorted
+        // tid): the kernel's one-report-per-(clause, thread) rule relies on it
+        if (i > 0 && rd.gtid[i] != rd.gtid[i - 1]) {
+            closed.insert(rd.gtid[i - 1]);
+            if (closed.count(rd.gtid[i]))
+                return fail(TSG_EINVAL, "thread %d's groups are not consecutive (group %d)", rd.gtid[i], i);
+        }
         rd.grow0[i] = r;
         r += rd.glanes[i];
     }
     rd.n_chunks = (n_groups + h->cfg.group_width - 1) / h->cfg.group_width;
-    rd.chunk_off.resize(rd.n_chunks);
-    int64_t off = 0;
-    for (int c = 0; c < rd.n_chunks; ++c) {
-        int G = std::min(h->cfg.group_width, n_groups - c * h->cfg.group_width);
-        rd.chunk_off[c] = off;
-        off += agg_bytes(h);
-        off += round_up(vstride(h) * G * lane_entry_bytes(h), 256);
-    }
+    rd.chunk_stride = chunk_bytes(h);
+    rd.per_bit = std::max(1, (rd.n_chunks + 31) / 32);
+    rd.top_off = (int64_t)rd.n_chunks * rd.chunk_stride;
+    const int64_t off = rd.top_off + (rd.n_chunks > 1 ? top_bytes(h) : 0);
     // table slots never shrink and hold at least one full chunk, so rounds of
     // up to group_width groups can be prepared while another is in flight
-    const int64_t one_chunk = agg_bytes(h) + round_up(vstride(h) * h->cfg.group_width * lane_entry_bytes(h), 256);
-    const int64_t slot = std::max(h->slot_bytes, round_up(std::max(off, one_chunk), 4096));
+    const int64_t slot = std::max(h->slot_bytes, round_up(std::max(off, chunk_bytes(h)), 4096));
     if (slot != h->slot_bytes) {
         // grow both slots; stream order keeps in-flight rounds valid: their
         // kernels precede the copy, and a later replay reads the moved slot
         int8_t* nt = nullptr;
-        CK(cudaStreamWaitEvent(h->st, h->ev_encoded, 0));  // an encode may still write the old slots
-        h->enc_wait_main = true;                             // the next encode writes the new buffer
         CKR(dalloc(h, (void**)&nt, 2 * slot));
         if (h->tables && any_inflight(h))
             for (int i = 0; i < 2; ++i)
@@ -1429,59 +1260,15 @@ int tsg_round_prepare(tsg_engine* h, const int32_t* group_lanes, const int32_t* 
                                    cudaMemcpyDeviceToDevice, h->st));
         dfree(h, h->tables);
         h->tables = nt;
-        h->tables_cap = 2 * slot;
         h->slot_bytes = slot;
-        h->persist_base = nullptr;
     }
     h->tables_bytes = off;
     h->rd = std::move(rd);
-    persist_tables(h);
     return TSG_OK;
 }
 
-// Persisting L2 window over both table slots, so the 640 MB clause stream
-// and the report records cannot evict the tables.  Set once per table
-// allocation: changing the device-wide persisting limit stalls the device,
-// so it must stay off the per-round path.  Best effort: another context may
-// hold the device-wide persisting carve-out.
-void persist_tables(tsg_engine* h) {
-    const void* base = h->tables;
-    if (!h->l2_persist || h->tables_bytes <= 0 || h->persist_base == base) return;
-    h->persist_base = base;
-    int max_persist = 0, max_window = 0;
-    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, h->dev);
-    cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, h->dev);
-    const size_t win = (size_t)std::min<int64_t>(h->slot_bytes + h->tables_bytes, max_window);
-    if (max_persist <= 0 || win == 0 ||
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(win, (size_t)max_persist)) != cudaSuccess) {
-        cudaGetLastError();
-        return;
-    }
-    cudaStreamAttrValue attr{};
-    attr.accessPolicyWindow.base_ptr = const_cast<void*>(base);
-    attr.accessPolicyWindow.num_bytes = win;
-    attr.accessPolicyWindow.hitRatio = std::min(1.0f, (float)max_persist / (float)win);
-    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    if (cudaStreamSetAttribute(h->st, cudaStreamAttributeAccessPolicyWindow, &attr) != cudaSuccess)
-        cudaGetLastError();
-}
-
-// Make round state k's record buffers the active ones (the fields of
-// tsg_engine); the other state's buffers wait in `alt`.
-void use_reports(tsg_engine* h, int k) {
-    if (h->report_rs == k) return;
-    std::swap(h->out, h->alt.out); std::swap(h->out2, h->alt.out2);
-    std::swap(h->out_cap, h->alt.out_cap); std::swap(h->out2_cap, h->alt.out2_cap);
-    std::swap(h->out12, h->alt.out12); std::swap(h->out12_cap, h->alt.out12_cap);
-    std::swap(h->ev_cur, h->alt.ev);
-    std::swap(h->n_out, h->alt.n_out); std::swap(h->n_alloc, h->alt.n_alloc);
-    std::swap(h->compacted, h->alt.compacted);
-    h->report_rs = k;
-}
-
 // Launch the test of the prepared, encoded round (table slot h->tslot) in
-// the next round state: kernels, counter copy-out and its event are queued,
+// the next round state: group upload, kernel and its event are queued,
 // nothing waits.  At most two rounds are in flight.
 int round_launch(tsg_engine* h, double inc, bool flip) {
     const int k = h->next_rs;
@@ -1490,31 +1277,23 @@ int round_launch(tsg_engine* h, double inc, bool flip) {
     for (const auto& Q : h->rs)
         if (Q.inflight && Q.slot == h->tslot)
             return fail(TSG_EINVAL, "table slot %d still belongs to an uncollected round", h->tslot);
-    use_reports(h, k);
-    if (!h->out) {
-        h->out_cap = std::max<int64_t>(h->alt.out_cap, 1 << 16);
-        CKR(dalloc(h, (void**)&h->out, h->out_cap * (int64_t)sizeof(tsg_report)));
-    }
-    // this state's buffers may still be copying out from two rounds ago
-    // (no-op if never recorded)
-    CK(cudaStreamWaitEvent(h->st, h->ev_cur, 0));
-    h->n_out = 0;
-    h->n_alloc = 0;
-    h->compacted = true;
+    // this state's record buffer may still be copying out from two rounds ago
+    CK(cudaStreamWaitEvent(h->st, R.ev_copied, 0));
+    R.n_out = 0;
     R.fl = h->rd;
     R.slot = h->tslot;
     R.inc = inc;
     R.seq = ++h->round_seq;
-    R.run = 0;
+    R.all_pairs = h->all_pairs;
     // 8-byte egress: the kernel writes the packed u64 records itself when
     // they fit (ids < 2^27, <= 32 groups, 32-bit lane masks)
     R.rec8 = h->record_bytes == 8 && !wide_lane(h) && h->max_id < (int64_t(1) << 27) && h->rd.n_groups <= 32;
-    if (R.fl.n_chunks && h->oob) {  // out-of-range literal stored: numpy would raise IndexError
+    const RoundDesc& rd = R.fl;
+    if (rd.n_chunks && h->oob) {  // out-of-range literal stored: numpy would raise IndexError
         CK(cudaMemsetAsync(h->mctr + 4, 0, 8, h->st));
-        for_parts(h, [&](Bucket& b, Part& p) {
-            if (p.count && b.size)
-                k_max_var<<<grid_for(p.count * b.size), 256, 0, h->st>>>(p.lits, p.count, b.size, h->mctr + 4);
-        });
+        for (auto& b : h->buckets)
+            if (b.count && b.size)
+                k_max_var<<<grid_for(b.count * b.size), 256, 0, h->st>>>(b.lits, b.count, b.size, h->mctr + 4);
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(h->h_mctr + 4, h->mctr + 4, 8, cudaMemcpyDeviceToHost, h->st));
         CK(cudaStreamSynchronize(h->st));
@@ -1522,22 +1301,27 @@ int round_launch(tsg_engine* h, double inc, bool flip) {
             return fail(TSG_ERANGE, "index %lld is out of bounds for axis 0 with size %d", (long long)h->h_mctr[4], h->V + 1);
         h->oob = false;
     }
-    if (R.fl.n_chunks) {
+    if (rd.n_chunks) {
         CKR(build_desc(h));
-        if (h->n_tiles >= (int64_t)INT32_MAX / 2)  // the kernels index tiles with 32-bit integers
+        if (h->n_tiles >= (int64_t)1 << 30)  // the kernel indexes tiles and slots with 32-bit integers
             return fail(TSG_ECAPACITY, "store of %lld tiles exceeds the 32-bit tile index", (long long)h->n_tiles);
-        if (R.fl.n_chunks > 1) {
-            // carry stamps are matched by value ((round, run) << 32 | tid): the
-            // buffer is cleared every multi-chunk round, so neither a recycled
-            // allocation (another engine's stamps) nor a round 2^25 launches ago
-            // can fake a "(engine id, tid) already reported"
-            CKR(dgrow(h, &R.carry, &R.carry_cap, std::max<int64_t>(1, h->n_tiles * STRIDE)));
-            CK(cudaMemsetAsync(R.carry, 0, (size_t)std::max<int64_t>(1, h->n_tiles * STRIDE) * sizeof(int64_t), h->st));
+        if (rd.n_groups > R.groups_cap) {
+            dfree(h, R.d_groups);
+            R.d_groups = nullptr;
+            if (R.h_groups) { CK(cudaStreamSynchronize(h->st)); cudaFreeHost(R.h_groups); R.h_groups = nullptr; }
+            const int64_t cap = std::max<int64_t>(64, rd.n_groups);
+            CKR(dalloc(h, (void**)&R.d_groups, cap * (int64_t)sizeof(GroupDesc)));
+            CK(cudaMallocHost(&R.h_groups, cap * sizeof(GroupDesc)));
+            R.groups_cap = cap;
         }
+        // (the pinned staging is free: this state's previous round was collected)
+        for (int g = 0; g < rd.n_groups; ++g)
+            R.h_groups[g] = GroupDesc{width_mask<uint64_t>(rd.glanes[g]), rd.gtid[g], 0};
+        CK(cudaMemcpyAsync(R.d_groups, R.h_groups, rd.n_groups * sizeof(GroupDesc), cudaMemcpyHostToDevice, h->st));
         const bool timing = timed_round(h, R.seq);
         R.timed = timing;
         if (timing) CK(cudaEventRecord(R.ev_tst[0], h->st));
-        CKR(run_tests(h, k, inc, 0));
+        if (h->n_tiles) CKR(run_test(h, k, 0));
         if (timing) CK(cudaEventRecord(R.ev_tst[1], h->st));
         if (h->n_tiles == 0) {  // no kernel ran to publish the counters
             CK(cudaMemcpyAsync(R.h_ctr, R.ctr, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
@@ -1553,9 +1337,9 @@ int round_launch(tsg_engine* h, double inc, bool flip) {
 }
 
 // Collect the oldest launched round: wait for its counters; grow its record
-// buffer and replay emission if it overflowed (its table slot and carry
-// stamps are its own, so the replay is exact even with the next round in
-// flight); fill its figures.  The fetch calls then read its records.
+// buffer and replay emission if it overflowed (its table slot is its own, so
+// the replay is exact even with the next round in flight); fill its figures.
+// The fetch calls then read its records.
 int round_collect(tsg_engine* h, tsg_round_result* out) {
     int k = -1;
     for (int j = 0; j < 2; ++j)
@@ -1563,7 +1347,6 @@ int round_collect(tsg_engine* h, tsg_round_result* out) {
     if (k < 0) return fail(TSG_EINVAL, "no launched round to collect");
     auto& R = h->rs[k];
     R.inflight = false;
-    use_reports(h, k);
     h->fetch_rs = k;
     const RoundDesc& rd = R.fl;
     tsg_round_result res{};
@@ -1575,46 +1358,32 @@ int round_collect(tsg_engine* h, tsg_round_result* out) {
         // after the pivot (ends the early-exit recurrence sooner)
         if (!h->prefer_fixed && R.h_ctr[6] + R.h_ctr[7] > 0)
             h->prefer = R.h_ctr[7] < R.h_ctr[6] ? 1 : (R.h_ctr[7] > R.h_ctr[6] ? -1 : 0);
-        int64_t n_slots = (int64_t)R.h_ctr[0];
-        int64_t positives = (int64_t)R.h_ctr[1];
+        const int64_t n_rec = (int64_t)R.h_ctr[0];
+        const int64_t positives = (int64_t)R.h_ctr[1];
         res.lane_triggers = (int64_t)R.h_ctr[2];
-        int64_t n_rec = (int64_t)R.h_ctr[3];
-        // overflow: grow, replay emission only (no activity / counter side
-        // effects).  Slot reservation depends on which warp tests which tile,
-        // so a replay may need a different count.
-        while (n_slots > h->out_cap) {
-            dfree(h, h->out);
-            h->out = nullptr;
-            h->out_cap = n_slots + n_slots / 4 + 1024 + (int64_t)h->nsm * 64 * (int64_t)REPORT_CHUNK;
-            if (h->out_cap >= (int64_t)INT32_MAX)  // report slots are 32-bit in the kernels
-                return fail(TSG_ECAPACITY, "%lld report slots exceed the 32-bit record index", (long long)n_slots);
-            CKR(dalloc(h, (void**)&h->out, h->out_cap * (int64_t)sizeof(tsg_report)));
+        // overflow: grow and replay emission only (no activity / counter side
+        // effects); the record count is exact, so one replay suffices
+        if (n_rec > R.out_cap) {
+            dfree(h, R.out);
+            R.out = nullptr;
+            R.out_cap = n_rec + n_rec / 4 + 1024;
+            CKR(dalloc(h, (void**)&R.out, R.out_cap * (int64_t)sizeof(tsg_report)));
             CK(cudaMemsetAsync(R.ctr, 0, 4 * sizeof(unsigned long long), h->st));
-            R.run++;
-            CKR(run_tests(h, k, R.inc, 1));
+            CKR(run_test(h, k, 1));
             CK(cudaMemcpyAsync(R.h_ctr, R.ctr, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
+            CK(cudaMemsetAsync(R.ctr, 0, 4 * sizeof(unsigned long long), h->st));
             CK(cudaStreamSynchronize(h->st));
-            if ((int64_t)R.h_ctr[3] != n_rec)
-                return fail(TSG_ECUDA, "report replay mismatch: %lld records, %lld in the first run (replay %d, %d chunks)",
-                            (long long)R.h_ctr[3], (long long)n_rec, R.run, rd.n_chunks);
-            n_slots = (int64_t)R.h_ctr[0];
-            res.reruns++;
+            if ((int64_t)R.h_ctr[0] != n_rec)
+                return fail(TSG_ECUDA, "report replay mismatch: %lld records, %lld in the first run",
+                            (long long)R.h_ctr[0], (long long)n_rec);
+            res.reruns = 1;
         }
-        if (res.reruns) CK(cudaMemsetAsync(R.ctr, 0, 4 * sizeof(unsigned long long), h->st));
-        h->n_out = n_rec;
-        h->n_alloc = n_slots;
-        h->compacted = n_slots == n_rec;
-        int64_t n = store_size(h);
+        R.n_out = n_rec;
+        const int64_t n = store_size(h);
         int64_t lanes_total = 0;
-        for (int c = 0; c < rd.n_chunks; ++c) {
-            int32_t g0 = c * h->cfg.group_width;
-            int G = std::min(h->cfg.group_width, rd.n_groups - g0);
-            int64_t lanes = 0;
-            for (int gg = 0; gg < G; ++gg) lanes += rd.glanes[g0 + gg];
-            res.aggregate_tests += n * G;
-            lanes_total += lanes;
-        }
+        for (int g = 0; g < rd.n_groups; ++g) lanes_total += rd.glanes[g];
         res.clauses_tested = n * rd.n_chunks;
+        res.aggregate_tests = n * rd.n_groups;
         res.lane_tests = n * lanes_total;
         res.aggregate_tests_negative = res.aggregate_tests - positives;
         res.reports = n_rec;
@@ -1643,36 +1412,22 @@ int round_collect(tsg_engine* h, tsg_round_result* out) {
 int tsg_round_encode(tsg_engine* h) {
     CKR(validate_handle(h));
     DevGuard g(h->dev);
-    int64_t need_rows = h->rd.n_groups ? h->rd.grow0.back() + h->rd.glanes.back() : 0;
+    const int64_t need_rows = h->rd.n_groups ? h->rd.grow0.back() + h->rd.glanes.back() : 0;
     if (need_rows > h->n_rows) return fail(TSG_EINVAL, "groups need %lld rows, %lld staged", (long long)need_rows, (long long)h->n_rows);
     if (!h->rd.n_chunks) return TSG_OK;
     for (const auto& Q : h->rs)
         if (Q.inflight && Q.slot == h->tslot)
             return fail(TSG_EINVAL, "table slot %d still belongs to an uncollected round", h->tslot);
-    // The encoder's inputs: rows (ingress stream, or st for int8 / device
-    // copies), the table slot (free once its round was collected -- the host
-    // waited for it), the state's polarity counters (zeroed by that round).
-    h->est = h->async_encode ? h->enc_st : h->st;
-    if (h->est != h->st && h->enc_wait_main) {
-        CK(cudaEventRecord(h->ev_main, h->st));
-        CK(cudaStreamWaitEvent(h->est, h->ev_main, 0));
-        h->enc_wait_main = false;
-    }
-    if (h->packed && h->pstaged) CK(cudaStreamWaitEvent(h->est, h->ev_staged[h->pk], 0));  // rows copied in
+    if (h->packed && h->pstaged) CK(cudaStreamWaitEvent(h->st, h->ev_staged[h->pk], 0));  // rows copied in
     const bool timing = timed_round(h, h->round_seq + 1);  // the round this encode feeds
-    if (timing) CK(cudaEventRecord(h->ev_enc[h->tslot][0], h->est));
+    if (timing) CK(cudaEventRecord(h->ev_enc[h->tslot][0], h->st));
     auto& Rn = h->rs[h->next_rs];
     if (Rn.pol_pending)  // re-encoded without a launch: count this encode only
-        CK(cudaMemsetAsync(Rn.ctr + 6, 0, 2 * sizeof(unsigned long long), h->est));
+        CK(cudaMemsetAsync(Rn.ctr + 6, 0, 2 * sizeof(unsigned long long), h->st));
     Rn.pol_pending = true;
     const int rc = do_encode(h);
-    if (h->packed && h->pstaged) CK(cudaEventRecord(h->ev_read[h->pk], h->est));
-    if (timing) CK(cudaEventRecord(h->ev_enc[h->tslot][1], h->est));
-    if (h->est != h->st) {  // everything after this on st (test, broadcast) sees the tables
-        CK(cudaEventRecord(h->ev_encoded, h->est));
-        CK(cudaStreamWaitEvent(h->st, h->ev_encoded, 0));
-    }
-    h->est = h->st;
+    if (h->packed && h->pstaged) CK(cudaEventRecord(h->ev_read[h->pk], h->st));
+    if (timing) CK(cudaEventRecord(h->ev_enc[h->tslot][1], h->st));
     return rc;
 }
 
@@ -1704,15 +1459,15 @@ int tsg_round_encode_groups(tsg_engine* h, int32_t g_begin, int32_t g_end, int32
     return rc;
 }
 
-// Byte layout of the prepared round's tables (one chunk): the aggregate
+// Byte layout of the prepared round's tables (first chunk): the aggregate
 // table at agg_off (agg_bytes), then group g's lane entries at lane_off +
 // g * group_bytes -- the regions tsg_round_encode_groups ranks combine.
 int tsg_round_layout(tsg_engine* h, int64_t* agg_off, int64_t* agg_len, int64_t* lane_off, int64_t* group_bytes) {
     CKR(validate_handle(h));
     if (h->rd.n_chunks < 1) return fail(TSG_EINVAL, "no prepared round");
-    *agg_off = h->rd.chunk_off[0];
+    *agg_off = 0;
     *agg_len = (int64_t)(h->V + 2) * agg_entry_bytes(h);
-    *lane_off = h->rd.chunk_off[0] + agg_bytes(h);
+    *lane_off = agg_bytes(h);
     *group_bytes = vstride(h) * lane_entry_bytes(h);
     return TSG_OK;
 }
@@ -1721,6 +1476,48 @@ int tsg_round_tables(tsg_engine* h, void** device_ptr, int64_t* bytes) {
     CKR(validate_handle(h));
     *device_ptr = h->tables + h->tslot * h->slot_bytes;
     *bytes = h->tables_bytes;
+    return TSG_OK;
+}
+
+// In-process table broadcast (one engine per GPU in one process, DESIGN.md
+// §6): copy the encoded tables of `src`'s prepared round into `dst`'s table
+// slot over NVLink (peer copy), ordered after src's encode on dst's stream;
+// src's next use of its slot waits for the copy.  Both must have prepared
+// the same round.
+int tsg_round_tables_copy(tsg_engine* dst, tsg_engine* src) {
+    CKR(validate_handle(dst));
+    CKR(validate_handle(src));
+    if (dst->tables_bytes != src->tables_bytes || dst->V != src->V || dst->rd.n_groups != src->rd.n_groups)
+        return fail(TSG_EINVAL, "the engines have not prepared the same round");
+    for (const auto& Q : dst->rs)
+        if (Q.inflight && Q.slot == dst->tslot)
+            return fail(TSG_EINVAL, "table slot %d still belongs to an uncollected round", dst->tslot);
+    if (dst->tables_bytes == 0) return TSG_OK;
+    {
+        DevGuard g(src->dev);
+        CK(cudaEventRecord(src->ev_peer, src->st));
+    }
+    DevGuard g(dst->dev);
+    if (dst->dev != src->dev) {
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, dst->dev, src->dev);
+        if (can) {
+            cudaError_t e = cudaDeviceEnablePeerAccess(src->dev, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return fail(TSG_ECUDA, "peer access: %s", cudaGetErrorString(e));
+            cudaGetLastError();
+        }
+    }
+    CK(cudaStreamWaitEvent(dst->st, src->ev_peer, 0));
+    CK(cudaMemcpyPeerAsync(dst->tables + dst->tslot * dst->slot_bytes, dst->dev,
+                           src->tables + src->tslot * src->slot_bytes, src->dev, dst->tables_bytes, dst->st));
+    CK(cudaEventRecord(dst->ev_peer, dst->st));
+    {
+        DevGuard g2(src->dev);
+        CK(cudaStreamWaitEvent(src->st, dst->ev_peer, 0));
+    }
+    auto& Rn = dst->rs[dst->next_rs];  // no encode counted polarity for dst's next round
+    if (Rn.pol_pending) CK(cudaMemsetAsync(Rn.ctr + 6, 0, 2 * sizeof(unsigned long long), dst->st));
+    Rn.pol_pending = false;
     return TSG_OK;
 }
 
@@ -1750,45 +1547,47 @@ int tsg_round(tsg_engine* h, const int32_t* group_lanes, const int32_t* group_ti
     return tsg_round_test(h, activity_inc, out);
 }
 
-// the source and size of the round's first k records in the egress format
+namespace {
+// the source and size of the last collected round's first k records in the
+// egress format (repacked on the compute stream when it differs)
 int egress_view(tsg_engine* h, int64_t k, const void** src, int64_t* bytes) {
-    if (h->rs[h->fetch_rs].rec8) {  // written as 8-byte records by the kernel
+    auto& R = h->rs[h->fetch_rs];
+    if (R.rec8) {  // written as 8-byte records by the kernel
         if (h->record_bytes != 8)
             return fail(TSG_EINVAL, "the round was launched with 8-byte records; fetch it before changing the format");
-        *src = h->out;
+        *src = R.out;
         *bytes = k * 8;
         return TSG_OK;
     }
     if (h->record_bytes == 16 || k <= 0) {
-        *src = h->out;
+        *src = R.out;
         *bytes = k * (int64_t)sizeof(tsg_report);
         return TSG_OK;
     }
     if (h->record_bytes == 8) {
-        if (h->max_id >= (int64_t(1) << 27) || h->rs[h->fetch_rs].fl.n_groups > 32)
+        if (h->max_id >= (int64_t(1) << 27) || R.fl.n_groups > 32)
             return fail(TSG_ECAPACITY, "8-byte records need engine ids < 2^27 and <= 32 groups (largest id %lld, "
-                        "%d groups): use 12-byte records", (long long)h->max_id, h->rs[h->fetch_rs].fl.n_groups);
-        CKR(dgrow(h, &h->out12, &h->out12_cap, k * 8));
-        k_pack_records8<<<grid_for(k), 256, 0, h->st>>>(h->out, k, reinterpret_cast<uint64_t*>(h->out12));
+                        "%d groups): use 12-byte records", (long long)h->max_id, R.fl.n_groups);
+        CKR(dgrow(h, &R.out12, &R.out12_cap, k * 8));
+        k_pack_records8<<<grid_for(k), 256, 0, h->st>>>(R.out, k, reinterpret_cast<uint64_t*>(R.out12));
         CK(cudaGetLastError());
-        *src = h->out12;
+        *src = R.out12;
         *bytes = k * 8;
         return TSG_OK;
     }
-    CKR(dgrow(h, &h->out12, &h->out12_cap, k * 12));
-    k_pack_records12<<<grid_for(k), 256, 0, h->st>>>(h->out, k, h->out12);
+    CKR(dgrow(h, &R.out12, &R.out12_cap, k * 12));
+    k_pack_records12<<<grid_for(k), 256, 0, h->st>>>(R.out, k, R.out12);
     CK(cudaGetLastError());
-    *src = h->out12;
+    *src = R.out12;
     *bytes = k * 12;
     return TSG_OK;
 }
+}  // namespace
 
 int tsg_fetch_reports(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n) {
     CKR(validate_handle(h));
     DevGuard g(h->dev);
-    use_reports(h, h->fetch_rs);
-    CKR(compact_reports(h));
-    int64_t k = std::min(cap, h->n_out);
+    const int64_t k = std::min(cap, h->rs[h->fetch_rs].n_out);
     if (k > 0) {
         const void* src = nullptr;
         int64_t bytes = 0;
@@ -1796,7 +1595,7 @@ int tsg_fetch_reports(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n) {
         CK(cudaMemcpyAsync(out, src, bytes, cudaMemcpyDeviceToHost, h->st));
         CK(cudaStreamSynchronize(h->st));
     }
-    *n = k;
+    *n = std::max<int64_t>(k, 0);
     return TSG_OK;
 }
 
@@ -1813,10 +1612,9 @@ int tsg_set_record_bytes(tsg_engine* h, int32_t bytes) {
 int tsg_fetch_reports_async(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n) {
     CKR(validate_handle(h));
     DevGuard g(h->dev);
-    use_reports(h, h->fetch_rs);
-    CKR(compact_reports(h));
-    const int64_t k = std::min(cap, h->n_out);
-    *n = k;
+    auto& R = h->rs[h->fetch_rs];
+    const int64_t k = std::min(cap, R.n_out);
+    *n = std::max<int64_t>(k, 0);
     if (k <= 0) return TSG_OK;
     const void* src = nullptr;
     int64_t bytes = 0;
@@ -1824,7 +1622,7 @@ int tsg_fetch_reports_async(tsg_engine* h, tsg_report* out, int64_t cap, int64_t
     CK(cudaEventRecord(h->ev_ready, h->st));
     CK(cudaStreamWaitEvent(h->egress, h->ev_ready, 0));
     CK(cudaMemcpyAsync(out, src, bytes, cudaMemcpyDeviceToHost, h->egress));
-    CK(cudaEventRecord(h->ev_cur, h->egress));
+    CK(cudaEventRecord(R.ev_copied, h->egress));
     return TSG_OK;
 }
 
@@ -1837,13 +1635,10 @@ int tsg_fetch_wait(tsg_engine* h) {
 
 int tsg_reports_device(tsg_engine* h, void** device_ptr, int64_t* n) {
     CKR(validate_handle(h));
-    DevGuard g(h->dev);
-    use_reports(h, h->fetch_rs);
-    if (h->rs[h->fetch_rs].rec8)
-        return fail(TSG_EINVAL, "the round's records are 8-byte u64 (tsg_set_record_bytes(8)), not tsg_report");
-    CKR(compact_reports(h));
-    *device_ptr = h->out;
-    *n = h->n_out;
+    auto& R = h->rs[h->fetch_rs];
+    if (R.rec8) return fail(TSG_EINVAL, "the round's records are 8-byte u64 (tsg_set_record_bytes(8)), not tsg_report");
+    *device_ptr = R.out;
+    *n = R.n_out;
     return TSG_OK;
 }
 

@@ -19,17 +19,6 @@ constexpr int MAXG = 64;
 #ifndef TSG_TEST_MIN_BLOCKS
 #define TSG_TEST_MIN_BLOCKS 3
 #endif
-#ifndef TSG_LANE_TAIL2  // stage-2 literals past the prefetched rows two at a time
-#define TSG_LANE_TAIL2 0
-#endif
-#ifndef TSG_TAIL  // stage-1 gather batch after the first four literals
-#define TSG_TAIL 2
-#endif
-#ifdef TSG_LIT_L1  // literal rows through L1 (default: streamed past L1, keeping it for the tables)
-#define LD_LIT(p) __ldg(p)
-#else
-#define LD_LIT(p) ld_lit(p)
-#endif
 
 // ---------------------------------------------------------------------------
 // K1+K2: encoder.
@@ -297,13 +286,7 @@ __global__ void __launch_bounds__(256) k_encode_packed(const uint64_t* __restric
 // HBM rate rather than waiting on each group's load.  A lane reads back only
 // the row it copied, so no warp barrier is needed; the two 16-byte halves
 // are swapped on every other 4-lane quad (conflict-free 128-bit reads).
-constexpr int ENC_MAX_GPW = 8;
-#ifndef TSG_ENC_WAIT_ALL
-#define TSG_ENC_WAIT_ALL 0
-#endif
-#ifndef TSG_ENC_PAIR
-#define TSG_ENC_PAIR 0
-#endif  // groups per warp (G <= 64, 8 warps)
+constexpr int ENC_MAX_GPW = 8;  // groups per warp (G <= 64, 8 warps)
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
@@ -357,28 +340,6 @@ struct Transpose32 {
         }
         return x;
     }
-    // Two transposes, one shuffle per stage: a lane only ever uses the half
-    // of its partner's word the partner discards (the ~keep blocks), so A's
-    // discarded blocks and B's, rotated into the keep blocks, share one word.
-    __device__ __forceinline__ void pair(uint32_t& a, uint32_t& b) const {
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {  // byte stages: shuffle + PRMT each
-            a = __byte_perm(a, __shfl_xor_sync(0xffffffffu, a, 16 >> i), sel[i]);
-            b = __byte_perm(b, __shfl_xor_sync(0xffffffffu, b, 16 >> i), sel[i]);
-        }
-#pragma unroll
-        for (int i = 2; i < 5; ++i) {
-            const uint32_t br = __funnelshift_r(b, b, amt[i]);  // B's ~keep blocks onto the keep blocks
-            uint32_t p, na, nb;
-            asm("lop3.b32 %0, %1, %2, %3, 0xE2;" : "=r"(p) : "r"(br), "r"(keep[i]), "r"(a));  // keep ? br : a
-            const uint32_t q = __shfl_xor_sync(0xffffffffu, p, 16 >> i);
-            const uint32_t qa = __funnelshift_l(q, q, amt[i]);  // partner's A blocks into place
-            asm("lop3.b32 %0, %1, %2, %3, 0xE2;" : "=r"(na) : "r"(a), "r"(keep[i]), "r"(qa));  // keep ? a : qa
-            asm("lop3.b32 %0, %1, %2, %3, 0xE2;" : "=r"(nb) : "r"(b), "r"(keep[i]), "r"(q));   // keep ? b : q
-            a = na;
-            b = nb;
-        }
-    }
 };
 
 template <class GW, int GPW>
@@ -405,12 +366,11 @@ __global__ void __launch_bounds__(256) k_encode_packed32(const uint64_t* __restr
         cp_async_commit();
     }
     const Transpose32 xp(lane);
-    if (TSG_ENC_WAIT_ALL) cp_async_wait_upto(0);  // all groups landed: the compiler may interleave them
     uint32_t nT[4] = {0, 0, 0, 0}, nF[4] = {0, 0, 0, 0}, nU[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int j = 0; j < GPW; ++j) {
         const int g = y + 8 * j;
-        if (!TSG_ENC_WAIT_ALL) cp_async_wait_upto(GPW - 1 - j);
+        cp_async_wait_upto(GPW - 1 - j);
         // no branch around the shuffles (they must stay provably converged):
         // groups past G transpose zero-filled rows and store nothing
         const bool live = g >= c.gbeg && g < c.gend;
@@ -422,9 +382,9 @@ __global__ void __launch_bounds__(256) k_encode_packed32(const uint64_t* __restr
 #pragma unroll
         for (int k = 0; k < 4; ++k) { T[k] = tv[k]; S[k] = sv[k]; }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {  // eight independent shuffle chains (paired in the bit stages)
-            if (TSG_ENC_PAIR) xp.pair(T[k], S[k]);
-            else { T[k] = xp(T[k]); S[k] = xp(S[k]); }
+        for (int k = 0; k < 4; ++k) {  // eight independent shuffle chains
+            T[k] = xp(T[k]);
+            S[k] = xp(S[k]);
         }
         LaneEntry<uint32_t>* dst = lane_tab + (int64_t)g * c.vstride + vbase + lane;
 #pragma unroll
@@ -477,8 +437,8 @@ __global__ void __launch_bounds__(256) k_encode_packed32(const uint64_t* __restr
 }
 
 // ---------------------------------------------------------------------------
-// K3+K4+K5: trigger test.  Persistent grid; one warp per tile of 32 clauses
-// of one bucket, one clause per lane.
+// K3+K4+K5: trigger test, one launch per round.  Persistent grid; one warp
+// per tile of 32 clauses of one bucket, one clause per lane.
 //
 // The kernel is bound by L2 sectors (every table gather touches a 32-byte
 // sector: DESIGN.md §4) and by the latency of the gather chains, so:
@@ -492,14 +452,20 @@ __global__ void __launch_bounds__(256) k_encode_packed32(const uint64_t* __restr
 //    word is final;
 //  * stage 2 (lane test, bitpack.py:120-135) runs per positive group with
 //    the same early exit; the clause's activity and engine id are loaded at
-//    stage-2 entry, off the report path.
+//    stage-2 entry.
+// Rounds of more than one chunk (engine.py:403-407) run in the same launch:
+// a chunk-level aggregate (the 32x32x32 hierarchy of PAPER.md:425, k_top)
+// is swept first, and only the chunks it leaves positive get a stage 1.  A
+// lane walks its clause's chunks in order, so the reference's "one report
+// per (clause, thread)" set (engine.py:462-464) is a register: the tid of
+// the last report (a thread's groups are contiguous in round order).
 // Every triggering group bumps the clause's activity by inc * popcount (fp64
 // round-to-nearest mul then add, no FMA: engine.py:460); the first
-// triggering group of each thread emits the report (engine.py:462-464).
-// Report slots come from a warp-private chunk refilled by one atomic per
-// REPORT_CHUNK slots, reserved for an upper bound (the positive-group
-// count); unused slots are written as padding (key = ~0) and squeezed out
-// when the records are fetched.
+// triggering group of each thread emits the report, or every triggering
+// group in all-pairs mode (multi_trigger's pair set, bitpack.py:282-300).
+// Records collect in a per-warp shared-memory buffer and leave in coalesced
+// batches, each reserved with one atomic for exactly its count: the record
+// buffer has no holes and needs no compaction pass.
 
 struct BucketDesc {
     const int32_t* lits;
@@ -511,156 +477,41 @@ struct BucketDesc {
     int64_t tile0;  // first global tile of the bucket
 };
 
+// one group of the round, in round order (engine.py:390-399)
+struct GroupDesc {
+    uint64_t lane_mask;
+    int32_t tid;
+    int32_t pad;
+};
+
 template <class LW, class GW>
 struct TestParams {
     const BucketDesc* buckets;
     int32_t nb;
-    int32_t G;                 // groups in this chunk
-    int64_t n_tiles;
-    const AggEntry<GW>* agg;
-    const void* codes;         // per-literal-code table (shared-memory variant), codes_bytes long
-    int64_t codes_bytes;
-    const LaneEntry<LW>* lane; // [G][vstride]
-    int64_t vstride;
-    int32_t sentinel;          // num_vars + 1
-    int32_t g0;                // global index of the chunk's first group
-    GW group_mask;
+    int32_t n_tiles;                 // the host keeps tiles < 2^30
+    const uint8_t* tables;           // the round's table slot: chunk c at tables + c * chunk_stride
+    int64_t chunk_stride;
+    int64_t lane_off;                // lane table offset inside a chunk (after its aggregate table)
+    int64_t vstride;                 // lane-table row length
+    const AggEntry<uint32_t>* top;   // chunk-level aggregate (n_chunks > 1)
+    int32_t n_chunks, group_width, n_groups, per_bit;  // per_bit: chunks per bit of the top table
+    int32_t sentinel;                // num_vars + 1
+    const GroupDesc* groups;         // [n_groups]
     double inc;
-    tsg_report* out;
-    unsigned long long* ctr;   // [0] slots reserved, [1] aggregate positives, [2] lane triggers, [3] reports
-    int64_t out_cap;
-    int64_t* carry;            // per-clause "(round, tid) reported" stamp for multi-chunk rounds
-    int64_t stamp_base;        // round sequence << 32
-    int32_t carry_in_tid;      // first tid of the chunk if it continues from the previous chunk, else -1
-    int32_t carry_out_tid;     // last tid of the chunk if it continues into the next chunk, else -1
-    int32_t emit_only;         // replay after report-buffer overflow: no activity / counter side effects
-    unsigned long long* pub;   // last launch of a round: host-mapped [8] the last CTA publishes ctr to
-    int32_t dyn_tiles;         // tiles from the counters `tiles` (DynTiles) instead of a static stride
-    int32_t rec8;              // records as 8-byte u64 (st_record)
-    unsigned long long* tiles; // [TSG_DYN_NC * DYN_STRIDE] per-launch tile counters (zero between launches)
-    const int64_t* slab_tile0; // slab kernel: first tile of each slab (+ end)
-    const int32_t* slab_desc0; // slab kernel: first descriptor of each slab (+ end)
-    const uint64_t* sched;     // slab kernel: per CTA slab << 32 | rank << 16 | CTAs on the slab
-    int32_t n_sched;
-    int32_t slab_w;            // slab kernel: variables per slab
-    int32_t tid[MAXG];
-    LW lane_mask[MAXG];
+    void* out;                       // records: tsg_report, or u64 (rec8)
+    unsigned long long out_cap;
+    unsigned long long* ctr;         // [0] records, [1] aggregate positives, [2] lane triggers, [5] CTAs done
+    unsigned long long* pub;         // the round's first run: host-mapped [8] the last CTA publishes ctr to
+    int32_t emit_only;               // replay after record-buffer overflow: no activity / counter side effects
+    int32_t rec8;                    // 8-byte records engine_id << 37 | group << 32 | lane_mask
+    int32_t all_pairs;               // every triggering (clause, group), not the first per thread
 };
 
-constexpr int PF = 8;  // literal rows prefetched per tile
-#ifndef TSG_TEST_THREADS
-#define TSG_TEST_THREADS 256
-#endif
-constexpr int TEST_THREADS = TSG_TEST_THREADS;  // block of the L2-table variant
-constexpr int TEST_THREADS_SMEM = 768;  // block of the shared-memory-table variant (one per SM)
-constexpr int64_t SMEM_TABLE_MAX = 200 * 1024;
-#ifndef TSG_SLAB_THREADS
-#define TSG_SLAB_THREADS 768
-#endif
-constexpr int TEST_THREADS_SLAB = TSG_SLAB_THREADS;  // block of the slab variant (one per SM)
-constexpr int64_t SLAB_SMEM_BYTES = 132 * 1024;     // one slab's words: keeps the CTA under the 164 KB carveout,
-                                                    // leaving ~92 KB of L1 for in-flight gathers (measured cliff below ~60 KB)
-
-constexpr uint64_t REPORT_PAD = ~0ull;
-#ifndef REPORT_CHUNK  // report slots a warp reserves per atomic
-#define REPORT_CHUNK 128ull
-#endif
-
-__device__ __forceinline__ void st_report(tsg_report* p, uint64_t key, uint64_t mask) {
-    *reinterpret_cast<ulonglong2*>(p) = make_ulonglong2(key, mask);
-}
-// Record i of the round: 16-byte tsg_report, or -- rounds launched for
-// 8-byte egress (TestParams::rec8) -- one u64 engine_id << 37 | group << 32 |
-// lane_mask written straight from the kernel (half the bytes, no pack pass).
-// `hi` is the engine id already shifted for the format.
-__device__ __forceinline__ void st_record(tsg_report* out, int rec8, int pos, uint64_t hi, uint32_t group,
-                                          uint64_t mask) {
-    if (rec8) reinterpret_cast<uint64_t*>(out)[pos] = hi | ((uint64_t)group << 32) | (uint32_t)mask;
-    else st_report(out + pos, hi | group, mask);
-}
-__device__ __forceinline__ void st_pad(tsg_report* out, int rec8, int pos) {
-    if (rec8) reinterpret_cast<uint64_t*>(out)[pos] = REPORT_PAD;
-    else st_report(out + pos, REPORT_PAD, 0);
-}
+constexpr int PF = 8;          // literal rows prefetched per tile
+constexpr int TEST_THREADS = 256;
+constexpr int RECBUF = 64;     // records buffered per warp
 
 __device__ __forceinline__ int lit_var(int32_t lit) { return lit < 0 ? -lit : lit; }
-
-// Polarity-adjusted value subset of a literal in every group of the chunk:
-// bit g of t / f / u says that some lane of group g makes the literal True /
-// False / leaves it Undef (bitpack.py:138-182 seen through a literal,
-// bitpack.py:263-268).
-template <class GW>
-struct Subset {
-    GW t, f, u;
-};
-
-// Aggregates gathered from the L2-resident table AggEntry[num_vars + 2]:
-// one 32-byte sector per lookup; works for any num_vars.
-template <class GW>
-struct GlobalTable {
-    static constexpr bool kSmem = false;
-    static constexpr bool kSlab = false;
-    const AggEntry<GW>* agg;
-    __device__ __forceinline__ Subset<GW> get(int32_t lit) const {
-        const AggEntry<GW> e = ld_agg(agg + lit_var(lit));
-        return lit < 0 ? Subset<GW>{e.f, e.t, e.u} : Subset<GW>{e.t, e.f, e.u};
-    }
-};
-
-// Per-literal-code words {can_be_false | can_be_undef << H} in shared memory
-// (code = 2 * var + negative): used when 2 * (num_vars + 2) codes fit, i.e.
-// small num_vars x groups; stage 1 then needs no L2 gathers at all.
-template <class GW, class EW>
-struct SmemTable {
-    static constexpr bool kSmem = true;
-    static constexpr bool kSlab = false;
-    static constexpr int H = sizeof(EW) * 4;
-    const EW* code;
-    __device__ __forceinline__ Subset<GW> get(int32_t lit) const {
-        const int c = 2 * lit_var(lit) + (lit < 0);
-        const EW a = code[c], b = code[c ^ 1];
-        const EW m = (EW)((EW(1) << H) - 1);
-        return Subset<GW>{(GW)(b & m), (GW)(a & m), (GW)(a >> H)};  // True for lit = False for ~lit
-    }
-};
-
-// One variable slab [lo, lo + w) in shared memory (slab kernel): the
-// can-be-False word of each literal code and the can-be-Undef word of each
-// variable; literals outside the slab are gathered from the L2 table.
-template <class GW>
-struct SlabTable {
-    static constexpr bool kSmem = true;
-    static constexpr bool kSlab = true;
-    const GW* fc;  // [2 * w]: code 2i = +(lo+i), 2i+1 = -(lo+i)
-    const GW* u;   // [w]
-    const AggEntry<GW>* agg;
-    int32_t lo, w;
-    __device__ __forceinline__ bool hot(int32_t lit) const {
-        return (uint32_t)(lit_var(lit) - lo) < (uint32_t)w;
-    }
-    __device__ __forceinline__ void get_hot(int32_t lit, GW& f, GW& uu) const {
-        const int i = lit_var(lit) - lo;
-        f = fc[2 * i + (lit < 0)];
-        uu = u[i];
-    }
-    __device__ __forceinline__ Subset<GW> get(int32_t lit) const {
-        const AggEntry<GW> e = ld_agg(agg + lit_var(lit));
-        return lit < 0 ? Subset<GW>{e.f, e.t, e.u} : Subset<GW>{e.t, e.f, e.u};
-    }
-};
-
-template <class EW>
-__global__ void k_codes(const AggEntry<uint32_t>* __restrict__ agg, int64_t nv2, EW* __restrict__ code) {
-    constexpr int H = sizeof(EW) * 4;
-    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (; v < nv2; v += (int64_t)gridDim.x * blockDim.x) {
-        const AggEntry<uint32_t> e = agg[v];
-        const EW m = (EW)((EW(1) << H) - 1);
-        code[2 * v] = (EW)((EW)(e.f & m) | (EW)((EW)(e.u & m) << H));      // +v is False where v is False
-        code[2 * v + 1] = (EW)((EW)(e.t & m) | (EW)((EW)(e.u & m) << H));  // -v is False where v is True
-    }
-}
-
 
 // Tiles of a warp increase monotonically, so the warp walks the bucket table
 // forward: `bi` is the tile's bucket, `nt0` the first tile of bucket bi + 1.
@@ -677,7 +528,7 @@ __device__ __forceinline__ const int32_t* lane_lits(const BucketDesc* bd, int ti
 }
 
 __device__ __forceinline__ bool lane_active(const BucketDesc* bd, int tile, int lane) {
-    return (tile - bd->tile0) * STRIDE + lane < bd->count;
+    return (int64_t)(tile - bd->tile0) * STRIDE + lane < bd->count;
 }
 
 // load the first PF literal rows of a tile (this lane's column)
@@ -687,349 +538,261 @@ __device__ __forceinline__ void load_rows(const BucketDesc* bd, int tile, int la
     const bool act = lane_active(bd, tile, lane);
     const int size = bd->size;
 #pragma unroll
-    for (int u = 0; u < PF; ++u) buf[u] = (act && u < size) ? LD_LIT(lp + u * STRIDE) : sentinel;
+    for (int u = 0; u < PF; ++u) buf[u] = (act && u < size) ? ld_lit(lp + u * STRIDE) : sentinel;
 }
 
-template <class GW, class TAB, int THREADS>
-constexpr size_t test_smem_bytes(int64_t codes_bytes) {
-    return TAB::kSmem ? (size_t)codes_bytes : 16;
+// Polarity-adjusted (can be False, can be Undef) words of a literal
+// (bitpack.py:138-182 seen through a literal, bitpack.py:263-268).
+template <class W>
+__device__ __forceinline__ void lit_fu(const AggEntry<W>* agg, int32_t lit, W& f, W& u) {
+    const AggEntry<W> e = ld_agg(agg + lit_var(lit));
+    f = lit < 0 ? e.t : e.f;
+    u = e.u;
 }
 
-// The current tile's first PF literal rows of this lane's clause.
-// RegRows keeps them in registers (indexed with compile-time positions);
-// SmemRows keeps them in a per-warp shared-memory buffer [PF][32] so the slab
-// kernel can index them with lane-dependent positions (one LDS, no select
-// chains, no local memory).
-struct RegRows {
-    int32_t r[PF];
-    __device__ __forceinline__ int32_t get(int j) const { return r[j]; }
-    __device__ __forceinline__ void take(const int32_t (&nxt)[PF]) {
+// Stage 1 over one aggregate table (a chunk's groups, or the chunk-level
+// table): the live word (all_false | one_undef) of the clause whose first PF
+// literals are `r` and whose literal j sits at lp[j * STRIDE].
+template <class W>
+__device__ __forceinline__ W sweep(const AggEntry<W>* agg, const int32_t (&r)[PF], const int32_t* lp, int size,
+                                   int32_t sentinel) {
+    W af = ~W(0), ou = W(0);
+    {  // literals 0..3 together: nearly every clause needs them (sentinel past the end)
+        W f[4], u[4];
 #pragma unroll
-        for (int u = 0; u < PF; ++u) r[u] = nxt[u];
-    }
-};
-struct SmemRows {
-    int32_t* buf;  // this warp's [PF][32] buffer, offset by lane
-    __device__ __forceinline__ int32_t get(int j) const { return buf[j * 32]; }
-    __device__ __forceinline__ void take(const int32_t (&nxt)[PF]) {
-        __syncwarp();
+        for (int k = 0; k < 4; ++k) lit_fu<W>(agg, r[k], f[k], u[k]);
 #pragma unroll
-        for (int u = 0; u < PF; ++u) buf[u * 32] = nxt[u];
-        __syncwarp();
+        for (int k = 0; k < 4; ++k) step<W>(af, ou, f[k], u[k]);
     }
-};
+#pragma unroll
+    for (int h = 4; h < PF; h += 2) {  // then two at a time while any group is live
+        if (h >= size || (af | ou) == W(0)) break;
+        W f0, u0, f1, u1;
+        lit_fu<W>(agg, r[h], f0, u0);
+        lit_fu<W>(agg, r[h + 1], f1, u1);
+        step<W>(af, ou, f0, u0);
+        step<W>(af, ou, f1, u1);
+    }
+    for (int j = PF; j < size && (af | ou) != W(0); j += 4) {  // the rest, four at a time
+        int32_t l[4];
+        W f[4], u[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) l[k] = (j + k < size) ? ld_lit_tail(lp + (j + k) * STRIDE) : sentinel;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) lit_fu<W>(agg, l[k], f[k], u[k]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) step<W>(af, ou, f[k], u[k]);
+    }
+    return af | ou;
+}
 
-// one batch of stage-2 literals (lane words of group g for literals h..h+3)
-template <class LW, class ROWS>
-__device__ __forceinline__ void lane_batch(const LaneEntry<LW>* lt, const ROWS& rows, int h, int size, LW& lf,
-                                           LW& lo) {
+// one batch of stage-2 literals (lane words for literals h..h+3)
+template <class LW>
+__device__ __forceinline__ void lane_batch(const LaneEntry<LW>* lt, const int32_t (&r)[PF], int h, int size,
+                                           LW& lf, LW& lo) {
     LaneEntry<LW> e[4];
-    int32_t l[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) l[u] = rows.get(h + u);
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-        if (h + u < size) e[u] = ld_lane(lt + lit_var(l[u]));
+        if (h + u < size) e[u] = ld_lane(lt + lit_var(r[h + u]));
 #pragma unroll
     for (int u = 0; u < 4; ++u)
         if (h + u < size)
-            step<LW>(lf, lo, l[u] < 0 ? (e[u].s & e[u].t) : (e[u].s & ~e[u].t), ~e[u].s);
+            step<LW>(lf, lo, r[h + u] < 0 ? (e[u].s & e[u].t) : (e[u].s & ~e[u].t), ~e[u].s);
 }
 
-// Per-warp running state of the tile loop: the warp's report-slot chunk
-// [cpos, cend) and its counter accumulators.
-struct WarpAcc {
-    int cpos = 0, cend = 0;  // report slots (the host keeps out_cap < 2^31)
-    unsigned int pos = 0, trig = 0, rep = 0;
+// Stage 2 (assignment_trigger, bitpack.py:120-135) for one group's lane table.
+template <class LW>
+__device__ __forceinline__ LW lane_test(const LaneEntry<LW>* lt, const int32_t (&r)[PF], const int32_t* lp,
+                                        int size) {
+    LW lf = ~LW(0), lo = LW(0);
+    lane_batch<LW>(lt, r, 0, size, lf, lo);
+    if (size > 4 && (lf | lo) != LW(0)) lane_batch<LW>(lt, r, 4, size, lf, lo);
+    for (int j = PF; j < size && (lf | lo) != LW(0); ++j) {
+        const int32_t l = ld_lit_tail(lp + j * STRIDE);
+        const LaneEntry<LW> e = ld_lane(lt + lit_var(l));
+        step<LW>(lf, lo, l < 0 ? (e.s & e.t) : (e.s & ~e.t), ~e.s);
+    }
+    return lf | lo;
+}
+
+// The warp's record buffer: `n` records (warp-uniform) in `buf`; flush()
+// reserves exactly n slots with one atomic and writes them coalesced.
+struct RecBuf {
+    ulonglong2* buf;
+    int n = 0;
+    __device__ __forceinline__ void flush(void* out, unsigned long long cap, unsigned long long* ctr, int rec8,
+                                          int lane) {
+        __syncwarp();
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(ctr, (unsigned long long)n);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        for (int i = lane; i < n; i += 32) {
+            const unsigned long long q = base + (unsigned long long)i;
+            if (q < cap) {  // past the capacity only counted: the host grows the buffer and replays
+                if (rec8) reinterpret_cast<uint64_t*>(out)[q] = buf[i].x;
+                else reinterpret_cast<ulonglong2*>(out)[q] = buf[i];
+            }
+        }
+        __syncwarp();
+        n = 0;
+    }
+    // warp-wide: lanes with `has` append `rec`
+    __device__ __forceinline__ void append(bool has, ulonglong2 rec, void* out, unsigned long long cap,
+                                           unsigned long long* ctr, int rec8, int lane) {
+        const unsigned b = __ballot_sync(0xffffffffu, has);
+        if (has) buf[n + __popc(b & ((1u << lane) - 1u))] = rec;
+        n += __popc(b);
+        if (n > RECBUF - 32) flush(out, cap, ctr, rec8, lane);
+    }
 };
 
-#ifndef TSG_COLD0  // literals in the first cold gather batch of the slab kernel
-#define TSG_COLD0 3
-#endif
-
-// Stage 1 of the slab kernel for one clause: the hot prefix (literals whose
-// variable lies in the CTA's slab, stored first) is looked up in shared
-// memory; the cold rest is gathered from the L2-resident table in batches
-// aligned to each lane's own first cold position (TSG_COLD0 literals, then
-// 2 at a time) while any group is live, so a warp needs only as many L2
-// round trips as its lanes' longest chain.
-template <class LW, class GW>
-__device__ __forceinline__ void stage1_slab(const TestParams<LW, GW>& p, const SlabTable<GW>& tab,
-                                            const SmemRows& rows, const int32_t* lp, int size, GW& af, GW& ou) {
-    auto lit_at = [&](int i) -> int32_t {
-        if (i >= size) return p.sentinel;
-        return i < PF ? rows.get(i) : __ldg(lp + i * STRIDE);
-    };
-    int hp = 0;  // hot prefix length
-    while (hp < size) {
-        const int32_t l = lit_at(hp);
-        if (!tab.hot(l)) break;
-        GW f, uu;
-        tab.get_hot(l, f, uu);
-        step<GW>(af, ou, f, uu);
-        ++hp;
-    }
-    int j = hp;  // next cold position of this lane
-    if (j < size && (af | ou) != GW(0)) {
-        int32_t l[TSG_COLD0];
-#pragma unroll
-        for (int k = 0; k < TSG_COLD0; ++k) l[k] = lit_at(j + k);
-        Subset<GW> sb[TSG_COLD0];
-#pragma unroll
-        for (int k = 0; k < TSG_COLD0; ++k) sb[k] = tab.get(l[k]);
-#pragma unroll
-        for (int k = 0; k < TSG_COLD0; ++k) step<GW>(af, ou, sb[k].f, sb[k].u);
-        j += TSG_COLD0;
-        while (j < size && (af | ou) != GW(0)) {
-            const int32_t l0 = lit_at(j), l1 = lit_at(j + 1);
-            const Subset<GW> s0 = tab.get(l0), s1 = tab.get(l1);
-            step<GW>(af, ou, s0.f, s0.u);
-            step<GW>(af, ou, s1.f, s1.u);
-            j += 2;
+// Chunk-level aggregate: bit b of top[v].{t,f,u} = some
+// group of a chunk of slot b (chunks b*per_bit .. b*per_bit + per_bit - 1)
+// has the bit in its aggregate entry.  Sound: a group that stays positive
+// through stage 1 keeps its slot positive here (the recurrence is monotone
+// in its inputs).  The always-False sentinel entry stays always False.
+template <class GW>
+__global__ void k_top(const uint8_t* __restrict__ tables, int64_t chunk_stride, int32_t n_chunks, int32_t per_bit,
+                      int64_t nv2, AggEntry<uint32_t>* __restrict__ top) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; v < nv2; v += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t t = 0, f = 0, u = 0;
+        for (int c = 0; c < n_chunks; ++c) {
+            const AggEntry<GW> e = ld_agg(reinterpret_cast<const AggEntry<GW>*>(tables + c * chunk_stride) + v);
+            const uint32_t bit = 1u << (c / per_bit);
+            if (e.t) t |= bit;
+            if (e.f) f |= bit;
+            if (e.u) u |= bit;
         }
+        top[v] = AggEntry<uint32_t>{t, f, u, 0u};
     }
 }
 
-// Tile sources (warp-uniform, strictly increasing per warp; -1 = done).
-// Warps take tiles one at a time from TSG_DYN_NC per-launch counters
-// (counter c hands out tiles c, c + NC, c + 2 NC, ...; warp w uses counter
-// w % NC), so SMs that run faster -- the two dies' L2 distances differ --
-// take more tiles instead of idling at the end of a static share.  The
-// atomic for the tile after next is issued when `next` returns, so its
-// latency overlaps a whole tile.
-#ifndef TSG_DYN_NC
-#define TSG_DYN_NC 8
-#endif
-constexpr int DYN_STRIDE = 32;  // u64 words between counters (separate L2 lines)
-struct DynTiles {
-    unsigned long long* ctr;  // this warp's counter
-    int c, end;
-    unsigned long long ahead = 0;  // lane 0: the next k, in flight
-    bool primed = false;
-    __device__ __forceinline__ int next(int lane) {
-        if (!primed) {
-            primed = true;
-            if (lane == 0) ahead = atomicAdd(ctr, 1ull);
-        }
-        const unsigned long long k = __shfl_sync(0xffffffffu, ahead, 0);
-        const long long t = (long long)c + (long long)TSG_DYN_NC * (long long)k;
-        if (t >= end) return -1;
-        if (lane == 0) ahead = atomicAdd(ctr, 1ull);
-        return (int)t;
-    }
-};
+template <class LW, class GW, bool MULTI>
+__global__ void __launch_bounds__(TEST_THREADS, (sizeof(LW) == 8 || sizeof(GW) == 8) ? 2 : TSG_TEST_MIN_BLOCKS)
+k_test(const __grid_constant__ TestParams<LW, GW> p) {
+    constexpr int WARPS = TEST_THREADS / 32;
+    __shared__ ulonglong2 s_rec[WARPS][RECBUF];
+    __shared__ unsigned int s_acc[2][WARPS];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int nwarps = (int)(((int64_t)gridDim.x * TEST_THREADS) >> 5);
+    RecBuf rb{s_rec[warp]};
+    unsigned int pos_acc = 0, trig_acc = 0;
+    const uint32_t top_mask = MULTI ? width_mask<uint32_t>((p.n_chunks + p.per_bit - 1) / p.per_bit) : 1u;
 
-struct StrideTiles {  // tiles t, t + step, ... < end
-    int t, step, end;  // tile indices (the host keeps n_tiles < 2^31)
-    bool started = false;
-    __device__ __forceinline__ int next(int) {
-        if (started) t += step;
-        started = true;
-        return t < end ? t : -1;
-    }
-};
-// The tile loop shared by every k_test variant (one clause per lane).
-// `descs[0, nb)` covers every tile the source hands out (global memory, or
-// the slab's share staged in shared memory).
-template <class LW, class GW, class TAB, class SRC, class ROWS>
-__device__ __forceinline__ void test_tiles(const TestParams<LW, GW>& p, const TAB& tab, const BucketDesc* descs,
-                                           int nb, SRC& src, ROWS& cur, int lane, WarpAcc& acc) {
-    int tile = src.next(lane);
-    if (tile < 0) return;
-    int bi = 0;
-    int nt0 = 0;
-    {  // first bucket by binary search, then walk forward
-        int lo = 0, hi = nb - 1;
+    int tile = (int)(((int64_t)blockIdx.x * TEST_THREADS + threadIdx.x) >> 5);
+    int bi = 0, nt0 = 0;
+    int32_t cur[PF], nxt[PF];
+    if (tile < p.n_tiles) {  // first bucket by binary search, then walk forward
+        int lo = 0, hi = p.nb - 1;
         while (lo < hi) {
-            int mid = (lo + hi + 1) >> 1;
-            if (descs[mid].tile0 <= tile) lo = mid; else hi = mid - 1;
+            const int mid = (lo + hi + 1) >> 1;
+            if (p.buckets[mid].tile0 <= tile) lo = mid; else hi = mid - 1;
         }
         bi = lo;
-        nt0 = bi + 1 < nb ? (int)descs[bi + 1].tile0 : INT_MAX;
+        nt0 = bi + 1 < p.nb ? (int)p.buckets[bi + 1].tile0 : INT_MAX;
+        load_rows(p.buckets + bi, tile, lane, p.sentinel, cur);
     }
-    int32_t nxt[PF];
-    load_rows(descs + bi, tile, lane, p.sentinel, nxt);
-    cur.take(nxt);
-
-    while (tile >= 0) {
-        const BucketDesc* bd = descs + bi;
+    while (tile < p.n_tiles) {
+        const BucketDesc* bd = p.buckets + bi;
         // software pipeline: the next tile's first rows are in flight while this one is tested
-        const int ntile = src.next(lane);
-        if (ntile >= 0) {
-            seek_bucket(descs, nb, ntile, bi, nt0);
-            load_rows(descs + bi, ntile, lane, p.sentinel, nxt);
+        const int ntile = tile + nwarps;
+        if (ntile < p.n_tiles) {
+            seek_bucket(p.buckets, p.nb, ntile, bi, nt0);
+            load_rows(p.buckets + bi, ntile, lane, p.sentinel, nxt);
         }
         const int size = bd->size;
         const bool active = lane_active(bd, tile, lane);
+        const int slot = (tile - (int)bd->tile0) * STRIDE + lane;
+        const int32_t* lp = lane_lits(bd, tile, lane);
 
-        // ---- stage 1: aggregate filter (engine.py:238-254) -----------------
-        GW af = ~GW(0), ou = GW(0);
+        uint32_t cw = 0;  // chunk slots left positive by the chunk-level sweep
         if (active) {
-            if constexpr (TAB::kSlab) {
-                stage1_slab<LW, GW>(p, tab, cur, lane_lits(bd, tile, lane), size, af, ou);
-            } else {
-                {  // literals 0..3 together: nearly every clause needs them
-                    Subset<GW> s[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) s[u] = tab.get(cur.get(u));
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) step<GW>(af, ou, s[u].f, s[u].u);
+            if constexpr (MULTI) cw = sweep<uint32_t>(p.top, cur, lp, size, p.sentinel) & top_mask;
+            else cw = 1u;
+        }
+        uint32_t wcw = __reduce_or_sync(0xffffffffu, cw);
+        bool loaded = false, touched = false;
+        double act = 0.0;
+        uint64_t key_hi = 0;
+        int last_tid = INT_MIN;
+        while (wcw) {
+            const int b = __ffs(wcw) - 1;
+            wcw &= wcw - 1u;
+            const bool mine = (cw >> b) & 1u;
+            const int c1 = MULTI ? min((b + 1) * p.per_bit, p.n_chunks) : 1;
+            for (int c = MULTI ? b * p.per_bit : 0; c < c1; ++c) {
+                const uint8_t* tab = p.tables + c * p.chunk_stride;
+                const int g0 = c * p.group_width;
+                const int G = min(p.group_width, p.n_groups - g0);
+                // ---- stage 1: aggregate filter (engine.py:238-254) -------------
+                GW left = GW(0);
+                if (mine)
+                    left = sweep<GW>(reinterpret_cast<const AggEntry<GW>*>(tab), cur, lp, size, p.sentinel) &
+                           width_mask<GW>(G);
+                pos_acc += __popcll((unsigned long long)left);
+                if (left != GW(0) && !loaded) {  // stage-2 entry: id and activity of the clause
+                    loaded = true;
+                    key_hi = (uint64_t)bd->ids[slot] << (p.rec8 ? 37 : 16);
+                    if (!p.emit_only) act = bd->acts[slot];
                 }
-#pragma unroll
-                for (int h = 4; h < PF; h += TSG_TAIL) {  // then batches of TSG_TAIL while any group is live
-                    if (h >= size || (af | ou) == GW(0)) break;
-                    Subset<GW> s[TSG_TAIL];
-#pragma unroll
-                    for (int u = 0; u < TSG_TAIL; ++u) s[u] = tab.get(cur.get(h + u));
-#pragma unroll
-                    for (int u = 0; u < TSG_TAIL; ++u) step<GW>(af, ou, s[u].f, s[u].u);
-                }
-                if (size > PF && (af | ou) != GW(0)) {
-                    const int32_t* lp = lane_lits(bd, tile, lane);
-                    for (int j = PF; j < size && (af | ou) != GW(0); j += 4) {
-                        int32_t l[4];
-                        Subset<GW> s[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) l[u] = (j + u < size) ? ld_lit_tail(lp + (j + u) * STRIDE) : p.sentinel;
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) s[u] = tab.get(l[u]);
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) step<GW>(af, ou, s[u].f, s[u].u);
+                const LaneEntry<LW>* lanes = reinterpret_cast<const LaneEntry<LW>*>(tab + p.lane_off);
+                // ---- stage 2: exact lane test per positive group ----------------
+                while (__any_sync(0xffffffffu, left != GW(0))) {
+                    bool has = false;
+                    ulonglong2 rec = make_ulonglong2(0, 0);
+                    if (left != GW(0)) {
+                        const int g = __ffsll((long long)(unsigned long long)left) - 1;
+                        left &= left - GW(1);
+                        const GroupDesc gd = p.groups[g0 + g];
+                        const LW mask = lane_test<LW>(lanes + (int64_t)g * p.vstride, cur, lp, size) & (LW)gd.lane_mask;
+                        if (mask != LW(0)) {
+                            const int hits = __popcll((unsigned long long)mask);
+                            trig_acc += hits;
+                            if (!p.emit_only) {
+                                act = __dadd_rn(act, __dmul_rn(p.inc, (double)hits));
+                                touched = true;
+                            }
+                            if (p.all_pairs || gd.tid != last_tid) {  // first triggering group of its thread
+                                last_tid = gd.tid;
+                                has = true;
+                                const uint64_t grp = (uint64_t)(g0 + g);
+                                rec = p.rec8 ? make_ulonglong2(key_hi | (grp << 32) | (uint32_t)mask, 0)
+                                             : make_ulonglong2(key_hi | grp, (unsigned long long)mask);
+                            }
+                        }
                     }
+                    rb.append(has, rec, p.out, p.out_cap, p.ctr, p.rec8, lane);
                 }
             }
         }
-        const GW word = active ? ((af | ou) & p.group_mask) : GW(0);
-
-        // ---- report slot reservation from the warp's chunk ------------------
-        const int ub = __popcll((unsigned long long)word);
-        int incl = ub;
+        if (touched) bd->acts[slot] = act;
+        if (ntile < p.n_tiles) {
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            int o = __shfl_up_sync(0xffffffffu, incl, d);
-            if (lane >= d) incl += o;
+            for (int u = 0; u < PF; ++u) cur[u] = nxt[u];
         }
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
-        if (total) {
-            if (acc.cpos + total > acc.cend) {  // chunk exhausted: pad its tail, take a new one
-                for (int q = acc.cpos + lane; q < acc.cend; q += 32)
-                    if (q < p.out_cap) st_pad(p.out, p.rec8, q);
-                const unsigned long long want = total > REPORT_CHUNK ? (unsigned long long)total : REPORT_CHUNK;
-                unsigned long long base = 0;
-                if (lane == 31) base = atomicAdd(p.ctr, want);
-                acc.cpos = (int)__shfl_sync(0xffffffffu, base, 31);
-                acc.cend = acc.cpos + (int)want;
-            }
-            int pos = acc.cpos + incl - ub;
-            const int pend = pos + ub;
-            acc.cpos += total;
-
-            // ---- stage 2: exact lane test per positive group (bitpack.py:120-135)
-            if (word) {
-                acc.pos += ub;
-                const int slot = (tile - (int)bd->tile0) * STRIDE + lane;
-                double act = 0.0;
-                if (!p.emit_only) act = bd->acts[slot];
-                const uint64_t key_hi = (uint64_t)bd->ids[slot] << (p.rec8 ? 37 : 16);  // issued early: off the report's path
-                bool touched = false;
-                int last_tid = INT_MIN;
-                GW left = word;
-                // the first triggering group of each thread emits the report
-                // (engine.py:462); every triggering group bumps the activity
-                // in group order (engine.py:460, fp64 mul then add, no FMA)
-                auto settle = [&](int g, LW mask) {
-                    if (!mask) return;
-                    const int hits = __popcll((unsigned long long)mask);
-                    acc.trig += hits;
-                    if (!p.emit_only) {
-                        act = __dadd_rn(act, __dmul_rn(p.inc, (double)hits));
-                        touched = true;
-                    }
-                    const int tid = p.tid[g];
-                    if (tid != last_tid) {
-                        last_tid = tid;
-                        bool dup = false;
-                        if (tid == p.carry_in_tid)
-                            dup = p.carry[bd->tile0 * STRIDE + slot] == (p.stamp_base | (uint32_t)tid);
-                        if (!dup) {
-                            if (pos < p.out_cap) st_record(p.out, p.rec8, pos, key_hi, (uint32_t)(p.g0 + g), (uint64_t)mask);
-                            ++pos;
-                            ++acc.rep;
-                        }
-                    }
-                };
-                auto lane_tail = [&](const LaneEntry<LW>* lt, LW& lf, LW& lo2) {
-                    if (size > PF && (lf | lo2) != LW(0)) {
-                        const int32_t* lp = lane_lits(bd, tile, lane);
-#if TSG_LANE_TAIL2
-                        for (int j = PF; j < size && (lf | lo2) != LW(0); j += 2) {  // two lane gathers in flight
-                            const int32_t l0 = ld_lit_tail(lp + j * STRIDE);
-                            const int32_t l1 = j + 1 < size ? ld_lit_tail(lp + (j + 1) * STRIDE) : p.sentinel;
-                            const LaneEntry<LW> e0 = ld_lane(lt + lit_var(l0)), e1 = ld_lane(lt + lit_var(l1));
-                            step<LW>(lf, lo2, l0 < 0 ? (e0.s & e0.t) : (e0.s & ~e0.t), ~e0.s);
-                            step<LW>(lf, lo2, l1 < 0 ? (e1.s & e1.t) : (e1.s & ~e1.t), ~e1.s);
-                        }
-#else
-                        for (int j = PF; j < size && (lf | lo2) != LW(0); ++j) {
-                            const int32_t l = ld_lit_tail(lp + j * STRIDE);
-                            const LaneEntry<LW> e = ld_lane(lt + lit_var(l));
-                            step<LW>(lf, lo2, l < 0 ? (e.s & e.t) : (e.s & ~e.t), ~e.s);
-                        }
-#endif
-                    }
-                };
-                while (left) {
-                    const int g = __ffsll((long long)(unsigned long long)left) - 1;
-                    left &= left - GW(1);
-                    const LaneEntry<LW>* lt = p.lane + (int64_t)g * p.vstride;
-                    LW lf = ~LW(0), lo2 = LW(0);
-                    lane_batch<LW>(lt, cur, 0, size, lf, lo2);
-                    if (size > 4 && (lf | lo2) != LW(0)) lane_batch<LW>(lt, cur, 4, size, lf, lo2);
-                    lane_tail(lt, lf, lo2);
-                    settle(g, (lf | lo2) & p.lane_mask[g]);
-                }
-                if (touched) bd->acts[slot] = act;
-                if (p.carry_out_tid >= 0 && last_tid == p.carry_out_tid)
-                    p.carry[bd->tile0 * STRIDE + slot] = p.stamp_base | (uint32_t)last_tid;
-                for (; pos < pend; ++pos)  // padding for reserved-but-unused slots
-                    if (pos < p.out_cap) st_pad(p.out, p.rec8, pos);
-            }
-        }
-        if (ntile >= 0) cur.take(nxt);
         tile = ntile;
     }
-}
+    if (rb.n) rb.flush(p.out, p.out_cap, p.ctr, p.rec8, lane);
 
-// pad the warp's last chunk; counters: warp reduce, block reduce, one atomic per block
-template <class LW, class GW, int WARPS>
-__device__ __forceinline__ void finish_block(const TestParams<LW, GW>& p, WarpAcc& acc, int lane, int warp,
-                                             unsigned int (&s_acc)[3][WARPS]) {
-    for (int q = acc.cpos + lane; q < acc.cend; q += 32)
-        if (q < p.out_cap) st_pad(p.out, p.rec8, q);
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-        acc.pos += __shfl_down_sync(0xffffffffu, acc.pos, d);
-        acc.trig += __shfl_down_sync(0xffffffffu, acc.trig, d);
-        acc.rep += __shfl_down_sync(0xffffffffu, acc.rep, d);
-    }
-    if (lane == 0) { s_acc[0][warp] = acc.pos; s_acc[1][warp] = acc.trig; s_acc[2][warp] = acc.rep; }
+    // counters: warp reduce, block reduce, one atomic per block
+    pos_acc = __reduce_add_sync(0xffffffffu, pos_acc);
+    trig_acc = __reduce_add_sync(0xffffffffu, trig_acc);
+    if (lane == 0) { s_acc[0][warp] = pos_acc; s_acc[1][warp] = trig_acc; }
     __syncthreads();
     if (threadIdx.x == 0) {
-        unsigned long long a = 0, bb = 0, r = 0;
-        for (int i = 0; i < WARPS; ++i) { a += s_acc[0][i]; bb += s_acc[1][i]; r += s_acc[2][i]; }
-        if (r) atomicAdd(p.ctr + 3, r);
+        unsigned long long a = 0, t = 0;
+        for (int i = 0; i < WARPS; ++i) { a += s_acc[0][i]; t += s_acc[1][i]; }
         if (!p.emit_only) {
             if (a) atomicAdd(p.ctr + 1, a);
-            if (bb) atomicAdd(p.ctr + 2, bb);
+            if (t) atomicAdd(p.ctr + 2, t);
         }
-        // the launch's last CTA re-zeroes the tile counters and the CTA count
-        // [5]; on a round's last launch it also hands the counters to the
-        // host and re-zeroes them
+        // the launch's last CTA hands the counters to the host (the round's
+        // first run) and re-zeroes them, or just re-zeroes the CTA count
         __threadfence();
         if (atomicAdd(p.ctr + 5, 1ull) == gridDim.x - 1) {
             __threadfence();
-            if (p.tiles)
-                for (int c = 0; c < TSG_DYN_NC; ++c) atomicExch(p.tiles + c * DYN_STRIDE, 0ull);
             if (p.pub) {
 #pragma unroll
                 for (int i = 0; i < 8; ++i) p.pub[i] = atomicExch(p.ctr + i, 0ull);
@@ -1039,94 +802,6 @@ __device__ __forceinline__ void finish_block(const TestParams<LW, GW>& p, WarpAc
             }
         }
     }
-}
-
-// Grid-stride variant: persistent warps over all tiles; the aggregate table
-// is gathered from L2 (GlobalTable) or held whole in shared memory (SmemTable).
-template <class LW, class GW, class TAB, int THREADS, int MINB>
-__global__ void __launch_bounds__(THREADS, MINB) k_test(const __grid_constant__ TestParams<LW, GW> p) {
-    constexpr int WARPS = THREADS / 32;
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ unsigned int s_acc[3][WARPS];
-    TAB tab;
-    if constexpr (TAB::kSmem) {  // per-block copy of the literal-code table
-        const uint4* src = reinterpret_cast<const uint4*>(p.codes);
-        uint4* dst = reinterpret_cast<uint4*>(smem);
-        for (int64_t i = threadIdx.x; i < p.codes_bytes / 16; i += THREADS) dst[i] = __ldg(src + i);
-        __syncthreads();
-        tab.code = reinterpret_cast<decltype(tab.code)>(smem);
-    } else {
-        tab.agg = p.agg;
-    }
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const int nwarps = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
-    WarpAcc acc;
-    RegRows rows;
-    if (p.dyn_tiles) {
-        const int gw = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-        const int c = gw % TSG_DYN_NC;
-        DynTiles src{p.tiles + c * DYN_STRIDE, c, (int)p.n_tiles};
-        test_tiles<LW, GW, TAB>(p, tab, p.buckets, p.nb, src, rows, lane, acc);
-    } else {
-        StrideTiles src{(int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5), nwarps, (int)p.n_tiles};
-        test_tiles<LW, GW, TAB>(p, tab, p.buckets, p.nb, src, rows, lane, acc);
-    }
-    finish_block<LW, GW, WARPS>(p, acc, lane, warp, s_acc);
-}
-
-// Slab variant: one CTA per SM.  The host schedule gives
-// every CTA one slab and its rank among the n CTAs sharing that slab (n
-// proportional to the slab's tiles).  The CTA stages the slab's aggregate
-// words in shared memory (can-be-False word per literal code, can-be-Undef
-// word per variable) plus the slab's tile descriptors, then its warps walk
-// the slab's tiles interleaved with the other CTAs of the slab
-// (tile = first + rank * WARPS + warp + k * n * WARPS), which mixes short-
-// and long-clause tiles evenly over the CTAs.  sched[c] = slab << 32 |
-// rank << 16 | n; a CTA index beyond the schedule picks up entries c + grid...
-constexpr int SLAB_DESC_MAX = 80;  // descriptors staged in shared memory (else read from global)
-
-template <class LW, class GW, int THREADS>
-__global__ void __launch_bounds__(THREADS, 1) k_test_slab(const __grid_constant__ TestParams<LW, GW> p) {
-    constexpr int WARPS = THREADS / 32;
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ unsigned int s_acc[3][WARPS];
-    __shared__ BucketDesc s_desc[SLAB_DESC_MAX];
-    __shared__ int32_t s_rows[WARPS][PF][32];
-    SlabTable<GW> tab;
-    tab.fc = reinterpret_cast<GW*>(smem);
-    tab.u = tab.fc + 2 * (int64_t)p.slab_w;
-    tab.agg = p.agg;
-    tab.w = p.slab_w;
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    WarpAcc acc;
-    for (int c = blockIdx.x; c < p.n_sched; c += gridDim.x) {
-        const uint64_t e = p.sched[c];
-        const int s = (int)(e >> 32), rank = (int)((e >> 16) & 0xFFFF), n = (int)(e & 0xFFFF);
-        const int64_t lo = (int64_t)s * p.slab_w;
-        const int d0 = p.slab_desc0[s], nd = p.slab_desc0[s + 1] - d0;
-        __syncthreads();  // the previous entry's table and descriptors are no longer read
-        GW* fc = const_cast<GW*>(tab.fc);
-        GW* us = const_cast<GW*>(tab.u);
-        for (int i = threadIdx.x; i < p.slab_w; i += THREADS) {
-            const int64_t v = lo + i;
-            AggEntry<GW> ae{~GW(0), ~GW(0), GW(0), GW(0)};
-            if (v <= p.sentinel) ae = ld_agg(p.agg + v);
-            fc[2 * i] = ae.f;      // +v is False where v can be False
-            fc[2 * i + 1] = ae.t;  // -v is False where v can be True
-            us[i] = ae.u;
-        }
-        const bool staged = nd <= SLAB_DESC_MAX;
-        if (staged)
-            for (int i = threadIdx.x; i < nd; i += THREADS) s_desc[i] = p.buckets[d0 + i];
-        __syncthreads();
-        tab.lo = (int32_t)lo;
-        StrideTiles src{(int)p.slab_tile0[s] + rank * WARPS + warp, n * WARPS, (int)p.slab_tile0[s + 1]};
-        SmemRows rows{&s_rows[warp][0][lane]};
-        test_tiles<LW, GW, SlabTable<GW>>(p, tab, staged ? s_desc : p.buckets + d0, nd, src, rows, lane, acc);
-    }
-    finish_block<LW, GW, WARPS>(p, acc, lane, warp, s_acc);
 }
 
 }  // namespace tsg

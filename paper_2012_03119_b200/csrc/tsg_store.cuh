@@ -79,7 +79,7 @@ __global__ void k_pack_records12(const tsg_report* __restrict__ in, int64_t n, u
 }
 
 // Clause lookup by engine id (tsg_get_clauses): every stored slot binary-
-// searches the sorted query ids; a hit records (part, slot) for its query.
+// searches the sorted query ids; a hit records (bucket, slot) for its query.
 __global__ void k_find_ids(const int64_t* __restrict__ ids, int64_t n, const int64_t* __restrict__ q,
                            const int64_t* __restrict__ qidx, int64_t nq, int64_t part, int64_t* __restrict__ loc) {
     int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -126,42 +126,116 @@ __global__ void k_pack_records8(const tsg_report* __restrict__ in, int64_t n, ui
     }
 }
 
-// K7: reduce keys over the whole store.  Eligible clauses (id < watermark,
-// engine.py:486) get their activity bits as key (non-negative doubles order
-// like their IEEE bit patterns); ineligible ones sort last.
-__global__ void k_reduce_keys(const double* __restrict__ acts, const int64_t* __restrict__ ids,
-                              int64_t n, int64_t base, int64_t watermark,
-                              uint64_t* __restrict__ key_act, uint64_t* __restrict__ key_id,
-                              int64_t* __restrict__ idx, unsigned long long* n_eligible) {
+// K7: reduce_store's selection (engine.py:482-490) as an exact radix select
+// on the 128-bit key (activity bits, engine id) -- non-negative doubles order
+// like their IEEE bit patterns and ids are unique, so "the `target` smallest
+// keys" is "every key <= the target-th smallest".  The store's slots are laid
+// out bucket by bucket in one flat key array, each bucket padded to a
+// multiple of KEEP_BLOCK slots; ineligible slots (id >= watermark,
+// engine.py:486) and padding carry the key_act NO_KEY.
+constexpr uint64_t NO_KEY = ~0ull;  // a NaN with the sign bit: never a stored activity
+constexpr int KEEP_BLOCK = 1024;    // compaction block (one slot per thread)
+
+__global__ void k_reduce_keys(const double* __restrict__ acts, const int64_t* __restrict__ ids, int64_t n,
+                              int64_t base, int64_t watermark, uint64_t* __restrict__ key_act,
+                              uint64_t* __restrict__ key_id, uint8_t* __restrict__ keep,
+                              unsigned long long* n_eligible) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long mine = 0;
     for (; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        bool el = ids[i] < watermark;
-        key_act[base + i] = el ? (uint64_t)__double_as_longlong(acts[i]) : ~0ull;
+        const bool el = ids[i] < watermark;
+        key_act[base + i] = el ? (uint64_t)__double_as_longlong(acts[i]) : NO_KEY;
         key_id[base + i] = (uint64_t)ids[i];
-        idx[base + i] = base + i;
+        keep[base + i] = 1;
         mine += el;
     }
-    for (int d = 16; d > 0; d >>= 1) mine += __shfl_down_sync(0xffffffffu, mine, d);
+    mine = __reduce_add_sync(0xffffffffu, (unsigned)mine);
     if ((threadIdx.x & 31) == 0 && mine) atomicAdd(n_eligible, mine);
 }
 
-__global__ void k_gather_u64(const uint64_t* __restrict__ src, const int64_t* __restrict__ idx, int64_t n,
-                             uint64_t* __restrict__ dst) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (; i < n; i += (int64_t)gridDim.x * blockDim.x) dst[i] = src[idx[i]];
-}
-
-__global__ void k_mark_doomed(const int64_t* __restrict__ idx, int64_t n, uint8_t* __restrict__ keep,
-                              const uint64_t* __restrict__ key_id, int64_t* __restrict__ doomed_ids) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        keep[idx[i]] = 0;
-        doomed_ids[i] = (int64_t)key_id[idx[i]];
+// the key's top `bits` bits (the rest zeroed), as (hi, lo)
+__device__ __forceinline__ void key_top(uint64_t a, uint64_t id, int bits, uint64_t& hi, uint64_t& lo) {
+    if (bits <= 64) {
+        hi = bits == 0 ? 0 : a & (~0ull << (64 - bits));
+        lo = 0;
+    } else {
+        hi = a;
+        lo = id & (~0ull << (128 - bits));
     }
 }
 
-// explicit delete: keep[i] = ids[i] not in sorted(del)
+// histogram of the next 8 key bits among eligible keys whose top `bits` bits are (ph, pl)
+__global__ void k_select_hist(const uint64_t* __restrict__ key_act, const uint64_t* __restrict__ key_id, int64_t n,
+                              uint64_t ph, uint64_t pl, int bits, unsigned long long* __restrict__ hist) {
+    __shared__ unsigned int sh[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t a = key_act[i];
+        if (a == NO_KEY) continue;
+        const uint64_t id = key_id[i];
+        uint64_t hi, lo;
+        key_top(a, id, bits, hi, lo);
+        if (hi != ph || lo != pl) continue;
+        const int d = bits < 64 ? (int)((a >> (56 - bits)) & 0xFF) : (int)((id >> (120 - bits)) & 0xFF);
+        atomicAdd(&sh[d], 1u);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < 256; d += blockDim.x)
+        if (sh[d]) atomicAdd(hist + d, (unsigned long long)sh[d]);
+}
+
+// doom every eligible key whose top `bits` bits are <= (ph, pl)
+__global__ void k_select_mark(const uint64_t* __restrict__ key_act, const uint64_t* __restrict__ key_id, int64_t n,
+                              uint64_t ph, uint64_t pl, int bits, uint8_t* __restrict__ keep,
+                              int64_t* __restrict__ doomed_ids, unsigned long long* n_doomed) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t a = key_act[i];
+        if (a == NO_KEY) continue;
+        uint64_t hi, lo;
+        key_top(a, key_id[i], bits, hi, lo);
+        if (hi < ph || (hi == ph && lo <= pl)) {
+            keep[i] = 0;
+            doomed_ids[atomicAdd(n_doomed, 1ull)] = (int64_t)key_id[i];
+        }
+    }
+}
+
+// Order-preserving stream compaction of the flat keep array (K8's slot
+// selection): kept slots per KEEP_BLOCK block, then -- with the host's
+// exclusive scan of those counts in blk_off -- the flat index of every kept
+// slot at its rank.
+__global__ void __launch_bounds__(KEEP_BLOCK) k_keep_count(const uint8_t* __restrict__ keep, int32_t* __restrict__ cnt) {
+    const int64_t i = (int64_t)blockIdx.x * KEEP_BLOCK + threadIdx.x;
+    const int c = __syncthreads_count(keep[i] != 0);
+    if (threadIdx.x == 0) cnt[blockIdx.x] = c;
+}
+
+__global__ void __launch_bounds__(KEEP_BLOCK) k_keep_select(const uint8_t* __restrict__ keep,
+                                                            const int64_t* __restrict__ blk_off,
+                                                            int64_t* __restrict__ sel) {
+    __shared__ int warp_sum[KEEP_BLOCK / 32];
+    const int64_t i = (int64_t)blockIdx.x * KEEP_BLOCK + threadIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const bool k = keep[i] != 0;
+    const unsigned b = __ballot_sync(0xffffffffu, k);
+    if (lane == 0) warp_sum[w] = __popc(b);
+    __syncthreads();
+    if (w == 0) {  // exclusive scan of the warp sums
+        int x = warp_sum[lane], inc = x;
+        for (int d = 1; d < 32; d <<= 1) {
+            const int o = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += o;
+        }
+        warp_sum[lane] = inc - x;
+    }
+    __syncthreads();
+    if (k) sel[blk_off[blockIdx.x] + warp_sum[w] + __popc(b & ((1u << lane) - 1u))] = i;
+}
+
+// explicit delete: keep[base + i] = ids[i] not in sorted(del)
 __global__ void k_mark_deleted(const int64_t* __restrict__ ids, int64_t n, int64_t base,
                                const int64_t* __restrict__ del, int64_t nd, uint8_t* __restrict__ keep,
                                unsigned long long* removed) {
@@ -183,8 +257,8 @@ __global__ void k_mark_deleted(const int64_t* __restrict__ ids, int64_t n, int64
 }
 
 // K8: order-preserving compaction, _SizeBucket.compact (engine.py:184-200).
-// src_slot[k] = old slot of new slot k (from a stable select of kept slots).
-__global__ void k_compact(const int64_t* __restrict__ src_slot, int64_t kept, int32_t size,
+// sel[k] - base = old slot of new slot k (k_keep_select over the bucket's range).
+__global__ void k_compact(const int64_t* __restrict__ sel, int64_t base, int64_t kept, int32_t size,
                           const int32_t* __restrict__ lits_in, const double* __restrict__ acts_in,
                           const int64_t* __restrict__ ids_in, const int32_t* __restrict__ org_in,
                           const uint64_t* __restrict__ hm_in,
@@ -193,7 +267,7 @@ __global__ void k_compact(const int64_t* __restrict__ src_slot, int64_t kept, in
                           uint64_t* __restrict__ hm_out) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     for (; k < kept; k += (int64_t)gridDim.x * blockDim.x) {
-        int64_t o = src_slot[k];
+        const int64_t o = sel[k] - base;
         acts_out[k] = acts_in[o];
         ids_out[k] = ids_in[o];
         org_out[k] = org_in[o];

@@ -142,6 +142,16 @@ class NativeEngine:
                 o += s
         return out
 
+    def set_all_pairs(self, on: bool) -> None:
+        """Emit every triggering (clause, group) -- multi_trigger's pair set --
+        instead of the first per (clause, thread) (tsg_set_all_pairs)."""
+        check(self.L.tsg_set_all_pairs(self.h, 1 if on else 0))
+
+    def tables_from(self, src: "NativeEngine") -> None:
+        """Copy src's encoded round tables into this engine over NVLink
+        (tsg_round_tables_copy); both have prepared the same round."""
+        check(self.L.tsg_round_tables_copy(self.h, src.h))
+
     def set_timing(self, every: int) -> None:
         """With timing=True: events on every `every`-th round only (tsg_set_timing)."""
         check(self.L.tsg_set_timing(self.h, every))

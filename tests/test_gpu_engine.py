@@ -131,26 +131,14 @@ def test_literal_out_of_range_raises(P):
 
 # ---- config-scale parity vs the CPU oracle ---------------------------------
 
-# stage-1 table variants, selected per engine at tsg_create:
-#   smem       whole literal-code table in shared memory (small num_vars x groups)
-#   l2         aggregate table gathered from L2, unpartitioned store
-#   slab       store partitioned into variable slabs (opt-in layout), hot prefix from shared memory
-#   smem_slab  partitioned store (hot-prefix literal order) tested by the smem kernel
-#   l2_dyn     l2 with dynamic tile counters (opt-in scheduling)
-TABLES = {"smem": {"TSG_SMEM_TABLE": "1", "TSG_SLABS": "0", "TSG_DYN_TILES": "0"},
-          "l2": {"TSG_SMEM_TABLE": "0", "TSG_SLABS": "0", "TSG_DYN_TILES": "0"},
-          "l2_dyn": {"TSG_SMEM_TABLE": "0", "TSG_SLABS": "0", "TSG_DYN_TILES": "1"},
-          "slab": {"TSG_SMEM_TABLE": "0", "TSG_SLABS": "4", "TSG_DYN_TILES": "0"},
-          "smem_slab": {"TSG_SMEM_TABLE": "1", "TSG_SLABS": "4", "TSG_DYN_TILES": "0"}}
-
-
-def use_table(monkeypatch, table):
-    for k, v in TABLES[table].items():
-        monkeypatch.setenv(k, v)
-
-
 def run_both(P, cfg_name=None, n=None, threads=None, lanes=None, nv=None, lane_width=32, group_width=32,
-             seed=0, inc=1.0, rounds=1, size_lo=2, size_hi=30):
+             seed=0, inc=1.0, rounds=1, size_lo=2, size_hi=30, all_pairs=False, packed=False):
+    """The device engine and the oracle on the same store and snapshots.
+    all_pairs: the device emits every triggering (clause, group) -- compared
+    with the oracle run with one thread per group, whose one-report-per-
+    (clause, thread) set is then exactly multi_trigger's pair set
+    (bitpack.py:282-300; tests/test_oracle_golden.py pins the oracle to it)."""
+    import os
     from paper_2012_03119_b200 import workload as W
     from paper_2012_03119_b200.native import NativeEngine
     if cfg_name:
@@ -160,21 +148,28 @@ def run_both(P, cfg_name=None, n=None, threads=None, lanes=None, nv=None, lane_w
     buckets = W.clause_buckets(n, nv, rng, size_lo, size_hi)
     flat, offs, ids = W.flatten(buckets)
     org = (ids % 7).astype(np.int32)
-    dev = NativeEngine(nv, lane_width, group_width)
+    dev = NativeEngine(nv, lane_width, group_width, report_capacity=1 << 20)
+    if all_pairs:
+        dev.set_all_pairs(True)
     dev.add_clauses(flat, offs, ids, org, 1.0)
     ora = O.OracleStore()
-    k = 0
-    for s, arr in buckets.items():
-        for row in arr:
-            ora.insert(row.tolist(), int(ids[k]), int(org[k]), 1.0)
-            k += 1
+    ora.insert_flat(flat, offs, ids, org)
+    del flat
     for r in range(rounds):
         snaps = W.snapshots(threads, lanes, nv, rng)
         gl, gt = W.groups_for(threads, lanes, lane_width)
-        dev.stage(snaps)
+        if packed:
+            from paper_2012_03119_b200.native import pack_rows
+            dev.stage_packed(pack_rows(snaps, nv, threads=os.cpu_count() or 1))
+        else:
+            dev.stage(snaps)
         res = dev.round(gl, gt, inc)
         recs = dev.fetch(res.reports)
-        orecs, octr = ora.test_round(nv, snaps, gl, gt, lane_width, group_width, inc, nthreads=8)
+        ogt = np.arange(len(gl), dtype=np.int32) if all_pairs else gt
+        orecs, octr = ora.test_round(nv, snaps, gl, ogt, lane_width, group_width, inc,
+                                     nthreads=os.cpu_count() or 8)
+        if all_pairs:
+            assert len(set(gt.tolist())) < len(gl)  # threads with several groups: pairs != reports
         recs = W.in_reference_order(recs, offs, ids, buckets, group_width)
         assert len(recs) == len(orecs)
         for f in ("engine_id", "lane_mask", "group"):
@@ -192,52 +187,62 @@ def run_both(P, cfg_name=None, n=None, threads=None, lanes=None, nv=None, lane_w
     return res
 
 
-@pytest.mark.parametrize("table", ["smem", "slab"])
-def test_c1_parity_vs_oracle(P, monkeypatch, table):
-    use_table(monkeypatch, table)
+def test_c1_parity_vs_oracle(P):
     res = run_both(P, "C1", rounds=2)
     assert res.reports > 0 and res.lane_triggers > 0
 
 
-@pytest.mark.parametrize("table", ["smem", "l2", "l2_dyn", "slab", "smem_slab"])
+def test_c2_full_size_parity(P):
+    # C2 at its full size: 1M clauses x 256 assignments (8 threads x 32), 50k vars
+    res = run_both(P, "C2", packed=True)
+    assert res.reports > 100_000
+
+
+# pair-set parity: every triggering (clause, group) at
+# the configs' full clause counts, with lane width 16 so every thread owns
+# two groups (the pair set then differs from the first-per-thread reports);
+# C3 at lane width 16 is 64 groups = two chunks, i.e. the chunk-level
+# aggregate path at full size
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3"])
+def test_pair_set_parity_full_size(P, cfg):
+    res = run_both(P, cfg, lane_width=16, all_pairs=True, packed=True)
+    assert res.reports > 0 and res.n_chunks == (2 if cfg == "C3" else 1)
+
+
 @pytest.mark.parametrize("lw,gw,threads,lanes", [(32, 32, 3, 40), (64, 64, 2, 64), (64, 8, 5, 70),
-                                                 (7, 3, 4, 20), (1, 64, 3, 30), (32, 16, 40, 32)])
-def test_widths_and_multichunk_parity(P, monkeypatch, table, lw, gw, threads, lanes):
-    # small num_vars: every table variant applies to the same inputs
-    use_table(monkeypatch, table)
+                                                 (7, 3, 4, 20), (1, 64, 3, 30), (32, 16, 40, 32),
+                                                 (1, 1, 3, 40), (4, 2, 33, 20)])
+@pytest.mark.parametrize("all_pairs", [False, True])
+def test_widths_and_multichunk_parity(P, lw, gw, threads, lanes, all_pairs):
+    # every word-width variant of the trigger kernel; (1, 1, 3, 40): 120
+    # chunks of one group, i.e. four chunks per bit of the chunk-level table
     run_both(P, n=20_000, threads=threads, lanes=lanes, nv=300, lane_width=lw, group_width=gw,
-             seed=lw * 100 + gw, rounds=2, size_lo=0, size_hi=12)
+             seed=lw * 100 + gw, rounds=2, size_lo=0, size_hi=12, all_pairs=all_pairs and lanes > lw)
 
 
-@pytest.mark.parametrize("table", ["smem", "l2", "l2_dyn", "slab"])
-def test_c2_shape_parity(P, monkeypatch, table):
-    # C2's 50k vars x 8 groups is the largest code table that fits shared memory;
-    # with it disabled the store's 3 natural slabs drive the slab kernel
-    use_table(monkeypatch, table)
-    if table == "slab":
-        monkeypatch.setenv("TSG_SLABS", "1")
-    run_both(P, n=60_000, threads=8, lanes=32, nv=50_000, seed=22)
-
-
-@pytest.mark.parametrize("table", ["l2", "slab"])
-def test_c3_shape_parity(P, monkeypatch, table):
-    # C3's 200k vars x 32 groups: 11 natural slabs (the benchmark's kernel)
-    use_table(monkeypatch, table)
-    if table == "slab":
-        monkeypatch.setenv("TSG_SLABS", "1")
+def test_c3_shape_parity(P):
     run_both(P, n=150_000, threads=32, lanes=32, nv=200_000, seed=23)
 
 
-@pytest.mark.parametrize("table", ["smem", "slab"])
-def test_long_clauses_parity(P, monkeypatch, table):
-    # hot prefixes longer than the prefetched rows, hot literals past position 64
-    use_table(monkeypatch, table)
+def test_long_clauses_parity(P):
+    # clauses far longer than the prefetched rows (and past the 58 ordered positions)
     run_both(P, n=3000, threads=4, lanes=32, nv=2000, seed=9, size_lo=100, size_hi=400)
+    run_both(P, n=3000, threads=4, lanes=64, nv=2000, seed=9, size_lo=100, size_hi=400, group_width=1,
+             all_pairs=True)
 
 
-@pytest.mark.parametrize("table", ["smem", "slab"])
-def test_reduce_and_remove_parity(P, monkeypatch, table):
-    use_table(monkeypatch, table)
+def test_non_consecutive_thread_groups_rejected(P):
+    # the one-report-per-(clause, thread) rule needs a thread's groups to be
+    # consecutive, as run_round's grouping makes them (engine.py:390-399)
+    from paper_2012_03119_b200.native import NativeEngine
+    e = NativeEngine(10)
+    with pytest.raises(ValueError):
+        e.prepare(np.array([1, 1, 1], np.int32), np.array([0, 1, 0], np.int32))
+    e.prepare(np.array([1, 1, 1], np.int32), np.array([0, 0, 1], np.int32))
+    e.close()
+
+
+def test_reduce_and_remove_parity(P):
     from paper_2012_03119_b200 import workload as W
     from paper_2012_03119_b200.native import NativeEngine
     rng = np.random.default_rng(3)
@@ -263,7 +268,11 @@ def test_reduce_and_remove_parity(P, monkeypatch, table):
         inc *= 2
     got = dev.reduce(20_000, 9_000)
     n, want = ora.reduce(20_000, 9_000)
-    assert np.array_equal(got, want)
+    assert len(got) == n == 9_000 and np.array_equal(got, np.sort(want))  # ids ascending
+    # ties at the threshold: equal activities are ordered by id (engine.py:488-489)
+    got2 = dev.reduce(10 ** 9, 1234)
+    n2, want2 = ora.reduce(10 ** 9, 1234)
+    assert np.array_equal(got2, np.sort(want2))
     dels = rng.choice(ids, 2000, replace=False)
     assert dev.remove(dels) == ora.remove(dels.tolist())
     dev.scale(1e-100)
@@ -280,18 +289,15 @@ def test_reduce_and_remove_parity(P, monkeypatch, table):
     assert res.reports == len(recs) and res.lane_triggers == ctr["lane_triggers"]
 
 
-@pytest.mark.parametrize("table", ["smem", "slab"])
-def test_report_buffer_overflow_replay(P, monkeypatch, table):
-    use_table(monkeypatch, table)
-    if table == "slab":
-        monkeypatch.setenv("TSG_SLABS", "2")
+@pytest.mark.parametrize("gw", [32, 2])
+def test_report_buffer_overflow_replay(P, gw):
     from paper_2012_03119_b200 import workload as W
     from paper_2012_03119_b200.native import NativeEngine
     rng = np.random.default_rng(11)
     nv = 50
     buckets = W.clause_buckets(50_000, nv, rng, 1, 3)
     flat, offs, ids = W.flatten(buckets)
-    dev = NativeEngine(nv, report_capacity=16)
+    dev = NativeEngine(nv, 32, gw, report_capacity=16)
     dev.add_clauses(flat, offs, ids)
     snaps = W.snapshots(4, 32, nv, rng)
     gl, gt = W.groups_for(4, 32)
@@ -299,12 +305,8 @@ def test_report_buffer_overflow_replay(P, monkeypatch, table):
     res = dev.round(gl, gt, 1.0)
     assert res.reruns == 1 and res.reports > 16
     ora = O.OracleStore()
-    k = 0
-    for s, arr in buckets.items():
-        for row in arr:
-            ora.insert(row.tolist(), int(ids[k]), 0, 1.0)
-            k += 1
-    orecs, octr = ora.test_round(nv, snaps, gl, gt, 32, 32, 1.0)
+    ora.insert_flat(flat, offs, ids)
+    orecs, octr = ora.test_round(nv, snaps, gl, gt, 32, gw, 1.0)
     recs = dev.fetch(res.reports)
     assert sorted(zip(recs["engine_id"].tolist(), recs["group"].tolist(), recs["lane_mask"].tolist())) == \
         sorted(zip(orecs["engine_id"].tolist(), orecs["group"].tolist(), orecs["lane_mask"].tolist()))
@@ -331,14 +333,18 @@ def _defined_tables(raw, nv, lw, gw, gl):
     aeb = 32 if gw > 32 else 16
     leb = 16 if lw > 32 else 8
     vstride = up(nv + 2, 4)
-    parts, off = [], 0
+    stride = up((nv + 2) * aeb, 256) + up(vstride * gw * leb, 256)  # every chunk's tables, uniform stride
+    parts = []
     for c in range(0, len(gl), gw):
         G = min(gw, len(gl) - c)
+        off = c // gw * stride
         parts.append(raw[off:off + (nv + 2) * aeb].reshape(nv + 2, aeb)[:, :3 * aeb // 4])  # t, f, u
         off += up((nv + 2) * aeb, 256)
         lane = raw[off:off + vstride * G * leb].reshape(G, vstride, leb)[:, :nv + 2]
         parts.append(lane.reshape(-1))
-        off += up(vstride * G * leb, 256)
+    if len(gl) > gw:  # the chunk-level aggregate after the chunks: t, f, u of every variable
+        off = (len(gl) + gw - 1) // gw * stride
+        parts.append(raw[off:off + (nv + 2) * 16].reshape(nv + 2, 16)[:, :12])
     return np.concatenate([x.reshape(-1) for x in parts])
 
 
@@ -453,11 +459,10 @@ def test_c3_full_size_parity(P):
 
 
 @pytest.mark.parametrize("cap", [1 << 20, 64])  # 64: every round overflows and replays with the next in flight
-@pytest.mark.parametrize("gw", [32, 1])  # gw 1: multi-chunk rounds (carry stamps per round state)
-# pinned: rows copy in asynchronously on the ingress stream; rec 8: the kernel writes 8-byte records;
-# aenc: the encoder runs on its own stream (TSG_ASYNC_ENCODE)
-@pytest.mark.parametrize("pinned,rec,aenc", [(False, 16, 0), (True, 16, 0), (False, 8, 0), (True, 8, 1)])
-def test_async_rounds_match_sync_rounds(P, monkeypatch, cap, gw, pinned, rec, aenc):
+@pytest.mark.parametrize("gw", [32, 1])  # gw 1: multi-chunk rounds (chunk-level aggregate)
+# pinned: rows copy in asynchronously on the ingress stream; rec 8: the kernel writes 8-byte records
+@pytest.mark.parametrize("pinned,rec", [(False, 16), (True, 16), (False, 8), (True, 8)])
+def test_async_rounds_match_sync_rounds(P, cap, gw, pinned, rec):
     # two rounds in flight: launch(k-1), launch(k), collect(k-1) ...: identical
     # figures, records and activities to synchronous rounds, overflow replays included
     from paper_2012_03119_b200 import workload as W
@@ -471,9 +476,7 @@ def test_async_rounds_match_sync_rounds(P, monkeypatch, cap, gw, pinned, rec, ae
         threads = 2 + k % 3
         snaps = W.snapshots(threads, 32, nv, rng)
         rounds.append((snaps, *W.groups_for(threads, 32)))
-    monkeypatch.setenv("TSG_ASYNC_ENCODE", str(aenc))
     a = NativeEngine(nv, 32, gw, report_capacity=cap)
-    monkeypatch.setenv("TSG_ASYNC_ENCODE", "0")
     b = NativeEngine(nv, 32, gw)
     if rec == 8:
         a.set_record_bytes(8)
@@ -665,10 +668,10 @@ def test_timing_sampling(P):
     e.close()
 
 
-def test_replay_with_threads_spanning_chunks_after_recycled_memory(P):
-    # regression: overflow replays of rounds whose threads span chunk
-    # boundaries, in a second engine of the process (its carry-stamp buffer
-    # recycled from the first engine's) -- every run must match the oracle
+def test_replay_with_threads_spanning_chunks(P):
+    # overflow replays of rounds whose threads span chunk boundaries (the
+    # one-report-per-(clause, thread) rule across chunks), engine after
+    # engine in one process -- every run must match the oracle
     from paper_2012_03119_b200 import workload as W
     from paper_2012_03119_b200.native import NativeEngine
     nv = 300

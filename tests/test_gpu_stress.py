@@ -45,6 +45,8 @@ def test_randomised_parity_vs_oracle():
         dev = NativeEngine(nv, lw, gw)
         if lw <= 32 and rng.random() < 0.5:
             dev.set_record_bytes(12)
+        all_pairs = rng.random() < 0.3  # every triggering (clause, group): the oracle with a thread per group
+        dev.set_all_pairs(all_pairs)
         dev.add_clauses(flat, offs, ids, org, 1.0)
         ora = O.OracleStore()
         k = 0
@@ -63,7 +65,8 @@ def test_randomised_parity_vs_oracle():
                 raise AssertionError(f"case {cases} round {r}: lw {lw} gw {gw} nv {nv} n {n} sizes {lo}-{hi} "
                                      f"threads {threads} lanes {lanes} store {len(dev)}: {exc}") from exc
             recs = dev.fetch(res.reports)
-            orecs, octr = ora.test_round(nv, snaps, gl, gt, lw, gw, inc, nthreads=8)
+            ogt = np.arange(len(gl), dtype=np.int32) if all_pairs else gt
+            orecs, octr = ora.test_round(nv, snaps, gl, ogt, lw, gw, inc, nthreads=8)
             recs = W.in_reference_order(recs, offs, ids, buckets, gw)
             assert len(recs) == len(orecs), (len(recs), len(orecs), lw, gw, nv, n)
             for f in ("engine_id", "lane_mask", "group"):
