@@ -118,6 +118,8 @@ def _declare(L):
         "tsg_aggregate_trigger": ([I32, P, P, P, I32, I32, I32, P, P, I64, P], C.c_int),
     }
     for name, (args, res) in sig.items():
+        if os.environ.get("TSG_LIB") and not hasattr(L, name):
+            continue  # an older library loaded for a side-by-side measurement
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = res

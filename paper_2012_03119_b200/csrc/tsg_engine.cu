@@ -181,7 +181,7 @@ struct tsg_engine {
     bool enc_sentinel = true;
     tsg_counters_t totals{};        // cumulative figures (tsg_counters)
     int32_t timing_every = 1;       // TSG_F_TIMING: events on rounds whose sequence is a multiple (tsg_set_timing)
-    int64_t grid[8] = {0};          // persistent grid per k_test variant (0: not computed)
+    int64_t grid[16] = {0};         // persistent grid per k_test variant (0: not computed)
 
     // a reduce selection in progress (tsg_reduce_begin .. tsg_reduce_commit):
     // the flat key arrays over the store as it was at begin
@@ -436,15 +436,16 @@ int launch_test(tsg_engine* h, int k, int emit_only) {
     p.all_pairs = R.all_pairs ? 1 : 0;
     const bool multi = rd.n_chunks > 1;
     auto* fn = multi ? k_test<LW, GW, true> : k_test<LW, GW, false>;
-    const int key = (int)(sizeof(LW) / 8) * 4 + (int)(sizeof(GW) / 8) * 2 + (multi ? 1 : 0);
+    const size_t smem = (size_t)test_smem_bytes(R.rec8);
+    const int key = (int)(sizeof(LW) / 8) * 8 + (int)(sizeof(GW) / 8) * 4 + (multi ? 2 : 0) + (R.rec8 ? 1 : 0);
     if (!h->grid[key]) {  // persistent grid: as many CTAs as fit on every SM
         int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, TEST_THREADS, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, TEST_THREADS, smem));
         h->grid[key] = (int64_t)std::max(1, per_sm) * h->nsm;
     }
     const int64_t want = (h->n_tiles + TEST_THREADS / 32 - 1) / (TEST_THREADS / 32);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, h->grid[key]));
-    fn<<<grid, TEST_THREADS, 0, h->st>>>(p);
+    fn<<<grid, TEST_THREADS, smem, h->st>>>(p);
     CK(cudaGetLastError());
     return TSG_OK;
 }

@@ -509,7 +509,12 @@ struct TestParams {
 
 constexpr int PF = 8;          // literal rows prefetched per tile
 constexpr int TEST_THREADS = 256;
-constexpr int RECBUF = 64;     // records buffered per warp
+#ifndef TSG_RECBUF  // 128: measured best (64: 0.277 ms, 128: 0.265 ms at C3)
+#define TSG_RECBUF 128
+#endif
+constexpr int RECBUF = TSG_RECBUF;  // records buffered per warp
+// dynamic shared memory of k_test: the warps' record buffers
+__host__ __device__ constexpr int test_smem_bytes(bool rec8) { return (TEST_THREADS / 32) * RECBUF * (rec8 ? 8 : 16); }
 
 __device__ __forceinline__ int lit_var(int32_t lit) { return lit < 0 ? -lit : lit; }
 
@@ -553,8 +558,8 @@ __device__ __forceinline__ void lit_fu(const AggEntry<W>* agg, int32_t lit, W& f
 // Stage 1 over one aggregate table (a chunk's groups, or the chunk-level
 // table): the live word (all_false | one_undef) of the clause whose first PF
 // literals are `r` and whose literal j sits at lp[j * STRIDE].
-template <class W>
-__device__ __forceinline__ W sweep(const AggEntry<W>* agg, const int32_t (&r)[PF], const int32_t* lp, int size,
+template <class W, class ROWS>
+__device__ __forceinline__ W sweep(const AggEntry<W>* agg, const ROWS& r, const int32_t* lp, int size,
                                    int32_t sentinel) {
     W af = ~W(0), ou = W(0);
     {  // literals 0..3 together: nearly every clause needs them (sentinel past the end)
@@ -587,23 +592,24 @@ __device__ __forceinline__ W sweep(const AggEntry<W>* agg, const int32_t (&r)[PF
 }
 
 // one batch of stage-2 literals (lane words for literals h..h+3)
-template <class LW>
-__device__ __forceinline__ void lane_batch(const LaneEntry<LW>* lt, const int32_t (&r)[PF], int h, int size,
-                                           LW& lf, LW& lo) {
+template <class LW, class ROWS>
+__device__ __forceinline__ void lane_batch(const LaneEntry<LW>* lt, const ROWS& r, int h, int size, LW& lf, LW& lo) {
     LaneEntry<LW> e[4];
+    int32_t l[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) l[u] = r[h + u];
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-        if (h + u < size) e[u] = ld_lane(lt + lit_var(r[h + u]));
+        if (h + u < size) e[u] = ld_lane(lt + lit_var(l[u]));
 #pragma unroll
     for (int u = 0; u < 4; ++u)
         if (h + u < size)
-            step<LW>(lf, lo, r[h + u] < 0 ? (e[u].s & e[u].t) : (e[u].s & ~e[u].t), ~e[u].s);
+            step<LW>(lf, lo, l[u] < 0 ? (e[u].s & e[u].t) : (e[u].s & ~e[u].t), ~e[u].s);
 }
 
 // Stage 2 (assignment_trigger, bitpack.py:120-135) for one group's lane table.
-template <class LW>
-__device__ __forceinline__ LW lane_test(const LaneEntry<LW>* lt, const int32_t (&r)[PF], const int32_t* lp,
-                                        int size) {
+template <class LW, class ROWS>
+__device__ __forceinline__ LW lane_test(const LaneEntry<LW>* lt, const ROWS& r, const int32_t* lp, int size) {
     LW lf = ~LW(0), lo = LW(0);
     lane_batch<LW>(lt, r, 0, size, lf, lo);
     if (size > 4 && (lf | lo) != LW(0)) lane_batch<LW>(lt, r, 4, size, lf, lo);
@@ -615,13 +621,16 @@ __device__ __forceinline__ LW lane_test(const LaneEntry<LW>* lt, const int32_t (
     return lf | lo;
 }
 
-// The warp's record buffer: `n` records (warp-uniform) in `buf`; flush()
-// reserves exactly n slots with one atomic and writes them coalesced.
+// The warp's record buffer in shared memory: `n` records (warp-uniform),
+// u64 in 8-byte rounds (rec8) else 16-byte tsg_report; flush() reserves
+// exactly n slots with one atomic and writes them coalesced.  (A double-
+// buffered form that issues the atomic one half-buffer early measured
+// slower: profiles/r02_k_test_variants.md.)
 struct RecBuf {
-    ulonglong2* buf;
+    unsigned char* buf;
+    int rec8;
     int n = 0;
-    __device__ __forceinline__ void flush(void* out, unsigned long long cap, unsigned long long* ctr, int rec8,
-                                          int lane) {
+    __device__ __forceinline__ void flush(void* out, unsigned long long cap, unsigned long long* ctr, int lane) {
         __syncwarp();
         unsigned long long base = 0;
         if (lane == 0) base = atomicAdd(ctr, (unsigned long long)n);
@@ -629,8 +638,8 @@ struct RecBuf {
         for (int i = lane; i < n; i += 32) {
             const unsigned long long q = base + (unsigned long long)i;
             if (q < cap) {  // past the capacity only counted: the host grows the buffer and replays
-                if (rec8) reinterpret_cast<uint64_t*>(out)[q] = buf[i].x;
-                else reinterpret_cast<ulonglong2*>(out)[q] = buf[i];
+                if (rec8) reinterpret_cast<uint64_t*>(out)[q] = reinterpret_cast<const uint64_t*>(buf)[i];
+                else reinterpret_cast<ulonglong2*>(out)[q] = reinterpret_cast<const ulonglong2*>(buf)[i];
             }
         }
         __syncwarp();
@@ -638,11 +647,15 @@ struct RecBuf {
     }
     // warp-wide: lanes with `has` append `rec`
     __device__ __forceinline__ void append(bool has, ulonglong2 rec, void* out, unsigned long long cap,
-                                           unsigned long long* ctr, int rec8, int lane) {
+                                           unsigned long long* ctr, int lane) {
         const unsigned b = __ballot_sync(0xffffffffu, has);
-        if (has) buf[n + __popc(b & ((1u << lane) - 1u))] = rec;
+        if (has) {
+            const int i = n + __popc(b & ((1u << lane) - 1u));
+            if (rec8) reinterpret_cast<uint64_t*>(buf)[i] = rec.x;
+            else reinterpret_cast<ulonglong2*>(buf)[i] = rec;
+        }
         n += __popc(b);
-        if (n > RECBUF - 32) flush(out, cap, ctr, rec8, lane);
+        if (n > RECBUF - 32) flush(out, cap, ctr, lane);
     }
 };
 
@@ -668,22 +681,39 @@ __global__ void k_top(const uint8_t* __restrict__ tables, int64_t chunk_stride, 
     }
 }
 
+// The current tile's first PF literal rows of this lane's clause (sentinel
+// past the clause end and on inactive lanes), in registers, loaded one tile
+// ahead.  (A per-warp shared-memory ring filled 1-3 tiles ahead with
+// cp.async freed 16 registers -- 4 CTAs per SM -- but measured slower at
+// every depth: profiles/r02_k_test_variants.md.)
+struct RegRows {
+    int32_t r[PF];
+    __device__ __forceinline__ int32_t operator[](int u) const { return r[u]; }
+};
+
 template <class LW, class GW, bool MULTI>
 __global__ void __launch_bounds__(TEST_THREADS, (sizeof(LW) == 8 || sizeof(GW) == 8) ? 2 : TSG_TEST_MIN_BLOCKS)
 k_test(const __grid_constant__ TestParams<LW, GW> p) {
     constexpr int WARPS = TEST_THREADS / 32;
-    __shared__ ulonglong2 s_rec[WARPS][RECBUF];
+    extern __shared__ __align__(16) unsigned char s_rec[];  // [WARPS][RECBUF] records (test_smem_bytes)
     __shared__ unsigned int s_acc[2][WARPS];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int nwarps = (int)(((int64_t)gridDim.x * TEST_THREADS) >> 5);
-    RecBuf rb{s_rec[warp]};
+    RecBuf rb{s_rec + (size_t)warp * RECBUF * (p.rec8 ? 8 : 16), p.rec8};
     unsigned int pos_acc = 0, trig_acc = 0;
     const uint32_t top_mask = MULTI ? width_mask<uint32_t>((p.n_chunks + p.per_bit - 1) / p.per_bit) : 1u;
+    // single-chunk rounds (<= 64 groups): the group table in shared memory
+    const GroupDesc* groups = p.groups;
+    if constexpr (!MULTI) {
+        __shared__ GroupDesc s_groups[MAXG];
+        for (int i = threadIdx.x; i < p.n_groups; i += TEST_THREADS) s_groups[i] = p.groups[i];
+        __syncthreads();
+        groups = s_groups;
+    }
 
     int tile = (int)(((int64_t)blockIdx.x * TEST_THREADS + threadIdx.x) >> 5);
     int bi = 0, nt0 = 0;
-    int32_t cur[PF], nxt[PF];
     if (tile < p.n_tiles) {  // first bucket by binary search, then walk forward
         int lo = 0, hi = p.nb - 1;
         while (lo < hi) {
@@ -692,89 +722,91 @@ k_test(const __grid_constant__ TestParams<LW, GW> p) {
         }
         bi = lo;
         nt0 = bi + 1 < p.nb ? (int)p.buckets[bi + 1].tile0 : INT_MAX;
-        load_rows(p.buckets + bi, tile, lane, p.sentinel, cur);
     }
+    RegRows cur, nxt;
+    if (tile < p.n_tiles) load_rows(p.buckets + bi, tile, lane, p.sentinel, cur.r);
     while (tile < p.n_tiles) {
         const BucketDesc* bd = p.buckets + bi;
-        // software pipeline: the next tile's first rows are in flight while this one is tested
         const int ntile = tile + nwarps;
+        // software pipeline: the next tile's first rows are in flight while this one is tested
         if (ntile < p.n_tiles) {
             seek_bucket(p.buckets, p.nb, ntile, bi, nt0);
-            load_rows(p.buckets + bi, ntile, lane, p.sentinel, nxt);
+            load_rows(p.buckets + bi, ntile, lane, p.sentinel, nxt.r);
         }
         const int size = bd->size;
         const bool active = lane_active(bd, tile, lane);
-        const int slot = (tile - (int)bd->tile0) * STRIDE + lane;
         const int32_t* lp = lane_lits(bd, tile, lane);
-
-        uint32_t cw = 0;  // chunk slots left positive by the chunk-level sweep
-        if (active) {
-            if constexpr (MULTI) cw = sweep<uint32_t>(p.top, cur, lp, size, p.sentinel) & top_mask;
-            else cw = 1u;
-        }
-        uint32_t wcw = __reduce_or_sync(0xffffffffu, cw);
+        // stage-2 state of this lane's clause, across the chunks of the round
         bool loaded = false, touched = false;
         double act = 0.0;
         uint64_t key_hi = 0;
         int last_tid = INT_MIN;
-        while (wcw) {
-            const int b = __ffs(wcw) - 1;
-            wcw &= wcw - 1u;
-            const bool mine = (cw >> b) & 1u;
-            const int c1 = MULTI ? min((b + 1) * p.per_bit, p.n_chunks) : 1;
-            for (int c = MULTI ? b * p.per_bit : 0; c < c1; ++c) {
-                const uint8_t* tab = p.tables + c * p.chunk_stride;
-                const int g0 = c * p.group_width;
-                const int G = min(p.group_width, p.n_groups - g0);
-                // ---- stage 1: aggregate filter (engine.py:238-254) -------------
-                GW left = GW(0);
-                if (mine)
-                    left = sweep<GW>(reinterpret_cast<const AggEntry<GW>*>(tab), cur, lp, size, p.sentinel) &
-                           width_mask<GW>(G);
-                pos_acc += __popcll((unsigned long long)left);
-                if (left != GW(0) && !loaded) {  // stage-2 entry: id and activity of the clause
-                    loaded = true;
-                    key_hi = (uint64_t)bd->ids[slot] << (p.rec8 ? 37 : 16);
-                    if (!p.emit_only) act = bd->acts[slot];
-                }
-                const LaneEntry<LW>* lanes = reinterpret_cast<const LaneEntry<LW>*>(tab + p.lane_off);
-                // ---- stage 2: exact lane test per positive group ----------------
-                while (__any_sync(0xffffffffu, left != GW(0))) {
-                    bool has = false;
-                    ulonglong2 rec = make_ulonglong2(0, 0);
-                    if (left != GW(0)) {
-                        const int g = __ffsll((long long)(unsigned long long)left) - 1;
-                        left &= left - GW(1);
-                        const GroupDesc gd = p.groups[g0 + g];
-                        const LW mask = lane_test<LW>(lanes + (int64_t)g * p.vstride, cur, lp, size) & (LW)gd.lane_mask;
-                        if (mask != LW(0)) {
-                            const int hits = __popcll((unsigned long long)mask);
-                            trig_acc += hits;
-                            if (!p.emit_only) {
-                                act = __dadd_rn(act, __dmul_rn(p.inc, (double)hits));
-                                touched = true;
-                            }
-                            if (p.all_pairs || gd.tid != last_tid) {  // first triggering group of its thread
-                                last_tid = gd.tid;
-                                has = true;
-                                const uint64_t grp = (uint64_t)(g0 + g);
-                                rec = p.rec8 ? make_ulonglong2(key_hi | (grp << 32) | (uint32_t)mask, 0)
-                                             : make_ulonglong2(key_hi | grp, (unsigned long long)mask);
-                            }
+        // stage 1 + stage 2 of chunk c for the lanes with `mine` (warp-uniform call)
+        auto test_chunk = [&](const uint8_t* tab, int g0, int G, bool mine) {
+            // ---- stage 1: aggregate filter (engine.py:238-254) -----------------
+            GW left = GW(0);
+            if (mine)
+                left = sweep<GW>(reinterpret_cast<const AggEntry<GW>*>(tab), cur, lp, size, p.sentinel) &
+                       width_mask<GW>(G);
+            pos_acc += __popcll((unsigned long long)left);
+            if (left != GW(0) && !loaded) {  // stage-2 entry: id and activity of the clause
+                loaded = true;
+                const int slot = (tile - (int)bd->tile0) * STRIDE + lane;
+                key_hi = (uint64_t)bd->ids[slot] << (p.rec8 ? 37 : 16);
+                if (!p.emit_only) act = bd->acts[slot];
+            }
+            const LaneEntry<LW>* lanes = reinterpret_cast<const LaneEntry<LW>*>(tab + p.lane_off);
+            // ---- stage 2: exact lane test per positive group --------------------
+            while (__any_sync(0xffffffffu, left != GW(0))) {
+                bool has = false;
+                ulonglong2 rec = make_ulonglong2(0, 0);
+                if (left != GW(0)) {
+                    const int g = __ffsll((long long)(unsigned long long)left) - 1;
+                    left &= left - GW(1);
+                    const LW mask = lane_test<LW>(lanes + (int64_t)g * p.vstride, cur, lp, size) &
+                                    (LW)groups[g0 + g].lane_mask;
+                    if (mask != LW(0)) {
+                        const int hits = __popcll((unsigned long long)mask);
+                        trig_acc += hits;
+                        if (!p.emit_only) {
+                            act = __dadd_rn(act, __dmul_rn(p.inc, (double)hits));
+                            touched = true;
+                        }
+                        const int tid = groups[g0 + g].tid;
+                        if (p.all_pairs || tid != last_tid) {  // first triggering group of its thread
+                            last_tid = tid;
+                            has = true;
+                            const uint64_t grp = (uint64_t)(g0 + g);
+                            rec = p.rec8 ? make_ulonglong2(key_hi | (grp << 32) | (uint32_t)mask, 0)
+                                         : make_ulonglong2(key_hi | grp, (unsigned long long)mask);
                         }
                     }
-                    rb.append(has, rec, p.out, p.out_cap, p.ctr, p.rec8, lane);
+                }
+                rb.append(has, rec, p.out, p.out_cap, p.ctr, lane);
+            }
+        };
+        if constexpr (MULTI) {
+            // chunk-level sweep first: only the chunks it leaves positive get a stage 1
+            const uint32_t cw = active ? sweep<uint32_t>(p.top, cur, lp, size, p.sentinel) & top_mask : 0u;
+            uint32_t wcw = __reduce_or_sync(0xffffffffu, cw);
+            while (wcw) {
+                const int b = __ffs(wcw) - 1;
+                wcw &= wcw - 1u;
+                const bool mine = (cw >> b) & 1u;
+                const int c1 = min((b + 1) * p.per_bit, p.n_chunks);
+                for (int c = b * p.per_bit; c < c1; ++c) {
+                    const int g0 = c * p.group_width;
+                    test_chunk(p.tables + c * p.chunk_stride, g0, min(p.group_width, p.n_groups - g0), mine);
                 }
             }
+        } else {
+            test_chunk(p.tables, 0, p.n_groups, active);
         }
-        if (touched) bd->acts[slot] = act;
-        if (ntile < p.n_tiles) {
-#pragma unroll
-            for (int u = 0; u < PF; ++u) cur[u] = nxt[u];
-        }
+        if (touched) bd->acts[(tile - (int)bd->tile0) * STRIDE + lane] = act;
+        if (ntile < p.n_tiles) cur = nxt;
         tile = ntile;
     }
-    if (rb.n) rb.flush(p.out, p.out_cap, p.ctr, p.rec8, lane);
+    if (rb.n) rb.flush(p.out, p.out_cap, p.ctr, lane);
 
     // counters: warp reduce, block reduce, one atomic per block
     pos_acc = __reduce_add_sync(0xffffffffu, pos_acc);

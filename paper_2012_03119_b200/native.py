@@ -114,6 +114,25 @@ class NativeEngine:
         check(self.L.tsg_reduce(self.h, eligible_below, target, C.byref(removed), ptr(ids)))
         return ids[:removed.value]
 
+    # split reduce selection over shards (sharded.global_reduce)
+    def reduce_begin(self, eligible_below: int) -> int:
+        n = C.c_int64(0)
+        check(self.L.tsg_reduce_begin(self.h, eligible_below, C.byref(n)))
+        return n.value
+
+    def reduce_hist(self, prefix_hi: int, prefix_lo: int, bits: int) -> np.ndarray:
+        h = np.zeros(256, np.uint64)
+        check(self.L.tsg_reduce_hist(self.h, C.c_uint64(prefix_hi), C.c_uint64(prefix_lo), bits, ptr(h)))
+        return h
+
+    def reduce_commit(self, prefix_hi: int, prefix_lo: int, bits: int) -> np.ndarray:
+        n = max(len(self), 1)
+        ids = np.zeros(n, np.int64)
+        removed = C.c_int64(0)
+        check(self.L.tsg_reduce_commit(self.h, C.c_uint64(prefix_hi), C.c_uint64(prefix_lo), bits, C.byref(removed),
+                                       ptr(ids), n))
+        return ids[:removed.value]
+
     def remove(self, ids) -> int:
         a = np.ascontiguousarray(ids, np.int64)
         removed = C.c_int64(0)

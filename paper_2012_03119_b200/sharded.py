@@ -1,27 +1,30 @@
-"""Multi-GPU sharding of the clause store (one process per GPU).
+"""Multi-GPU sharding of the clause store.
 
 Clauses are tested independently, so the store shards by
-clause: every rank owns a disjoint set of clauses in its own HBM store.  One
+clause: every shard owns a disjoint set of clauses in its own HBM store.  One
 round (engine.py:369-467) becomes
 
-    rank 0: group + stage + encode the round's snapshots (K1/K2)
-    all   : broadcast the packed tables over NVLink (NCCL)      <- the only data-path collective
-or, with the snapshot ingress split (`run_split`):
-    rank r: stage + encode the rows of its 1/N of the groups only (its own PCIe link)
-    all   : all-gather the lane entries + sum-all-reduce the aggregate words
-    all   : test the local shard (K3/K4/K5)
-    all   : gather the report records to rank 0, merge in the reference order
+    shard 0: stage + encode the round's snapshots (K1/K2)
+    all    : replicate the packed tables over NVLink     <- the only data-path collective
+or, with the snapshot ingress split:
+    shard r: stage + encode the rows of its 1/N of the groups only (its own PCIe link)
+    all    : all-gather the lane entries + sum-all-reduce the aggregate words
+then
+    all    : test the local shard (K3/K4/K5)
+    all    : gather the report records, merge in the reference order
 
-Rank 0 owns the solver-facing side (the reference's producer API,
-engine.py:305-343) and drives the round; every rank makes the same
-collective calls in the same order (`ShardedRound.run`).  Global reduce_store (engine.py:469-505) is exact:
-the doomed set is "the `target` smallest (activity, engine_id) keys among
-eligible clauses", so rank 0 finds the target-th smallest key over all
-shards and every rank removes exactly its keys <= that threshold.
+Two drivers use it: the Engine itself when EngineConfig.devices names
+several GPUs (one process, one engine per device, tables copied peer to
+peer: tsg_round_tables_copy), and one process per GPU under
+torch.distributed (NCCL; `ShardedRound`, bench.py).  The global
+reduce_store (engine.py:469-505) is exact in both: the doomed set is "the
+`target` smallest (activity, engine_id) keys among eligible clauses", found
+by a radix select whose per-pass histograms are summed over the shards
+(`select_prefix`, tsg_reduce_begin/hist/commit), after which every shard
+removes exactly its keys <= the selected prefix.
 
-The helpers below (shard assignment, record merge, threshold selection,
-array collectives) are pure host logic; tests/test_sharded_gloo.py runs them
-with world_size 2 on the gloo backend.
+The pure host logic (shard assignment, record merge, prefix selection) is
+tested on CPU with world_size 2 over gloo (tests/test_sharded_gloo.py).
 """
 from __future__ import annotations
 
@@ -30,7 +33,6 @@ from typing import Dict, List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import reports
-from ._lib import REPORT_DTYPE
 
 
 # ---------------------------------------------------------------------------
@@ -58,41 +60,66 @@ def assign_shards(sizes: Sequence[int], world: int, load: Optional[Dict[Tuple[in
 
 def merge_reports(parts: Sequence[np.ndarray], group_width: int, bucket_rank_of: Dict[int, int],
                   size_of_eid: Dict[int, int]) -> np.ndarray:
-    """Merge per-shard 16-byte records into the reference's report order.
+    """Merge per-shard records (raw egress records or decoded) into the
+    reference's report order.
 
     Within a bucket, slot order equals engine-id order (clauses are appended
     in id order and compaction preserves order, engine.py:150-163,184-200),
     so (chunk, global bucket rank, engine_id, group) is the unsharded order
     (engine.py:403-464) no matter which shard holds a clause.  Returns decoded
     records (reports.DECODED_DTYPE)."""
-    raw = [p for p in parts if len(p)]
-    dec = reports.decode(np.concatenate(raw)) if raw else np.zeros(0, reports.DECODED_DTYPE)
+    raw = [p if p.dtype == reports.DECODED_DTYPE else reports.decode(p) for p in parts if len(p)]
+    dec = np.concatenate(raw) if raw else np.zeros(0, reports.DECODED_DTYPE)
     if len(dec) == 0:
         return dec
     brank = reports.bucket_ranks(dec, size_of_eid, bucket_rank_of)
     return dec[reports.reference_order(dec, group_width, brank)]
 
 
-def kth_key(key_parts: Sequence[Tuple[np.ndarray, np.ndarray]], k: int) -> Optional[Tuple[float, int]]:
-    """The k-th smallest (activity, engine_id) over all shards (1-based), or
-    None if fewer than k keys exist (then everything eligible goes)."""
-    acts = np.concatenate([a for a, _ in key_parts]) if key_parts else np.zeros(0)
-    ids = np.concatenate([i for _, i in key_parts]) if key_parts else np.zeros(0, np.int64)
-    if k <= 0:
-        return None
-    if k > len(ids):
-        return None
-    order = np.lexsort((ids, acts))
-    j = order[k - 1]
-    return float(acts[j]), int(ids[j])
+def select_prefix(hist, k: int) -> Tuple[int, int, int]:
+    """Steer the radix select of the k smallest 128-bit keys (activity bits,
+    engine id) over any number of shards: `hist(prefix_hi, prefix_lo, bits)`
+    returns the 256-bin histogram of the next 8 key bits, summed over the
+    shards, among keys whose top `bits` bits equal the prefix.  Returns the
+    prefix and its length such that exactly k keys have top bits <= it
+    (bits = 0 and nothing selected when k == 0)."""
+    ph = pl = bits = 0
+    while k > 0 and bits < 128:
+        h = np.asarray(hist(ph, pl, bits), dtype=np.int64)
+        d = 0
+        while d < 256 and h[d] < k:
+            k -= int(h[d])
+            d += 1
+        if d == 256:
+            raise RuntimeError("reduce select: the histograms lost keys")
+        if bits < 64:
+            ph |= d << (56 - bits)
+        else:
+            pl |= d << (120 - bits)
+        bits += 8
+        if h[d] == k:
+            break
+    return ph, pl, bits
 
 
-def count_le(acts: np.ndarray, ids: np.ndarray, key: Optional[Tuple[float, int]]) -> int:
-    """How many local keys are <= the global threshold key."""
-    if key is None:
-        return len(ids)
-    a, i = key
-    return int(np.count_nonzero((acts < a) | ((acts == a) & (ids <= i))))
+def global_reduce(engines, eligible_below: int, target: int, allreduce=None) -> Tuple[int, np.ndarray]:
+    """reduce_store over clause shards (engine.py:469-505), exact: remove the
+    `target` smallest (activity, engine_id) keys among clauses with id <
+    eligible_below across all `engines` (NativeEngine shards of this
+    process).  `allreduce(np.int64 array) -> summed array` extends the sum
+    over other processes (torch.distributed).  Returns (removed count here,
+    removed ids here, ascending)."""
+    ar = allreduce or (lambda a: a)
+    n_el = ar(np.array([sum(e.reduce_begin(eligible_below) for e in engines)], np.int64))[0]
+    rem = int(min(target, n_el))
+
+    def hist(ph, pl, bits):
+        return ar(np.sum([e.reduce_hist(ph, pl, bits) for e in engines], axis=0).astype(np.int64))
+
+    ph, pl, bits = select_prefix(hist, rem) if rem > 0 else (0, 0, 0)
+    gone = [e.reduce_commit(ph, pl, bits) for e in engines]
+    ids = np.sort(np.concatenate(gone)) if gone else np.zeros(0, np.int64)
+    return len(ids), ids
 
 
 # ---------------------------------------------------------------------------
@@ -117,26 +144,40 @@ def bcast_array(dist, arr: Optional[np.ndarray], src: int, dtype) -> np.ndarray:
 
 
 def gather_records(dist, recs: np.ndarray, dst: int = 0) -> Optional[List[np.ndarray]]:
-    """Gather variable-length report record arrays to `dst` (padded all_gather
-    of the byte view, sizes first)."""
+    """Gather variable-length decoded record arrays (reports.DECODED_DTYPE)
+    to `dst` only: sizes first (all-gather of one int), then a gather of
+    the padded byte views."""
     import torch
     dev = _device(dist)
     world = dist.get_world_size()
-    raw = np.ascontiguousarray(recs).view(np.uint8)
+    raw = np.ascontiguousarray(recs, dtype=reports.DECODED_DTYPE).view(np.uint8)
     n = torch.tensor([raw.size], dtype=torch.int64, device=dev)
     sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
     dist.all_gather(sizes, n)
-    m = max(int(s.item()) for s in sizes)
+    sizes = [int(x.item()) for x in sizes]
+    m = max(sizes)
     if m == 0:
-        return [np.zeros(0, REPORT_DTYPE) for _ in range(world)] if dist.get_rank() == dst else None
+        return [np.zeros(0, reports.DECODED_DTYPE) for _ in range(world)] if dist.get_rank() == dst else None
     buf = torch.zeros(m, dtype=torch.uint8, device=dev)
     if raw.size:
         buf[:raw.size] = torch.from_numpy(raw).to(dev)
-    bufs = [torch.zeros(m, dtype=torch.uint8, device=dev) for _ in range(world)]
-    dist.all_gather(bufs, buf)
+    bufs = [torch.zeros(m, dtype=torch.uint8, device=dev) for _ in range(world)] if dist.get_rank() == dst else None
+    dist.gather(buf, bufs, dst=dst)
     if dist.get_rank() != dst:
         return None
-    return [b[:int(s.item())].cpu().numpy().view(REPORT_DTYPE) for b, s in zip(bufs, sizes)]
+    return [b[:k].cpu().numpy().view(reports.DECODED_DTYPE) for b, k in zip(bufs, sizes)]
+
+
+def allreduce_np(dist):
+    """np.int64 array -> its sum over the process group (for global_reduce)."""
+    import torch
+    dev = _device(dist)
+
+    def f(a):
+        t = torch.from_numpy(np.ascontiguousarray(a, np.int64)).to(dev)
+        dist.all_reduce(t)
+        return t.cpu().numpy()
+    return f
 
 
 def broadcast_tables(dist, engine, src: int = 0, stream=None) -> None:
@@ -223,8 +264,7 @@ class ShardedRound:
         combine_tables(self.dist, self.eng, n_groups, self.stream)
         self.stream.synchronize()
         res = self.eng.test(activity_inc)
-        recs = self.eng.fetch_raw(res.reports)
-        return res, gather_records(self.dist, recs, 0)
+        return res, gather_records(self.dist, self.eng.fetch(res.reports), 0)
 
     def run(self, group_lanes, group_tid, activity_inc: float, rows: Optional[np.ndarray] = None):
         """Rank 0 passes the round's grouped rows; every rank passes the same
@@ -237,5 +277,8 @@ class ShardedRound:
         self.eng.sync()
         broadcast_tables(self.dist, self.eng, 0, self.stream)
         res = self.eng.test(activity_inc)
-        recs = self.eng.fetch_raw(res.reports)
-        return res, gather_records(self.dist, recs, 0)
+        return res, gather_records(self.dist, self.eng.fetch(res.reports), 0)
+
+    def reduce(self, eligible_below: int, target: int) -> Tuple[int, np.ndarray]:
+        """The exact global reduce_store over every rank's shard."""
+        return global_reduce([self.eng], eligible_below, target, allreduce_np(self.dist))

@@ -1,10 +1,12 @@
 """Host-side logic of the multi-GPU path, world_size 2 on gloo (CPU).
 
-The product's shard assignment, record gather/merge and exact global-reduce
-threshold (paper_2012_03119_b200/sharded.py) are exercised across two real
-processes; each rank's shard compute is done here by the CPU oracle (test
-infrastructure), and the merged result must equal the unsharded oracle run:
-same ordered report list, same reduce victims."""
+The product's shard assignment, record gather/merge and exact global
+reduce (paper_2012_03119_b200/sharded.py: select_prefix / global_reduce,
+histograms summed over the process group) are exercised across two real
+processes; each rank's shard compute is done here by the CPU oracle and a
+numpy stand-in for tsg_reduce_begin/hist/commit (test infrastructure), and
+the merged result must equal the unsharded oracle run: same ordered report
+list, same reduce victims."""
 import os
 import socket
 
@@ -23,6 +25,45 @@ def _free_port():
     return p
 
 
+class OracleShard:
+    """tsg_reduce_begin / hist / commit over an oracle store (numpy), the
+    interface sharded.global_reduce drives."""
+
+    def __init__(self, st):
+        self.st = st
+
+    def reduce_begin(self, eligible_below):
+        b = self.st.buckets()
+        acts = np.concatenate([x[5] for x in b]) if b else np.zeros(0)
+        ids = np.concatenate([x[3] for x in b]) if b else np.zeros(0, np.int64)
+        el = ids < eligible_below
+        self.a = acts[el].view(np.uint64).astype(object)
+        self.i = ids[el].astype(object)
+        return int(el.sum())
+
+    def _top(self, bits):
+        key = [(int(a) << 64) | int(i) for a, i in zip(self.a, self.i)]
+        return [k >> (128 - bits) if bits else 0 for k in key], key
+
+    def reduce_hist(self, ph, pl, bits):
+        pref = ((ph << 64) | pl) >> (128 - bits) if bits else 0
+        top, key = self._top(bits)
+        h = np.zeros(256, np.int64)
+        for t, k in zip(top, key):
+            if t == pref:
+                h[(k >> (120 - bits)) & 0xFF] += 1
+        return h
+
+    def reduce_commit(self, ph, pl, bits):
+        if bits == 0:
+            return np.zeros(0, np.int64)
+        pref = ((ph << 64) | pl) >> (128 - bits)
+        top, key = self._top(bits)
+        doomed = [int(k & ((1 << 64) - 1)) for t, k in zip(top, key) if t <= pref]
+        self.st.remove(doomed)
+        return np.sort(np.asarray(doomed, np.int64))
+
+
 def _worker(rank, world, port, out_q):
     import sys
     sys.path.insert(0, ROOT)
@@ -30,7 +71,6 @@ def _worker(rank, world, port, out_q):
     from oracle import oracle as O
     from paper_2012_03119_b200 import sharded as S
     from paper_2012_03119_b200 import workload as W
-    from paper_2012_03119_b200._lib import REPORT_DTYPE
 
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     try:
@@ -50,16 +90,10 @@ def _worker(rank, world, port, out_q):
         gl, gt = W.groups_for(3, 32, 16)  # lane_width 16 -> 6 groups
         recs, ctr = st.test_round(nv, snaps, gl, gt, 16, 4, 1.0)  # group_width 4 -> 2 chunks
         from paper_2012_03119_b200 import reports as R
-        parts = S.gather_records(dist, R.encode(recs["engine_id"], recs["group"], recs["lane_mask"]), 0)
-        # global reduce: gather eligible keys, exact threshold, local victim counts
-        acts = np.concatenate([b[5] for b in st.buckets()]) if st.buckets() else np.zeros(0)
-        kid = np.concatenate([b[3] for b in st.buckets()]) if st.buckets() else np.zeros(0, np.int64)
-        a_all = S.gather_records(dist, np.zeros(0, REPORT_DTYPE), 0)  # empty gather
-        keyparts = [None] * world
-        dist.all_gather_object(keyparts, (acts, kid))
-        thr = S.kth_key(keyparts, 1500)
-        local = S.count_le(acts, kid, thr)
-        removed, victims = st.reduce(10 ** 9, local)
+        parts = S.gather_records(dist, R.decode(R.encode(recs["engine_id"], recs["group"], recs["lane_mask"])), 0)
+        a_all = S.gather_records(dist, np.zeros(0, R.DECODED_DTYPE), 0)  # empty gather
+        # exact global reduce: histograms summed over the ranks
+        removed, victims = S.global_reduce([OracleShard(st)], 10 ** 9, 1500, S.allreduce_np(dist))
         all_victims = [None] * world
         dist.all_gather_object(all_victims, sorted(victims.tolist()))
         if rank == 0:
@@ -118,15 +152,32 @@ def test_assign_shards_balances_every_bucket():
         assert c.max() - c.min() <= 1
 
 
-def test_kth_key_and_count_le_are_exact():
-    from paper_2012_03119_b200.sharded import count_le, kth_key
+def test_select_prefix_is_exact():
+    # the radix select over shards: exactly k keys <= the selected prefix,
+    # with heavy activity ties (ids break them, engine.py:488-489)
+    from paper_2012_03119_b200.sharded import select_prefix
     rng = np.random.default_rng(1)
-    acts = [rng.integers(0, 5, 50).astype(float), rng.integers(0, 5, 70).astype(float)]
-    ids = [rng.permutation(200)[:50].astype(np.int64), 200 + rng.permutation(200)[:70].astype(np.int64)]
-    for k in (1, 17, 60, 120):
-        thr = kth_key(list(zip(acts, ids)), k)
-        assert sum(count_le(a, i, thr) for a, i in zip(acts, ids)) == k
-    assert kth_key(list(zip(acts, ids)), 500) is None
+    shards = []
+    for n in (50, 70, 0):
+        acts = rng.integers(0, 5, n).astype(np.float64).view(np.uint64).astype(object)
+        ids = rng.permutation(10 ** 6)[:n].astype(object)
+        shards.append([(int(a) << 64) | int(i) for a, i in zip(acts, ids)])
+    keys = sorted(sum(shards, []))
+
+    def hist(ph, pl, bits):
+        pref = ((ph << 64) | pl) >> (128 - bits) if bits else 0
+        h = np.zeros(256, np.int64)
+        for k in keys:
+            if (k >> (128 - bits) if bits else 0) == pref:
+                h[(k >> (120 - bits)) & 0xFF] += 1
+        return h
+
+    for k in (1, 17, 60, 119, 120):
+        ph, pl, bits = select_prefix(hist, k)
+        pref = ((ph << 64) | pl) >> (128 - bits)
+        assert sum(1 for x in keys if x >> (128 - bits) <= pref) == k
+        assert max(x for x in keys if x >> (128 - bits) <= pref) == keys[k - 1]
+    assert select_prefix(hist, 0) == (0, 0, 0)
 
 
 def test_split_groups_equal_contiguous_shares():
