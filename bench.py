@@ -18,14 +18,18 @@ busy_seconds, instrumentation.py:248-250).
 * cpu_baseline: the C oracle (a port of the reference algorithm) on the
   box's host cores, rank 0 only, on a bounded slice of the same workload.
 
-Multi-GPU (torchrun): every rank holds its own C3-sized clause shard
-(weak scaling) and the round's packed rows (the host sends each GPU its copy
-over that GPU's own PCIe link); every rank encodes the round's tables and
-tests its shard -- no data-path collective -- and the time is the max over
-ranks.  `--tables bcast`: rank 0 encodes and NCCL broadcasts the tables over
-NVLink instead.  `--e2e-ingress split`: in the e2e leg each rank copies in
-only the rows of its 1/N of the groups and the encoded tables are combined
-by an all-gather + sum all-reduce (sharded.combine_tables).
+Multi-GPU (torchrun, one rank per GPU): strong scaling by default -- the
+C3 store of 10M clauses is split across the ranks (W.shard: every size
+bucket round-robin), so every GPU holds 10M/N clauses.  The round's tables
+reach every shard over NCCL (`--tables split`, default): rank r encodes only
+its 1/N of the groups (tsg_round_encode_groups) and an all-gather of the
+lane entries plus a sum all-reduce of the aggregate words complete the
+tables on every rank (sharded.combine_tables, on the engine's stream);
+`--tables bcast`: rank 0 encodes and broadcasts them; `--tables
+replicated`: every rank encodes all groups (no collective).  In the e2e
+leg each rank copies in only its groups' rows over its own PCIe link
+(split) and copies its own records out.  Time = max over ranks;
+`--scaling weak` gives every rank its own C3-sized shard instead.
 """
 from __future__ import annotations
 
@@ -127,11 +131,18 @@ class ClockSampler:
 
 # ---------------------------------------------------------------------------
 
-def build_shard(cfg: W.Config, rank: int):
+def build_shard(cfg: W.Config, rank: int, world: int, scaling: str):
+    """This rank's clauses: strong -- its share of the one C3 store (same
+    seed on every rank, global engine ids); weak -- a C3-sized store of its
+    own."""
+    if scaling == "strong":
+        buckets = W.clause_buckets(cfg.n_clauses, cfg.num_vars, np.random.default_rng(cfg.seed), cfg.size_lo,
+                                   cfg.size_hi)
+        flat, offs, ids = W.shard(buckets, world, rank) if world > 1 else W.flatten(buckets)
+        return flat, offs, ids
     rng = np.random.default_rng(cfg.seed + 1000 * rank)
     buckets = W.clause_buckets(cfg.n_clauses, cfg.num_vars, rng, cfg.size_lo, cfg.size_hi)
-    flat, offs, ids = W.flatten(buckets, id0=rank * cfg.n_clauses)
-    return buckets, flat, offs, ids
+    return W.flatten(buckets, id0=rank * cfg.n_clauses)
 
 
 def algorithmic_bytes(sum_lits, num_vars, A, G, P, rec_bytes=16):
@@ -142,7 +153,8 @@ def algorithmic_bytes(sum_lits, num_vars, A, G, P, rec_bytes=16):
 
 def cpu_baseline(cfg: W.Config, snaps, gl, gt, slice_clauses=2_000_000, repeats=1):
     """The C oracle (port of the reference algorithm, oracle/tsg_oracle.c) with
-    all host threads on a bounded slice of the workload."""
+    all host threads on a bounded slice of the workload (the full-config CPU
+    figure is the --impl reference arm)."""
     from oracle import oracle as O
     rng = np.random.default_rng(cfg.seed + 777)
     b = W.clause_buckets(slice_clauses, cfg.num_vars, rng, cfg.size_lo, cfg.size_hi)
@@ -195,6 +207,11 @@ def reference_python_rate(cfg: W.Config, snaps, n_clauses=200_000):
 
 
 def run_reference(args, cfg):
+    """The reference arm: the CPU implementation of the path on this box's
+    host cores, on the SAME workload as the GPU arm -- every step one round of
+    the full config (C3: all 10M clauses x 1024 assignments) through the C
+    port of the reference algorithm (oracle/tsg_oracle.c, engine.py:238-467,
+    all host threads; the reference itself is pure Python).  Rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -202,11 +219,12 @@ def run_reference(args, cfg):
     snaps = W.snapshots(cfg.threads, cfg.lanes, cfg.num_vars, rng)
     gl, gt = W.groups_for(cfg.threads, cfg.lanes)
     from oracle import oracle as O
-    n_sample = min(2_000_000, cfg.n_clauses)  # the same bounded slice as the cpu_baseline leg
-    b = W.clause_buckets(n_sample, cfg.num_vars, np.random.default_rng(cfg.seed + 777), cfg.size_lo, cfg.size_hi)
+    b = W.clause_buckets(cfg.n_clauses, cfg.num_vars, np.random.default_rng(cfg.seed), cfg.size_lo, cfg.size_hi)
     flat, offs, ids = W.flatten(b)
+    del b
     st = O.OracleStore()
     st.insert_flat(flat, offs, ids)
+    del flat
     threads = os.cpu_count() or 1
     for _ in range(args.warmup):
         st.test_round(cfg.num_vars, snaps, gl, gt, 32, 32, 1.0, nthreads=threads)
@@ -217,18 +235,23 @@ def run_reference(args, cfg):
         tests += ctr["lane_tests"]
     dt = time.perf_counter() - t0
     v = tests / dt
-    sample = (f"{n_sample} clauses of the {cfg.name} generator x {snaps.shape[0]} assignments per step, "
+    sample = (f"the full {cfg.name} workload per step ({cfg.n_clauses} clauses x {snaps.shape[0]} assignments), "
               f"oracle/tsg_oracle.c (C port of engine.py:238-467) with {threads} pthreads")
+    try:
+        ref_py = reference_python_rate(cfg, snaps)
+    except Exception as exc:  # side figure, never fatal
+        ref_py = {"value": None, "error": repr(exc)}
     print(json.dumps({
         "impl": "reference", "metric": "clause_assignment_tests_per_second", "value": v,
         "unit": "clause_assignment_tests/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "strong" if args.gpus > 1 else "weak",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {cfg.n_clauses} clauses (size U[2,30]) x {cfg.assignments} "
-                               f"assignments ({cfg.threads} threads x {cfg.lanes}), {cfg.num_vars} vars",
-                   "parallelism": f"host threads x{threads}"},
+                               f"assignments ({cfg.threads} threads x {cfg.lanes}), {cfg.num_vars} vars, seed {cfg.seed}",
+                   "same_config": True, "parallelism": f"host threads x{threads}"},
         "cpu_baseline": {"value": v, "unit": "clause_assignment_tests/s", "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "reference_python": ref_py},
         "e2e": {"value": v, "unit": "clause_assignment_tests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -242,13 +265,16 @@ def main():
     ap.add_argument("--config", default="C3", choices=sorted(W.CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
-    ap.add_argument("--tables", default="replicated", choices=["replicated", "bcast"],
-                    help="N>1: every rank encodes the round's tables from its own copy of the rows "
-                         "(default; no data-path collective), or rank 0 encodes and NCCL broadcasts them")
-    ap.add_argument("--e2e-ingress", default="replicated", choices=["split", "replicated"],
-                    help="N>1 e2e: every rank copies in all rows (default, no collective), or each rank "
-                         "copies in only its share of the round's groups and the encoded tables are combined "
-                         "over the process group (split; SURVEY.md §8(e))")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N>1: split the one store across the ranks (strong, default) or give every rank a "
+                         "store of the config's size (weak)")
+    ap.add_argument("--tables", default="split", choices=["split", "bcast", "replicated"],
+                    help="N>1: how the round's tables reach every shard -- each rank encodes its 1/N of the groups "
+                         "and NCCL all-gathers them (split, default), rank 0 encodes and NCCL broadcasts (bcast), "
+                         "or every rank encodes everything (replicated, no collective)")
+    ap.add_argument("--verify", action="store_true",
+                    help="after timing: gather every rank's records of one round to rank 0 and compare them with "
+                         "the unsharded store's records on rank 0's GPU (adds 'verify' to the line)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = W.CONFIGS[args.config]
@@ -271,14 +297,17 @@ def main():
     if world > 1:
         import torch.distributed as dist
         if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # the init lines show every rank joining
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
+    tables_mode = args.tables if world > 1 else "replicated"
 
-    from paper_2012_03119_b200.native import NativeEngine
+    from paper_2012_03119_b200 import sharded as S
+    from paper_2012_03119_b200.native import NativeEngine, pack_rows, packed_words
 
     t_build = time.perf_counter()
-    buckets, flat, offs, ids = build_shard(cfg, rank)
+    flat, offs, ids = build_shard(cfg, rank, world, args.scaling)
     sum_lits = int(offs[-1])
     eng = NativeEngine(cfg.num_vars, 32, 32, device=local, timing=True, report_capacity=8 << 20)
     # kernel durations from CUDA events around every TIMING_EVERY-th round of
@@ -286,7 +315,9 @@ def main():
     # round for the four), which would otherwise inflate ms_per_step
     eng.set_timing(TIMING_EVERY)
     eng.add_clauses(flat, offs, ids)
-    del flat
+    n_local = len(ids)
+    max_id = int(ids.max(initial=0))
+    del flat, ids
     rng = np.random.default_rng(cfg.seed + 999)
     snaps = W.snapshots(cfg.threads, cfg.lanes, cfg.num_vars, rng)  # same on every rank
     gl, gt = W.groups_for(cfg.threads, cfg.lanes)
@@ -296,53 +327,52 @@ def main():
     # 8-byte records (engine id << 37 | group << 32 | lane mask), written by
     # the trigger kernel itself: ids < 2^27 and 32 groups here; 12 bytes is
     # the general egress form
-    rec_bytes = 8 if (int(ids.max(initial=0)) < (1 << 27) and len(gl) <= 32) else 12
+    rec_bytes = 8 if (max_id < (1 << 27) and len(gl) <= 32) else 12
     eng.set_record_bytes(rec_bytes)
 
     stream = torch.cuda.ExternalStream(eng.stream(), device=torch.device("cuda", local))
+    # the round's groups this rank encodes (split tables): equal contiguous shares
+    split = S.split_groups(G, world, rank) if tables_mode == "split" else None
+    if tables_mode == "split" and split is None:
+        raise SystemExit(f"--tables split needs the {G} groups to divide over {world} ranks")
+    split_row0 = int(sum(gl[:split[0]])) if split else 0
+    split_rows = int(sum(gl[split[0]:split[1]])) if split else A
     # device-resident snapshots for the `value` leg, in the ingress format the
     # solver threads hand over: packed rows, 2 bits per variable (tsg_pack_rows)
-    from paper_2012_03119_b200.native import pack_rows, packed_words
     pw = packed_words(cfg.num_vars)
     host_threads = os.cpu_count() or 1
     d_packed = torch.from_numpy(pack_rows(snaps, cfg.num_vars, threads=host_threads).view(np.int64)).to(
         f"cuda:{local}")
     torch.cuda.synchronize()
-    eng.stage_packed_ptr(d_packed.data_ptr(), A, pw, on_device=True)
+    if tables_mode == "split":  # this rank's groups' rows only
+        eng.stage_packed_ptr(d_packed.data_ptr() + split_row0 * pw * 8, split_rows, pw, on_device=True)
+    else:
+        eng.stage_packed_ptr(d_packed.data_ptr(), A, pw, on_device=True)
     eng.prepare(gl, gt)
 
-    tables_t = None
-    if dist is not None and args.tables == "bcast":
-        ptr, nbytes = eng.tables()
-
-        class _CAI:
-            __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3,
-                                        "stream": None}
-        tables_t = torch.as_tensor(_CAI(), device=f"cuda:{local}")
-
-    launches_per_step = 2 * ((G + 31) // 32)
-
-    def step():
-        if rank == 0:
+    def encode_round():
+        """The round's tables on this rank: encoded, or completed over NCCL."""
+        if tables_mode == "split":
+            eng.encode_groups(split[0], split[1], rank == 0)
+            S.combine_tables(dist, eng, G, stream)
+        elif tables_mode == "bcast":
+            if rank == 0:
+                eng.encode()
+            S.broadcast_tables(dist, eng, 0, stream)
+        else:
             eng.encode()
-        if tables_t is not None:
-            with torch.cuda.stream(stream):
-                dist.broadcast(tables_t, src=0)
-        return eng.test(1.0)
+
+    launches_per_step = 2  # encode + test (k_test handles every chunk in one launch)
 
     def run_steps(n, record):
-        """n rounds.  Device rounds back to back with two in flight: round
-        i is encoded and launched (tsg_round_launch) before round i-1 is
-        collected (tsg_round_collect), so the GPU always has the next round
-        queued.  --tables bcast: encode, NCCL broadcast, test."""
-        if tables_t is not None:
-            for _ in range(n):
-                record(step())
-            return
-        for i in range(n):  # two rounds in flight
+        """n device rounds back to back with two in flight: round i is encoded
+        (and its tables completed over NCCL) and launched (tsg_round_launch)
+        before round i-1 is collected (tsg_round_collect), so the GPU always
+        has the next round queued."""
+        for i in range(n):
             if i >= 2:
                 record(eng.collect())  # round i-2 owns the table slot round i encodes into
-            eng.encode()
+            encode_round()
             eng.launch(1.0)
         for _ in range(min(n, 2)):
             record(eng.collect())
@@ -377,194 +407,212 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
     elapsed_ms = e0.elapsed_time(e1)
-    if tables_t is not None:  # the broadcast tables must be identical on every rank
-        with torch.cuda.stream(stream):
-            cs = torch.stack([tables_t.to(torch.int64).sum(), (tables_t.to(torch.int64) * 131).remainder(
-                1000003).sum()])
-        lo, hi = cs.clone(), cs.clone()
-        dist.all_reduce(lo, op=dist.ReduceOp.MIN)
-        dist.all_reduce(hi, op=dist.ReduceOp.MAX)
-        if not torch.equal(lo, hi):
-            raise RuntimeError("round tables differ across ranks after the broadcast")
+    tests_per_step = res.lane_tests
+    reports_total = float(np.mean(reports))
     if dist is not None:
         t = torch.tensor([elapsed_ms], device=f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed_ms = float(t.item())
+        t = torch.tensor([tests_per_step, reports_total], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t)  # whole-job tests and records per step
+        tests_per_step, reports_total = int(t[0].item()), float(t[1].item())
     ms_per_step = elapsed_ms / args.steps
-    tests_per_step = res.lane_tests * world
     value = tests_per_step / (ms_per_step * 1e-3)
 
     # ---- e2e: host buffers through the C ABI -------------------------------
-    # Primary: the step's input is the round's snapshots as packed 2-bit rows in
-    # pinned host memory -- the ingress format solver threads produce when they
-    # submit (tsg_pack_rows replaces the int8 values.copy() the reference solver
-    # makes per snapshot, solver.py:280-282) -- copied H2D (tsg_stage_packed),
-    # the round, and the report records copied D2H (tsg_fetch_reports), every
-    # step, wall clock.  Also measured: the host packing itself and the same
-    # step from raw int8 rows (205 MB H2D).
+    # The step's input is the round's snapshots as packed 2-bit rows in pinned
+    # host memory -- the ingress format solver threads produce when they submit
+    # (tsg_pack_rows replaces the int8 values.copy() the reference solver makes
+    # per snapshot, solver.py:280-282) -- copied H2D (tsg_stage_packed), the
+    # round, and the report records copied D2H, every step, wall clock.  N>1
+    # (split): each rank copies in only its groups' rows and copies out its
+    # own records, both over its own PCIe link.  Also measured: the host
+    # packing itself and the same step from raw int8 rows (205 MB H2D).
     e2e = None
     e2e_steps = args.e2e_steps or max(3, args.steps)
-    if True:  # every rank, over its own PCIe link; time = max over ranks
-        from paper_2012_03119_b200 import _lib
-        import ctypes as C
-        rec_buf = torch.empty((8 << 20) * 16, dtype=torch.uint8).pin_memory()
-        rec_bufs = [torch.empty((8 << 20) * 16, dtype=torch.uint8).pin_memory() for _ in range(2)]
-        k_step = [0]
-        h_packed_t = torch.empty((A, pw), dtype=torch.int64).pin_memory()
-        h_packed = h_packed_t.numpy().view(np.uint64)
-        h_int8_t = torch.from_numpy(snaps).pin_memory()
-        L = eng.L
+    from paper_2012_03119_b200 import _lib
+    import ctypes as C
+    cap_recs = 8 << 20
+    rec_buf = torch.empty(cap_recs * 16, dtype=torch.uint8).pin_memory()
+    rec_bufs = [torch.empty(cap_recs * 16, dtype=torch.uint8).pin_memory() for _ in range(2)]
+    k_step = [0]
+    h_packed_t = torch.empty((A, pw), dtype=torch.int64).pin_memory()
+    h_packed = h_packed_t.numpy().view(np.uint64)
+    h_int8_t = torch.from_numpy(snaps).pin_memory()
+    L = eng.L
 
-        def finish(r):
-            got = C.c_int64(0)
-            n = min(r.reports, (8 << 20))
-            _lib.check(L.tsg_fetch_reports(eng.h, C.c_void_p(rec_buf.data_ptr()), n, C.byref(got)))
-            return r
+    def finish(r):
+        got = C.c_int64(0)
+        _lib.check(L.tsg_fetch_reports(eng.h, C.c_void_p(rec_buf.data_ptr()), min(r.reports, cap_recs),
+                                       C.byref(got)))
+        return r
 
-        # N>1: split ingress -- rank r copies in only the rows
-        # of its 1/N of the groups over its own PCIe link, encodes them, and
-        # the tables are combined over NCCL before every rank tests its shard
-        from paper_2012_03119_b200 import sharded as S
-        split = (S.split_groups(G, world, rank) if (dist is not None and args.e2e_ingress == "split")
-                 else None)
-        split_row0, split_rows = 0, A
-        if split is not None:
-            split_row0 = int(sum(gl[:split[0]]))
-            split_rows = int(sum(gl[split[0]:split[1]]))
+    def fetch_async(r):
+        got = C.c_int64(0)
+        buf = rec_bufs[k_step[0] % 2]
+        k_step[0] += 1
+        _lib.check(L.tsg_fetch_reports_async(eng.h, C.c_void_p(buf.data_ptr()), min(r.reports, cap_recs),
+                                             C.byref(got)))
 
-        def step_packed():
-            _lib.check(L.tsg_stage_packed(eng.h, C.c_void_p(h_packed_t.data_ptr()), A, pw, 0))
-            return finish(eng.round(gl, gt, 1.0))
+    def stage_host():
+        _lib.check(L.tsg_stage_packed(eng.h, C.c_void_p(h_packed_t.data_ptr() + split_row0 * pw * 8),
+                                      split_rows, pw, 0))
 
-        def fetch_async(r):
-            got = C.c_int64(0)
-            buf = rec_bufs[k_step[0] % 2]
-            k_step[0] += 1
-            _lib.check(L.tsg_fetch_reports_async(eng.h, C.c_void_p(buf.data_ptr()), min(r.reports, 8 << 20),
-                                                 C.byref(got)))
-
-        def loop_pipelined(k, warm=0):
-            # same transfers per round, pipelined over three engines of the
-            # link: round i+1's rows copy in on the ingress stream (two staging
-            # buffers) while round i is encoded and tested and round i-1's
-            # records copy out on the egress stream (tsg_fetch_reports_async)
-            # The first `warm` steps fill the pipeline; the clock starts at
-            # step `warm` (round warm-1 still in flight) and stops when the
-            # last round's records are on the host.
-            r, pending, w0 = None, 0, None
-            eng.prepare(gl, gt)
-            for i in range(warm + k):
-                if i == warm:
-                    w0 = time.perf_counter()
-                _lib.check(L.tsg_stage_packed(eng.h, C.c_void_p(h_packed_t.data_ptr() + split_row0 * pw * 8),
-                                              split_rows, pw, 0))
-                if pending:
-                    r = eng.collect()
-                    fetch_async(r)
-                    pending -= 1
-                if split is not None:  # this rank's groups, then all-gather / all-reduce the tables
-                    eng.encode_groups(split[0], split[1], rank == 0)
-                    S.combine_tables(dist, eng, G, stream)
-                else:
-                    eng.encode()
-                eng.launch(1.0)
-                pending += 1
-            while pending:
+    def loop_pipelined(k, warm=0):
+        # same transfers per round, pipelined over three engines of the link:
+        # round i+1's rows copy in on the ingress stream (two staging buffers)
+        # while round i is encoded and tested and round i-1's records copy out
+        # on the egress stream (tsg_fetch_reports_async).  The first `warm`
+        # steps fill the pipeline; the clock starts at step `warm` (round
+        # warm-1 still in flight) and stops when the last round's records are
+        # on the host.
+        r, pending, w0 = None, 0, None
+        eng.prepare(gl, gt)
+        for i in range(warm + k):
+            if i == warm:
+                w0 = time.perf_counter()
+            stage_host()
+            if pending:
                 r = eng.collect()
                 fetch_async(r)
                 pending -= 1
-            return w0, r
+            encode_round()
+            eng.launch(1.0)
+            pending += 1
+        while pending:
+            r = eng.collect()
+            fetch_async(r)
+            pending -= 1
+        return w0, r
 
-        def step_int8():
-            _lib.check(L.tsg_stage_snapshots(eng.h, C.c_void_p(h_int8_t.data_ptr()), A, cfg.num_vars + 1, 0))
-            return finish(eng.round(gl, gt, 1.0))
+    def step_packed():
+        stage_host()
+        eng.prepare(gl, gt)
+        encode_round()
+        return finish(eng.test(1.0))
 
-        def timed_loop(fn, k):
-            eng.sync()
-            _lib.check(L.tsg_fetch_wait(eng.h))
-            w0, r = fn(k, warm=3)
-            eng.sync()
-            _lib.check(L.tsg_fetch_wait(eng.h))
-            return (time.perf_counter() - w0) / k * 1e3, r, r.reports * rec_bytes + 48
+    def step_int8():
+        _lib.check(L.tsg_stage_snapshots(eng.h, C.c_void_p(h_int8_t.data_ptr()), A, cfg.num_vars + 1, 0))
+        return finish(eng.round(gl, gt, 1.0))
 
-        def timed(fn, k):
-            for _ in range(2):
-                fn()
-            eng.sync()
-            _lib.check(L.tsg_fetch_wait(eng.h))
-            w0 = time.perf_counter()
-            d2h = 0
-            for _ in range(k):
-                r = fn()
-                d2h += r.reports * rec_bytes + 48
-            eng.sync()
-            _lib.check(L.tsg_fetch_wait(eng.h))
-            return (time.perf_counter() - w0) / k * 1e3, r, d2h // k
+    def timed_loop(fn, k):
+        eng.sync()
+        _lib.check(L.tsg_fetch_wait(eng.h))
+        w0, r = fn(k, warm=3)
+        eng.sync()
+        _lib.check(L.tsg_fetch_wait(eng.h))
+        return (time.perf_counter() - w0) / k * 1e3, r, r.reports * rec_bytes + 48
 
-        err = None
-        ms = ms_seq = ms8 = float("inf")
-        pack_ms, d2h, r, r8 = None, 0, res, res
-        try:
+    def timed(fn, k):
+        for _ in range(2):
+            fn()
+        eng.sync()
+        _lib.check(L.tsg_fetch_wait(eng.h))
+        if dist is not None:
+            dist.barrier()
+        w0 = time.perf_counter()
+        d2h = 0
+        for _ in range(k):
+            r = fn()
+            d2h += r.reports * rec_bytes + 48
+        eng.sync()
+        _lib.check(L.tsg_fetch_wait(eng.h))
+        return (time.perf_counter() - w0) / k * 1e3, r, d2h // k
+
+    err = None
+    ms = ms_seq = ms8 = float("inf")
+    pack_ms, d2h, r, r8 = None, 0, res, res
+    try:
+        pack_rows(snaps, cfg.num_vars, out=h_packed, threads=host_threads)
+        p0 = time.perf_counter()
+        for _ in range(3):
             pack_rows(snaps, cfg.num_vars, out=h_packed, threads=host_threads)
-            p0 = time.perf_counter()
-            for _ in range(3):
-                pack_rows(snaps, cfg.num_vars, out=h_packed, threads=host_threads)
-            pack_ms = (time.perf_counter() - p0) / 3 * 1e3
-            if dist is not None:
-                dist.barrier()
-            ms, r, d2h = timed_loop(loop_pipelined, e2e_steps)
-            ms_seq, _, _ = timed(step_packed, max(3, e2e_steps // 2))
+        pack_ms = (time.perf_counter() - p0) / 3 * 1e3
+        if dist is not None:
+            dist.barrier()
+        ms, r, d2h = timed_loop(loop_pipelined, e2e_steps)
+        ms_seq, _, _ = timed(step_packed, max(3, e2e_steps // 2))
+        if world == 1:
             ms8, r8, _ = timed(step_int8, max(3, e2e_steps // 2))
-        except Exception as exc:  # reported in the line, never fatal to it
-            err = repr(exc)
-        if dist is not None:  # max over ranks (inf marks a failed rank)
-            t = torch.tensor([ms, ms_seq, ms8], dtype=torch.float64, device=f"cuda:{local}")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms, ms_seq, ms8 = (float(x) for x in t.tolist())
-        try:
-            if err is not None or not np.isfinite(min(ms, ms_seq)):
-                raise RuntimeError(err or "e2e failed on another rank")
-            # two operating modes of the same API, both measured; the engine's
-            # faster mode on this box is the headline (the other is reported)
-            mode = "pipelined" if ms <= ms_seq else "sequential"
-            best = min(ms, ms_seq)
-            e2e = {"value": r.lane_tests * world / (best * 1e-3), "unit": "clause_assignment_tests/s",
-                   "h2d_bytes_per_step": int((split_rows if mode == "pipelined" else A) * pw * 8) * world,
-                   "d2h_bytes_per_step": int(d2h) * world,
-                   "ms_per_step": best,
-                   "ingress": ("split: each rank copies in its 1/N of the groups' rows; tables combined by NCCL "
-                               "all-gather + all-reduce" if (split is not None and mode == "pipelined")
-                               else "every rank copies in all rows"),
-                   "input": "packed 2-bit snapshot rows in pinned host memory (solver-side ingress format)",
-                   "mode": mode,
-                   "pipelined_ms_per_step": ms,
-                   "pipelined": "round i+1's rows copy in (ingress stream) while round i is encoded and tested "
-                                "and round i-1's records copy out (egress stream)",
-                   "sequential_ms_per_step": ms_seq,
-                   "host_pack_ms_per_round": pack_ms, "host_pack_threads": host_threads,
-                   "int8_rows": {"value": r8.lane_tests * world / (ms8 * 1e-3), "ms_per_step": ms8,
-                                 "h2d_bytes_per_step": int(A * (cfg.num_vars + 1))}}
-        except Exception as exc:  # reported in the line, never fatal to it
-            e2e = {"value": None, "error": repr(exc)}
+    except Exception as exc:  # reported in the line, never fatal to it
+        err = repr(exc)
+    tot = [float(r.lane_tests), float(d2h)]
+    if dist is not None:  # max over ranks (inf marks a failed rank); sums of the per-rank work
+        t = torch.tensor([ms, ms_seq, ms8], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, ms_seq, ms8 = (float(x) for x in t.tolist())
+        t = torch.tensor(tot, dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t)
+        tot = [float(x) for x in t.tolist()]
+    try:
+        if err is not None or not np.isfinite(min(ms, ms_seq)):
+            raise RuntimeError(err or "e2e failed on another rank")
+        # two operating modes of the same API, both measured; the engine's
+        # faster mode on this box is the headline (the other is reported)
+        mode = "pipelined" if ms <= ms_seq else "sequential"
+        best = min(ms, ms_seq)
+        e2e = {"value": tot[0] / (best * 1e-3), "unit": "clause_assignment_tests/s",
+               "h2d_bytes_per_step": int(split_rows * pw * 8) * world,
+               "d2h_bytes_per_step": int(tot[1]),
+               "ms_per_step": best,
+               "ingress": ("split: each rank copies in its 1/N of the groups' rows; tables completed by NCCL "
+                           "all-gather + all-reduce" if split is not None else "every rank copies in all rows"
+                           if tables_mode == "replicated" else "every rank copies in all rows; rank 0's tables "
+                           "broadcast"),
+               "egress": "every rank copies out its own records",
+               "input": "packed 2-bit snapshot rows in pinned host memory (solver-side ingress format)",
+               "mode": mode,
+               "pipelined_ms_per_step": ms,
+               "pipelined": "round i+1's rows copy in (ingress stream) while round i is encoded and tested "
+                            "and round i-1's records copy out (egress stream)",
+               "sequential_ms_per_step": ms_seq,
+               "host_pack_ms_per_round": pack_ms, "host_pack_threads": host_threads}
+        if world == 1:
+            e2e["int8_rows"] = {"value": r8.lane_tests / (ms8 * 1e-3), "ms_per_step": ms8,
+                                "h2d_bytes_per_step": int(A * (cfg.num_vars + 1))}
+    except Exception as exc:  # reported in the line, never fatal to it
+        e2e = {"value": None, "error": repr(exc)}
+
+    verify = None
+    if args.verify:  # one more round: the shards' records together == the unsharded store's
+        eng.stage_packed_ptr(d_packed.data_ptr() + split_row0 * pw * 8, split_rows, pw, on_device=True)
+        eng.prepare(gl, gt)
+        encode_round()
+        rv = eng.test(1.0)
+        mine = eng.fetch(rv.reports)
+        parts = S.gather_records(dist, mine, 0) if dist is not None else [mine]
+        if rank == 0:
+            got = np.sort(np.concatenate(parts), order=["engine_id", "group"])
+            ref = NativeEngine(cfg.num_vars, 32, 32, device=local, report_capacity=8 << 20)
+            f_all, o_all, i_all = build_shard(cfg, 0, 1, "strong") if args.scaling == "strong" else (None,) * 3
+            if f_all is not None:
+                ref.add_clauses(f_all, o_all, i_all)
+                del f_all
+                ref.stage_packed_ptr(d_packed.data_ptr(), A, pw, on_device=True)
+                rr = ref.round(gl, gt, 1.0)
+                want = np.sort(ref.fetch(rr.reports), order=["engine_id", "group"])
+                verify = {"records": int(len(got)), "match_unsharded": bool(len(got) == len(want) and all(
+                    np.array_equal(got[f], want[f]) for f in ("engine_id", "group", "lane_mask")))}
+            ref.close()
 
     # ---- roofline of the trigger kernel --------------------------------------
     peak, peak_kind = load_peaks()
     test_ms = [t for t in test_ms if t >= 0]  # sampled rounds (tsg_set_timing)
     enc_ms = [t for t in enc_ms if t >= 0]
     test_ms_avg = float(np.mean(test_ms))
-    P = float(np.mean(reports))
+    P = float(np.mean(reports))  # this rank's records per round
     b_alg = algorithmic_bytes(sum_lits, cfg.num_vars, A, G, P, 8 if rec_bytes == 8 else 16)
     achieved = b_alg / (test_ms_avg * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": load_traffic(cfg.name), "kernel": "tsg::k_test",
+                "traffic": load_traffic(cfg.name) if world == 1 else None, "kernel": "tsg::k_test",
                 "kernel_ms": test_ms_avg, "encode_ms": float(np.mean(enc_ms)),
                 "kernel_ms_samples": len(test_ms),
                 "kernel_timing": f"CUDA events on the library stream around every {TIMING_EVERY}th round "
-                                 f"of the timed region",
+                                 f"of the timed region (rank {rank})",
                 "algorithmic_bytes": b_alg, "peak_kind": peak_kind}
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             cpu = cpu_baseline(cfg, snaps, gl, gt)
         except Exception as exc:  # reported, never fatal
@@ -576,7 +624,7 @@ def main():
         # random table gathers, from the committed ncu capture) per SM clock,
         # against the measured random-gather ceiling
         try:
-            sectors = load_traffic(cfg.name + "_l2_read_sectors")
+            sectors = load_traffic(cfg.name + "_l2_read_sectors") if world == 1 else None
             nsm = torch.cuda.get_device_properties(local).multi_processor_count
             mhz = float(clocks.get("sm_mhz") or 0) if isinstance(clocks, dict) else 0.0
             if sectors and mhz > 0:
@@ -584,33 +632,39 @@ def main():
                 roofline["l2_gather"] = {
                     "sectors_per_launch": sectors, "achieved_sectors_per_clk_per_sm": per_clk,
                     "ceiling_sectors_per_clk_per_sm": L2_GATHER_CEILING, "frac": per_clk / L2_GATHER_CEILING,
-                    "ceiling_source": "tools/microbench/gather_modes.cu: random 16-byte gathers from an "
-                                      "L2-resident table as divergent LDGs, B200"}
+                    "ceiling_source": "profiles/r01_gather_modes.md (tools/microbench/gather_modes.cu): random "
+                                      "16-byte gathers from an L2-resident table as divergent LDGs, B200"}
         except Exception:
             pass
+        strong = args.scaling == "strong" or world == 1
         line = {
             "metric": "clause_assignment_tests_per_second", "value": value, "unit": "clause_assignment_tests/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-            "data": "synthetic",
-            "config": {"workload": f"{cfg.name}: {cfg.n_clauses} clauses/GPU (size U[2,30], mean 16) x "
-                                   f"{A} assignments ({cfg.threads} threads x {cfg.lanes}), {cfg.num_vars} vars, "
-                                   f"seed {cfg.seed}",
-                       "clauses_per_gpu": cfg.n_clauses, "assignments": A, "groups": G, "num_vars": cfg.num_vars,
-                       "sum_literals_per_gpu": sum_lits, "reports_per_step": P,
+            "higher_is_better": True, "scaling": "strong" if (args.scaling == "strong" and world > 1) else "weak",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": (f"{cfg.name}: {cfg.n_clauses} clauses (size U[2,30], mean 16) x "
+                                    f"{A} assignments ({cfg.threads} threads x {cfg.lanes}), {cfg.num_vars} vars, "
+                                    f"seed {cfg.seed}" + (f"; {'split across' if strong else 'per GPU on'} {world} GPUs"
+                                                          if world > 1 else "")),
+                       "clauses_per_gpu": n_local, "assignments": A, "groups": G, "num_vars": cfg.num_vars,
+                       "sum_literals_per_gpu": sum_lits, "reports_per_step": reports_total,
                        "l2": (f"inputs larger than L2 ({4 * sum_lits / 1e6:.0f} MB clause literals + "
                               f"{A * pw * 8 / 1e6:.0f} MB packed snapshot rows per GPU vs 126 MB L2)"
                               if 4 * sum_lits + A * pw * 8 > 126e6 else
                               f"inputs fit in L2 ({4 * sum_lits / 1e6:.0f} MB + {A * pw * 8 / 1e6:.0f} MB): "
                               f"a parity config, not the headline workload (C3)"),
                        "parallelism": "1 GPU" if world == 1 else (
-                           f"clause shards x{world}; tables broadcast from rank 0 (NCCL)" if args.tables == "bcast"
-                           else f"clause shards x{world}; every rank encodes the round's tables from its copy of "
-                                f"the packed rows (no data-path collective)")},
+                           f"clause shards x{world}; " + {
+                               "split": "each rank encodes 1/N of the groups, tables completed by NCCL all-gather "
+                                        "(lane entries) + all-reduce (aggregate words) on the engine stream",
+                               "bcast": "rank 0 encodes, NCCL broadcasts the tables",
+                               "replicated": "every rank encodes all groups (no data-path collective)"}[tables_mode])},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,
             "build_seconds": build_s,
         }
+        if verify is not None:
+            line["verify"] = verify
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()

@@ -109,6 +109,22 @@ def flatten(buckets: Dict[int, np.ndarray], id0: int = 0) -> Tuple[np.ndarray, n
     return flat, off, (np.concatenate(ids) if ids else np.zeros(0, np.int64))
 
 
+def shard(buckets: Dict[int, np.ndarray], world: int, rank: int) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """Rank `rank`'s clause shard of a store filled by `flatten(buckets)`:
+    rows rank, rank + world, ... of every size bucket (balanced buckets,
+    SURVEY.md §8(e)), with the global engine ids flatten assigns.  The union
+    over ranks is the whole store."""
+    sub: Dict[int, np.ndarray] = {}
+    idl: List[np.ndarray] = []
+    nxt = 0
+    for s, arr in buckets.items():
+        sub[s] = arr[rank::world]
+        idl.append(nxt + np.arange(rank, arr.shape[0], world, dtype=np.int64))
+        nxt += arr.shape[0]
+    flat, off, _ = flatten(sub)
+    return flat, off, (np.concatenate(idl) if idl else np.zeros(0, np.int64))
+
+
 def in_reference_order(dec: np.ndarray, offsets: np.ndarray, ids: np.ndarray,
                        buckets: Dict[int, np.ndarray], group_width: int) -> np.ndarray:
     """Decoded report records (reports.decode) of a store filled by `flatten`

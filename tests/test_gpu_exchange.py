@@ -9,7 +9,11 @@ reference orchestrator unchanged.
   test_acceptance.py:382-442), so solver threads import exactly the clauses
   the reference engine would have reported.
 
-Skipped when the reference package is not installed (baseline/_ref).
+The live-loop tests need the reference package (baseline/_ref); the
+replay test below does not: it feeds the GPU Engine the reference solver's
+recorded rounds (tests/golden/c5_replay_*.npz, tests/golden/make_c5_replay.py)
+and checks every drained report list against what the reference engine
+delivered.
 """
 import numpy as np
 import pytest
@@ -27,6 +31,40 @@ def X():
     if X.import_reference() is None:
         pytest.skip("reference package not installed (baseline/_ref)")
     return X
+
+
+@pytest.mark.parametrize("name", ["w32", "w8x2"])
+def test_replay_reference_solver_rounds(name):
+    # every recorded round rebuilt on the GPU Engine through the reference API:
+    # the same clauses under the same engine ids (inserted in id order, so the
+    # size buckets are created in the reference's order), the round's
+    # snapshots submitted per thread, then run_round and drain_reports --
+    # per-destination report lists (engine id, lane mask, literals) in the
+    # reference's order and the RoundResult must be identical
+    require_device()
+    import paper_2012_03119_b200 as P
+    from golden_io import c5_replays, c5_round
+    fx = c5_replays()[name]
+    nv, th, lw, gw = (int(fx[k]) for k in ("num_vars", "threads", "lane_width", "group_width"))
+    n_reports = 0
+    for k in range(int(fx["rounds"])):
+        clauses, live, snaps, reps, result = c5_round(fx, k)
+        eng = P.Engine(nv, th, P.EngineConfig(lane_width=lw, group_width=gw))
+        for lits in clauses:
+            eng.add_clause(lits, origin=0)
+        eng.run_round()  # integrate (no snapshots: no activity or counter effects)
+        eng.remove_clauses([e for e in range(len(clauses)) if e not in live])
+        for i, (tid, v) in enumerate(snaps):
+            assert eng.submit_assignment(P.AssignmentSnapshot(int(tid), v, i))
+        r = eng.run_round()
+        assert [r.reports_emitted, r.clauses_tested, r.assignments_consumed, r.aggregate_tests_negative] == result
+        for t in range(th):
+            got = [(d.engine_id, d.lane_mask, d.lits) for d in eng.drain_reports(t)]
+            want = [(e, m, clauses[e]) for dst, e, m in reps if dst == t]
+            assert got == want, (name, k, t)
+        n_reports += len(reps)
+        eng.close()
+    assert n_reports > 0
 
 
 def check_trace(eng, nv):
