@@ -268,6 +268,30 @@ int tsg_fetch_wait(tsg_engine* h);
  * bytes, when every engine id ever added is < 2^27 and the round has <= 32
  * groups (a fetch that does not fit fails with TSG_ECAPACITY). */
 int tsg_set_record_bytes(tsg_engine* h, int32_t bytes);
+/* The last collected round's records of n_h engines (one engine, or clause
+ * shards that ran the same round) in the reference's delivery order
+ * (engine.py:403-414, 462-464): destination thread major (ascending tid),
+ * then chunk, creation rank of the clause's size bucket (rank_of_size[size]
+ * = the caller's global bucket creation order), engine id, group.  Ordered
+ * on hs[0]'s device (keys per shard, stable LSD radix sort); writes engine
+ * ids (eid_bytes 4 or 8 per id), lane masks (mask_bytes 4 or 8) and, if
+ * `groups` is not NULL, the int32 group of each record into the host arrays
+ * and, per destination d (the d-th run of equal tids in the
+ * round's groups), its record count into dest_counts[d].  *n = records;
+ * TSG_ECAPACITY if they exceed cap or a field does not fit. */
+int tsg_fetch_ordered(tsg_engine* const* hs, int32_t n_h, const int32_t* rank_of_size, int32_t n_sizes,
+                      void* eids, int32_t eid_bytes, void* masks, int32_t mask_bytes, int32_t* groups,
+                      int64_t* dest_counts, int64_t cap, int64_t* n);
+/* The next round's packed rows from n_segs host segments (segment i: rows[i]
+ * rows at segs[i], pitch_words apart), concatenated in order -- e.g. the
+ * per-thread snapshot queues in pinned memory -- staged like
+ * tsg_stage_packed (ingress stream; the segments must stay unchanged until
+ * the round encoded from them is collected). */
+int tsg_stage_packed_segments(tsg_engine* h, const uint64_t* const* segs, const int64_t* rows, int32_t n_segs,
+                              int64_t pitch_words);
+/* Page-locked host memory (cudaMallocHost) for ingress rows and records. */
+int tsg_host_alloc(int64_t bytes, void** p);
+int tsg_host_free(void* p);
 /* device pointer + count of the round's records (for device-side consumers) */
 int tsg_reports_device(tsg_engine* h, void** device_ptr, int64_t* n);
 int tsg_sync(tsg_engine* h);

@@ -60,7 +60,7 @@ EXPORTS = (
     "tsg_fetch_reports_async", "tsg_fetch_wait", "tsg_round_launch", "tsg_round_collect",
     "tsg_set_record_bytes", "tsg_get_clauses", "tsg_counters", "tsg_set_timing", "tsg_round_encode_groups",
     "tsg_round_layout", "tsg_set_all_pairs", "tsg_round_tables_copy", "tsg_reduce_begin", "tsg_reduce_hist",
-    "tsg_reduce_commit",
+    "tsg_reduce_commit", "tsg_fetch_ordered", "tsg_stage_packed_segments", "tsg_host_alloc", "tsg_host_free",
 )
 
 _lib = None
@@ -91,6 +91,10 @@ def _declare(L):
         "tsg_round_layout": ([P, pI64, pI64, pI64, pI64], C.c_int),
         "tsg_reduce": ([P, I64, I64, pI64, P], C.c_int),
         "tsg_reduce_begin": ([P, I64, pI64], C.c_int),
+        "tsg_fetch_ordered": ([P, I32, P, I32, P, I32, P, I32, P, P, I64, pI64], C.c_int),
+        "tsg_stage_packed_segments": ([P, P, P, I32, I64], C.c_int),
+        "tsg_host_alloc": ([I64, C.POINTER(P)], C.c_int),
+        "tsg_host_free": ([P], C.c_int),
         "tsg_reduce_hist": ([P, C.c_uint64, C.c_uint64, I32, P], C.c_int),
         "tsg_reduce_commit": ([P, C.c_uint64, C.c_uint64, I32, pI64, P, I64], C.c_int),
         "tsg_remove_clauses": ([P, P, I64, pI64], C.c_int),

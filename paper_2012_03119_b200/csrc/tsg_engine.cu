@@ -20,6 +20,7 @@
 #include "../../include/tsg.h"
 #include "tsg_kernels.cuh"
 #include "tsg_store.cuh"
+#include "tsg_sort.cuh"
 
 using namespace tsg;
 
@@ -173,6 +174,8 @@ struct tsg_engine {
     int32_t record_bytes = 16;      // egress record format (tsg_set_record_bytes)
     bool all_pairs = false;         // tsg_set_all_pairs
     int64_t max_id = -1;            // largest engine id ever added (8-byte records need < 2^27)
+    int32_t* size_of_id = nullptr;  // clause size by engine id (record ordering, tsg_fetch_ordered)
+    int64_t size_of_id_cap = 0;
     bool oob = false;               // a stored literal may exceed num_vars (checked before testing)
     int64_t round_seq = 0;
     int enc_attr = 0;               // k_encode_packed32 shared-memory attribute set, per (GPW, GW)
@@ -645,6 +648,7 @@ int tsg_destroy(tsg_engine* h) {
         for (auto& b : h->buckets) bucket_free(h, b);
         dfree(h, h->rows_own); dfree(h, h->pbuf[0]); dfree(h, h->pbuf[1]); dfree(h, h->tables); dfree(h, h->d_desc);
         dfree(h, h->mctr);
+        dfree(h, h->size_of_id);
         for (auto& R : h->rs) { dfree(h, R.ctr); dfree(h, R.out); dfree(h, R.out12); dfree(h, R.d_groups); }
         cudaStreamSynchronize(h->st);
     }
@@ -756,6 +760,33 @@ int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, 
         CK(cudaGetLastError());
         b.count += k;
         CK(cudaStreamSynchronize(h->st));  // host vectors go out of scope
+    }
+    // clause size by engine id (ids are non-negative and, per the reference,
+    // below 2^40 here): the record ordering looks up each record's bucket
+    if (h->max_id < ((int64_t)1 << 40)) {
+        const int64_t need = h->max_id + 1;
+        if (need > h->size_of_id_cap) {
+            int64_t nc = std::max<int64_t>(need, 2 * h->size_of_id_cap);
+            int32_t* np = nullptr;
+            CKR(dalloc(h, (void**)&np, nc * 4));
+            if (h->size_of_id) CK(cudaMemcpyAsync(np, h->size_of_id, h->size_of_id_cap * 4, cudaMemcpyDeviceToDevice, h->st));
+            dfree(h, h->size_of_id);
+            h->size_of_id = np;
+            h->size_of_id_cap = nc;
+        }
+        std::vector<int32_t> hs(n);
+        for (int64_t i = 0; i < n; ++i) hs[i] = (int32_t)(offsets[i + 1] - offsets[i]);
+        int64_t* did = nullptr;
+        int32_t* dsz = nullptr;
+        CKR(dalloc(h, (void**)&did, n * 8));
+        CKR(dalloc(h, (void**)&dsz, n * 4));
+        CK(cudaMemcpyAsync(did, ids, n * 8, cudaMemcpyHostToDevice, h->st));
+        CK(cudaMemcpyAsync(dsz, hs.data(), n * 4, cudaMemcpyHostToDevice, h->st));
+        k_set_sizes<<<grid_for(n), 256, 0, h->st>>>(did, dsz, n, h->size_of_id);
+        CK(cudaGetLastError());
+        dfree(h, did);
+        dfree(h, dsz);
+        CK(cudaStreamSynchronize(h->st));  // hs goes out of scope
     }
     h->totals.clauses_added += n;
     return TSG_OK;
@@ -1653,6 +1684,237 @@ int tsg_sync(tsg_engine* h) {
 int tsg_stream(tsg_engine* h, void** stream) {
     CKR(validate_handle(h));
     *stream = (void*)h->st;
+    return TSG_OK;
+}
+
+// Pinned host memory for ingress rows / egress records (page-locked, so the
+// copies run at link rate and asynchronously).
+int tsg_host_alloc(int64_t bytes, void** p) {
+    if (!p || bytes < 0) return fail(TSG_EINVAL, "bad arguments");
+    *p = nullptr;
+    if (bytes == 0) return TSG_OK;
+    CK(cudaMallocHost(p, (size_t)bytes));
+    return TSG_OK;
+}
+
+int tsg_host_free(void* p) {
+    if (p) CK(cudaFreeHost(p));
+    return TSG_OK;
+}
+
+// The next round's packed rows from several host segments (segment i:
+// rows[i] rows at segs[i], pitch_words apart), concatenated in order -- the
+// per-thread snapshot queues of the Engine, grouped by tid, without a host
+// copy.  Same staging buffers and ingress stream as tsg_stage_packed.
+int tsg_stage_packed_segments(tsg_engine* h, const uint64_t* const* segs, const int64_t* rows, int32_t n_segs,
+                              int64_t pitch_words) {
+    CKR(validate_handle(h));
+    if (n_segs < 0 || (n_segs > 0 && (!segs || !rows))) return fail(TSG_EINVAL, "bad arguments");
+    DevGuard g(h->dev);
+    const int64_t words = packed_words(h->V);
+    if (pitch_words < words) return fail(TSG_EINVAL, "packed pitch %lld < %lld words", (long long)pitch_words, (long long)words);
+    int64_t n_rows = 0;
+    for (int32_t i = 0; i < n_segs; ++i) {
+        if (rows[i] < 0) return fail(TSG_EINVAL, "segment %d: negative row count", i);
+        n_rows += rows[i];
+    }
+    h->n_rows = n_rows;
+    h->packed = true;
+    h->pstaged = false;
+    if (n_rows == 0) return TSG_OK;
+    const int b = h->pk ^ 1;
+    const int64_t need = words * n_rows;
+    CK(cudaStreamWaitEvent(h->ingress, h->ev_read[b], 0));
+    if (need > h->pbuf_cap[b]) {
+        dfree(h, h->pbuf[b]);
+        h->pbuf[b] = nullptr;
+        const int64_t cap = std::max(need, h->pbuf_cap[b] * 2);
+        CKR(dalloc(h, (void**)&h->pbuf[b], cap * 8));
+        h->pbuf_cap[b] = cap;
+        CK(cudaEventRecord(h->ev_staged[b], h->st));
+        CK(cudaStreamWaitEvent(h->ingress, h->ev_staged[b], 0));
+    }
+    int64_t r = 0;
+    for (int32_t i = 0; i < n_segs; ++i) {
+        if (!rows[i]) continue;
+        if (pitch_words == words)
+            CK(cudaMemcpyAsync(h->pbuf[b] + r * words, segs[i], rows[i] * words * 8, cudaMemcpyDefault, h->ingress));
+        else
+            CK(cudaMemcpy2DAsync(h->pbuf[b] + r * words, words * 8, segs[i], pitch_words * 8, words * 8, rows[i],
+                                 cudaMemcpyDefault, h->ingress));
+        r += rows[i];
+    }
+    CK(cudaEventRecord(h->ev_staged[b], h->ingress));
+    h->pk = b;
+    h->pstaged = true;
+    h->prows = h->pbuf[b];
+    h->ppitch = words;
+    return TSG_OK;
+}
+
+namespace {
+int bits_for(int64_t max_value) {  // bits to hold 0..max_value
+    int b = 0;
+    while (b < 63 && (max_value >> b) > 0) ++b;
+    return b;
+}
+}  // namespace
+
+// The last collected round's records of one or more engines (clause shards
+// of one round: same groups) in the reference's delivery order: destination
+// thread (ascending tid) major, then chunk, creation rank of the clause's
+// size bucket (rank_of_size[size], the caller's global bucket order), engine
+// id, group (engine.py:403-414, 462-464).  Keys are built on each engine's
+// device, the shards' records gathered to hs[0]'s device, sorted there
+// (stable LSD radix sort, tsg_sort.cuh) and written into the host arrays:
+// eids (eid_bytes 4 or 8), masks (mask_bytes 4 or 8), and per destination
+// the record count (dest_counts[d], d = index of the thread's run of groups).
+int tsg_fetch_ordered(tsg_engine* const* hs, int32_t n_h, const int32_t* rank_of_size, int32_t n_sizes,
+                      void* eids, int32_t eid_bytes, void* masks, int32_t mask_bytes, int32_t* groups,
+                      int64_t* dest_counts, int64_t cap, int64_t* n) {
+    if (!hs || n_h < 1 || !n || !dest_counts || !rank_of_size || n_sizes < 1) return fail(TSG_EINVAL, "bad arguments");
+    if ((eid_bytes != 4 && eid_bytes != 8) || (mask_bytes != 4 && mask_bytes != 8))
+        return fail(TSG_EINVAL, "eid_bytes / mask_bytes must be 4 or 8");
+    tsg_engine* h0 = hs[0];
+    CKR(validate_handle(h0));
+    const RoundDesc& rd = h0->rs[h0->fetch_rs].fl;
+    const bool rec8 = h0->rs[h0->fetch_rs].rec8;
+    int64_t total = 0, max_id = 0;
+    for (int32_t s = 0; s < n_h; ++s) {
+        CKR(validate_handle(hs[s]));
+        const auto& R = hs[s]->rs[hs[s]->fetch_rs];
+        if (R.fl.n_groups != rd.n_groups || R.fl.gtid != rd.gtid || R.rec8 != rec8 ||
+            hs[s]->cfg.group_width != h0->cfg.group_width)
+            return fail(TSG_EINVAL, "engine %d's last round differs from engine 0's", s);
+        if (!hs[s]->size_of_id && R.n_out) return fail(TSG_EINVAL, "engine %d has no clause size table", s);
+        total += R.n_out;
+        max_id = std::max(max_id, hs[s]->max_id);
+    }
+    // destinations: runs of equal tids in round order
+    std::vector<int32_t> dest_of(rd.n_groups);
+    int32_t n_dest = 0;
+    for (int g = 0; g < rd.n_groups; ++g) {
+        if (g > 0 && rd.gtid[g] != rd.gtid[g - 1]) ++n_dest;
+        dest_of[g] = n_dest;
+    }
+    n_dest = rd.n_groups ? n_dest + 1 : 0;
+    for (int32_t d = 0; d < n_dest; ++d) dest_counts[d] = 0;
+    *n = total;
+    if (total == 0) return TSG_OK;
+    if (total > cap) return fail(TSG_ECAPACITY, "%lld records exceed %lld", (long long)total, (long long)cap);
+    if (total >= ((int64_t)1 << 32)) return fail(TSG_ECAPACITY, "%lld records exceed the 32-bit sort index", (long long)total);
+    if (eid_bytes == 4 && max_id >= ((int64_t)1 << 31)) return fail(TSG_ECAPACITY, "engine ids do not fit 4 bytes");
+    if (mask_bytes == 4 && h0->cfg.lane_width > 32) return fail(TSG_ECAPACITY, "lane masks do not fit 4 bytes");
+    const int gw = h0->cfg.group_width;
+    const int dest_bits = bits_for(n_dest - 1), chunk_bits = bits_for(rd.n_chunks - 1);
+    const int rank_bits = bits_for(n_sizes - 1), id_bits = bits_for(max_id), g_bits = bits_for(gw - 1);
+    const int key_bits = dest_bits + chunk_bits + rank_bits + id_bits + g_bits;
+    if (key_bits > 64) return fail(TSG_ECAPACITY, "record order key needs %d bits", key_bits);
+    std::vector<uint64_t> gkey(rd.n_groups);
+    for (int g = 0; g < rd.n_groups; ++g) gkey[g] = ((uint64_t)dest_of[g] << chunk_bits) | (uint64_t)(g / gw);
+    const int64_t rec_bytes = rec8 ? 8 : 16;
+    // device 0: concatenated records, keys / vals double buffers, counters
+    DevGuard g0(h0->dev);
+    uint8_t* recs = nullptr;
+    uint64_t *k0 = nullptr, *k1 = nullptr;
+    uint32_t *v0 = nullptr, *v1 = nullptr, *hist = nullptr, *rowsum = nullptr;
+    unsigned long long *gcount = nullptr, *gscratch = nullptr;
+    uint8_t* out = nullptr;
+    const int64_t nblk = (total + SORT_TILE - 1) / SORT_TILE;
+    if (n_h > 1) CKR(dalloc(h0, (void**)&recs, total * rec_bytes));
+    CKR(dalloc(h0, (void**)&k0, total * 8));
+    CKR(dalloc(h0, (void**)&k1, total * 8));
+    CKR(dalloc(h0, (void**)&v0, total * 4));
+    CKR(dalloc(h0, (void**)&v1, total * 4));
+    CKR(dalloc(h0, (void**)&hist, 256 * nblk * 4 + 256 * 4));
+    rowsum = hist + 256 * nblk;
+    CKR(dalloc(h0, (void**)&gcount, (int64_t)rd.n_groups * 8));
+    if (n_h > 1) CKR(dalloc(h0, (void**)&gscratch, (int64_t)rd.n_groups * 8));
+    const int64_t eid_sec = round_up(total * eid_bytes, 256), mask_sec = round_up(total * mask_bytes, 256);
+    CKR(dalloc(h0, (void**)&out, eid_sec + mask_sec + (groups ? total * 4 : 0)));
+    CK(cudaMemsetAsync(gcount, 0, (size_t)rd.n_groups * 8, h0->st));
+    CK(cudaEventRecord(h0->ev_peer, h0->st));  // device 0's buffers exist before any shard copies into them
+    // per shard: keys on its device, then (if not device 0's own) its keys,
+    // vals, records and group counts copied to device 0
+    int64_t base = 0;
+    for (int32_t s = 0; s < n_h; ++s) {
+        tsg_engine* h = hs[s];
+        const auto& R = h->rs[h->fetch_rs];
+        if (!R.n_out) continue;
+        DevGuard gs(h->dev);
+        uint64_t* dg = nullptr;
+        int32_t* dr = nullptr;
+        uint64_t* kk = k0 + base;
+        uint32_t* vv = v0 + base;
+        unsigned long long* gc = gcount;
+        if (s > 0) {
+            CK(cudaStreamWaitEvent(h->st, h0->ev_peer, 0));
+            CKR(dalloc(h, (void**)&kk, R.n_out * 8));
+            CKR(dalloc(h, (void**)&vv, R.n_out * 4));
+            CKR(dalloc(h, (void**)&gc, (int64_t)rd.n_groups * 8));
+            CK(cudaMemsetAsync(gc, 0, (size_t)rd.n_groups * 8, h->st));
+        }
+        CKR(dalloc(h, (void**)&dg, (int64_t)rd.n_groups * 8));
+        CKR(dalloc(h, (void**)&dr, (int64_t)n_sizes * 4));
+        CK(cudaMemcpyAsync(dg, gkey.data(), rd.n_groups * 8, cudaMemcpyHostToDevice, h->st));
+        CK(cudaMemcpyAsync(dr, rank_of_size, n_sizes * 4, cudaMemcpyHostToDevice, h->st));
+        OrderKey ok{dg, h->size_of_id, dr, n_sizes, rank_bits, id_bits, g_bits, gw, rec8 ? 1 : 0};
+        k_order_keys<<<grid_for(R.n_out), 256, 0, h->st>>>(R.out, R.n_out, base, ok, kk, vv, gc);
+        CK(cudaGetLastError());
+        if (s > 0) {
+            CK(cudaMemcpyPeerAsync(k0 + base, h0->dev, kk, h->dev, R.n_out * 8, h->st));
+            CK(cudaMemcpyPeerAsync(v0 + base, h0->dev, vv, h->dev, R.n_out * 4, h->st));
+            CK(cudaMemcpyPeerAsync(recs + base * rec_bytes, h0->dev, R.out, h->dev, R.n_out * rec_bytes, h->st));
+            // the shard's group counts: added on device 0 below
+            CK(cudaMemcpyPeerAsync(gscratch, h0->dev, gc, h->dev, (size_t)rd.n_groups * 8, h->st));
+            CK(cudaEventRecord(h->ev_peer, h->st));
+            dfree(h, kk); dfree(h, vv); dfree(h, gc);
+        } else if (n_h > 1) {
+            CK(cudaMemcpyAsync(recs, R.out, R.n_out * rec_bytes, cudaMemcpyDeviceToDevice, h->st));
+        }
+        CK(cudaStreamSynchronize(h->st));  // gkey / rank_of_size uploads, and k1 reused per shard
+        if (s > 0) {  // (host-ordered: the shard's copies are done, device 0's stream is drained)
+            DevGuard gz(h0->dev);
+            std::vector<unsigned long long> hc(rd.n_groups), acc(rd.n_groups);
+            CK(cudaStreamSynchronize(h0->st));
+            CK(cudaMemcpyAsync(hc.data(), gscratch, rd.n_groups * 8, cudaMemcpyDeviceToHost, h0->st));
+            CK(cudaMemcpyAsync(acc.data(), gcount, rd.n_groups * 8, cudaMemcpyDeviceToHost, h0->st));
+            CK(cudaStreamSynchronize(h0->st));
+            for (int g = 0; g < rd.n_groups; ++g) acc[g] += hc[g];
+            CK(cudaMemcpyAsync(gcount, acc.data(), rd.n_groups * 8, cudaMemcpyHostToDevice, h0->st));
+            CK(cudaStreamSynchronize(h0->st));
+        }
+        dfree(h, dg); dfree(h, dr);
+        base += R.n_out;
+    }
+    const void* src = n_h > 1 ? (const void*)recs : (const void*)h0->rs[h0->fetch_rs].out;
+    // LSD passes over the key's significant bits
+    uint64_t *ka = k0, *kb = k1;
+    uint32_t *va = v0, *vb = v1;
+    for (int shift = 0; shift < key_bits; shift += 8) {
+        k_sort_hist<<<(unsigned)nblk, SORT_THREADS, 0, h0->st>>>(ka, total, shift, hist);
+        k_scan_rows<<<256, 1024, 0, h0->st>>>(hist, nblk, rowsum);
+        k_scan_add<<<256, 1024, 0, h0->st>>>(hist, nblk, rowsum);
+        k_sort_scatter<<<(unsigned)nblk, SORT_THREADS, 0, h0->st>>>(ka, va, total, shift, hist, kb, vb);
+        CK(cudaGetLastError());
+        std::swap(ka, kb);
+        std::swap(va, vb);
+    }
+    uint8_t* oe = out;
+    uint8_t* om = out + eid_sec;  // sections 256-byte aligned for the 8-byte fields
+    int32_t* og = groups ? reinterpret_cast<int32_t*>(om + mask_sec) : nullptr;
+    k_order_gather<<<grid_for(total), 256, 0, h0->st>>>(va, total, src, rec8 ? 1 : 0, eid_bytes, mask_bytes, oe, om,
+                                                        og);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(eids, oe, total * eid_bytes, cudaMemcpyDeviceToHost, h0->st));
+    CK(cudaMemcpyAsync(masks, om, total * mask_bytes, cudaMemcpyDeviceToHost, h0->st));
+    if (groups) CK(cudaMemcpyAsync(groups, og, total * 4, cudaMemcpyDeviceToHost, h0->st));
+    std::vector<unsigned long long> gc(rd.n_groups);
+    CK(cudaMemcpyAsync(gc.data(), gcount, rd.n_groups * 8, cudaMemcpyDeviceToHost, h0->st));
+    CK(cudaStreamSynchronize(h0->st));
+    for (int g = 0; g < rd.n_groups; ++g) dest_counts[dest_of[g]] += (int64_t)gc[g];
+    dfree(h0, recs); dfree(h0, k0); dfree(h0, k1); dfree(h0, v0); dfree(h0, v1); dfree(h0, hist);
+    dfree(h0, gcount); dfree(h0, gscratch); dfree(h0, out);
     return TSG_OK;
 }
 

@@ -1,4 +1,4 @@
-"""The clause-exchange engine on a B200: drop-in for triggersat.engine.Engine.
+"""The clause-exchange engine on B200s: drop-in for triggersat.engine.Engine.
 
 Same public surface as the reference (engine.py:44-525): ``EngineConfig``,
 ``AssignmentSnapshot``, ``Report``, ``RoundResult``, ``RoundTrace`` and
@@ -8,8 +8,23 @@ Same public surface as the reference (engine.py:44-525): ``EngineConfig``,
 keeps on its producer side -- the id lock, the staging list, the per-thread
 snapshot and report queues (engine.py:273-279) -- and the clause store lives
 in HBM behind the C ABI (include/tsg.h): size buckets, activities, ids and
-the round's kernels.  The only host copy of clause data is the literal tuple
-per engine id that Reports carry (engine.py:90-102).
+the round's kernels.
+
+Host data paths, none of them per-record Python work:
+
+* snapshots are packed (2 bits per variable, tsg_pack_rows, GIL released)
+  by the submitting solver thread straight into that thread's page-locked
+  queue region, and a round stages every thread's region as one segment
+  (tsg_stage_packed_segments) -- no host copy of the rows;
+* a round's reports are ordered on the GPU into the reference's delivery
+  order (tsg_fetch_ordered) and queued per destination as array slices;
+  the ``Report`` objects, with their literals from an append-only literal
+  arena, are built by the draining solver thread;
+* ``EngineConfig.devices`` names several GPUs: the clauses are sharded
+  across them (every size bucket balanced), the round's tables are encoded
+  once and copied peer to peer (tsg_round_tables_copy, NVLink), every GPU
+  tests its shard, and the records of all shards are ordered together;
+  ``reduce_store`` stays exact (sharded.global_reduce).
 
 There is no CPU path: constructing an Engine without the CUDA library or a
 CUDA device raises.
@@ -17,18 +32,18 @@ CUDA device raises.
 from __future__ import annotations
 
 import ctypes as C
-import itertools
 import threading
 import time
 from collections import deque
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 
 from . import _lib
-from . import reports as _reports
-from ._lib import REPORT_DTYPE, check, ptr
+from . import sharded as _sharded
+from ._lib import check, ptr
+from .native import NativeEngine
 
 #: Activities are rescaled when the bump increment passes this (engine.py:39-40).
 _ACTIVITY_RESCALE = 1e100
@@ -37,7 +52,7 @@ _ACTIVITY_RESCALE = 1e100
 @dataclass
 class EngineConfig:
     """Tunables, identical to the reference (engine.py:44-74) plus the device
-    ordinal and the initial report-buffer size."""
+    ordinal(s) and the initial report-buffer size."""
 
     max_clauses: int = 5_000_000
     assignment_queue_capacity: Optional[int] = None
@@ -50,6 +65,7 @@ class EngineConfig:
     device: int = 0
     report_capacity: int = 0
     timing: bool = False
+    devices: Optional[Sequence[int]] = None  # clause shards, one engine per entry (default: [device])
 
     def __post_init__(self):
         if self.max_clauses < 1:
@@ -62,6 +78,8 @@ class EngineConfig:
             self.assignment_queue_capacity = 2 * self.lane_width
         if self.assignment_queue_capacity < 1:
             raise ValueError("assignment_queue_capacity must be >= 1")
+        if self.devices is not None and len(self.devices) < 1:
+            raise ValueError("devices must name at least one GPU")
 
 
 @dataclass
@@ -85,11 +103,15 @@ class Report:
 
 @dataclass
 class _ReportBatch:
-    """One round's reports for one destination, in emission order."""
+    """One round's reports for one destination, in delivery order: engine
+    ids and lane masks, with the literal arena as it was at round time."""
 
-    lits: list
-    eids: list
-    masks: list
+    eids: np.ndarray
+    masks: np.ndarray
+    arena: "_Arena"
+
+    def __len__(self):
+        return len(self.eids)
 
 
 @dataclass
@@ -107,120 +129,187 @@ class RoundTrace:
     reports: list
 
 
-class BucketView:
-    """Live view of one device size bucket (the reference's _SizeBucket,
-    engine.py:122-200).  Every attribute read fetches from HBM."""
+class _Arena:
+    """Append-only literal arena by engine id (Report.lits, engine.py:90-102).
+    Grows by replacing its arrays, never by rewriting them, so a report batch
+    holding the arena of its round keeps valid literals even after the
+    clause was removed."""
 
-    def __init__(self, engine: "Engine", index: int, size: int):
-        self._e, self.index, self.size = engine, index, size
+    __slots__ = ("lits", "off", "size", "used")
 
-    @property
-    def count(self) -> int:
-        s = C.c_int32(0)
-        n = C.c_int64(0)
-        check(self._e._L.tsg_bucket_info(self._e._h, self.index, C.byref(s), C.byref(n)))
-        return n.value
+    def __init__(self, lits=None, off=None, size=None, used=0):
+        self.lits = np.zeros(1024, np.int32) if lits is None else lits
+        self.off = np.zeros(1024, np.int64) if off is None else off
+        self.size = np.zeros(1024, np.int32) if size is None else size
+        self.used = used
 
-    def _read(self, lits=False, ids=False, origins=False, acts=False):
-        n = self.count
-        out = [np.zeros((n, self.size), np.int32) if lits else None,
-               np.zeros(n, np.int64) if ids else None,
-               np.zeros(n, np.int32) if origins else None,
-               np.zeros(n, np.float64) if acts else None]
-        if n:
-            check(self._e._L.tsg_bucket_read(self._e._h, self.index, *(ptr(a) for a in out)))
-        return out
+    def snapshot(self) -> "_Arena":
+        return _Arena(self.lits, self.off, self.size, self.used)
 
-    @property
-    def activities(self) -> np.ndarray:
-        return self._read(acts=True)[3]
+    def append(self, ids: np.ndarray, lens: np.ndarray, flat: np.ndarray) -> None:
+        total = int(flat.size)
+        if self.used + total > self.lits.size:
+            grown = np.zeros(max(self.used + total, 2 * self.lits.size), np.int32)
+            grown[:self.used] = self.lits[:self.used]
+            self.lits = grown
+        self.lits[self.used:self.used + total] = flat
+        top = int(ids.max()) + 1 if ids.size else 0
+        if top > self.off.size:
+            n = max(top, 2 * self.off.size)
+            off = np.zeros(n, np.int64)
+            off[:self.off.size] = self.off
+            size = np.zeros(n, np.int32)
+            size[:self.size.size] = self.size
+            self.off, self.size = off, size
+        starts = np.zeros(len(lens), np.int64)
+        if len(lens) > 1:
+            np.cumsum(lens[:-1], out=starts[1:])
+        self.off[ids] = self.used + starts
+        self.size[ids] = lens
+        self.used += total
 
-    @property
-    def engine_ids(self) -> np.ndarray:
-        return self._read(ids=True)[1]
-
-    @property
-    def origins(self) -> np.ndarray:
-        return self._read(origins=True)[2]
-
-    def lits_at(self, slot: int) -> tuple:
-        return tuple(int(x) for x in self._read(lits=True)[0][slot])
-
-    def literal_columns(self) -> list:
-        lits = self._read(lits=True)[0]
-        return [lits[:, j].copy() for j in range(self.size)]
+    def lits_of(self, eid: int) -> tuple:
+        o = int(self.off[eid])
+        return tuple(self.lits[o:o + int(self.size[eid])].tolist())
 
 
-class DeviceClauseStore:
-    """The clause store as seen from the host (engine.py:203-235)."""
+class _SnapQueue:
+    """One solver thread's snapshot queue: packed rows in one of two
+    page-locked regions (the round drains one while submissions fill the
+    other), plus the snapshot objects for trace mode."""
+
+    def __init__(self, lib, cap: int, words: int):
+        self.lock = threading.Lock()
+        self.cap, self.words = cap, words
+        self._lib = lib
+        self._raw = [None, None]
+        self.rows = [None, None]
+        for r in range(2):
+            p = C.c_void_p()
+            check(lib.tsg_host_alloc(cap * words * 8, C.byref(p)))
+            self._raw[r] = p
+            self.rows[r] = np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_uint64)), shape=(cap, words))
+        self.cur = 0
+        self.n = 0
+        self.snaps: List[object] = []
+        self.bad: List[int] = []  # lengths of rejected snapshots (raised by run_round)
+
+    def close(self):
+        for r in range(2):
+            if self._raw[r] is not None:
+                self._lib.tsg_host_free(self._raw[r])
+                self._raw[r] = None
+
+
+class _StoreShards:
+    """The store as seen from the host: the shards' buckets merged by size,
+    slots in engine-id order (engine.py:122-235)."""
 
     def __init__(self, engine: "Engine"):
         self._e = engine
 
     def __len__(self) -> int:
-        n = C.c_int64(0)
-        check(self._e._L.tsg_store_size(self._e._h, C.byref(n)))
-        return n.value
+        return sum(len(s) for s in self._e._shards)
 
     @property
-    def buckets(self) -> Dict[int, BucketView]:
+    def buckets(self) -> Dict[int, "BucketView"]:
         """Size -> bucket, in creation order (dict insertion order)."""
-        nb = C.c_int32(0)
-        check(self._e._L.tsg_bucket_count(self._e._h, C.byref(nb)))
-        out = {}
-        for b in range(nb.value):
-            s = C.c_int32(0)
-            n = C.c_int64(0)
-            check(self._e._L.tsg_bucket_info(self._e._h, b, C.byref(s), C.byref(n)))
-            out[s.value] = BucketView(self._e, b, s.value)
-        return out
+        return {s: BucketView(self._e, s) for s in self._e._sizes_in_order}
 
     def clauses(self):
         """(engine_id, lits, origin, activity), sorted by size then slot (engine.py:221-231)."""
-        for size, bv in sorted(self.buckets.items()):
-            lits, ids, org, acts = bv._read(True, True, True, True)
+        for size in sorted(self._e._sizes_in_order):
+            lits, ids, org, acts = BucketView(self._e, size)._read()
             for k in range(len(ids)):
                 yield int(ids[k]), tuple(int(x) for x in lits[k]), int(org[k]), float(acts[k])
 
     def scale_activities(self, factor: float) -> None:
-        check(self._e._L.tsg_scale_activities(self._e._h, factor))
+        for s in self._e._shards:
+            s.scale(factor)
+
+
+class BucketView:
+    """Live view of one size bucket across the shards (the reference's
+    _SizeBucket, engine.py:122-200).  Every attribute read fetches from HBM."""
+
+    def __init__(self, engine: "Engine", size: int):
+        self._e, self.size = engine, size
+
+    def _read(self):
+        parts = []
+        for sh in self._e._shards:
+            nb = C.c_int32(0)
+            check(sh.L.tsg_bucket_count(sh.h, C.byref(nb)))
+            for b in range(nb.value):
+                s, n = C.c_int32(0), C.c_int64(0)
+                check(sh.L.tsg_bucket_info(sh.h, b, C.byref(s), C.byref(n)))
+                if s.value != self.size or not n.value:
+                    continue
+                out = [np.zeros((n.value, self.size), np.int32), np.zeros(n.value, np.int64),
+                       np.zeros(n.value, np.int32), np.zeros(n.value, np.float64)]
+                check(sh.L.tsg_bucket_read(sh.h, b, *(ptr(a) for a in out)))
+                parts.append(out)
+        if not parts:
+            return (np.zeros((0, self.size), np.int32), np.zeros(0, np.int64), np.zeros(0, np.int32),
+                    np.zeros(0, np.float64))
+        lits, ids, org, acts = (np.concatenate([p[i] for p in parts]) for i in range(4))
+        o = np.argsort(ids, kind="stable")
+        return lits[o], ids[o], org[o], acts[o]
+
+    @property
+    def count(self) -> int:
+        return len(self._read()[1])
+
+    @property
+    def activities(self) -> np.ndarray:
+        return self._read()[3]
+
+    @property
+    def engine_ids(self) -> np.ndarray:
+        return self._read()[1]
+
+    @property
+    def origins(self) -> np.ndarray:
+        return self._read()[2]
+
+    def lits_at(self, slot: int) -> tuple:
+        return tuple(int(x) for x in self._read()[0][slot])
+
+    def literal_columns(self) -> list:
+        lits = self._read()[0]
+        return [lits[:, j].copy() for j in range(self.size)]
 
 
 class Engine:
-    """Owns the HBM clause store and runs the exchange rounds on the GPU."""
+    """Owns the HBM clause store (one shard per configured GPU) and runs the
+    exchange rounds on the GPU(s)."""
 
     def __init__(self, num_vars: int, thread_count: int, config: Optional[EngineConfig] = None):
         self.config = config or EngineConfig()
         self.num_vars = num_vars
         self.thread_count = thread_count
         self._L = _lib.load()
-        cfg = _lib.tsg_config(self.config.lane_width, self.config.group_width, self.config.device,
-                              _lib.TSG_F_TIMING if self.config.timing else 0,
-                              self.config.report_capacity)
-        h = C.c_void_p()
-        check(self._L.tsg_create(num_vars, C.byref(cfg), C.byref(h)))
-        self._h = h
+        devices = list(self.config.devices) if self.config.devices else [self.config.device]
+        self._shards = [NativeEngine(num_vars, self.config.lane_width, self.config.group_width, device=d,
+                                     timing=self.config.timing, report_capacity=self.config.report_capacity)
+                        for d in devices]
+        self._h = self._shards[0].h  # the first shard: staging, encode, record ordering
         w = C.c_int64(0)
         check(self._L.tsg_packed_words(num_vars, C.byref(w)))
         self._packed_words = w.value
-        self._rec_dtype = REPORT_DTYPE
         self._rec_bytes = 16
-        if self.config.lane_width <= 32:  # 12-byte egress records: a quarter fewer bytes D2H
-            check(self._L.tsg_set_record_bytes(self._h, 12))
-            self._rec_dtype = _reports.RECORD12_DTYPE
-            self._rec_bytes = 12
-        self.store = DeviceClauseStore(self)
-        self._lits: Dict[int, tuple] = {}
-        self._size_rank: Dict[int, int] = {}
-        self._rank_of_size = np.zeros(64, dtype=np.int64)   # bucket creation rank by clause size
-        self._size_of = np.zeros(1024, dtype=np.int32)      # clause size by engine id
+        self.store = _StoreShards(self)
+        self._arena = _Arena()
+        self._sizes_in_order: List[int] = []                # bucket creation order (dict order)
+        self._rank_of_size = np.zeros(64, dtype=np.int32)   # creation rank by clause size
+        self._shard_load = np.zeros((len(self._shards), 64), dtype=np.int64)  # clauses per (shard, size)
 
         self._id_lock = threading.Lock()
         self._next_id = 0
         self._staged: List[Tuple[int, tuple, int]] = []
 
-        self._queue_lock = threading.Lock()
-        self._snapshots: Dict[int, deque] = {t: deque() for t in range(thread_count)}
+        self._queue_lock = threading.Lock()  # report queues, counters, the set of snapshot queues
+        self._squeues: Dict[int, _SnapQueue] = {}
         self._reports: Dict[int, deque] = {t: deque() for t in range(thread_count)}
         self._pending_reports: Dict[int, int] = {}
 
@@ -237,9 +326,12 @@ class Engine:
         self.trace: List[RoundTrace] = []
 
     def close(self) -> None:
-        if getattr(self, "_h", None):
-            self._L.tsg_destroy(self._h)
-            self._h = None
+        for q in getattr(self, "_squeues", {}).values():
+            q.close()
+        for s in getattr(self, "_shards", []):
+            s.close()
+        self._shards = []
+        self._h = None
 
     def __del__(self):
         try:
@@ -258,39 +350,46 @@ class Engine:
             self._staged.append((engine_id, lits, origin))
         return engine_id
 
-    def submit_assignment(self, snapshot) -> bool:
-        """engine.py:319-333.  The snapshot is packed to 2 bits per variable
-        here, in the submitting solver thread (tsg_pack_rows releases the GIL),
-        where the reference keeps the int8 array; a wrong length is reported
-        by run_round, as in the reference (bitpack.py:92-103)."""
-        cap = self.config.assignment_queue_capacity
-        with self._queue_lock:
-            q = self._snapshots.setdefault(snapshot.thread_id, deque())
-            if len(q) >= cap:
-                self.counters["snapshots_dropped"] += 1
-                return False
-        packed = self._pack(snapshot.values)
-        with self._queue_lock:
-            q = self._snapshots.setdefault(snapshot.thread_id, deque())
-            if len(q) >= cap:  # filled up while this thread was packing
-                self.counters["snapshots_dropped"] += 1
-                return False
-            q.append((snapshot, packed))
-            self.counters["snapshots_accepted"] += 1
-            return True
+    def _queue(self, tid: int) -> _SnapQueue:
+        q = self._squeues.get(tid)
+        if q is None:
+            with self._queue_lock:
+                q = self._squeues.get(tid)
+                if q is None:
+                    q = _SnapQueue(self._L, self.config.assignment_queue_capacity, self._packed_words)
+                    self._squeues[tid] = q
+        return q
 
-    def _pack(self, values):
-        vals = np.ascontiguousarray(np.asarray(values, dtype=np.int8))
-        if vals.ndim != 1 or vals.shape[0] != self.num_vars + 1:
-            return vals.shape[0] if vals.ndim == 1 else -1  # length error, raised by run_round
-        out = np.empty((1, self._packed_words), dtype=np.uint64)
-        check(self._L.tsg_pack_rows(ptr(vals), 1, vals.shape[0], self.num_vars, ptr(out), self._packed_words))
-        return out
+    def submit_assignment(self, snapshot) -> bool:
+        """engine.py:319-333: drop the newest when the thread's queue is full.
+        The snapshot is packed into the thread's page-locked queue region
+        here, in the submitting solver thread (the reference keeps the int8
+        array); a wrong length is reported by run_round, as in the reference
+        (bitpack.py:92-103)."""
+        q = self._queue(snapshot.thread_id)
+        with q.lock:
+            if q.n >= q.cap:
+                ok = False
+            else:
+                vals = np.ascontiguousarray(np.asarray(snapshot.values, dtype=np.int8))
+                if vals.ndim != 1 or vals.shape[0] != self.num_vars + 1:
+                    q.bad.append(vals.shape[0] if vals.ndim == 1 else -1)
+                else:  # (the GIL is released while the row is packed)
+                    check(self._L.tsg_pack_rows(ptr(vals), 1, vals.shape[0], self.num_vars,
+                                                C.c_void_p(q.rows[q.cur].ctypes.data + q.n * q.words * 8),
+                                                q.words))
+                    q.n += 1
+                if self.config.trace:
+                    q.snaps.append(snapshot)
+                ok = True
+        with self._queue_lock:
+            self.counters["snapshots_accepted" if ok else "snapshots_dropped"] += 1
+        return ok
 
     def drain_reports(self, thread_id: int) -> List[Report]:
         """engine.py:335-343.  A round queues each destination's reports as
-        one batch (literals captured at round time); the Report objects are
-        built here, in the draining solver thread, off the engine worker."""
+        one batch; the Report objects (literals from the arena of that round)
+        are built here, in the draining solver thread, off the engine worker."""
         with self._queue_lock:
             q = self._reports.get(thread_id)
             if not q:
@@ -301,7 +400,12 @@ class Engine:
         out: List[Report] = []
         for it in items:
             if isinstance(it, _ReportBatch):
-                out.extend(map(Report, itertools.repeat(thread_id, len(it.eids)), it.lits, it.eids, it.masks))
+                ar = it.arena
+                offs = ar.off[it.eids].tolist()
+                sizes = ar.size[it.eids].tolist()
+                lits = ar.lits
+                out.extend(Report(thread_id, tuple(lits[o:o + s].tolist()), e, m)
+                           for o, s, e, m in zip(offs, sizes, it.eids.tolist(), it.masks.tolist()))
             else:
                 out.append(it)
         return out
@@ -310,8 +414,9 @@ class Engine:
     # engine worker side
 
     def _insert(self, batch) -> None:
-        """Append staged (id, lits, origin) to the device store at the current
-        activity increment (engine.py:357)."""
+        """Append staged (id, lits, origin) to the store at the current
+        activity increment (engine.py:357): shard by size (every bucket
+        balanced over the devices), literals into the arena."""
         if not batch:
             return
         n = len(batch)
@@ -319,29 +424,47 @@ class Engine:
         offs = np.zeros(n + 1, dtype=np.int64)
         np.cumsum(lens, out=offs[1:])
         total = int(offs[-1])
-        flat = np.fromiter(itertools.chain.from_iterable(b[1] for b in batch), dtype=np.int32, count=total) \
-            if total else np.zeros(1, dtype=np.int32)
+        flat = np.fromiter((x for b in batch for x in b[1]), dtype=np.int32, count=total) \
+            if total else np.zeros(0, dtype=np.int32)
         ids = np.fromiter((b[0] for b in batch), dtype=np.int64, count=n)
         org = np.fromiter((b[2] for b in batch), dtype=np.int32, count=n)
-        check(self._L.tsg_add_clauses(self._h, ptr(flat), ptr(offs), n, ptr(ids), ptr(org),
-                                      self._activity_inc))
-        self._lits.update((b[0], b[1]) for b in batch)
         # bucket creation order (dict insertion order): new sizes in first-seen order
         sizes, first = np.unique(lens, return_index=True)
+        top = int(sizes[-1]) + 1
+        if top > self._rank_of_size.size:
+            grown = np.zeros(max(top, 2 * self._rank_of_size.size), np.int32)
+            grown[:self._rank_of_size.size] = self._rank_of_size
+            self._rank_of_size = grown
+            load = np.zeros((len(self._shards), grown.size), np.int64)
+            load[:, :self._shard_load.shape[1]] = self._shard_load
+            self._shard_load = load
+        known = set(self._sizes_in_order)
         for size in sizes[np.argsort(first, kind="stable")].tolist():
-            if size not in self._size_rank:
-                self._size_rank[size] = len(self._size_rank)
-                if size >= len(self._rank_of_size):
-                    grown = np.zeros(max(size + 1, 2 * len(self._rank_of_size)), dtype=np.int64)
-                    grown[:len(self._rank_of_size)] = self._rank_of_size
-                    self._rank_of_size = grown
-                self._rank_of_size[size] = self._size_rank[size]
-        top = int(ids.max()) + 1
-        if top > len(self._size_of):
-            grown = np.zeros(max(top, 2 * len(self._size_of)), dtype=np.int32)
-            grown[:len(self._size_of)] = self._size_of
-            self._size_of = grown
-        self._size_of[ids] = lens
+            if size not in known:
+                self._rank_of_size[size] = len(self._sizes_in_order)
+                self._sizes_in_order.append(size)
+                known.add(size)
+        ns = len(self._shards)
+        if ns == 1:
+            self._shards[0].add_clauses(flat, offs, ids, org, self._activity_inc)
+        else:  # per size round-robin from each shard's current count: balanced buckets
+            order = np.argsort(lens, kind="stable")
+            sl = lens[order]
+            starts = np.searchsorted(sl, sl, side="left")
+            within = np.arange(n) - starts
+            base = self._shard_load.sum(axis=0)[sl]
+            shard_of = np.empty(n, np.int64)
+            shard_of[order] = (base + within) % ns
+            for r, sh in enumerate(self._shards):
+                sel = np.nonzero(shard_of == r)[0]
+                if not sel.size:
+                    continue
+                so = np.zeros(sel.size + 1, np.int64)
+                np.cumsum(lens[sel], out=so[1:])
+                sf = np.concatenate([flat[offs[i]:offs[i + 1]] for i in sel]) if so[-1] else np.zeros(0, np.int32)
+                sh.add_clauses(sf, so, ids[sel], org[sel], self._activity_inc)
+                np.add.at(self._shard_load[r], lens[sel], 1)
+        self._arena.append(ids, lens.astype(np.int32), flat)
         self.counters["clauses_added"] += n
 
     def _integrate_exports(self) -> None:
@@ -365,17 +488,25 @@ class Engine:
                 self.counters["clauses_dropped"] += 1
                 i += 1
 
-    def _drain_snapshots(self) -> Dict[int, list]:
+    def _drain_snapshots(self):
+        """Every thread's queued rows, tids ascending: [(tid, rows, n, snaps, bad)];
+        each queue switches to its other region for new submissions."""
         with self._queue_lock:
-            pending = {}
-            for tid, q in self._snapshots.items():
-                if q:
-                    pending[tid] = list(q)
-                    q.clear()
-            return pending
+            queues = sorted(self._squeues.items())
+        out = []
+        for tid, q in queues:
+            with q.lock:
+                if not q.n and not q.bad:
+                    continue
+                out.append((tid, q.rows[q.cur], q.n, q.snaps, q.bad))
+                q.cur ^= 1
+                q.n = 0
+                q.snaps = []
+                q.bad = []
+        return out
 
     def run_round(self) -> RoundResult:
-        """engine.py:369-435 with the test phase on the GPU."""
+        """engine.py:369-435 with the test phase on the GPU(s)."""
         started = time.perf_counter()
         self._integrate_exports()
         store_snapshot = None
@@ -383,39 +514,37 @@ class Engine:
             store_snapshot = [(eid, lits) for eid, lits, _, _ in self.store.clauses()]
         pending = self._drain_snapshots()
         result = RoundResult()
-        result.assignments_consumed = sum(len(v) for v in pending.values())
+        result.assignments_consumed = sum(n + len(bad) for _, _, n, _, bad in pending)
         self.counters["snapshots_consumed"] += result.assignments_consumed
+        for _, _, _, _, bad in pending:
+            if bad:  # pack_assignments' length check (bitpack.py:92-103)
+                raise ValueError(f"assignment has {bad[0]} slots, expected {self.num_vars + 1}")
 
         # grouping (engine.py:390-399): tids ascending, lane_width per group
-        lane_width = self.config.lane_width
-        rows, lanes, tids = [], [], []
-        for tid in sorted(pending):
-            snaps = pending[tid]
-            for i in range(0, len(snaps), lane_width):
-                chunk = snaps[i:i + lane_width]
-                for j, (_, packed) in enumerate(chunk):
-                    if not isinstance(packed, np.ndarray):
-                        raise ValueError(f"assignment {j} has {packed} slots, expected {self.num_vars + 1}")
-                    rows.append(packed)
-                lanes.append(len(chunk))
+        lw = self.config.lane_width
+        lanes, tids = [], []
+        for tid, _, n, _, _ in pending:
+            for i in range(0, n, lw):
+                lanes.append(min(lw, n - i))
                 tids.append(tid)
-
         n_rep = 0
+        emitted: list = []
+        batches = []
         if lanes:
-            block = np.concatenate(rows)
-            check(self._L.tsg_stage_packed(self._h, ptr(block), block.shape[0], block.shape[1], 0))
             gl = np.asarray(lanes, dtype=np.int32)
             gt = np.asarray(tids, dtype=np.int32)
-            if self.config.lane_width <= 32:
+            segs = (C.c_void_p * len(pending))(*[rows.ctypes.data for _, rows, _, _, _ in pending])
+            cnts = np.asarray([n for _, _, n, _, _ in pending], dtype=np.int64)
+            check(self._L.tsg_stage_packed_segments(self._h, segs, ptr(cnts), len(pending), self._packed_words))
+            if lw <= 32:
                 # 8-byte records written by the kernel when ids and groups fit,
-                # else the 12-byte form (include/tsg.h tsg_set_record_bytes)
-                nb = 8 if (self._next_id <= (1 << 27) and len(lanes) <= 32) else 12
+                # else the general 16-byte form (ordered on the device either way)
+                nb = 8 if (self._next_id <= (1 << 27) and len(lanes) <= 32) else 16
                 if nb != self._rec_bytes:
-                    check(self._L.tsg_set_record_bytes(self._h, nb))
+                    for s in self._shards:
+                        s.set_record_bytes(nb)
                     self._rec_bytes = nb
-                    self._rec_dtype = _reports.RECORD8_DTYPE if nb == 8 else _reports.RECORD12_DTYPE
-            res = _lib.tsg_round_result()
-            check(self._L.tsg_round(self._h, ptr(gl), ptr(gt), len(lanes), self._activity_inc, C.byref(res)))
+            res = self._round(gl, gt)
             self.last_round = res
             self.counters["aggregate_tests"] += res.aggregate_tests
             self.counters["lane_tests"] += res.lane_tests
@@ -423,32 +552,28 @@ class Engine:
             self.counters["aggregate_tests_negative"] += res.aggregate_tests_negative
             result.clauses_tested = res.clauses_tested
             result.aggregate_tests_negative = res.aggregate_tests_negative
-            recs = _reports.decode(self._fetch(res.reports))
-            if len(recs):
-                brank = self._rank_of_size[self._size_of[recs["engine_id"]]]
-                recs = recs[_reports.reference_order(recs, self.config.group_width, brank)]
-                dest = np.asarray(tids, dtype=np.int64)[recs["group"]]
-                order = np.argsort(dest, kind="stable")  # per destination, in emission order
-                eids = recs["engine_id"][order].tolist()
-                lits_of = self._lits
-                lits = [lits_of[e] for e in eids]  # captured now: a later reduce may drop the clause
-                masks = recs["lane_mask"][order].tolist()
-                dsorted = dest[order]
-                cuts = np.flatnonzero(np.diff(dsorted)) + 1
-                bounds = [0] + cuts.tolist() + [len(eids)]
-                batches = [(int(dsorted[a]), _ReportBatch(lits[a:b], eids[a:b], masks[a:b]))
-                           for a, b in zip(bounds[:-1], bounds[1:])]
-                n_rep = len(eids)
-                if self.config.trace:  # the trace keeps Report objects in emission order
-                    emitted = [None] * n_rep
-                    for k, i in enumerate(order.tolist()):
-                        emitted[i] = Report(int(dsorted[k]), lits[k], eids[k], masks[k])
+            if res.reports:
+                eids, masks, groups, counts = self._fetch_ordered(res.reports, len(pending))
+                arena = self._arena.snapshot()  # literals as of this round (a later reduce may drop the clause)
+                cut = np.concatenate([[0], np.cumsum(counts)])
+                dests = [tid for tid, _, _, _, _ in pending]
+                for d, tid in enumerate(dests):
+                    if counts[d]:
+                        batches.append((tid, _ReportBatch(eids[cut[d]:cut[d + 1]], masks[cut[d]:cut[d + 1]],
+                                                          arena)))
+                n_rep = int(cut[-1])
+                if self.config.trace:  # the trace keeps Report objects in emission order (engine.py:403-464)
+                    dest_of = np.repeat(np.asarray(dests, np.int64), counts)
+                    brank = self._rank_of_size[arena.size[eids]]
+                    order = np.lexsort((groups, eids, brank, groups // self.config.group_width))
+                    emitted = [Report(int(dest_of[i]), arena.lits_of(int(eids[i])), int(eids[i]), int(masks[i]))
+                               for i in order.tolist()]
 
         if n_rep:
             with self._queue_lock:
                 for d, batch in batches:
                     self._reports.setdefault(d, deque()).append(batch)
-                    self._pending_reports[d] = self._pending_reports.get(d, 0) + len(batch.eids)
+                    self._pending_reports[d] = self._pending_reports.get(d, 0) + len(batch)
             self.counters["reports_delivered"] += n_rep
             result.reports_emitted = n_rep
 
@@ -464,38 +589,65 @@ class Engine:
         if self.config.trace:
             self.trace.append(RoundTrace(
                 snapshots=[(s.thread_id, np.array(s.values, copy=True))
-                           for snaps in pending.values() for s, _ in snaps],
-                store=store_snapshot, reports=emitted if n_rep else []))
+                           for _, _, _, snaps, _ in pending for s in snaps],
+                store=store_snapshot, reports=emitted))
 
         self.counters["rounds"] += 1
         self.counters["busy_seconds"] += time.perf_counter() - started
         return result
 
-    def _fetch(self, n: int) -> np.ndarray:
-        recs = np.zeros(n, dtype=self._rec_dtype)
-        if n:
-            got = C.c_int64(0)
-            check(self._L.tsg_fetch_reports(self._h, ptr(recs), n, C.byref(got)))
-            recs = recs[:got.value]
-        return recs
+    def _round(self, gl: np.ndarray, gt: np.ndarray) -> _lib.tsg_round_result:
+        """Prepare on every shard, encode on the first, copy its tables to the
+        others over NVLink, launch all, collect all; the figures summed."""
+        s0 = self._shards[0]
+        for s in self._shards:
+            s.prepare(gl, gt)
+        s0.encode()
+        for s in self._shards[1:]:
+            s.tables_from(s0)
+        for s in self._shards:
+            s.launch(self._activity_inc)
+        rs = [s.collect() for s in self._shards]
+        res = rs[0]
+        for r in rs[1:]:
+            for f in ("reports", "clauses_tested", "aggregate_tests", "aggregate_tests_negative", "lane_tests",
+                      "lane_triggers"):
+                setattr(res, f, getattr(res, f) + getattr(r, f))
+            res.reruns += r.reruns
+        return res
+
+    def _fetch_ordered(self, n: int, n_dest: int):
+        """The round's records in delivery order (tsg_fetch_ordered)."""
+        eid_bytes = 4 if self._next_id < (1 << 31) else 8
+        mask_bytes = 4 if self.config.lane_width <= 32 else 8
+        eids = np.empty(n, np.int32 if eid_bytes == 4 else np.int64)
+        masks = np.empty(n, np.uint32 if mask_bytes == 4 else np.uint64)
+        groups = np.empty(n, np.int32) if self.config.trace else None
+        counts = np.zeros(max(n_dest, 1), np.int64)
+        got = C.c_int64(0)
+        hs = (C.c_void_p * len(self._shards))(*[s.h.value for s in self._shards])
+        check(self._L.tsg_fetch_ordered(hs, len(self._shards), ptr(self._rank_of_size), self._rank_of_size.size,
+                                        ptr(eids), eid_bytes, ptr(masks), mask_bytes, ptr(groups), ptr(counts), n,
+                                        C.byref(got)))
+        return eids[:got.value], masks[:got.value], groups, counts[:n_dest]
 
     def reduce_store(self) -> int:
-        """engine.py:469-505; selection and compaction run on the GPU."""
+        """engine.py:469-505; selection and compaction run on the GPU(s),
+        exact across shards."""
         total = len(self.store)
         if total == 0:
             self._reduce_watermark = self._next_id
             return 0
         target = int(total * (1.0 - self.config.reduce_keep_fraction))
-        removed = C.c_int64(0)
-        ids = np.zeros(max(target, 1), dtype=np.int64)
-        check(self._L.tsg_reduce(self._h, self._reduce_watermark, target, C.byref(removed), ptr(ids)))
-        for eid in ids[:removed.value].tolist():
-            self._lits.pop(eid, None)
+        if len(self._shards) == 1:
+            removed = len(self._shards[0].reduce(self._reduce_watermark, target))
+        else:
+            removed, _ = _sharded.global_reduce(self._shards, self._reduce_watermark, target)
         with self._id_lock:
             self._reduce_watermark = self._next_id
         self.counters["reduces"] += 1
-        self.counters["clauses_removed"] += removed.value
-        return removed.value
+        self.counters["clauses_removed"] += removed
+        return removed
 
     def remove_clauses(self, engine_ids: Sequence[int]) -> int:
         """Explicit deletion (streaming config C4); order-preserving like
@@ -504,12 +656,9 @@ class Engine:
         ids = np.asarray(list(engine_ids), dtype=np.int64)
         if ids.size == 0:
             return 0
-        removed = C.c_int64(0)
-        check(self._L.tsg_remove_clauses(self._h, ptr(ids), ids.size, C.byref(removed)))
-        for eid in ids.tolist():
-            self._lits.pop(eid, None)
-        self.counters["clauses_deleted"] = self.counters.get("clauses_deleted", 0) + removed.value
-        return removed.value
+        removed = sum(s.remove(ids) for s in self._shards)
+        self.counters["clauses_deleted"] = self.counters.get("clauses_deleted", 0) + removed
+        return removed
 
     def serve(self, stop: threading.Event, idle_sleep: float = 0.0005) -> None:
         while not stop.is_set():
@@ -524,5 +673,6 @@ class Engine:
             out["staged_pending"] = len(self._staged)
         with self._queue_lock:
             out["reports_pending"] = sum(self._pending_reports.values())
-            out["snapshots_pending"] = sum(len(q) for q in self._snapshots.values())
+            queues = list(self._squeues.values())
+        out["snapshots_pending"] = sum(q.n + len(q.bad) for q in queues)
         return out

@@ -24,8 +24,8 @@ def P():
     return P
 
 
-def replay(P, spec):
-    eng = P.Engine(spec["num_vars"], spec["threads"], P.EngineConfig(**spec["config"]))
+def replay(P, spec, devices=None):
+    eng = P.Engine(spec["num_vars"], spec["threads"], P.EngineConfig(**spec["config"], devices=devices))
     for op, exp in zip(spec["ops"], spec["expect"]):
         if op[0] == "add":
             assert eng.add_clause(op[1], origin=op[2]) == exp["id"]
@@ -51,9 +51,13 @@ def replay(P, spec):
     eng.close()
 
 
-def test_reference_scenarios_bit_exact(P):
+# devices [0, 0]: the store sharded over two engines (one per listed GPU;
+# both on the test box's one GPU), tables copied peer to peer, records
+# ordered together, reduce exact across the shards
+@pytest.mark.parametrize("devices", [None, [0, 0]])
+def test_reference_scenarios_bit_exact(P, devices):
     for spec in engine_golden():
-        replay(P, spec)
+        replay(P, spec, devices)
 
 
 # ---- ported from the reference's tests/test_engine.py ---------------------

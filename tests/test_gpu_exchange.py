@@ -33,8 +33,8 @@ def X():
     return X
 
 
-@pytest.mark.parametrize("name", ["w32", "w8x2"])
-def test_replay_reference_solver_rounds(name):
+@pytest.mark.parametrize("name,devices", [("w32", None), ("w8x2", None), ("w8x2", [0, 0])])
+def test_replay_reference_solver_rounds(name, devices):
     # every recorded round rebuilt on the GPU Engine through the reference API:
     # the same clauses under the same engine ids (inserted in id order, so the
     # size buckets are created in the reference's order), the round's
@@ -49,7 +49,7 @@ def test_replay_reference_solver_rounds(name):
     n_reports = 0
     for k in range(int(fx["rounds"])):
         clauses, live, snaps, reps, result = c5_round(fx, k)
-        eng = P.Engine(nv, th, P.EngineConfig(lane_width=lw, group_width=gw))
+        eng = P.Engine(nv, th, P.EngineConfig(lane_width=lw, group_width=gw, devices=devices))
         for lits in clauses:
             eng.add_clause(lits, origin=0)
         eng.run_round()  # integrate (no snapshots: no activity or counter effects)

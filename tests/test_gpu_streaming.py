@@ -50,15 +50,17 @@ def store_of_oracle(ora):  # ClauseStore.clauses order (engine.py:221-231): size
     return [(eid, l, o, float(a).hex()) for eid, l, o, a in ora.store.clauses()]
 
 
-@pytest.mark.parametrize("seed,lw,gw,threads,cap,max_clauses", [
-    (1, 8, 4, 6, 20, 3000),     # multi-chunk rounds, capacity reduces
-    (2, 32, 32, 32, 64, 5000),  # the C4 shape: 32 threads, 64-deep queues -> 2 chunks
-    (3, 5, 64, 9, 11, 800),     # tiny store: reduce inside integrate, drops
+@pytest.mark.parametrize("seed,lw,gw,threads,cap,max_clauses,devices", [
+    (1, 8, 4, 6, 20, 3000, None),     # multi-chunk rounds, capacity reduces
+    (2, 32, 32, 32, 64, 5000, None),  # the C4 shape: 32 threads, 64-deep queues -> 2 chunks
+    (3, 5, 64, 9, 11, 800, None),     # tiny store: reduce inside integrate, drops
+    (1, 8, 4, 6, 20, 3000, [0, 0]),   # two clause shards (exact global reduce, merged records)
+    (2, 32, 32, 32, 64, 5000, [0, 0, 0]),
 ])
-def test_streaming_parity_vs_oracle_engine(P, seed, lw, gw, threads, cap, max_clauses):
+def test_streaming_parity_vs_oracle_engine(P, seed, lw, gw, threads, cap, max_clauses, devices):
     nv = 300
     cfg = dict(max_clauses=max_clauses, lane_width=lw, group_width=gw, assignment_queue_capacity=cap)
-    eng = P.Engine(nv, threads, P.EngineConfig(**cfg))
+    eng = P.Engine(nv, threads, P.EngineConfig(**cfg, devices=devices))
     ora = O.OracleEngine(nv, threads, **cfg)
     rng = np.random.default_rng(seed)
     for r in range(14):
