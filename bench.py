@@ -256,6 +256,87 @@ def run_reference(args, cfg):
     }), flush=True)
 
 
+def api_leg(cfg: W.Config, snaps, steps: int, local: int):
+    """The drop-in API timed the reference's way (instrumentation.py:248-250:
+    clauses_tested_per_second = lane_tests / busy_seconds, busy_seconds =
+    the Engine.run_round wall time, engine.py:379, 434): the reference's
+    Python surface (paper_2012_03119_b200.Engine) on the config's store.
+    Per round the solver side submits every thread's snapshots from a pool
+    of host threads (packing into page-locked queues) and drains its
+    reports (building the Report objects); both are timed apart from
+    run_round.  C4: a 1M-clause store at capacity, +20k
+    adds and 5k explicit deletes per round, 32 threads x 64 snapshots."""
+    from concurrent.futures import ThreadPoolExecutor
+    import paper_2012_03119_b200 as P
+    out = {}
+    for name in ("C3", "C4"):
+        if name == "C3":
+            nv, threads, per, n_store, adds, dels = cfg.num_vars, cfg.threads, cfg.lanes, cfg.n_clauses, 0, 0
+            rows = snaps
+        else:
+            nv, threads, per, n_store, adds, dels = 50_000, 32, 64, 1_000_000, 20_000, 5_000
+            rows = W.snapshots(threads, per, nv, np.random.default_rng(20121 + 4))
+        rng = np.random.default_rng(cfg.seed + 4242)
+        eng = P.Engine(nv, threads, P.EngineConfig(max_clauses=n_store, assignment_queue_capacity=per, device=local))
+        b = W.clause_buckets(n_store, nv, np.random.default_rng(cfg.seed if name == "C3" else 20121 + 4))
+        flat, offs, _ = W.flatten(b)
+        del b
+        eng.add_clauses(flat, offs)
+        del flat
+        eng.run_round()  # integrate (untimed)
+        pool = ThreadPoolExecutor(16)
+
+        def submit_all():
+            def one(t):
+                for i in range(per):
+                    eng.submit_assignment(P.AssignmentSnapshot(t, rows[t * per + i], i))
+            list(pool.map(one, range(threads)))
+
+        t_sub = t_drain = t_add = 0.0
+        n_rep = 0
+        phases = {}
+        for k in range(2 + steps):
+            if k == 2:  # measure from here
+                eng.counters["busy_seconds"] = 0.0
+                eng.counters["lane_tests"] = 0
+                t_sub = t_drain = t_add = 0.0
+                n_rep = 0
+            t0 = time.perf_counter()
+            if adds:
+                nb = W.clause_buckets(adds, nv, rng)
+                for arr in nb.values():
+                    for row in arr.tolist():
+                        eng.add_clause(row, origin=0)
+                eng.remove_clauses(rng.integers(0, eng._next_id, dels))
+            t1 = time.perf_counter()
+            submit_all()
+            t2 = time.perf_counter()
+            eng.run_round()
+            t3 = time.perf_counter()
+            if k >= 2:
+                for key, v in eng.last_phases.items():
+                    phases[key] = phases.get(key, 0.0) + v / steps
+            n_rep += sum(len(eng.drain_reports(t)) for t in range(threads))
+            t4 = time.perf_counter()
+            t_add += t1 - t0
+            t_sub += t2 - t1
+            t_drain += t4 - t3
+        c = eng.raw_counters()
+        out[name] = {"value": c["lane_tests"] / c["busy_seconds"], "unit": "clause_assignment_tests/s",
+                     "run_round_ms": c["busy_seconds"] / steps * 1e3, "rounds": steps,
+                     "run_round_phases_ms": phases,
+                     "store": c["store_size"], "assignments_per_round": threads * per,
+                     "reports_per_round": n_rep / steps,
+                     "solver_side_ms_per_round": {"submit": t_sub / steps * 1e3, "drain_reports": t_drain / steps * 1e3,
+                                                  "add_clause_and_deletes": t_add / steps * 1e3},
+                     "workload": (f"{name}: {n_store} clauses, {nv} vars, {threads} threads x {per} snapshots"
+                                  + (f", +{adds} adds / -{dels} deletes per round" if adds else ""))}
+        pool.shutdown()
+        eng.close()
+    out["metric"] = "lane_tests / busy_seconds (instrumentation.py:248-250) through Engine.run_round"
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -272,6 +353,7 @@ def main():
                     help="N>1: how the round's tables reach every shard -- each rank encodes its 1/N of the groups "
                          "and NCCL all-gathers them (split, default), rank 0 encodes and NCCL broadcasts (bcast), "
                          "or every rank encodes everything (replicated, no collective)")
+    ap.add_argument("--no-api", action="store_true", help="skip the Engine.run_round legs (C3, C4)")
     ap.add_argument("--verify", action="store_true",
                     help="after timing: gather every rank's records of one round to rank 0 and compare them with "
                          "the unsharded store's records on rank 0's GPU (adds 'verify' to the line)")
@@ -611,6 +693,13 @@ def main():
                                  f"of the timed region (rank {rank})",
                 "algorithmic_bytes": b_alg, "peak_kind": peak_kind}
 
+    api = None
+    if world == 1 and not args.no_api:
+        try:
+            api = api_leg(cfg, snaps, max(3, min(args.steps, 10)), local)
+        except Exception as exc:  # reported in the line, never fatal to it
+            api = {"error": repr(exc)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -665,6 +754,8 @@ def main():
         }
         if verify is not None:
             line["verify"] = verify
+        if api is not None:
+            line["api"] = api
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()

@@ -282,13 +282,22 @@ int tsg_set_record_bytes(tsg_engine* h, int32_t bytes);
 int tsg_fetch_ordered(tsg_engine* const* hs, int32_t n_h, const int32_t* rank_of_size, int32_t n_sizes,
                       void* eids, int32_t eid_bytes, void* masks, int32_t mask_bytes, int32_t* groups,
                       int64_t* dest_counts, int64_t cap, int64_t* n);
-/* The next round's packed rows from n_segs host segments (segment i: rows[i]
- * rows at segs[i], pitch_words apart), concatenated in order -- e.g. the
- * per-thread snapshot queues in pinned memory -- staged like
- * tsg_stage_packed (ingress stream; the segments must stay unchanged until
- * the round encoded from them is collected). */
+/* The next round's packed rows from n_segs segments in host or device memory
+ * (segment i: rows[i] rows at segs[i], pitch_words apart), concatenated in
+ * order -- e.g. the per-thread snapshot queues -- staged like
+ * tsg_stage_packed on the ingress stream, after every copy queued there by
+ * tsg_ingress_copy (the segments must stay unchanged until the round encoded
+ * from them is collected). */
 int tsg_stage_packed_segments(tsg_engine* h, const uint64_t* const* segs, const int64_t* rows, int32_t n_segs,
                               int64_t pitch_words);
+/* Device memory on the engine's device, and an asynchronous copy on the
+ * engine's ingress stream (host -> device for queued snapshot rows).
+ * tsg_ingress_copy may be called from any host thread concurrently with the
+ * engine worker; the source must stay unchanged until the next round that
+ * stages from the destination is collected. */
+int tsg_device_alloc(tsg_engine* h, int64_t bytes, void** p);
+int tsg_device_free(tsg_engine* h, void* p);
+int tsg_ingress_copy(tsg_engine* h, void* dst, const void* src, int64_t bytes);
 /* Page-locked host memory (cudaMallocHost) for ingress rows and records. */
 int tsg_host_alloc(int64_t bytes, void** p);
 int tsg_host_free(void* p);

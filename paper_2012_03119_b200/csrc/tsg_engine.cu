@@ -9,10 +9,12 @@
 #include <immintrin.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <unordered_set>
 #include <vector>
@@ -686,6 +688,12 @@ int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, 
     }
     if (offsets[n] > offsets[0] && !lits) return fail(TSG_EINVAL, "null literals");
     DevGuard g(h->dev);
+    static const bool trace_host = getenv("TSG_TRACE_HOST") != nullptr;
+    std::vector<std::pair<const char*, double>> tp;
+    auto mark = [&](const char* what) {
+        if (trace_host) tp.push_back({what, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count()});
+    };
+    mark("start");
     h->desc_dirty = true;
     h->store_seq++;
     // group clauses by size, preserving arrival order; new sizes create buckets
@@ -710,63 +718,94 @@ int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, 
             bucket_of[i] = it->second;
         }
     }
+    mark("buckets");
     // place every clause (pivot first), then one H2D + scatter per bucket
     std::vector<int32_t> placed((size_t)std::max<int64_t>(offsets[n] - offsets[0], 1));
     std::vector<uint64_t> hm(n);
+    {  // placement is independent per clause: split large batches over host threads
+        auto place_range = [&](int64_t a, int64_t b) {
+            for (int64_t i = a; i < b; ++i)
+                place_clause(h, lits + offsets[i], (int32_t)(offsets[i + 1] - offsets[i]),
+                             placed.data() + (offsets[i] - offsets[0]), &hm[i]);
+        };
+        const int64_t nt = std::min<int64_t>({(int64_t)std::max(1u, std::thread::hardware_concurrency()), 16, n / 2048});
+        if (nt > 1) {
+            std::vector<std::thread> pool;
+            for (int64_t t = 0; t < nt; ++t) pool.emplace_back(place_range, n * t / nt, n * (t + 1) / nt);
+            for (auto& t : pool) t.join();
+        } else {
+            place_range(0, n);
+        }
+    }
+    mark("place");
     std::vector<std::vector<int64_t>> members(h->buckets.size());
-    for (int64_t i = 0; i < n; ++i) {
-        const int32_t s = (int32_t)(offsets[i + 1] - offsets[i]);
-        place_clause(h, lits + offsets[i], s, placed.data() + (offsets[i] - offsets[0]), &hm[i]);
-        members[bucket_of[i]].push_back(i);
+    for (int64_t i = 0; i < n; ++i) members[bucket_of[i]].push_back(i);
+    mark("members");
+    if (h->pivot) {  // each bucket's new clauses in pivot-variable order (stable: ties keep arrival order)
+        // only batches dense enough for a 32-clause tile to share pivot lines
+        // gain from the order; a streaming batch of a few hundred clauses per
+        // bucket would only pay for the sort
+        std::vector<uint64_t> key;
+        for (auto& mem : members) {
+            if (mem.size() < 4096) continue;
+            key.resize(mem.size());
+            for (size_t c = 0; c < mem.size(); ++c) {
+                const int64_t i = mem[c];
+                const uint64_t v = offsets[i + 1] > offsets[i] ? (uint64_t)std::llabs((long long)placed[offsets[i] - offsets[0]]) : 0;
+                key[c] = v << 32 | (uint64_t)c;  // (pivot variable, position in the batch's bucket list)
+            }
+            std::sort(key.begin(), key.end());
+            std::vector<int64_t> sorted(mem.size());
+            for (size_t c = 0; c < mem.size(); ++c) sorted[c] = mem[key[c] & 0xFFFFFFFFu];
+            mem.swap(sorted);
+        }
     }
-    if (h->pivot) {  // each bucket's new clauses in pivot-variable order (stable)
-        for (auto& mem : members)
-            std::stable_sort(mem.begin(), mem.end(), [&](int64_t x, int64_t y) {
-                const int64_t sx = offsets[x + 1] - offsets[x], sy = offsets[y + 1] - offsets[y];
-                const int64_t vx = sx ? std::llabs((long long)placed[offsets[x] - offsets[0]]) : 0;
-                const int64_t vy = sy ? std::llabs((long long)placed[offsets[y] - offsets[0]]) : 0;
-                return vx < vy;
-            });
-    }
+    mark("sort");
+    // one host staging block for the whole batch (a pageable copy waits for
+    // the stream, so there is exactly one), clauses bucket-major: literals,
+    // ids, origins, order words, then the buckets' append descriptors; one
+    // append kernel for every bucket (k_append_batch)
+    auto al8 = [](int64_t x) { return (x + 7) / 8 * 8; };
+    int64_t n_lits = 0;
+    std::vector<AppendDesc> desc;
+    int64_t first = 0;
     for (size_t bi = 0; bi < members.size(); ++bi) {
-        auto& mem = members[bi];
-        if (mem.empty()) continue;
+        const int64_t k = (int64_t)members[bi].size();
+        if (!k) continue;
         Bucket& b = h->buckets[bi];
-        const int64_t k = (int64_t)mem.size();
         CKR(bucket_reserve(h, b, b.count + k));
-        std::vector<int32_t> hl((size_t)(k * b.size));
-        std::vector<int64_t> hid(k);
-        std::vector<int32_t> hor(k);
-        std::vector<uint64_t> hmk(k);
-        for (int64_t c = 0; c < k; ++c) {
-            const int64_t i = mem[c];
-            if (b.size) memcpy(&hl[c * b.size], placed.data() + (offsets[i] - offsets[0]), b.size * 4);
-            hid[c] = ids[i];
-            hor[c] = origins[i];
-            hmk[c] = hm[i];
-        }
-        if (b.size) {
-            int32_t* tmp = nullptr;
-            CKR(dalloc(h, (void**)&tmp, k * b.size * 4));
-            CK(cudaMemcpyAsync(tmp, hl.data(), k * b.size * 4, cudaMemcpyHostToDevice, h->st));
-            k_append<<<grid_for(k * b.size), 256, 0, h->st>>>(tmp, k, b.size, b.count, b.lits);
-            CK(cudaGetLastError());
-            dfree(h, tmp);
-        }
-        CK(cudaMemcpyAsync(b.ids + b.count, hid.data(), k * 8, cudaMemcpyHostToDevice, h->st));
-        CK(cudaMemcpyAsync(b.origins + b.count, hor.data(), k * 4, cudaMemcpyHostToDevice, h->st));
-        CK(cudaMemcpyAsync(b.order + b.count, hmk.data(), k * 8, cudaMemcpyHostToDevice, h->st));
-        k_fill_f64<<<grid_for(k), 256, 0, h->st>>>(b.acts + b.count, k, activity);
-        CK(cudaGetLastError());
+        desc.push_back(AppendDesc{b.lits, b.acts, b.ids, b.origins, b.order, b.count, first, n_lits, b.size, 0});
+        first += k;
+        n_lits += k * b.size;
         b.count += k;
-        CK(cudaStreamSynchronize(h->st));  // host vectors go out of scope
     }
-    // clause size by engine id (ids are non-negative and, per the reference,
-    // below 2^40 here): the record ordering looks up each record's bucket
-    if (h->max_id < ((int64_t)1 << 40)) {
+    const int64_t o_ids = al8(n_lits * 4), o_org = o_ids + n * 8, o_ord = o_org + al8(n * 4), o_desc = o_ord + n * 8;
+    const int64_t total_bytes = o_desc + (int64_t)(desc.size() * sizeof(AppendDesc));
+    std::vector<uint8_t> host((size_t)total_bytes);
+    {
+        int32_t* hl = reinterpret_cast<int32_t*>(host.data());
+        int64_t* hid = reinterpret_cast<int64_t*>(host.data() + o_ids);
+        int32_t* hor = reinterpret_cast<int32_t*>(host.data() + o_org);
+        uint64_t* hmk = reinterpret_cast<uint64_t*>(host.data() + o_ord);
+        int64_t c = 0, l = 0;
+        for (size_t bi = 0; bi < members.size(); ++bi) {
+            const int32_t sz = h->buckets[bi].size;
+            for (const int64_t i : members[bi]) {
+                if (sz) memcpy(hl + l, placed.data() + (offsets[i] - offsets[0]), sz * 4);
+                l += sz;
+                hid[c] = ids[i];
+                hor[c] = origins[i];
+                hmk[c] = hm[i];
+                ++c;
+            }
+        }
+        memcpy(host.data() + o_desc, desc.data(), desc.size() * sizeof(AppendDesc));
+    }
+    const bool sizes_by_id = h->max_id < ((int64_t)1 << 40);
+    if (sizes_by_id) {  // clause size by engine id: the record ordering looks up each record's bucket
         const int64_t need = h->max_id + 1;
         if (need > h->size_of_id_cap) {
-            int64_t nc = std::max<int64_t>(need, 2 * h->size_of_id_cap);
+            const int64_t nc = std::max<int64_t>(need, 2 * h->size_of_id_cap);
             int32_t* np = nullptr;
             CKR(dalloc(h, (void**)&np, nc * 4));
             if (h->size_of_id) CK(cudaMemcpyAsync(np, h->size_of_id, h->size_of_id_cap * 4, cudaMemcpyDeviceToDevice, h->st));
@@ -774,19 +813,25 @@ int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, 
             h->size_of_id = np;
             h->size_of_id_cap = nc;
         }
-        std::vector<int32_t> hs(n);
-        for (int64_t i = 0; i < n; ++i) hs[i] = (int32_t)(offsets[i + 1] - offsets[i]);
-        int64_t* did = nullptr;
-        int32_t* dsz = nullptr;
-        CKR(dalloc(h, (void**)&did, n * 8));
-        CKR(dalloc(h, (void**)&dsz, n * 4));
-        CK(cudaMemcpyAsync(did, ids, n * 8, cudaMemcpyHostToDevice, h->st));
-        CK(cudaMemcpyAsync(dsz, hs.data(), n * 4, cudaMemcpyHostToDevice, h->st));
-        k_set_sizes<<<grid_for(n), 256, 0, h->st>>>(did, dsz, n, h->size_of_id);
-        CK(cudaGetLastError());
-        dfree(h, did);
-        dfree(h, dsz);
-        CK(cudaStreamSynchronize(h->st));  // hs goes out of scope
+    }
+    mark("block");
+    uint8_t* dev = nullptr;
+    CKR(dalloc(h, (void**)&dev, std::max<int64_t>(total_bytes, 8)));
+    CK(cudaMemcpyAsync(dev, host.data(), total_bytes, cudaMemcpyHostToDevice, h->st));  // host block consumed on return
+    mark("h2d");
+    k_append_batch<<<grid_for(n), 256, 0, h->st>>>(reinterpret_cast<const AppendDesc*>(dev + o_desc), (int32_t)desc.size(), n,
+                                                   reinterpret_cast<const int32_t*>(dev),
+                                                   reinterpret_cast<const int64_t*>(dev + o_ids),
+                                                   reinterpret_cast<const int32_t*>(dev + o_org),
+                                                   reinterpret_cast<const uint64_t*>(dev + o_ord), activity,
+                                                   sizes_by_id ? h->size_of_id : nullptr);
+    CK(cudaGetLastError());
+    dfree(h, dev);
+    mark("launches");
+    if (trace_host) {
+        fprintf(stderr, "tsg_add_clauses n=%lld:", (long long)n);
+        for (size_t i = 1; i < tp.size(); ++i) fprintf(stderr, " %s %.3f", tp[i].first, tp[i].second - tp[i - 1].second);
+        fprintf(stderr, " ms\n");
     }
     h->totals.clauses_added += n;
     return TSG_OK;
@@ -1702,10 +1747,47 @@ int tsg_host_free(void* p) {
     return TSG_OK;
 }
 
-// The next round's packed rows from several host segments (segment i:
-// rows[i] rows at segs[i], pitch_words apart), concatenated in order -- the
-// per-thread snapshot queues of the Engine, grouped by tid, without a host
-// copy.  Same staging buffers and ingress stream as tsg_stage_packed.
+// Device memory on the engine's device, and a host-to-device copy on the
+// engine's ingress stream -- the snapshot queues of the Engine: a solver
+// thread packs its snapshot into page-locked memory and queues its copy into
+// the thread's device queue region at submit time, so a round's rows are on
+// the device before the round starts.  tsg_ingress_copy is the one entry
+// point that other host threads may call concurrently with the engine's
+// worker (it touches only the ingress stream).
+int tsg_device_alloc(tsg_engine* h, int64_t bytes, void** p) {
+    CKR(validate_handle(h));
+    if (!p || bytes < 0) return fail(TSG_EINVAL, "bad arguments");
+    *p = nullptr;
+    if (!bytes) return TSG_OK;
+    DevGuard g(h->dev);
+    CK(cudaMalloc(p, (size_t)bytes));
+    return TSG_OK;
+}
+
+int tsg_device_free(tsg_engine* h, void* p) {
+    CKR(validate_handle(h));
+    if (!p) return TSG_OK;
+    DevGuard g(h->dev);
+    CK(cudaStreamSynchronize(h->ingress));  // no queued copy still targets it
+    CK(cudaFree(p));
+    return TSG_OK;
+}
+
+int tsg_ingress_copy(tsg_engine* h, void* dst, const void* src, int64_t bytes) {
+    CKR(validate_handle(h));
+    if (bytes < 0 || (bytes && (!dst || !src))) return fail(TSG_EINVAL, "bad arguments");
+    if (!bytes) return TSG_OK;
+    DevGuard g(h->dev);
+    CK(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, h->ingress));
+    return TSG_OK;
+}
+
+// The next round's packed rows from several segments in host or device
+// memory (segment i: rows[i] rows at segs[i], pitch_words apart),
+// concatenated in order -- the per-thread snapshot queues of the Engine,
+// grouped by tid, without a host copy.  Same staging buffers and ingress
+// stream as tsg_stage_packed (so copies queued by tsg_ingress_copy land
+// first).
 int tsg_stage_packed_segments(tsg_engine* h, const uint64_t* const* segs, const int64_t* rows, int32_t n_segs,
                               int64_t pitch_words) {
     CKR(validate_handle(h));
@@ -1808,17 +1890,18 @@ int tsg_fetch_ordered(tsg_engine* const* hs, int32_t n_h, const int32_t* rank_of
     const int gw = h0->cfg.group_width;
     const int dest_bits = bits_for(n_dest - 1), chunk_bits = bits_for(rd.n_chunks - 1);
     const int rank_bits = bits_for(n_sizes - 1), id_bits = bits_for(max_id), g_bits = bits_for(gw - 1);
-    const int key_bits = dest_bits + chunk_bits + rank_bits + id_bits + g_bits;
+    const int low_bits = chunk_bits + rank_bits + id_bits + g_bits;  // the destination field sits above
+    const int key_bits = dest_bits + low_bits;
     if (key_bits > 64) return fail(TSG_ECAPACITY, "record order key needs %d bits", key_bits);
     std::vector<uint64_t> gkey(rd.n_groups);
     for (int g = 0; g < rd.n_groups; ++g) gkey[g] = ((uint64_t)dest_of[g] << chunk_bits) | (uint64_t)(g / gw);
     const int64_t rec_bytes = rec8 ? 8 : 16;
-    // device 0: concatenated records, keys / vals double buffers, counters
+    // device 0: concatenated records (several shards), keys / vals double buffers
     DevGuard g0(h0->dev);
     uint8_t* recs = nullptr;
     uint64_t *k0 = nullptr, *k1 = nullptr;
     uint32_t *v0 = nullptr, *v1 = nullptr, *hist = nullptr, *rowsum = nullptr;
-    unsigned long long *gcount = nullptr, *gscratch = nullptr;
+    int64_t* starts = nullptr;
     uint8_t* out = nullptr;
     const int64_t nblk = (total + SORT_TILE - 1) / SORT_TILE;
     if (n_h > 1) CKR(dalloc(h0, (void**)&recs, total * rec_bytes));
@@ -1828,14 +1911,12 @@ int tsg_fetch_ordered(tsg_engine* const* hs, int32_t n_h, const int32_t* rank_of
     CKR(dalloc(h0, (void**)&v1, total * 4));
     CKR(dalloc(h0, (void**)&hist, 256 * nblk * 4 + 256 * 4));
     rowsum = hist + 256 * nblk;
-    CKR(dalloc(h0, (void**)&gcount, (int64_t)rd.n_groups * 8));
-    if (n_h > 1) CKR(dalloc(h0, (void**)&gscratch, (int64_t)rd.n_groups * 8));
+    CKR(dalloc(h0, (void**)&starts, (int64_t)(n_dest + 1) * 8));
     const int64_t eid_sec = round_up(total * eid_bytes, 256), mask_sec = round_up(total * mask_bytes, 256);
     CKR(dalloc(h0, (void**)&out, eid_sec + mask_sec + (groups ? total * 4 : 0)));
-    CK(cudaMemsetAsync(gcount, 0, (size_t)rd.n_groups * 8, h0->st));
     CK(cudaEventRecord(h0->ev_peer, h0->st));  // device 0's buffers exist before any shard copies into them
     // per shard: keys on its device, then (if not device 0's own) its keys,
-    // vals, records and group counts copied to device 0
+    // vals and records copied to device 0
     int64_t base = 0;
     for (int32_t s = 0; s < n_h; ++s) {
         tsg_engine* h = hs[s];
@@ -1846,47 +1927,33 @@ int tsg_fetch_ordered(tsg_engine* const* hs, int32_t n_h, const int32_t* rank_of
         int32_t* dr = nullptr;
         uint64_t* kk = k0 + base;
         uint32_t* vv = v0 + base;
-        unsigned long long* gc = gcount;
         if (s > 0) {
             CK(cudaStreamWaitEvent(h->st, h0->ev_peer, 0));
             CKR(dalloc(h, (void**)&kk, R.n_out * 8));
             CKR(dalloc(h, (void**)&vv, R.n_out * 4));
-            CKR(dalloc(h, (void**)&gc, (int64_t)rd.n_groups * 8));
-            CK(cudaMemsetAsync(gc, 0, (size_t)rd.n_groups * 8, h->st));
         }
         CKR(dalloc(h, (void**)&dg, (int64_t)rd.n_groups * 8));
         CKR(dalloc(h, (void**)&dr, (int64_t)n_sizes * 4));
         CK(cudaMemcpyAsync(dg, gkey.data(), rd.n_groups * 8, cudaMemcpyHostToDevice, h->st));
         CK(cudaMemcpyAsync(dr, rank_of_size, n_sizes * 4, cudaMemcpyHostToDevice, h->st));
         OrderKey ok{dg, h->size_of_id, dr, n_sizes, rank_bits, id_bits, g_bits, gw, rec8 ? 1 : 0};
-        k_order_keys<<<grid_for(R.n_out), 256, 0, h->st>>>(R.out, R.n_out, base, ok, kk, vv, gc);
+        k_order_keys<<<grid_for(R.n_out), 256, 0, h->st>>>(R.out, R.n_out, base, ok, kk, vv);
         CK(cudaGetLastError());
         if (s > 0) {
             CK(cudaMemcpyPeerAsync(k0 + base, h0->dev, kk, h->dev, R.n_out * 8, h->st));
             CK(cudaMemcpyPeerAsync(v0 + base, h0->dev, vv, h->dev, R.n_out * 4, h->st));
             CK(cudaMemcpyPeerAsync(recs + base * rec_bytes, h0->dev, R.out, h->dev, R.n_out * rec_bytes, h->st));
-            // the shard's group counts: added on device 0 below
-            CK(cudaMemcpyPeerAsync(gscratch, h0->dev, gc, h->dev, (size_t)rd.n_groups * 8, h->st));
             CK(cudaEventRecord(h->ev_peer, h->st));
-            dfree(h, kk); dfree(h, vv); dfree(h, gc);
+            dfree(h, kk); dfree(h, vv);
+            DevGuard gz(h0->dev);
+            CK(cudaStreamWaitEvent(h0->st, h->ev_peer, 0));  // device 0 sorts after the copies
         } else if (n_h > 1) {
             CK(cudaMemcpyAsync(recs, R.out, R.n_out * rec_bytes, cudaMemcpyDeviceToDevice, h->st));
         }
-        CK(cudaStreamSynchronize(h->st));  // gkey / rank_of_size uploads, and k1 reused per shard
-        if (s > 0) {  // (host-ordered: the shard's copies are done, device 0's stream is drained)
-            DevGuard gz(h0->dev);
-            std::vector<unsigned long long> hc(rd.n_groups), acc(rd.n_groups);
-            CK(cudaStreamSynchronize(h0->st));
-            CK(cudaMemcpyAsync(hc.data(), gscratch, rd.n_groups * 8, cudaMemcpyDeviceToHost, h0->st));
-            CK(cudaMemcpyAsync(acc.data(), gcount, rd.n_groups * 8, cudaMemcpyDeviceToHost, h0->st));
-            CK(cudaStreamSynchronize(h0->st));
-            for (int g = 0; g < rd.n_groups; ++g) acc[g] += hc[g];
-            CK(cudaMemcpyAsync(gcount, acc.data(), rd.n_groups * 8, cudaMemcpyHostToDevice, h0->st));
-            CK(cudaStreamSynchronize(h0->st));
-        }
-        dfree(h, dg); dfree(h, dr);
+        dfree(h, dg); dfree(h, dr);  // (stream-ordered after the kernel)
         base += R.n_out;
     }
+    // (pageable sources: the gkey / rank_of_size copies consumed them on return)
     const void* src = n_h > 1 ? (const void*)recs : (const void*)h0->rs[h0->fetch_rs].out;
     // LSD passes over the key's significant bits
     uint64_t *ka = k0, *kb = k1;
@@ -1900,6 +1967,7 @@ int tsg_fetch_ordered(tsg_engine* const* hs, int32_t n_h, const int32_t* rank_of
         std::swap(ka, kb);
         std::swap(va, vb);
     }
+    k_dest_starts<<<grid_for(total + 1), 256, 0, h0->st>>>(ka, total, low_bits, n_dest, starts);
     uint8_t* oe = out;
     uint8_t* om = out + eid_sec;  // sections 256-byte aligned for the 8-byte fields
     int32_t* og = groups ? reinterpret_cast<int32_t*>(om + mask_sec) : nullptr;
@@ -1909,12 +1977,12 @@ int tsg_fetch_ordered(tsg_engine* const* hs, int32_t n_h, const int32_t* rank_of
     CK(cudaMemcpyAsync(eids, oe, total * eid_bytes, cudaMemcpyDeviceToHost, h0->st));
     CK(cudaMemcpyAsync(masks, om, total * mask_bytes, cudaMemcpyDeviceToHost, h0->st));
     if (groups) CK(cudaMemcpyAsync(groups, og, total * 4, cudaMemcpyDeviceToHost, h0->st));
-    std::vector<unsigned long long> gc(rd.n_groups);
-    CK(cudaMemcpyAsync(gc.data(), gcount, rd.n_groups * 8, cudaMemcpyDeviceToHost, h0->st));
+    std::vector<int64_t> st(n_dest + 1);
+    CK(cudaMemcpyAsync(st.data(), starts, (n_dest + 1) * 8, cudaMemcpyDeviceToHost, h0->st));
     CK(cudaStreamSynchronize(h0->st));
-    for (int g = 0; g < rd.n_groups; ++g) dest_counts[dest_of[g]] += (int64_t)gc[g];
+    for (int32_t d = 0; d < n_dest; ++d) dest_counts[d] = st[d + 1] - st[d];
     dfree(h0, recs); dfree(h0, k0); dfree(h0, k1); dfree(h0, v0); dfree(h0, v1); dfree(h0, hist);
-    dfree(h0, gcount); dfree(h0, gscratch); dfree(h0, out);
+    dfree(h0, starts); dfree(h0, out);
     return TSG_OK;
 }
 

@@ -45,10 +45,9 @@ __device__ __forceinline__ void rec_fields(const void* recs, int rec8, int64_t i
     }
 }
 
-// keys of records [0, n) (vals = base + i) and the per-group record counts
+// keys of records [0, n) (vals = base + i)
 __global__ void k_order_keys(const void* __restrict__ recs, int64_t n, int64_t base, OrderKey k,
-                             uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                             unsigned long long* __restrict__ group_count) {
+                             uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     for (; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         uint64_t eid, mask;
@@ -61,7 +60,19 @@ __global__ void k_order_keys(const void* __restrict__ recs, int64_t n, int64_t b
         key = (key << k.g_bits) | (uint64_t)(g % (uint32_t)k.group_width);
         keys[i] = key;
         vals[i] = (uint32_t)(base + i);
-        atomicAdd(group_count + g, 1ull);
+    }
+}
+
+// first sorted position of every destination: start[d] for d in [0, n_dest]
+// (start[n_dest] = n), from the destination field (key >> dshift) of the
+// sorted keys -- each position opens the destinations since its neighbour's
+__global__ void k_dest_starts(const uint64_t* __restrict__ keys, int64_t n, int dshift, int32_t n_dest,
+                              int64_t* __restrict__ start) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i <= n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t d = i < n ? (int64_t)(dshift >= 64 ? 0 : keys[i] >> dshift) : n_dest;
+        const int64_t dp = i > 0 ? (int64_t)(dshift >= 64 ? 0 : keys[i - 1] >> dshift) : -1;
+        for (int64_t x = dp + 1; x <= d; ++x) start[x] = i;
     }
 }
 

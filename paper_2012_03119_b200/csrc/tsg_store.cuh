@@ -24,6 +24,44 @@ __global__ void k_append(const int32_t* __restrict__ src, int64_t n, int32_t siz
     }
 }
 
+// K6 for a whole insert batch: the batch's clauses bucket-major (bucket b's
+// at [first, first + k) of the batch, literals clause-major from lit0), each
+// appended at slot count0 + local of its bucket with its id, origin, order
+// word and initial activity; also the clause size by engine id.
+struct AppendDesc {
+    int32_t* lits;
+    double* acts;
+    int64_t* ids;
+    int32_t* org;
+    uint64_t* order;
+    int64_t count0, first, lit0;
+    int32_t size, pad;
+};
+
+__global__ void k_append_batch(const AppendDesc* __restrict__ d, int32_t nd, int64_t k_total,
+                               const int32_t* __restrict__ lits_src, const int64_t* __restrict__ ids_src,
+                               const int32_t* __restrict__ org_src, const uint64_t* __restrict__ order_src,
+                               double act, int32_t* __restrict__ size_of_id) {
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; c < k_total; c += (int64_t)gridDim.x * blockDim.x) {
+        int lo = 0, hi = nd - 1;  // the bucket: last descriptor with first <= c
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (d[mid].first <= c) lo = mid; else hi = mid - 1;
+        }
+        const AppendDesc b = d[lo];
+        const int64_t local = c - b.first, slot = b.count0 + local;
+        b.ids[slot] = ids_src[c];
+        b.org[slot] = org_src[c];
+        b.order[slot] = order_src[c];
+        b.acts[slot] = act;
+        if (size_of_id) size_of_id[ids_src[c]] = b.size;
+        const int32_t* src = lits_src + b.lit0 + local * b.size;
+        int32_t* dst = b.lits + (slot / STRIDE) * b.size * STRIDE + (slot % STRIDE);
+        for (int j = 0; j < b.size; ++j) dst[(int64_t)j * STRIDE] = src[j];
+    }
+}
+
 __global__ void k_fill_f64(double* p, int64_t n, double v) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     for (; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;

@@ -13,9 +13,11 @@ the round's kernels.
 Host data paths, none of them per-record Python work:
 
 * snapshots are packed (2 bits per variable, tsg_pack_rows, GIL released)
-  by the submitting solver thread straight into that thread's page-locked
-  queue region, and a round stages every thread's region as one segment
-  (tsg_stage_packed_segments) -- no host copy of the rows;
+  by the submitting solver thread into that thread's page-locked queue
+  region and copied to the device at once (tsg_ingress_copy, the engine's
+  ingress stream); a round stages every thread's device region as one
+  segment (tsg_stage_packed_segments) -- no host copy of the rows and no
+  host-to-device copy on the round's path;
 * a round's reports are ordered on the GPU into the reference's delivery
   order (tsg_fetch_ordered) and queued per destination as array slices;
   the ``Report`` objects, with their literals from an append-only literal
@@ -31,6 +33,7 @@ CUDA device raises.
 """
 from __future__ import annotations
 
+import array
 import ctypes as C
 import threading
 import time
@@ -104,11 +107,13 @@ class Report:
 @dataclass
 class _ReportBatch:
     """One round's reports for one destination, in delivery order: engine
-    ids and lane masks, with the literal arena as it was at round time."""
+    ids and lane masks (views of the round's page-locked record buffer,
+    `keep`), with the literal arena as it was at round time."""
 
     eids: np.ndarray
     masks: np.ndarray
     arena: "_Arena"
+    keep: object = None
 
     def __len__(self):
         return len(self.eids)
@@ -173,22 +178,95 @@ class _Arena:
         return tuple(self.lits[o:o + int(self.size[eid])].tolist())
 
 
-class _SnapQueue:
-    """One solver thread's snapshot queue: packed rows in one of two
-    page-locked regions (the round drains one while submissions fill the
-    other), plus the snapshot objects for trace mode."""
+class _Run:
+    """Clauses staged by consecutive add_clause calls (engine.py:305-317),
+    kept flat (C arrays appended under the id lock) so integration needs no
+    per-literal Python work."""
 
-    def __init__(self, lib, cap: int, words: int):
+    __slots__ = ("first", "lits", "lens", "org")
+
+    def __init__(self, first: int):
+        self.first = first
+        self.lits = array.array("i")
+        self.lens = array.array("i")
+        self.org = array.array("i")
+
+    def arrays(self):
+        n = len(self.lens)
+        return (np.arange(self.first, self.first + n, dtype=np.int64),
+                np.frombuffer(self.lens, dtype=np.int32).astype(np.int64) if n else np.zeros(0, np.int64),
+                np.frombuffer(self.lits, dtype=np.int32) if len(self.lits) else np.zeros(0, np.int32),
+                np.frombuffer(self.org, dtype=np.int32) if n else np.zeros(0, np.int32))
+
+
+class _PinnedPool:
+    """Page-locked host buffers for the rounds' ordered records: the device
+    writes them at link rate, and the report batches view them in place.  A
+    buffer returns to the pool when the last batch viewing it is drained."""
+
+    class Buf:
+        def __init__(self, pool, p, nbytes):
+            self.pool, self.p, self.nbytes = pool, p, nbytes
+
+        def __del__(self):
+            self.pool._release(self.p, self.nbytes)
+
+    def __init__(self, lib):
+        self._lib = lib
+        self._lock = threading.Lock()
+        self._free: List[Tuple[object, int]] = []
+        self._closed = False
+
+    def get(self, nbytes: int) -> "_PinnedPool.Buf":
+        with self._lock:
+            fit = [f for f in self._free if f[1] >= nbytes]
+            if fit:
+                f = min(fit, key=lambda x: x[1])
+                self._free.remove(f)
+                return _PinnedPool.Buf(self, *f)
+        size = max(nbytes + nbytes // 2, 1 << 20)
+        p = C.c_void_p()
+        check(self._lib.tsg_host_alloc(size, C.byref(p)))
+        return _PinnedPool.Buf(self, p, size)
+
+    def _release(self, p, nbytes):
+        with self._lock:
+            if self._closed:
+                self._lib.tsg_host_free(p)
+            else:
+                self._free.append((p, nbytes))
+
+    def close(self):
+        with self._lock:
+            self._closed = True
+            free, self._free = self._free, []
+        for p, _ in free:
+            self._lib.tsg_host_free(p)
+
+
+class _SnapQueue:
+    """One solver thread's snapshot queue: packed rows in one of two regions
+    (the round drains one while submissions fill the other), each a
+    page-locked host region plus its device copy -- a submit packs the row
+    into host memory and queues its copy to the device on the engine's
+    ingress stream (tsg_ingress_copy), so the round finds its rows on the
+    device -- plus the snapshot objects for trace mode."""
+
+    def __init__(self, lib, h, cap: int, words: int):
         self.lock = threading.Lock()
         self.cap, self.words = cap, words
-        self._lib = lib
+        self._lib, self._h = lib, h
         self._raw = [None, None]
+        self.dev = [None, None]
         self.rows = [None, None]
         for r in range(2):
             p = C.c_void_p()
             check(lib.tsg_host_alloc(cap * words * 8, C.byref(p)))
             self._raw[r] = p
             self.rows[r] = np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_uint64)), shape=(cap, words))
+            d = C.c_void_p()
+            check(lib.tsg_device_alloc(h, cap * words * 8, C.byref(d)))
+            self.dev[r] = d
         self.cur = 0
         self.n = 0
         self.snaps: List[object] = []
@@ -199,6 +277,9 @@ class _SnapQueue:
             if self._raw[r] is not None:
                 self._lib.tsg_host_free(self._raw[r])
                 self._raw[r] = None
+            if self.dev[r] is not None:
+                self._lib.tsg_device_free(self._h, self.dev[r])
+                self.dev[r] = None
 
 
 class _StoreShards:
@@ -300,6 +381,7 @@ class Engine:
         self._rec_bytes = 16
         self.store = _StoreShards(self)
         self._arena = _Arena()
+        self._pinned = _PinnedPool(self._L)
         self._sizes_in_order: List[int] = []                # bucket creation order (dict order)
         self._rank_of_size = np.zeros(64, dtype=np.int32)   # creation rank by clause size
         self._shard_load = np.zeros((len(self._shards), 64), dtype=np.int64)  # clauses per (shard, size)
@@ -316,6 +398,7 @@ class Engine:
         self._activity_inc = 1.0
         self._reduce_watermark = 0
         self.last_round: Optional[_lib.tsg_round_result] = None
+        self.last_phases: Dict[str, float] = {}  # wall ms of the last run_round's phases
 
         self.counters = {
             "rounds": 0, "clauses_added": 0, "clauses_dropped": 0, "clauses_removed": 0,
@@ -328,6 +411,8 @@ class Engine:
     def close(self) -> None:
         for q in getattr(self, "_squeues", {}).values():
             q.close()
+        if getattr(self, "_pinned", None) is not None:
+            self._pinned.close()
         for s in getattr(self, "_shards", []):
             s.close()
         self._shards = []
@@ -343,11 +428,17 @@ class Engine:
     # producer side (solver threads), engine.py:305-343
 
     def add_clause(self, lits: Sequence[int], origin: int) -> int:
-        lits = tuple(lits)
         with self._id_lock:
             engine_id = self._next_id
             self._next_id += 1
-            self._staged.append((engine_id, lits, origin))
+            run = self._staged[-1] if self._staged and isinstance(self._staged[-1], _Run) else None
+            if run is None:
+                run = _Run(engine_id)
+                self._staged.append(run)
+            n0 = len(run.lits)
+            run.lits.extend(lits)
+            run.lens.append(len(run.lits) - n0)
+            run.org.append(origin)
         return engine_id
 
     def _queue(self, tid: int) -> _SnapQueue:
@@ -356,7 +447,7 @@ class Engine:
             with self._queue_lock:
                 q = self._squeues.get(tid)
                 if q is None:
-                    q = _SnapQueue(self._L, self.config.assignment_queue_capacity, self._packed_words)
+                    q = _SnapQueue(self._L, self._h, self.config.assignment_queue_capacity, self._packed_words)
                     self._squeues[tid] = q
         return q
 
@@ -375,9 +466,10 @@ class Engine:
                 if vals.ndim != 1 or vals.shape[0] != self.num_vars + 1:
                     q.bad.append(vals.shape[0] if vals.ndim == 1 else -1)
                 else:  # (the GIL is released while the row is packed)
-                    check(self._L.tsg_pack_rows(ptr(vals), 1, vals.shape[0], self.num_vars,
-                                                C.c_void_p(q.rows[q.cur].ctypes.data + q.n * q.words * 8),
-                                                q.words))
+                    off = q.n * q.words * 8
+                    host = C.c_void_p(q.rows[q.cur].ctypes.data + off)
+                    check(self._L.tsg_pack_rows(ptr(vals), 1, vals.shape[0], self.num_vars, host, q.words))
+                    check(self._L.tsg_ingress_copy(self._h, C.c_void_p(q.dev[q.cur].value + off), host, q.words * 8))
                     q.n += 1
                 if self.config.trace:
                     q.snaps.append(snapshot)
@@ -413,21 +505,32 @@ class Engine:
     # ------------------------------------------------------------------
     # engine worker side
 
-    def _insert(self, batch) -> None:
-        """Append staged (id, lits, origin) to the store at the current
+    def add_clauses(self, flat, offsets, origin=0) -> int:
+        """Bulk add_clause (an extension of the reference API for loading a
+        store): clause i is flat[offsets[i]:offsets[i+1]]; consecutive engine
+        ids are assigned under the id lock and the batch is staged like
+        add_clause's.  `origin`: one int or one per clause.  Returns the
+        first id."""
+        flat = np.ascontiguousarray(flat, np.int32)
+        offsets = np.ascontiguousarray(offsets, np.int64)
+        n = len(offsets) - 1
+        org = np.broadcast_to(np.asarray(origin, np.int32), (n,)).copy()
+        with self._id_lock:
+            first = self._next_id
+            self._next_id += n
+            self._staged.append((np.arange(first, first + n, dtype=np.int64), np.diff(offsets),
+                                 flat[offsets[0]:offsets[-1]], org))
+        return first
+
+    def _insert(self, ids: np.ndarray, lens: np.ndarray, flat: np.ndarray, org: np.ndarray) -> None:
+        """Append clauses (engine ids ascending) to the store at the current
         activity increment (engine.py:357): shard by size (every bucket
         balanced over the devices), literals into the arena."""
-        if not batch:
+        n = len(ids)
+        if not n:
             return
-        n = len(batch)
-        lens = np.fromiter((len(b[1]) for b in batch), dtype=np.int64, count=n)
         offs = np.zeros(n + 1, dtype=np.int64)
         np.cumsum(lens, out=offs[1:])
-        total = int(offs[-1])
-        flat = np.fromiter((x for b in batch for x in b[1]), dtype=np.int32, count=total) \
-            if total else np.zeros(0, dtype=np.int32)
-        ids = np.fromiter((b[0] for b in batch), dtype=np.int64, count=n)
-        org = np.fromiter((b[2] for b in batch), dtype=np.int32, count=n)
         # bucket creation order (dict insertion order): new sizes in first-seen order
         sizes, first = np.unique(lens, return_index=True)
         top = int(sizes[-1]) + 1
@@ -461,8 +564,8 @@ class Engine:
                     continue
                 so = np.zeros(sel.size + 1, np.int64)
                 np.cumsum(lens[sel], out=so[1:])
-                sf = np.concatenate([flat[offs[i]:offs[i + 1]] for i in sel]) if so[-1] else np.zeros(0, np.int32)
-                sh.add_clauses(sf, so, ids[sel], org[sel], self._activity_inc)
+                keep = np.repeat(shard_of == r, lens)
+                sh.add_clauses(flat[keep], so, ids[sel], org[sel], self._activity_inc)
                 np.add.at(self._shard_load[r], lens[sel], 1)
         self._arena.append(ids, lens.astype(np.int32), flat)
         self.counters["clauses_added"] += n
@@ -472,15 +575,22 @@ class Engine:
         reduce once per incoming clause and drop it if still full."""
         with self._id_lock:
             staged, self._staged = self._staged, []
-        i, n = 0, len(staged)
+        if not staged:
+            return
+        # the staged clauses as arrays, in id order (add_clause runs and add_clauses batches)
+        parts = [b.arrays() if isinstance(b, _Run) else b for b in staged]
+        ids, lens, flat, org = (np.concatenate([p[k] for p in parts]) for k in range(4))
+        offs = np.zeros(len(ids) + 1, dtype=np.int64)
+        np.cumsum(lens, out=offs[1:])
+        i, n = 0, len(ids)
         size = len(self.store)
         while i < n:
             room = self.config.max_clauses - size
             if room > 0:
-                take = staged[i:i + room]
-                self._insert(take)
-                size += len(take)
-                i += len(take)
+                j = min(n, i + room)
+                self._insert(ids[i:j], lens[i:j], flat[offs[i]:offs[j]], org[i:j])
+                size += j - i
+                i = j
                 continue
             self.reduce_store()
             size = len(self.store)
@@ -498,7 +608,7 @@ class Engine:
             with q.lock:
                 if not q.n and not q.bad:
                     continue
-                out.append((tid, q.rows[q.cur], q.n, q.snaps, q.bad))
+                out.append((tid, q.dev[q.cur].value, q.n, q.snaps, q.bad))
                 q.cur ^= 1
                 q.n = 0
                 q.snaps = []
@@ -508,7 +618,9 @@ class Engine:
     def run_round(self) -> RoundResult:
         """engine.py:369-435 with the test phase on the GPU(s)."""
         started = time.perf_counter()
+        ph = {}
         self._integrate_exports()
+        ph["integrate"] = time.perf_counter()
         store_snapshot = None
         if self.config.trace:
             store_snapshot = [(eid, lits) for eid, lits, _, _ in self.store.clauses()]
@@ -533,7 +645,7 @@ class Engine:
         if lanes:
             gl = np.asarray(lanes, dtype=np.int32)
             gt = np.asarray(tids, dtype=np.int32)
-            segs = (C.c_void_p * len(pending))(*[rows.ctypes.data for _, rows, _, _, _ in pending])
+            segs = (C.c_void_p * len(pending))(*[dev for _, dev, _, _, _ in pending])
             cnts = np.asarray([n for _, _, n, _, _ in pending], dtype=np.int64)
             check(self._L.tsg_stage_packed_segments(self._h, segs, ptr(cnts), len(pending), self._packed_words))
             if lw <= 32:
@@ -544,7 +656,9 @@ class Engine:
                     for s in self._shards:
                         s.set_record_bytes(nb)
                     self._rec_bytes = nb
+            ph["drain_stage"] = time.perf_counter()
             res = self._round(gl, gt)
+            ph["gpu_round"] = time.perf_counter()
             self.last_round = res
             self.counters["aggregate_tests"] += res.aggregate_tests
             self.counters["lane_tests"] += res.lane_tests
@@ -553,14 +667,15 @@ class Engine:
             result.clauses_tested = res.clauses_tested
             result.aggregate_tests_negative = res.aggregate_tests_negative
             if res.reports:
-                eids, masks, groups, counts = self._fetch_ordered(res.reports, len(pending))
+                eids, masks, groups, counts, keep = self._fetch_ordered(res.reports, len(pending))
+                ph["order_fetch"] = time.perf_counter()
                 arena = self._arena.snapshot()  # literals as of this round (a later reduce may drop the clause)
                 cut = np.concatenate([[0], np.cumsum(counts)])
                 dests = [tid for tid, _, _, _, _ in pending]
                 for d, tid in enumerate(dests):
                     if counts[d]:
                         batches.append((tid, _ReportBatch(eids[cut[d]:cut[d + 1]], masks[cut[d]:cut[d + 1]],
-                                                          arena)))
+                                                          arena, keep)))
                 n_rep = int(cut[-1])
                 if self.config.trace:  # the trace keeps Report objects in emission order (engine.py:403-464)
                     dest_of = np.repeat(np.asarray(dests, np.int64), counts)
@@ -593,7 +708,13 @@ class Engine:
                 store=store_snapshot, reports=emitted))
 
         self.counters["rounds"] += 1
-        self.counters["busy_seconds"] += time.perf_counter() - started
+        done = time.perf_counter()
+        self.counters["busy_seconds"] += done - started
+        ph["rest"] = done
+        t, self.last_phases = started, {}
+        for k, v in ph.items():
+            self.last_phases[k] = (v - t) * 1e3
+            t = v
         return result
 
     def _round(self, gl: np.ndarray, gt: np.ndarray) -> _lib.tsg_round_result:
@@ -617,19 +738,24 @@ class Engine:
         return res
 
     def _fetch_ordered(self, n: int, n_dest: int):
-        """The round's records in delivery order (tsg_fetch_ordered)."""
+        """The round's records in delivery order (tsg_fetch_ordered), in a
+        page-locked buffer the report batches view."""
         eid_bytes = 4 if self._next_id < (1 << 31) else 8
         mask_bytes = 4 if self.config.lane_width <= 32 else 8
-        eids = np.empty(n, np.int32 if eid_bytes == 4 else np.int64)
-        masks = np.empty(n, np.uint32 if mask_bytes == 4 else np.uint64)
+        e_sec = (n * eid_bytes + 255) // 256 * 256
+        buf = self._pinned.get(e_sec + n * mask_bytes)
+        base = buf.p.value
+        eids = np.ctypeslib.as_array(C.cast(base, C.POINTER(C.c_int32 if eid_bytes == 4 else C.c_int64)), shape=(n,))
+        masks = np.ctypeslib.as_array(C.cast(base + e_sec, C.POINTER(C.c_uint32 if mask_bytes == 4 else C.c_uint64)),
+                                      shape=(n,))
         groups = np.empty(n, np.int32) if self.config.trace else None
         counts = np.zeros(max(n_dest, 1), np.int64)
         got = C.c_int64(0)
         hs = (C.c_void_p * len(self._shards))(*[s.h.value for s in self._shards])
         check(self._L.tsg_fetch_ordered(hs, len(self._shards), ptr(self._rank_of_size), self._rank_of_size.size,
-                                        ptr(eids), eid_bytes, ptr(masks), mask_bytes, ptr(groups), ptr(counts), n,
-                                        C.byref(got)))
-        return eids[:got.value], masks[:got.value], groups, counts[:n_dest]
+                                        C.c_void_p(base), eid_bytes, C.c_void_p(base + e_sec), mask_bytes,
+                                        ptr(groups), ptr(counts), n, C.byref(got)))
+        return eids[:got.value], masks[:got.value], groups, counts[:n_dest], buf
 
     def reduce_store(self) -> int:
         """engine.py:469-505; selection and compaction run on the GPU(s),
@@ -670,7 +796,7 @@ class Engine:
         out = dict(self.counters)
         out["store_size"] = len(self.store)
         with self._id_lock:
-            out["staged_pending"] = len(self._staged)
+            out["staged_pending"] = sum(len(b.lens) if isinstance(b, _Run) else len(b[0]) for b in self._staged)
         with self._queue_lock:
             out["reports_pending"] = sum(self._pending_reports.values())
             queues = list(self._squeues.values())
