@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define TSG_ABI_VERSION 1
+#define TSG_ABI_VERSION 2
 
 #define TSG_OK 0
 #define TSG_EINVAL 1    /* ValueError    (bad width / length / config)   */
@@ -52,6 +52,9 @@ typedef struct tsg_config {
 
 #define TSG_F_TIMING 1    /* record CUDA events around encode/test (fills *_ms)      */
 #define TSG_F_ALL_PAIRS 2 /* every triggering (clause, group), see tsg_set_all_pairs  */
+#define TSG_F_CHUNK_FILTER 4 /* multi-chunk rounds sweep a chunk-level aggregate first
+                                (PAPER.md:425's 32x32x32 hierarchy; env TSG_CHUNK_FILTER=0/1
+                                overrides); off by default: profiles/r02_hier_aggregate.md */
 
 /* Per-round figures, the quantities engine.py:437-467 adds to its counters. */
 typedef struct tsg_round_result {
@@ -65,6 +68,9 @@ typedef struct tsg_round_result {
     int32_t reruns;                   /* record-buffer overflow replays (0 or 1)  */
     double encode_ms;                 /* device time, TSG_F_TIMING (-1: not sampled, tsg_set_timing) */
     double test_ms;                   /* device time of the trigger kernels       */
+    int64_t chunk_positives;          /* (clause, chunk) pairs the chunk-level aggregate sweep
+                                          left for stage 1; = clauses_tested when
+                                         the round has one chunk                   */
 } tsg_round_result;
 
 /* Cumulative figures of an engine (tsg_counters): the reference's counter
@@ -187,8 +193,9 @@ int tsg_remove_clauses(tsg_engine* h, const int64_t* ids, int64_t n, int64_t* re
  *    False, like bitpack.py:108-109).  `row_pitch` is the byte distance between
  *    rows at `rows`; on_device=1 means `rows` is a device pointer.
  * 2. tsg_round: encode (K1/K2) and test (K3+K4+K5) every chunk of
- *    group_width groups against every bucket in ONE trigger launch (rounds
- *    of several chunks sweep a chunk-level aggregate first);
+ *    group_width groups against every bucket in ONE trigger launch (each
+ *    clause's literal rows are read once for all chunks; with
+ *    TSG_F_CHUNK_FILTER a chunk-level aggregate is swept first);
  *    bumps activities by activity_inc * hits (engine.py:460, fp64, no FMA).
  *    A thread's groups must be consecutive (TSG_EINVAL otherwise).
  * 3. tsg_fetch_reports: copy the round's report records out (exactly

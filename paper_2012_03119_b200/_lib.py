@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("TSG_LIB", os.path.join(HERE, "libtsg.so"))
 TSG_OK, TSG_EINVAL, TSG_ECAPACITY, TSG_ERANGE, TSG_ECUDA, TSG_ENOMEM = range(6)
 TSG_F_TIMING = 1
 TSG_F_ALL_PAIRS = 2
+TSG_F_CHUNK_FILTER = 4
 
 
 class CapacityError(ValueError):
@@ -38,7 +39,7 @@ class tsg_round_result(C.Structure):
     _fields_ = [("reports", C.c_int64), ("clauses_tested", C.c_int64), ("aggregate_tests", C.c_int64),
                 ("aggregate_tests_negative", C.c_int64), ("lane_tests", C.c_int64),
                 ("lane_triggers", C.c_int64), ("n_chunks", C.c_int32), ("reruns", C.c_int32),
-                ("encode_ms", C.c_double), ("test_ms", C.c_double)]
+                ("encode_ms", C.c_double), ("test_ms", C.c_double), ("chunk_positives", C.c_int64)]
 
 
 class tsg_counters_t(C.Structure):

@@ -201,6 +201,11 @@ struct tsg_engine {
     int64_t store_seq = 0;          // bumped by every store change (a selection must not outlive one)
 
     bool pivot = true;              // pivot-first clause layout (TSG_PIVOT=0 disables)
+    // chunk-level aggregate sweep before the chunks of a multi-chunk round
+    // (TSG_F_CHUNK_FILTER or TSG_CHUNK_FILTER=1): measured
+    // faster on synthetic per-thread windows, slower on real CDCL snapshots
+    // (profiles/r02_hier_aggregate.md), so off by default
+    bool chunk_filter = false;
     // literal polarity placed right after the pivot (+1 / -1 / 0 none).  Prior
     // before any round: +1 -- in the paper's measured value subsets
     // a variable can be True in a window more often
@@ -377,7 +382,7 @@ int do_encode(tsg_engine* h) {
         else r = wide_group(h) ? launch_encode<uint32_t, uint64_t>(h, c) : launch_encode<uint32_t, uint32_t>(h, c);
         if (r) return r;
     }
-    if (rd.n_chunks > 1) {  // chunk-level aggregate over the chunks' tables
+    if (rd.n_chunks > 1 && h->chunk_filter) {  // chunk-level aggregate over the chunks' tables
         const uint8_t* slot = reinterpret_cast<const uint8_t*>(h->tables + h->tslot * h->slot_bytes);
         auto* top = reinterpret_cast<AggEntry<uint32_t>*>(h->tables + h->tslot * h->slot_bytes + rd.top_off);
         const int64_t nv2 = (int64_t)h->V + 2;
@@ -424,7 +429,7 @@ int launch_test(tsg_engine* h, int k, int emit_only) {
     p.chunk_stride = rd.chunk_stride;
     p.lane_off = agg_bytes(h);
     p.vstride = vstride(h);
-    p.top = reinterpret_cast<const AggEntry<uint32_t>*>(p.tables + rd.top_off);
+    p.top = h->chunk_filter ? reinterpret_cast<const AggEntry<uint32_t>*>(p.tables + rd.top_off) : nullptr;
     p.n_chunks = rd.n_chunks;
     p.group_width = h->cfg.group_width;
     p.n_groups = rd.n_groups;
@@ -597,7 +602,9 @@ int tsg_create(int32_t num_vars, const tsg_config* cfg, tsg_engine** out) {
     h->cfg = *cfg;
     h->V = num_vars;
     h->all_pairs = (cfg->flags & TSG_F_ALL_PAIRS) != 0;
+    h->chunk_filter = (cfg->flags & TSG_F_CHUNK_FILTER) != 0;
     if (const char* e = getenv("TSG_PIVOT")) h->pivot = atoi(e) != 0;
+    if (const char* e = getenv("TSG_CHUNK_FILTER")) h->chunk_filter = atoi(e) != 0;
     if (const char* e = getenv("TSG_PREFER")) { h->prefer = atoi(e); h->prefer_fixed = true; }
     DevGuard g(h->dev);
     cudaDeviceProp prop;
@@ -1447,12 +1454,13 @@ int round_collect(tsg_engine* h, tsg_round_result* out) {
             CKR(dalloc(h, (void**)&R.out, R.out_cap * (int64_t)sizeof(tsg_report)));
             CK(cudaMemsetAsync(R.ctr, 0, 4 * sizeof(unsigned long long), h->st));
             CKR(run_test(h, k, 1));
-            CK(cudaMemcpyAsync(R.h_ctr, R.ctr, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
+            unsigned long long rc[4];
+            CK(cudaMemcpyAsync(rc, R.ctr, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
             CK(cudaMemsetAsync(R.ctr, 0, 4 * sizeof(unsigned long long), h->st));
             CK(cudaStreamSynchronize(h->st));
-            if ((int64_t)R.h_ctr[0] != n_rec)
+            if ((int64_t)rc[0] != n_rec)
                 return fail(TSG_ECUDA, "report replay mismatch: %lld records, %lld in the first run",
-                            (long long)R.h_ctr[0], (long long)n_rec);
+                            (long long)rc[0], (long long)n_rec);
             res.reruns = 1;
         }
         R.n_out = n_rec;
@@ -1460,6 +1468,8 @@ int round_collect(tsg_engine* h, tsg_round_result* out) {
         int64_t lanes_total = 0;
         for (int g = 0; g < rd.n_groups; ++g) lanes_total += rd.glanes[g];
         res.clauses_tested = n * rd.n_chunks;
+        // (clause, chunk) pairs past the chunk-level sweep (every pair when it does not run)
+        res.chunk_positives = rd.n_chunks > 1 && h->chunk_filter ? (int64_t)R.h_ctr[3] : res.clauses_tested;
         res.aggregate_tests = n * rd.n_groups;
         res.lane_tests = n * lanes_total;
         res.aggregate_tests_negative = res.aggregate_tests - positives;

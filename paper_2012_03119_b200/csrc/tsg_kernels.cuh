@@ -493,21 +493,26 @@ struct TestParams {
     int64_t chunk_stride;
     int64_t lane_off;                // lane table offset inside a chunk (after its aggregate table)
     int64_t vstride;                 // lane-table row length
-    const AggEntry<uint32_t>* top;   // chunk-level aggregate (n_chunks > 1)
+    const AggEntry<uint32_t>* top;   // chunk-level aggregate (n_chunks > 1; null: every chunk tested)
     int32_t n_chunks, group_width, n_groups, per_bit;  // per_bit: chunks per bit of the top table
     int32_t sentinel;                // num_vars + 1
     const GroupDesc* groups;         // [n_groups]
     double inc;
     void* out;                       // records: tsg_report, or u64 (rec8)
     unsigned long long out_cap;
-    unsigned long long* ctr;         // [0] records, [1] aggregate positives, [2] lane triggers, [5] CTAs done
+    unsigned long long* ctr;         // [0] records, [1] aggregate positives, [2] lane triggers,
+                                     // [3] (clause, chunk) pairs left positive by the chunk-level sweep, [5] CTAs done
     unsigned long long* pub;         // the round's first run: host-mapped [8] the last CTA publishes ctr to
     int32_t emit_only;               // replay after record-buffer overflow: no activity / counter side effects
     int32_t rec8;                    // 8-byte records engine_id << 37 | group << 32 | lane_mask
     int32_t all_pairs;               // every triggering (clause, group), not the first per thread
 };
 
-constexpr int PF = 8;          // literal rows prefetched per tile
+#ifndef TSG_PF
+#define TSG_PF 8
+#endif
+constexpr int PF = TSG_PF;     // literal rows prefetched per tile (4..8)
+static_assert(PF >= 4 && PF <= 8, "PF");
 constexpr int TEST_THREADS = 256;
 #ifndef TSG_RECBUF  // 128: measured best (64: 0.277 ms, 128: 0.265 ms at C3)
 #define TSG_RECBUF 128
@@ -593,11 +598,13 @@ __device__ __forceinline__ W sweep(const AggEntry<W>* agg, const ROWS& r, const 
 
 // one batch of stage-2 literals (lane words for literals h..h+3)
 template <class LW, class ROWS>
-__device__ __forceinline__ void lane_batch(const LaneEntry<LW>* lt, const ROWS& r, int h, int size, LW& lf, LW& lo) {
+__device__ __forceinline__ void lane_batch(const LaneEntry<LW>* lt, const ROWS& r, const int32_t* lp, int h, int size,
+                                           LW& lf, LW& lo) {
     LaneEntry<LW> e[4];
     int32_t l[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) l[u] = r[h + u];
+    for (int u = 0; u < 4; ++u)  // rows past the prefetched ones from memory (L1)
+        l[u] = h + u < PF ? r[h + u] : (h + u < size ? ld_lit_tail(lp + (h + u) * STRIDE) : 0);
 #pragma unroll
     for (int u = 0; u < 4; ++u)
         if (h + u < size) e[u] = ld_lane(lt + lit_var(l[u]));
@@ -611,9 +618,9 @@ __device__ __forceinline__ void lane_batch(const LaneEntry<LW>* lt, const ROWS& 
 template <class LW, class ROWS>
 __device__ __forceinline__ LW lane_test(const LaneEntry<LW>* lt, const ROWS& r, const int32_t* lp, int size) {
     LW lf = ~LW(0), lo = LW(0);
-    lane_batch<LW>(lt, r, 0, size, lf, lo);
-    if (size > 4 && (lf | lo) != LW(0)) lane_batch<LW>(lt, r, 4, size, lf, lo);
-    for (int j = PF; j < size && (lf | lo) != LW(0); ++j) {
+    lane_batch<LW>(lt, r, lp, 0, size, lf, lo);
+    if (size > 4 && (lf | lo) != LW(0)) lane_batch<LW>(lt, r, lp, 4, size, lf, lo);
+    for (int j = 8; j < size && (lf | lo) != LW(0); ++j) {
         const int32_t l = ld_lit_tail(lp + j * STRIDE);
         const LaneEntry<LW> e = ld_lane(lt + lit_var(l));
         step<LW>(lf, lo, l < 0 ? (e.s & e.t) : (e.s & ~e.t), ~e.s);
@@ -696,12 +703,12 @@ __global__ void __launch_bounds__(TEST_THREADS, (sizeof(LW) == 8 || sizeof(GW) =
 k_test(const __grid_constant__ TestParams<LW, GW> p) {
     constexpr int WARPS = TEST_THREADS / 32;
     extern __shared__ __align__(16) unsigned char s_rec[];  // [WARPS][RECBUF] records (test_smem_bytes)
-    __shared__ unsigned int s_acc[2][WARPS];
+    __shared__ unsigned int s_acc[3][WARPS];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int nwarps = (int)(((int64_t)gridDim.x * TEST_THREADS) >> 5);
     RecBuf rb{s_rec + (size_t)warp * RECBUF * (p.rec8 ? 8 : 16), p.rec8};
-    unsigned int pos_acc = 0, trig_acc = 0;
+    unsigned int pos_acc = 0, trig_acc = 0, top_acc = 0;
     const uint32_t top_mask = MULTI ? width_mask<uint32_t>((p.n_chunks + p.per_bit - 1) / p.per_bit) : 1u;
     // single-chunk rounds (<= 64 groups): the group table in shared memory
     const GroupDesc* groups = p.groups;
@@ -787,7 +794,8 @@ k_test(const __grid_constant__ TestParams<LW, GW> p) {
         };
         if constexpr (MULTI) {
             // chunk-level sweep first: only the chunks it leaves positive get a stage 1
-            const uint32_t cw = active ? sweep<uint32_t>(p.top, cur, lp, size, p.sentinel) & top_mask : 0u;
+            const uint32_t cw = !active ? 0u : p.top ? sweep<uint32_t>(p.top, cur, lp, size, p.sentinel) & top_mask : top_mask;
+            top_acc += __popc(cw);
             uint32_t wcw = __reduce_or_sync(0xffffffffu, cw);
             while (wcw) {
                 const int b = __ffs(wcw) - 1;
@@ -811,14 +819,16 @@ k_test(const __grid_constant__ TestParams<LW, GW> p) {
     // counters: warp reduce, block reduce, one atomic per block
     pos_acc = __reduce_add_sync(0xffffffffu, pos_acc);
     trig_acc = __reduce_add_sync(0xffffffffu, trig_acc);
-    if (lane == 0) { s_acc[0][warp] = pos_acc; s_acc[1][warp] = trig_acc; }
+    top_acc = __reduce_add_sync(0xffffffffu, top_acc);
+    if (lane == 0) { s_acc[0][warp] = pos_acc; s_acc[1][warp] = trig_acc; s_acc[2][warp] = top_acc; }
     __syncthreads();
     if (threadIdx.x == 0) {
-        unsigned long long a = 0, t = 0;
-        for (int i = 0; i < WARPS; ++i) { a += s_acc[0][i]; t += s_acc[1][i]; }
+        unsigned long long a = 0, t = 0, c = 0;
+        for (int i = 0; i < WARPS; ++i) { a += s_acc[0][i]; t += s_acc[1][i]; c += s_acc[2][i]; }
         if (!p.emit_only) {
             if (a) atomicAdd(p.ctr + 1, a);
             if (t) atomicAdd(p.ctr + 2, t);
+            if (c) atomicAdd(p.ctr + 3, c);
         }
         // the launch's last CTA hands the counters to the host (the round's
         // first run) and re-zeroes them, or just re-zeroes the CTA count

@@ -69,6 +69,7 @@ class EngineConfig:
     report_capacity: int = 0
     timing: bool = False
     devices: Optional[Sequence[int]] = None  # clause shards, one engine per entry (default: [device])
+    chunk_filter: bool = False  # multi-chunk rounds: chunk-level aggregate sweep first
 
     def __post_init__(self):
         if self.max_clauses < 1:
@@ -372,7 +373,8 @@ class Engine:
         self._L = _lib.load()
         devices = list(self.config.devices) if self.config.devices else [self.config.device]
         self._shards = [NativeEngine(num_vars, self.config.lane_width, self.config.group_width, device=d,
-                                     timing=self.config.timing, report_capacity=self.config.report_capacity)
+                                     timing=self.config.timing, report_capacity=self.config.report_capacity,
+                                     chunk_filter=self.config.chunk_filter)
                         for d in devices]
         self._h = self._shards[0].h  # the first shard: staging, encode, record ordering
         w = C.c_int64(0)

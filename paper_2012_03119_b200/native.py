@@ -52,11 +52,12 @@ def pack_rows(rows: np.ndarray, num_vars: int, out: Optional[np.ndarray] = None,
 
 class NativeEngine:
     def __init__(self, num_vars: int, lane_width: int = 32, group_width: int = 32, device: int = 0,
-                 timing: bool = False, report_capacity: int = 0):
+                 timing: bool = False, report_capacity: int = 0, chunk_filter: bool = False):
         self.L = _lib.load()
         self.num_vars = num_vars
         self.lane_width, self.group_width = lane_width, group_width
-        cfg = _lib.tsg_config(lane_width, group_width, device, _lib.TSG_F_TIMING if timing else 0,
+        cfg = _lib.tsg_config(lane_width, group_width, device,
+                              (_lib.TSG_F_TIMING if timing else 0) | (_lib.TSG_F_CHUNK_FILTER if chunk_filter else 0),
                               report_capacity)
         h = C.c_void_p()
         check(self.L.tsg_create(num_vars, C.byref(cfg), C.byref(h)))

@@ -25,7 +25,7 @@ def test_library_loads_and_exports_every_symbol():
     L = _lib.load()
     for name in header_symbols():
         assert hasattr(L, name), name
-    assert L.tsg_abi_version() == 1
+    assert L.tsg_abi_version() == 2
 
 
 def test_no_cpu_fallback_without_device():

@@ -136,7 +136,7 @@ def test_literal_out_of_range_raises(P):
 # ---- config-scale parity vs the CPU oracle ---------------------------------
 
 def run_both(P, cfg_name=None, n=None, threads=None, lanes=None, nv=None, lane_width=32, group_width=32,
-             seed=0, inc=1.0, rounds=1, size_lo=2, size_hi=30, all_pairs=False, packed=False):
+             seed=0, inc=1.0, rounds=1, size_lo=2, size_hi=30, all_pairs=False, packed=False, chunk_filter=False):
     """The device engine and the oracle on the same store and snapshots.
     all_pairs: the device emits every triggering (clause, group) -- compared
     with the oracle run with one thread per group, whose one-report-per-
@@ -152,7 +152,7 @@ def run_both(P, cfg_name=None, n=None, threads=None, lanes=None, nv=None, lane_w
     buckets = W.clause_buckets(n, nv, rng, size_lo, size_hi)
     flat, offs, ids = W.flatten(buckets)
     org = (ids % 7).astype(np.int32)
-    dev = NativeEngine(nv, lane_width, group_width, report_capacity=1 << 20)
+    dev = NativeEngine(nv, lane_width, group_width, report_capacity=1 << 20, chunk_filter=chunk_filter)
     if all_pairs:
         dev.set_all_pairs(True)
     dev.add_clauses(flat, offs, ids, org, 1.0)
@@ -209,19 +209,20 @@ def test_c2_full_size_parity(P):
 # aggregate path at full size
 @pytest.mark.parametrize("cfg", ["C1", "C2", "C3"])
 def test_pair_set_parity_full_size(P, cfg):
-    res = run_both(P, cfg, lane_width=16, all_pairs=True, packed=True)
+    res = run_both(P, cfg, lane_width=16, all_pairs=True, packed=True, chunk_filter=cfg == "C3")
     assert res.reports > 0 and res.n_chunks == (2 if cfg == "C3" else 1)
 
 
 @pytest.mark.parametrize("lw,gw,threads,lanes", [(32, 32, 3, 40), (64, 64, 2, 64), (64, 8, 5, 70),
                                                  (7, 3, 4, 20), (1, 64, 3, 30), (32, 16, 40, 32),
                                                  (1, 1, 3, 40), (4, 2, 33, 20)])
-@pytest.mark.parametrize("all_pairs", [False, True])
-def test_widths_and_multichunk_parity(P, lw, gw, threads, lanes, all_pairs):
+@pytest.mark.parametrize("all_pairs,chunk_filter", [(False, False), (True, False), (False, True), (True, True)])
+def test_widths_and_multichunk_parity(P, lw, gw, threads, lanes, all_pairs, chunk_filter):
     # every word-width variant of the trigger kernel; (1, 1, 3, 40): 120
     # chunks of one group, i.e. four chunks per bit of the chunk-level table
     run_both(P, n=20_000, threads=threads, lanes=lanes, nv=300, lane_width=lw, group_width=gw,
-             seed=lw * 100 + gw, rounds=2, size_lo=0, size_hi=12, all_pairs=all_pairs and lanes > lw)
+             seed=lw * 100 + gw, rounds=2, size_lo=0, size_hi=12, all_pairs=all_pairs and lanes > lw,
+             chunk_filter=chunk_filter)
 
 
 def test_c3_shape_parity(P):

@@ -33,8 +33,9 @@ def X():
     return X
 
 
-@pytest.mark.parametrize("name,devices", [("w32", None), ("w8x2", None), ("w8x2", [0, 0])])
-def test_replay_reference_solver_rounds(name, devices):
+@pytest.mark.parametrize("name,devices,chunk_filter", [("w32", None, False), ("w8x2", None, False),
+                                                       ("w8x2", None, True), ("w8x2", [0, 0], True)])
+def test_replay_reference_solver_rounds(name, devices, chunk_filter):
     # every recorded round rebuilt on the GPU Engine through the reference API:
     # the same clauses under the same engine ids (inserted in id order, so the
     # size buckets are created in the reference's order), the round's
@@ -49,7 +50,8 @@ def test_replay_reference_solver_rounds(name, devices):
     n_reports = 0
     for k in range(int(fx["rounds"])):
         clauses, live, snaps, reps, result = c5_round(fx, k)
-        eng = P.Engine(nv, th, P.EngineConfig(lane_width=lw, group_width=gw, devices=devices))
+        eng = P.Engine(nv, th, P.EngineConfig(lane_width=lw, group_width=gw, devices=devices,
+                                              chunk_filter=chunk_filter))
         for lits in clauses:
             eng.add_clause(lits, origin=0)
         eng.run_round()  # integrate (no snapshots: no activity or counter effects)
