@@ -512,7 +512,7 @@ struct TestParams {
 #define TSG_PF 8
 #endif
 constexpr int PF = TSG_PF;     // literal rows prefetched per tile (4..8)
-static_assert(PF >= 4 && PF <= 8, "PF");
+static_assert(PF >= 4 && PF <= 8 && PF % 2 == 0, "PF: 4, 6 or 8 (stage 1 takes rows 4.. in pairs)");
 constexpr int TEST_THREADS = 256;
 #ifndef TSG_RECBUF  // 128: measured best (64: 0.277 ms, 128: 0.265 ms at C3)
 #define TSG_RECBUF 128
@@ -730,89 +730,97 @@ k_test(const __grid_constant__ TestParams<LW, GW> p) {
         bi = lo;
         nt0 = bi + 1 < p.nb ? (int)p.buckets[bi + 1].tile0 : INT_MAX;
     }
+    // one tile: test it with its rows in `cur` while the next tile's rows
+    // load into `nxt` (unrolling the loop by two over alternating buffers, or
+    // an L2 prefetch two tiles ahead, measured no faster:
+    // profiles/r02_k_test_variants.md)
+    auto tile_step = [&](const RegRows& cur, RegRows& nxt) -> bool {
+            const BucketDesc* bd = p.buckets + bi;
+            const int ntile = tile + nwarps;
+            // software pipeline: the next tile's first rows are in flight while this one is tested
+            if (ntile < p.n_tiles) {
+                seek_bucket(p.buckets, p.nb, ntile, bi, nt0);
+                load_rows(p.buckets + bi, ntile, lane, p.sentinel, nxt.r);
+            }
+            const int size = bd->size;
+            const bool active = lane_active(bd, tile, lane);
+            const int32_t* lp = lane_lits(bd, tile, lane);
+            // stage-2 state of this lane's clause, across the chunks of the round
+            bool loaded = false, touched = false;
+            double act = 0.0;
+            uint64_t key_hi = 0;
+            int last_tid = INT_MIN;
+            // stage 1 + stage 2 of chunk c for the lanes with `mine` (warp-uniform call)
+            auto test_chunk = [&](const uint8_t* tab, int g0, int G, bool mine) {
+                // ---- stage 1: aggregate filter (engine.py:238-254) -----------------
+                GW left = GW(0);
+                if (mine)
+                    left = sweep<GW>(reinterpret_cast<const AggEntry<GW>*>(tab), cur, lp, size, p.sentinel) &
+                           width_mask<GW>(G);
+                pos_acc += __popcll((unsigned long long)left);
+                if (left != GW(0) && !loaded) {  // stage-2 entry: id and activity of the clause
+                    loaded = true;
+                    const int slot = (tile - (int)bd->tile0) * STRIDE + lane;
+                    key_hi = (uint64_t)bd->ids[slot] << (p.rec8 ? 37 : 16);
+                    if (!p.emit_only) act = bd->acts[slot];
+                }
+                const LaneEntry<LW>* lanes = reinterpret_cast<const LaneEntry<LW>*>(tab + p.lane_off);
+                // ---- stage 2: exact lane test per positive group --------------------
+                while (__any_sync(0xffffffffu, left != GW(0))) {
+                    bool has = false;
+                    ulonglong2 rec = make_ulonglong2(0, 0);
+                    if (left != GW(0)) {
+                        const int g = __ffsll((long long)(unsigned long long)left) - 1;
+                        left &= left - GW(1);
+                        const LW mask = lane_test<LW>(lanes + (int64_t)g * p.vstride, cur, lp, size) &
+                                        (LW)groups[g0 + g].lane_mask;
+                        if (mask != LW(0)) {
+                            const int hits = __popcll((unsigned long long)mask);
+                            trig_acc += hits;
+                            if (!p.emit_only) {
+                                act = __dadd_rn(act, __dmul_rn(p.inc, (double)hits));
+                                touched = true;
+                            }
+                            const int tid = groups[g0 + g].tid;
+                            if (p.all_pairs || tid != last_tid) {  // first triggering group of its thread
+                                last_tid = tid;
+                                has = true;
+                                const uint64_t grp = (uint64_t)(g0 + g);
+                                rec = p.rec8 ? make_ulonglong2(key_hi | (grp << 32) | (uint32_t)mask, 0)
+                                             : make_ulonglong2(key_hi | grp, (unsigned long long)mask);
+                            }
+                        }
+                    }
+                    rb.append(has, rec, p.out, p.out_cap, p.ctr, lane);
+                }
+            };
+            if constexpr (MULTI) {
+                // chunk-level sweep first: only the chunks it leaves positive get a stage 1
+                const uint32_t cw = !active ? 0u : p.top ? sweep<uint32_t>(p.top, cur, lp, size, p.sentinel) & top_mask : top_mask;
+                top_acc += __popc(cw);
+                uint32_t wcw = __reduce_or_sync(0xffffffffu, cw);
+                while (wcw) {
+                    const int b = __ffs(wcw) - 1;
+                    wcw &= wcw - 1u;
+                    const bool mine = (cw >> b) & 1u;
+                    const int c1 = min((b + 1) * p.per_bit, p.n_chunks);
+                    for (int c = b * p.per_bit; c < c1; ++c) {
+                        const int g0 = c * p.group_width;
+                        test_chunk(p.tables + c * p.chunk_stride, g0, min(p.group_width, p.n_groups - g0), mine);
+                    }
+                }
+            } else {
+                test_chunk(p.tables, 0, p.n_groups, active);
+            }
+            if (touched) bd->acts[(tile - (int)bd->tile0) * STRIDE + lane] = act;
+            tile = ntile;
+            return tile < p.n_tiles;
+    };
     RegRows cur, nxt;
     if (tile < p.n_tiles) load_rows(p.buckets + bi, tile, lane, p.sentinel, cur.r);
     while (tile < p.n_tiles) {
-        const BucketDesc* bd = p.buckets + bi;
-        const int ntile = tile + nwarps;
-        // software pipeline: the next tile's first rows are in flight while this one is tested
-        if (ntile < p.n_tiles) {
-            seek_bucket(p.buckets, p.nb, ntile, bi, nt0);
-            load_rows(p.buckets + bi, ntile, lane, p.sentinel, nxt.r);
-        }
-        const int size = bd->size;
-        const bool active = lane_active(bd, tile, lane);
-        const int32_t* lp = lane_lits(bd, tile, lane);
-        // stage-2 state of this lane's clause, across the chunks of the round
-        bool loaded = false, touched = false;
-        double act = 0.0;
-        uint64_t key_hi = 0;
-        int last_tid = INT_MIN;
-        // stage 1 + stage 2 of chunk c for the lanes with `mine` (warp-uniform call)
-        auto test_chunk = [&](const uint8_t* tab, int g0, int G, bool mine) {
-            // ---- stage 1: aggregate filter (engine.py:238-254) -----------------
-            GW left = GW(0);
-            if (mine)
-                left = sweep<GW>(reinterpret_cast<const AggEntry<GW>*>(tab), cur, lp, size, p.sentinel) &
-                       width_mask<GW>(G);
-            pos_acc += __popcll((unsigned long long)left);
-            if (left != GW(0) && !loaded) {  // stage-2 entry: id and activity of the clause
-                loaded = true;
-                const int slot = (tile - (int)bd->tile0) * STRIDE + lane;
-                key_hi = (uint64_t)bd->ids[slot] << (p.rec8 ? 37 : 16);
-                if (!p.emit_only) act = bd->acts[slot];
-            }
-            const LaneEntry<LW>* lanes = reinterpret_cast<const LaneEntry<LW>*>(tab + p.lane_off);
-            // ---- stage 2: exact lane test per positive group --------------------
-            while (__any_sync(0xffffffffu, left != GW(0))) {
-                bool has = false;
-                ulonglong2 rec = make_ulonglong2(0, 0);
-                if (left != GW(0)) {
-                    const int g = __ffsll((long long)(unsigned long long)left) - 1;
-                    left &= left - GW(1);
-                    const LW mask = lane_test<LW>(lanes + (int64_t)g * p.vstride, cur, lp, size) &
-                                    (LW)groups[g0 + g].lane_mask;
-                    if (mask != LW(0)) {
-                        const int hits = __popcll((unsigned long long)mask);
-                        trig_acc += hits;
-                        if (!p.emit_only) {
-                            act = __dadd_rn(act, __dmul_rn(p.inc, (double)hits));
-                            touched = true;
-                        }
-                        const int tid = groups[g0 + g].tid;
-                        if (p.all_pairs || tid != last_tid) {  // first triggering group of its thread
-                            last_tid = tid;
-                            has = true;
-                            const uint64_t grp = (uint64_t)(g0 + g);
-                            rec = p.rec8 ? make_ulonglong2(key_hi | (grp << 32) | (uint32_t)mask, 0)
-                                         : make_ulonglong2(key_hi | grp, (unsigned long long)mask);
-                        }
-                    }
-                }
-                rb.append(has, rec, p.out, p.out_cap, p.ctr, lane);
-            }
-        };
-        if constexpr (MULTI) {
-            // chunk-level sweep first: only the chunks it leaves positive get a stage 1
-            const uint32_t cw = !active ? 0u : p.top ? sweep<uint32_t>(p.top, cur, lp, size, p.sentinel) & top_mask : top_mask;
-            top_acc += __popc(cw);
-            uint32_t wcw = __reduce_or_sync(0xffffffffu, cw);
-            while (wcw) {
-                const int b = __ffs(wcw) - 1;
-                wcw &= wcw - 1u;
-                const bool mine = (cw >> b) & 1u;
-                const int c1 = min((b + 1) * p.per_bit, p.n_chunks);
-                for (int c = b * p.per_bit; c < c1; ++c) {
-                    const int g0 = c * p.group_width;
-                    test_chunk(p.tables + c * p.chunk_stride, g0, min(p.group_width, p.n_groups - g0), mine);
-                }
-            }
-        } else {
-            test_chunk(p.tables, 0, p.n_groups, active);
-        }
-        if (touched) bd->acts[(tile - (int)bd->tile0) * STRIDE + lane] = act;
-        if (ntile < p.n_tiles) cur = nxt;
-        tile = ntile;
+        if (!tile_step(cur, nxt)) break;
+        cur = nxt;
     }
     if (rb.n) rb.flush(p.out, p.out_cap, p.ctr, lane);
 
