@@ -721,7 +721,7 @@ def main():
                 roofline["l2_gather"] = {
                     "sectors_per_launch": sectors, "achieved_sectors_per_clk_per_sm": per_clk,
                     "ceiling_sectors_per_clk_per_sm": L2_GATHER_CEILING, "frac": per_clk / L2_GATHER_CEILING,
-                    "ceiling_source": "profiles/r01_gather_modes.md (tools/microbench/gather_modes.cu): random "
+                    "ceiling_source": "profiles/r02_gather_modes.md (tools/microbench/gather_modes.cu): random "
                                       "16-byte gathers from an L2-resident table as divergent LDGs, B200"}
         except Exception:
             pass
