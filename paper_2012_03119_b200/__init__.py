@@ -6,9 +6,11 @@ and the bit-parallel library (pack_assignments, build_aggregate_batch,
 assignment_trigger, aggregate_trigger, multi_trigger).  Compute runs in the
 hand-written sm_100a kernels of libtsg.so behind the C ABI in include/tsg.h.
 """
-from .core import FALSE, TRUE, UNDEF
 from ._lib import CapacityError, TsgError
 from .bitpack import (
+    FALSE,
+    TRUE,
+    UNDEF,
     AggregateAssignment,
     AggregateBatch,
     PackedAssignmentBatch,

@@ -18,10 +18,14 @@ import numpy as np
 
 from . import _lib
 from ._lib import CapacityError, check, ptr
-from .core import FALSE, TRUE, UNDEF
 
 WORD_BITS = 64
 _U64_ONE = np.uint64(1)
+
+# value conventions of the reference (core.py:20-22): a variable is True,
+# False or Undef; a literal is +v / -v; assignments are indexed by variable
+# with slot 0 unused
+TRUE, FALSE, UNDEF = 1, -1, 0
 
 #: CUDA device used by the library-level kernels.
 DEVICE = 0
@@ -64,10 +68,12 @@ class PackedAssignmentBatch:
     is_set: np.ndarray
 
     def literal_words(self, lit: int) -> tuple:
-        v = lit if lit > 0 else -lit
-        t = int(self.is_true[v])
-        s = int(self.is_set[v])
-        return s, (s & ~t) if lit > 0 else (s & t)
+        """(lanes where the literal's variable is set, lanes where the literal
+        is False): a set lane is False for +v where v is not True, for -v
+        where it is."""
+        t, s = int(self.is_true[abs(lit)]), int(self.is_set[abs(lit)])
+        false_lanes = s & (t if lit < 0 else ~t)
+        return s, false_lanes
 
     def lane_assignment(self, lane: int) -> list:
         if not 0 <= lane < self.lane_count:
@@ -133,14 +139,9 @@ class AggregateAssignment:
         return cls(batch.num_vars, agg.can_be_true != 0, agg.can_be_false != 0, agg.can_be_undef != 0)
 
     def values_at(self, v: int) -> frozenset:
-        out = set()
-        if self.has_true[v]:
-            out.add(TRUE)
-        if self.has_false[v]:
-            out.add(FALSE)
-        if self.has_undef[v]:
-            out.add(UNDEF)
-        return frozenset(out)
+        """The values variable v takes somewhere in the group."""
+        return frozenset(val for val, has in ((TRUE, self.has_true), (FALSE, self.has_false),
+                                              (UNDEF, self.has_undef)) if has[v])
 
 
 @dataclass(frozen=True)
@@ -207,18 +208,15 @@ def aggregate_trigger(agg: AggregateBatch, clause: Sequence[int]) -> int:
 
 def iter_set_bits(word: int) -> Iterator[int]:
     """Indices of the set bits of a word, ascending (bitpack.py:274-279)."""
-    while word:
-        low = word & -word
-        yield low.bit_length() - 1
-        word ^= low
+    return (i for i in range(int(word).bit_length()) if (word >> i) & 1)
 
 
 def multi_trigger(agg: AggregateBatch, per_group_batches: Sequence[PackedAssignmentBatch],
                   clause: Sequence[int], report: Callable[[int, int], None]) -> None:
     """bitpack.py:282-300: two-stage test; report(group, lane_mask) for exactly
     the groups with a genuinely triggering lane."""
-    word = aggregate_trigger(agg, clause)
-    for i in iter_set_bits(word):
-        mask = assignment_trigger(per_group_batches[i], clause)
-        if mask:
+    groups = list(iter_set_bits(aggregate_trigger(agg, clause)))  # stage 1 on the GPU
+    masks = [assignment_trigger(per_group_batches[i], clause) for i in groups]  # stage 2 per positive group
+    for i, mask in zip(groups, masks):
+        if mask:  # a positive aggregate without a triggering lane is not reported
             report(i, mask)
