@@ -330,7 +330,7 @@ def _tables(eng):
     return torch.as_tensor(_CAI(), device="cuda").cpu().numpy().copy()
 
 
-def _defined_tables(raw, nv, lw, gw, gl):
+def _defined_tables(raw, nv, lw, gw, gl, chunk_filter=False):
     """The written entries of the round tables (tsg_engine.cu layout: per chunk
     agg[V+2] then lane[G][vstride], each region 256-byte aligned)."""
     def up(x, m):
@@ -347,7 +347,7 @@ def _defined_tables(raw, nv, lw, gw, gl):
         off += up((nv + 2) * aeb, 256)
         lane = raw[off:off + vstride * G * leb].reshape(G, vstride, leb)[:, :nv + 2]
         parts.append(lane.reshape(-1))
-    if len(gl) > gw:  # the chunk-level aggregate after the chunks: t, f, u of every variable
+    if chunk_filter and len(gl) > gw:  # the chunk-level aggregate after the chunks: t, f, u of every variable
         off = (len(gl) + gw - 1) // gw * stride
         parts.append(raw[off:off + (nv + 2) * 16].reshape(nv + 2, 16)[:, :12])
     return np.concatenate([x.reshape(-1) for x in parts])
@@ -355,7 +355,8 @@ def _defined_tables(raw, nv, lw, gw, gl):
 
 @pytest.mark.parametrize("lw,gw,threads,lanes,nv", [(32, 32, 3, 40, 1000), (64, 64, 2, 100, 333),
                                                     (64, 8, 5, 70, 4095), (7, 3, 4, 20, 31), (32, 32, 32, 32, 20_000)])
-def test_packed_rows_encode_identically(P, lw, gw, threads, lanes, nv):
+@pytest.mark.parametrize("chunk_filter", [False, True])
+def test_packed_rows_encode_identically(P, lw, gw, threads, lanes, nv, chunk_filter):
     # snapshot ingress in 2-bit packed rows: the packed encoder must build
     # byte-identical lane/aggregate tables, and the round identical results
     from paper_2012_03119_b200 import workload as W
@@ -369,7 +370,7 @@ def test_packed_rows_encode_identically(P, lw, gw, threads, lanes, nv):
     gl, gt = W.groups_for(threads, lanes, lw)
     out = []
     for packed in (False, True):
-        e = NativeEngine(nv, lw, gw)
+        e = NativeEngine(nv, lw, gw, chunk_filter=chunk_filter)
         e.add_clauses(flat, offs, ids)
         if packed:
             e.stage_packed(pack_rows(snaps, nv, threads=2))
@@ -377,7 +378,7 @@ def test_packed_rows_encode_identically(P, lw, gw, threads, lanes, nv):
             e.stage(snaps)
         e.prepare(gl, gt)
         e.encode()
-        tab = _defined_tables(_tables(e), nv, lw, gw, gl)
+        tab = _defined_tables(_tables(e), nv, lw, gw, gl, chunk_filter)
         res = e.test(1.0)
         recs = np.sort(e.fetch(res.reports), order=["engine_id", "group"])
         out.append((tab, res.lane_triggers, res.aggregate_tests_negative, recs))
