@@ -82,3 +82,71 @@ def test_randomised_parity_vs_oracle():
         cases += 1
     print(f"parity ok: {cases} stores, {rounds_done} rounds, seed {seed}")
     assert cases > 0
+
+
+def test_randomised_engine_streams_vs_oracle_engine():
+    """The drop-in Engine under random operation streams (adds, explicit
+    deletes, reduces, snapshot bursts that overflow queues, wrong-free
+    rounds) against the oracle's restatement of the reference engine, with
+    random word widths, 1-3 clause shards and the chunk filter on or off:
+    every round's result, every thread's drained reports in order, the
+    counters and the store (fp64 activities bit-exact)."""
+    from gpu_util import require_device
+    require_device()
+    import paper_2012_03119_b200 as P
+    secs = float(os.environ.get("TSG_STRESS_SECONDS", "20"))
+    seed = int(os.environ.get("TSG_STRESS_SEED", "7"))
+    rng = np.random.default_rng(seed + 1)
+    t_end = time.time() + secs
+    streams = rounds_done = 0
+    while time.time() < t_end:
+        nv = int(rng.choice([20, 200, 3000]))
+        threads = int(rng.integers(1, 7))
+        lw = int(rng.choice([1, 4, 16, 32, 64]))
+        gw = int(rng.choice([1, 3, 8, 32, 64]))
+        cap = int(rng.integers(1, 3 * lw + 2))
+        max_clauses = int(rng.integers(50, 4000))
+        devices = [None, [0, 0], [0, 0, 0]][int(rng.integers(0, 3))]
+        chunk_filter = bool(rng.random() < 0.5)
+        cfg = dict(max_clauses=max_clauses, lane_width=lw, group_width=gw, assignment_queue_capacity=cap)
+        eng = P.Engine(nv, threads, P.EngineConfig(**cfg, devices=devices, chunk_filter=chunk_filter))
+        ora = O.OracleEngine(nv, threads, **cfg)
+        hi = min(nv, 14)
+        for r in range(int(rng.integers(2, 8))):
+            for _ in range(int(rng.integers(0, max_clauses // 2 + 2))):
+                s = int(rng.integers(0, hi + 1))
+                vs = rng.choice(nv, s, replace=False) + 1
+                lits = tuple(int(v) * (1 if b else -1) for v, b in zip(vs, rng.integers(0, 2, s)))
+                o = int(rng.integers(0, threads))
+                assert eng.add_clause(lits, o) == ora.add_clause(lits, o)
+            if rng.random() < 0.3:
+                ids = rng.integers(0, max(1, ora.next_id), int(rng.integers(1, 200)))
+                assert eng.remove_clauses(ids) == ora.remove_clauses(ids)
+            for t in range(threads):
+                for _ in range(int(rng.integers(0, cap + 3))):
+                    v = rng.choice(np.array([1, -1, 0], np.int8), size=nv + 1, p=[0.3, 0.3, 0.4])
+                    v[0] = 0
+                    assert eng.submit_assignment(P.AssignmentSnapshot(t, v, 0)) == ora.submit_assignment(t, v, 0)
+            if rng.random() < 0.2:
+                assert eng.reduce_store() == ora.reduce_store()
+            res, ores = eng.run_round(), ora.run_round()
+            ctx = (streams, r, nv, threads, lw, gw, cap, max_clauses, devices, chunk_filter)
+            assert [res.reports_emitted, res.clauses_tested, res.assignments_consumed,
+                    res.aggregate_tests_negative] == [ores["reports_emitted"], ores["clauses_tested"],
+                                                      ores["assignments_consumed"],
+                                                      ores["aggregate_tests_negative"]], ctx
+            for t in range(threads):
+                got = [(x.destination, x.lits, x.engine_id, x.lane_mask) for x in eng.drain_reports(t)]
+                want = [(x.destination, x.lits, x.engine_id, x.lane_mask) for x in ora.drain_reports(t)]
+                assert got == want, ctx
+            c = eng.raw_counters()
+            for k, v in ora.counters.items():
+                assert c[k] == v, (ctx, k)
+            rounds_done += 1
+        got = [(eid, tuple(l), o, float(a).hex()) for eid, l, o, a in eng.store.clauses()]
+        want = [(eid, l, o, float(a).hex()) for eid, l, o, a in ora.store.clauses()]
+        assert got == want, (streams, nv, threads, lw, gw, devices)
+        eng.close()
+        streams += 1
+    print(f"engine streams ok: {streams} streams, {rounds_done} rounds, seed {seed}")
+    assert streams > 0

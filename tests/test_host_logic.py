@@ -1,0 +1,49 @@
+"""Pure host logic of the product, on CPU: the strong-scaling shard split
+(workload.shard) and the Engine's append-only literal arena (Report.lits
+stay valid for a batch after later inserts grow the arena)."""
+import numpy as np
+
+
+def test_shard_split_is_a_partition_with_global_ids():
+    from paper_2012_03119_b200 import workload as W
+    b = W.clause_buckets(5000, 300, np.random.default_rng(1), 1, 9)
+    flat, offs, ids = W.flatten(b)
+    want = {int(i): tuple(flat[offs[k]:offs[k + 1]].tolist()) for k, i in enumerate(ids)}
+    for world in (1, 2, 3, 8):
+        got = {}
+        for r in range(world):
+            f, o, i = W.shard(b, world, r)
+            assert np.all(np.diff(i) > 0)  # engine ids ascend within a shard (tsg_add_clauses)
+            for k, e in enumerate(i.tolist()):
+                assert e not in got
+                got[e] = tuple(f[o[k]:o[k + 1]].tolist())
+            # every size bucket balanced across the ranks
+            sizes = np.diff(o)
+            for s, arr in b.items():
+                share = int((sizes == s).sum())
+                assert abs(share - arr.shape[0] / world) <= 1
+        assert got == want
+
+
+def test_arena_keeps_round_literals():
+    from paper_2012_03119_b200.engine import _Arena
+    a = _Arena()
+    rng = np.random.default_rng(2)
+    ref = {}
+    snaps = []
+    nxt = 0
+    for r in range(30):
+        n = int(rng.integers(1, 400))
+        lens = rng.integers(0, 12, n).astype(np.int32)
+        flat = rng.integers(-50, 50, int(lens.sum())).astype(np.int32)
+        ids = np.arange(nxt, nxt + n, dtype=np.int64)
+        nxt += n
+        a.append(ids, lens, flat)
+        o = 0
+        for i, s in zip(ids.tolist(), lens.tolist()):
+            ref[i] = tuple(flat[o:o + s].tolist())
+            o += s
+        snaps.append((a.snapshot(), nxt))
+    for snap, upto in snaps:  # every round's arena still answers for the ids it knew
+        for i in rng.integers(0, upto, 50).tolist():
+            assert snap.lits_of(i) == ref[i]
