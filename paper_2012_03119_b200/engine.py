@@ -390,7 +390,7 @@ class Engine:
 
         self._id_lock = threading.Lock()
         self._next_id = 0
-        self._staged: List[Tuple[int, tuple, int]] = []
+        self._staged: list = []  # _Run (add_clause) and array batches (add_clauses), in id order
 
         self._queue_lock = threading.Lock()  # report queues, counters, the set of snapshot queues
         self._squeues: Dict[int, _SnapQueue] = {}
@@ -461,7 +461,7 @@ class Engine:
         (bitpack.py:92-103)."""
         q = self._queue(snapshot.thread_id)
         with q.lock:
-            if q.n >= q.cap:
+            if q.n + len(q.bad) >= q.cap:  # (a rejected snapshot still occupies its queue slot)
                 ok = False
             else:
                 vals = np.ascontiguousarray(np.asarray(snapshot.values, dtype=np.int8))
