@@ -260,9 +260,9 @@ class ShardedRound:
         self.eng.prepare(group_lanes, group_tid)
         self.eng.stage_packed(packed_rows)
         self.eng.encode_groups(gb, ge, self.rank == 0)
-        self.eng.sync()
+        # the collectives run on the engine's own stream: ordered after the
+        # encode and before the test without a host sync
         combine_tables(self.dist, self.eng, n_groups, self.stream)
-        self.stream.synchronize()
         res = self.eng.test(activity_inc)
         return res, gather_records(self.dist, self.eng.fetch(res.reports), 0)
 
@@ -274,8 +274,7 @@ class ShardedRound:
             if rows is not None:
                 self.eng.stage(rows)
             self.eng.encode()
-        self.eng.sync()
-        broadcast_tables(self.dist, self.eng, 0, self.stream)
+        broadcast_tables(self.dist, self.eng, 0, self.stream)  # on the engine's stream, after the encode
         res = self.eng.test(activity_inc)
         return res, gather_records(self.dist, self.eng.fetch(res.reports), 0)
 
