@@ -765,31 +765,39 @@ k_test(const __grid_constant__ TestParams<LW, GW> p) {
                     if (!p.emit_only) act = bd->acts[slot];
                 }
                 const LaneEntry<LW>* lanes = reinterpret_cast<const LaneEntry<LW>*>(tab + p.lane_off);
+                // one triggering group's effects on this lane's clause, in group
+                // order: hits, the fp64 bump (engine.py:460), the first
+                // triggering group of each thread (or every one) as a record
+                auto settle = [&](int g, LW mask, bool& has, ulonglong2& rec) {
+                    if (mask == LW(0)) return;
+                    const int hits = __popcll((unsigned long long)mask);
+                    trig_acc += hits;
+                    if (!p.emit_only) {
+                        act = __dadd_rn(act, __dmul_rn(p.inc, (double)hits));
+                        touched = true;
+                    }
+                    const int tid = groups[g0 + g].tid;
+                    if (p.all_pairs || tid != last_tid) {  // first triggering group of its thread
+                        last_tid = tid;
+                        has = true;
+                        const uint64_t grp = (uint64_t)(g0 + g);
+                        rec = p.rec8 ? make_ulonglong2(key_hi | (grp << 32) | (uint32_t)mask, 0)
+                                     : make_ulonglong2(key_hi | grp, (unsigned long long)mask);
+                    }
+                };
                 // ---- stage 2: exact lane test per positive group --------------------
+                // (each lane settles one group per iteration; a task-parallel
+                // form -- the tile's (clause, group) pairs spread over all lanes,
+                // literal rows by shuffle -- measured slower:
+                // profiles/r02_k_test_variants.md)
                 while (__any_sync(0xffffffffu, left != GW(0))) {
                     bool has = false;
                     ulonglong2 rec = make_ulonglong2(0, 0);
                     if (left != GW(0)) {
                         const int g = __ffsll((long long)(unsigned long long)left) - 1;
                         left &= left - GW(1);
-                        const LW mask = lane_test<LW>(lanes + (int64_t)g * p.vstride, cur, lp, size) &
-                                        (LW)groups[g0 + g].lane_mask;
-                        if (mask != LW(0)) {
-                            const int hits = __popcll((unsigned long long)mask);
-                            trig_acc += hits;
-                            if (!p.emit_only) {
-                                act = __dadd_rn(act, __dmul_rn(p.inc, (double)hits));
-                                touched = true;
-                            }
-                            const int tid = groups[g0 + g].tid;
-                            if (p.all_pairs || tid != last_tid) {  // first triggering group of its thread
-                                last_tid = tid;
-                                has = true;
-                                const uint64_t grp = (uint64_t)(g0 + g);
-                                rec = p.rec8 ? make_ulonglong2(key_hi | (grp << 32) | (uint32_t)mask, 0)
-                                             : make_ulonglong2(key_hi | grp, (unsigned long long)mask);
-                            }
-                        }
+                        settle(g, lane_test<LW>(lanes + (int64_t)g * p.vstride, cur, lp, size) &
+                                      (LW)groups[g0 + g].lane_mask, has, rec);
                     }
                     rb.append(has, rec, p.out, p.out_cap, p.ctr, lane);
                 }
