@@ -758,6 +758,9 @@ k_test(const __grid_constant__ TestParams<LW, GW> p) {
                     left = sweep<GW>(reinterpret_cast<const AggEntry<GW>*>(tab), cur, lp, size, p.sentinel) &
                            width_mask<GW>(G);
                 pos_acc += __popcll((unsigned long long)left);
+#ifdef TSG_ABL_NO_STAGE2  // ablation timing only (wrong results)
+                left = GW(0);
+#endif
                 if (left != GW(0) && !loaded) {  // stage-2 entry: id and activity of the clause
                     loaded = true;
                     const int slot = (tile - (int)bd->tile0) * STRIDE + lane;
@@ -799,7 +802,11 @@ k_test(const __grid_constant__ TestParams<LW, GW> p) {
                         settle(g, lane_test<LW>(lanes + (int64_t)g * p.vstride, cur, lp, size) &
                                       (LW)groups[g0 + g].lane_mask, has, rec);
                     }
+#ifndef TSG_ABL_NO_RECORDS  // ablation timing only (wrong results)
                     rb.append(has, rec, p.out, p.out_cap, p.ctr, lane);
+#else
+                    if (has && rec.x == 1234567) trig_acc += 1;
+#endif
                 }
             };
             if constexpr (MULTI) {
