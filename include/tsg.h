@@ -314,6 +314,33 @@ int tsg_sync(tsg_engine* h);
 /* the handle's CUDA stream (cudaStream_t), for interop */
 int tsg_stream(tsg_engine* h, void** stream);
 
+/* ---- host report ring (north_star subsystem 4) ---------------
+ * Replaces the copy-out of engine.py:462-464's report emission: while a ring
+ * is open, every launched round's trigger kernel writes its records through
+ * warp-aggregated reservations straight into page-locked host memory mapped
+ * into the device, and CPU threads drain them while the kernel still runs --
+ * no device record buffer, no D2H copy, no fetch call.  Records arrive in
+ * reservation order (not the reference's delivery order); the (eid, tid)
+ * dedup and counters are the round's as usual.  A full ring stalls the
+ * reserving warps until the drainer frees slots, for at most wait_us per
+ * flush; past that the round's remaining records are dropped and its collect
+ * fails with TSG_ECAPACITY (the ring stays failed until reopened).
+ * lane_width <= 32, engine ids < 2^48.  The fetch calls fail for ringed
+ * rounds. */
+/* open a ring of >= capacity records (rounded up to a power of two, >= 128);
+ * no round may be in flight */
+int tsg_ring_open(tsg_engine* h, int64_t capacity, int64_t wait_us);
+int tsg_ring_close(tsg_engine* h);
+/* Copy up to cap landed records, in ring order, into out (key = engine_id <<
+ * 16 | group, lane_mask) and free their slots.  Returns as soon as at least one
+ * record was copied and the next has not landed, or after timeout_us with
+ * none.  Thread-safe against the round calls on other threads (drainers
+ * serialise on the ring's lock). */
+int tsg_ring_drain(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n, int64_t timeout_us);
+/* records of the rounds collected so far, records drained, whether records
+ * were dropped */
+int tsg_ring_status(tsg_engine* h, int64_t* expected, int64_t* consumed, int32_t* failed);
+
 /* ---- standalone bit-parallel kernels (bitpack.py) ----------------------------
  * Same device code as the engine path, exposed for the library-level API.
  * All arrays are host arrays of uint64 words indexed by variable (slot 0

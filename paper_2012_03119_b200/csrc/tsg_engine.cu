@@ -9,10 +9,12 @@
 #include <immintrin.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <unordered_map>
@@ -146,6 +148,7 @@ struct tsg_engine {
         bool timed = false;                   // its encode / test are bracketed by timing events
         bool rec8 = false;                    // its records are 8-byte u64
         bool all_pairs = false;
+        bool ringed = false;                  // its records went to the host report ring
         GroupDesc* d_groups = nullptr;        // the round's groups (device)
         GroupDesc* h_groups = nullptr;        // pinned staging of the same
         int64_t groups_cap = 0;
@@ -212,6 +215,20 @@ struct tsg_engine {
     // (.208) than False (.153), so positive literals are non-False more often
     int prefer = 1;
     bool prefer_fixed = false;      // TSG_PREFER fixes it; else set from each round's statistics
+
+    // host report ring (tsg_ring_open): rounds launched while
+    // it is open write their records into it instead of the device buffer
+    struct Ring {
+        unsigned long long* slots = nullptr;    // page-locked, mapped: [cap][2] tagged words
+        unsigned long long* d_slots = nullptr;  // its device view
+        unsigned long long* ctl = nullptr;      // page-locked, mapped: [0] consumed (tail), [1] failed
+        unsigned long long* d_ctl = nullptr;
+        unsigned long long* d_pos = nullptr;    // device: positions reserved by the kernels
+        int64_t cap = 0, wait_ns = 0;
+        std::mutex mtx;                         // one drainer at a time
+        int64_t consumed = 0;                   // under mtx
+        std::atomic<int64_t> expected{0};       // records of the collected rounds
+    } ring;
 };
 
 namespace {
@@ -444,6 +461,13 @@ int launch_test(tsg_engine* h, int k, int emit_only) {
     p.emit_only = emit_only;
     p.rec8 = R.rec8 ? 1 : 0;
     p.all_pairs = R.all_pairs ? 1 : 0;
+    if (R.ringed) {  // records straight into the host ring (never replayed: no device buffer to overflow)
+        p.out = nullptr;
+        p.out_cap = 0;
+        p.ring = RingDesc{h->ring.d_slots, h->ring.d_pos, h->ring.d_ctl, h->ring.d_ctl + 1,
+                          (unsigned long long)(h->ring.cap - 1), (unsigned long long)h->ring.wait_ns,
+                          (unsigned long long)(R.seq % 65535 + 1)};
+    }
     const bool multi = rd.n_chunks > 1;
     auto* fn = multi ? k_test<LW, GW, true> : k_test<LW, GW, false>;
     const size_t smem = (size_t)test_smem_bytes(R.rec8);
@@ -534,6 +558,8 @@ std::vector<int64_t> bucket_bases(tsg_engine* h, int64_t* flat) {
     *flat = acc;
     return base;
 }
+
+void ring_free(tsg_engine* h);  // the host report ring (end of file)
 
 void select_free(tsg_engine* h) {
     auto& S = h->sel;
@@ -650,6 +676,7 @@ int tsg_destroy(tsg_engine* h) {
     if (!h) return TSG_OK;
     DevGuard g(h->dev);
     if (h->st) select_free(h);
+    if (h->st) ring_free(h);
     if (h->st) cudaStreamSynchronize(h->st);
     if (h->ingress) cudaStreamSynchronize(h->ingress);
     if (h->egress) cudaStreamSynchronize(h->egress);
@@ -1361,6 +1388,12 @@ int round_launch(tsg_engine* h, double inc, bool flip) {
     for (const auto& Q : h->rs)
         if (Q.inflight && Q.slot == h->tslot)
             return fail(TSG_EINVAL, "table slot %d still belongs to an uncollected round", h->tslot);
+    if (h->ring.slots) {
+        if (h->ring.ctl[1])
+            return fail(TSG_ECAPACITY, "the report ring dropped records of an earlier round: close and reopen it");
+        if (h->max_id >= (int64_t(1) << 48))
+            return fail(TSG_ECAPACITY, "report ring records carry 48-bit engine ids (largest id %lld)", (long long)h->max_id);
+    }
     // this state's record buffer may still be copying out from two rounds ago
     CK(cudaStreamWaitEvent(h->st, R.ev_copied, 0));
     R.n_out = 0;
@@ -1372,6 +1405,8 @@ int round_launch(tsg_engine* h, double inc, bool flip) {
     // 8-byte egress: the kernel writes the packed u64 records itself when
     // they fit (ids < 2^27, <= 32 groups, 32-bit lane masks)
     R.rec8 = h->record_bytes == 8 && !wide_lane(h) && h->max_id < (int64_t(1) << 27) && h->rd.n_groups <= 32;
+    R.ringed = h->ring.slots != nullptr;
+    if (R.ringed) R.rec8 = false;  // the kernel's buffer holds 16-byte records; the ring words are its own
     const RoundDesc& rd = R.fl;
     if (rd.n_chunks && h->oob) {  // out-of-range literal stored: numpy would raise IndexError
         CK(cudaMemsetAsync(h->mctr + 4, 0, 8, h->st));
@@ -1447,7 +1482,13 @@ int round_collect(tsg_engine* h, tsg_round_result* out) {
         res.lane_triggers = (int64_t)R.h_ctr[2];
         // overflow: grow and replay emission only (no activity / counter side
         // effects); the record count is exact, so one replay suffices
-        if (n_rec > R.out_cap) {
+        if (R.ringed) {
+            h->ring.expected += n_rec;
+            if (h->ring.ctl[1])
+                return fail(TSG_ECAPACITY, "report ring full for longer than %lld us: records of round %lld were dropped "
+                            "(drain the ring while rounds run, or open a larger one)",
+                            (long long)(h->ring.wait_ns / 1000), (long long)R.seq);
+        } else if (n_rec > R.out_cap) {
             dfree(h, R.out);
             R.out = nullptr;
             R.out_cap = n_rec + n_rec / 4 + 1024;
@@ -1463,7 +1504,7 @@ int round_collect(tsg_engine* h, tsg_round_result* out) {
                             (long long)rc[0], (long long)n_rec);
             res.reruns = 1;
         }
-        R.n_out = n_rec;
+        R.n_out = R.ringed ? 0 : n_rec;
         const int64_t n = store_size(h);
         int64_t lanes_total = 0;
         for (int g = 0; g < rd.n_groups; ++g) lanes_total += rd.glanes[g];
@@ -1671,8 +1712,17 @@ int egress_view(tsg_engine* h, int64_t k, const void** src, int64_t* bytes) {
 }
 }  // namespace
 
+namespace {
+int not_ringed(const tsg_engine* h) {
+    if (h->rs[h->fetch_rs].ringed)
+        return fail(TSG_EINVAL, "the round's records went to the host report ring: read them with tsg_ring_drain");
+    return TSG_OK;
+}
+}  // namespace
+
 int tsg_fetch_reports(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n) {
     CKR(validate_handle(h));
+    CKR(not_ringed(h));
     DevGuard g(h->dev);
     const int64_t k = std::min(cap, h->rs[h->fetch_rs].n_out);
     if (k > 0) {
@@ -1698,6 +1748,7 @@ int tsg_set_record_bytes(tsg_engine* h, int32_t bytes) {
 
 int tsg_fetch_reports_async(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n) {
     CKR(validate_handle(h));
+    CKR(not_ringed(h));
     DevGuard g(h->dev);
     auto& R = h->rs[h->fetch_rs];
     const int64_t k = std::min(cap, R.n_out);
@@ -1722,6 +1773,7 @@ int tsg_fetch_wait(tsg_engine* h) {
 
 int tsg_reports_device(tsg_engine* h, void** device_ptr, int64_t* n) {
     CKR(validate_handle(h));
+    CKR(not_ringed(h));
     auto& R = h->rs[h->fetch_rs];
     if (R.rec8) return fail(TSG_EINVAL, "the round's records are 8-byte u64 (tsg_set_record_bytes(8)), not tsg_report");
     *device_ptr = R.out;
@@ -1874,6 +1926,7 @@ int tsg_fetch_ordered(tsg_engine* const* hs, int32_t n_h, const int32_t* rank_of
     int64_t total = 0, max_id = 0;
     for (int32_t s = 0; s < n_h; ++s) {
         CKR(validate_handle(hs[s]));
+        CKR(not_ringed(hs[s]));
         const auto& R = hs[s]->rs[hs[s]->fetch_rs];
         if (R.fl.n_groups != rd.n_groups || R.fl.gtid != rd.gtid || R.rec8 != rec8 ||
             hs[s]->cfg.group_width != h0->cfg.group_width)
@@ -1997,3 +2050,118 @@ int tsg_fetch_ordered(tsg_engine* const* hs, int32_t n_h, const int32_t* rank_of
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Host report ring (north_star subsystem 4)
+
+namespace {
+void ring_free(tsg_engine* h) {
+    auto& r = h->ring;
+    if (!r.slots) return;
+    cudaStreamSynchronize(h->st);
+    dfree(h, r.d_pos);
+    cudaStreamSynchronize(h->st);
+    cudaFreeHost(r.slots);
+    cudaFreeHost(r.ctl);
+    r.slots = r.d_slots = r.ctl = r.d_ctl = r.d_pos = nullptr;
+    r.cap = 0;
+    r.consumed = 0;
+    r.expected = 0;
+}
+}  // namespace
+
+int tsg_ring_open(tsg_engine* h, int64_t capacity, int64_t wait_us) {
+    CKR(validate_handle(h));
+    if (any_inflight(h)) return fail(TSG_EINVAL, "a launched round is not collected");
+    if (h->ring.slots) return fail(TSG_EINVAL, "a report ring is already open");
+    if (wide_lane(h))
+        return fail(TSG_EINVAL, "report ring records carry 32-bit lane masks: lane_width %d > 32", h->cfg.lane_width);
+    if (capacity < RECBUF || capacity > (int64_t(1) << 36))
+        return fail(TSG_EINVAL, "ring capacity must be in %d..2^36 records, got %lld", RECBUF, (long long)capacity);
+    if (wait_us <= 0) return fail(TSG_EINVAL, "wait_us must be positive");
+    int64_t cap = 1;
+    while (cap < capacity) cap <<= 1;
+    DevGuard g(h->dev);
+    auto& r = h->ring;
+    void *slots = nullptr, *ctl = nullptr, *dv = nullptr;
+    CK(cudaHostAlloc(&slots, (size_t)cap * 16, cudaHostAllocMapped | cudaHostAllocPortable));
+    if (cudaHostAlloc(&ctl, 64, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFreeHost(slots);
+        return fail(TSG_ENOMEM, "report ring control block");
+    }
+    std::memset(slots, 0, (size_t)cap * 16);
+    std::memset(ctl, 0, 64);
+    r.slots = static_cast<unsigned long long*>(slots);
+    r.ctl = static_cast<unsigned long long*>(ctl);
+    CK(cudaHostGetDevicePointer(&dv, slots, 0));
+    r.d_slots = static_cast<unsigned long long*>(dv);
+    CK(cudaHostGetDevicePointer(&dv, ctl, 0));
+    r.d_ctl = static_cast<unsigned long long*>(dv);
+    CKR(dalloc(h, (void**)&r.d_pos, 8));
+    CK(cudaMemsetAsync(r.d_pos, 0, 8, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    r.cap = cap;
+    r.wait_ns = wait_us * 1000;
+    r.consumed = 0;
+    r.expected = 0;
+    return TSG_OK;
+}
+
+int tsg_ring_close(tsg_engine* h) {
+    CKR(validate_handle(h));
+    if (any_inflight(h)) return fail(TSG_EINVAL, "a launched round is not collected");
+    DevGuard g(h->dev);
+    std::lock_guard<std::mutex> lk(h->ring.mtx);
+    ring_free(h);
+    return TSG_OK;
+}
+
+int tsg_ring_drain(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n, int64_t timeout_us) {
+    if (!h || !n || (cap > 0 && !out)) return fail(TSG_EINVAL, "bad arguments");
+    *n = 0;
+    auto& r = h->ring;
+    std::lock_guard<std::mutex> lk(r.mtx);
+    if (!r.slots) return fail(TSG_EINVAL, "no report ring is open");
+    volatile unsigned long long* S = r.slots;
+    volatile unsigned long long* ctl = r.ctl;
+    const uint64_t mask = (uint64_t)r.cap - 1;
+    const auto t0 = std::chrono::steady_clock::now();
+    int64_t k = 0;
+    int rc = TSG_OK;
+    while (k < cap) {
+        volatile unsigned long long* s = S + 2 * ((uint64_t)r.consumed & mask);
+        const unsigned long long w0 = s[0], w1 = s[1];
+        if (w0 == 0 || w1 == 0) {  // not landed (yet)
+            if (k > 0 || ctl[1]) break;
+            if (std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count() >= timeout_us)
+                break;
+            _mm_pause();
+            continue;
+        }
+        if ((w0 >> 48) != (w1 >> 48)) {
+            rc = fail(TSG_ECUDA, "report ring slot %lld holds words of two rounds", (long long)r.consumed);
+            break;
+        }
+        out[k].key = ((w0 & ((1ull << 48) - 1)) << 16) | ((w1 >> 32) & 0xFFFFull);
+        out[k].lane_mask = w1 & 0xFFFFFFFFull;
+        s[0] = 0;  // free the slot before publishing the tail past it (x86 keeps store order)
+        s[1] = 0;
+        ++r.consumed;
+        ++k;
+        if ((k & 1023) == 0) ctl[0] = (unsigned long long)r.consumed;
+    }
+    ctl[0] = (unsigned long long)r.consumed;
+    *n = k;
+    return rc;
+}
+
+int tsg_ring_status(tsg_engine* h, int64_t* expected, int64_t* consumed, int32_t* failed) {
+    if (!h) return fail(TSG_EINVAL, "null engine handle");
+    auto& r = h->ring;
+    if (!r.slots) return fail(TSG_EINVAL, "no report ring is open");
+    if (expected) *expected = r.expected.load();
+    if (consumed) *consumed = (int64_t)((volatile unsigned long long*)r.ctl)[0];
+    if (failed) *failed = ((volatile unsigned long long*)r.ctl)[1] ? 1 : 0;
+    return TSG_OK;
+}

@@ -484,6 +484,31 @@ struct GroupDesc {
     int32_t pad;
 };
 
+// Host report ring (north_star subsystem 4): k_test writes
+// its records straight into page-locked host memory mapped into the device
+// address space -- no device record buffer, no copy-out -- and CPU threads
+// drain them while the kernel runs (tsg_ring_drain).  A record is two u64
+// words, each tagged with the round's 16-bit tag in its top bits so the
+// drainer knows it landed (an aligned 8-byte store reaches host memory
+// whole); the drainer zeroes the slots it consumed and publishes how many in
+// `tail`.  Warps reserve ring positions with one atomic per record-buffer
+// flush and wait (bounded by wait_ns) while the ring is full.
+struct RingDesc {
+    unsigned long long* slots;                 // host-mapped [cap][2] words; null: ring off
+    unsigned long long* pos;                   // device: positions reserved so far (monotone over rounds)
+    const volatile unsigned long long* tail;   // host-mapped: positions the drainer consumed
+    unsigned long long* fail;                  // host-mapped: set when a flush gave up waiting for room
+    unsigned long long mask;                   // cap - 1 (cap a power of two, >= RECBUF)
+    unsigned long long wait_ns;                // longest wait for room, per flush
+    unsigned long long tag;                    // the round's tag, 1..65535
+};
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 template <class LW, class GW>
 struct TestParams {
     const BucketDesc* buckets;
@@ -506,6 +531,7 @@ struct TestParams {
     int32_t emit_only;               // replay after record-buffer overflow: no activity / counter side effects
     int32_t rec8;                    // 8-byte records engine_id << 37 | group << 32 | lane_mask
     int32_t all_pairs;               // every triggering (clause, group), not the first per thread
+    RingDesc ring;                   // host report ring (16-byte records, lane width <= 32), or off
 };
 
 #ifndef TSG_PF
@@ -519,7 +545,9 @@ constexpr int TEST_THREADS = 256;
 #endif
 constexpr int RECBUF = TSG_RECBUF;  // records buffered per warp
 // dynamic shared memory of k_test: the warps' record buffers
-__host__ __device__ constexpr int test_smem_bytes(bool rec8) { return (TEST_THREADS / 32) * RECBUF * (rec8 ? 8 : 16); }
+// (+ 16 bytes per warp: the report ring's cached tail)
+__host__ __device__ constexpr int test_rec_stride(bool rec8) { return RECBUF * (rec8 ? 8 : 16) + 16; }
+__host__ __device__ constexpr int test_smem_bytes(bool rec8) { return (TEST_THREADS / 32) * test_rec_stride(rec8); }
 
 __device__ __forceinline__ int lit_var(int32_t lit) { return lit < 0 ? -lit : lit; }
 
@@ -637,8 +665,52 @@ struct RecBuf {
     unsigned char* buf;
     int rec8;
     int n = 0;
-    __device__ __forceinline__ void flush(void* out, unsigned long long cap, unsigned long long* ctr, int lane) {
+    // ring form of flush (lane width <= 32, 16-byte records in `buf`)
+    __device__ __forceinline__ void flush_ring(unsigned long long* ctr, const RingDesc& r, int lane) {
+        unsigned long long base = 0;
+        int ok = 1;
+        if (lane == 0) {
+            // the drainer's progress as last read, kept after this warp's records (test_smem_bytes)
+            unsigned long long& tail_seen = *reinterpret_cast<unsigned long long*>(buf + RECBUF * 16);
+            base = atomicAdd(r.pos, (unsigned long long)n);
+            atomicAdd(ctr, (unsigned long long)n);
+            const unsigned long long cap = r.mask + 1;
+            if (base + n > tail_seen + cap) {  // wait for the drainer to free the slots
+                const unsigned long long t0 = globaltimer_ns();
+                for (;;) {
+                    tail_seen = *r.tail;
+                    if (base + n <= tail_seen + cap) break;
+                    if (*(volatile unsigned long long*)r.fail || globaltimer_ns() - t0 > r.wait_ns) {
+                        *(volatile unsigned long long*)r.fail = 1;  // records dropped: the round fails
+                        ok = 0;
+                        break;
+                    }
+                    __nanosleep(1000);
+                }
+            }
+        }
+        base = __shfl_sync(0xffffffffu, base, 0);
+        ok = __shfl_sync(0xffffffffu, ok, 0);
+        if (ok) {
+            const unsigned long long tag = r.tag << 48;
+            for (int i = lane; i < n; i += 32) {
+                const ulonglong2 rec = reinterpret_cast<const ulonglong2*>(buf)[i];
+                unsigned long long* slot = r.slots + 2 * ((base + (unsigned long long)i) & r.mask);
+                // id | group, lane mask: both words tagged (nonzero), each an aligned 8-byte store
+                slot[0] = tag | (rec.x >> 16);
+                slot[1] = tag | ((rec.x & 0xFFFFull) << 32) | (rec.y & 0xFFFFFFFFull);
+            }
+        }
         __syncwarp();
+        n = 0;
+    }
+    __device__ __forceinline__ void flush(void* out, unsigned long long cap, unsigned long long* ctr,
+                                          const RingDesc& ring, int lane) {
+        __syncwarp();
+        if (__builtin_expect(ring.slots != nullptr, 0)) {
+            flush_ring(ctr, ring, lane);
+            return;
+        }
         unsigned long long base = 0;
         if (lane == 0) base = atomicAdd(ctr, (unsigned long long)n);
         base = __shfl_sync(0xffffffffu, base, 0);
@@ -654,7 +726,7 @@ struct RecBuf {
     }
     // warp-wide: lanes with `has` append `rec`
     __device__ __forceinline__ void append(bool has, ulonglong2 rec, void* out, unsigned long long cap,
-                                           unsigned long long* ctr, int lane) {
+                                           unsigned long long* ctr, const RingDesc& ring, int lane) {
         const unsigned b = __ballot_sync(0xffffffffu, has);
         if (has) {
             const int i = n + __popc(b & ((1u << lane) - 1u));
@@ -662,7 +734,7 @@ struct RecBuf {
             else reinterpret_cast<ulonglong2*>(buf)[i] = rec;
         }
         n += __popc(b);
-        if (n > RECBUF - 32) flush(out, cap, ctr, lane);
+        if (n > RECBUF - 32) flush(out, cap, ctr, ring, lane);
     }
 };
 
@@ -707,7 +779,8 @@ k_test(const __grid_constant__ TestParams<LW, GW> p) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int nwarps = (int)(((int64_t)gridDim.x * TEST_THREADS) >> 5);
-    RecBuf rb{s_rec + (size_t)warp * RECBUF * (p.rec8 ? 8 : 16), p.rec8};
+    RecBuf rb{s_rec + (size_t)warp * test_rec_stride(p.rec8), p.rec8};
+    if (lane == 0 && p.ring.slots) *reinterpret_cast<unsigned long long*>(rb.buf + RECBUF * 16) = 0;
     unsigned int pos_acc = 0, trig_acc = 0, top_acc = 0;
     const uint32_t top_mask = MULTI ? width_mask<uint32_t>((p.n_chunks + p.per_bit - 1) / p.per_bit) : 1u;
     // single-chunk rounds (<= 64 groups): the group table in shared memory
@@ -803,7 +876,7 @@ k_test(const __grid_constant__ TestParams<LW, GW> p) {
                                       (LW)groups[g0 + g].lane_mask, has, rec);
                     }
 #ifndef TSG_ABL_NO_RECORDS  // ablation timing only (wrong results)
-                    rb.append(has, rec, p.out, p.out_cap, p.ctr, lane);
+                    rb.append(has, rec, p.out, p.out_cap, p.ctr, p.ring, lane);
 #else
                     if (has && rec.x == 1234567) trig_acc += 1;
 #endif
@@ -837,7 +910,8 @@ k_test(const __grid_constant__ TestParams<LW, GW> p) {
         if (!tile_step(cur, nxt)) break;
         cur = nxt;
     }
-    if (rb.n) rb.flush(p.out, p.out_cap, p.ctr, lane);
+    if (rb.n) rb.flush(p.out, p.out_cap, p.ctr, p.ring, lane);
+    if (p.ring.slots) __threadfence_system();  // ring records visible before the counters are published
 
     // counters: warp reduce, block reduce, one atomic per block
     pos_acc = __reduce_add_sync(0xffffffffu, pos_acc);

@@ -7,7 +7,7 @@ memory, split encode/test for table broadcast, record fetch.
 from __future__ import annotations
 
 import ctypes as C
-from typing import Optional, Tuple
+from typing import List, Optional, Tuple
 
 import numpy as np
 
@@ -279,6 +279,32 @@ class NativeEngine:
         """Decoded records: (engine_id, group, lane_mask), unordered."""
         return reports.decode(self.fetch_raw(n))
 
+    # ---- host report ring (tsg_ring_*, DESIGN.md §4.4) ----------------------
+    def ring_open(self, capacity: int = 1 << 20, wait_ms: float = 2000.0) -> None:
+        """Records of the rounds launched from now on go straight into a
+        page-locked host ring, drained with ring_drain while the kernel runs."""
+        check(self.L.tsg_ring_open(self.h, int(capacity), max(1, int(wait_ms * 1000))))
+
+    def ring_close(self) -> None:
+        check(self.L.tsg_ring_close(self.h))
+
+    def ring_drain(self, max_records: int = 1 << 16, timeout_ms: float = 0.0,
+                   out: Optional[np.ndarray] = None) -> np.ndarray:
+        """Landed records in ring order (raw REPORT_DTYPE); empty after
+        timeout_ms with none.  Safe to call from a thread other than the one
+        running the rounds (ctypes releases the GIL)."""
+        if out is None or len(out) < max_records:
+            out = np.zeros(max(1, max_records), REPORT_DTYPE)
+        got = C.c_int64(0)
+        check(self.L.tsg_ring_drain(self.h, ptr(out), max_records, C.byref(got), int(timeout_ms * 1000)))
+        return out[:got.value]
+
+    def ring_status(self):
+        """(records of the collected rounds, records drained, dropped?)"""
+        e, c, f = C.c_int64(0), C.c_int64(0), C.c_int32(0)
+        check(self.L.tsg_ring_status(self.h, C.byref(e), C.byref(c), C.byref(f)))
+        return e.value, c.value, bool(f.value)
+
     def sync(self) -> None:
         check(self.L.tsg_sync(self.h))
 
@@ -286,3 +312,63 @@ class NativeEngine:
         s = C.c_void_p()
         check(self.L.tsg_stream(self.h, C.byref(s)))
         return s.value or 0
+
+
+class RingDrainer:
+    """CPU threads draining an engine's host report ring (tsg_ring_drain)
+    while its rounds run -- the consumer side of north_star subsystem 4.
+    Records accumulate as raw REPORT_DTYPE arrays; `take(n)` waits until n
+    records were drained in all and returns them (reservation order when one
+    thread drains)."""
+
+    def __init__(self, eng: NativeEngine, threads: int = 1, batch: int = 1 << 16):
+        import threading
+        self.eng = eng
+        self._parts: List[np.ndarray] = []
+        self._count = 0
+        self._lock = threading.Lock()
+        self._cv = threading.Condition(self._lock)
+        self._stop = threading.Event()
+        self.error: Optional[BaseException] = None
+        self._threads = [threading.Thread(target=self._run, args=(batch,), daemon=True) for _ in range(threads)]
+        for t in self._threads:
+            t.start()
+
+    def _run(self, batch: int) -> None:
+        buf = np.zeros(batch, REPORT_DTYPE)
+        try:
+            while not self._stop.is_set():
+                got = self.eng.ring_drain(batch, timeout_ms=1.0, out=buf)
+                if len(got):
+                    with self._cv:
+                        self._parts.append(got.copy())
+                        self._count += len(got)
+                        self._cv.notify_all()
+        except BaseException as e:  # surfaced by take()
+            with self._cv:
+                self.error = e
+                self._cv.notify_all()
+
+    def take(self, n: int, timeout_s: float = 60.0) -> np.ndarray:
+        """The first n records not taken yet (blocks until drained)."""
+        import time
+        end = time.monotonic() + timeout_s
+        with self._cv:
+            while self._count < n and self.error is None:
+                left = end - time.monotonic()
+                if left <= 0:
+                    raise TimeoutError(f"ring drained {self._count} of {n} records")
+                self._cv.wait(min(left, 0.1))
+            if self.error is not None:
+                raise self.error
+            allr = np.concatenate(self._parts) if self._parts else np.zeros(0, REPORT_DTYPE)
+            out, rest = allr[:n], allr[n:]
+            self._parts = [rest] if len(rest) else []
+            self._count -= n
+            return out
+
+    def close(self) -> None:
+        self._stop.set()
+        for t in self._threads:
+            t.join()
+
