@@ -332,9 +332,9 @@ int tsg_stream(tsg_engine* h, void** stream);
 int tsg_ring_open(tsg_engine* h, int64_t capacity, int64_t wait_us);
 int tsg_ring_close(tsg_engine* h);
 /* Copy up to cap landed records, in ring order, into out (key = engine_id <<
- * 16 | group, lane_mask) and free their slots.  Returns as soon as at least one
- * record was copied and the next has not landed, or after timeout_us with
- * none.  Thread-safe against the round calls on other threads (drainers
+ * 16 | group, lane_mask) and free their slots.  Returns when cap records were
+ * copied, when at least one was and the next has not landed for
+ * min(timeout_us, 20) microseconds, or after timeout_us with none.  Thread-safe against the round calls on other threads (drainers
  * serialise on the ring's lock). */
 int tsg_ring_drain(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n, int64_t timeout_us);
 /* records of the rounds collected so far, records drained, whether records

@@ -14,7 +14,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <set>
 #include <string>
 #include <thread>
 #include <unordered_map>
@@ -225,8 +227,15 @@ struct tsg_engine {
         unsigned long long* d_ctl = nullptr;
         unsigned long long* d_pos = nullptr;    // device: positions reserved by the kernels
         int64_t cap = 0, wait_ns = 0;
-        std::mutex mtx;                         // one drainer at a time
-        int64_t consumed = 0;                   // under mtx
+        int32_t shift = 0;                      // log2(cap)
+        // drainers claim blocks of `blk` consecutive positions (block b =
+        // positions b*blk ..), consume a block in order, and hand it back
+        // when they stop early; the tail is the consumed prefix
+        int64_t blk = 1;
+        std::mutex mtx;                         // guards the block bookkeeping below
+        int64_t next_block = 0;                 // blocks handed out so far
+        std::map<int64_t, int64_t> open;        // handed-out, unfinished block -> positions consumed
+        std::set<int64_t> idle;                 // open blocks no drainer holds (resumable)
         std::atomic<int64_t> expected{0};       // records of the collected rounds
     } ring;
 };
@@ -466,7 +475,7 @@ int launch_test(tsg_engine* h, int k, int emit_only) {
         p.out_cap = 0;
         p.ring = RingDesc{h->ring.d_slots, h->ring.d_pos, h->ring.d_ctl, h->ring.d_ctl + 1,
                           (unsigned long long)(h->ring.cap - 1), (unsigned long long)h->ring.wait_ns,
-                          (unsigned long long)(R.seq % 65535 + 1)};
+                          h->ring.shift};
     }
     const bool multi = rd.n_chunks > 1;
     auto* fn = multi ? k_test<LW, GW, true> : k_test<LW, GW, false>;
@@ -2065,7 +2074,9 @@ void ring_free(tsg_engine* h) {
     cudaFreeHost(r.ctl);
     r.slots = r.d_slots = r.ctl = r.d_ctl = r.d_pos = nullptr;
     r.cap = 0;
-    r.consumed = 0;
+    r.next_block = 0;
+    r.open.clear();
+    r.idle.clear();
     r.expected = 0;
 }
 }  // namespace
@@ -2102,8 +2113,13 @@ int tsg_ring_open(tsg_engine* h, int64_t capacity, int64_t wait_us) {
     CK(cudaMemsetAsync(r.d_pos, 0, 8, h->st));
     CK(cudaStreamSynchronize(h->st));
     r.cap = cap;
+    r.shift = 0;
+    while ((int64_t(1) << r.shift) < cap) ++r.shift;
+    r.blk = std::max<int64_t>(1, std::min<int64_t>(4096, cap / 8));  // >= 8 blocks per lap
     r.wait_ns = wait_us * 1000;
-    r.consumed = 0;
+    r.next_block = 0;
+    r.open.clear();
+    r.idle.clear();
     r.expected = 0;
     return TSG_OK;
 }
@@ -2117,43 +2133,84 @@ int tsg_ring_close(tsg_engine* h) {
     return TSG_OK;
 }
 
+namespace {
+// the consumed prefix: every block below the lowest open one is finished
+int64_t ring_tail(const tsg_engine::Ring& r) {
+    if (r.open.empty()) return r.next_block * r.blk;
+    return r.open.begin()->first * r.blk + r.open.begin()->second;
+}
+}  // namespace
+
 int tsg_ring_drain(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n, int64_t timeout_us) {
     if (!h || !n || (cap > 0 && !out)) return fail(TSG_EINVAL, "bad arguments");
     *n = 0;
     auto& r = h->ring;
-    std::lock_guard<std::mutex> lk(r.mtx);
-    if (!r.slots) return fail(TSG_EINVAL, "no report ring is open");
-    volatile unsigned long long* S = r.slots;
+    {
+        std::lock_guard<std::mutex> lk(r.mtx);
+        if (!r.slots) return fail(TSG_EINVAL, "no report ring is open");
+    }
+    const volatile unsigned long long* S = r.slots;
     volatile unsigned long long* ctl = r.ctl;
     const uint64_t mask = (uint64_t)r.cap - 1;
-    const auto t0 = std::chrono::steady_clock::now();
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
+    auto last = t0;  // when the last record was taken
+    // with records in hand, wait this long for the next one before returning
+    // (records land out of order while the kernel runs)
+    const double linger_us = std::min<double>((double)timeout_us, 20.0);
     int64_t k = 0;
-    int rc = TSG_OK;
     while (k < cap) {
-        volatile unsigned long long* s = S + 2 * ((uint64_t)r.consumed & mask);
-        const unsigned long long w0 = s[0], w1 = s[1];
-        if (w0 == 0 || w1 == 0) {  // not landed (yet)
-            if (k > 0 || ctl[1]) break;
-            if (std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count() >= timeout_us)
-                break;
-            _mm_pause();
-            continue;
+        // take the lowest idle block, or the next new one
+        int64_t b, p;
+        {
+            std::lock_guard<std::mutex> lk(r.mtx);
+            if (!r.idle.empty()) {
+                b = *r.idle.begin();
+                r.idle.erase(r.idle.begin());
+                p = r.open[b];
+            } else {
+                b = r.next_block++;
+                p = r.open[b] = 0;
+            }
         }
-        if ((w0 >> 48) != (w1 >> 48)) {
-            rc = fail(TSG_ECUDA, "report ring slot %lld holds words of two rounds", (long long)r.consumed);
-            break;
+        // consume it in order while its records have landed
+        bool stalled = false;
+        while (p < r.blk && k < cap) {
+            const uint64_t q = (uint64_t)(b * r.blk + p);
+            const volatile unsigned long long* s = S + 2 * (q & mask);
+            const unsigned long long tag = ring_tag(q, r.shift);
+            const unsigned long long w0 = s[0], w1 = s[1];
+            if ((w0 >> 48) != tag || (w1 >> 48) != tag) {  // not landed (yet)
+                const auto now = clk::now();
+                if (ctl[1] || (k > 0 && std::chrono::duration<double, std::micro>(now - last).count() >= linger_us) ||
+                    std::chrono::duration<double, std::micro>(now - t0).count() >= timeout_us) {
+                    stalled = true;
+                    break;
+                }
+                _mm_pause();
+                continue;
+            }
+            if ((k & 255) == 0) last = clk::now();
+            if (p + 16 < r.blk) _mm_prefetch((const char*)(S + 2 * ((q + 16) & mask)), _MM_HINT_T0);
+            out[k].key = ((w0 & ((1ull << 48) - 1)) << 16) | ((w1 >> 32) & 0xFFFFull);
+            out[k].lane_mask = w1 & 0xFFFFFFFFull;
+            ++p;
+            ++k;
         }
-        out[k].key = ((w0 & ((1ull << 48) - 1)) << 16) | ((w1 >> 32) & 0xFFFFull);
-        out[k].lane_mask = w1 & 0xFFFFFFFFull;
-        s[0] = 0;  // free the slot before publishing the tail past it (x86 keeps store order)
-        s[1] = 0;
-        ++r.consumed;
-        ++k;
-        if ((k & 1023) == 0) ctl[0] = (unsigned long long)r.consumed;
+        {
+            std::lock_guard<std::mutex> lk(r.mtx);
+            if (p == r.blk) {
+                r.open.erase(b);
+            } else {
+                r.open[b] = p;
+                r.idle.insert(b);
+            }
+            ctl[0] = (unsigned long long)ring_tail(r);  // the slots below are free for the kernel
+        }
+        if (stalled) break;
     }
-    ctl[0] = (unsigned long long)r.consumed;
     *n = k;
-    return rc;
+    return TSG_OK;
 }
 
 int tsg_ring_status(tsg_engine* h, int64_t* expected, int64_t* consumed, int32_t* failed) {

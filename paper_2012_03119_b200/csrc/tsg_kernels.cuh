@@ -488,20 +488,25 @@ struct GroupDesc {
 // its records straight into page-locked host memory mapped into the device
 // address space -- no device record buffer, no copy-out -- and CPU threads
 // drain them while the kernel runs (tsg_ring_drain).  A record is two u64
-// words, each tagged with the round's 16-bit tag in its top bits so the
-// drainer knows it landed (an aligned 8-byte store reaches host memory
-// whole); the drainer zeroes the slots it consumed and publishes how many in
-// `tail`.  Warps reserve ring positions with one atomic per record-buffer
-// flush and wait (bounded by wait_ns) while the ring is full.
+// words, each tagged in its top 16 bits with its lap (position / capacity,
+// mod 65535, plus one), so a drainer knows a slot holds this lap's record
+// without the slots ever being cleared (an aligned 8-byte store reaches host
+// memory whole); drainers publish how many positions they consumed in
+// `tail`.  Warps reserve positions with one atomic per record-buffer flush
+// and wait (bounded by wait_ns) while the ring is full.
 struct RingDesc {
     unsigned long long* slots;                 // host-mapped [cap][2] words; null: ring off
     unsigned long long* pos;                   // device: positions reserved so far (monotone over rounds)
-    const volatile unsigned long long* tail;   // host-mapped: positions the drainer consumed
+    const volatile unsigned long long* tail;   // host-mapped: positions the drainers consumed
     unsigned long long* fail;                  // host-mapped: set when a flush gave up waiting for room
     unsigned long long mask;                   // cap - 1 (cap a power of two, >= RECBUF)
     unsigned long long wait_ns;                // longest wait for room, per flush
-    unsigned long long tag;                    // the round's tag, 1..65535
+    int32_t shift;                             // log2(cap)
 };
+
+__host__ __device__ __forceinline__ unsigned long long ring_tag(unsigned long long q, int shift) {
+    return (q >> shift) % 65535ull + 1ull;
+}
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
     unsigned long long t;
@@ -692,13 +697,14 @@ struct RecBuf {
         base = __shfl_sync(0xffffffffu, base, 0);
         ok = __shfl_sync(0xffffffffu, ok, 0);
         if (ok) {
-            const unsigned long long tag = r.tag << 48;
             for (int i = lane; i < n; i += 32) {
                 const ulonglong2 rec = reinterpret_cast<const ulonglong2*>(buf)[i];
-                unsigned long long* slot = r.slots + 2 * ((base + (unsigned long long)i) & r.mask);
-                // id | group, lane mask: both words tagged (nonzero), each an aligned 8-byte store
-                slot[0] = tag | (rec.x >> 16);
-                slot[1] = tag | ((rec.x & 0xFFFFull) << 32) | (rec.y & 0xFFFFFFFFull);
+                const unsigned long long q = base + (unsigned long long)i;
+                const unsigned long long tag = ring_tag(q, r.shift) << 48;
+                // id | group, lane mask: both words tagged, one 16-byte store (a warp
+                // covers whole 128-byte lines; each 8-byte half lands whole)
+                reinterpret_cast<ulonglong2*>(r.slots)[q & r.mask] =
+                    make_ulonglong2(tag | (rec.x >> 16), tag | ((rec.x & 0xFFFFull) << 32) | (rec.y & 0xFFFFFFFFull));
             }
         }
         __syncwarp();

@@ -335,15 +335,16 @@ class RingDrainer:
             t.start()
 
     def _run(self, batch: int) -> None:
-        buf = np.zeros(batch, REPORT_DTYPE)
+        buf = np.empty(batch, REPORT_DTYPE)
         try:
             while not self._stop.is_set():
                 got = self.eng.ring_drain(batch, timeout_ms=1.0, out=buf)
                 if len(got):
                     with self._cv:
-                        self._parts.append(got.copy())
+                        self._parts.append(got)  # a view of buf: a fresh buf follows
                         self._count += len(got)
                         self._cv.notify_all()
+                    buf = np.empty(batch, REPORT_DTYPE)
         except BaseException as e:  # surfaced by take()
             with self._cv:
                 self.error = e
@@ -361,9 +362,13 @@ class RingDrainer:
                 self._cv.wait(min(left, 0.1))
             if self.error is not None:
                 raise self.error
-            allr = np.concatenate(self._parts) if self._parts else np.zeros(0, REPORT_DTYPE)
-            out, rest = allr[:n], allr[n:]
-            self._parts = [rest] if len(rest) else []
+            if len(self._parts) == 1 and len(self._parts[0]) == n:
+                out = self._parts[0]
+                self._parts = []
+            else:
+                allr = np.concatenate(self._parts) if self._parts else np.zeros(0, REPORT_DTYPE)
+                out, rest = allr[:n], allr[n:]
+                self._parts = [rest] if len(rest) else []
             self._count -= n
             return out
 
