@@ -236,6 +236,8 @@ struct tsg_engine {
         int64_t next_block = 0;                 // blocks handed out so far
         std::map<int64_t, int64_t> open;        // handed-out, unfinished block -> positions consumed
         std::set<int64_t> idle;                 // open blocks no drainer holds (resumable)
+        int active = 0;                         // drainers inside tsg_ring_drain (under mtx)
+        std::atomic<bool> closing{false};       // tsg_ring_close waits for active == 0
         std::atomic<int64_t> expected{0};       // records of the collected rounds
     } ring;
 };
@@ -2128,9 +2130,23 @@ int tsg_ring_close(tsg_engine* h) {
     CKR(validate_handle(h));
     if (any_inflight(h)) return fail(TSG_EINVAL, "a launched round is not collected");
     DevGuard g(h->dev);
-    std::lock_guard<std::mutex> lk(h->ring.mtx);
-    ring_free(h);
-    return TSG_OK;
+    auto& r = h->ring;
+    {
+        std::lock_guard<std::mutex> lk(r.mtx);
+        if (!r.slots) return TSG_OK;
+        r.closing = true;  // new drain calls fail; the ones inside finish (their waits are bounded)
+    }
+    for (;;) {
+        {
+            std::lock_guard<std::mutex> lk(r.mtx);
+            if (r.active == 0) {
+                ring_free(h);
+                r.closing = false;
+                return TSG_OK;
+            }
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
 }
 
 namespace {
@@ -2147,8 +2163,13 @@ int tsg_ring_drain(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n, int6
     auto& r = h->ring;
     {
         std::lock_guard<std::mutex> lk(r.mtx);
-        if (!r.slots) return fail(TSG_EINVAL, "no report ring is open");
+        if (!r.slots || r.closing) return fail(TSG_EINVAL, "no report ring is open");
+        ++r.active;
     }
+    struct Leave {  // the drainer count drops on every exit path
+        tsg_engine::Ring& r;
+        ~Leave() { std::lock_guard<std::mutex> lk(r.mtx); --r.active; }
+    } leave{r};
     const volatile unsigned long long* S = r.slots;
     volatile unsigned long long* ctl = r.ctl;
     const uint64_t mask = (uint64_t)r.cap - 1;
@@ -2182,7 +2203,7 @@ int tsg_ring_drain(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n, int6
             const unsigned long long w0 = s[0], w1 = s[1];
             if ((w0 >> 48) != tag || (w1 >> 48) != tag) {  // not landed (yet)
                 const auto now = clk::now();
-                if (ctl[1] || (k > 0 && std::chrono::duration<double, std::micro>(now - last).count() >= linger_us) ||
+                if (ctl[1] || r.closing || (k > 0 && std::chrono::duration<double, std::micro>(now - last).count() >= linger_us) ||
                     std::chrono::duration<double, std::micro>(now - t0).count() >= timeout_us) {
                     stalled = true;
                     break;
@@ -2216,6 +2237,7 @@ int tsg_ring_drain(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n, int6
 int tsg_ring_status(tsg_engine* h, int64_t* expected, int64_t* consumed, int32_t* failed) {
     if (!h) return fail(TSG_EINVAL, "null engine handle");
     auto& r = h->ring;
+    std::lock_guard<std::mutex> lk(r.mtx);
     if (!r.slots) return fail(TSG_EINVAL, "no report ring is open");
     if (expected) *expected = r.expected.load();
     if (consumed) *consumed = (int64_t)((volatile unsigned long long*)r.ctl)[0];

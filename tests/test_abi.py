@@ -74,3 +74,16 @@ def test_pack_rows_host_encoding(num_vars):
     want = (t.reshape(9, w, 32) * bit).sum(2).astype(np.uint64) | \
         ((s.reshape(9, w, 32) * bit).sum(2).astype(np.uint64) << np.uint64(32))
     assert np.array_equal(got, want)
+
+
+def test_ring_entry_points_validate_without_a_device():
+    # the report ring's host-side argument checks (include/tsg.h tsg_ring_*)
+    # need no GPU: a null handle or a missing ring is TSG_EINVAL
+    import ctypes as C
+    from paper_2012_03119_b200 import _lib
+    L = _lib.load()
+    n = C.c_int64(0)
+    assert L.tsg_ring_drain(None, None, 0, C.byref(n), 0) == _lib.TSG_EINVAL
+    assert L.tsg_ring_status(None, None, None, None) == _lib.TSG_EINVAL
+    assert L.tsg_ring_open(None, 1024, 1000) == _lib.TSG_EINVAL
+    assert L.tsg_ring_close(None) == _lib.TSG_EINVAL

@@ -187,3 +187,24 @@ def test_ring_argument_checks(W):
     assert len(e.ring_drain(8, timeout_ms=1)) == 0
     e.ring_close()
     e.close()
+
+
+def test_ring_close_while_drainers_run(W):
+    """tsg_ring_close waits for drainers inside tsg_ring_drain; later drain
+    calls fail cleanly (no use of the freed ring)."""
+    from paper_2012_03119_b200.native import RingDrainer
+    eng, rng, buckets, flat, offs, ids = store(W, 50_000, 3000, 3)
+    snaps = W.snapshots(3, 32, 3000, rng)
+    gl, gt = W.groups_for(3, 32, 32)
+    eng.stage(snaps)
+    eng.ring_open(capacity=1 << 12)
+    dr = RingDrainer(eng, threads=3, batch=128)
+    res = eng.round(gl, gt, 1.0)
+    assert len(dr.take(res.reports)) == res.reports
+    eng.ring_close()  # drainers still polling
+    time.sleep(0.05)
+    dr.close()
+    assert dr.error is None or isinstance(dr.error, ValueError)
+    res = eng.round(gl, gt, 1.0)  # the device buffer path again
+    assert len(eng.fetch(res.reports)) == res.reports
+    eng.close()
