@@ -245,7 +245,7 @@ def run_reference(args, cfg):
         "impl": "reference", "metric": "clause_assignment_tests_per_second", "value": v,
         "unit": "clause_assignment_tests/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "strong" if args.gpus > 1 else "weak",
+        "scaling": args.scaling,  # the same label at every N of a scaling series
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {cfg.n_clauses} clauses (size U[2,30]) x {cfg.assignments} "
                                f"assignments ({cfg.threads} threads x {cfg.lanes}), {cfg.num_vars} vars, seed {cfg.seed}",
@@ -763,7 +763,7 @@ def main():
         line = {
             "metric": "clause_assignment_tests_per_second", "value": value, "unit": "clause_assignment_tests/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "strong" if (args.scaling == "strong" and world > 1) else "weak",
+            "higher_is_better": True, "scaling": args.scaling,  # the same label at every N of a scaling series
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": (f"{cfg.name}: {cfg.n_clauses} clauses (size U[2,30], mean 16) x "
                                     f"{A} assignments ({cfg.threads} threads x {cfg.lanes}), {cfg.num_vars} vars, "
