@@ -11,10 +11,13 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <set>
 #include <string>
@@ -585,24 +588,112 @@ void select_free(tsg_engine* h) {
 // under the recent rounds' assignments: they end the early-exit recurrence
 // sooner), then the rest.  The order word lets readback restore the
 // reference's literal order.
+// Host worker threads for batch-parallel loops (clause placement), created
+// once: spawning threads per tsg_add_clauses call cost more than the
+// placement of a streaming batch itself.  parallel_for(n, f) runs f(a, b) over
+// [0, n) in contiguous ranges on up to `workers` threads plus the caller.
+class HostPool {
+  public:
+    static HostPool& get() {
+        static HostPool p;
+        return p;
+    }
+    int workers() const { return (int)th_.size(); }
+    template <class F>
+    void parallel_for(int64_t n, int parts, F&& f) {
+        parts = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)parts, (int64_t)workers() + 1, n}));
+        if (parts == 1) { f(0, n); return; }
+        std::unique_lock<std::mutex> run(run_mtx_);  // one batch at a time
+        std::function<void(int64_t, int64_t)> job = f;
+        {
+            std::lock_guard<std::mutex> lk(mtx_);
+            job_ = &job;
+            n_ = n;
+            parts_ = parts;
+            next_ = 1;  // part 0 is the caller's
+            left_ = parts - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        f(0, n / parts);
+        std::unique_lock<std::mutex> lk(mtx_);
+        done_cv_.wait(lk, [&] { return left_ == 0; });
+        job_ = nullptr;
+    }
+
+  private:
+    HostPool() {
+        const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+        for (int i = 0; i < std::min(hw, 16) - 1; ++i) th_.emplace_back([this] { loop(); });
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> lk(mtx_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    void loop() {
+        uint64_t seen = 0;
+        std::unique_lock<std::mutex> lk(mtx_);
+        for (;;) {
+            cv_.wait(lk, [&] { return stop_ || (gen_ != seen && next_ < parts_); });
+            if (stop_) return;
+            seen = gen_;
+            while (next_ < parts_) {
+                const int k = next_++;
+                const int64_t a = n_ * k / parts_, b = n_ * (k + 1) / parts_;
+                auto* job = job_;
+                lk.unlock();
+                (*job)(a, b);
+                lk.lock();
+                if (--left_ == 0) done_cv_.notify_all();
+            }
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex mtx_, run_mtx_;
+    std::condition_variable cv_, done_cv_;
+    std::function<void(int64_t, int64_t)>* job_ = nullptr;
+    int64_t n_ = 0;
+    int parts_ = 0, next_ = 0, left_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
 void place_clause(const tsg_engine* h, const int32_t* lits, int32_t size, int32_t* out, uint64_t* order) {
     const int32_t lim = std::min(size, ORDER_MASK_BITS);
     int32_t jp = -1;
     uint64_t m = 0;
     if (h->pivot && lim > 0) {
         jp = 0;
-        for (int32_t j = 1; j < lim; ++j)
-            if (std::llabs((long long)lits[j]) < std::llabs((long long)lits[jp])) jp = j;
-        if (h->prefer != 0)
-            for (int32_t j = 0; j < lim; ++j)
-                if (j != jp && (lits[j] > 0) == (h->prefer > 0)) m |= 1ull << j;
+        int64_t best = std::llabs((long long)lits[0]);
+        for (int32_t j = 1; j < lim; ++j) {
+            const int64_t a = std::llabs((long long)lits[j]);
+            if (a < best) { best = a; jp = j; }
+        }
+        if (h->prefer != 0) {  // branch-free: the signs are random
+            const bool pos = h->prefer > 0;
+            for (int32_t j = 0; j < lim; ++j) m |= (uint64_t)((j != jp) & ((lits[j] > 0) == pos)) << j;
+        }
     }
+    // pivot, the preferred-polarity literals, the others (each group in
+    // clause order) -- branch-free compaction through a small buffer -- then
+    // the literals past the order word's reach, in clause order
+    int32_t tmp[ORDER_MASK_BITS + 2];
     int32_t o = 0;
-    if (jp >= 0) out[o++] = lits[jp];
-    for (int32_t j = 0; j < lim; ++j)
-        if ((m >> j) & 1) out[o++] = lits[j];
-    for (int32_t j = 0; j < size; ++j)
-        if (j != jp && (j >= lim || !((m >> j) & 1))) out[o++] = lits[j];
+    if (jp >= 0) tmp[o++] = lits[jp];
+    for (int32_t j = 0; j < lim; ++j) {
+        tmp[o] = lits[j];
+        o += (int32_t)((m >> j) & 1);
+    }
+    for (int32_t j = 0; j < lim; ++j) {
+        tmp[o] = lits[j];
+        o += (int32_t)((j != jp) & !((m >> j) & 1));
+    }
+    std::memcpy(out, tmp, (size_t)lim * 4);
+    if (size > lim) std::memcpy(out + lim, lits + lim, (size_t)(size - lim) * 4);
     *order = order_word(jp, m);
 }
 
@@ -744,23 +835,41 @@ int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, 
     // group clauses by size, preserving arrival order; new sizes create buckets
     // in first-seen order (dict insertion order of ClauseStore.buckets)
     std::vector<int> bucket_of(n);
-    for (int64_t i = 0; i < n; ++i) {
-        const int32_t s = (int32_t)(offsets[i + 1] - offsets[i]);
-        for (int64_t j = offsets[i]; j < offsets[i + 1]; ++j) {
-            const int64_t v = lits[j] < 0 ? -(int64_t)lits[j] : lits[j];
-            if (v > h->V) h->oob = true;  // stored as-is; testing raises (numpy IndexError, engine.py:251)
+    {
+        // literal range check over the batch at once (stored as-is; testing
+        // raises, numpy IndexError, engine.py:251)
+        int32_t lo = 0, hi = 0;
+        for (int64_t j = offsets[0]; j < offsets[n]; ++j) {
+            lo = std::min(lo, lits[j]);
+            hi = std::max(hi, lits[j]);
         }
-        if (ids[i] < 0 || ids[i] > h->max_id) h->max_id = std::max<int64_t>(h->max_id, ids[i] < 0 ? INT64_MAX : ids[i]);
-        auto it = h->by_size.find(s);
-        if (it == h->by_size.end()) {
-            Bucket b;
-            b.size = s;
-            b.rank = (int32_t)h->buckets.size();
-            h->by_size[s] = (int)h->buckets.size();
-            bucket_of[i] = (int)h->buckets.size();
-            h->buckets.push_back(b);
-        } else {
-            bucket_of[i] = it->second;
+        if ((int64_t)hi > h->V || -(int64_t)lo > h->V) h->oob = true;
+        int64_t top = h->max_id;
+        for (int64_t i = 0; i < n; ++i) top = std::max<int64_t>(top, ids[i] < 0 ? INT64_MAX : ids[i]);
+        h->max_id = top;
+        // size -> bucket through a small direct cache (sizes < 256), the map beyond
+        int cache[256];
+        std::fill(cache, cache + 256, -1);
+        for (const auto& kv : h->by_size)
+            if (kv.first < 256) cache[kv.first] = kv.second;
+        for (int64_t i = 0; i < n; ++i) {
+            const int32_t s = (int32_t)(offsets[i + 1] - offsets[i]);
+            int b = s < 256 ? cache[s] : -1;
+            if (b < 0) {
+                auto it = h->by_size.find(s);
+                if (it == h->by_size.end()) {
+                    Bucket nb;
+                    nb.size = s;
+                    nb.rank = (int32_t)h->buckets.size();
+                    b = (int)h->buckets.size();
+                    h->by_size[s] = b;
+                    h->buckets.push_back(nb);
+                } else {
+                    b = it->second;
+                }
+                if (s < 256) cache[s] = b;
+            }
+            bucket_of[i] = b;
         }
     }
     mark("buckets");
@@ -773,14 +882,7 @@ int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, 
                 place_clause(h, lits + offsets[i], (int32_t)(offsets[i + 1] - offsets[i]),
                              placed.data() + (offsets[i] - offsets[0]), &hm[i]);
         };
-        const int64_t nt = std::min<int64_t>({(int64_t)std::max(1u, std::thread::hardware_concurrency()), 16, n / 2048});
-        if (nt > 1) {
-            std::vector<std::thread> pool;
-            for (int64_t t = 0; t < nt; ++t) pool.emplace_back(place_range, n * t / nt, n * (t + 1) / nt);
-            for (auto& t : pool) t.join();
-        } else {
-            place_range(0, n);
-        }
+        HostPool::get().parallel_for(n, (int)std::min<int64_t>(16, n / 1024), place_range);
     }
     mark("place");
     std::vector<std::vector<int64_t>> members(h->buckets.size());
@@ -826,7 +928,9 @@ int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, 
     }
     const int64_t o_ids = al8(n_lits * 4), o_org = o_ids + n * 8, o_ord = o_org + al8(n * 4), o_desc = o_ord + n * 8;
     const int64_t total_bytes = o_desc + (int64_t)(desc.size() * sizeof(AppendDesc));
-    std::vector<uint8_t> host((size_t)total_bytes);
+    // (not zero-filled: every field below is written; alignment padding is never read)
+    std::unique_ptr<uint8_t[]> host_buf(new uint8_t[(size_t)std::max<int64_t>(total_bytes, 8)]);
+    struct { uint8_t* p; uint8_t* data() const { return p; } } host{host_buf.get()};
     {
         int32_t* hl = reinterpret_cast<int32_t*>(host.data());
         int64_t* hid = reinterpret_cast<int64_t*>(host.data() + o_ids);
