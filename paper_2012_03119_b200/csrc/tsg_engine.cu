@@ -7,6 +7,7 @@
 // tsg_store.cuh; no library kernels.
 #include <cuda_runtime.h>
 #include <immintrin.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -601,6 +602,8 @@ class HostPool {
     int workers() const { return (int)th_.size(); }
     template <class F>
     void parallel_for(int64_t n, int parts, F&& f) {
+        // a forked child has none of the parent's workers: run in the caller
+        if (getpid() != pid_) parts = 1;
         parts = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)parts, (int64_t)workers() + 1, n}));
         if (parts == 1) { f(0, n); return; }
         std::unique_lock<std::mutex> run(run_mtx_);  // one batch at a time
@@ -622,7 +625,7 @@ class HostPool {
     }
 
   private:
-    HostPool() {
+    HostPool() : pid_(getpid()) {
         const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
         for (int i = 0; i < std::min(hw, 16) - 1; ++i) th_.emplace_back([this] { loop(); });
     }
@@ -652,6 +655,7 @@ class HostPool {
             }
         }
     }
+    const pid_t pid_;
     std::vector<std::thread> th_;
     std::mutex mtx_, run_mtx_;
     std::condition_variable cv_, done_cv_;
