@@ -596,8 +596,10 @@ void select_free(tsg_engine* h) {
 class HostPool {
   public:
     static HostPool& get() {
-        static HostPool p;
-        return p;
+        // never destroyed: the workers end with the process (no join at exit,
+        // where a forked child would join threads it does not have)
+        static HostPool* p = new HostPool;
+        return *p;
     }
     int workers() const { return (int)th_.size(); }
     template <class F>
@@ -629,20 +631,11 @@ class HostPool {
         const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
         for (int i = 0; i < std::min(hw, 16) - 1; ++i) th_.emplace_back([this] { loop(); });
     }
-    ~HostPool() {
-        {
-            std::lock_guard<std::mutex> lk(mtx_);
-            stop_ = true;
-        }
-        cv_.notify_all();
-        for (auto& t : th_) t.join();
-    }
     void loop() {
         uint64_t seen = 0;
         std::unique_lock<std::mutex> lk(mtx_);
         for (;;) {
-            cv_.wait(lk, [&] { return stop_ || (gen_ != seen && next_ < parts_); });
-            if (stop_) return;
+            cv_.wait(lk, [&] { return gen_ != seen && next_ < parts_; });
             seen = gen_;
             while (next_ < parts_) {
                 const int k = next_++;
@@ -656,14 +649,13 @@ class HostPool {
         }
     }
     const pid_t pid_;
-    std::vector<std::thread> th_;
+    std::vector<std::thread> th_;  // detached in effect: the pool lives until exit
     std::mutex mtx_, run_mtx_;
     std::condition_variable cv_, done_cv_;
     std::function<void(int64_t, int64_t)>* job_ = nullptr;
     int64_t n_ = 0;
     int parts_ = 0, next_ = 0, left_ = 0;
     uint64_t gen_ = 0;
-    bool stop_ = false;
 };
 
 void place_clause(const tsg_engine* h, const int32_t* lits, int32_t size, int32_t* out, uint64_t* order) {
