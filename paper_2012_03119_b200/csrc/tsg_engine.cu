@@ -189,6 +189,9 @@ struct tsg_engine {
     int64_t size_of_id_cap = 0;
     bool oob = false;               // a stored literal may exceed num_vars (checked before testing)
     int64_t round_seq = 0;
+    uint8_t* add_host = nullptr;    // page-locked staging block of tsg_add_clauses (streaming batches)
+    int64_t add_host_cap = 0;
+    cudaEvent_t ev_add = nullptr;   // its last copy
     int enc_attr = 0;               // k_encode_packed32 shared-memory attribute set, per (GPW, GW)
     // tsg_round_encode_groups: encode groups [enc_g0, enc_g1) only (enc_g1 < 0: all)
     int32_t enc_g0 = 0, enc_g1 = -1;
@@ -787,6 +790,8 @@ int tsg_destroy(tsg_engine* h) {
         cudaStreamSynchronize(h->st);
     }
     if (h->h_mctr) cudaFreeHost(h->h_mctr);
+    if (h->add_host) cudaFreeHost(h->add_host);
+    if (h->ev_add) cudaEventDestroy(h->ev_add);
     for (auto& R : h->rs) {
         if (R.h_ctr) cudaFreeHost(R.h_ctr);
         if (R.h_groups) cudaFreeHost(R.h_groups);
@@ -830,16 +835,21 @@ int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, 
     h->store_seq++;
     // group clauses by size, preserving arrival order; new sizes create buckets
     // in first-seen order (dict insertion order of ClauseStore.buckets)
-    std::vector<int> bucket_of(n);
+    std::unique_ptr<int[]> bucket_of(new int[n]);  // (uninitialised buffers below: every element is written)
     {
         // literal range check over the batch at once (stored as-is; testing
         // raises, numpy IndexError, engine.py:251)
-        int32_t lo = 0, hi = 0;
-        for (int64_t j = offsets[0]; j < offsets[n]; ++j) {
-            lo = std::min(lo, lits[j]);
-            hi = std::max(hi, lits[j]);
-        }
-        if ((int64_t)hi > h->V || -(int64_t)lo > h->V) h->oob = true;
+        const int64_t nl = offsets[n] - offsets[0];
+        std::atomic<bool> oob{false};
+        HostPool::get().parallel_for(nl, (int)std::min<int64_t>(16, nl / (1 << 18)), [&](int64_t a, int64_t b) {
+            int32_t lo = 0, hi = 0;
+            for (int64_t j = offsets[0] + a; j < offsets[0] + b; ++j) {
+                lo = std::min(lo, lits[j]);
+                hi = std::max(hi, lits[j]);
+            }
+            if ((int64_t)hi > h->V || -(int64_t)lo > h->V) oob = true;
+        });
+        if (oob) h->oob = true;
         int64_t top = h->max_id;
         for (int64_t i = 0; i < n; ++i) top = std::max<int64_t>(top, ids[i] < 0 ? INT64_MAX : ids[i]);
         h->max_id = top;
@@ -870,38 +880,48 @@ int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, 
     }
     mark("buckets");
     // place every clause (pivot first), then one H2D + scatter per bucket
-    std::vector<int32_t> placed((size_t)std::max<int64_t>(offsets[n] - offsets[0], 1));
-    std::vector<uint64_t> hm(n);
+    std::unique_ptr<int32_t[]> placed(new int32_t[(size_t)std::max<int64_t>(offsets[n] - offsets[0], 1)]);
+    std::unique_ptr<uint64_t[]> hm(new uint64_t[n]);
     {  // placement is independent per clause: split large batches over host threads
         auto place_range = [&](int64_t a, int64_t b) {
             for (int64_t i = a; i < b; ++i)
                 place_clause(h, lits + offsets[i], (int32_t)(offsets[i + 1] - offsets[i]),
-                             placed.data() + (offsets[i] - offsets[0]), &hm[i]);
+                             placed.get() + (offsets[i] - offsets[0]), &hm[i]);
         };
         HostPool::get().parallel_for(n, (int)std::min<int64_t>(16, n / 1024), place_range);
     }
     mark("place");
     std::vector<std::vector<int64_t>> members(h->buckets.size());
-    for (int64_t i = 0; i < n; ++i) members[bucket_of[i]].push_back(i);
+    {
+        std::vector<int64_t> cnt(h->buckets.size(), 0);
+        for (int64_t i = 0; i < n; ++i) ++cnt[bucket_of[i]];
+        for (size_t b = 0; b < cnt.size(); ++b) members[b].reserve(cnt[b]);
+        for (int64_t i = 0; i < n; ++i) members[bucket_of[i]].push_back(i);
+    }
     mark("members");
     if (h->pivot) {  // each bucket's new clauses in pivot-variable order (stable: ties keep arrival order)
         // only batches dense enough for a 32-clause tile to share pivot lines
         // gain from the order; a streaming batch of a few hundred clauses per
         // bucket would only pay for the sort
-        std::vector<uint64_t> key;
-        for (auto& mem : members) {
-            if (mem.size() < 4096) continue;
-            key.resize(mem.size());
-            for (size_t c = 0; c < mem.size(); ++c) {
-                const int64_t i = mem[c];
-                const uint64_t v = offsets[i + 1] > offsets[i] ? (uint64_t)std::llabs((long long)placed[offsets[i] - offsets[0]]) : 0;
-                key[c] = v << 32 | (uint64_t)c;  // (pivot variable, position in the batch's bucket list)
+        std::vector<int> big;  // buckets sorted, in parallel (one per worker at a time)
+        for (size_t bi = 0; bi < members.size(); ++bi)
+            if (members[bi].size() >= 4096) big.push_back((int)bi);
+        HostPool::get().parallel_for((int64_t)big.size(), (int)std::min<size_t>(16, big.size()), [&](int64_t a, int64_t b) {
+            std::vector<uint64_t> key;
+            for (int64_t q = a; q < b; ++q) {
+                auto& mem = members[big[q]];
+                key.resize(mem.size());
+                for (size_t c = 0; c < mem.size(); ++c) {
+                    const int64_t i = mem[c];
+                    const uint64_t v = offsets[i + 1] > offsets[i] ? (uint64_t)std::llabs((long long)placed[offsets[i] - offsets[0]]) : 0;
+                    key[c] = v << 32 | (uint64_t)c;  // (pivot variable, position in the batch's bucket list)
+                }
+                std::sort(key.begin(), key.end());
+                std::vector<int64_t> sorted(mem.size());
+                for (size_t c = 0; c < mem.size(); ++c) sorted[c] = mem[key[c] & 0xFFFFFFFFu];
+                mem.swap(sorted);
             }
-            std::sort(key.begin(), key.end());
-            std::vector<int64_t> sorted(mem.size());
-            for (size_t c = 0; c < mem.size(); ++c) sorted[c] = mem[key[c] & 0xFFFFFFFFu];
-            mem.swap(sorted);
-        }
+        });
     }
     mark("sort");
     // one host staging block for the whole batch (a pageable copy waits for
@@ -924,26 +944,57 @@ int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, 
     }
     const int64_t o_ids = al8(n_lits * 4), o_org = o_ids + n * 8, o_ord = o_org + al8(n * 4), o_desc = o_ord + n * 8;
     const int64_t total_bytes = o_desc + (int64_t)(desc.size() * sizeof(AppendDesc));
-    // (not zero-filled: every field below is written; alignment padding is never read)
-    std::unique_ptr<uint8_t[]> host_buf(new uint8_t[(size_t)std::max<int64_t>(total_bytes, 8)]);
-    struct { uint8_t* p; uint8_t* data() const { return p; } } host{host_buf.get()};
+    // The staging block (not zero-filled: every field below is written;
+    // alignment padding is never read).  Streaming batches (<= 64 MB) go
+    // through a persistent page-locked block -- an asynchronous copy, reused
+    // once the previous batch's copy is done; bulk loads through pageable
+    // memory (page-locking hundreds of MB once costs more than it saves).
+    std::unique_ptr<uint8_t[]> host_buf;
+    uint8_t* host_p = nullptr;
+    const bool pinned_stage = total_bytes <= ((int64_t)64 << 20);
+    if (pinned_stage) {
+        if (h->ev_add) CK(cudaEventSynchronize(h->ev_add));  // the last batch's copy has read the block
+        else CK(cudaEventCreateWithFlags(&h->ev_add, cudaEventDisableTiming));
+        if (total_bytes > h->add_host_cap) {
+            const int64_t cap = std::max<int64_t>({total_bytes, 2 * h->add_host_cap, (int64_t)1 << 20});
+            if (h->add_host) cudaFreeHost(h->add_host);
+            h->add_host = nullptr;
+            h->add_host_cap = 0;
+            CK(cudaHostAlloc((void**)&h->add_host, (size_t)cap, cudaHostAllocPortable));
+            h->add_host_cap = cap;
+        }
+        host_p = h->add_host;
+    } else {
+        host_buf.reset(new uint8_t[(size_t)std::max<int64_t>(total_bytes, 8)]);
+        host_p = host_buf.get();
+    }
+    struct { uint8_t* p; uint8_t* data() const { return p; } } host{host_p};
     {
         int32_t* hl = reinterpret_cast<int32_t*>(host.data());
         int64_t* hid = reinterpret_cast<int64_t*>(host.data() + o_ids);
         int32_t* hor = reinterpret_cast<int32_t*>(host.data() + o_org);
         uint64_t* hmk = reinterpret_cast<uint64_t*>(host.data() + o_ord);
-        int64_t c = 0, l = 0;
+        // every bucket's first clause / literal slot in the block, then the
+        // buckets filled in parallel
+        std::vector<int64_t> c0(members.size() + 1, 0), l0(members.size() + 1, 0);
         for (size_t bi = 0; bi < members.size(); ++bi) {
-            const int32_t sz = h->buckets[bi].size;
-            for (const int64_t i : members[bi]) {
-                if (sz) memcpy(hl + l, placed.data() + (offsets[i] - offsets[0]), sz * 4);
-                l += sz;
-                hid[c] = ids[i];
-                hor[c] = origins[i];
-                hmk[c] = hm[i];
-                ++c;
-            }
+            c0[bi + 1] = c0[bi] + (int64_t)members[bi].size();
+            l0[bi + 1] = l0[bi] + (int64_t)members[bi].size() * h->buckets[bi].size;
         }
+        HostPool::get().parallel_for((int64_t)members.size(), n >= 8192 ? 16 : 1, [&](int64_t a, int64_t b) {
+            for (int64_t bi = a; bi < b; ++bi) {
+                const int32_t sz = h->buckets[bi].size;
+                int64_t c = c0[bi], l = l0[bi];
+                for (const int64_t i : members[bi]) {
+                    if (sz) memcpy(hl + l, placed.get() + (offsets[i] - offsets[0]), sz * 4);
+                    l += sz;
+                    hid[c] = ids[i];
+                    hor[c] = origins[i];
+                    hmk[c] = hm[i];
+                    ++c;
+                }
+            }
+        });
         memcpy(host.data() + o_desc, desc.data(), desc.size() * sizeof(AppendDesc));
     }
     const bool sizes_by_id = h->max_id < ((int64_t)1 << 40);
@@ -962,7 +1013,8 @@ int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, 
     mark("block");
     uint8_t* dev = nullptr;
     CKR(dalloc(h, (void**)&dev, std::max<int64_t>(total_bytes, 8)));
-    CK(cudaMemcpyAsync(dev, host.data(), total_bytes, cudaMemcpyHostToDevice, h->st));  // host block consumed on return
+    CK(cudaMemcpyAsync(dev, host.data(), total_bytes, cudaMemcpyHostToDevice, h->st));  // pageable: consumed on return
+    if (pinned_stage) CK(cudaEventRecord(h->ev_add, h->st));
     mark("h2d");
     k_append_batch<<<grid_for(n), 256, 0, h->st>>>(reinterpret_cast<const AppendDesc*>(dev + o_desc), (int32_t)desc.size(), n,
                                                    reinterpret_cast<const int32_t*>(dev),
