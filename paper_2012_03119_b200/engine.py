@@ -136,43 +136,96 @@ class RoundTrace:
 
 
 class _Arena:
-    """Append-only literal arena by engine id (Report.lits, engine.py:90-102).
-    Grows by replacing its arrays, never by rewriting them, so a report batch
-    holding the arena of its round keeps valid literals even after the
-    clause was removed."""
+    """Literal arena by engine id (Report.lits, engine.py:90-102).  Arrays
+    are never rewritten in place where a report batch may read them: appends
+    write past `used` and set the entries of new ids only, and reclaiming the
+    literals of removed clauses (once they outweigh the live ones) builds
+    new arrays -- a batch holding the arena of its round keeps valid
+    literals even after its clause was removed."""
 
-    __slots__ = ("lits", "off", "size", "used")
+    __slots__ = ("lits", "off", "size", "used", "alive", "live_lits", "dead_lits")
+    RECLAIM_MIN = 1 << 20  # dead literals below this are never worth a rebuild
 
     def __init__(self, lits=None, off=None, size=None, used=0):
         self.lits = np.zeros(1024, np.int32) if lits is None else lits
         self.off = np.zeros(1024, np.int64) if off is None else off
         self.size = np.zeros(1024, np.int32) if size is None else size
         self.used = used
+        self.alive = np.zeros(self.off.size, bool)  # (the live arena only; snapshots do not use it)
+        self.live_lits = 0
+        self.dead_lits = 0
 
     def snapshot(self) -> "_Arena":
-        return _Arena(self.lits, self.off, self.size, self.used)
+        """A read-only view for a report batch (lits_of only)."""
+        v = object.__new__(_Arena)
+        v.lits, v.off, v.size, v.used = self.lits, self.off, self.size, self.used
+        v.alive, v.live_lits, v.dead_lits = None, 0, 0
+        return v
 
     def append(self, ids: np.ndarray, lens: np.ndarray, flat: np.ndarray) -> None:
         total = int(flat.size)
-        if self.used + total > self.lits.size:
-            grown = np.zeros(max(self.used + total, 2 * self.lits.size), np.int32)
+        if self.used + total > self.lits.size:  # grow by half again (no zero fill: only [0, used) is read)
+            grown = np.empty(max(self.used + total, self.lits.size + self.lits.size // 2), np.int32)
             grown[:self.used] = self.lits[:self.used]
             self.lits = grown
         self.lits[self.used:self.used + total] = flat
         top = int(ids.max()) + 1 if ids.size else 0
         if top > self.off.size:
-            n = max(top, 2 * self.off.size)
+            n = max(top, self.off.size + self.off.size // 2)
             off = np.zeros(n, np.int64)
             off[:self.off.size] = self.off
             size = np.zeros(n, np.int32)
             size[:self.size.size] = self.size
-            self.off, self.size = off, size
+            alive = np.zeros(n, bool)
+            alive[:self.alive.size] = self.alive
+            self.off, self.size, self.alive = off, size, alive
         starts = np.zeros(len(lens), np.int64)
         if len(lens) > 1:
             np.cumsum(lens[:-1], out=starts[1:])
-        self.off[ids] = self.used + starts
-        self.size[ids] = lens
+        if ids.size and int(ids[-1]) - int(ids[0]) == ids.size - 1:  # consecutive ids (the usual batch)
+            sl = slice(int(ids[0]), int(ids[-1]) + 1)
+            self.off[sl] = self.used + starts
+            self.size[sl] = lens
+            self.alive[sl] = True
+        else:
+            self.off[ids] = self.used + starts
+            self.size[ids] = lens
+            self.alive[ids] = True
         self.used += total
+        self.live_lits += total
+
+    def remove(self, ids: np.ndarray) -> None:
+        """Clauses gone from the store: their literals are reclaimed once the
+        dead outweigh the live (a new set of arrays; report batches keep
+        theirs)."""
+        ids = np.asarray(ids, np.int64)
+        ids = ids[(ids >= 0) & (ids < self.alive.size)]
+        ids = np.unique(ids[self.alive[ids]])
+        if not ids.size:
+            return
+        self.alive[ids] = False
+        dead = int(self.size[ids].sum())
+        self.live_lits -= dead
+        self.dead_lits += dead
+        if self.dead_lits > max(self.live_lits, self.RECLAIM_MIN):
+            self._compact()
+
+    def _compact(self) -> None:
+        live = np.nonzero(self.alive)[0]
+        sizes = self.size[live].astype(np.int64)
+        total = int(sizes.sum())
+        starts = np.zeros(live.size, np.int64)
+        if live.size > 1:
+            np.cumsum(sizes[:-1], out=starts[1:])
+        src = np.repeat(self.off[live] - starts, sizes) + np.arange(total, dtype=np.int64)
+        lits = np.empty(max(total + total // 2, 1024), np.int32)
+        lits[:total] = self.lits[src]
+        off = np.zeros(self.off.size, np.int64)
+        size = np.zeros(self.size.size, np.int32)
+        off[live] = starts
+        size[live] = sizes
+        self.lits, self.off, self.size, self.used = lits, off, size, total
+        self.live_lits, self.dead_lits = total, 0
 
     def lits_of(self, eid: int) -> tuple:
         o = int(self.off[eid])
@@ -768,9 +821,11 @@ class Engine:
             return 0
         target = int(total * (1.0 - self.config.reduce_keep_fraction))
         if len(self._shards) == 1:
-            removed = len(self._shards[0].reduce(self._reduce_watermark, target))
+            gone = self._shards[0].reduce(self._reduce_watermark, target)
+            removed = len(gone)
         else:
-            removed, _ = _sharded.global_reduce(self._shards, self._reduce_watermark, target)
+            removed, gone = _sharded.global_reduce(self._shards, self._reduce_watermark, target)
+        self._arena.remove(gone)
         with self._id_lock:
             self._reduce_watermark = self._next_id
         self.counters["reduces"] += 1
@@ -785,6 +840,7 @@ class Engine:
         if ids.size == 0:
             return 0
         removed = sum(s.remove(ids) for s in self._shards)
+        self._arena.remove(ids)  # (ids not stored yet are not in the arena either)
         self.counters["clauses_deleted"] = self.counters.get("clauses_deleted", 0) + removed
         return removed
 

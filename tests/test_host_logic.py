@@ -47,3 +47,50 @@ def test_arena_keeps_round_literals():
     for snap, upto in snaps:  # every round's arena still answers for the ids it knew
         for i in rng.integers(0, upto, 50).tolist():
             assert snap.lits_of(i) == ref[i]
+
+
+def test_literal_arena_reclaims_removed_clauses_without_touching_old_batches():
+    # engine.py's Report-literal arena: appends, removals, compaction; a view
+    # taken for a round's report batch keeps its literals through all of it
+    import numpy as np
+    from paper_2012_03119_b200.engine import _Arena
+    rng = np.random.default_rng(3)
+
+    class Small(_Arena):  # reclaim at any size, and count the rebuilds
+        RECLAIM_MIN = 0
+        rebuilds = 0
+
+        def _compact(self):
+            Small.rebuilds += 1
+            super()._compact()
+
+    a = Small()
+    want = {}
+    nxt = 0
+    views = []
+    for rnd in range(30):
+        n = int(rng.integers(1, 4000))
+        lens = rng.integers(2, 31, n).astype(np.int32)
+        flat = rng.integers(-500, 500, int(lens.sum())).astype(np.int32)
+        ids = np.arange(nxt, nxt + n, dtype=np.int64)
+        nxt += n
+        a.append(ids, lens, flat)
+        o = 0
+        for i, L in zip(ids.tolist(), lens.tolist()):
+            want[i] = tuple(flat[o:o + L].tolist())
+            o += L
+        view = a.snapshot()
+        sample = rng.choice(nxt, min(50, nxt), replace=False)
+        views.append((view, {int(i): want[int(i)] for i in sample if int(i) in want}))
+        gone = rng.choice(nxt, nxt // 3, replace=False)
+        a.remove(gone)
+        a.remove(gone[:10])  # twice: ignored
+        for i in gone.tolist():
+            want.pop(i, None)
+    assert Small.rebuilds > 3 and a.dead_lits <= a.live_lits  # reclaimed along the way
+    assert a.used <= 2 * a.live_lits
+    for i, lits in want.items():
+        assert a.lits_of(i) == lits
+    for view, expect in views:  # old batches: literals as of their round
+        for i, lits in expect.items():
+            assert view.lits_of(i) == lits
