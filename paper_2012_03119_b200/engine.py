@@ -20,7 +20,7 @@ Host data paths, none of them per-record Python work:
   host-to-device copy on the round's path;
 * a round's reports are ordered on the GPU into the reference's delivery
   order (tsg_fetch_ordered) and queued per destination as array slices;
-  the ``Report`` objects, with their literals from an append-only literal
+  the ``Report`` objects, with their literals from a literal
   arena, are built by the draining solver thread;
 * ``EngineConfig.devices`` names several GPUs: the clauses are sharded
   across them (every size bucket balanced), the round's tables are encoded
