@@ -757,6 +757,13 @@ def main():
                     "ceiling_sectors_per_clk_per_sm": L2_GATHER_CEILING, "frac": per_clk / L2_GATHER_CEILING,
                     "ceiling_source": "profiles/r02_gather_modes.md (tools/microbench/gather_modes.cu): random "
                                       "16-byte gathers from an L2-resident table as divergent LDGs, B200"}
+            gc = os.path.join(ROOT, "profiles", "gather_ceiling.json")
+            if os.path.exists(gc):  # the same ceiling in ncu's request-interface counter (committed capture)
+                g = json.load(open(gc))
+                roofline.setdefault("l2_gather", {})["request_interface"] = {
+                    "counter": "l1tex__m_l1tex2xbar_req_cycles_active.avg.pct_of_peak_sustained_elapsed",
+                    "k_test_pct": g["k_test_pct"], "ceiling_pct": g["ceiling_pct"],
+                    "frac": g["k_test_pct"] / g["ceiling_pct"], "source": g["source"]}
         except Exception:
             pass
         strong = args.scaling == "strong" or world == 1
