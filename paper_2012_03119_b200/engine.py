@@ -46,7 +46,7 @@ import numpy as np
 from . import _lib
 from . import sharded as _sharded
 from ._lib import check, ptr
-from .native import NativeEngine
+from .native import NativeEngine, RingDrainer
 
 #: Activities are rescaled when the bump increment passes this (engine.py:39-40).
 _ACTIVITY_RESCALE = 1e100
@@ -70,6 +70,11 @@ class EngineConfig:
     timing: bool = False
     devices: Optional[Sequence[int]] = None  # clause shards, one engine per entry (default: [device])
     chunk_filter: bool = False  # multi-chunk rounds: chunk-level aggregate sweep first
+    # > 0: the rounds' records go through a page-locked host ring of this many
+    # records, drained by CPU threads while the kernel runs (tsg_ring_*,
+    # DESIGN.md §4.4), and are put in delivery order on the host -- for rounds
+    # with few reports; 0: device record buffer, ordered on the GPU
+    report_ring: int = 0
 
     def __post_init__(self):
         if self.max_clauses < 1:
@@ -84,6 +89,10 @@ class EngineConfig:
             raise ValueError("assignment_queue_capacity must be >= 1")
         if self.devices is not None and len(self.devices) < 1:
             raise ValueError("devices must name at least one GPU")
+        if self.report_ring < 0:
+            raise ValueError("report_ring must be >= 0")
+        if self.report_ring and self.lane_width > 32:
+            raise ValueError("report_ring carries 32-bit lane masks: lane_width must be <= 32")
 
 
 @dataclass
@@ -430,6 +439,12 @@ class Engine:
                                      chunk_filter=self.config.chunk_filter)
                         for d in devices]
         self._h = self._shards[0].h  # the first shard: staging, encode, record ordering
+        self._drainers: List[RingDrainer] = []  # report_ring: one drainer thread per shard
+        self._shard_reports: List[int] = []     # the last round's records per shard
+        if self.config.report_ring:
+            for s in self._shards:
+                s.ring_open(self.config.report_ring)
+                self._drainers.append(RingDrainer(s, threads=1))
         w = C.c_int64(0)
         check(self._L.tsg_packed_words(num_vars, C.byref(w)))
         self._packed_words = w.value
@@ -464,6 +479,11 @@ class Engine:
         self.trace: List[RoundTrace] = []
 
     def close(self) -> None:
+        for d in getattr(self, "_drainers", []):
+            d.close()
+        for s in getattr(self, "_shards", []) if getattr(self, "_drainers", None) else []:
+            s.ring_close()
+        self._drainers = []
         for q in getattr(self, "_squeues", {}).values():
             q.close()
         if getattr(self, "_pinned", None) is not None:
@@ -722,7 +742,10 @@ class Engine:
             result.clauses_tested = res.clauses_tested
             result.aggregate_tests_negative = res.aggregate_tests_negative
             if res.reports:
-                eids, masks, groups, counts, keep = self._fetch_ordered(res.reports, len(pending))
+                if self._drainers:
+                    eids, masks, groups, counts, keep = self._ring_ordered(gt, [t for t, _, _, _, _ in pending])
+                else:
+                    eids, masks, groups, counts, keep = self._fetch_ordered(res.reports, len(pending))
                 ph["order_fetch"] = time.perf_counter()
                 arena = self._arena.snapshot()  # literals as of this round (a later reduce may drop the clause)
                 cut = np.concatenate([[0], np.cumsum(counts)])
@@ -784,6 +807,7 @@ class Engine:
         for s in self._shards:
             s.launch(self._activity_inc)
         rs = [s.collect() for s in self._shards]
+        self._shard_reports = [r.reports for r in rs]
         res = rs[0]
         for r in rs[1:]:
             for f in ("reports", "clauses_tested", "aggregate_tests", "aggregate_tests_negative", "lane_tests",
@@ -811,6 +835,21 @@ class Engine:
                                         C.c_void_p(base), eid_bytes, C.c_void_p(base + e_sec), mask_bytes,
                                         ptr(groups), ptr(counts), n, C.byref(got)))
         return eids[:got.value], masks[:got.value], groups, counts[:n_dest], buf
+
+    def _ring_ordered(self, gt: np.ndarray, dests: List[int]):
+        """The round's records from the shards' host rings (drained by their
+        threads while the kernels ran), put in the delivery order
+        tsg_fetch_ordered produces on the GPU: destination, chunk, bucket
+        creation rank, engine id, group (engine.py:403-464)."""
+        parts = [d.take(n) for d, n in zip(self._drainers, self._shard_reports) if n]
+        raw = np.concatenate(parts) if len(parts) > 1 else parts[0]
+        eid = (raw["key"] >> np.uint64(16)).astype(np.int64)
+        grp = (raw["key"] & np.uint64(0xFFFF)).astype(np.int32)
+        dest = np.searchsorted(np.asarray(dests, np.int64), gt[grp].astype(np.int64))
+        rank = self._rank_of_size[self._arena.size[eid]]
+        order = np.lexsort((grp, eid, rank, grp // self.config.group_width, dest))
+        counts = np.bincount(dest, minlength=len(dests)).astype(np.int64)
+        return eid[order], raw["lane_mask"][order], grp[order], counts, None
 
     def reduce_store(self) -> int:
         """engine.py:469-505; selection and compaction run on the GPU(s),

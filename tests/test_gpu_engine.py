@@ -24,8 +24,9 @@ def P():
     return P
 
 
-def replay(P, spec, devices=None):
-    eng = P.Engine(spec["num_vars"], spec["threads"], P.EngineConfig(**spec["config"], devices=devices))
+def replay(P, spec, devices=None, report_ring=0):
+    eng = P.Engine(spec["num_vars"], spec["threads"], P.EngineConfig(**spec["config"], devices=devices,
+                                                                     report_ring=report_ring))
     for op, exp in zip(spec["ops"], spec["expect"]):
         if op[0] == "add":
             assert eng.add_clause(op[1], origin=op[2]) == exp["id"]
@@ -58,6 +59,20 @@ def replay(P, spec, devices=None):
 def test_reference_scenarios_bit_exact(P, devices):
     for spec in engine_golden():
         replay(P, spec, devices)
+
+
+# the records through the host report ring (drainer threads, host ordering)
+# instead of the device buffer: the same reference results (the ring carries
+# 32-bit lane masks, so the width-64 scenarios are not eligible)
+@pytest.mark.parametrize("devices", [None, [0, 0]])
+def test_reference_scenarios_through_the_report_ring(P, devices):
+    n = 0
+    for spec in engine_golden():
+        if spec["config"].get("lane_width", 32) > 32:
+            continue
+        replay(P, spec, devices, report_ring=256)
+        n += 1
+    assert n >= 10
 
 
 # ---- ported from the reference's tests/test_engine.py ---------------------

@@ -33,9 +33,10 @@ def X():
     return X
 
 
-@pytest.mark.parametrize("name,devices,chunk_filter", [("w32", None, False), ("w8x2", None, False),
-                                                       ("w8x2", None, True), ("w8x2", [0, 0], True)])
-def test_replay_reference_solver_rounds(name, devices, chunk_filter):
+@pytest.mark.parametrize("name,devices,chunk_filter,ring", [("w32", None, False, 0), ("w8x2", None, False, 0),
+                                                            ("w8x2", None, True, 0), ("w8x2", [0, 0], True, 0),
+                                                            ("w32", None, False, 1024), ("w8x2", [0, 0], False, 128)])
+def test_replay_reference_solver_rounds(name, devices, chunk_filter, ring):
     # every recorded round rebuilt on the GPU Engine through the reference API:
     # the same clauses under the same engine ids (inserted in id order, so the
     # size buckets are created in the reference's order), the round's
@@ -51,7 +52,7 @@ def test_replay_reference_solver_rounds(name, devices, chunk_filter):
     for k in range(int(fx["rounds"])):
         clauses, live, snaps, reps, result = c5_round(fx, k)
         eng = P.Engine(nv, th, P.EngineConfig(lane_width=lw, group_width=gw, devices=devices,
-                                              chunk_filter=chunk_filter))
+                                              chunk_filter=chunk_filter, report_ring=ring))
         for lits in clauses:
             eng.add_clause(lits, origin=0)
         eng.run_round()  # integrate (no snapshots: no activity or counter effects)
