@@ -847,7 +847,16 @@ class Engine:
         grp = (raw["key"] & np.uint64(0xFFFF)).astype(np.int32)
         dest = np.searchsorted(np.asarray(dests, np.int64), gt[grp].astype(np.int64))
         rank = self._rank_of_size[self._arena.size[eid]]
-        order = np.lexsort((grp, eid, rank, grp // self.config.group_width, dest))
+        chunk = grp // self.config.group_width
+        fields = (dest, chunk, rank, eid, grp)  # most significant first
+        widths = [max(int(f.max()), 0).bit_length() for f in fields]
+        if sum(widths) <= 64:  # one packed key (unique per record), as the GPU ordering packs it
+            key = np.zeros(len(eid), np.uint64)
+            for f, w in zip(fields, widths):
+                key = (key << np.uint64(w)) | f.astype(np.uint64)
+            order = np.argsort(key)
+        else:
+            order = np.lexsort(fields[::-1])
         counts = np.bincount(dest, minlength=len(dests)).astype(np.int64)
         return eid[order], raw["lane_mask"][order], grp[order], counts, None
 

@@ -8,7 +8,9 @@ all records on the host), in two egress modes:
           CPU threads (RingDrainer) while the kernel runs
 
 Reports the median wall ms per round (until the host holds every record),
-the trigger kernel's event time in each mode and the record count.
+the trigger kernel's event time in each mode and the record count; then
+the same comparison through the drop-in Engine.run_round (EngineConfig
+report_ring) for the configs other than C3.
 
     python tools/ring_probe.py [C1,C2,C3] [rounds=20] > gpurun_out/ring_probe.json
 """
@@ -110,6 +112,43 @@ def probe(name):
     return out
 
 
+
+
+def api_probe(name, rounds=30):
+    """Engine.run_round (the drop-in API) with the device record buffer vs the
+    report ring: median ms per round."""
+    import paper_2012_03119_b200 as P
+    cfg = W.CONFIGS[name]
+    out = {"config": name, "api": True}
+    for ring in (0, 1 << 16):
+        rng = np.random.default_rng(cfg.seed)
+        flat, offs, _ = W.flatten(W.clause_buckets(cfg.n_clauses, cfg.num_vars, rng))
+        eng = P.Engine(cfg.num_vars, cfg.threads, P.EngineConfig(max_clauses=2 * cfg.n_clauses, report_ring=ring,
+                                                                assignment_queue_capacity=cfg.lanes))
+        eng.add_clauses(flat, offs)
+        eng.run_round()
+        snaps = W.snapshots(cfg.threads, cfg.lanes, cfg.num_vars, np.random.default_rng(cfg.seed + 999))
+        ms, reps = [], 0
+        for r in range(rounds + 3):
+            for i in range(snaps.shape[0]):
+                eng.submit_assignment(P.AssignmentSnapshot(i // cfg.lanes, snaps[i], i))
+            t0 = time.perf_counter()
+            res = eng.run_round()
+            t1 = time.perf_counter()
+            for t in range(cfg.threads):
+                eng.drain_reports(t)
+            if r >= 3:
+                ms.append((t1 - t0) * 1e3)
+            reps = res.reports_emitted
+        out["ring" if ring else "buffer"] = {"run_round_ms": float(np.median(ms))}
+        out["reports_per_round"] = reps
+        eng.close()
+    return out
+
+
 if __name__ == "__main__":
     for n in names:
         print(json.dumps(probe(n)), flush=True)
+    for n in names:
+        if n != "C3":
+            print(json.dumps(api_probe(n)), flush=True)
