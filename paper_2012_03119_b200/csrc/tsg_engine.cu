@@ -484,7 +484,7 @@ int launch_test(tsg_engine* h, int k, int emit_only) {
         p.out_cap = 0;
         p.ring = RingDesc{h->ring.d_slots, h->ring.d_pos, h->ring.d_ctl, h->ring.d_ctl + 1,
                           (unsigned long long)(h->ring.cap - 1), (unsigned long long)h->ring.wait_ns,
-                          h->ring.shift};
+                          ((volatile unsigned long long*)h->ring.ctl)[0], h->ring.shift};
     }
     const bool multi = rd.n_chunks > 1;
     auto* fn = multi ? k_test<LW, GW, true> : k_test<LW, GW, false>;

@@ -501,6 +501,8 @@ struct RingDesc {
     unsigned long long* fail;                  // host-mapped: set when a flush gave up waiting for room
     unsigned long long mask;                   // cap - 1 (cap a power of two, >= RECBUF)
     unsigned long long wait_ns;                // longest wait for room, per flush
+    unsigned long long tail0;                  // the drainers' tail when the launch was queued (a lower
+                                               // bound: flushes read the host copy only past it)
     int32_t shift;                             // log2(cap)
 };
 
@@ -706,6 +708,10 @@ struct RecBuf {
                 reinterpret_cast<ulonglong2*>(r.slots)[q & r.mask] =
                     make_ulonglong2(tag | (rec.x >> 16), tag | ((rec.x & 0xFFFFull) << 32) | (rec.y & 0xFFFFFFFFull));
             }
+            // the writers' records reach the system before anything they do
+            // after -- in particular before their CTA reports itself done and
+            // the launch's last CTA publishes the record count
+            __threadfence_system();
         }
         __syncwarp();
         n = 0;
@@ -786,7 +792,7 @@ k_test(const __grid_constant__ TestParams<LW, GW> p) {
     const int warp = threadIdx.x >> 5;
     const int nwarps = (int)(((int64_t)gridDim.x * TEST_THREADS) >> 5);
     RecBuf rb{s_rec + (size_t)warp * test_rec_stride(p.rec8), p.rec8};
-    if (lane == 0 && p.ring.slots) *reinterpret_cast<unsigned long long*>(rb.buf + RECBUF * 16) = 0;
+    if (lane == 0 && p.ring.slots) *reinterpret_cast<unsigned long long*>(rb.buf + RECBUF * 16) = p.ring.tail0;
     unsigned int pos_acc = 0, trig_acc = 0, top_acc = 0;
     const uint32_t top_mask = MULTI ? width_mask<uint32_t>((p.n_chunks + p.per_bit - 1) / p.per_bit) : 1u;
     // single-chunk rounds (<= 64 groups): the group table in shared memory
@@ -917,7 +923,6 @@ k_test(const __grid_constant__ TestParams<LW, GW> p) {
         cur = nxt;
     }
     if (rb.n) rb.flush(p.out, p.out_cap, p.ctr, p.ring, lane);
-    if (p.ring.slots) __threadfence_system();  // ring records visible before the counters are published
 
     // counters: warp reduce, block reduce, one atomic per block
     pos_acc = __reduce_add_sync(0xffffffffu, pos_acc);

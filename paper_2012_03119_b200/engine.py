@@ -799,6 +799,10 @@ class Engine:
         """Prepare on every shard, encode on the first, copy its tables to the
         others over NVLink, launch all, collect all; the figures summed."""
         s0 = self._shards[0]
+        if len(self._shards) == 1:  # one C call: prepare + encode + launch + collect
+            res = s0.round(gl, gt, self._activity_inc)
+            self._shard_reports = [res.reports]
+            return res
         for s in self._shards:
             s.prepare(gl, gt)
         s0.encode()
