@@ -577,7 +577,8 @@ std::vector<int64_t> bucket_bases(tsg_engine* h, int64_t* flat) {
     return base;
 }
 
-void ring_free(tsg_engine* h);  // the host report ring (end of file)
+void ring_free(tsg_engine* h);      // the host report ring (end of file)
+void ring_shutdown(tsg_engine* h);
 
 void select_free(tsg_engine* h) {
     auto& S = h->sel;
@@ -777,7 +778,7 @@ int tsg_destroy(tsg_engine* h) {
     if (!h) return TSG_OK;
     DevGuard g(h->dev);
     if (h->st) select_free(h);
-    if (h->st) ring_free(h);
+    if (h->st) ring_shutdown(h);
     if (h->st) cudaStreamSynchronize(h->st);
     if (h->ingress) cudaStreamSynchronize(h->ingress);
     if (h->egress) cudaStreamSynchronize(h->egress);
@@ -2278,15 +2279,15 @@ int tsg_ring_open(tsg_engine* h, int64_t capacity, int64_t wait_us) {
     return TSG_OK;
 }
 
-int tsg_ring_close(tsg_engine* h) {
-    CKR(validate_handle(h));
-    if (any_inflight(h)) return fail(TSG_EINVAL, "a launched round is not collected");
-    DevGuard g(h->dev);
+namespace {
+// close the ring once no drainer is inside tsg_ring_drain: new drain calls
+// fail at once, the ones inside return (their waits end on `closing`)
+void ring_shutdown(tsg_engine* h) {
     auto& r = h->ring;
     {
         std::lock_guard<std::mutex> lk(r.mtx);
-        if (!r.slots) return TSG_OK;
-        r.closing = true;  // new drain calls fail; the ones inside finish (their waits are bounded)
+        if (!r.slots) return;
+        r.closing = true;
     }
     for (;;) {
         {
@@ -2294,11 +2295,20 @@ int tsg_ring_close(tsg_engine* h) {
             if (r.active == 0) {
                 ring_free(h);
                 r.closing = false;
-                return TSG_OK;
+                return;
             }
         }
         std::this_thread::sleep_for(std::chrono::microseconds(50));
     }
+}
+}  // namespace
+
+int tsg_ring_close(tsg_engine* h) {
+    CKR(validate_handle(h));
+    if (any_inflight(h)) return fail(TSG_EINVAL, "a launched round is not collected");
+    DevGuard g(h->dev);
+    ring_shutdown(h);
+    return TSG_OK;
 }
 
 namespace {
