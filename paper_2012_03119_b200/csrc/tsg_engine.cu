@@ -189,6 +189,9 @@ struct tsg_engine {
     int64_t size_of_id_cap = 0;
     bool oob = false;               // a stored literal may exceed num_vars (checked before testing)
     int64_t round_seq = 0;
+    uint8_t* ord_host = nullptr;    // tsg_fetch_ordered small-round scratch: page-locked host ...
+    uint8_t* ord_dev = nullptr;     // ... and device, same size
+    int64_t ord_cap = 0;
     uint8_t* add_host = nullptr;    // page-locked staging block of tsg_add_clauses (streaming batches)
     int64_t add_host_cap = 0;
     cudaEvent_t ev_add = nullptr;   // its last copy
@@ -787,11 +790,13 @@ int tsg_destroy(tsg_engine* h) {
         dfree(h, h->rows_own); dfree(h, h->pbuf[0]); dfree(h, h->pbuf[1]); dfree(h, h->tables); dfree(h, h->d_desc);
         dfree(h, h->mctr);
         dfree(h, h->size_of_id);
+        dfree(h, h->ord_dev);
         for (auto& R : h->rs) { dfree(h, R.ctr); dfree(h, R.out); dfree(h, R.out12); dfree(h, R.d_groups); }
         cudaStreamSynchronize(h->st);
     }
     if (h->h_mctr) cudaFreeHost(h->h_mctr);
     if (h->add_host) cudaFreeHost(h->add_host);
+    if (h->ord_host) cudaFreeHost(h->ord_host);
     if (h->ev_add) cudaEventDestroy(h->ev_add);
     for (auto& R : h->rs) {
         if (R.h_ctr) cudaFreeHost(R.h_ctr);
@@ -959,6 +964,7 @@ int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, 
         if (total_bytes > h->add_host_cap) {
             const int64_t cap = std::max<int64_t>({total_bytes, 2 * h->add_host_cap, (int64_t)1 << 20});
             if (h->add_host) cudaFreeHost(h->add_host);
+    if (h->ord_host) cudaFreeHost(h->ord_host);
             h->add_host = nullptr;
             h->add_host_cap = 0;
             CK(cudaHostAlloc((void**)&h->add_host, (size_t)cap, cudaHostAllocPortable));
@@ -2077,6 +2083,8 @@ int bits_for(int64_t max_value) {  // bits to hold 0..max_value
 // (stable LSD radix sort, tsg_sort.cuh) and written into the host arrays:
 // eids (eid_bytes 4 or 8), masks (mask_bytes 4 or 8), and per destination
 // the record count (dest_counts[d], d = index of the thread's run of groups).
+constexpr int64_t SMALL_ORDER_MAX = 16384;  // records ordered on the host below this (tsg_fetch_ordered)
+
 int tsg_fetch_ordered(tsg_engine* const* hs, int32_t n_h, const int32_t* rank_of_size, int32_t n_sizes,
                       void* eids, int32_t eid_bytes, void* masks, int32_t mask_bytes, int32_t* groups,
                       int64_t* dest_counts, int64_t cap, int64_t* n) {
@@ -2123,6 +2131,69 @@ int tsg_fetch_ordered(tsg_engine* const* hs, int32_t n_h, const int32_t* rank_of
     std::vector<uint64_t> gkey(rd.n_groups);
     for (int g = 0; g < rd.n_groups; ++g) gkey[g] = ((uint64_t)dest_of[g] << chunk_bits) | (uint64_t)(g / gw);
     const int64_t rec_bytes = rec8 ? 8 : 16;
+    if (n_h == 1 && total <= SMALL_ORDER_MAX) {
+        // a small round: the keys from the device (one launch), then keys and
+        // records copied out together and sorted on the host -- the radix
+        // pipeline's ~20 launches cost more than the sort itself here
+        DevGuard g1(h0->dev);
+        const auto& R = h0->rs[h0->fetch_rs];
+        // persistent scratch (page-locked host, device): group keys and size
+        // ranks up, keys and records down, all asynchronous, one sync
+        const int64_t o_rank = round_up((int64_t)rd.n_groups * 8, 16), o_keys = o_rank + round_up((int64_t)n_sizes * 4, 16);
+        const int64_t o_recs = o_keys + round_up(total * 8, 16), o_vals = o_recs + round_up(total * rec_bytes, 16);
+        const int64_t need = o_vals + round_up(total * 4, 16);
+        if (need > h0->ord_cap) {
+            CK(cudaStreamSynchronize(h0->st));
+            if (h0->ord_host) cudaFreeHost(h0->ord_host);
+            h0->ord_host = nullptr;
+            dfree(h0, h0->ord_dev);
+            h0->ord_dev = nullptr;
+            h0->ord_cap = 0;
+            const int64_t cap = std::max<int64_t>(need * 2, (int64_t)1 << 20);
+            CK(cudaHostAlloc((void**)&h0->ord_host, (size_t)cap, cudaHostAllocPortable));
+            CKR(dalloc(h0, (void**)&h0->ord_dev, cap));
+            h0->ord_cap = cap;
+        }
+        uint8_t* hb = h0->ord_host;
+        uint8_t* db = h0->ord_dev;
+        memcpy(hb, gkey.data(), (size_t)rd.n_groups * 8);
+        memcpy(hb + o_rank, rank_of_size, (size_t)n_sizes * 4);
+        CK(cudaMemcpyAsync(db, hb, o_keys, cudaMemcpyHostToDevice, h0->st));
+        OrderKey ok{reinterpret_cast<const uint64_t*>(db), h0->size_of_id, reinterpret_cast<const int32_t*>(db + o_rank),
+                    n_sizes, rank_bits, id_bits, g_bits, gw, rec8 ? 1 : 0};
+        k_order_keys<<<grid_for(total), 256, 0, h0->st>>>(R.out, total, 0, ok, reinterpret_cast<uint64_t*>(db + o_keys),
+                                                         reinterpret_cast<uint32_t*>(db + o_vals));
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(hb + o_keys, db + o_keys, total * 8, cudaMemcpyDeviceToHost, h0->st));
+        CK(cudaMemcpyAsync(hb + o_recs, R.out, total * rec_bytes, cudaMemcpyDeviceToHost, h0->st));
+        CK(cudaStreamSynchronize(h0->st));
+        const uint64_t* keys = reinterpret_cast<const uint64_t*>(hb + o_keys);
+        const uint8_t* recs = hb + o_recs;
+        std::vector<uint32_t> idx((size_t)total);
+        for (uint32_t i = 0; i < (uint32_t)total; ++i) idx[i] = i;
+        std::sort(idx.begin(), idx.end(), [&](uint32_t a, uint32_t b) { return keys[a] < keys[b]; });
+        for (int64_t j = 0; j < total; ++j) {
+            const uint32_t i = idx[j];
+            uint64_t eid, mask;
+            int32_t grp;
+            if (rec8) {
+                uint64_t x;
+                memcpy(&x, recs + (size_t)i * 8, 8);
+                eid = x >> 37; grp = (int32_t)((x >> 32) & 31u); mask = x & 0xFFFFFFFFull;
+            } else {
+                tsg_report r;
+                memcpy(&r, recs + (size_t)i * 16, 16);
+                eid = r.key >> 16; grp = (int32_t)(r.key & 0xFFFFu); mask = r.lane_mask;
+            }
+            if (eid_bytes == 4) static_cast<int32_t*>(eids)[j] = (int32_t)eid;
+            else static_cast<int64_t*>(eids)[j] = (int64_t)eid;
+            if (mask_bytes == 4) static_cast<uint32_t*>(masks)[j] = (uint32_t)mask;
+            else static_cast<uint64_t*>(masks)[j] = mask;
+            if (groups) groups[j] = grp;
+            ++dest_counts[(int64_t)(keys[i] >> low_bits)];
+        }
+        return TSG_OK;
+    }
     // device 0: concatenated records (several shards), keys / vals double buffers
     DevGuard g0(h0->dev);
     uint8_t* recs = nullptr;

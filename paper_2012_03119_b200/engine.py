@@ -44,6 +44,7 @@ from typing import Dict, List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _lib
+from . import reports as _reports
 from . import sharded as _sharded
 from ._lib import check, ptr
 from .native import NativeEngine, RingDrainer
@@ -742,8 +743,9 @@ class Engine:
             result.clauses_tested = res.clauses_tested
             result.aggregate_tests_negative = res.aggregate_tests_negative
             if res.reports:
+                dests = [t for t, _, _, _, _ in pending]
                 if self._drainers:
-                    eids, masks, groups, counts, keep = self._ring_ordered(gt, [t for t, _, _, _, _ in pending])
+                    eids, masks, groups, counts, keep = self._ring_ordered(gt, dests)
                 else:
                     eids, masks, groups, counts, keep = self._fetch_ordered(res.reports, len(pending))
                 ph["order_fetch"] = time.perf_counter()
@@ -846,9 +848,12 @@ class Engine:
         tsg_fetch_ordered produces on the GPU: destination, chunk, bucket
         creation rank, engine id, group (engine.py:403-464)."""
         parts = [d.take(n) for d, n in zip(self._drainers, self._shard_reports) if n]
-        raw = np.concatenate(parts) if len(parts) > 1 else parts[0]
-        eid = (raw["key"] >> np.uint64(16)).astype(np.int64)
-        grp = (raw["key"] & np.uint64(0xFFFF)).astype(np.int32)
+        return self._host_ordered(_reports.decode(np.concatenate(parts) if len(parts) > 1 else parts[0]), gt, dests)
+
+    def _host_ordered(self, dec: np.ndarray, gt: np.ndarray, dests: List[int]):
+        """Decoded records (reports.decode) in delivery order, on the host."""
+        eid = dec["engine_id"].astype(np.int64)
+        grp = dec["group"].astype(np.int32)
         dest = np.searchsorted(np.asarray(dests, np.int64), gt[grp].astype(np.int64))
         rank = self._rank_of_size[self._arena.size[eid]]
         chunk = grp // self.config.group_width
@@ -862,7 +867,7 @@ class Engine:
         else:
             order = np.lexsort(fields[::-1])
         counts = np.bincount(dest, minlength=len(dests)).astype(np.int64)
-        return eid[order], raw["lane_mask"][order], grp[order], counts, None
+        return eid[order], dec["lane_mask"][order], grp[order], counts, None
 
     def reduce_store(self) -> int:
         """engine.py:469-505; selection and compaction run on the GPU(s),

@@ -3,7 +3,8 @@ LSD radix sort, tsg_sort.cuh) against the host ordering of the same records
 (reports.reference_order, numpy lexsort): destination-major, then chunk,
 bucket creation rank, engine id, group -- the reference's delivery order
 (engine.py:403-414, 462-464) -- at sizes where the sort runs many blocks and
-every key width is exercised."""
+every key width is exercised; small rounds take the host-sort path of the
+same call."""
 import ctypes as C
 
 import numpy as np
@@ -19,6 +20,10 @@ pytestmark = pytest.mark.gpu
     (200_000, 3000, 5, 70, 32, 4, 16),      # 16-byte records, 3 chunks, threads spanning chunks
     (60_000, 500, 3, 90, 64, 64, 16),       # 64-bit lane masks
     (2_000_000, 50_000, 8, 32, 32, 32, 8),  # C2-sized store
+    # small rounds (<= 16384 records): keys from the device, sorted on the host
+    (20_000, 2000, 3, 32, 32, 32, 8),
+    (20_000, 2000, 3, 40, 32, 4, 16),
+    (8_000, 500, 2, 70, 64, 64, 16),
 ])
 def test_device_order_matches_host_order(n, nv, threads, lanes, lw, gw, rec):
     require_device()
