@@ -669,8 +669,14 @@ __device__ __forceinline__ LW lane_test(const LaneEntry<LW>* lt, const ROWS& r, 
 // buffered form that issues the atomic one half-buffer early measured
 // slower: profiles/r02_k_test_variants.md.)
 struct RecBuf {
-    unsigned char* buf;
+    uint32_t off;  // this warp's buffer: byte offset into the dynamic shared memory
     int rec8;
+    // (addressed through the shared array itself, not a generic pointer,
+    // so the stores are plain STS with no shared-window base recomputed)
+    __device__ __forceinline__ unsigned char* buf() const {
+        extern __shared__ __align__(16) unsigned char s_rec[];
+        return s_rec + off;
+    }
     int n = 0;
     // ring form of flush (lane width <= 32, 16-byte records in `buf`)
     __device__ __forceinline__ void flush_ring(unsigned long long* ctr, const RingDesc& r, int lane) {
@@ -678,7 +684,7 @@ struct RecBuf {
         int ok = 1;
         if (lane == 0) {
             // the drainer's progress as last read, kept after this warp's records (test_smem_bytes)
-            unsigned long long& tail_seen = *reinterpret_cast<unsigned long long*>(buf + RECBUF * 16);
+            unsigned long long& tail_seen = *reinterpret_cast<unsigned long long*>(buf() + RECBUF * 16);
             base = atomicAdd(r.pos, (unsigned long long)n);
             atomicAdd(ctr, (unsigned long long)n);
             const unsigned long long cap = r.mask + 1;
@@ -700,7 +706,7 @@ struct RecBuf {
         ok = __shfl_sync(0xffffffffu, ok, 0);
         if (ok) {
             for (int i = lane; i < n; i += 32) {
-                const ulonglong2 rec = reinterpret_cast<const ulonglong2*>(buf)[i];
+                const ulonglong2 rec = reinterpret_cast<const ulonglong2*>(buf())[i];
                 const unsigned long long q = base + (unsigned long long)i;
                 const unsigned long long tag = ring_tag(q, r.shift) << 48;
                 // id | group, lane mask: both words tagged, one 16-byte store (a warp
@@ -729,8 +735,8 @@ struct RecBuf {
         for (int i = lane; i < n; i += 32) {
             const unsigned long long q = base + (unsigned long long)i;
             if (q < cap) {  // past the capacity only counted: the host grows the buffer and replays
-                if (rec8) reinterpret_cast<uint64_t*>(out)[q] = reinterpret_cast<const uint64_t*>(buf)[i];
-                else reinterpret_cast<ulonglong2*>(out)[q] = reinterpret_cast<const ulonglong2*>(buf)[i];
+                if (rec8) reinterpret_cast<uint64_t*>(out)[q] = reinterpret_cast<const uint64_t*>(buf())[i];
+                else reinterpret_cast<ulonglong2*>(out)[q] = reinterpret_cast<const ulonglong2*>(buf())[i];
             }
         }
         __syncwarp();
@@ -742,8 +748,8 @@ struct RecBuf {
         const unsigned b = __ballot_sync(0xffffffffu, has);
         if (has) {
             const int i = n + __popc(b & ((1u << lane) - 1u));
-            if (rec8) reinterpret_cast<uint64_t*>(buf)[i] = rec.x;
-            else reinterpret_cast<ulonglong2*>(buf)[i] = rec;
+            if (rec8) reinterpret_cast<uint64_t*>(buf())[i] = rec.x;
+            else reinterpret_cast<ulonglong2*>(buf())[i] = rec;
         }
         n += __popc(b);
         if (n > RECBUF - 32) flush(out, cap, ctr, ring, lane);
@@ -791,18 +797,23 @@ k_test(const __grid_constant__ TestParams<LW, GW> p) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int nwarps = (int)(((int64_t)gridDim.x * TEST_THREADS) >> 5);
-    RecBuf rb{s_rec + (size_t)warp * test_rec_stride(p.rec8), p.rec8};
-    if (lane == 0 && p.ring.slots) *reinterpret_cast<unsigned long long*>(rb.buf + RECBUF * 16) = p.ring.tail0;
+    RecBuf rb{(uint32_t)(warp * test_rec_stride(p.rec8)), p.rec8};
+    if (lane == 0 && p.ring.slots) *reinterpret_cast<unsigned long long*>(rb.buf() + RECBUF * 16) = p.ring.tail0;
     unsigned int pos_acc = 0, trig_acc = 0, top_acc = 0;
     const uint32_t top_mask = MULTI ? width_mask<uint32_t>((p.n_chunks + p.per_bit - 1) / p.per_bit) : 1u;
     // single-chunk rounds (<= 64 groups): the group table in shared memory
-    const GroupDesc* groups = p.groups;
+    // (read through group(i): a direct shared-memory access in single-chunk
+    // rounds -- a generic pointer would recompute the shared window's base
+    // on every stage-2 iteration)
+    __shared__ GroupDesc s_groups[MULTI ? 1 : MAXG];
     if constexpr (!MULTI) {
-        __shared__ GroupDesc s_groups[MAXG];
         for (int i = threadIdx.x; i < p.n_groups; i += TEST_THREADS) s_groups[i] = p.groups[i];
         __syncthreads();
-        groups = s_groups;
     }
+    auto group = [&](int i) -> const GroupDesc& {
+        if constexpr (MULTI) return p.groups[i];
+        else return s_groups[i];
+    };
 
     int tile = (int)(((int64_t)blockIdx.x * TEST_THREADS + threadIdx.x) >> 5);
     int bi = 0, nt0 = 0;
@@ -864,7 +875,7 @@ k_test(const __grid_constant__ TestParams<LW, GW> p) {
                         act = __dadd_rn(act, __dmul_rn(p.inc, (double)hits));
                         touched = true;
                     }
-                    const int tid = groups[g0 + g].tid;
+                    const int tid = group(g0 + g).tid;
                     if (p.all_pairs || tid != last_tid) {  // first triggering group of its thread
                         last_tid = tid;
                         has = true;
@@ -884,8 +895,11 @@ k_test(const __grid_constant__ TestParams<LW, GW> p) {
                     if (left != GW(0)) {
                         const int g = __ffsll((long long)(unsigned long long)left) - 1;
                         left &= left - GW(1);
-                        settle(g, lane_test<LW>(lanes + (int64_t)g * p.vstride, cur, lp, size) &
-                                      (LW)groups[g0 + g].lane_mask, has, rec);
+                        // the group's lane table, addressed once (kept opaque, so the
+                        // literals' loads do not each redo the 64-bit g * vstride)
+                        const LaneEntry<LW>* lt = lanes + (int64_t)g * p.vstride;
+                        asm volatile("" : "+l"(lt));
+                        settle(g, lane_test<LW>(lt, cur, lp, size) & (LW)group(g0 + g).lane_mask, has, rec);
                     }
 #ifndef TSG_ABL_NO_RECORDS  // ablation timing only (wrong results)
                     rb.append(has, rec, p.out, p.out_cap, p.ctr, p.ring, lane);
