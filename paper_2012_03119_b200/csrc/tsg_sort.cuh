@@ -15,7 +15,7 @@
 namespace tsg {
 
 constexpr int SORT_THREADS = 256;
-constexpr int SORT_ITEMS = 16;                          // items per thread per block
+constexpr int SORT_ITEMS = 8;                           // items per thread per block
 constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;    // items per block
 
 // Key layout of one round (host-computed): key = ((((gkey[g] << rank_bits) |
@@ -152,19 +152,39 @@ __global__ void __launch_bounds__(1024) k_scan_add(uint32_t* __restrict__ hist, 
 // pass `shift`: stable scatter of (key, val) by digit.  Items of a block are
 // taken in SORT_ITEMS rounds of one per thread (item order = round-major,
 // then thread order), each ranked among equal digits with warp match +
-// per-warp digit counts, so the block writes every digit's items in input
-// order at its scanned offset.
+// per-warp digit counts.  They are first placed in shared memory in digit
+// order (the block's own digit histogram, scanned, gives each digit's run),
+// then written out run by run, so consecutive threads write consecutive
+// output slots -- coalesced, instead of one partial sector per item.
 __global__ void __launch_bounds__(SORT_THREADS) k_sort_scatter(const uint64_t* __restrict__ keys,
                                                                 const uint32_t* __restrict__ vals, int64_t n,
                                                                 int shift, const uint32_t* __restrict__ offs,
                                                                 uint64_t* __restrict__ keys_out,
                                                                 uint32_t* __restrict__ vals_out) {
     constexpr int WARPS = SORT_THREADS / 32;
-    __shared__ uint32_t base[256];       // next output slot per digit for this block
+    __shared__ uint32_t gbase[256];      // this block's first output slot per digit
+    __shared__ uint32_t lbase[256];      // the digit's run in the block's shared tile
+    __shared__ uint32_t next[256];       // next free slot of the digit's run
     __shared__ uint32_t wc[WARPS][256];  // per-warp digit counts of the current round
+    __shared__ uint32_t wsum[33];
+    __shared__ uint64_t skey[SORT_TILE];
+    __shared__ uint32_t sval[SORT_TILE];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    base[threadIdx.x] = offs[(int64_t)threadIdx.x * gridDim.x + blockIdx.x];
     const int64_t b0 = (int64_t)blockIdx.x * SORT_TILE;
+    const int cnt = (int)(n - b0 < SORT_TILE ? n - b0 : SORT_TILE);
+    next[threadIdx.x] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < SORT_ITEMS; ++r) {
+        const int64_t i = b0 + (int64_t)r * SORT_THREADS + threadIdx.x;
+        if (i < n) atomicAdd(&next[(keys[i] >> shift) & 0xFF], 1u);
+    }
+    __syncthreads();
+    uint32_t total;
+    const uint32_t ex = block_excl_scan(next[threadIdx.x], wsum, total);
+    lbase[threadIdx.x] = ex;
+    next[threadIdx.x] = ex;
+    gbase[threadIdx.x] = offs[(int64_t)threadIdx.x * gridDim.x + blockIdx.x];
     for (int r = 0; r < SORT_ITEMS; ++r) {
 #pragma unroll
         for (int k = 0; k < WARPS; ++k) wc[k][threadIdx.x] = 0;
@@ -172,7 +192,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_sort_scatter(const uint64_t* _
         const int64_t i = b0 + (int64_t)r * SORT_THREADS + threadIdx.x;
         const bool ok = i < n;
         uint64_t key = 0;
-        uint32_t d = 256u + lane;  // out of range items: a digit of their own (never written)
+        uint32_t d = 256u + lane;  // out of range items: a digit of their own (never placed)
         if (ok) {
             key = keys[i];
             d = (uint32_t)(key >> shift) & 0xFFu;
@@ -182,17 +202,24 @@ __global__ void __launch_bounds__(SORT_THREADS) k_sort_scatter(const uint64_t* _
         if (ok && before == 0) wc[w][d] = __popc(peers);
         __syncthreads();
         if (ok) {
-            uint32_t pos = base[d] + before;
+            uint32_t pos = next[d] + before;
             for (int k = 0; k < w; ++k) pos += wc[k][d];
-            keys_out[pos] = key;
-            vals_out[pos] = vals[i];
+            skey[pos] = key;
+            sval[pos] = vals[i];
         }
         __syncthreads();
         uint32_t t = 0;
 #pragma unroll
         for (int k = 0; k < WARPS; ++k) t += wc[k][threadIdx.x];
-        base[threadIdx.x] += t;
-        __syncthreads();
+        next[threadIdx.x] += t;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < cnt; j += SORT_THREADS) {
+        const uint64_t key = skey[j];
+        const uint32_t d = (uint32_t)(key >> shift) & 0xFFu;
+        const uint32_t pos = gbase[d] + (uint32_t)j - lbase[d];
+        keys_out[pos] = key;
+        vals_out[pos] = sval[j];
     }
 }
 
