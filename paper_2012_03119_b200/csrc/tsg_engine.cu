@@ -1400,15 +1400,18 @@ int tsg_packed_words(int32_t num_vars, int64_t* words) {
 }
 
 // SWAR pack of one row into 2-bit words (AVX2 when the host has it)
+__attribute__((target("avx2"))) static inline uint64_t pack_word_avx2(const int8_t* r) {
+    const __m256i x = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(r));
+    const uint32_t t = (uint32_t)_mm256_movemask_epi8(_mm256_cmpeq_epi8(x, _mm256_set1_epi8(1)));
+    const uint32_t z = (uint32_t)_mm256_movemask_epi8(_mm256_cmpeq_epi8(x, _mm256_setzero_si256()));
+    return (uint64_t)t | ((uint64_t)~z << 32);
+}
+
 __attribute__((target("avx2"))) static void pack_row_avx2(const int8_t* r, int64_t nv1, uint64_t* out, int64_t words) {
-    const __m256i one = _mm256_set1_epi8(1), zero = _mm256_setzero_si256();
+    // (plain stores: the packed rows stay in the last-level cache for the
+    // copy engine's read -- streaming stores measured slower in the e2e loop)
     int64_t k = 0;
-    for (; 32 * k + 32 <= nv1; ++k) {
-        const __m256i x = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(r + 32 * k));
-        const uint32_t t = (uint32_t)_mm256_movemask_epi8(_mm256_cmpeq_epi8(x, one));
-        const uint32_t z = (uint32_t)_mm256_movemask_epi8(_mm256_cmpeq_epi8(x, zero));
-        out[k] = (uint64_t)t | ((uint64_t)~z << 32);
-    }
+    for (; 32 * k + 32 <= nv1; ++k) out[k] = pack_word_avx2(r + 32 * k);
     for (; k < words; ++k) {
         uint32_t t = 0, st = 0;
         for (int64_t i = 32 * k; i < 32 * k + 32 && i < nv1; ++i) {
@@ -1439,12 +1442,19 @@ int tsg_pack_rows(const int8_t* rows, int64_t n_rows, int64_t row_pitch, int32_t
         return fail(TSG_EINVAL, "row pitch %lld < num_vars+1", (long long)row_pitch);
     if (out_pitch_words < words) return fail(TSG_EINVAL, "out pitch %lld < %lld words", (long long)out_pitch_words, (long long)words);
     static const bool avx2 = __builtin_cpu_supports("avx2");
-    for (int64_t r = 0; r < n_rows; ++r) {
-        uint64_t* o = out + r * out_pitch_words;
-        if (avx2) pack_row_avx2(rows + r * row_pitch, (int64_t)num_vars + 1, o, words);
-        else pack_row_scalar(rows + r * row_pitch, (int64_t)num_vars + 1, o, words);
-        for (int64_t k = words; k < out_pitch_words; ++k) o[k] = 0;
-    }
+    auto pack = [&](int64_t a, int64_t b) {
+        for (int64_t r = a; r < b; ++r) {
+            uint64_t* o = out + r * out_pitch_words;
+            if (avx2) pack_row_avx2(rows + r * row_pitch, (int64_t)num_vars + 1, o, words);
+            else pack_row_scalar(rows + r * row_pitch, (int64_t)num_vars + 1, o, words);
+            for (int64_t k = words; k < out_pitch_words; ++k) o[k] = 0;
+        }
+    };
+    // a round's worth of rows (the solver threads pack one row each at
+    // submit): split over the host worker pool -- the packing is bound by
+    // host memory bandwidth, which one thread cannot draw
+    const int64_t bytes = n_rows * ((int64_t)num_vars + 1);
+    HostPool::get().parallel_for(n_rows, bytes >= ((int64_t)4 << 20) ? 16 : 1, pack);
     return TSG_OK;
 }
 

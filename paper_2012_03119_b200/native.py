@@ -24,29 +24,18 @@ def packed_words(num_vars: int) -> int:
 
 def pack_rows(rows: np.ndarray, num_vars: int, out: Optional[np.ndarray] = None, threads: int = 1) -> np.ndarray:
     """int8 snapshot rows [n, >= num_vars+1] -> packed rows uint64[n, packed_words]
-    (2 bits per variable; tsg_pack_rows).  The C call releases the GIL, so
-    `threads` > 1 packs row chunks in parallel -- the way solver threads pack
-    their own snapshots."""
+    (2 bits per variable; tsg_pack_rows, GIL released).  A round's worth of
+    rows is split over the library's host worker pool inside the one call
+    (the packing is bound by host memory bandwidth); `threads` is accepted
+    for compatibility and no longer used."""
     rows = np.ascontiguousarray(rows, np.int8)
     n = rows.shape[0]
     w = packed_words(num_vars)
     if out is None:
         out = np.empty((n, w), np.uint64)
-    L = _lib.load()
-
-    def run(a, b):
-        if b > a:
-            check(L.tsg_pack_rows(C.c_void_p(rows.ctypes.data + a * rows.strides[0]), b - a, rows.strides[0],
-                                  num_vars, C.c_void_p(out.ctypes.data + a * out.strides[0]),
-                                  out.strides[0] // 8))
-
-    if threads <= 1 or n < 2 * threads:
-        run(0, n)
-    else:
-        from concurrent.futures import ThreadPoolExecutor
-        cuts = [n * i // threads for i in range(threads + 1)]
-        with ThreadPoolExecutor(threads) as ex:
-            list(ex.map(lambda i: run(cuts[i], cuts[i + 1]), range(threads)))
+    if n:
+        check(_lib.load().tsg_pack_rows(C.c_void_p(rows.ctypes.data), n, rows.strides[0], num_vars,
+                                        C.c_void_p(out.ctypes.data), out.strides[0] // 8))
     return out
 
 
