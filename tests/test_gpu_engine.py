@@ -244,6 +244,16 @@ def test_c3_shape_parity(P):
     run_both(P, n=150_000, threads=32, lanes=32, nv=200_000, seed=23)
 
 
+@pytest.mark.parametrize("lw,gw,all_pairs,chunk_filter", [(1, 64, False, False), (1, 64, True, False),
+                                                          (2, 32, False, True), (3, 8, True, True)])
+def test_many_chunks_parity(P, lw, gw, all_pairs, chunk_filter):
+    # hundreds of groups in one round: 1200 groups of one lane = 19 chunks of
+    # 64 (group indices far past 8 bits, the group table read from global
+    # memory), threads spanning chunks, with and without the chunk filter
+    run_both(P, n=6000, threads=4, lanes=300, nv=400, seed=13, lane_width=lw, group_width=gw,
+             size_lo=2, size_hi=12, all_pairs=all_pairs, chunk_filter=chunk_filter)
+
+
 def test_long_clauses_parity(P):
     # clauses far longer than the prefetched rows (and past the 58 ordered positions)
     run_both(P, n=3000, threads=4, lanes=32, nv=2000, seed=9, size_lo=100, size_hi=400)

@@ -24,6 +24,9 @@ pytestmark = pytest.mark.gpu
     (20_000, 2000, 3, 32, 32, 32, 8),
     (20_000, 2000, 3, 40, 32, 4, 16),
     (8_000, 500, 2, 70, 64, 64, 16),
+    # 1200 one-lane groups: 19 chunks, wide chunk and group fields (both paths)
+    (60_000, 600, 4, 300, 1, 64, 16),
+    (2_000, 600, 4, 300, 1, 64, 16),
 ])
 def test_device_order_matches_host_order(n, nv, threads, lanes, lw, gw, rec):
     require_device()
@@ -42,7 +45,7 @@ def test_device_order_matches_host_order(n, nv, threads, lanes, lw, gw, rec):
     gl, gt = W.groups_for(threads, lanes, lw)
     e.stage(snaps)
     r = e.round(gl, gt, 1.0)
-    assert r.reports > 1000
+    assert r.reports > 500
     # the bucket creation rank by size, shuffled: the order must follow the table passed in
     sizes = list(buckets)
     rank_of_size = np.zeros(max(sizes) + 1, np.int32)
