@@ -230,15 +230,21 @@ def scripted():
     return S
 
 
+def rand_clause_repeats(rng, nv, size):
+    """Variables drawn with replacement: repeated literals and x / -x pairs."""
+    return [rng.randint(1, nv) * (1 if rng.random() < 0.5 else -1) for _ in range(size)]
+
+
 def randomized(seed, n_rounds, nv, threads, cfg, adds_per_round, snaps_per_round, p_set, size_hi,
-               reduce_every=0, name=None):
+               reduce_every=0, name=None, repeats=False):
     rng = random.Random(seed)
     ops = []
     seq = {t: 0 for t in range(threads)}
     for r in range(n_rounds):
         for _ in range(rng.randint(*adds_per_round)):
-            size = rng.randint(0, min(size_hi, nv))
-            ops.append(["add", rand_clause(rng, nv, size), rng.randrange(threads)])
+            size = rng.randint(0, min(size_hi, nv) if not repeats else size_hi)
+            clause = rand_clause_repeats(rng, nv, size) if repeats else rand_clause(rng, nv, size)
+            ops.append(["add", clause, rng.randrange(threads)])
         for _ in range(rng.randint(*snaps_per_round)):
             t = rng.randrange(threads)
             ops.append(["submit", t, seq[t], rand_values(rng, nv, p_set)])
@@ -271,6 +277,10 @@ def engine_scenarios():
     S.append(randomized(6, 4, 40, 3, {}, (20, 60), (10, 40), 0.95, 30))
     S.append(randomized(7, 5, 16, 5, {"lane_width": 1, "group_width": 1, "assignment_queue_capacity": 3},
                         (3, 10), (2, 12), 0.85, 3))
+    # repeated literals and tautologies (x or -x): the engine takes any literal list
+    S.append(randomized(8, 6, 5, 2, {"lane_width": 8, "group_width": 4, "max_clauses": 40},
+                        (4, 12), (2, 16), 0.7, 6, reduce_every=3, name="repeats_and_tautologies",
+                        repeats=True))
     return [run_scenario(s) for s in S]
 
 

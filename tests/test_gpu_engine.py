@@ -725,3 +725,49 @@ def test_replay_with_threads_spanning_chunks(P):
             for f in ("engine_id", "lane_mask", "group"):
                 assert np.array_equal(recs[f], want[f]), f
             e.close()
+
+
+@pytest.mark.parametrize("all_pairs", [False, True])
+def test_repeated_literals_and_tautologies_parity(P, all_pairs):
+    # the reference accepts any literal list (engine.py:305-317): repeated
+    # literals and x or -x in one clause change nothing in its recurrences,
+    # and the store keeps them; drawn from 40 variables so both are common
+    import os
+    from paper_2012_03119_b200 import workload as W
+    from paper_2012_03119_b200.native import NativeEngine
+    rng = np.random.default_rng(23)
+    nv, threads, lanes = 40, 3, 32
+    sizes = rng.integers(1, 9, 4000)
+    buckets = {}
+    for s in np.unique(sizes):  # bucket creation order = first-seen size order (flatten keeps dict order)
+        k = int((sizes == s).sum())
+        v = rng.integers(1, nv + 1, (k, int(s)))
+        sg = rng.integers(0, 2, (k, int(s))) * 2 - 1
+        buckets[int(s)] = (v * sg).astype(np.int32)
+    flat, offs, ids = W.flatten(buckets)
+    lits = [flat[offs[i]:offs[i + 1]] for i in range(len(ids))]
+    assert any(len(set(np.abs(c).tolist())) < len(c) for c in lits)  # repeats and tautologies present
+    assert any(set(c.tolist()) & set((-c).tolist()) for c in lits)
+    dev = NativeEngine(nv, 32, 32, report_capacity=1 << 16)
+    if all_pairs:
+        dev.set_all_pairs(True)
+    dev.add_clauses(flat, offs, ids)
+    ora = O.OracleStore()
+    ora.insert_flat(flat, offs, ids)
+    for r in range(3):
+        snaps = W.snapshots(threads, lanes, nv, rng)
+        gl, gt = W.groups_for(threads, lanes, 32)
+        dev.stage(snaps)
+        res = dev.round(gl, gt, 1.0 + r)
+        recs = W.in_reference_order(dev.fetch(res.reports), offs, ids, buckets, 32)
+        ogt = np.arange(len(gl), dtype=np.int32) if all_pairs else gt
+        orecs, octr = ora.test_round(nv, snaps, gl, ogt, 32, 32, 1.0 + r, nthreads=os.cpu_count() or 8)
+        assert len(recs) == len(orecs) > 0
+        for f in ("engine_id", "lane_mask", "group"):
+            assert np.array_equal(recs[f], orecs[f]), f
+        assert res.lane_triggers == octr["lane_triggers"]
+        assert res.aggregate_tests_negative == octr["aggregate_tests_negative"]
+    for d, o in zip(dev.buckets(), ora.buckets()):
+        assert np.array_equal(d[1], o[2])  # the stored literals, as given (repeats and all)
+        assert np.array_equal(d[4].view(np.uint64), o[5].view(np.uint64))
+    dev.close()
