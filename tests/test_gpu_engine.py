@@ -254,6 +254,13 @@ def test_many_chunks_parity(P, lw, gw, all_pairs, chunk_filter):
              size_lo=2, size_hi=12, all_pairs=all_pairs, chunk_filter=chunk_filter)
 
 
+def test_large_variable_range_parity(P):
+    # 3M variables: table rows of 3M entries (lane table ~0.8 GB per slot),
+    # variable ids past 2^21 in every index computation
+    res = run_both(P, n=20_000, threads=2, lanes=32, nv=3_000_000, seed=29, size_lo=1, size_hi=6)
+    assert res.reports > 0
+
+
 def test_long_clauses_parity(P):
     # clauses far longer than the prefetched rows (and past the 58 ordered positions)
     run_both(P, n=3000, threads=4, lanes=32, nv=2000, seed=9, size_lo=100, size_hi=400)
