@@ -331,12 +331,17 @@ int tsg_stream(tsg_engine* h, void** stream);
  * no round may be in flight */
 int tsg_ring_open(tsg_engine* h, int64_t capacity, int64_t wait_us);
 int tsg_ring_close(tsg_engine* h);
-/* Copy up to cap landed records, in ring order, into out (key = engine_id <<
- * 16 | group, lane_mask) and free their slots.  Returns when cap records were
- * copied, when at least one was and the next has not landed for
- * min(timeout_us, 20) microseconds, or after timeout_us with none.  Thread-safe against the round calls on other threads (drainers
- * serialise on the ring's lock). */
-int tsg_ring_drain(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n, int64_t timeout_us);
+/* Copy up to cap landed records of one contiguous run of ring positions,
+ * in order, into out (key = engine_id << 16 | group, lane_mask) and free
+ * their slots; *first_pos (may be NULL) = the ring position of out[0] --
+ * records are numbered by position from the ring's opening, rounds in launch
+ * order, so drainers on several threads can reassemble them.  Returns when
+ * cap records were copied, when the run ends, when at least one was and the
+ * next has not landed for min(timeout_us, 20) microseconds, or after
+ * timeout_us with none.  Thread-safe against the round calls on other
+ * threads; several drainers consume disjoint runs concurrently. */
+int tsg_ring_drain(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n, int64_t timeout_us,
+                   int64_t* first_pos);
 /* records of the rounds collected so far, records drained, whether records
  * were dropped */
 int tsg_ring_status(tsg_engine* h, int64_t* expected, int64_t* consumed, int32_t* failed);

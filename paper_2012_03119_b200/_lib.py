@@ -103,7 +103,7 @@ def _declare(L):
         "tsg_ingress_copy": ([P, P, P, I64], C.c_int),
         "tsg_ring_open": ([P, I64, I64], C.c_int),
         "tsg_ring_close": ([P], C.c_int),
-        "tsg_ring_drain": ([P, P, I64, pI64, I64], C.c_int),
+        "tsg_ring_drain": ([P, P, I64, pI64, I64, pI64], C.c_int),
         "tsg_ring_status": ([P, pI64, pI64, C.POINTER(I32)], C.c_int),
         "tsg_reduce_hist": ([P, C.c_uint64, C.c_uint64, I32, P], C.c_int),
         "tsg_reduce_commit": ([P, C.c_uint64, C.c_uint64, I32, pI64, P, I64], C.c_int),

@@ -2400,9 +2400,10 @@ int64_t ring_tail(const tsg_engine::Ring& r) {
 }
 }  // namespace
 
-int tsg_ring_drain(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n, int64_t timeout_us) {
+int tsg_ring_drain(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n, int64_t timeout_us, int64_t* first_pos) {
     if (!h || !n || (cap > 0 && !out)) return fail(TSG_EINVAL, "bad arguments");
     *n = 0;
+    if (first_pos) *first_pos = -1;
     auto& r = h->ring;
     {
         std::lock_guard<std::mutex> lk(r.mtx);
@@ -2437,7 +2438,10 @@ int tsg_ring_drain(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n, int6
                 p = r.open[b] = 0;
             }
         }
-        // consume it in order while its records have landed
+        // consume it in order while its records have landed (one call hands
+        // out one contiguous run of positions: drainers on several threads
+        // can put their batches back in ring order)
+        if (first_pos) *first_pos = b * r.blk + p;
         bool stalled = false;
         while (p < r.blk && k < cap) {
             const uint64_t q = (uint64_t)(b * r.blk + p);
@@ -2471,7 +2475,7 @@ int tsg_ring_drain(tsg_engine* h, tsg_report* out, int64_t cap, int64_t* n, int6
             }
             ctl[0] = (unsigned long long)ring_tail(r);  // the slots below are free for the kernel
         }
-        if (stalled) break;
+        if (stalled || k > 0) break;  // one run per call
     }
     *n = k;
     return TSG_OK;

@@ -278,15 +278,18 @@ class NativeEngine:
         check(self.L.tsg_ring_close(self.h))
 
     def ring_drain(self, max_records: int = 1 << 16, timeout_ms: float = 0.0,
-                   out: Optional[np.ndarray] = None) -> np.ndarray:
-        """Landed records in ring order (raw REPORT_DTYPE); empty after
-        timeout_ms with none.  Safe to call from a thread other than the one
-        running the rounds (ctypes releases the GIL)."""
+                   out: Optional[np.ndarray] = None, with_pos: bool = False):
+        """One contiguous run of landed records, in ring order (raw
+        REPORT_DTYPE); empty after timeout_ms with none.  with_pos: also the
+        ring position of the first (records are numbered from the ring's
+        opening, rounds in launch order).  Safe to call from threads other
+        than the one running the rounds (ctypes releases the GIL)."""
         if out is None or len(out) < max_records:
             out = np.zeros(max(1, max_records), REPORT_DTYPE)
-        got = C.c_int64(0)
-        check(self.L.tsg_ring_drain(self.h, ptr(out), max_records, C.byref(got), int(timeout_ms * 1000)))
-        return out[:got.value]
+        got, pos = C.c_int64(0), C.c_int64(-1)
+        check(self.L.tsg_ring_drain(self.h, ptr(out), max_records, C.byref(got), int(timeout_ms * 1000),
+                                    C.byref(pos)))
+        return (out[:got.value], pos.value) if with_pos else out[:got.value]
 
     def ring_status(self):
         """(records of the collected rounds, records drained, dropped?)"""
@@ -306,15 +309,16 @@ class NativeEngine:
 class RingDrainer:
     """CPU threads draining an engine's host report ring (tsg_ring_drain)
     while its rounds run -- the consumer side of north_star subsystem 4.
-    Records accumulate as raw REPORT_DTYPE arrays; `take(n)` waits until n
-    records were drained in all and returns them (reservation order when one
-    thread drains)."""
+    Each drained run carries its ring position, so `take(n)` returns exactly
+    the next n records in ring order -- the next round's when n is that
+    round's report count -- however many threads drain and however many
+    rounds are in flight."""
 
     def __init__(self, eng: NativeEngine, threads: int = 1, batch: int = 1 << 16):
         import threading
         self.eng = eng
-        self._parts: List[np.ndarray] = []
-        self._count = 0
+        self._runs: dict = {}   # ring position -> records landed from there
+        self._next = 0          # position of the next record take() hands out
         self._lock = threading.Lock()
         self._cv = threading.Condition(self._lock)
         self._stop = threading.Event()
@@ -327,11 +331,10 @@ class RingDrainer:
         buf = np.empty(batch, REPORT_DTYPE)
         try:
             while not self._stop.is_set():
-                got = self.eng.ring_drain(batch, timeout_ms=1.0, out=buf)
+                got, pos = self.eng.ring_drain(batch, timeout_ms=1.0, out=buf, with_pos=True)
                 if len(got):
                     with self._cv:
-                        self._parts.append(got)  # a view of buf: a fresh buf follows
-                        self._count += len(got)
+                        self._runs[pos] = got  # a view of buf: a fresh buf follows
                         self._cv.notify_all()
                     buf = np.empty(batch, REPORT_DTYPE)
         except BaseException as e:  # surfaced by take()
@@ -339,27 +342,36 @@ class RingDrainer:
                 self.error = e
                 self._cv.notify_all()
 
+    def _ready(self) -> int:
+        """Records available contiguously from self._next (lock held)."""
+        k, pos = 0, self._next
+        while pos in self._runs:
+            k += len(self._runs[pos])
+            pos += len(self._runs[pos])
+        return k
+
     def take(self, n: int, timeout_s: float = 60.0) -> np.ndarray:
-        """The first n records not taken yet (blocks until drained)."""
+        """The next n records in ring order (blocks until drained)."""
         import time
         end = time.monotonic() + timeout_s
         with self._cv:
-            while self._count < n and self.error is None:
+            while self._ready() < n and self.error is None:
                 left = end - time.monotonic()
                 if left <= 0:
-                    raise TimeoutError(f"ring drained {self._count} of {n} records")
+                    raise TimeoutError(f"ring drained {self._ready()} of {n} records")
                 self._cv.wait(min(left, 0.1))
             if self.error is not None:
                 raise self.error
-            if len(self._parts) == 1 and len(self._parts[0]) == n:
-                out = self._parts[0]
-                self._parts = []
-            else:
-                allr = np.concatenate(self._parts) if self._parts else np.zeros(0, REPORT_DTYPE)
-                out, rest = allr[:n], allr[n:]
-                self._parts = [rest] if len(rest) else []
-            self._count -= n
-            return out
+            parts, got = [], 0
+            while got < n:
+                run = self._runs.pop(self._next)
+                use = min(len(run), n - got)
+                parts.append(run[:use])
+                if use < len(run):  # the rest starts the next take
+                    self._runs[self._next + use] = run[use:]
+                self._next += use
+                got += use
+            return parts[0] if len(parts) == 1 else (np.concatenate(parts) if parts else np.zeros(0, REPORT_DTYPE))
 
     def close(self) -> None:
         self._stop.set()

@@ -83,7 +83,7 @@ def test_ring_entry_points_validate_without_a_device():
     from paper_2012_03119_b200 import _lib
     L = _lib.load()
     n = C.c_int64(0)
-    assert L.tsg_ring_drain(None, None, 0, C.byref(n), 0) == _lib.TSG_EINVAL
+    assert L.tsg_ring_drain(None, None, 0, C.byref(n), 0, None) == _lib.TSG_EINVAL
     assert L.tsg_ring_status(None, None, None, None) == _lib.TSG_EINVAL
     assert L.tsg_ring_open(None, 1024, 1000) == _lib.TSG_EINVAL
     assert L.tsg_ring_close(None) == _lib.TSG_EINVAL

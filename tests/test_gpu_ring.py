@@ -111,9 +111,12 @@ def test_ring_wraps_and_matches_device_buffer(W):
     eng.close()
 
 
-def test_ring_two_rounds_in_flight(W):
-    """launch A, launch B, collect both: one drainer sees all of A's records
-    before B's (B's kernel reserves after A's finished)."""
+@pytest.mark.parametrize("drainers,cap", [(1, 1 << 12), (4, 1 << 12), (3, 256)])
+def test_ring_two_rounds_in_flight(W, drainers, cap):
+    """launch A, launch B, collect both: the ring positions of A's records
+    all precede B's (B's kernel reserves after A's finished), and take()
+    reassembles the drainer threads' runs in position order -- A's records,
+    then B's, however many threads drain."""
     from paper_2012_03119_b200.native import RingDrainer, pack_rows
     nv = 5000
     eng, rng, buckets, flat, offs, ids = store(W, 60_000, nv, 9)
@@ -124,8 +127,8 @@ def test_ring_two_rounds_in_flight(W):
         eng.stage(snaps)
         res = eng.round(gl, gt, 1.0)
         rounds.append((pack_rows(snaps, nv), gl, gt, as_set(eng.fetch(res.reports)), res.reports))
-    eng.ring_open(capacity=1 << 12)
-    dr = RingDrainer(eng, threads=1, batch=256)
+    eng.ring_open(capacity=cap)
+    dr = RingDrainer(eng, threads=drainers, batch=256)
     try:
         for packed, gl, gt, _, _ in rounds:
             eng.stage_packed(packed)
