@@ -88,7 +88,8 @@ def test_randomised_engine_streams_vs_oracle_engine():
     """The drop-in Engine under random operation streams (adds, explicit
     deletes, reduces, snapshot bursts that overflow queues, wrong-free
     rounds) against the oracle's restatement of the reference engine, with
-    random word widths, 1-3 clause shards and the chunk filter on or off:
+    random word widths, 1-3 clause shards, the chunk filter on or off and
+    the records through the device buffer or the host report ring:
     every round's result, every thread's drained reports in order, the
     counters and the store (fp64 activities bit-exact)."""
     from gpu_util import require_device
@@ -108,8 +109,10 @@ def test_randomised_engine_streams_vs_oracle_engine():
         max_clauses = int(rng.integers(50, 4000))
         devices = [None, [0, 0], [0, 0, 0]][int(rng.integers(0, 3))]
         chunk_filter = bool(rng.random() < 0.5)
+        ring = int(rng.choice([0, 0, 256, 4096])) if lw <= 32 else 0  # records through the host report ring
         cfg = dict(max_clauses=max_clauses, lane_width=lw, group_width=gw, assignment_queue_capacity=cap)
-        eng = P.Engine(nv, threads, P.EngineConfig(**cfg, devices=devices, chunk_filter=chunk_filter))
+        eng = P.Engine(nv, threads, P.EngineConfig(**cfg, devices=devices, chunk_filter=chunk_filter,
+                                                   report_ring=ring))
         ora = O.OracleEngine(nv, threads, **cfg)
         hi = min(nv, 14)
         for r in range(int(rng.integers(2, 8))):
@@ -130,7 +133,7 @@ def test_randomised_engine_streams_vs_oracle_engine():
             if rng.random() < 0.2:
                 assert eng.reduce_store() == ora.reduce_store()
             res, ores = eng.run_round(), ora.run_round()
-            ctx = (streams, r, nv, threads, lw, gw, cap, max_clauses, devices, chunk_filter)
+            ctx = (streams, r, nv, threads, lw, gw, cap, max_clauses, devices, chunk_filter, ring)
             assert [res.reports_emitted, res.clauses_tested, res.assignments_consumed,
                     res.aggregate_tests_negative] == [ores["reports_emitted"], ores["clauses_tested"],
                                                       ores["assignments_consumed"],
