@@ -90,10 +90,15 @@ class ClockSampler:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device),
                  "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # nvidia-smi takes a while to start: the timed region (milliseconds
+            # at C3) begins once it is sampling
+            t_end = time.time() + 5.0
+            while not self.samples and time.time() < t_end:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
@@ -576,20 +581,33 @@ def main():
 
     h_packed2 = [h_packed_t, torch.empty((A, pw), dtype=torch.int64).pin_memory()]
 
-    def loop_with_pack(k, warm=0):
-        # as loop_pipelined, but every round's int8 snapshots are packed to
-        # 2-bit rows on the host threads inside the timed loop (into the
-        # pinned buffer the round before last used) while the previous round
-        # runs on the GPU -- the cost the solver threads pay at submit time
+    h_int8_np = h_int8_t.numpy()
+
+    def loop_with_pack(k, warm=0, frac=1.0):
+        # as loop_pipelined, but every round starts from the int8 snapshot
+        # rows: the first `frac` of this rank's rows are packed to 2-bit rows
+        # on the host threads inside the timed loop (into the pinned buffer
+        # the round before last used) while the previous round runs on the
+        # GPU, the rest cross the link as int8 and are packed on the device
+        # (tsg_stage_packed_mixed) -- host memory and the link share the
+        # ingress
+        rp = int(round(frac * split_rows))
         r, pending, w0 = None, 0, None
         eng.prepare(gl, gt)
         for i in range(warm + k):
             if i == warm:
                 w0 = time.perf_counter()
             buf = h_packed2[i % 2]  # this rank's rows only, on its share of the host threads
-            pack_rows(snaps[split_row0:split_row0 + split_rows], cfg.num_vars,
-                      out=buf.numpy().view(np.uint64)[:split_rows], threads=pack_threads)
-            _lib.check(L.tsg_stage_packed(eng.h, C.c_void_p(buf.data_ptr()), split_rows, pw, 0))
+            if rp:
+                pack_rows(h_int8_np[split_row0:split_row0 + rp], cfg.num_vars,
+                          out=buf.numpy().view(np.uint64)[:rp], threads=pack_threads)
+            if rp == split_rows:
+                _lib.check(L.tsg_stage_packed(eng.h, C.c_void_p(buf.data_ptr()), split_rows, pw, 0))
+            else:
+                _lib.check(L.tsg_stage_packed_mixed(
+                    eng.h, C.c_void_p(buf.data_ptr()), rp, pw,
+                    C.c_void_p(h_int8_t.data_ptr() + (split_row0 + rp) * h_int8_np.strides[0]),
+                    split_rows - rp, h_int8_np.strides[0]))
             if pending:
                 r = eng.collect()
                 fetch_async(r)
@@ -633,6 +651,8 @@ def main():
 
     err = None
     ms = ms_seq = ms8 = ms_pack = float("inf")
+    SPLITS = tuple(float(x) for x in os.environ.get("TSG_BENCH_SPLITS", "1.0,0.9,0.85,0.8,0.75,0.7").split(","))
+    ms_split, best_frac = {}, 1.0
     pack_ms, d2h, r, r8 = None, 0, res, res
     try:
         pack_rows(snaps, cfg.num_vars, out=h_packed, threads=host_threads)
@@ -644,16 +664,25 @@ def main():
             dist.barrier()
         ms, r, d2h = timed_loop(loop_pipelined, e2e_steps)
         ms_seq, _, _ = timed(step_packed, max(3, e2e_steps // 2))
-        ms_pack, _, _ = timed_loop(loop_with_pack, e2e_steps)
+        # the share of rows packed on the host: every round from int8 rows,
+        # the faster split on this box is the headline (all reported)
+        for frac in SPLITS:
+            ms_split[frac], _, _ = timed_loop(lambda k, warm=0, f=frac: loop_with_pack(k, warm, f), e2e_steps)
+        best_frac = min(ms_split, key=ms_split.get)
+        ms_pack = ms_split[best_frac]
         if world == 1:
             ms8, r8, _ = timed(step_int8, max(3, e2e_steps // 2))
     except Exception as exc:  # reported in the line, never fatal to it
         err = repr(exc)
     tot = [float(r.lane_tests), float(d2h)]
     if dist is not None:  # max over ranks (inf marks a failed rank); sums of the per-rank work
-        t = torch.tensor([ms, ms_seq, ms8, ms_pack], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([ms, ms_seq, ms8] + [ms_split.get(f, float("inf")) for f in SPLITS], dtype=torch.float64,
+                         device=f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, ms_seq, ms8, ms_pack = (float(x) for x in t.tolist())
+        ms, ms_seq, ms8 = (float(x) for x in t.tolist()[:3])
+        ms_split = dict(zip(SPLITS, t.tolist()[3:]))
+        best_frac = min(ms_split, key=ms_split.get)
+        ms_pack = ms_split[best_frac]
         t = torch.tensor(tot, dtype=torch.float64, device=f"cuda:{local}")
         dist.all_reduce(t)
         tot = [float(x) for x in t.tolist()]
@@ -673,13 +702,18 @@ def main():
                    if tables_mode == "replicated" else "every rank copies in all rows; rank 0's tables "
                    "broadcast")
         e2e = {"value": tot[0] / (ms_pack * 1e-3), "unit": "clause_assignment_tests/s",
-               "h2d_bytes_per_step": int(split_rows * pw * 8) * world,
+               "h2d_bytes_per_step": int(round(best_frac * split_rows) * pw * 8
+                                         + (split_rows - round(best_frac * split_rows)) * (cfg.num_vars + 1)) * world,
                "d2h_bytes_per_step": int(tot[1]),
                "ms_per_step": ms_pack,
-               "input": (f"int8 snapshot rows (the reference's format) in host memory, packed to 2-bit rows on "
-                         f"{pack_threads} host thread(s) per rank inside the timed loop"),
+               "input": (f"int8 snapshot rows (the reference's format) in pinned host memory; {best_frac:.0%} of "
+                         f"them packed to 2-bit rows on {pack_threads} host thread(s) per rank inside the timed "
+                         f"loop, the rest copied in as int8 and packed on the GPU"),
                "how": "pipelined: round i+1's rows are packed and copy in (ingress stream) while round i is "
                       "encoded and tested and round i-1's records copy out (egress stream)",
+               "host_packed_share": best_frac,
+               "ms_per_step_by_host_packed_share": {f"{f:.2f}": v for f, v in ms_split.items()},
+               "h2d_bytes_per_step_note": "packed rows + int8 rows of the share not packed on the host",
                "ingress": ingress,
                "egress": "every rank copies out its own records",
                "host_pack_ms_per_round": pack_ms, "host_pack_threads": host_threads,

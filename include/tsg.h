@@ -226,6 +226,15 @@ int tsg_pack_rows(const int8_t* rows, int64_t n_rows, int64_t row_pitch, int32_t
                   uint64_t* out, int64_t out_pitch_words);
 int tsg_stage_packed(tsg_engine* h, const uint64_t* rows, int64_t n_rows,
                      int64_t pitch_words, int32_t on_device);
+/* Stage a round whose rows arrive partly packed and partly as int8: rows
+ * 0..n_packed-1 from `packed` (tsg_pack_rows words), rows n_packed.. from
+ * `raw` (int8, num_vars+1 values each), copied in on the ingress stream and
+ * packed on the device behind the packed ones -- host packing and the link
+ * share a round's ingress (the host packs part of the rows while the rest
+ * crosses as int8).  Host sources must stay unchanged until the round is
+ * collected (as tsg_stage_packed's pinned rows). */
+int tsg_stage_packed_mixed(tsg_engine* h, const uint64_t* packed, int64_t n_packed, int64_t pitch_words,
+                           const int8_t* raw, int64_t n_raw, int64_t raw_pitch);
 int tsg_round_prepare(tsg_engine* h, const int32_t* group_lanes,
                       const int32_t* group_tid, int32_t n_groups);
 int tsg_round_encode(tsg_engine* h);

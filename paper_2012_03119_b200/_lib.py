@@ -63,7 +63,7 @@ EXPORTS = (
     "tsg_round_layout", "tsg_set_all_pairs", "tsg_round_tables_copy", "tsg_reduce_begin", "tsg_reduce_hist",
     "tsg_reduce_commit", "tsg_fetch_ordered", "tsg_stage_packed_segments", "tsg_host_alloc", "tsg_host_free",
     "tsg_device_alloc", "tsg_device_free", "tsg_ingress_copy", "tsg_ring_open", "tsg_ring_close",
-    "tsg_ring_drain", "tsg_ring_status",
+    "tsg_ring_drain", "tsg_ring_status", "tsg_stage_packed_mixed",
 )
 
 _lib = None
@@ -105,6 +105,7 @@ def _declare(L):
         "tsg_ring_close": ([P], C.c_int),
         "tsg_ring_drain": ([P, P, I64, pI64, I64, pI64], C.c_int),
         "tsg_ring_status": ([P, pI64, pI64, C.POINTER(I32)], C.c_int),
+        "tsg_stage_packed_mixed": ([P, P, I64, I64, P, I64, I64], C.c_int),
         "tsg_reduce_hist": ([P, C.c_uint64, C.c_uint64, I32, P], C.c_int),
         "tsg_reduce_commit": ([P, C.c_uint64, C.c_uint64, I32, pI64, P, I64], C.c_int),
         "tsg_remove_clauses": ([P, P, I64, pI64], C.c_int),

@@ -120,6 +120,8 @@ struct tsg_engine {
     // i+1 copy in while round i is encoded and tested
     uint64_t* pbuf[2] = {nullptr, nullptr};
     int64_t pbuf_cap[2] = {0, 0};
+    int8_t* rawbuf[2] = {nullptr, nullptr};  // tsg_stage_packed_mixed: int8 rows packed on the device
+    int64_t rawbuf_cap[2] = {0, 0};
     int pk = 1;                           // buffer of the last stage
     bool pstaged = false;                 // prows is pbuf[pk], copied on the ingress stream
     cudaStream_t ingress = nullptr;
@@ -788,6 +790,7 @@ int tsg_destroy(tsg_engine* h) {
     if (h->st) {
         for (auto& b : h->buckets) bucket_free(h, b);
         dfree(h, h->rows_own); dfree(h, h->pbuf[0]); dfree(h, h->pbuf[1]); dfree(h, h->tables); dfree(h, h->d_desc);
+        dfree(h, h->rawbuf[0]); dfree(h, h->rawbuf[1]);
         dfree(h, h->mctr);
         dfree(h, h->size_of_id);
         dfree(h, h->ord_dev);
@@ -1498,6 +1501,70 @@ int tsg_stage_packed(tsg_engine* h, const uint64_t* rows, int64_t n_rows, int64_
     else
         CK(cudaMemcpy2DAsync(h->pbuf[b], words * 8, rows, pitch_words * 8, words * 8, n_rows,
                              on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDefault, h->ingress));
+    CK(cudaEventRecord(h->ev_staged[b], h->ingress));
+    h->pk = b;
+    h->pstaged = true;
+    h->prows = h->pbuf[b];
+    h->ppitch = words;
+    return TSG_OK;
+}
+
+int tsg_stage_packed_mixed(tsg_engine* h, const uint64_t* packed, int64_t n_packed, int64_t pitch_words,
+                           const int8_t* raw, int64_t n_raw, int64_t raw_pitch) {
+    CKR(validate_handle(h));
+    DevGuard g(h->dev);
+    const int64_t words = packed_words(h->V);
+    if (n_packed < 0 || n_raw < 0) return fail(TSG_EINVAL, "negative row count");
+    if (n_packed > 0 && (!packed || pitch_words < words))
+        return fail(TSG_EINVAL, "packed rows: null or pitch %lld < %lld words", (long long)pitch_words, (long long)words);
+    if (n_raw > 0 && (!raw || raw_pitch < (int64_t)h->V + 1))
+        return fail(TSG_EINVAL, "int8 rows: null or pitch %lld < num_vars+1", (long long)raw_pitch);
+    const int64_t n = n_packed + n_raw;
+    h->n_rows = n;
+    h->packed = true;
+    h->pstaged = false;
+    if (n == 0) return TSG_OK;
+    // as tsg_stage_packed: the staging buffer the previous stage did not use,
+    // on the ingress stream; the int8 rows land in a device buffer of the
+    // same slot and are packed on the device behind the packed ones
+    const int b = h->pk ^ 1;
+    const int64_t need = words * n;
+    const int64_t rpitch = round_up((int64_t)h->V + 1, 16);
+    CK(cudaStreamWaitEvent(h->ingress, h->ev_read[b], 0));
+    bool grown = false;
+    if (need > h->pbuf_cap[b]) {
+        dfree(h, h->pbuf[b]);
+        h->pbuf[b] = nullptr;
+        const int64_t cap = std::max(need, h->pbuf_cap[b] * 2);
+        CKR(dalloc(h, (void**)&h->pbuf[b], cap * 8));
+        h->pbuf_cap[b] = cap;
+        grown = true;
+    }
+    if (rpitch * n_raw > h->rawbuf_cap[b]) {
+        dfree(h, h->rawbuf[b]);
+        h->rawbuf[b] = nullptr;
+        const int64_t cap = std::max(rpitch * n_raw, h->rawbuf_cap[b] * 2);
+        CKR(dalloc(h, (void**)&h->rawbuf[b], cap));
+        h->rawbuf_cap[b] = cap;
+        grown = true;
+    }
+    if (grown) {  // the allocations (stream-ordered on st) come first
+        CK(cudaEventRecord(h->ev_staged[b], h->st));
+        CK(cudaStreamWaitEvent(h->ingress, h->ev_staged[b], 0));
+    }
+    if (n_packed > 0) {
+        if (pitch_words == words)
+            CK(cudaMemcpyAsync(h->pbuf[b], packed, n_packed * words * 8, cudaMemcpyDefault, h->ingress));
+        else
+            CK(cudaMemcpy2DAsync(h->pbuf[b], words * 8, packed, pitch_words * 8, words * 8, n_packed,
+                                 cudaMemcpyDefault, h->ingress));
+    }
+    if (n_raw > 0) {
+        CK(cudaMemcpy2DAsync(h->rawbuf[b], rpitch, raw, raw_pitch, h->V + 1, n_raw, cudaMemcpyDefault, h->ingress));
+        k_pack_rows<<<grid_for(n_raw * words), 256, 0, h->ingress>>>(h->rawbuf[b], rpitch, n_raw, (int64_t)h->V + 1,
+                                                                     h->pbuf[b] + n_packed * words, words, words);
+        CK(cudaGetLastError());
+    }
     CK(cudaEventRecord(h->ev_staged[b], h->ingress));
     h->pk = b;
     h->pstaged = true;

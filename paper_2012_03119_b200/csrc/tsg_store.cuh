@@ -334,4 +334,36 @@ __global__ void k_max_var(const int32_t* __restrict__ lits, int64_t n, int32_t s
     if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
 }
 
+// int8 snapshot rows -> 2-bit packed rows on the device (tsg_stage_packed_mixed):
+// the same words tsg_pack_rows writes on the host -- u64 word k of a row
+// holds variables 32k..32k+31, low half (value == 1), high half (value != 0),
+// zero past the row -- one thread per word.
+__global__ void k_pack_rows(const int8_t* __restrict__ raw, int64_t raw_pitch, int64_t n_rows, int64_t nv1,
+                            uint64_t* __restrict__ out, int64_t out_pitch_words, int64_t words) {
+    const int64_t total = n_rows * words;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / words, k = i - r * words;
+        const int8_t* src = raw + r * raw_pitch + 32 * k;
+        uint32_t t = 0, st = 0;
+        if (32 * k + 32 <= nv1 && (((uintptr_t)src) & 15) == 0) {
+            const uint4 a = *reinterpret_cast<const uint4*>(src), b = *reinterpret_cast<const uint4*>(src + 16);
+            const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint32_t eq1 = __vcmpeq4(w[q], 0x01010101u), nz = __vcmpne4(w[q], 0u);  // 0xFF per matching byte
+                t |= ((eq1 & 1u) | ((eq1 >> 7) & 2u) | ((eq1 >> 14) & 4u) | ((eq1 >> 21) & 8u)) << (4 * q);
+                st |= ((nz & 1u) | ((nz >> 7) & 2u) | ((nz >> 14) & 4u) | ((nz >> 21) & 8u)) << (4 * q);
+            }
+        } else {
+            for (int j = 0; j < 32; ++j) {
+                if (32 * k + j >= nv1) break;
+                const int8_t v = src[j];
+                t |= (uint32_t)(v == 1) << j;
+                st |= (uint32_t)(v != 0) << j;
+            }
+        }
+        out[r * out_pitch_words + k] = (uint64_t)t | ((uint64_t)st << 32);
+    }
+}
+
 }  // namespace tsg

@@ -187,6 +187,17 @@ class NativeEngine:
         check(self.L.tsg_stage_packed(self.h, C.c_void_p(packed.ctypes.data), packed.shape[0],
                                       packed.strides[0] // 8, 0))
 
+    def stage_packed_mixed(self, packed: np.ndarray, raw: np.ndarray) -> None:
+        """Rows 0..len(packed)-1 packed on the host (pack_rows), the rest as
+        int8 rows, packed on the device (tsg_stage_packed_mixed).  Both
+        arrays must stay unchanged until the round is collected."""
+        packed = np.ascontiguousarray(packed, np.uint64)
+        raw = np.ascontiguousarray(raw, np.int8)
+        np_, nr = (packed.shape[0] if packed.size else 0), (raw.shape[0] if raw.size else 0)
+        check(self.L.tsg_stage_packed_mixed(self.h, ptr(packed) if np_ else None, np_,
+                                            packed.shape[1] if np_ else packed_words(self.num_vars),
+                                            ptr(raw) if nr else None, nr, raw.strides[0] if nr else self.num_vars + 1))
+
     def stage_packed_ptr(self, ptr_: int, n_rows: int, pitch_words: int, on_device: bool) -> None:
         check(self.L.tsg_stage_packed(self.h, C.c_void_p(ptr_), n_rows, pitch_words, 1 if on_device else 0))
 

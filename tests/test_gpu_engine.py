@@ -420,6 +420,42 @@ def test_packed_rows_encode_identically(P, lw, gw, threads, lanes, nv, chunk_fil
     assert np.array_equal(out[0][3], out[1][3])
 
 
+@pytest.mark.parametrize("nv", [1000, 333, 4095, 31])
+def test_mixed_staging_encodes_identically(P, nv):
+    # rows partly packed on the host and partly copied as int8 and packed on
+    # the device (tsg_stage_packed_mixed): byte-identical tables to all-packed
+    # staging at every split, and identical round results
+    from paper_2012_03119_b200 import workload as W
+    from paper_2012_03119_b200.native import NativeEngine, pack_rows
+    rng = np.random.default_rng(nv + 1)
+    buckets = W.clause_buckets(4000, nv, rng, 1, 10)
+    flat, offs, ids = W.flatten(buckets)
+    snaps = W.snapshots(3, 40, nv, rng)
+    snaps[:, 0] = rng.integers(-1, 2, snaps.shape[0])  # slot 0 must be ignored
+    snaps[::7, 5 % (nv + 1)] = 9                       # non-{1,-1,0} values read as False
+    gl, gt = W.groups_for(3, 40, 32)
+    packed_all = pack_rows(snaps, nv)
+    want = None
+    for split in (snaps.shape[0], 0, 1, 57, snaps.shape[0] - 1):
+        e = NativeEngine(nv, 32, 32)
+        e.add_clauses(flat, offs, ids)
+        if split == snaps.shape[0]:
+            e.stage_packed(packed_all)
+        else:
+            e.stage_packed_mixed(packed_all[:split], snaps[split:])
+        e.prepare(gl, gt)
+        e.encode()
+        tab = _defined_tables(_tables(e), nv, 32, 32, gl)
+        res = e.test(1.0)
+        got = (tab, res.lane_triggers, np.sort(e.fetch(res.reports), order=["engine_id", "group"]))
+        e.close()
+        if want is None:
+            want = got
+        else:
+            assert np.array_equal(got[0], want[0]), split
+            assert got[1] == want[1] and np.array_equal(got[2], want[2]), split
+
+
 def test_async_report_egress_double_buffered(P):
     # round k's records copy out on the egress stream while round k+1 runs;
     # every round's records must equal a synchronous fetch of the same round
