@@ -11,7 +11,7 @@ for tool in memcheck racecheck synccheck; do
   timeout 900 compute-sanitizer --tool $tool --error-exitcode 99 --target-processes all \
     python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
 done
-T="tests/test_gpu_engine.py::test_widths_and_multichunk_parity tests/test_gpu_engine.py::test_reduce_and_remove_parity
+T="tests/test_gpu_engine.py::test_mixed_staging_encodes_identically tests/test_gpu_engine.py::test_widths_and_multichunk_parity tests/test_gpu_engine.py::test_reduce_and_remove_parity
    tests/test_gpu_engine.py::test_report_buffer_overflow_replay tests/test_gpu_engine.py::test_packed_rows_encode_identically
    tests/test_gpu_engine.py::test_twelve_byte_egress_records tests/test_gpu_engine.py::test_get_clauses_and_counters
    tests/test_gpu_ordering.py tests/test_gpu_exchange.py::test_replay_reference_solver_rounds
