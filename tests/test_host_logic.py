@@ -94,3 +94,48 @@ def test_literal_arena_reclaims_removed_clauses_without_touching_old_batches():
     for view, expect in views:  # old batches: literals as of their round
         for i, lits in expect.items():
             assert view.lits_of(i) == lits
+
+
+def test_ring_drainer_reassembles_runs_in_ring_order():
+    # native.RingDrainer: several threads drain runs of ring positions in any
+    # order; take(n) must return exactly the next n positions -- one
+    # round's records, then the next's
+    import threading
+    import numpy as np
+    from paper_2012_03119_b200._lib import REPORT_DTYPE
+    from paper_2012_03119_b200.native import RingDrainer
+
+    total = 5000
+    rng = np.random.default_rng(5)
+    cuts = np.unique(np.concatenate([[0, total], rng.integers(1, total, 300)]))
+    runs = [(int(a), int(b)) for a, b in zip(cuts[:-1], cuts[1:])]
+    order = rng.permutation(len(runs))  # handed out in random order to random threads
+
+    class FakeEngine:
+        def __init__(self):
+            self.lock = threading.Lock()
+            self.i = 0
+
+        def ring_drain(self, max_records, timeout_ms=0.0, out=None, with_pos=False):
+            with self.lock:
+                if self.i >= len(order):
+                    time.sleep(0.001)
+                    return np.zeros(0, REPORT_DTYPE), -1
+                a, b = runs[order[self.i]]
+                self.i += 1
+            recs = np.zeros(b - a, REPORT_DTYPE)
+            recs["key"] = np.arange(a, b, dtype=np.uint64)  # the record's position, as its payload
+            time.sleep(float(rng.random()) * 1e-4)
+            return recs, a
+
+    import time
+    dr = RingDrainer(FakeEngine(), threads=4, batch=64)
+    try:
+        got, pos = [], 0
+        for n in (1, 777, 0, 1500, 2222, total - 4500):  # "rounds" of these sizes
+            part = dr.take(n, timeout_s=10)
+            assert len(part) == n
+            assert np.array_equal(part["key"], np.arange(pos, pos + n, dtype=np.uint64))
+            pos += n
+    finally:
+        dr.close()
