@@ -139,3 +139,36 @@ def test_ring_drainer_reassembles_runs_in_ring_order():
             pos += n
     finally:
         dr.close()
+
+
+def test_engine_host_ordering_matches_the_reference_order():
+    # Engine._host_ordered (report ring path): records into delivery order --
+    # destination, chunk, bucket creation rank, engine id, group
+    # (engine.py:403-464) -- from one packed 64-bit key
+    import numpy as np
+    from paper_2012_03119_b200 import reports
+    from paper_2012_03119_b200.engine import Engine, EngineConfig, _Arena
+    rng = np.random.default_rng(9)
+    for n_ids, n_groups, gw in ((5000, 40, 8), (2_000_000, 3000, 64)):
+        e = object.__new__(Engine)
+        e.config = EngineConfig(group_width=gw)
+        n = 3000
+        eids = rng.choice(n_ids, n, replace=False).astype(np.int64)
+        sizes = rng.integers(1, 30, n).astype(np.int32)
+        e._arena = _Arena()
+        e._arena.size = np.zeros(n_ids, np.int32)
+        e._arena.size[eids] = sizes  # only the size lookups matter here
+        e._rank_of_size = rng.permutation(64).astype(np.int32)
+        gt = np.sort(rng.integers(0, 7, n_groups)).astype(np.int32)  # a thread's groups are consecutive
+        dec = np.zeros(n, reports.DECODED_DTYPE)
+        dec["engine_id"] = eids
+        dec["group"] = rng.integers(0, n_groups, n)
+        dec["lane_mask"] = rng.integers(1, 1 << 32, n, dtype=np.uint64)
+        dests = sorted(set(gt.tolist()))
+        got_e, got_m, got_g, counts, _ = e._host_ordered(dec, gt, dests)
+        dest = np.searchsorted(np.asarray(dests), gt[dec["group"]])
+        want = np.lexsort((dec["group"], dec["engine_id"], e._rank_of_size[sizes], dec["group"] // gw, dest))
+        assert np.array_equal(got_e, dec["engine_id"][want])
+        assert np.array_equal(got_g, dec["group"][want])
+        assert np.array_equal(got_m, dec["lane_mask"][want])
+        assert np.array_equal(counts, np.bincount(dest, minlength=len(dests)))
