@@ -846,19 +846,7 @@ int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, 
     // in first-seen order (dict insertion order of ClauseStore.buckets)
     std::unique_ptr<int[]> bucket_of(new int[n]);  // (uninitialised buffers below: every element is written)
     {
-        // literal range check over the batch at once (stored as-is; testing
-        // raises, numpy IndexError, engine.py:251)
-        const int64_t nl = offsets[n] - offsets[0];
-        std::atomic<bool> oob{false};
-        HostPool::get().parallel_for(nl, (int)std::min<int64_t>(16, nl / (1 << 18)), [&](int64_t a, int64_t b) {
-            int32_t lo = 0, hi = 0;
-            for (int64_t j = offsets[0] + a; j < offsets[0] + b; ++j) {
-                lo = std::min(lo, lits[j]);
-                hi = std::max(hi, lits[j]);
-            }
-            if ((int64_t)hi > h->V || -(int64_t)lo > h->V) oob = true;
-        });
-        if (oob) h->oob = true;
+        // (the literal range check runs in the placement pass below)
         int64_t top = h->max_id;
         for (int64_t i = 0; i < n; ++i) top = std::max<int64_t>(top, ids[i] < 0 ? INT64_MAX : ids[i]);
         h->max_id = top;
@@ -892,12 +880,24 @@ int tsg_add_clauses(tsg_engine* h, const int32_t* lits, const int64_t* offsets, 
     std::unique_ptr<int32_t[]> placed(new int32_t[(size_t)std::max<int64_t>(offsets[n] - offsets[0], 1)]);
     std::unique_ptr<uint64_t[]> hm(new uint64_t[n]);
     {  // placement is independent per clause: split large batches over host threads
+        // the literals are read once: placed, and range-checked on the way
+        // (stored as-is; testing raises, numpy IndexError, engine.py:251)
+        std::atomic<bool> oob{false};
         auto place_range = [&](int64_t a, int64_t b) {
-            for (int64_t i = a; i < b; ++i)
-                place_clause(h, lits + offsets[i], (int32_t)(offsets[i + 1] - offsets[i]),
-                             placed.get() + (offsets[i] - offsets[0]), &hm[i]);
+            int32_t lo = 0, hi = 0;
+            for (int64_t i = a; i < b; ++i) {
+                const int32_t* l = lits + offsets[i];
+                const int32_t sz = (int32_t)(offsets[i + 1] - offsets[i]);
+                for (int32_t j = 0; j < sz; ++j) {
+                    lo = std::min(lo, l[j]);
+                    hi = std::max(hi, l[j]);
+                }
+                place_clause(h, l, sz, placed.get() + (offsets[i] - offsets[0]), &hm[i]);
+            }
+            if ((int64_t)hi > h->V || -(int64_t)lo > h->V) oob = true;
         };
         HostPool::get().parallel_for(n, (int)std::min<int64_t>(16, n / 1024), place_range);
+        if (oob) h->oob = true;
     }
     mark("place");
     std::vector<std::vector<int64_t>> members(h->buckets.size());
