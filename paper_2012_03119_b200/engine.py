@@ -455,6 +455,7 @@ class Engine:
         self._pinned = _PinnedPool(self._L)
         self._sizes_in_order: List[int] = []                # bucket creation order (dict order)
         self._rank_of_size = np.zeros(64, dtype=np.int32)   # creation rank by clause size
+        self._size_known = np.zeros(64, dtype=bool)           # sizes with a bucket
         self._shard_load = np.zeros((len(self._shards), 64), dtype=np.int64)  # clauses per (shard, size)
 
         self._id_lock = threading.Lock()
@@ -607,22 +608,29 @@ class Engine:
             return
         offs = np.zeros(n + 1, dtype=np.int64)
         np.cumsum(lens, out=offs[1:])
-        # bucket creation order (dict insertion order): new sizes in first-seen order
-        sizes, first = np.unique(lens, return_index=True)
-        top = int(sizes[-1]) + 1
-        if top > self._rank_of_size.size:
+        # bucket creation order (dict insertion order): new sizes in first-seen
+        # order (a batch of known sizes only -- the streaming case -- skips it)
+        top = int(lens.max()) + 1
+        if top <= self._size_known.size and self._size_known[lens].all():
+            sizes = None
+        else:
+            sizes, first = np.unique(lens, return_index=True)
+        if sizes is not None and top > self._rank_of_size.size:
             grown = np.zeros(max(top, 2 * self._rank_of_size.size), np.int32)
             grown[:self._rank_of_size.size] = self._rank_of_size
             self._rank_of_size = grown
             load = np.zeros((len(self._shards), grown.size), np.int64)
             load[:, :self._shard_load.shape[1]] = self._shard_load
             self._shard_load = load
-        known = set(self._sizes_in_order)
-        for size in sizes[np.argsort(first, kind="stable")].tolist():
-            if size not in known:
-                self._rank_of_size[size] = len(self._sizes_in_order)
-                self._sizes_in_order.append(size)
-                known.add(size)
+        if sizes is not None:
+            known = set(self._sizes_in_order)
+            for size in sizes[np.argsort(first, kind="stable")].tolist():
+                if size not in known:
+                    self._rank_of_size[size] = len(self._sizes_in_order)
+                    self._sizes_in_order.append(size)
+                    known.add(size)
+            self._size_known = np.zeros(self._rank_of_size.size, bool)
+            self._size_known[self._sizes_in_order] = True
         ns = len(self._shards)
         if ns == 1:
             self._shards[0].add_clauses(flat, offs, ids, org, self._activity_inc)
